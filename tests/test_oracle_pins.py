@@ -1,0 +1,656 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (-m "not gpu").
+
+Every check compares the oracle with something other than itself: closed forms,
+independent libraries (scipy Rotation/Slerp, scipy real SH, numpy cumsum, Monte Carlo),
+brute force on tiny inputs, hand-worked golden fixtures (tests/golden/) and invariants.
+Citations: P:n = PAPER.md line n; S:n = SPEC.md line n (test ideas only).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy.spatial.transform import Rotation, Slerp
+
+from paper_2510_12901_b200 import synth as S
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def qmul(a, b):
+    w1, x1, y1, z1 = a
+    w2, x2, y2, z2 = b
+    return np.array([w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2, w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+                     w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2, w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2])
+
+
+def ident_pose(t=(0.0, 0.0, 0.0)):
+    return np.array([1.0, 0, 0, 0, *t])
+
+
+# ---------------------------------------------------------------- O1 covariance
+def test_covariance_closed_forms(oracle_mod):
+    O = oracle_mod
+    assert np.allclose(O.covariance([1, 0, 0, 0], [1, 1, 1]), np.eye(3), atol=1e-15)
+    assert np.allclose(O.covariance([1, 0, 0, 0], [2, 1, 1]), np.diag([4, 1, 1]), atol=1e-15)
+    q90 = [math.cos(math.pi / 4), 0, 0, math.sin(math.pi / 4)]
+    assert np.allclose(O.covariance(q90, [2, 1, 1]), np.diag([1, 4, 1]), atol=1e-12)
+
+
+def test_rotation_matches_scipy_and_equivariance(oracle_mod):
+    O = oracle_mod
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        q = rng.normal(size=4)
+        R = O.quat_to_rot(q)
+        Rs = Rotation.from_quat([q[1], q[2], q[3], q[0]]).as_matrix()  # scipy: scalar-last
+        assert np.allclose(R, Rs, atol=1e-12)
+        q1 = rng.normal(size=4)
+        q1 /= np.linalg.norm(q1)
+        s = rng.uniform(0.1, 2, 3)
+        lhs = O.covariance(qmul(q1, q / np.linalg.norm(q)), s)
+        R1 = O.quat_to_rot(q1)
+        assert np.allclose(lhs, R1 @ O.covariance(q, s) @ R1.T, atol=1e-10)
+        assert np.allclose(np.sort(np.linalg.eigvalsh(O.covariance(q, s))), np.sort(s ** 2), atol=1e-10)
+
+
+# ---------------------------------------------------------------- O2 sigma points / UT
+@pytest.mark.parametrize("ut", [(1.0, 2.0, 0.0), (0.5, 2.0, 1.0), (1.0, 0.0, 2.0)])
+def test_sigma_points_reproduce_moments(oracle_mod, ut):
+    O = oracle_mod
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        mu, q, s = rng.normal(size=3) * 5, rng.normal(size=4), rng.uniform(0.01, 1.0, 3)
+        pts, wm, wc = O.sigma_points(mu, q, s, ut)
+        assert pts.shape == (7, 3)
+        assert abs(wm.sum() - 1.0) < 1e-12
+        mean = (wm[:, None] * pts).sum(0)
+        cov = sum(wc[i] * np.outer(pts[i] - mu, pts[i] - mu) for i in range(7))
+        assert np.allclose(mean, mu, atol=1e-12)
+        assert np.allclose(cov, O.covariance(q, s), atol=1e-12)
+
+
+@pytest.mark.parametrize("ut", [(1.0, 2.0, 0.0), (0.7, 2.0, 0.5)])
+def test_ut_exact_for_affine_sensor(oracle_mod, ut):
+    """north star: the UT of a linear projection equals the exact projected covariance."""
+    O = oracle_mod
+    rng = np.random.default_rng(2)
+    for _ in range(50):
+        mu, q, s = rng.normal(size=3) * 3, rng.normal(size=4), rng.uniform(0.01, 2.0, 3)
+        A, b = rng.normal(size=(2, 3)), rng.normal(size=2)
+        mean, cov = O.ut_affine(mu, q, s, A, b, ut)
+        Sig = O.covariance(q, s)
+        assert np.allclose(mean, A @ mu + b, atol=1e-12)
+        assert np.allclose(cov, A @ Sig @ A.T, atol=1e-12)
+
+
+def test_ut_lidar_monte_carlo(oracle_mod):
+    """UT conic of Eq. 3 vs 1e5 samples through atan2/asin: within 2% Frobenius."""
+    O = oracle_mod
+    cfg = S.lidar_config("A")
+    rng = np.random.default_rng(3)
+    cases = [((10.0, 0, 0), (0.3, 0.3, 0.3)), ((0, 10.0, 1.0), (0.5, 0.2, 0.1)), ((-5.0, 3.0, -1.0), (0.4, 0.1, 0.6))]
+    for mu, s in cases:
+        q = rng.normal(size=4)
+        scene = {"means": np.array([mu], np.float32), "quats": np.array([q], np.float32),
+                 "scales": np.array([s], np.float32), "opacity": np.array([0.9], np.float32),
+                 "sh": np.zeros((1, 16, 3), np.float32)}
+        p0 = S.pose([1, 0, 0, 0], [0, 0, 0])
+        proj = O.project_lidar(scene, cfg, p0, p0, K=0)
+        Sig = O.covariance(q, np.asarray(s, np.float32).astype(np.float64))
+        x = rng.multivariate_normal(np.asarray(mu, np.float32).astype(np.float64), Sig, 100000)
+        r = np.linalg.norm(x, axis=1)
+        ang = np.stack([np.arctan2(x[:, 1], x[:, 0]), np.arcsin(x[:, 2] / r)], 1)
+        C = np.cov(ang.T)
+        ut = proj["cov2d"][0]
+        Cu = np.array([[ut[0], ut[1]], [ut[1], ut[2]]])
+        assert np.linalg.norm(Cu - C) / np.linalg.norm(C) < 0.02
+        assert np.allclose(proj["mean2d"][0], ang.mean(0), atol=3 * np.sqrt(np.diag(C)).max() / 100)
+
+
+# ---------------------------------------------------------------- O3 poses (A4)
+def test_pose_interpolation(oracle_mod):
+    O = oracle_mod
+    p = np.array([0.9, 0.1, -0.2, 0.3, 1.0, 2.0, 3.0])
+    for s in (0.0, 0.3, 1.0):
+        R, t = O.pose_at(p, p, s)
+        assert np.array_equal(R, O.quat_to_rot(p[:4])) and np.array_equal(t, p[4:])
+    a, b = ident_pose((0, 0, 0)), ident_pose((1.0, 0, 0))  # 10 m/s over 0.1 s
+    assert np.allclose(O.pose_at(a, b, 1.0)[1], [1.0, 0, 0]) and np.allclose(O.pose_at(a, b, 0.5)[1], [0.5, 0, 0])
+    yaw90 = np.array([math.cos(math.pi / 4), 0, 0, math.sin(math.pi / 4), 0, 0, 0])
+    R, _ = O.pose_at(ident_pose(), yaw90, 0.5)
+    assert np.allclose(R, Rotation.from_euler("z", 45, degrees=True).as_matrix(), atol=1e-12)
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        q0, q1 = rng.normal(size=4), rng.normal(size=4)
+        q0 /= np.linalg.norm(q0)
+        q1 /= np.linalg.norm(q1)
+        sl = Slerp([0, 1], Rotation.from_quat([[*q0[1:], q0[0]], [*q1[1:], q1[0]]]))
+        for s in (0.25, 0.5, 0.9):
+            R, _ = O.pose_at(np.r_[q0, 0, 0, 0], np.r_[q1, 0, 0, 0], s)
+            assert np.allclose(R, sl([s]).as_matrix()[0], atol=1e-10)
+
+
+# ---------------------------------------------------------------- O4 Eq. 3 + rolling shutter
+def test_eq3_axis_points(oracle_mod):
+    O = oracle_mod
+    cfg = S.lidar_config("A")
+    p = ident_pose()
+    assert np.allclose(O.lidar_point([1, 0, 0], cfg, p, p, 0)[:3], [0, 0, 1], atol=1e-15)
+    assert np.allclose(O.lidar_point([0, 1, 0], cfg, p, p, 0)[:3], [math.pi / 2, 0, 1], atol=1e-15)
+    assert np.allclose(O.lidar_point([0, 0, 1], cfg, p, p, 0)[:3], [0, math.pi / 2, 1], atol=1e-15)
+
+
+def test_rolling_shutter_static_bitwise_and_fixed_point(oracle_mod):
+    from scipy.optimize import brentq
+    O = oracle_mod
+    cfg = S.lidar_config("A")
+    p = np.array([0.98, 0.0, 0.05, 0.2, 0.3, -0.1, 1.8])
+    x = np.array([7.0, -3.0, 0.5])
+    a = O.lidar_point(x, cfg, p, p, 0)
+    for K in (1, 2, 5):
+        b = O.lidar_point(x, cfg, p, p, K)
+        assert np.array_equal(a[:3], b[:3])
+    # linear motion along +y at 5 m per revolution; point at (10, 0, 0): phi(s) = atan2(-5 s, 10)
+    p0, p1 = ident_pose((0, 0, 0)), ident_pose((0, 5.0, 0))
+    a0 = float(np.float32(cfg.azimuth_start))  # the ABI's float32 phi_start
+    f = lambda s: (math.atan2(-5.0 * s, 10.0) - a0) / (2 * math.pi) - s  # noqa: E731
+    s_star = brentq(f, 0.0, 1.0, xtol=1e-15)
+    errs = [abs(O.lidar_point([10, 0, 0], cfg, p0, p1, K)[3] - s_star) for K in range(1, 14)]
+    assert errs[-1] < 1e-9
+    assert all(e2 <= e1 * 0.2 + 1e-15 for e1, e2 in zip(errs, errs[1:]))  # geometric contraction
+
+
+def test_seam_continuity(oracle_mod):
+    """A Gaussian swept across phi = pi (co-rotating with its azimuth, so by symmetry about
+    z its conic must stay the same) keeps a continuous conic and box."""
+    O = oracle_mod
+    cfg = S.lidar_config("A")
+    p = S.pose([1, 0, 0, 0], [0, 0, 0])
+    angs = np.linspace(math.pi - 0.02, math.pi + 0.02, 81)
+    means = np.stack([10 * np.cos(angs), 10 * np.sin(angs), np.full_like(angs, 1.0)], 1)
+    base = np.array([0.9, 0.1, 0.2, 0.3])
+    quats = np.array([qmul([math.cos(a / 2), 0, 0, math.sin(a / 2)], base) for a in angs])
+    n = len(angs)
+    scene = {"means": means.astype(np.float32), "quats": quats.astype(np.float32),
+             "scales": np.tile(np.array([[0.3, 0.1, 0.2]], np.float32), (n, 1)),
+             "opacity": np.full(n, 0.5, np.float32), "sh": np.zeros((n, 16, 3), np.float32)}
+    proj = O.project_lidar(scene, cfg, p, p, K=0)
+    cov = proj["cov2d"]
+    assert np.abs(cov - cov[0]).max() < 1e-5 * np.abs(cov).max()  # float32 inputs -> ~1e-7 rel.
+    width = proj["box"][:, 1].astype(np.float64) - proj["box"][:, 0]
+    assert np.abs(width - width[0]).max() < 1e-6
+    assert ((proj["mean2d"][:, 0] >= -math.pi) & (proj["mean2d"][:, 0] < math.pi)).all()
+    mean_unwrapped = np.unwrap(proj["mean2d"][:, 0])
+    off = mean_unwrapped - angs  # constant UT bias (w_m0 = 0), no jump at the seam
+    assert np.abs(off - off[0]).max() < 1e-6 and abs(off[0]) < 1e-3
+
+
+# ---------------------------------------------------------------- O9 SH
+def _real_sh_scipy(l, m, theta, phi):
+    from scipy.special import sph_harm_y
+    if m == 0:
+        return sph_harm_y(l, 0, theta, phi).real
+    y = sph_harm_y(l, abs(m), theta, phi)
+    return math.sqrt(2) * (-1) ** m * (y.imag if m < 0 else y.real)
+
+
+def test_sh_basis_orthonormal_and_scipy(oracle_mod):
+    O = oracle_mod
+    # quadrature over the sphere: Gauss-Legendre in cos(theta) x uniform phi
+    xg, wg = np.polynomial.legendre.leggauss(24)
+    phis = np.linspace(0, 2 * np.pi, 48, endpoint=False)
+    B, W = [], []
+    for ct, w in zip(xg, wg):
+        st = math.sqrt(1 - ct * ct)
+        for ph in phis:
+            d = np.array([st * math.cos(ph), st * math.sin(ph), ct])
+            row = []
+            for k in range(16):
+                sh = np.zeros((16, 3))
+                sh[k, 0] = 1.0
+                row.append(O.sh_eval(sh, d)[0])
+            B.append(row)
+            W.append(w * 2 * np.pi / len(phis))
+    B, W = np.array(B), np.array(W)
+    G = (B * W[:, None]).T @ B
+    assert np.allclose(G, np.eye(16), atol=1e-10)
+    # each basis function equals +-(scipy real SH) of its degree (3DGS sign convention)
+    rng = np.random.default_rng(5)
+    lm = [(0, 0)] + [(1, m) for m in (-1, 0, 1)] + [(2, m) for m in range(-2, 3)] + [(3, m) for m in range(-3, 4)]
+    dirs = rng.normal(size=(20, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    for k, (l, m) in enumerate(lm):
+        ours, ref = [], []
+        for d in dirs:
+            sh = np.zeros((16, 3))
+            sh[k, 0] = 1.0
+            ours.append(O.sh_eval(sh, d)[0])
+            ref.append(_real_sh_scipy(l, m, math.acos(d[2]), math.atan2(d[1], d[0])))
+        ours, ref = np.array(ours), np.array(ref)
+        sgn = np.sign(np.dot(ours, ref))
+        assert np.allclose(ours, sgn * ref, atol=1e-12), (l, m)
+
+
+def test_sh_dc_parity_linearity(oracle_mod):
+    O = oracle_mod
+    rng = np.random.default_rng(6)
+    sh = np.zeros((16, 3))
+    sh[0] = [1.0, 2.0, -3.0]
+    for _ in range(5):
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        assert np.allclose(O.sh_eval(sh, d), np.array([1, 2, -3]) * 0.2820947918, atol=1e-10)
+    z = np.zeros((16, 3))
+    z[2, 0] = 1.0  # degree-1 z coefficient
+    assert np.isclose(O.sh_eval(z, [0, 0, 1])[0], -O.sh_eval(z, [0, 0, -1])[0])
+    a, b = rng.normal(size=(16, 3)), rng.normal(size=(16, 3))
+    d = np.array([0.3, -0.5, 0.81])
+    d /= np.linalg.norm(d)
+    assert np.allclose(O.sh_eval(2 * a - 3 * b, d), 2 * O.sh_eval(a, d) - 3 * O.sh_eval(b, d), atol=1e-12)
+
+
+# ---------------------------------------------------------------- O12 response
+def _mrows(q, s):
+    R = Rotation.from_quat([q[1], q[2], q[3], q[0]]).as_matrix()
+    return (R.T / np.asarray(s)[:, None]).reshape(-1)
+
+
+def test_response_closed_forms(oracle_mod):
+    O = oracle_mod
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        mu = rng.normal(size=3) * 10
+        q, s = rng.normal(size=4), rng.uniform(0.05, 2.0, 3)
+        o = rng.normal(size=3)
+        d = mu - o
+        d /= np.linalg.norm(d)
+        tau, d2 = O.response(mu, _mrows(q, s), o, d)  # ray through the mean
+        assert abs(tau - np.linalg.norm(mu - o)) < 1e-9 and abs(d2) < 1e-12
+        # analytic tau_max = d^T Sigma^-1 (mu - o) / d^T Sigma^-1 d ; delta^2 = min Mahalanobis
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        Sinv = np.linalg.inv(O.covariance(q, s))
+        tau_a = d @ Sinv @ (mu - o) / (d @ Sinv @ d)
+        x = o + tau_a * d - mu
+        tau, d2 = O.response(mu, _mrows(q, s), o, d)
+        assert abs(tau - tau_a) < 1e-8 * (1 + abs(tau_a))
+        assert abs(d2 - x @ Sinv @ x) < 1e-8 * (1 + d2)
+    # isotropic: tau = (mu - o).d ; unit Mahalanobis -> exp(-1/2)
+    mu, o, d = np.array([5.0, 1.0, 0.0]), np.zeros(3), np.array([1.0, 0, 0])
+    tau, d2 = O.response(mu, _mrows([1, 0, 0, 0], [1, 1, 1]), o, d)
+    assert tau == pytest.approx(5.0) and d2 == pytest.approx(1.0) and math.exp(-d2 / 2) == pytest.approx(0.60653066)
+
+
+def test_response_dense_scan(oracle_mod):
+    """argmax of rho along the ray from a 1e4-step scan agrees within one step."""
+    O = oracle_mod
+    rng = np.random.default_rng(8)
+    for _ in range(50):
+        mu = rng.normal(size=3) * 3 + np.array([6.0, 0, 0])
+        q, s = rng.normal(size=4), rng.uniform(0.1, 1.0, 3)
+        o, d = np.zeros(3), rng.normal(size=3) * 0.2 + np.array([1.0, 0, 0])
+        d /= np.linalg.norm(d)
+        Sinv = np.linalg.inv(O.covariance(q, s))
+        taus = np.linspace(0, 15, 10001)
+        X = o[None] + taus[:, None] * d[None] - mu[None]
+        m = np.einsum("ni,ij,nj->n", X, Sinv, X)
+        tau, d2 = O.response(mu, _mrows(q, s), o, d)
+        assert abs(taus[np.argmin(m)] - tau) <= (taus[1] - taus[0]) * 1.01 or tau < 0 or tau > 15
+        assert d2 <= m.min() + 1e-9
+
+
+# ---------------------------------------------------------------- O12 compositing
+def _one_ray(O, mus, sigmas, feats, s=0.05, near=0.1, alpha_max=0.99, T_min=1e-4, alpha_min=1 / 255):
+    n = len(mus)
+    rec = {"mu": np.array(mus, float), "Mrows": np.tile(_mrows([1, 0, 0, 0], [s, s, s]), (n, 1)),
+           "sigma": np.array(sigmas, float), "feat": np.array(feats, float),
+           "box": np.tile(np.array([[-1, 1, -1, 1]], np.float32), (n, 1))}
+    keys = np.array([np.linalg.norm(m) for m in mus], np.float32)
+    ids, ranges = O.sort_all(np.ones(n, np.int32), keys)
+    od = np.array([[0, 0, 0, 1.0, 0, 0]])
+    return O.composite(rec, ids, ranges, np.zeros(1, np.int32), np.zeros(1, np.float32), np.zeros(1, np.float32),
+                       od, wrap=1, near=near, alpha_max=alpha_max, T_min=T_min, alpha_min=alpha_min)
+
+
+def test_composite_worked_examples(oracle_mod):
+    O = oracle_mod
+    out = _one_ray(O, [[4.0, 0, 0]], [0.8], [[1, 1, 1]])
+    assert out["opacity"][0] == pytest.approx(0.8) and out["depth"][0] == pytest.approx(4.0)
+    out = _one_ray(O, [[5.0, 0, 0], [2.0, 0, 0]], [0.5, 0.5], [[1, 0, 0], [1, 0, 0]])
+    assert out["opacity"][0] == pytest.approx(0.75) and out["depth"][0] == pytest.approx(3.0)
+    empty = _one_ray(O, [[5.0, 0, 0]], [0.5], [[0, 0, 0]], near=100.0)  # nothing in front -> no return
+    g, bd = O.decode_lidar(empty["feat"])
+    assert empty["opacity"][0] == 0 and bd[0] == pytest.approx(0.5)
+
+
+def test_composite_conservation_and_termination(oracle_mod):
+    O = oracle_mod
+    rng = np.random.default_rng(9)
+    for trial in range(20):
+        n = 60
+        mus = np.stack([rng.uniform(1, 30, n), rng.normal(0, 0.03, n), rng.normal(0, 0.03, n)], 1)
+        sig = rng.uniform(0.05, 0.99, n)
+        out = _one_ray(O, mus, sig, np.ones((n, 3)))
+        assert out["opacity"][0] + out["T_final"][0] == pytest.approx(1.0, abs=1e-12)
+        assert out["opacity"][0] <= 1.0
+        out0 = _one_ray(O, mus, sig, np.ones((n, 3)), T_min=0.0)
+        assert abs(out0["opacity"][0] - out["opacity"][0]) < 1e-3
+        # T monotone: removing the tail can only raise T
+        outh = _one_ray(O, mus[np.argsort(np.linalg.norm(mus, axis=1))][: n // 2],
+                        sig[np.argsort(np.linalg.norm(mus, axis=1))][: n // 2], np.ones((n // 2, 3)), T_min=0.0)
+        assert outh["T_final"][0] >= out0["T_final"][0] - 1e-15
+
+
+def test_decode_closed_forms(oracle_mod):
+    O = oracle_mod
+    g, bd = O.decode_lidar(np.array([[0.3, math.log(3.0), 0.0], [0.5, 1.7, 1.7], [0, 50.0, -50.0], [0, -50.0, 50.0]]))
+    assert g[0] == 0.3 and bd[0] == pytest.approx(0.25) and bd[1] == pytest.approx(0.5)
+    assert np.isfinite(bd).all() and bd[2] < 1e-40 and bd[3] == pytest.approx(1.0)
+
+
+def test_opaque_wall_depth(oracle_mod):
+    """Opaque wall of particles at 10 m -> hit rays return 10 m within 0.05 m."""
+    O = oracle_mod
+    cfg = S.lidar_config("A")
+    ys, zs = np.meshgrid(np.arange(-8, 8, 0.1), np.arange(-3.0, 4.0, 0.1))
+    n = ys.size
+    scene = {"means": np.stack([np.full(n, 10.0), ys.ravel(), zs.ravel()], 1).astype(np.float32),
+             "quats": np.tile(np.array([[1, 0, 0, 0]], np.float32), (n, 1)),
+             "scales": np.tile(np.array([[0.01, 0.08, 0.08]], np.float32), (n, 1)),
+             "opacity": np.full(n, 0.99, np.float32), "sh": np.zeros((n, 16, 3), np.float32)}
+    p = S.pose([1, 0, 0, 0], [0, 0, 0])
+    out = O.render_lidar(scene, cfg, pose0=p, pose1=p)
+    od = out["ray_od"]
+    hit = out["opacity"] > 0.99
+    assert hit.sum() > 50
+    expect = 10.0 / od[hit, 3]  # plane x = 10 along each ray
+    assert np.abs(out["depth"][hit] - expect).max() < 0.05
+
+
+# ---------------------------------------------------------------- O7 tiling
+def _tiling_for(beams_rad, A, n_phi, M, cull_az=1600):
+    cfg = S.LidarConfig("t", np.asarray(beams_rad, np.float32), A, n_phi=n_phi, max_rays_per_tile=M,
+                        cull_az_cells=cull_az)
+    from oracle import oracle as O
+    return O.Tiling(cfg)
+
+
+def test_proc1_handworked_golden(oracle_mod):
+    g = json.load(open(os.path.join(GOLDEN, "proc1_handworked.json")))
+    t = _tiling_for(np.radians(np.array(g["elevations_deg"], np.float64)).astype(np.float32), g["n_azimuth"],
+                    g["n_phi"], g["M"])
+    assert t.n_phi == g["expect_n_phi"] and t.n_theta == g["expect_n_theta"]
+    exp = np.radians(np.array(g["expect_bounds_deg"]))
+    assert np.allclose(t.bounds, exp, atol=1e-7)
+    assert (np.diff(t.tile_ray_offsets) == g["expect_rays_per_tile"]).all()
+    assert list(t.ray_tile[: g["n_azimuth"]] % t.n_theta) == g["expect_ray_cols"]
+
+
+def test_proc1_uniform_quartiles(oracle_mod):
+    """64 uniform beams in [-25, 15] deg, N_phi=4 -> 16/16/16/16, boundaries in the
+    gap between beams 15|16, 31|32, 47|48 (A8 reading of 'cross integer boundaries')."""
+    beams = np.radians(np.linspace(-25.0, 15.0, 64)).astype(np.float32)
+    t = _tiling_for(beams, 1800, 4, 32)
+    assert t.n_phi == 4
+    counts = np.bincount([t.elev_tile(float(b)) for b in beams], minlength=4)
+    assert list(counts) == [16, 16, 16, 16]
+    for k, (lo, hi) in enumerate([(15, 16), (31, 32), (47, 48)]):
+        assert beams[lo] < t.bounds[k + 1] <= beams[hi]
+        assert abs(float(t.bounds[k + 1]) - 0.5 * (float(beams[lo]) + float(beams[hi]))) < 1e-7
+    assert t.n_theta == math.ceil(16 * 1800 / 32)
+
+
+def test_proc1_skewed_and_invariants(oracle_mod):
+    beams = np.radians(np.r_[np.linspace(-1.0, 3.0, 60, endpoint=False), np.linspace(3.0, 19.0, 4)]).astype(np.float32)
+    t = _tiling_for(beams, 1800, 4, 32)
+    inside = sum(1 for k in range(t.n_phi) if t.bounds[k] >= np.radians(-1.0) - 1e-7
+                 and t.bounds[k + 1] <= np.radians(3.0) + 1e-7)
+    assert inside >= 3
+    rng = np.random.default_rng(10)
+    for trial in range(40):
+        B = int(rng.integers(1, 80))
+        beams = np.sort(rng.uniform(-0.5, 0.3, B)).astype(np.float32)
+        if trial % 5 == 0:
+            beams = np.round(beams, 2).astype(np.float32)  # duplicates / shared bins
+        A = int(rng.integers(16, 400))
+        n_phi = int(rng.integers(1, 40))
+        prev = None
+        for M in (8, 16, 32, 64, 128, 256):
+            t = _tiling_for(beams, A, n_phi, M)
+            assert 1 <= t.n_phi <= n_phi and t.bounds.shape[0] <= n_phi + 1
+            assert np.all(np.diff(t.bounds) > 0) or t.n_phi == 1
+            assert t.tile_ray_offsets[-1] == B * A  # total occupancy = ray count
+            beams_per = np.bincount([t.elev_tile(float(b)) for b in beams], minlength=t.n_phi)
+            assert (beams_per > 0).all()  # no empty elevation tile
+            assert t.n_theta == min(A, max(1, math.ceil(beams_per.max() * A / M)))
+            if prev is not None:
+                assert t.n_theta <= prev  # non-increasing in M
+            prev = t.n_theta
+            if beams_per.max() <= M and M % beams_per.max() == 0 and A % t.n_theta == 0:
+                assert t.max_rays_in_tile <= M  # "count per tile under M"
+        t2 = _tiling_for(beams, A, n_phi, 32)
+        t3 = _tiling_for(beams, A, n_phi, 32)
+        assert np.array_equal(t2.bounds, t3.bounds) and np.array_equal(t2.sat, t3.sat)  # bit-identical reruns
+
+
+def test_tiling_paper_configs(oracle_mod):
+    for name, exp in (("A", (8, 64, 32)), ("B", (16, 225, 32)), ("C", (16, 332, 32))):
+        t = oracle_mod.Tiling(S.lidar_config(name))
+        assert (t.n_phi, t.n_theta, t.max_rays_in_tile) == exp
+        assert t.tile_ray_offsets[-1] == t.n_rays
+
+
+# ---------------------------------------------------------------- SAT + culling
+def test_sat_bruteforce(oracle_mod):
+    O = oracle_mod
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        h, w = rng.integers(1, 64, 2)
+        mask = (rng.uniform(size=(h, w)) < rng.uniform(0, 0.5)).astype(np.int32)
+        sat = np.zeros((h + 1, w + 1), np.int32)
+        sat[1:, 1:] = mask.cumsum(0).cumsum(1)
+        for _ in range(50):
+            r0, r1 = np.sort(rng.integers(0, h, 2))
+            c0, c1 = np.sort(rng.integers(0, w, 2))
+            assert O.sat_query(sat, r0, r1, c0, c1) == mask[r0:r1 + 1, c0:c1 + 1].sum()
+    z = np.zeros((4, 4), np.int32)
+    assert O.sat_query(z, 0, 2, 0, 2) == 0
+    f = np.zeros((4, 4), np.int32)
+    f[1:, 1:] = np.ones((3, 3)).cumsum(0).cumsum(1)
+    assert O.sat_query(f, 0, 2, 0, 2) == 9
+
+
+def test_oracle_sat_matches_mask(oracle_mod):
+    t = oracle_mod.Tiling(S.lidar_config("B"))
+    rows, cols = t.sat_rows - 1, t.sat_cols - 1
+    mask = np.zeros((rows, cols), np.int32)
+    mask[t.ray_cell_row, t.ray_cell_col] = 1
+    ref = np.zeros_like(t.sat)
+    ref[1:, 1:] = mask.cumsum(0).cumsum(1)
+    assert np.array_equal(ref, t.sat)
+
+
+def _membership(box, a, b, pi_f, two_pi_f):
+    """Per-ray box membership (numpy float32 restatement of the O12 rule, for invariants);
+    a, b are float32 arrays of ray azimuth / elevation."""
+    lo, hi, lb, hb = [np.float32(x) for x in box]
+    inb = (lb <= b) & (b <= hb)
+    if np.float32(hi - lo) >= two_pi_f:
+        return inb
+    m = (lo <= a) & (a <= hi)
+    if lo < -pi_f:
+        m |= np.float32(lo + two_pi_f) <= a
+    if hi > pi_f:
+        m |= a <= np.float32(hi - two_pi_f)
+    return inb & m
+
+
+@pytest.mark.parametrize("config", ["A", "tiny"])
+def test_culling_exact_and_rect_contains_members(oracle_mod, config):
+    """Culled => no ray inside the box; every member ray's tile lies in the rect."""
+    O = oracle_mod
+    cfg = S.lidar_config(config)
+    t = O.Tiling(cfg)
+    scene = S.scene_for(config, seed=3)
+    proj = O.project_lidar(scene, cfg)
+    count, rect = O.cull_lidar(proj["valid"], proj["box"], t, True)
+    count0, _ = O.cull_lidar(proj["valid"], proj["box"], t, False)
+    assert (count <= count0).all()
+    tiles_of = lambda g: {r * t.n_theta + (rect[g, 2] + c) % t.n_theta  # noqa: E731
+                          for r in range(rect[g, 0], rect[g, 1] + 1) for c in range(rect[g, 3])}
+    for g in np.nonzero(proj["valid"])[0][:300]:
+        members = np.nonzero(_membership(proj["box"][g], t.ray_az, t.ray_el, t.pi_f, t.two_pi_f))[0]
+        if count[g] == 0:
+            assert len(members) == 0
+        else:
+            assert {int(t.ray_tile[r]) for r in members} <= tiles_of(g)
+
+
+# ---------------------------------------------------------------- O13 tiled == brute force
+def test_tiled_equals_bruteforce_config_a(oracle_mod):
+    O = oracle_mod
+    cfg = S.lidar_config("A")
+    scene = S.scene_for("A")
+    a = O.render_lidar(scene, cfg, mode="tiled")
+    b = O.render_lidar(scene, cfg, mode="brute")
+    for k in ("feat", "opacity", "depth_accum", "T_final", "n_contrib"):
+        assert np.array_equal(a[k], b[k]), k
+    assert (a["opacity"] > 0).mean() > 0.1
+
+
+def test_tiled_equals_bruteforce_tiny_scenes(oracle_mod):
+    O = oracle_mod
+    for seed in range(100):
+        cfg = S.lidar_config("tiny")
+        if seed % 3 == 1:
+            cfg.n_phi, cfg.max_rays_per_tile = 2, 64
+        if seed % 3 == 2:
+            cfg.cull_az_cells = 1600
+        scene = S.scene_for("tiny", seed=seed)
+        a = O.render_lidar(scene, cfg, mode="tiled", enable_cull=(seed % 2 == 0))
+        b = O.render_lidar(scene, cfg, mode="brute")
+        for k in ("feat", "opacity", "depth_accum", "T_final", "n_contrib"):
+            assert np.array_equal(a[k], b[k]), (seed, k)
+
+
+def test_tiling_invariance_of_outputs(oracle_mod):
+    """Tiling choice 'does not affect quality': outputs bit-identical across (N_phi, M)."""
+    O = oracle_mod
+    scene = S.scene_for("A")
+    ref = None
+    for n_phi, M in ((8, 32), (4, 64), (2, 256), (16, 16)):
+        cfg = S.lidar_config("A")
+        cfg.n_phi, cfg.max_rays_per_tile = n_phi, M
+        out = O.render_lidar(scene, cfg)
+        if ref is None:
+            ref = out
+        else:
+            for k in ("feat", "opacity", "depth_accum", "T_final", "n_contrib"):
+                assert np.array_equal(ref[k], out[k])
+
+
+def test_bin_sets_and_order(oracle_mod):
+    O = oracle_mod
+    cfg = S.lidar_config("tiny")
+    t = O.Tiling(cfg)
+    scene = S.scene_for("tiny", seed=7)
+    proj = O.project_lidar(scene, cfg)
+    count, rect = O.cull_lidar(proj["valid"], proj["box"], t, False)
+    keys, ids, ranges = O.bin_pairs(count, rect, proj["key"], t.n_tiles, t.n_theta)
+    assert len(ids) == count.sum()
+    kb = proj["key"].view(np.uint32)
+    for tile in range(t.n_tiles):
+        lo, hi = ranges[tile]
+        lst = ids[lo:hi]
+        expect = sorted([g for g in range(len(count)) if count[g] and
+                         tile in {r * t.n_theta + (rect[g, 2] + c) % t.n_theta
+                                  for r in range(rect[g, 0], rect[g, 1] + 1) for c in range(rect[g, 3])}],
+                        key=lambda g: (kb[g], g))
+        assert list(lst) == expect
+
+
+def test_depth_key_is_float32_distance(oracle_mod):
+    O = oracle_mod
+    scene = S.scene_for("A")
+    cfg = S.lidar_config("B")
+    proj = O.project_lidar(scene, cfg)
+    t0, t1 = cfg.pose_start["t"], cfg.pose_end["t"]
+    om = (t0 + np.float32(0.5) * (t1 - t0)).astype(np.float32)
+    d = (scene["means"] - om).astype(np.float32)
+    key = np.sqrt(((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]).astype(np.float32))
+    assert np.array_equal(key, proj["key"])
+
+
+# ---------------------------------------------------------------- O6 camera
+def test_camera_closed_forms(oracle_mod):
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    cam.k = (0.0, 0.0, 0.0, 0.0, 0.0)  # equidistant fisheye: r = f theta
+    p = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    for th in (0.0, 0.3, 1.0, 1.5):
+        x = np.array([math.sin(th), 0.0, math.cos(th)]) * 5
+        ok, uv = O.camera_point(x, cam, p, p, 0)
+        assert ok and uv[0] == pytest.approx(cam.cx + cam.fx * th) and uv[1] == pytest.approx(cam.cy)
+    pin = S.camera_config("pinhole-small")
+    pin.k = (0.0,) * 5
+    ok, uv = O.camera_point(np.array([1.0, -0.5, 4.0]), pin, p, p, 0)
+    assert uv[0] == pytest.approx(pin.fx * 0.25 + pin.cx) and uv[1] == pytest.approx(pin.fy * -0.125 + pin.cy)
+    # distorted models: unproject o project = identity
+    for cfg in (S.camera_config("D-small"), S.camera_config("pinhole-small")):
+        rng = np.random.default_rng(12)
+        for _ in range(100):
+            u, v = rng.uniform(0, cfg.width), rng.uniform(0, cfg.height)
+            ok, d = O.camera_unproject(cfg, u, v)
+            if not ok:
+                continue
+            ok2, uv = O.camera_point(d * 3.0, cfg, p, p, 0)
+            assert ok2 and abs(uv[0] - u) < 1e-8 and abs(uv[1] - v) < 1e-8
+
+
+def test_camera_rolling_shutter_degenerate(oracle_mod):
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    scene = S.scene_for("D", n=500)
+    p = cam.pose_start
+    a = O.project_camera(scene, cam, p, p, K=0)
+    b = O.project_camera(scene, cam, p, p, K=3)
+    assert np.array_equal(a["box"], b["box"], equal_nan=True) and np.array_equal(a["valid"], b["valid"])
+
+
+def test_camera_ut_monte_carlo(oracle_mod):
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    cam.rolling_shutter = 0
+    p = S.pose([1, 0, 0, 0], [0, 0, 0])
+    rng = np.random.default_rng(13)
+    for mu, s in (((0.0, 0.0, 6.0), (0.2, 0.2, 0.2)), ((2.0, -1.0, 5.0), (0.3, 0.1, 0.2))):
+        q = rng.normal(size=4)
+        scene = {"means": np.array([mu], np.float32), "quats": np.array([q], np.float32),
+                 "scales": np.array([s], np.float32), "opacity": np.array([0.9], np.float32),
+                 "sh": np.zeros((1, 16, 3), np.float32)}
+        proj = O.project_camera(scene, cam, p, p, K=0)
+        Sig = O.covariance(q, np.asarray(s, np.float32).astype(np.float64))
+        x = rng.multivariate_normal(np.asarray(mu, np.float32).astype(np.float64), Sig, 20000)
+        uv = np.array([O.camera_point(xx, cam, pose_np(p), pose_np(p), 0)[1][:2] for xx in x])
+        Cmc = np.cov(uv.T)
+        c = proj["cov2d"][0]
+        Cu = np.array([[c[0], c[1]], [c[1], c[2]]])
+        assert np.linalg.norm(Cu - Cmc) / np.linalg.norm(Cmc) < 0.03
+
+
+def pose_np(p):
+    return np.r_[np.asarray(p["q"], np.float64), np.asarray(p["t"], np.float64)]
+
+
+def test_camera_tiled_equals_bruteforce(oracle_mod):
+    O = oracle_mod
+    for name, seed in (("D-small", 1), ("pinhole-small", 2)):
+        cam = S.camera_config(name)
+        scene = S.corridor_scene(seed, 3000, x_range=(0.0, 40.0), kind="camera", ego=(1.5, 0, 1.6))
+        a = O.render_camera(scene, cam, mode="tiled")
+        b = O.render_camera(scene, cam, mode="brute")
+        for k in ("feat", "opacity", "depth_accum", "T_final", "n_contrib"):
+            assert np.array_equal(a[k], b[k]), (name, k)
+        assert (a["opacity"] > 0.01).mean() > 0.05
