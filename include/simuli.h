@@ -1,0 +1,292 @@
+/*
+ * simuli.h -- C ABI of the B200-native SimULi forward sensor-rendering hot path
+ * (arXiv 2510.12901).  libsimuli.so implements it with hand-written CUDA for sm_100a.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (section in brackets); readings of
+ * silent or garbled passages are DESIGN.md §3 ledger items "A<n>".
+ *
+ * The five calls, in path order:
+ *   simuli_build_tiles    Proc. ElevationTiling + ray table + culling SAT   [P:141-147, P:494-538]
+ *   simuli_project        7-sigma-point UT projection, ray-based culling,  [P:129, P:134-147,
+ *                         tile counts, depth keys, compositing records      P:544-562]
+ *   simuli_bin_sort       duplication into (tile|depth) keys + radix sort  [P:129 "as in 3DGS",
+ *                         + tile ranges                                     P:607 "Sort"]
+ *   simuli_render_lidar   per-ray front-to-back compositing, LiDAR decode  [P:114-129, Eq. 1]
+ *   simuli_render_camera  same for distorted rolling-shutter cameras       [P:112-129]
+ *
+ * ---- conventions (all calls) ----
+ * Status: every call returns int32: SIMULI_OK (0) or an error code below; the message of
+ *   the last error on the calling thread is simuli_last_error().  No exceptions cross the
+ *   ABI.  No global mutable state besides that thread-local message; calls on distinct
+ *   buffers / streams are thread-safe.
+ * Ownership: the library never allocates or frees memory.  Every buffer is caller-owned:
+ *   "host" pointers are ordinary CPU memory read/written during the call only; "device"
+ *   pointers are CUDA global memory (e.g. torch tensors) that must stay alive until the
+ *   enqueued work on `stream` has completed.  Scratch is the caller's `workspace`.
+ * Asynchrony: device work is enqueued on the caller's cudaStream_t (passed as void*, NULL =
+ *   legacy default stream); no call synchronises, except simuli_bin_sort with
+ *   pair_capacity < 0 (documented there).
+ * Degenerate particles are not errors: zero / non-finite quaternion or scale, a sigma
+ *   point closer than the minimum range / near plane, or a singular projected covariance
+ *   make a particle "invalid": tile count 0, never rendered (A20).
+ * Layouts: contiguous float32, row-major.  Quaternions are (w, x, y, z) and need not be
+ *   unit (normalised inside).  Scales are post-activation standard deviations (m, > 0);
+ *   opacity is post-sigmoid (A26).  SH coefficients are [n][(deg+1)^2][3]
+ *   (coefficient-major, channel-minor), degree <= 3 (48 values at degree 3).
+ *   Poses map sensor -> world.  LiDAR sensor frame: x forward, y left, z up (Eq. 3);
+ *   camera frame: OpenCV (x right, y down, z forward) (A6).
+ */
+#ifndef SIMULI_H
+#define SIMULI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIMULI_ABI_VERSION 1
+
+enum {
+  SIMULI_OK = 0,
+  SIMULI_ERR_INVALID_ARGUMENT = 1, /* bad pointer / size / parameter                         */
+  SIMULI_ERR_CAPACITY = 2,         /* a caller buffer is too small; *_required is filled    */
+  SIMULI_ERR_CUDA = 3,             /* a CUDA launch / API call failed (message has the text) */
+  SIMULI_ERR_UNSUPPORTED = 4       /* option not implemented (e.g. SH degree > 3)            */
+};
+
+enum { SIMULI_SENSOR_LIDAR = 0, SIMULI_SENSOR_CAMERA = 1 };
+enum { SIMULI_CAM_PINHOLE_RADTAN = 0, SIMULI_CAM_FISHEYE_KB = 1 };
+
+/* Thread-local text of the last error ("" if none).  Valid until the next call. */
+const char* simuli_last_error(void);
+int32_t simuli_abi_version(void);
+
+/* Rigid pose, sensor -> world: x_world = R(q) x_sensor + t. */
+typedef struct {
+  float q[4]; /* w, x, y, z */
+  float t[3];
+} simuli_pose;
+
+/* Spinning LiDAR (Fig. 3a; A5): every beam fires once per azimuth column;
+ * column j (0 <= j < n_azimuth) fires at normalised time s_j = (j + 0.5)/n_azimuth of the
+ * sweep, azimuth phi_j = wrap(azimuth_start + spin_direction (j + 0.5) 2 pi / n_azimuth).
+ * Ray id = beam * n_azimuth + column (range-image layout). */
+typedef struct {
+  int32_t n_beams;
+  const float* beam_elevation_rad; /* host [n_beams], any order, |omega| < pi/2         */
+  int32_t n_azimuth;               /* columns per revolution (A)                          */
+  float azimuth_start_rad;         /* phi_start in [-pi, pi)                              */
+  int32_t spin_direction;          /* +1: azimuth increases with time, -1: decreases      */
+  float min_range_m;               /* minimum range r_min (> 0)                           */
+} simuli_lidar;
+
+/* Tiling parameters: n_phi elevation tiles N_phi, M = max rays per tile,
+ * r = 400 histogram bins, dense culling grid 1600 azimuth cells x 8 rows per elevation
+ * tile (r^d_phi = 1600, r^d_omega = 8; A7, A10). */
+typedef struct {
+  int32_t n_phi;
+  int32_t max_rays_per_tile;
+  int32_t hist_bins;
+  int32_t cull_az_cells;
+  int32_t cull_rows_per_tile;
+} simuli_tiling_params;
+
+/* Output of simuli_build_tiles.  Host memory.  Call once with every array pointer NULL to
+ * get the sizes, allocate, call again to fill (the sizing fields are rewritten). */
+typedef struct {
+  /* sizes / scalars (always written) */
+  int32_t n_phi;            /* effective elevation tiles N_phi' <= requested n_phi         */
+  int32_t n_theta;          /* azimuth tiles N_theta = clamp(ceil(H_max / M), 1, A)        */
+  int32_t n_tiles;          /* n_phi * n_theta; tile id = elev_tile * n_theta + az_tile   */
+  int32_t max_rays_in_tile; /* may exceed M when beams per tile do not divide M (A9)      */
+  int32_t sat_rows, sat_cols; /* (8 n_phi + 1) x (1600 + 1)                              */
+  int32_t n_rays, n_beams, n_azimuth;
+  float pi_f, two_pi_f;     /* (float)pi, (float)(2 pi)                                    */
+  float az_tile_scale;      /* (float)(n_theta / 2pi)                                      */
+  float az_cell_scale;      /* (float)(cull_az_cells / 2pi)                                */
+  /* arrays (host, caller-allocated; NULL on the sizing call) */
+  float* elev_bounds;       /* [n_phi+1] float32 boundaries T, strictly increasing         */
+  float* cull_row_scale;    /* [n_phi] (float)(rows_per_tile / (T[k+1] - T[k]))             */
+  float* ray_az;            /* [n_rays] phi_j                                              */
+  float* ray_el;            /* [n_rays] omega_b                                            */
+  float* ray_s;             /* [n_rays] firing time s_j in [0, 1)                          */
+  int32_t* ray_tile;        /* [n_rays] render tile of each ray                             */
+  int32_t* tile_ray_offsets;/* [n_tiles+1] CSR tile -> rays                                 */
+  int32_t* tile_rays;       /* [n_rays] ray ids per tile, increasing                       */
+  int32_t* sat;             /* [sat_rows*sat_cols] summed-area table of the dense ray mask */
+  int32_t* elev_tile_beam_offsets; /* [n_phi+1] CSR elevation tile -> beams                */
+  int32_t* elev_tile_beams;        /* [n_beams]                                             */
+  int32_t* az_tile_col_offsets;    /* [n_theta+1] CSR azimuth tile -> columns               */
+  int32_t* az_tile_cols;           /* [n_azimuth]                                           */
+} simuli_tiling;
+
+/* Proc. ElevationTiling with the corrections of A8: histogram of per-ray
+ * elevations with r bins, one boundary per integer crossing of the normalised CDF
+ * (integer-exact test), boundaries at the float32 midpoint of the beam gap, empty tiles
+ * dropped, N_theta = ceil(H_max / M).  Also the ray table, tile -> ray CSR, dense ray
+ * mask and its zero-padded summed-area table.  Host only, once per
+ * sensor definition; the result is bit-exact and deterministic.
+ * Errors: INVALID_ARGUMENT for n_beams/n_azimuth/n_phi/M/bins/cells < 1, n_phi > hist_bins
+ * ("tile count exceeds histogram resolution"), |elevation| >= pi/2, |spin_direction| != 1.
+ * All elevations identical -> a single elevation tile (not an error). */
+int32_t simuli_build_tiles(const simuli_lidar* lidar, const simuli_tiling_params* params,
+                           simuli_tiling* inout);
+
+/* Device copy of a simuli_tiling (the caller uploads the arrays; the struct itself is
+ * host memory holding device pointers). */
+typedef struct {
+  int32_t n_phi, n_theta, n_tiles, max_rays_in_tile, sat_rows, sat_cols;
+  int32_t cull_az_cells, cull_rows_per_tile, n_rays, n_beams, n_azimuth;
+  float pi_f, two_pi_f, az_tile_scale, az_cell_scale;
+  const float *elev_bounds, *cull_row_scale, *ray_az, *ray_el, *ray_s;
+  const int32_t *ray_tile, *tile_ray_offsets, *tile_rays, *sat;
+  const int32_t *elev_tile_beam_offsets, *elev_tile_beams, *az_tile_col_offsets, *az_tile_cols;
+} simuli_tiling_dev;
+
+/* Gaussian particle set G_l or G_c: device pointers. */
+typedef struct {
+  int64_t n;
+  const float* means;   /* [n][3]              */
+  const float* quats;   /* [n][4] (w,x,y,z)    */
+  const float* scales;  /* [n][3]              */
+  const float* opacity; /* [n]                 */
+  const float* sh;      /* [n][(deg+1)^2][3]   */
+  int32_t sh_degree;    /* 0..3                */
+} simuli_gaussians;
+
+/* Camera (A22).  model PINHOLE_RADTAN: k = (k1, k2, p1, p2, k3) (OpenCV);
+ * FISHEYE_KB: k = (k1, k2, k3, k4, unused), theta_d = theta (1 + k1 th^2 + ... + k4 th^8).
+ * Pixel centres at (i + 0.5, j + 0.5); rolling shutter: row j fires at s = (j + 0.5)/H
+ * (top -> bottom); global shutter: s = 0.  tile_px must be a power of two (8, 16, 32). */
+typedef struct {
+  int32_t model;
+  int32_t width, height;
+  float fx, fy, cx, cy;
+  float k[5];
+  int32_t rolling_shutter;
+  float near_m;        /* near plane (KB: minimum distance; radtan: minimum depth z)   */
+  float max_theta_rad; /* KB validity limit on the ray angle                           */
+  int32_t tile_px;
+} simuli_camera;
+
+/* Parameters shared by projection and rendering of one sensor frame. */
+typedef struct {
+  int32_t kind;                     /* SIMULI_SENSOR_LIDAR | SIMULI_SENSOR_CAMERA          */
+  const simuli_lidar* lidar;        /* host struct (LiDAR)                                 */
+  const simuli_tiling_dev* tiling;  /* host struct of device pointers (LiDAR)              */
+  const simuli_camera* camera;      /* host struct (camera)                                */
+  simuli_pose pose_start;           /* pose at s = 0 (start of the sweep / first row)      */
+  simuli_pose pose_end;             /* pose at s = 1; lerp(t) + slerp(R) in between (A4)   */
+  int32_t rs_iterations;            /* K firing-time fixed-point iterations (A3), >= 0     */
+  float ut_alpha, ut_beta, ut_kappa;/* scaled-UT parameters (A1): default 1, 2, 0          */
+  float extent_sigma;               /* box half-width in std-devs (A11): default 3         */
+  int32_t enable_culling;           /* ray-based culling, LiDAR only: default 1    */
+  int32_t write_all_records;        /* 1: write the record of every particle (invalid ->
+                                       NaN box); 0: only particles with tile count > 0     */
+} simuli_project_params;
+
+/* Per-particle projection output (device, caller-allocated, n entries each).
+ * record[g] = 20 float32: mu[3], M[9] (row-major, M = diag(1/s) R^T, the canonical
+ * transform of P:129's 3D response), opacity, f[3] (SH features at the particle's
+ * view direction, A17), box lo_a, hi_a, lo_b, hi_b (LiDAR: azimuth/elevation, may extend
+ * past +-pi; camera: pixels).  tile_rect[g] = (row_lo, row_hi, col_start, n_cols): render
+ * tiles rows row_lo..row_hi x the circular column run col_start.. (mod n_cols_total).
+ * depth_key[g]: float32 range |mu - o_mid|, o_mid = t0 + 0.5 (t1 - t0), fixed op order
+ * without FMA (A19).  tile_count[g] = rows * n_cols, 0 if invalid or culled. */
+typedef struct {
+  float* record;
+  int32_t* tile_rect;
+  float* depth_key;
+  int32_t* tile_count;
+} simuli_projected;
+
+/* UT projection: 7 sigma points mu, mu +- sqrt(3+lambda) l_k (l_k = s_k R e_k,
+ * A2) pushed through the time-dependent sensor model: each sigma point is projected with
+ * the pose at its own firing time (K fixed-point iterations from s = 0, A3), LiDAR by
+ * Eq. 3, cameras by the lens model; UT mean / covariance -> axis-aligned box of
+ * extent_sigma std-devs (A11), rounded outward.  LiDAR: ray-based culling by the SAT
+ * rectangle count (Proc. RayOccupancyCount / ProjectParticles) and the
+ * coarse tile count; camera: tiles of tile_px pixels, no culling.
+ * Errors: INVALID_ARGUMENT (NULL / size mismatch / kind), UNSUPPORTED (sh_degree > 3),
+ * CUDA (launch failure).  Device pointers in `out` must hold n entries. */
+int32_t simuli_project(const simuli_gaussians* gaussians, const simuli_project_params* params,
+                       simuli_projected* out, void* stream);
+
+/* Scratch bytes simuli_bin_sort needs for n particles, pair_capacity pairs, n_tiles. */
+int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t n_tiles, size_t* bytes);
+
+/* Tile-Gaussian duplication and sort "as in 3DGS": exclusive scan of tile_count,
+ * one pair (key = tile << 32 | bits(depth_key), id = g) per (tile, particle), a stable
+ * LSD radix sort of the keys (onesweep, 8-bit digits over the 32 + ceil(log2 n_tiles)
+ * significant bits), and tile_ranges[t] = [begin, end) of tile t in the sorted arrays
+ * (0,0 if empty).  The order is (tile, depth key bits, id) -- unique, deterministic.
+ * n_cols_total: N_theta (LiDAR) or ceil(W / tile_px) (camera).
+ * sorted_keys / sorted_ids: device [pair_capacity]; tile_ranges: device [n_tiles][2];
+ * n_pairs_dev: device int64 (receives P).
+ * pair_capacity >= 0: fully asynchronous; if P > pair_capacity only the first
+ *   pair_capacity pairs are sorted and the result is INCOMPLETE -- the caller must check
+ *   *n_pairs_dev <= pair_capacity and retry with larger buffers.
+ * pair_capacity < 0: the call synchronises `stream` once after the scan; if P exceeds
+ *   |pair_capacity| it returns SIMULI_ERR_CAPACITY with *pairs_required (host) = P. */
+int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles, int32_t n_cols_total,
+                        void* workspace, size_t workspace_bytes, int64_t pair_capacity,
+                        uint64_t* sorted_keys, uint32_t* sorted_ids, int32_t* tile_ranges,
+                        int64_t* n_pairs_dev, int64_t* pairs_required, void* stream);
+
+/* Compositing thresholds (A13, A14): skip alpha < alpha_min (default 1/255), clamp alpha
+ * to alpha_max (0.99), stop a ray when T (1 - alpha) < T_min (1e-4) without compositing
+ * that particle. */
+typedef struct {
+  float alpha_min, alpha_max, T_min;
+} simuli_render_params;
+
+/* Per-ray LiDAR outputs (device, [n_rays] each; any pointer may be NULL to skip it).
+ * zeta [n_rays][3] = sum f_i alpha_i T_i; opacity omega = sum alpha_i T_i (Eq. 1);
+ * depth_accum D = sum tau_i alpha_i T_i; depth = D / omega (0 if omega = 0, A16);
+ * intensity gamma = zeta_0; raydrop beta_drop = softmax(zeta_1, zeta_2)_drop;
+ * final_T; n_contrib; ray_od [n_rays][6] double (origin, unit direction) as used. */
+typedef struct {
+  float* zeta;
+  float* opacity;
+  float* depth_accum;
+  float* depth;
+  float* intensity;
+  float* raydrop;
+  float* final_T;
+  int32_t* n_contrib;
+  double* ray_od;
+} simuli_lidar_out;
+
+/* Per-ray front-to-back compositing, Eq. 1: for every ray (origin t(s_j),
+ * direction R(s_j) u(phi_j, omega_b)) over its tile's sorted list, the particles whose box
+ * contains the ray (A12) contribute alpha = min(alpha_max, sigma rho) with the 3D
+ * response rho at tau_max, skipping tau < r_min (A15).  sorted_ids/tile_ranges
+ * are simuli_bin_sort outputs; `proj` must hold the records of every listed particle. */
+int32_t simuli_render_lidar(const simuli_projected* proj, const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                            const simuli_project_params* params, const simuli_render_params* rparams,
+                            simuli_lidar_out* out, void* stream);
+
+/* Per-pixel camera outputs (device, [H*W] each, row-major; NULL to skip): rgb [H*W][3] =
+ * foreground colour c_f (before the environment map / bilateral grid of Eq. 2), opacity,
+ * depth_accum, depth, final_T, n_contrib, ray_od [H*W][6] double.  Pixels whose ray is
+ * outside the lens model's validity (theta > max_theta) are not rendered (omega = 0). */
+typedef struct {
+  float* rgb;
+  float* opacity;
+  float* depth_accum;
+  float* depth;
+  float* final_T;
+  int32_t* n_contrib;
+  double* ray_od;
+} simuli_camera_out;
+
+int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                             const simuli_project_params* params, const simuli_render_params* rparams,
+                             simuli_camera_out* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIMULI_H */

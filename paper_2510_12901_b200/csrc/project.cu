@@ -1,0 +1,465 @@
+// simuli_project: per-particle UT projection + ray-based culling (sm_100a).
+//
+// One thread per particle; 256-thread CTAs.  For each particle: normalise q -> R,
+// l_k = s_k R e_k, 7 sigma points, each projected with the pose at its own firing
+// time (K fixed-point iterations, A3) by Eq. 3 or the lens model, UT moments,
+// outward-rounded 3-sigma box (A11), LiDAR culling by the summed-area-table rectangle count
+// (Proc. RayOccupancyCount / ProjectParticles), tile rectangle + count, SH
+// features (A17), float32 depth key (A19) and the 80-byte compositing record.
+#include <cmath>
+#include <cstdio>
+
+#include "abi_util.h"
+#include "common.cuh"
+
+namespace simuli {
+
+PoseInterpD make_pose_interp_d(const simuli_pose& a, const simuli_pose& b) {
+  PoseInterpD P{};
+  double qa[4], qb[4], na = 0, nb = 0;
+  for (int i = 0; i < 4; ++i) {
+    qa[i] = a.q[i];
+    qb[i] = b.q[i];
+    na += qa[i] * qa[i];
+    nb += qb[i] * qb[i];
+  }
+  na = std::sqrt(na);
+  nb = std::sqrt(nb);
+  for (int i = 0; i < 4; ++i) {
+    qa[i] /= na;
+    qb[i] /= nb;
+  }
+  bool same = true;
+  for (int i = 0; i < 4; ++i) same &= (a.q[i] == b.q[i]);
+  for (int i = 0; i < 3; ++i) same &= (a.t[i] == b.t[i]);
+  // relative rotation q_rel = conj(qa) * qb on the shortest arc
+  const double w1 = qa[0], x1 = -qa[1], y1 = -qa[2], z1 = -qa[3];
+  const double w2 = qb[0], x2 = qb[1], y2 = qb[2], z2 = qb[3];
+  double r[4] = {w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2, w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+                 w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2, w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2};
+  if (r[0] < 0)
+    for (double& v : r) v = -v;
+  const double vn = std::sqrt(r[1] * r[1] + r[2] * r[2] + r[3] * r[3]);
+  for (int i = 0; i < 4; ++i) P.q0[i] = qa[i];
+  if (vn > 0) {
+    P.half_theta = std::atan2(vn, r[0]);
+    for (int i = 0; i < 3; ++i) P.axis[i] = r[1 + i] / vn;
+  } else {
+    P.half_theta = 0;
+    P.axis[0] = 1;
+  }
+  for (int i = 0; i < 3; ++i) {
+    P.t0[i] = a.t[i];
+    P.dt[i] = static_cast<double>(b.t[i]) - static_cast<double>(a.t[i]);
+  }
+  P.same = same ? 1 : 0;
+  return P;
+}
+
+PoseInterpF make_pose_interp_f(const PoseInterpD& d) {
+  PoseInterpF f{};
+  for (int i = 0; i < 4; ++i) f.q0[i] = static_cast<float>(d.q0[i]);
+  for (int i = 0; i < 3; ++i) {
+    f.axis[i] = static_cast<float>(d.axis[i]);
+    f.t0[i] = static_cast<float>(d.t0[i]);
+    f.dt[i] = static_cast<float>(d.dt[i]);
+  }
+  f.half_theta = static_cast<float>(d.half_theta);
+  f.same = d.same;
+  return f;
+}
+
+namespace {
+
+struct UTW {
+  float spread, wm0, wmi, wc0, wci;
+};
+
+struct ProjArgs {
+  int64_t n;
+  const float *means, *quats, *scales, *opacity, *sh;
+  int sh_degree, n_coef;
+  PoseInterpF pose;
+  int K;
+  UTW ut;
+  float ks;
+  float o_mid[3];
+  int write_all;
+  // LiDAR
+  float az_start, r_min;
+  int dir;
+  int n_phi, n_theta, rows_per_tile, az_cells, sat_cols, enable_cull;
+  float pi_f, two_pi_f, az_tile_scale, az_cell_scale;
+  const float *bounds, *row_scale;
+  const int* sat;
+  // camera
+  int cam_model, width, height, rolling, tile_px, Wt, Ht;
+  float fx, fy, cx, cy, k[5], near_m, max_theta, inv_tile;
+  // out
+  float* record;
+  int* rect;
+  float* key;
+  int* count;
+};
+
+__device__ __forceinline__ int elev_tile(const ProjArgs& A, float w) {
+  // number of interior boundaries bounds[1..n_phi-1] <= w (binary search)
+  int lo = 1, hi = A.n_phi;  // first index in [1, n_phi) with bound > w
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(A.bounds + mid) <= w) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo - 1;
+}
+
+__device__ __forceinline__ int dense_row(const ProjArgs& A, float w) {
+  const int e = elev_tile(A, w);
+  const float u = __fmul_rn(__fsub_rn(w, __ldg(A.bounds + e)), __ldg(A.row_scale + e));
+  return e * A.rows_per_tile + clamp_floor(u, A.rows_per_tile);
+}
+
+__device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c0, int c1) {
+  const int sc = A.sat_cols;
+  return __ldg(A.sat + (r1 + 1) * sc + (c1 + 1)) - __ldg(A.sat + r0 * sc + (c1 + 1)) -
+         __ldg(A.sat + (r1 + 1) * sc + c0) + __ldg(A.sat + r0 * sc + c0);
+}
+
+// Eq. 3 with the firing-time fixed point; returns (phi, omega, r), s = final firing time
+__device__ __forceinline__ void lidar_point(const ProjArgs& A, const float x[3], float* phi, float* om, float* r,
+                                            float* s_out) {
+  float s = 0.f;
+  const int K = A.pose.same ? 0 : A.K;
+  const float inv2pi = 0.15915494309189535f;
+  for (int it = 0; it <= K; ++it) {
+    float R[9], t[3];
+    pose_at(A.pose, s, R, t);
+    const float d0 = x[0] - t[0], d1 = x[1] - t[1], d2 = x[2] - t[2];
+    const float px = R[0] * d0 + R[3] * d1 + R[6] * d2;
+    const float py = R[1] * d0 + R[4] * d1 + R[7] * d2;
+    const float pz = R[2] * d0 + R[5] * d1 + R[8] * d2;
+    *r = sqrtf(px * px + py * py + pz * pz);
+    *phi = atan2f(py, px);
+    const float z = *r > 0.f ? fminf(1.f, fmaxf(-1.f, pz / *r)) : 0.f;
+    *om = asinf(z);
+    if (it < K) {
+      float a = (float)A.dir * (*phi - A.az_start);
+      a = a - 6.283185307179586f * floorf(a * inv2pi);
+      s = fminf(fmaxf(a * inv2pi, 0.f), 1.f);
+    }
+  }
+  *s_out = s;
+}
+
+// lens projection of a camera-frame point; returns 1 valid, 0 invalid, -1 not computable
+__device__ __forceinline__ int cam_frame(const ProjArgs& A, float px, float py, float pz, float* u, float* v) {
+  if (A.cam_model == SIMULI_CAM_FISHEYE_KB) {
+    const float dist = sqrtf(px * px + py * py + pz * pz);
+    if (!(dist > 0.f)) return -1;
+    const float rho = sqrtf(px * px + py * py);
+    const float th = atan2f(rho, pz);
+    const float t2 = th * th;
+    const float thd = th * (1.f + t2 * (A.k[0] + t2 * (A.k[1] + t2 * (A.k[2] + t2 * A.k[3]))));
+    const float sc = rho > 0.f ? thd / rho : 0.f;
+    *u = A.fx * sc * px + A.cx;
+    *v = A.fy * sc * py + A.cy;
+    return (dist >= A.near_m && th <= A.max_theta) ? 1 : 0;
+  }
+  if (!(pz > 0.f)) return -1;
+  const float xp = px / pz, yp = py / pz;
+  const float r2 = xp * xp + yp * yp;
+  const float radial = 1.f + r2 * (A.k[0] + r2 * (A.k[1] + r2 * A.k[4]));
+  const float xd = xp * radial + 2.f * A.k[2] * xp * yp + A.k[3] * (r2 + 2.f * xp * xp);
+  const float yd = yp * radial + A.k[2] * (r2 + 2.f * yp * yp) + 2.f * A.k[3] * xp * yp;
+  *u = A.fx * xd + A.cx;
+  *v = A.fy * yd + A.cy;
+  return pz >= A.near_m ? 1 : 0;
+}
+
+__device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3], float* u, float* v, float* s_out) {
+  float s = 0.f;
+  int valid = 1;
+  const int K = A.pose.same ? 0 : A.K;
+  const float invH = 1.0f / (float)A.height;
+  for (int it = 0; it <= K; ++it) {
+    float R[9], t[3];
+    pose_at(A.pose, s, R, t);
+    const float d0 = x[0] - t[0], d1 = x[1] - t[1], d2 = x[2] - t[2];
+    const float px = R[0] * d0 + R[3] * d1 + R[6] * d2;
+    const float py = R[1] * d0 + R[4] * d1 + R[7] * d2;
+    const float pz = R[2] * d0 + R[5] * d1 + R[8] * d2;
+    const int st = cam_frame(A, px, py, pz, u, v);
+    if (st < 0) return -1;
+    if (st == 0) valid = 0;
+    if (it < K) s = A.rolling ? fminf(fmaxf(*v * invH, 0.f), 1.f) : 0.f;
+  }
+  *s_out = s;
+  return valid;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k_project(const ProjArgs A) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= A.n) return;
+  // ---- loads (SoA; quaternion as one 16-byte load)
+  float mu[3] = {__ldg(A.means + 3 * g), __ldg(A.means + 3 * g + 1), __ldg(A.means + 3 * g + 2)};
+  const float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + g);
+  const float sc[3] = {__ldg(A.scales + 3 * g), __ldg(A.scales + 3 * g + 1), __ldg(A.scales + 3 * g + 2)};
+  const float sigma = __ldg(A.opacity + g);
+
+  // ---- depth key (A19): exact float32 op sequence
+  {
+    const float d0 = __fsub_rn(mu[0], A.o_mid[0]), d1 = __fsub_rn(mu[1], A.o_mid[1]),
+                d2 = __fsub_rn(mu[2], A.o_mid[2]);
+    A.key[g] = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(d0, d0), __fmul_rn(d1, d1)), __fmul_rn(d2, d2)));
+  }
+  int count = 0;
+  int rect[4] = {0, 0, 0, 0};
+  float box[4] = {NAN, NAN, NAN, NAN};
+  float M[9] = {NAN, NAN, NAN, NAN, NAN, NAN, NAN, NAN, NAN}, f[3] = {0.f, 0.f, 0.f};
+  bool ok = true;
+
+  const float qn2 = q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w;
+  ok = qn2 > 0.f && isfinite(qn2);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) ok = ok && sc[c] > 0.f && isfinite(sc[c]) && isfinite(mu[c]);
+  if (ok) {
+    const float inv = rsqrtf(qn2);
+    const float q[4] = {q4.x * inv, q4.y * inv, q4.z * inv, q4.w * inv};
+    float R[9];
+    quat_rot(q, R);
+    float L[3][3];  // L[k] = spread * s_k * column k of R
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) L[k][c] = A.ut.spread * sc[k] * R[3 * c + k];
+
+    // ---- 7 sigma points through the sensor model
+    float ya[7], yb[7], s0 = 0.f;
+    bool valid = true, computable = true;
+#pragma unroll 1
+    for (int i = 0; i < 7; ++i) {
+      float x[3] = {mu[0], mu[1], mu[2]};
+      if (i > 0) {
+        const int k = (i - 1) % 3;
+        const float sg = i <= 3 ? 1.f : -1.f;
+        x[0] += sg * L[k][0];
+        x[1] += sg * L[k][1];
+        x[2] += sg * L[k][2];
+      }
+      float s;
+      if (KIND == SIMULI_SENSOR_LIDAR) {
+        float r;
+        lidar_point(A, x, &ya[i], &yb[i], &r, &s);
+        valid = valid && (r >= A.r_min);
+      } else {
+        const int st = camera_point(A, x, &ya[i], &yb[i], &s);
+        computable = computable && st >= 0;
+        valid = valid && st == 1;
+      }
+      if (i == 0) s0 = s;
+    }
+    // ---- UT moments (azimuth unwrapped about sigma point 0, A21)
+    float da[7];
+    const float a0 = ya[0];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      float d = ya[i] - a0;
+      if (KIND == SIMULI_SENSOR_LIDAR) {
+        if (d > 3.14159265f) d -= 6.28318531f;
+        else if (d <= -3.14159265f) d += 6.28318531f;
+      }
+      da[i] = d;
+    }
+    float ma = A.ut.wm0 * da[0], mb = A.ut.wm0 * yb[0];
+#pragma unroll
+    for (int i = 1; i < 7; ++i) {
+      ma += A.ut.wmi * da[i];
+      mb += A.ut.wmi * yb[i];
+    }
+    float caa = 0.f, cab = 0.f, cbb = 0.f;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      const float w = i == 0 ? A.ut.wc0 : A.ut.wci;
+      const float ea = da[i] - ma, eb = yb[i] - mb;
+      caa += w * ea * ea;
+      cab += w * ea * eb;
+      cbb += w * eb * eb;
+    }
+    float ya_bar = a0 + ma;
+    const float det = caa * cbb - cab * cab;
+    const bool boxok = computable && isfinite(ya_bar) && isfinite(mb) && caa > 0.f && cbb > 0.f && det > 0.f &&
+                       isfinite(det);
+    ok = boxok && valid;
+    if (boxok) {
+      if (KIND == SIMULI_SENSOR_LIDAR) {
+        if (ya_bar >= A.pi_f) ya_bar = __fsub_rn(ya_bar, A.two_pi_f);
+        else if (ya_bar < -A.pi_f) ya_bar = __fadd_rn(ya_bar, A.two_pi_f);
+      }
+      const float ha = A.ks * sqrtf(caa), hb = A.ks * sqrtf(cbb);
+      box[0] = __fsub_rd(ya_bar, ha);
+      box[1] = __fadd_ru(ya_bar, ha);
+      box[2] = __fsub_rd(mb, hb);
+      box[3] = __fadd_ru(mb, hb);
+    }
+    if (ok) {
+      // ---- culling + render-tile rectangle
+      if (KIND == SIMULI_SENSOR_LIDAR) {
+        const float b0 = __ldg(A.bounds), bl = __ldg(A.bounds + A.n_phi);
+        bool keep = !(box[3] < b0 || box[2] > bl);
+        if (keep && A.enable_cull) {
+          const int r0 = dense_row(A, box[2]), r1 = dense_row(A, box[3]);
+          int cs, cl;
+          az_run(box[0], box[1], A.pi_f, A.two_pi_f, A.az_cell_scale, A.az_cells, &cs, &cl);
+          const int ce = cs + cl - 1;
+          int occ;
+          if (ce < A.az_cells) occ = sat_rect(A, r0, r1, cs, ce);
+          else occ = sat_rect(A, r0, r1, cs, A.az_cells - 1) + sat_rect(A, r0, r1, 0, ce - A.az_cells);
+          keep = occ > 0;
+        }
+        if (keep) {
+          const int e0 = elev_tile(A, box[2]), e1 = elev_tile(A, box[3]);
+          int cs, cl;
+          az_run(box[0], box[1], A.pi_f, A.two_pi_f, A.az_tile_scale, A.n_theta, &cs, &cl);
+          rect[0] = e0; rect[1] = e1; rect[2] = cs; rect[3] = cl;
+          count = (e1 - e0 + 1) * cl;
+        }
+      } else {
+        const bool outside = box[1] < 0.5f || box[0] > (float)A.width - 0.5f || box[3] < 0.5f ||
+                             box[2] > (float)A.height - 0.5f;
+        if (!outside) {
+          const int c0 = clamp_floor(__fmul_rn(box[0], A.inv_tile), A.Wt);
+          const int c1 = clamp_floor(__fmul_rn(box[1], A.inv_tile), A.Wt);
+          const int r0 = clamp_floor(__fmul_rn(box[2], A.inv_tile), A.Ht);
+          const int r1 = clamp_floor(__fmul_rn(box[3], A.inv_tile), A.Ht);
+          rect[0] = r0; rect[1] = r1; rect[2] = c0; rect[3] = c1 - c0 + 1;
+          count = (r1 - r0 + 1) * (c1 - c0 + 1);
+        }
+      }
+    }
+    if (ok && (count > 0 || A.write_all)) {
+      // ---- record: canonical transform M = diag(1/s) R^T, SH features (A17)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float is = 1.0f / sc[k];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) M[3 * k + c] = R[3 * c + k] * is;
+      }
+      float Rs[9], ts[3];
+      pose_at(A.pose, s0, Rs, ts);
+      float vx = mu[0] - ts[0], vy = mu[1] - ts[1], vz = mu[2] - ts[2];
+      const float vn = rsqrtf(vx * vx + vy * vy + vz * vz);
+      vx *= vn; vy *= vn; vz *= vn;
+      if (isfinite(vn)) sh_eval(A.sh + g * A.n_coef * 3, A.sh_degree, vx, vy, vz, f);
+    }
+  }
+  A.count[g] = count;
+  reinterpret_cast<int4*>(A.rect)[g] = make_int4(rect[0], rect[1], rect[2], rect[3]);
+  if (count > 0 || A.write_all) {
+    float4* rec = reinterpret_cast<float4*>(A.record + g * kRecordFloats);
+    rec[0] = make_float4(mu[0], mu[1], mu[2], M[0]);
+    rec[1] = make_float4(M[1], M[2], M[3], M[4]);
+    rec[2] = make_float4(M[5], M[6], M[7], M[8]);
+    rec[3] = make_float4(sigma, f[0], f[1], f[2]);
+    rec[4] = ok ? make_float4(box[0], box[1], box[2], box[3]) : make_float4(NAN, NAN, NAN, NAN);
+  }
+}
+
+}  // namespace
+
+bool ut_weights(float alpha, float beta, float kappa, float* spread, float* wm0, float* wmi, float* wc0, float* wci) {
+  const double n = 3.0, a = alpha, b = beta, k = kappa;
+  const double lambda = a * a * (n + k) - n;
+  if (!(n + lambda > 0.0)) return false;
+  *spread = static_cast<float>(std::sqrt(n + lambda));
+  *wm0 = static_cast<float>(lambda / (n + lambda));
+  *wc0 = static_cast<float>(lambda / (n + lambda) + (1.0 - a * a + b));
+  *wmi = *wci = static_cast<float>(1.0 / (2.0 * (n + lambda)));
+  return true;
+}
+
+// o_mid = t0 + 0.5 (t1 - t0) with float32 ops (host, no FMA): bit-identical definition (A19)
+static void depth_origin(const simuli_pose& a, const simuli_pose& b, float out[3]) {
+  for (int c = 0; c < 3; ++c) {
+    volatile float h = b.t[c] - a.t[c];
+    volatile float hm = 0.5f * h;
+    volatile float om = a.t[c] + hm;
+    out[c] = om;
+  }
+}
+
+}  // namespace simuli
+
+extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_project_params* P, simuli_projected* out,
+                                  void* stream) {
+  using namespace simuli;
+  clear_error();
+  SIMULI_REQUIRE(G && P && out, "simuli_project: NULL argument");
+  SIMULI_REQUIRE(G->n >= 0, "simuli_project: n < 0");
+  if (G->sh_degree < 0 || G->sh_degree > 3) {
+    set_error("simuli_project: sh_degree %d not in 0..3", G->sh_degree);
+    return SIMULI_ERR_UNSUPPORTED;
+  }
+  if (G->n == 0) return SIMULI_OK;
+  SIMULI_REQUIRE(G->means && G->quats && G->scales && G->opacity && G->sh, "simuli_project: NULL Gaussian array");
+  SIMULI_REQUIRE(out->record && out->tile_rect && out->depth_key && out->tile_count, "simuli_project: NULL output");
+  SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(G->quats) % 16 == 0 && reinterpret_cast<uintptr_t>(out->record) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(out->tile_rect) % 16 == 0,
+                 "simuli_project: quats / record / tile_rect must be 16-byte aligned");
+  SIMULI_REQUIRE(P->rs_iterations >= 0 && P->rs_iterations <= 16, "rs_iterations must be in [0, 16]");
+  SIMULI_REQUIRE(P->extent_sigma > 0.f, "extent_sigma must be > 0");
+  ProjArgs A{};
+  A.n = G->n;
+  A.means = G->means; A.quats = G->quats; A.scales = G->scales; A.opacity = G->opacity; A.sh = G->sh;
+  A.sh_degree = G->sh_degree;
+  A.n_coef = (G->sh_degree + 1) * (G->sh_degree + 1);
+  A.pose = make_pose_interp_f(make_pose_interp_d(P->pose_start, P->pose_end));
+  A.K = P->rs_iterations;
+  SIMULI_REQUIRE(ut_weights(P->ut_alpha, P->ut_beta, P->ut_kappa, &A.ut.spread, &A.ut.wm0, &A.ut.wmi, &A.ut.wc0,
+                            &A.ut.wci),
+                 "invalid UT parameters: alpha^2 (3 + kappa) must be > 0");
+  A.ks = P->extent_sigma;
+  depth_origin(P->pose_start, P->pose_end, A.o_mid);
+  A.write_all = P->write_all_records;
+  A.record = out->record; A.rect = out->tile_rect; A.key = out->depth_key; A.count = out->tile_count;
+  const int threads = 256;
+  const unsigned blocks = static_cast<unsigned>((G->n + threads - 1) / threads);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (P->kind == SIMULI_SENSOR_LIDAR) {
+    SIMULI_REQUIRE(P->lidar && P->tiling, "LiDAR projection needs lidar and tiling");
+    const simuli_tiling_dev& T = *P->tiling;
+    SIMULI_REQUIRE(T.elev_bounds && T.cull_row_scale && T.sat && T.n_phi >= 1 && T.n_theta >= 1,
+                   "incomplete device tiling");
+    SIMULI_REQUIRE(P->lidar->min_range_m > 0.f, "min_range_m must be > 0");
+    A.az_start = P->lidar->azimuth_start_rad;
+    A.dir = P->lidar->spin_direction;
+    A.r_min = P->lidar->min_range_m;
+    A.n_phi = T.n_phi; A.n_theta = T.n_theta; A.rows_per_tile = T.cull_rows_per_tile;
+    A.az_cells = T.cull_az_cells; A.sat_cols = T.sat_cols; A.enable_cull = P->enable_culling;
+    A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f; A.az_tile_scale = T.az_tile_scale; A.az_cell_scale = T.az_cell_scale;
+    A.bounds = T.elev_bounds; A.row_scale = T.cull_row_scale; A.sat = T.sat;
+    k_project<SIMULI_SENSOR_LIDAR><<<blocks, threads, 0, st>>>(A);
+  } else if (P->kind == SIMULI_SENSOR_CAMERA) {
+    SIMULI_REQUIRE(P->camera, "camera projection needs camera");
+    const simuli_camera& C = *P->camera;
+    SIMULI_REQUIRE(C.width > 0 && C.height > 0 && C.fx > 0 && C.fy > 0, "invalid camera size / focal");
+    SIMULI_REQUIRE(C.tile_px > 0 && (C.tile_px & (C.tile_px - 1)) == 0 && C.tile_px <= 32,
+                   "tile_px must be a power of two <= 32");
+    SIMULI_REQUIRE(C.model == SIMULI_CAM_FISHEYE_KB || C.model == SIMULI_CAM_PINHOLE_RADTAN, "unknown camera model");
+    A.cam_model = C.model; A.width = C.width; A.height = C.height; A.rolling = C.rolling_shutter;
+    A.tile_px = C.tile_px; A.Wt = (C.width + C.tile_px - 1) / C.tile_px; A.Ht = (C.height + C.tile_px - 1) / C.tile_px;
+    A.fx = C.fx; A.fy = C.fy; A.cx = C.cx; A.cy = C.cy;
+    for (int i = 0; i < 5; ++i) A.k[i] = C.k[i];
+    A.near_m = C.near_m; A.max_theta = C.max_theta_rad; A.inv_tile = 1.0f / (float)C.tile_px;
+    k_project<SIMULI_SENSOR_CAMERA><<<blocks, threads, 0, st>>>(A);
+  } else {
+    set_error("simuli_project: unknown sensor kind %d", P->kind);
+    return SIMULI_ERR_INVALID_ARGUMENT;
+  }
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("simuli_project: launch failed: %s", cudaGetErrorString(e));
+    return SIMULI_ERR_CUDA;
+  }
+  return SIMULI_OK;
+}

@@ -1,0 +1,373 @@
+"""GPU parity tests (-m gpu): the CUDA path through the C ABI vs the CPU oracle.
+
+Tolerances (BASELINE.json north star): tile boundaries, tile-Gaussian lists and sorted key
+order bit-exact; depth within 1e-3 m (rays with omega >= 0.5, A16); intensity, ray drop,
+colour and opacity within 1e-4 absolute.  Tier 1 feeds the oracle stage the GPU's
+previous-stage outputs (so every discrete decision uses identical float32 values); tier 2
+runs the oracle from scratch and excludes the rays it flags as threshold-ambiguous (A23),
+which must stay below 0.5 %.
+"""
+import numpy as np
+import pytest
+
+from paper_2510_12901_b200 import synth as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL_FEAT = 1e-4
+TOL_DEPTH = 1e-3
+LIDAR_EPS = {"a": 4e-6, "b": 4e-6, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4}
+CAMERA_EPS = {"a": 2e-3, "b": 2e-3, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4}
+
+
+@pytest.fixture(scope="module")
+def SM():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2510_12901_b200 import build as B
+    B.build()
+    from paper_2510_12901_b200 import simuli
+    return simuli
+
+
+def gpu_records(r):
+    rec = r.record.cpu().numpy().astype(np.float64)
+    return {"mu": rec[:, 0:3], "Mrows": rec[:, 3:12], "sigma": rec[:, 12], "feat": rec[:, 13:16],
+            "box": r.record.cpu().numpy()[:, 16:20].copy()}
+
+
+def lidar_run(SM, cfg, scene, **kw):
+    r = SM.LidarRenderer(cfg, SM.to_device_scene(scene), **kw)
+    r.want_ray_od(True)
+    r.scan(sync_capacity=True)
+    torch.cuda.synchronize()
+    return r
+
+
+def sorted_lists(r):
+    P = int(r.n_pairs.item())
+    return (r.sorted_keys[:P].cpu().numpy().view(np.uint64), r.sorted_ids[:P].cpu().numpy().view(np.uint32),
+            r.tile_ranges.cpu().numpy())
+
+
+def compare_lidar(out, ref, mask=None, tol=TOL_FEAT):
+    g = {k: out[k].cpu().numpy().astype(np.float64) for k in ("opacity", "intensity", "raydrop", "depth")}
+    zeta = out["zeta"].cpu().numpy().astype(np.float64)
+    m = np.ones(len(g["opacity"]), bool) if mask is None else mask
+    errs = {"opacity": np.abs(g["opacity"] - ref["opacity"])[m].max(initial=0),
+            "intensity": np.abs(g["intensity"] - ref["intensity"])[m].max(initial=0),
+            "raydrop": np.abs(g["raydrop"] - ref["raydrop"])[m].max(initial=0),
+            "zeta": np.abs(zeta - ref["feat"])[m].max(initial=0)}
+    dm = m & (ref["opacity"] >= 0.5)
+    errs["depth"] = np.abs(g["depth"] - ref["depth"])[dm].max(initial=0)
+    assert max(errs[k] for k in ("opacity", "intensity", "raydrop", "zeta")) < tol, errs
+    assert errs["depth"] < TOL_DEPTH, errs
+    return errs
+
+
+# ------------------------------------------------------------------ stage 1 (a1): projection
+@pytest.mark.parametrize("config", ["A", "tiny", "B-sub"])
+def test_project_lidar_tier1(SM, oracle_mod, config):
+    O = oracle_mod
+    if config == "B-sub":
+        cfg, scene = S.lidar_config("B"), S.scene_for("B", n=200_000)
+    else:
+        cfg, scene = S.lidar_config(config), S.scene_for(config, seed=5 if config == "tiny" else None)
+    r = lidar_run(SM, cfg, scene, write_all_records=True)
+    rec = r.record.cpu().numpy()
+    proj = O.project_lidar(scene, cfg)
+    gv = np.isfinite(rec[:, 16])
+    ov = proj["valid"] != 0
+    amb = proj["ambiguous"] != 0
+    assert np.array_equal(gv[~amb], ov[~amb]), np.nonzero(gv[~amb] != ov[~amb])[0][:10]
+    both = gv & ov
+    # depth keys: bit-exact float32 (A19)
+    assert np.array_equal(r.depth_key.cpu().numpy().view(np.uint32), proj["key"].view(np.uint32))
+    db = np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both].astype(np.float64))
+    assert db.max() < 2e-6, db.max()
+    Mref = proj["Mrows"][both]
+    rel = np.abs(rec[both, 3:12] - Mref) / np.abs(Mref).max(1, keepdims=True)
+    assert rel.max() < 2e-6
+    assert np.abs(rec[both, 13:16] - proj["feat"][both]).max() < 2e-5
+
+
+# ------------------------------------------------------------------ stages 3-4 (a2-a4): cull, pairs, sort
+@pytest.mark.parametrize("config", ["A", "tiny", "B-sub"])
+def test_cull_bin_sort_tier1_bit_exact(SM, oracle_mod, config):
+    O = oracle_mod
+    if config == "B-sub":
+        cfg, scene = S.lidar_config("B"), S.scene_for("B", n=300_000)
+    else:
+        cfg, scene = S.lidar_config(config), S.scene_for(config, seed=9 if config == "tiny" else None)
+    r = lidar_run(SM, cfg, scene, write_all_records=True)
+    t = O.Tiling(cfg)
+    box = r.record.cpu().numpy()[:, 16:20].copy()
+    valid = np.isfinite(box[:, 0]).astype(np.int32)
+    count, rect = O.cull_lidar(valid, box, t, True)
+    assert np.array_equal(r.tile_count.cpu().numpy(), count)
+    gr = r.tile_rect.cpu().numpy()
+    nz = count > 0
+    assert np.array_equal(gr[nz], rect[nz])
+    keys, ids, ranges = O.bin_pairs(count, rect, r.depth_key.cpu().numpy(), t.n_tiles, t.n_theta)
+    gk, gi, granges = sorted_lists(r)
+    assert len(gk) == len(keys)
+    assert np.array_equal(gk, keys) and np.array_equal(gi, ids) and np.array_equal(granges, ranges)
+
+
+# ------------------------------------------------------------------ stage 5 (a5): compositing
+@pytest.mark.parametrize("config", ["A", "tiny", "B-sub"])
+def test_render_lidar_tier1(SM, oracle_mod, config):
+    O = oracle_mod
+    if config == "B-sub":
+        cfg, scene = S.lidar_config("B"), S.scene_for("B", n=300_000)
+    else:
+        cfg, scene = S.lidar_config(config), S.scene_for(config, seed=11 if config == "tiny" else None)
+    r = lidar_run(SM, cfg, scene)
+    t = O.Tiling(cfg)
+    _, ids, ranges = sorted_lists(r)
+    rec = gpu_records(r)
+    od = r.out["ray_od"].cpu().numpy()
+    ref = O.composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, wrap=1, near=cfg.min_range,
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4},
+                      pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    g, bd = O.decode_lidar(ref["feat"])
+    ref["intensity"], ref["raydrop"] = g, bd
+    ok = ref["flag"] == 0
+    assert ok.mean() > 0.999, ok.mean()
+    compare_lidar(r.out, ref, ok)
+    assert (r.out["opacity"].cpu().numpy() > 0.5).mean() > 0.05  # the scan sees geometry
+
+
+# ------------------------------------------------------------------ end to end (tier 2)
+@pytest.mark.parametrize("config", ["A", "tiny"])
+def test_lidar_end_to_end_tier2(SM, oracle_mod, config):
+    O = oracle_mod
+    cfg, scene = S.lidar_config(config), S.scene_for(config, seed=13 if config == "tiny" else None)
+    r = lidar_run(SM, cfg, scene)
+    t = O.Tiling(cfg)
+    ref = O.render_lidar(scene, cfg, tiling=t, flag_eps=LIDAR_EPS)  # oracle rays (double), own projection
+    ok = ref["flag"] == 0
+    assert ok.mean() > 0.995, ok.mean()
+    compare_lidar(r.out, ref, ok)
+    brute = O.render_lidar(scene, cfg, tiling=t, mode="brute")  # O13: no tiling, no culling
+    okb = ok
+    compare_lidar(r.out, brute, okb)
+
+
+def test_lidar_tiny_scenes_vs_bruteforce(SM, oracle_mod):
+    O = oracle_mod
+    worst = 0.0
+    flagged = 0
+    total = 0
+    for seed in range(0, 100, 5):
+        cfg, scene = S.lidar_config("tiny"), S.scene_for("tiny", seed=seed)
+        r = lidar_run(SM, cfg, scene)
+        ref = O.render_lidar(scene, cfg, mode="brute", flag_eps=LIDAR_EPS)
+        ok = ref["flag"] == 0
+        flagged += int((~ok).sum())
+        total += ok.size
+        e = compare_lidar(r.out, ref, ok)
+        worst = max(worst, e["opacity"], e["intensity"])
+    assert flagged / total < 0.005
+
+
+# ------------------------------------------------------------------ invariance on the GPU alone
+def test_gpu_invariance_tiling_and_culling(SM):
+    scene = S.scene_for("B", n=200_000)
+    outs = []
+    for n_phi, M, cull in ((16, 32, 1), (16, 32, 0), (8, 64, 1), (32, 16, 1), (4, 256, 1), (1, 8, 1)):
+        cfg = S.lidar_config("B")
+        cfg.n_phi, cfg.max_rays_per_tile = n_phi, M
+        r = lidar_run(SM, cfg, scene, enable_culling=bool(cull))
+        outs.append({k: v.cpu().numpy().copy() for k, v in r.out.items() if v is not None and k != "ray_od"})
+    for o in outs[1:]:
+        for k in outs[0]:
+            assert np.array_equal(o[k], outs[0][k]), k  # tiling "does not affect quality"
+
+
+def test_culling_reduces_pairs(SM):
+    scene = S.scene_for("B", n=300_000)
+    cfg = S.lidar_config("B")
+    on = lidar_run(SM, cfg, scene, enable_culling=True)
+    off = lidar_run(SM, cfg, scene, enable_culling=False)
+    assert on.n_pairs.item() < off.n_pairs.item()  # direction of tab:culling
+
+
+# ------------------------------------------------------------------ sort + edge cases
+def test_bin_sort_synthetic_keys_large_tiles(SM):
+    """Stable sort of many pairs over 8160 tiles (13 tile bits, 6 passes), ragged partition."""
+    dev = "cuda"
+    rng = np.random.default_rng(17)
+    n = 123_457
+    n_tiles, ncols = 8160, 120
+    count = rng.integers(0, 6, n).astype(np.int32)
+    rect = np.zeros((n, 4), np.int32)
+    rows = n_tiles // ncols
+    r0 = rng.integers(0, rows, n)
+    c0 = rng.integers(0, ncols, n)
+    for i in range(n):
+        h = int(rng.integers(1, 3))
+        rect[i] = [r0[i], min(rows - 1, r0[i] + h - 1), c0[i], 1]
+    count = ((rect[:, 1] - rect[:, 0] + 1) * rect[:, 3]).astype(np.int32)
+    count[rng.uniform(size=n) < 0.2] = 0
+    key = rng.choice(np.float32([0.5, 1.0, 2.0, 3.5]), n).astype(np.float32)  # many ties
+    key[rng.uniform(size=n) < 0.5] = rng.uniform(0.1, 200, (rng.uniform(size=n) < 0.5).sum())
+    t = {k: torch.from_numpy(v).to(dev) for k, v in (("count", count), ("rect", rect), ("key", key))}
+    proj = SM.Projected(0, t["rect"].data_ptr(), t["key"].data_ptr(), t["count"].data_ptr())
+    P = int(count.sum())
+    cap = P + 17
+    ws = torch.empty(SM.simuli_bin_sort_workspace_size(n, cap, n_tiles), dtype=torch.uint8, device=dev)
+    keys = torch.empty(cap, dtype=torch.int64, device=dev)
+    ids = torch.empty(cap, dtype=torch.int32, device=dev)
+    ranges = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
+    npairs = torch.zeros(1, dtype=torch.int64, device=dev)
+    SM.simuli_bin_sort(proj, n, n_tiles, ncols, ws, cap, keys, ids, ranges, npairs)
+    torch.cuda.synchronize()
+    assert npairs.item() == P
+    # reference: enumerate pairs in particle order, stable sort by key
+    g = np.repeat(np.arange(n), count)
+    j = np.concatenate([np.arange(c) for c in count if c > 0])
+    tile = (rect[g, 0] + j) * ncols + rect[g, 2]
+    k64 = (tile.astype(np.uint64) << np.uint64(32)) | key.view(np.uint32)[g].astype(np.uint64)
+    order = np.argsort(k64, kind="stable")
+    assert np.array_equal(keys[:P].cpu().numpy().view(np.uint64), k64[order])
+    assert np.array_equal(ids[:P].cpu().numpy(), g[order].astype(np.int32))
+    rr = ranges.cpu().numpy()
+    st = np.searchsorted(k64[order] >> np.uint64(32), np.arange(n_tiles), "left")
+    en = np.searchsorted(k64[order] >> np.uint64(32), np.arange(n_tiles), "right")
+    assert np.array_equal(rr[:, 0][en > st], st[en > st]) and np.array_equal(rr[:, 1], np.where(en > st, en, 0))
+
+
+def test_bin_sort_capacity_protocol(SM):
+    cfg, scene = S.lidar_config("A"), S.scene_for("A")
+    r = SM.LidarRenderer(cfg, SM.to_device_scene(scene), capacity=10)
+    r.project()
+    need = SM.simuli_bin_sort(r.projected, r.n, r.n_tiles, r.n_cols_total, r.workspace, -r.capacity, r.sorted_keys,
+                              r.sorted_ids, r.tile_ranges, r.n_pairs)
+    assert need is not None and need > 10
+    SM.simuli_bin_sort(r.projected, r.n, r.n_tiles, r.n_cols_total, r.workspace, r.capacity, r.sorted_keys,
+                       r.sorted_ids, r.tile_ranges, r.n_pairs)  # async: reports P, sorts a prefix
+    torch.cuda.synchronize()
+    assert r.n_pairs.item() == need
+    r.scan(sync_capacity=True)  # grows and completes
+    torch.cuda.synchronize()
+    assert r.capacity >= need
+
+
+def test_empty_and_degenerate_scenes(SM, oracle_mod):
+    cfg = S.lidar_config("tiny")
+    empty = {k: v[:0] for k, v in S.scene_for("tiny", seed=1).items()}
+    r = SM.LidarRenderer(cfg, SM.to_device_scene(empty))
+    out = r.scan(sync_capacity=True)
+    torch.cuda.synchronize()
+    assert (out["opacity"].cpu().numpy() == 0).all() and np.allclose(out["raydrop"].cpu().numpy(), 0.5)
+    bad = S.scene_for("tiny", seed=2)
+    n = bad["means"].shape[0]
+    bad["quats"][: n // 3] = 0.0            # zero quaternion -> invalid
+    bad["scales"][n // 3: n // 2, 0] = 0.0  # zero scale -> invalid
+    bad["means"][n // 2: n // 2 + 3] = np.array([0, 0, 1.8], np.float32)  # at the sensor -> range < r_min
+    r = lidar_run(SM, cfg, bad)
+    ref = oracle_mod.render_lidar(bad, cfg, flag_eps=LIDAR_EPS)
+    ok = ref["flag"] == 0
+    compare_lidar(r.out, ref, ok)
+    assert (r.tile_count.cpu().numpy()[: n // 2] == 0).all()
+
+
+def test_many_rays_per_tile_chunks(SM, oracle_mod):
+    """max_rays_in_tile > 32 (A9): warps over 32-ray chunks of one tile."""
+    cfg = S.lidar_config("A")
+    cfg.n_phi, cfg.max_rays_per_tile = 2, 128
+    scene = S.scene_for("A")
+    r = lidar_run(SM, cfg, scene)
+    assert r.tiling_host["max_rays_in_tile"] > 32
+    ref = oracle_mod.render_lidar(scene, cfg, flag_eps=LIDAR_EPS)
+    compare_lidar(r.out, ref, ref["flag"] == 0)
+
+
+# ------------------------------------------------------------------ full-size config B (sampled)
+def test_config_b_full_size_sampled(SM, oracle_mod):
+    """BASELINE configs[1] at full size in the bench's launch configuration; the oracle
+    checks the projection of every particle and composites a sample of 64 tiles."""
+    O = oracle_mod
+    cfg, scene = S.lidar_config("B"), S.scene_for("B")
+    r = lidar_run(SM, cfg, scene, write_all_records=False)
+    keys = r.depth_key.cpu().numpy()
+    proj = O.project_lidar(scene, cfg)
+    assert np.array_equal(keys.view(np.uint32), proj["key"].view(np.uint32))
+    t = O.Tiling(cfg)
+    rng = np.random.default_rng(3)
+    tiles = rng.choice(t.n_tiles, 64, replace=False)
+    rays = np.concatenate([t.tile_rays[t.tile_ray_offsets[x]:t.tile_ray_offsets[x + 1]] for x in tiles])
+    # tier 1 on the sample: GPU records / lists / rays
+    _, ids, ranges = sorted_lists(r)
+    rec = gpu_records(r)
+    od = r.out["ray_od"].cpu().numpy()
+    ref = O.composite(rec, ids, ranges, t.ray_tile[rays], t.ray_az[rays], t.ray_el[rays], od[rays], wrap=1,
+                      near=cfg.min_range, flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4},
+                      pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    ref["intensity"], ref["raydrop"] = O.decode_lidar(ref["feat"])
+    sub = {k: v[torch.from_numpy(rays).to(v.device)] for k, v in r.out.items() if v is not None}
+    compare_lidar(sub, ref, ref["flag"] == 0)
+    # tier 2 on the sample: oracle's own projection, lists and rays
+    rec2 = O.records_from_projection(proj, scene)
+    listed = ((proj["valid"] != 0) | (proj["ambiguous"] != 0)) & np.isfinite(proj["box"]).all(1)
+    lbox = O.expand_box(proj["box"], LIDAR_EPS["a"], LIDAR_EPS["b"])
+    count, rect = O.cull_lidar(listed.astype(np.int32), lbox, t, True)
+    _, ids2, ranges2 = O.bin_pairs(count, rect, proj["key"], t.n_tiles, t.n_theta)
+    od2 = O.lidar_rays(t, cfg.pose_start, cfg.pose_end)[rays]
+    gamb = np.where(proj["ambiguous"] != 0, np.where(proj["valid"] != 0, 1, 2), 0).astype(np.int32)
+    ref2 = O.composite(rec2, ids2, ranges2, t.ray_tile[rays], t.ray_az[rays], t.ray_el[rays], od2, wrap=1,
+                       near=cfg.min_range, gamb=gamb, flag_eps=LIDAR_EPS, pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    ref2["intensity"], ref2["raydrop"] = O.decode_lidar(ref2["feat"])
+    ok = ref2["flag"] == 0
+    assert ok.mean() > 0.995, ok.mean()
+    compare_lidar(sub, ref2, ok)
+
+
+# ------------------------------------------------------------------ camera (a6)
+def camera_run(SM, cam, scene, **kw):
+    c = SM.CameraRenderer(cam, SM.to_device_scene(scene), **kw)
+    c.want_ray_od(True)
+    c.frame(sync_capacity=True)
+    torch.cuda.synchronize()
+    return c
+
+
+@pytest.mark.parametrize("name", ["D-small", "pinhole-small"])
+def test_camera_tier1_and_tier2(SM, oracle_mod, name):
+    O = oracle_mod
+    cam = S.camera_config(name)
+    scene = S.corridor_scene(21, 20000, x_range=(0.0, 60.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    c = camera_run(SM, cam, scene, write_all_records=True)
+    rec = c.record.cpu().numpy()
+    proj = O.project_camera(scene, cam)
+    gv, ov, amb = np.isfinite(rec[:, 16]), proj["valid"] != 0, proj["ambiguous"] != 0
+    assert np.array_equal(gv[~amb], ov[~amb])
+    both = gv & ov
+    assert np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both]).max() < 2e-3
+    count, rect = O.cull_camera(gv.astype(np.int32), rec[:, 16:20].copy(), cam)
+    assert np.array_equal(c.tile_count.cpu().numpy(), count)
+    Wt, Ht = O.camera_tiles(cam)
+    keys, ids, ranges = O.bin_pairs(count, rect, c.depth_key.cpu().numpy(), Wt * Ht, Wt)
+    gk, gi, gr = sorted_lists(c)
+    assert np.array_equal(gk, keys) and np.array_equal(gi, ids) and np.array_equal(gr, ranges)
+    rays = O.camera_rays(cam)
+    gpu_od = c.out["ray_od"].cpu().numpy()
+    assert np.abs(gpu_od - rays["od"])[rays["valid"] != 0].max() < 1e-9
+    # tier 1: GPU records, lists, rays
+    ref = O.composite(gpu_records(c), ids, ranges, rays["tile"], rays["u"], rays["v"], gpu_od, wrap=0,
+                      near=cam.near, ray_valid=rays["valid"],
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4})
+    ok = ref["flag"] == 0
+    assert ok.mean() > 0.999
+    rgb = c.out["rgb"].cpu().numpy()
+    assert np.abs(rgb - ref["feat"])[ok].max() < TOL_FEAT
+    assert np.abs(c.out["opacity"].cpu().numpy() - ref["opacity"])[ok].max() < TOL_FEAT
+    # tier 2: oracle from scratch
+    ref2 = O.render_camera(scene, cam, flag_eps=CAMERA_EPS)
+    ok2 = ref2["flag"] == 0
+    assert ok2.mean() > 0.995, ok2.mean()
+    assert np.abs(rgb - ref2["feat"])[ok2].max() < TOL_FEAT
+    dm = ok2 & (ref2["opacity"] >= 0.5)
+    assert np.abs(c.out["depth"].cpu().numpy() - ref2["depth"])[dm].max() < TOL_DEPTH
+    assert (c.out["opacity"].cpu().numpy() > 0.5).mean() > 0.05
