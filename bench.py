@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the SimULi forward LiDAR hot path on B200 (BASELINE.json metric).
+
+    python bench.py --gpus N --steps K --warmup W [--impl reference]
+
+A step = one full LiDAR scan of BASELINE.json configs[1] ("B": Pandar64-like 64 x 1800
+rays, rolling-shutter spin pose interpolation, 2M Gaussians): simuli_project ->
+simuli_bin_sort -> simuli_render_lidar through the C ABI, scene resident in HBM.  Scans
+of the B-batch trajectory (poses 0.2 m apart) are sharded round-robin over
+ranks (weak scaling: K scans per rank); there is no collective on the data path, NCCL
+only reduces the timers / counters.
+
+Prints ONE JSON line on rank 0.  value = whole-job LiDAR rays/s (scans/s in
+``scans_per_s``); the timed region is bracketed by barrier + synchronize, each scan is
+timed with CUDA events on the launching stream (L2 flushed between scans by writing a
+256 MB buffer outside the events), and the max over ranks is taken.
+``--impl reference`` times the CPU oracle (oracle/, test infrastructure) on a bounded
+sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2510_12901_b200 import synth  # noqa: E402
+
+METRIC = "LiDAR rays/sec and scans/sec (64-beam, 2M Gaussians) at 1/2/4/8 B200; % roofline"
+UNIT = "rays/s"
+WORKLOAD = ("B: PandaSet-like Pandar64 scan, 64x1800 rays, 2M Gaussians (driving corridor), rolling-shutter "
+            "spin pose interpolation (1 m, 0.03 rad per sweep), K=1 fixed-point iteration, N_phi=16, M=32")
+
+# Algorithmic lane-instruction costs per compositing event; the counts
+# come from the kernel's own workload counters (entries visited / in box / composited).
+C_BOX, C_RESP, C_ACC, C_RAY = 8, 45, 8, 80
+
+
+def read_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return {"hbm_gbs": float(p["hbm_gbs"]), "sm_max_mhz": float(p.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "clocks_event_reasons.gpu_idle"]
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap", "gpu_idle"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        busy = [s for s in sm] or [float("nan")]
+        return {"sm_mhz": statistics.median(busy) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def shard_poses(n_total: int, world: int, rank: int):
+    """Round-robin shard of the B-batch trajectory: scan i -> rank i mod world."""
+    poses = synth.batch_poses(n_total)
+    return [poses[i] for i in range(n_total) if i % world == rank]
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------------ oracle (CPU) leg
+def oracle_scan_sample(scene, cfg, tiling, pose0, pose1, n_tiles_sample, rng):
+    """One bounded sample of the workload on the CPU oracle: the full projection + culling +
+    binning of every particle (needed to know any tile's list), compositing of the rays of
+    `n_tiles_sample` random tiles.  Returns (seconds, rays rendered)."""
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    proj = O.project_lidar(scene, cfg, pose0, pose1)
+    count, rect = O.cull_lidar(proj["valid"], proj["box"], tiling, True)
+    _, ids, ranges = O.bin_pairs(count, rect, proj["key"], tiling.n_tiles, tiling.n_theta)
+    tiles = rng.choice(tiling.n_tiles, min(n_tiles_sample, tiling.n_tiles), replace=False)
+    rays = np.concatenate([tiling.tile_rays[tiling.tile_ray_offsets[x]:tiling.tile_ray_offsets[x + 1]]
+                           for x in tiles])
+    od = O.lidar_rays(tiling, pose0, pose1)[rays]
+    rec = O.records_from_projection(proj, scene)
+    O.composite(rec, ids, ranges, tiling.ray_tile[rays], tiling.ray_az[rays], tiling.ray_el[rays], od, wrap=1,
+                near=cfg.min_range, pi_f=tiling.pi_f, two_pi_f=tiling.two_pi_f)
+    return time.perf_counter() - t0, len(rays)
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, timed on the host cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    cores = cpu_count()
+    O.set_threads(cores)
+    cfg = synth.lidar_config("B")
+    scene = synth.scene_for("B")
+    tiling = O.Tiling(cfg)
+    poses = synth.batch_poses(max(args.steps + args.warmup, 1))
+    rng = np.random.default_rng(0)
+    n_tiles_sample = tiling.n_tiles  # every tile: the sample is the whole scan
+    for i in range(args.warmup):
+        oracle_scan_sample(scene, cfg, tiling, poses[i][0], poses[i][1], 64, rng)
+    secs, rays = 0.0, 0
+    for i in range(args.steps):
+        p0, p1 = poses[args.warmup + i]
+        s, n = oracle_scan_sample(scene, cfg, tiling, p0, p1, n_tiles_sample, rng)
+        secs += s
+        rays += n
+    value = rays / secs
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample": "full scan per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"full config-B scan per step (2M particles projected, all {tiling.n_rays} "
+                                       f"rays composited), {args.steps} steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ GPU leg
+def roofline_entries(stage_ms, counters, peaks, clocks_mhz):
+    """Roofline of every stage from ALGORITHMIC bytes / instructions per launch."""
+    hbm = peaks["hbm_gbs"]
+    n, n_vis, P, R, passes, n_tiles = (counters[k] for k in ("n", "n_vis", "P", "R", "passes", "n_tiles"))
+    # stage bytes: inputs the method must read + outputs it must write
+    b_project = n * (12 + 16 + 12 + 4) + n * (4 + 16 + 4) + n_vis * (192 + 80)
+    b_sort = n * (4 + 16 + 4) + 12 * P + passes * 24 * P + 8 * P + 8 * n_tiles
+    lane_instr = (C_BOX * counters["visited"] + C_RESP * counters["inbox"] + C_ACC * counters["contrib"] +
+                  C_RAY * R)
+    b_render = n_vis * 80 + P * 4 + R * (40 + 12)
+    alu_peak = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e12  # T lane-instr/s at max clock
+    out = {}
+    for name, bytes_, bound in (("project", b_project, "hbm"), ("bin_sort", b_sort, "hbm")):
+        t = stage_ms[name] * 1e-3
+        ach = bytes_ / t / 1e9
+        out[name] = {"bound": bound, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                     "algorithmic_bytes": int(bytes_), "ms": stage_ms[name]}
+    t = stage_ms["render"] * 1e-3
+    ach = lane_instr / t / 1e12
+    out["render"] = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "T lane-instr/s",
+                     "frac": ach / alu_peak, "algorithmic_lane_instr": int(lane_instr),
+                     "algorithmic_bytes": int(b_render), "hbm_frac": b_render / t / 1e9 / hbm,
+                     "ms": stage_ms["render"]}
+    return out
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_12901_b200 import simuli as SM
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    SM.load()
+    cfg = synth.lidar_config("B")
+    scene_np = synth.scene_for("B")  # same seed on every rank: replicated scene
+    scene = SM.to_device_scene(scene_np, dev)
+    r = SM.LidarRenderer(cfg, scene, device=dev)
+    n_total = (args.steps + args.warmup) * ws
+    my = shard_poses(n_total, ws, rank)
+    # size the pair buffers once (one sync), with head room for every pose of the shard
+    need = 0
+    for p0, p1 in my[:: max(1, len(my) // 4)]:
+        r.scan(p0, p1, sync_capacity=True)
+        torch.cuda.synchronize()
+        need = max(need, int(r.n_pairs.item()))
+    r.set_capacity(int(need * 1.3) + 4096)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    passes = 4 + (1 if r.n_tiles > 1 else 0) + (1 if r.n_tiles > 256 else 0) + (1 if r.n_tiles > 65536 else 0)
+
+    def scan(p0, p1):
+        r.set_poses(p0, p1)
+        r.project()
+        r.bin_sort()
+        r.render()
+
+    for i in range(args.warmup):
+        scan(*my[i])
+    torch.cuda.synchronize()
+    # counters of one scan (outside the timed region)
+    r.want_counters(True)
+    scan(*my[args.warmup])
+    torch.cuda.synchronize()
+    counters = {"n": r.n, "n_vis": int((r.tile_count > 0).sum().item()), "P": int(r.n_pairs.item()),
+                "R": r.n_rays, "passes": passes, "n_tiles": r.n_tiles,
+                "visited": int(r.out["n_visited"].sum().item()), "inbox": int(r.out["n_inbox"].sum().item()),
+                "contrib": int(r.out["n_contrib"].sum().item())}
+    r.want_counters(False)
+    if int(r.n_pairs.item()) > r.capacity:
+        raise RuntimeError("pair capacity too small")
+
+    clocks = ClockSampler(dev.index if ws == 1 else local)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the events
+        p0, p1 = my[args.warmup + i]
+        r.set_poses(p0, p1)
+        e = ev[i]
+        e[0].record(stream)
+        r.project()
+        e[1].record(stream)
+        r.bin_sort()
+        e[2].record(stream)
+        r.render()
+        e[3].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    stage_ms = {"project": sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps,
+                "bin_sort": sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps,
+                "render": sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps}
+    total_ms = sum(step_ms)
+    max_ms = total_ms
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_ms = float(t.item())
+        c = torch.tensor([counters["P"]], dtype=torch.int64, device=dev)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+
+    # ---- e2e through the public API with host buffers: pose in (kernel parameters), all
+    # per-ray outputs copied device -> pinned host every scan, synchronised.
+    e2e = None
+    if rank == 0 or True:
+        host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in r.out.items() if v is not None}
+        d2h = sum(v.numel() * v.element_size() for v in host.values())
+        torch.cuda.synchronize()
+        ee = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        tt = 0.0
+        for i in range(args.steps):
+            flush.zero_()
+            p0, p1 = my[args.warmup + i]
+            ee[0].record(stream)
+            r.scan(p0, p1)
+            for k, v in host.items():
+                v.copy_(r.out[k], non_blocking=True)
+            ee[1].record(stream)
+            ee[1].synchronize()
+            tt += ee[0].elapsed_time(ee[1])
+        e2e_ms = tt
+        if ws > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": ws * args.steps * r.n_rays / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * 28, "d2h_bytes_per_step": int(d2h),
+               "note": "per scan: start/end pose (2 x 28 B) in as kernel parameters, every per-ray output "
+                       "(zeta, omega, D, depth, gamma, beta, T, n) copied to pinned host memory; scene resident"}
+
+    peaks = read_peaks()
+    roof = roofline_entries(stage_ms, counters, peaks, clk.get("sm_mhz"))
+    dom = max(roof, key=lambda k: roof[k]["ms"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    d = roof[dom]
+    roofline = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
+                "frac": d["frac"], "traffic": traffic, "kernel": dom, "peak_source": peaks["source"]}
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    value = ws * args.steps * r.n_rays / (max_ms * 1e-3)
+    launches_per_step = 1 + (3 + passes + 1) + 1
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_gaussians": r.n, "rays_per_scan": r.n_rays,
+                       "scans_per_rank": args.steps, "l2": "flushed between scans (256 MB write) and scene "
+                                                          "(472 MB) > 126 MB L2", "parallelism": f"dp{ws}"},
+            "scans_per_s": value / r.n_rays,
+            "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "roofline": roofline, "stages": roof, "counters": counters,
+            "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"],
+                       "samples": clk["samples"]},
+            "wall_s_timed_region": wall}
+    if ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(scene_np, cfg)
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(scene_np, cfg):
+    """The oracle as it stands on the host cores, one bounded sample of the workload."""
+    from oracle import oracle as O
+    cores = cpu_count()
+    O.set_threads(cores)
+    tiling = O.Tiling(cfg)
+    rng = np.random.default_rng(1)
+    secs, rays = oracle_scan_sample(scene_np, cfg, tiling, cfg.pose_start, cfg.pose_end, tiling.n_tiles, rng)
+    return {"value": rays / secs, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"one full config-B scan: all {scene_np['means'].shape[0]} particles projected/culled/binned "
+                      f"and all {rays} rays composited in double precision; {secs:.2f} s wall"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

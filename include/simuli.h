@@ -167,7 +167,8 @@ typedef struct {
   float k[5];
   int32_t rolling_shutter;
   float near_m;        /* near plane (KB: minimum distance; radtan: minimum depth z)   */
-  float max_theta_rad; /* KB validity limit on the ray angle                           */
+  float max_theta_rad; /* validity limit on the angle between a point and the optical
+                          axis (both models; radtan is only meaningful inside its FOV)  */
   int32_t tile_px;
 } simuli_camera;
 
@@ -246,7 +247,9 @@ typedef struct {
  * zeta [n_rays][3] = sum f_i alpha_i T_i; opacity omega = sum alpha_i T_i (Eq. 1);
  * depth_accum D = sum tau_i alpha_i T_i; depth = D / omega (0 if omega = 0, A16);
  * intensity gamma = zeta_0; raydrop beta_drop = softmax(zeta_1, zeta_2)_drop;
- * final_T; n_contrib; ray_od [n_rays][6] double (origin, unit direction) as used. */
+ * final_T; n_contrib; ray_od [n_rays][6] double (origin, unit direction) as used.
+ * Workload counters: n_visited = list entries examined before the ray
+ * stopped, n_inbox = entries whose box contained the ray. */
 typedef struct {
   float* zeta;
   float* opacity;
@@ -257,6 +260,8 @@ typedef struct {
   float* final_T;
   int32_t* n_contrib;
   double* ray_od;
+  int32_t* n_visited;
+  int32_t* n_inbox;
 } simuli_lidar_out;
 
 /* Per-ray front-to-back compositing, Eq. 1: for every ray (origin t(s_j),
@@ -271,7 +276,8 @@ int32_t simuli_render_lidar(const simuli_projected* proj, const uint32_t* sorted
 /* Per-pixel camera outputs (device, [H*W] each, row-major; NULL to skip): rgb [H*W][3] =
  * foreground colour c_f (before the environment map / bilateral grid of Eq. 2), opacity,
  * depth_accum, depth, final_T, n_contrib, ray_od [H*W][6] double.  Pixels whose ray is
- * outside the lens model's validity (theta > max_theta) are not rendered (omega = 0). */
+ * outside the lens model's validity (theta > max_theta) are not rendered (omega = 0).
+ * n_visited / n_inbox: workload counters as for LiDAR. */
 typedef struct {
   float* rgb;
   float* opacity;
@@ -280,6 +286,8 @@ typedef struct {
   float* final_T;
   int32_t* n_contrib;
   double* ray_od;
+  int32_t* n_visited;
+  int32_t* n_inbox;
 } simuli_camera_out;
 
 int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorted_ids, const int32_t* tile_ranges,

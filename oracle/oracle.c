@@ -269,7 +269,8 @@ static int cam_project_frame(const or_camera* C, const double p[3], double* u, d
     *v = C->fy * sc * p[1] + C->cy;
     return (dist >= C->near_m && th <= C->max_theta) ? 1 : 0;
   } else {
-    if (fabs(p[2] - C->near_m) < 1e-4) *edge = 1;
+    double th = atan2(sqrt(p[0] * p[0] + p[1] * p[1]), p[2]);
+    if (fabs(p[2] - C->near_m) < 1e-4 || fabs(th - C->max_theta) < 1e-5) *edge = 1;
     if (!(p[2] > 0.0)) return -1;
     double xp = p[0] / p[2], yp = p[1] / p[2];
     double r2 = xp * xp + yp * yp;
@@ -279,7 +280,7 @@ static int cam_project_frame(const or_camera* C, const double p[3], double* u, d
     double yd = yp * radial + p1 * (r2 + 2.0 * yp * yp) + 2.0 * p2 * xp * yp;
     *u = C->fx * xd + C->cx;
     *v = C->fy * yd + C->cy;
-    return p[2] >= C->near_m ? 1 : 0;
+    return (p[2] >= C->near_m && th <= C->max_theta) ? 1 : 0;
   }
 }
 
@@ -366,7 +367,7 @@ int or_camera_unproject(const or_camera* C, double u, double v, double dir[3]) {
     dir[0] = x / n;
     dir[1] = y / n;
     dir[2] = 1.0 / n;
-    return 1;
+    return atan(sqrt(x * x + y * y)) <= C->max_theta;
   }
 }
 
@@ -1044,8 +1045,15 @@ int or_composite(int64_t n_gauss, const double* mu, const double* Mrows, const d
                       (double)bx[2] - p->eps_b <= xb && xb <= (double)bx[3] + p->eps_b;
           int strict = in_interval_a_d(bx[0], bx[1], xa, p->wrap, -p->eps_a) &&
                        (double)bx[2] + p->eps_b <= xb && xb <= (double)bx[3] - p->eps_b;
-          if (loose != strict) flag |= 1;
-          if (gamb && gamb[g] && loose) flag |= 8;
+          if (loose != strict || (gamb && gamb[g] && loose)) {
+            /* ambiguous membership matters only if this particle could composite with a
+             * weight alpha T above the impact threshold (its alpha if it were a member) */
+            double rs0[2];
+            or_response(&mu[(int64_t)g * 3], &Mrows[(int64_t)g * 9], o, d, rs0);
+            double a0 = sigma[g] * exp(-0.5 * rs0[1]);
+            if (!(isfinite(a0)) || (a0 >= p->alpha_min - p->eps_alpha && a0 * T > p->eps_impact))
+              flag |= (loose != strict) ? 1 : 8;
+          }
         }
         if (gamb && gamb[g] == 2) continue; /* listed for flagging only (oracle-invalid) */
         if (!member) continue;

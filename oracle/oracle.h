@@ -125,6 +125,7 @@ typedef struct {
   int32_t flag_mode;         /* 1: compute A23 threshold flags                          */
   double eps_a, eps_b;       /* box-edge ambiguity margins (coordinate units)           */
   double eps_alpha, eps_T_rel, eps_tau;
+  double eps_impact;         /* box-edge flags only when alpha*T of the particle > this  */
 } or_render_params;
 
 typedef struct {

@@ -73,7 +73,8 @@ class OrRenderParams(C.Structure):
     _fields_ = [("near_tau", C.c_double), ("alpha_min", C.c_double), ("alpha_max", C.c_double),
                 ("T_min", C.c_double), ("wrap", C.c_int32), ("pi_f", C.c_float), ("two_pi_f", C.c_float),
                 ("flag_mode", C.c_int32), ("eps_a", C.c_double), ("eps_b", C.c_double),
-                ("eps_alpha", C.c_double), ("eps_T_rel", C.c_double), ("eps_tau", C.c_double)]
+                ("eps_alpha", C.c_double), ("eps_T_rel", C.c_double), ("eps_tau", C.c_double),
+                ("eps_impact", C.c_double)]
 
 
 class OrRenderOut(C.Structure):
@@ -366,7 +367,7 @@ def composite(records, ids, ranges, ray_tile, ray_a, ray_b, ray_od, *, wrap, nea
     prm = OrRenderParams(float(np.float32(near)), float(np.float32(alpha_min)), float(np.float32(alpha_max)),
                          float(np.float32(T_min)), int(wrap), pf, tpf, int(flag_eps is not None),
                          fe.get("a", 0.0), fe.get("b", 0.0), fe.get("alpha", 0.0), fe.get("T_rel", 0.0),
-                         fe.get("tau", 0.0))
+                         fe.get("tau", 0.0), fe.get("impact", 0.0))
     out = {"feat": np.zeros((R, 3)), "opacity": np.zeros(R), "depth_accum": np.zeros(R), "depth": np.zeros(R),
            "T_final": np.zeros(R), "n_contrib": np.zeros(R, np.int32), "flag": np.zeros(R, np.int32),
            "scanned": np.zeros(R, np.int64), "inbox": np.zeros(R, np.int64)}

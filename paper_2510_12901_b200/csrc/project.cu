@@ -166,6 +166,7 @@ __device__ __forceinline__ int cam_frame(const ProjArgs& A, float px, float py, 
     return (dist >= A.near_m && th <= A.max_theta) ? 1 : 0;
   }
   if (!(pz > 0.f)) return -1;
+  const float th = atan2f(sqrtf(px * px + py * py), pz);
   const float xp = px / pz, yp = py / pz;
   const float r2 = xp * xp + yp * yp;
   const float radial = 1.f + r2 * (A.k[0] + r2 * (A.k[1] + r2 * A.k[4]));
@@ -173,7 +174,7 @@ __device__ __forceinline__ int cam_frame(const ProjArgs& A, float px, float py, 
   const float yd = yp * radial + A.k[2] * (r2 + 2.f * yp * yp) + 2.f * A.k[3] * xp * yp;
   *u = A.fx * xd + A.cx;
   *v = A.fy * yd + A.cy;
-  return pz >= A.near_m ? 1 : 0;
+  return (pz >= A.near_m && th <= A.max_theta) ? 1 : 0;
 }
 
 __device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3], float* u, float* v, float* s_out) {

@@ -36,6 +36,7 @@ struct LidarArgs {
   float *zeta, *opacity, *depth_accum, *depth, *intensity, *raydrop, *final_T;
   int* n_contrib;
   double* ray_od;
+  int *n_visited, *n_inbox;
 };
 
 __global__ void __launch_bounds__(32 * kWarpsPerCta) k_render_lidar(const LidarArgs A) {
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_render_lidar(const LidarA
   split_ray(o, dd, rf);
 
   float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
-  int nc = 0;
+  int nc = 0, nv = 0, ni = 0;
   bool done = !active;
   const int2 rg = __ldg(A.ranges + tile);
   for (int b = rg.x; b < rg.y; b += 32) {
@@ -85,7 +86,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_render_lidar(const LidarA
     if (!done) {
       for (int j = 0; j < nb; ++j) {
         const float4 bx = s_rec[warp][j][4];
+        ++nv;
         if (!in_box_wrap(bx.x, bx.y, bx.z, bx.w, ra, rb, A.pi_f, A.two_pi_f)) continue;
+        ++ni;
         const float4 r0 = s_rec[warp][j][0], r1 = s_rec[warp][j][1], r2 = s_rec[warp][j][2],
                      r3 = s_rec[warp][j][3];
         const float mu[3] = {r0.x, r0.y, r0.z};
@@ -125,6 +128,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_render_lidar(const LidarA
   if (A.raydrop) A.raydrop[ray] = raydrop_prob(acc1, acc2);
   if (A.final_T) A.final_T[ray] = T;
   if (A.n_contrib) A.n_contrib[ray] = nc;
+  if (A.n_visited) A.n_visited[ray] = nv;
+  if (A.n_inbox) A.n_inbox[ray] = ni;
   if (A.ray_od) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -146,6 +151,7 @@ struct CameraArgs {
   float *rgb, *opacity, *depth_accum, *depth, *final_T;
   int* n_contrib;
   double* ray_od;
+  int *n_visited, *n_inbox;
 };
 
 // inverse lens model in double (A22): KB by Newton on theta_d(theta) = r_d, radtan by
@@ -195,7 +201,7 @@ __device__ bool unproject(const CameraArgs& A, double u, double v, double dir[3]
   dir[0] = x / n;
   dir[1] = y / n;
   dir[2] = 1.0 / n;
-  return true;
+  return atan(sqrt(x * x + y * y)) <= A.max_theta;
 }
 
 template <int TP>
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(TP* TP) k_render_camera(const CameraArgs A) {
   RayF rf;
   split_ray(o, d, rf);
   float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
-  int nc = 0;
+  int nc = 0, nv = 0, ni = 0;
   bool done = !(inside && valid);
   const int2 rg = __ldg(A.ranges + tile);
   for (int b = rg.x; b < rg.y; b += NT) {
@@ -238,7 +244,9 @@ __global__ void __launch_bounds__(TP* TP) k_render_camera(const CameraArgs A) {
     if (!done) {
       for (int jj = 0; jj < nb; ++jj) {
         const float4 bx = s_rec[jj][4];
+        ++nv;
         if (!(bx.x <= pu && pu <= bx.y && bx.z <= pv && pv <= bx.w)) continue;
+        ++ni;
         const float4 r0 = s_rec[jj][0], r1 = s_rec[jj][1], r2 = s_rec[jj][2], r3 = s_rec[jj][3];
         const float mu[3] = {r0.x, r0.y, r0.z};
         const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
@@ -275,6 +283,8 @@ __global__ void __launch_bounds__(TP* TP) k_render_camera(const CameraArgs A) {
   if (A.depth) A.depth[p] = W > 0.f ? D / W : 0.f;
   if (A.final_T) A.final_T[p] = T;
   if (A.n_contrib) A.n_contrib[p] = nc;
+  if (A.n_visited) A.n_visited[p] = nv;
+  if (A.n_inbox) A.n_inbox[p] = ni;
   if (A.ray_od)
     for (int k = 0; k < 3; ++k) {
       A.ray_od[6 * p + k] = o[k];
@@ -322,6 +332,8 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   A.zeta = out->zeta; A.opacity = out->opacity; A.depth_accum = out->depth_accum; A.depth = out->depth;
   A.intensity = out->intensity; A.raydrop = out->raydrop; A.final_T = out->final_T; A.n_contrib = out->n_contrib;
   A.ray_od = out->ray_od;
+  A.n_visited = out->n_visited;
+  A.n_inbox = out->n_inbox;
   const int64_t warps = (int64_t)T.n_tiles * A.chunks_per_tile;
   const unsigned blocks = (unsigned)((warps + kWarpsPerCta - 1) / kWarpsPerCta);
   k_render_lidar<<<blocks, 32 * kWarpsPerCta, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A);
@@ -357,6 +369,7 @@ extern "C" int32_t simuli_render_camera(const simuli_projected* proj, const uint
   A.alpha_min = rp->alpha_min; A.alpha_max = rp->alpha_max; A.T_min = rp->T_min;
   A.rgb = out->rgb; A.opacity = out->opacity; A.depth_accum = out->depth_accum; A.depth = out->depth;
   A.final_T = out->final_T; A.n_contrib = out->n_contrib; A.ray_od = out->ray_od;
+  A.n_visited = out->n_visited; A.n_inbox = out->n_inbox;
   const unsigned blocks = (unsigned)(A.Wt * Ht);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   switch (C.tile_px) {

@@ -106,12 +106,12 @@ class RenderParams(C.Structure):
 
 class LidarOut(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("zeta", "opacity", "depth_accum", "depth", "intensity", "raydrop",
-                                          "final_T", "n_contrib", "ray_od")]
+                                          "final_T", "n_contrib", "ray_od", "n_visited", "n_inbox")]
 
 
 class CameraOut(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("rgb", "opacity", "depth_accum", "depth", "final_T", "n_contrib",
-                                          "ray_od")]
+                                          "ray_od", "n_visited", "n_inbox")]
 
 
 _lib = None
@@ -327,13 +327,20 @@ class LidarRenderer(_Frame):
         f = lambda *s: torch.empty(s, dtype=torch.float32, device=device)  # noqa: E731
         self.out = {"zeta": f(R, 3), "opacity": f(R), "depth_accum": f(R), "depth": f(R), "intensity": f(R),
                     "raydrop": f(R), "final_T": f(R), "n_contrib": torch.empty(R, dtype=torch.int32, device=device),
-                    "ray_od": None}
+                    "ray_od": None, "n_visited": None, "n_inbox": None}
         self._out_struct()
 
     def _out_struct(self):
         o = self.out
         self.out_struct = LidarOut(*[_ptr(o[k]) for k in ("zeta", "opacity", "depth_accum", "depth", "intensity",
-                                                          "raydrop", "final_T", "n_contrib", "ray_od")])
+                                                          "raydrop", "final_T", "n_contrib", "ray_od", "n_visited",
+                                                          "n_inbox")])
+
+    def want_counters(self, flag=True):
+        import torch
+        for k in ("n_visited", "n_inbox"):
+            self.out[k] = torch.empty(self.n_rays, dtype=torch.int32, device=self.device) if flag else None
+        self._out_struct()
 
     def want_ray_od(self, flag=True):
         import torch
@@ -380,13 +387,21 @@ class CameraRenderer(_Frame):
         P = cam.width * cam.height
         f = lambda *s: torch.empty(s, dtype=torch.float32, device=device)  # noqa: E731
         self.out = {"rgb": f(P, 3), "opacity": f(P), "depth_accum": f(P), "depth": f(P), "final_T": f(P),
-                    "n_contrib": torch.empty(P, dtype=torch.int32, device=device), "ray_od": None}
+                    "n_contrib": torch.empty(P, dtype=torch.int32, device=device), "ray_od": None,
+                    "n_visited": None, "n_inbox": None}
         self._out_struct()
 
     def _out_struct(self):
         o = self.out
         self.out_struct = CameraOut(*[_ptr(o[k]) for k in ("rgb", "opacity", "depth_accum", "depth", "final_T",
-                                                           "n_contrib", "ray_od")])
+                                                           "n_contrib", "ray_od", "n_visited", "n_inbox")])
+
+    def want_counters(self, flag=True):
+        import torch
+        P = self.cam_cfg.width * self.cam_cfg.height
+        for k in ("n_visited", "n_inbox"):
+            self.out[k] = torch.empty(P, dtype=torch.int32, device=self.device) if flag else None
+        self._out_struct()
 
     def want_ray_od(self, flag=True):
         import torch

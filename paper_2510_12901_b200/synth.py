@@ -151,7 +151,7 @@ def camera_config(name: str = "D") -> CameraConfig:
         return cfg
     if name == "pinhole-small":
         cfg = CameraConfig("pinhole-small", 0, 320, 240, 250.0, 250.0, 160.0, 120.0,
-                           (-0.1, 0.01, 0.001, -0.0005, 0.0))
+                           (-0.1, 0.01, 0.001, -0.0005, 0.0), max_theta=math.radians(50.0))
         cfg.pose_end = pose(yaw_quat(0.01, CAM_FORWARD_Q), [1.8, 0.1, 1.6])
         return cfg
     raise ValueError(name)

@@ -17,8 +17,11 @@ pytestmark = pytest.mark.gpu
 
 TOL_FEAT = 1e-4
 TOL_DEPTH = 1e-3
-LIDAR_EPS = {"a": 4e-6, "b": 4e-6, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4}
-CAMERA_EPS = {"a": 2e-3, "b": 2e-3, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4}
+# A23 flag margins: box edges (rad / px) at the measured GPU-vs-oracle box error bound,
+# alpha / T / tau thresholds at the float32 response error; box-edge flips only count when
+# the particle's alpha*T could move an output by more than a tenth of the tolerance.
+LIDAR_EPS = {"a": 2e-6, "b": 1e-6, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
+CAMERA_EPS = {"a": 1e-3, "b": 1e-3, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
 
 
 @pytest.fixture(scope="module")
@@ -84,7 +87,8 @@ def test_project_lidar_tier1(SM, oracle_mod, config):
     # depth keys: bit-exact float32 (A19)
     assert np.array_equal(r.depth_key.cpu().numpy().view(np.uint32), proj["key"].view(np.uint32))
     db = np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both].astype(np.float64))
-    assert db.max() < 2e-6, db.max()
+    print(f"box edge |gpu - oracle| max {db.max():.3e} p99.99 {np.percentile(db, 99.99):.3e}")
+    assert db[:, :2].max() < LIDAR_EPS["a"] and db[:, 2:].max() < LIDAR_EPS["b"], db.max(0)
     Mref = proj["Mrows"][both]
     rel = np.abs(rec[both, 3:12] - Mref) / np.abs(Mref).max(1, keepdims=True)
     assert rel.max() < 2e-6
@@ -128,7 +132,7 @@ def test_render_lidar_tier1(SM, oracle_mod, config):
     rec = gpu_records(r)
     od = r.out["ray_od"].cpu().numpy()
     ref = O.composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, wrap=1, near=cfg.min_range,
-                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4},
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4},
                       pi_f=t.pi_f, two_pi_f=t.two_pi_f)
     g, bd = O.decode_lidar(ref["feat"])
     ref["intensity"], ref["raydrop"] = g, bd
@@ -211,7 +215,8 @@ def test_bin_sort_synthetic_keys_large_tiles(SM):
     count = ((rect[:, 1] - rect[:, 0] + 1) * rect[:, 3]).astype(np.int32)
     count[rng.uniform(size=n) < 0.2] = 0
     key = rng.choice(np.float32([0.5, 1.0, 2.0, 3.5]), n).astype(np.float32)  # many ties
-    key[rng.uniform(size=n) < 0.5] = rng.uniform(0.1, 200, (rng.uniform(size=n) < 0.5).sum())
+    half = rng.uniform(size=n) < 0.5
+    key[half] = rng.uniform(0.1, 200, int(half.sum())).astype(np.float32)
     t = {k: torch.from_numpy(v).to(dev) for k, v in (("count", count), ("rect", rect), ("key", key))}
     proj = SM.Projected(0, t["rect"].data_ptr(), t["key"].data_ptr(), t["count"].data_ptr())
     P = int(count.sum())
@@ -303,7 +308,7 @@ def test_config_b_full_size_sampled(SM, oracle_mod):
     rec = gpu_records(r)
     od = r.out["ray_od"].cpu().numpy()
     ref = O.composite(rec, ids, ranges, t.ray_tile[rays], t.ray_az[rays], t.ray_el[rays], od[rays], wrap=1,
-                      near=cfg.min_range, flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4},
+                      near=cfg.min_range, flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4},
                       pi_f=t.pi_f, two_pi_f=t.two_pi_f)
     ref["intensity"], ref["raydrop"] = O.decode_lidar(ref["feat"])
     sub = {k: v[torch.from_numpy(rays).to(v.device)] for k, v in r.out.items() if v is not None}
@@ -344,7 +349,9 @@ def test_camera_tier1_and_tier2(SM, oracle_mod, name):
     gv, ov, amb = np.isfinite(rec[:, 16]), proj["valid"] != 0, proj["ambiguous"] != 0
     assert np.array_equal(gv[~amb], ov[~amb])
     both = gv & ov
-    assert np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both]).max() < 2e-3
+    db = np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both])
+    print(f"camera box edge |gpu - oracle| max {db.max():.3e} px")
+    assert db.max() < CAMERA_EPS["a"]
     count, rect = O.cull_camera(gv.astype(np.int32), rec[:, 16:20].copy(), cam)
     assert np.array_equal(c.tile_count.cpu().numpy(), count)
     Wt, Ht = O.camera_tiles(cam)
@@ -357,7 +364,7 @@ def test_camera_tier1_and_tier2(SM, oracle_mod, name):
     # tier 1: GPU records, lists, rays
     ref = O.composite(gpu_records(c), ids, ranges, rays["tile"], rays["u"], rays["v"], gpu_od, wrap=0,
                       near=cam.near, ray_valid=rays["valid"],
-                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-5, "T_rel": 2e-3, "tau": 1e-4})
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4})
     ok = ref["flag"] == 0
     assert ok.mean() > 0.999
     rgb = c.out["rgb"].cpu().numpy()
