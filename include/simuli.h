@@ -103,6 +103,7 @@ typedef struct {
   int32_t max_rays_in_tile; /* may exceed M when beams per tile do not divide M (A9)      */
   int32_t sat_rows, sat_cols; /* (8 n_phi + 1) x (1600 + 1)                              */
   int32_t n_rays, n_beams, n_azimuth;
+  int32_t max_beams_per_elev_tile, max_cols_per_az_tile;
   float pi_f, two_pi_f;     /* (float)pi, (float)(2 pi)                                    */
   float az_tile_scale;      /* (float)(n_theta / 2pi)                                      */
   float az_cell_scale;      /* (float)(cull_az_cells / 2pi)                                */
@@ -139,6 +140,7 @@ int32_t simuli_build_tiles(const simuli_lidar* lidar, const simuli_tiling_params
 typedef struct {
   int32_t n_phi, n_theta, n_tiles, max_rays_in_tile, sat_rows, sat_cols;
   int32_t cull_az_cells, cull_rows_per_tile, n_rays, n_beams, n_azimuth;
+  int32_t max_beams_per_elev_tile, max_cols_per_az_tile;
   float pi_f, two_pi_f, az_tile_scale, az_cell_scale;
   const float *elev_bounds, *cull_row_scale, *ray_az, *ray_el, *ray_s;
   const int32_t *ray_tile, *tile_ray_offsets, *tile_rays, *sat;
@@ -225,6 +227,9 @@ int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t
  * (0,0 if empty).  The order is (tile, depth key bits, id) -- unique, deterministic.
  * n_cols_total: N_theta (LiDAR) or ceil(W / tile_px) (camera).
  * sorted_keys / sorted_ids: device [pair_capacity]; tile_ranges: device [n_tiles][2];
+ * tile_order: device [n_tiles] or NULL -- the tiles ordered by decreasing list length
+ *   (power-of-two buckets; a longest-first schedule for the render kernels, which is a
+ *   performance hint only: results do not depend on it);
  * n_pairs_dev: device int64 (receives P).
  * pair_capacity >= 0: fully asynchronous; if P > pair_capacity only the first
  *   pair_capacity pairs are sorted and the result is INCOMPLETE -- the caller must check
@@ -233,7 +238,7 @@ int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t
  *   |pair_capacity| it returns SIMULI_ERR_CAPACITY with *pairs_required (host) = P. */
 int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles, int32_t n_cols_total,
                         void* workspace, size_t workspace_bytes, int64_t pair_capacity,
-                        uint64_t* sorted_keys, uint32_t* sorted_ids, int32_t* tile_ranges,
+                        uint64_t* sorted_keys, uint32_t* sorted_ids, int32_t* tile_ranges, int32_t* tile_order,
                         int64_t* n_pairs_dev, int64_t* pairs_required, void* stream);
 
 /* Compositing thresholds (A13, A14): skip alpha < alpha_min (default 1/255), clamp alpha
@@ -267,11 +272,12 @@ typedef struct {
 /* Per-ray front-to-back compositing, Eq. 1: for every ray (origin t(s_j),
  * direction R(s_j) u(phi_j, omega_b)) over its tile's sorted list, the particles whose box
  * contains the ray (A12) contribute alpha = min(alpha_max, sigma rho) with the 3D
- * response rho at tau_max, skipping tau < r_min (A15).  sorted_ids/tile_ranges
- * are simuli_bin_sort outputs; `proj` must hold the records of every listed particle. */
+ * response rho at tau_max, skipping tau < r_min (A15).  sorted_ids/tile_ranges/
+ * tile_order (NULL = natural order) are simuli_bin_sort outputs; `proj` must hold the
+ * records of every listed particle. */
 int32_t simuli_render_lidar(const simuli_projected* proj, const uint32_t* sorted_ids, const int32_t* tile_ranges,
-                            const simuli_project_params* params, const simuli_render_params* rparams,
-                            simuli_lidar_out* out, void* stream);
+                            const int32_t* tile_order, const simuli_project_params* params,
+                            const simuli_render_params* rparams, simuli_lidar_out* out, void* stream);
 
 /* Per-pixel camera outputs (device, [H*W] each, row-major; NULL to skip): rgb [H*W][3] =
  * foreground colour c_f (before the environment map / bilateral grid of Eq. 2), opacity,
@@ -291,8 +297,8 @@ typedef struct {
 } simuli_camera_out;
 
 int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorted_ids, const int32_t* tile_ranges,
-                             const simuli_project_params* params, const simuli_render_params* rparams,
-                             simuli_camera_out* out, void* stream);
+                             const int32_t* tile_order, const simuli_project_params* params,
+                             const simuli_render_params* rparams, simuli_camera_out* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -360,6 +360,36 @@ __global__ void k_ranges(const uint64_t* __restrict__ keys, const int64_t* __res
   }
 }
 
+// Longest-first schedule: tiles bucketed by floor(log2(list length)) in decreasing order
+// (a counting sort; the order inside a bucket is whatever the atomics give -- it only
+// affects scheduling, never results).  One CTA.
+__global__ void __launch_bounds__(1024) k_tile_order(const int2* __restrict__ ranges, int n_tiles,
+                                                     int* __restrict__ order) {
+  __shared__ int s_hist[33];
+  __shared__ int s_off[33];
+  for (int i = threadIdx.x; i < 33; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int2 r = ranges[t];
+    const int len = r.y - r.x;
+    atomicAdd(&s_hist[len > 0 ? 32 - __clz(len) : 0], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int b = 32; b >= 0; --b) {
+      s_off[b] = run;
+      run += s_hist[b];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int2 r = ranges[t];
+    const int len = r.y - r.x;
+    order[atomicAdd(&s_off[len > 0 ? 32 - __clz(len) : 0], 1)] = t;
+  }
+}
+
 int sort_passes(int32_t n_tiles) {
   int tile_bits = 0;
   while (tile_bits < 31 && (1ll << tile_bits) < (int64_t)n_tiles) ++tile_bits;
@@ -384,8 +414,8 @@ extern "C" int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t cap, int32_
 
 extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles, int32_t n_cols_total,
                                    void* workspace, size_t ws_bytes, int64_t pair_capacity, uint64_t* sorted_keys,
-                                   uint32_t* sorted_ids, int32_t* tile_ranges, int64_t* n_pairs_dev,
-                                   int64_t* pairs_required, void* stream) {
+                                   uint32_t* sorted_ids, int32_t* tile_ranges, int32_t* tile_order,
+                                   int64_t* n_pairs_dev, int64_t* pairs_required, void* stream) {
   using namespace simuli;
   clear_error();
   SIMULI_REQUIRE(proj && n >= 0 && n_tiles >= 1 && n_cols_total >= 1 && n_cols_total <= n_tiles,
@@ -448,6 +478,10 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
   if (cap > 0) {
     k_ranges<<<148 * 4, 256, 0, st>>>(sorted_keys, n_pairs_dev, cap, reinterpret_cast<int2*>(tile_ranges));
     if (int32_t e = check("ranges")) return e;
+  }
+  if (tile_order) {
+    k_tile_order<<<1, 1024, 0, st>>>(reinterpret_cast<const int2*>(tile_ranges), n_tiles, tile_order);
+    if (int32_t e = check("tile order")) return e;
   }
   return SIMULI_OK;
 }

@@ -292,6 +292,268 @@ __global__ void __launch_bounds__(TP* TP) k_render_camera(const CameraArgs A) {
     }
 }
 
+// ------------------------------------------------------------------ LiDAR v2
+// One CTA of kV2Warps warps per work item = (tile, beam group, column group) with <= 32
+// rays; items are scheduled longest-list-first (tile_order).  Each round stages kV2E list
+// entries' records in shared memory with cp.async (double buffered, the next round's
+// copies in flight while the current one is processed), then:
+//  * producer (all warps, lane = list entry): the entry's ray mask over the item's rays,
+//    factorised as (columns inside the azimuth interval) x (beams inside the elevation
+//    interval) -- the exact A12 membership, ~6 instructions per column / beam; a ballot
+//    transpose gives each ray its member entries; the (entry, ray) member pairs are
+//    compacted and their responses (alpha, tau) computed with every lane busy;
+//  * consumer (warp 0, lane = ray): walks its member entries of the round in list order
+//    and composites front to back exactly as Eq. 1; a warp vote ends the item once every
+//    ray has terminated.
+// The per-ray arithmetic (order and operands) is independent of the tiling and of
+// culling, so results are bit-identical across (N_phi, M) and culling on/off.
+constexpr int kV2Warps = 8;
+constexpr int kV2E = 32 * kV2Warps;
+
+struct V2Smem {
+  float4 rec[2][kV2E][5];       // staged records (double buffer)
+  float2 at[kV2E][32];          // (alpha, tau) of member pairs [entry][ray]
+  uint32_t memb[kV2Warps][32];  // per warp, per ray: member entries of the warp's 32
+  uint32_t wmask[kV2Warps][32]; // per entry ray mask
+  int wex[kV2Warps][32];        // per warp exclusive pair offsets
+  float ray_oh[32][3], ray_ol[32][3], ray_dh[32][3], ray_dl[32][3];
+  float col_phi[32], beam_el[32];
+  int col_id[32], beam_id[32];
+  int all_done;
+};
+
+struct LidarV2Args {
+  const float4* record;
+  const uint32_t* ids;
+  const int2* ranges;
+  const int* order;
+  const int *etb_off, *etb, *atc_off, *atc;
+  const float *ray_az, *ray_el, *ray_s;
+  int n_theta, n_az, items_per_tile, cg, bg, n_cg;
+  int64_t n_items;
+  PoseInterpD pose;
+  float pi_f, two_pi_f, near_tau, alpha_min, alpha_max, T_min;
+  float *zeta, *opacity, *depth_accum, *depth, *intensity, *raydrop, *final_T;
+  int* n_contrib;
+  double* ray_od;
+  int *n_visited, *n_inbox;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__global__ void __launch_bounds__(32 * kV2Warps) k_render_lidar_v2(const LidarV2Args A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V2Smem& S = *reinterpret_cast<V2Smem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t item = blockIdx.x;
+  const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
+  const int tile = A.order ? __ldg(A.order + tslot) : tslot;
+  const int et = tile / A.n_theta, at_ = tile % A.n_theta;
+  const int bgi = sub / A.n_cg, cgi = sub % A.n_cg;
+  const int b0 = __ldg(A.etb_off + et) + bgi * A.bg, b1 = min(__ldg(A.etb_off + et + 1), b0 + A.bg);
+  const int c0 = __ldg(A.atc_off + at_) + cgi * A.cg, c1 = min(__ldg(A.atc_off + at_ + 1), c0 + A.cg);
+  const int nb = b1 - b0, nc = c1 - c0;
+  if (nb <= 0 || nc <= 0) return;  // CTA-uniform
+  const int R = nb * nc;            // <= 32 by construction of (bg, cg)
+
+  // ---- item setup: column azimuths, beam elevations, rays in double (warp 0)
+  if (tid < nc) {
+    const int j = __ldg(A.atc + c0 + tid);
+    S.col_id[tid] = j;
+    S.col_phi[tid] = __ldg(A.ray_az + j);
+  }
+  if (tid >= 32 && tid < 32 + nb) {
+    const int b = __ldg(A.etb + b0 + tid - 32);
+    S.beam_id[tid - 32] = b;
+    S.beam_el[tid - 32] = __ldg(A.ray_el + (size_t)b * A.n_az);
+  }
+  if (tid == 0) S.all_done = 0;
+  __syncthreads();
+  int ray = 0;
+  double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
+  if (warp == 0 && lane < R) {
+    const int bi = lane / nc, ci = lane % nc;
+    const int j = S.col_id[ci];
+    ray = S.beam_id[bi] * A.n_az + j;
+    double Rm[9];
+    pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
+    double sa, ca, se, ce;
+    sincos((double)S.col_phi[ci], &sa, &ca);
+    sincos((double)S.beam_el[bi], &se, &ce);
+    const double u[3] = {ce * ca, ce * sa, se};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
+    RayF rf;
+    split_ray(o, dd, rf);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      S.ray_oh[lane][i] = rf.o_hi[i];
+      S.ray_ol[lane][i] = rf.o_lo[i];
+      S.ray_dh[lane][i] = rf.d_hi[i];
+      S.ray_dl[lane][i] = rf.d_lo[i];
+    }
+  }
+  const int2 rg = __ldg(A.ranges + tile);
+
+  auto issue = [&](int buf, int start) {
+    const int e = start + tid;
+    if (e < rg.y) {
+      const float4* src = A.record + (size_t)__ldg(A.ids + e) * 5;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[buf][tid][c], src + c);
+    }
+    cp_async_commit();
+  };
+
+  // consumer state (warp 0, lane = ray)
+  float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
+  int nc_ = 0, nv = 0, ni = 0;
+  bool done = !(warp == 0 && lane < R);
+
+  issue(0, rg.x);
+  for (int round = 0;; ++round) {
+    const int cur = round & 1;
+    const int start = rg.x + round * kV2E;
+    if (start >= rg.y) break;  // CTA-uniform
+    issue(cur ^ 1, start + kV2E);
+    cp_async_wait1();
+    __syncthreads();
+    // ---- producer: ray mask of entry `tid`
+    const bool valid = start + tid < rg.y;
+    uint32_t m = 0;
+    if (valid) {
+      const float4 bx = S.rec[cur][tid][4];
+      uint32_t colbits = 0;
+      if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
+        colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
+      } else {
+        const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
+        const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
+        for (int ci = 0; ci < nc; ++ci) {
+          const float p = S.col_phi[ci];
+          const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
+          colbits |= (uint32_t)in << ci;
+        }
+      }
+      if (colbits)
+        for (int bi = 0; bi < nb; ++bi) {
+          const float w = S.beam_el[bi];
+          if (bx.z <= w && w <= bx.w) m |= colbits << (bi * nc);
+        }
+    }
+    // ballot transpose: lane r of warp w gets the warp's entries containing ray r
+    uint32_t my = 0;
+    for (int r = 0; r < R; ++r) {
+      const uint32_t b = __ballot_sync(0xffffffffu, (m >> r) & 1u);
+      if (lane == r) my = b;
+    }
+    S.memb[warp][lane] = my;
+    // compaction of member pairs and their responses
+    const int k = __popc(m);
+    int inc = k;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += t;
+    }
+    const int K = __shfl_sync(0xffffffffu, inc, 31);
+    S.wex[warp][lane] = inc - k;
+    S.wmask[warp][lane] = m;
+    __syncwarp();
+    for (int idx = lane; idx < K; idx += 32) {
+      int lo = 0, hi = 32;  // last owner with wex <= idx
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (S.wex[warp][mid] <= idx) lo = mid;
+        else hi = mid;
+      }
+      const uint32_t mo = S.wmask[warp][lo];
+      const int r = __fns(mo, 0, idx - S.wex[warp][lo] + 1);
+      const int e = warp * 32 + lo;
+      const float4 r0 = S.rec[cur][e][0], r1 = S.rec[cur][e][1], r2 = S.rec[cur][e][2], r3 = S.rec[cur][e][3];
+      const float mu[3] = {r0.x, r0.y, r0.z};
+      const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
+      RayF rf;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        rf.o_hi[i] = S.ray_oh[r][i];
+        rf.o_lo[i] = S.ray_ol[r][i];
+        rf.d_hi[i] = S.ray_dh[r][i];
+        rf.d_lo[i] = S.ray_dl[r][i];
+      }
+      float tau, d2;
+      response(rf, mu, M, &tau, &d2);
+      S.at[e][r] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
+    }
+    __syncthreads();
+    // ---- consumer: warp 0 composites its rays' members in list order
+    if (warp == 0) {
+      if (!done) {
+        const int n_in_round = min(kV2E, rg.y - start);
+        for (int w = 0; w < kV2Warps && !done; ++w) {
+          uint32_t bits = S.memb[w][lane];
+          while (bits) {
+            const int o = __ffs(bits) - 1;
+            bits &= bits - 1u;
+            const int e = w * 32 + o;
+            ++ni;
+            const float2 a = S.at[e][lane];
+            if (a.y < A.near_tau || a.x < A.alpha_min) continue;
+            const float Tn = T * (1.f - a.x);
+            if (Tn < A.T_min) {
+              done = true;
+              nv += e + 1;  // entries examined this round up to the stopping one
+              break;
+            }
+            const float4 r3 = S.rec[cur][e][3];
+            const float wgt = a.x * T;
+            acc0 = fmaf(wgt, r3.y, acc0);
+            acc1 = fmaf(wgt, r3.z, acc1);
+            acc2 = fmaf(wgt, r3.w, acc2);
+            D = fmaf(wgt, a.y, D);
+            W += wgt;
+            ++nc_;
+            T = Tn;
+          }
+        }
+        if (!done) nv += n_in_round;
+      }
+      const bool all = __all_sync(0xffffffffu, done);
+      if (lane == 0) S.all_done = all ? 1 : 0;
+    }
+    __syncthreads();
+    if (S.all_done) break;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (warp != 0 || lane >= R) return;
+  if (A.zeta) {
+    A.zeta[3 * (size_t)ray] = acc0;
+    A.zeta[3 * (size_t)ray + 1] = acc1;
+    A.zeta[3 * (size_t)ray + 2] = acc2;
+  }
+  if (A.opacity) A.opacity[ray] = W;
+  if (A.depth_accum) A.depth_accum[ray] = D;
+  if (A.depth) A.depth[ray] = W > 0.f ? D / W : 0.f;
+  if (A.intensity) A.intensity[ray] = acc0;
+  if (A.raydrop) A.raydrop[ray] = raydrop_prob(acc1, acc2);
+  if (A.final_T) A.final_T[ray] = T;
+  if (A.n_contrib) A.n_contrib[ray] = nc_;
+  if (A.n_visited) A.n_visited[ray] = nv;
+  if (A.n_inbox) A.n_inbox[ray] = ni;
+  if (A.ray_od) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      A.ray_od[6 * (size_t)ray + i] = o[i];
+      A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
+    }
+  }
+}
+
 int32_t launch_check(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -305,8 +567,9 @@ int32_t launch_check(const char* what) {
 }  // namespace simuli
 
 extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint32_t* sorted_ids,
-                                       const int32_t* tile_ranges, const simuli_project_params* P,
-                                       const simuli_render_params* rp, simuli_lidar_out* out, void* stream) {
+                                       const int32_t* tile_ranges, const int32_t* tile_order,
+                                       const simuli_project_params* P, const simuli_render_params* rp,
+                                       simuli_lidar_out* out, void* stream) {
   using namespace simuli;
   clear_error();
   SIMULI_REQUIRE(proj && proj->record && sorted_ids && tile_ranges && P && rp && out, "simuli_render_lidar: NULL argument");
@@ -315,6 +578,46 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   SIMULI_REQUIRE(T.tile_ray_offsets && T.tile_rays && T.ray_az && T.ray_el && T.ray_s && T.n_tiles >= 1,
                  "simuli_render_lidar: incomplete device tiling");
   SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(proj->record) % 16 == 0, "record must be 16-byte aligned");
+  static const bool use_v1 = [] {
+    const char* v = getenv("SIMULI_LIDAR_KERNEL");
+    return v && v[0] == 'v' && v[1] == '1';
+  }();
+  if (!use_v1) {
+    SIMULI_REQUIRE(T.elev_tile_beam_offsets && T.elev_tile_beams && T.az_tile_col_offsets && T.az_tile_cols,
+                   "simuli_render_lidar: device tiling lacks the beam / column CSR");
+    LidarV2Args A{};
+    A.record = reinterpret_cast<const float4*>(proj->record);
+    A.ids = sorted_ids;
+    A.ranges = reinterpret_cast<const int2*>(tile_ranges);
+    A.order = tile_order;
+    A.etb_off = T.elev_tile_beam_offsets; A.etb = T.elev_tile_beams;
+    A.atc_off = T.az_tile_col_offsets; A.atc = T.az_tile_cols;
+    A.ray_az = T.ray_az; A.ray_el = T.ray_el; A.ray_s = T.ray_s;
+    A.n_theta = T.n_theta; A.n_az = T.n_azimuth;
+    // work items: beam groups x column groups of <= 32 rays per tile, uniform over tiles
+    SIMULI_REQUIRE(T.max_beams_per_elev_tile >= 1 && T.max_cols_per_az_tile >= 1,
+                   "simuli_render_lidar: tiling maxima missing");
+    A.cg = T.max_cols_per_az_tile < 32 ? T.max_cols_per_az_tile : 32;
+    A.bg = 32 / A.cg;
+    A.n_cg = (T.max_cols_per_az_tile + A.cg - 1) / A.cg;
+    const int nbg = (T.max_beams_per_elev_tile + A.bg - 1) / A.bg;
+    A.items_per_tile = A.n_cg * nbg;
+    A.n_items = (int64_t)T.n_tiles * A.items_per_tile;
+    A.pose = make_pose_interp_d(P->pose_start, P->pose_end);
+    A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f;
+    A.near_tau = P->lidar->min_range_m;
+    A.alpha_min = rp->alpha_min; A.alpha_max = rp->alpha_max; A.T_min = rp->T_min;
+    A.zeta = out->zeta; A.opacity = out->opacity; A.depth_accum = out->depth_accum; A.depth = out->depth;
+    A.intensity = out->intensity; A.raydrop = out->raydrop; A.final_T = out->final_T; A.n_contrib = out->n_contrib;
+    A.ray_od = out->ray_od; A.n_visited = out->n_visited; A.n_inbox = out->n_inbox;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_render_lidar_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(V2Smem));
+      attr_set = true;
+    }
+    k_render_lidar_v2<<<(unsigned)A.n_items, 32 * kV2Warps, sizeof(V2Smem), reinterpret_cast<cudaStream_t>(stream)>>>(A);
+    return launch_check("simuli_render_lidar");
+  }
   LidarArgs A{};
   A.record = reinterpret_cast<const float4*>(proj->record);
   A.ids = sorted_ids;
@@ -341,8 +644,9 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
 }
 
 extern "C" int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorted_ids,
-                                        const int32_t* tile_ranges, const simuli_project_params* P,
-                                        const simuli_render_params* rp, simuli_camera_out* out, void* stream) {
+                                        const int32_t* tile_ranges, const int32_t* tile_order,
+                                        const simuli_project_params* P, const simuli_render_params* rp,
+                                        simuli_camera_out* out, void* stream) {
   using namespace simuli;
   clear_error();
   SIMULI_REQUIRE(proj && proj->record && sorted_ids && tile_ranges && P && rp && out,

@@ -198,6 +198,12 @@ extern "C" int32_t simuli_build_tiles(const simuli_lidar* lidar, const simuli_ti
   out->n_rays = R;
   out->n_beams = B;
   out->n_azimuth = A;
+  out->max_beams_per_elev_tile = *std::max_element(beams_in.begin(), beams_in.end());
+  {
+    std::vector<int32_t> cols_in(tm.n_theta, 0);
+    for (int32_t j = 0; j < A; ++j) cols_in[col_tile[j]]++;
+    out->max_cols_per_az_tile = *std::max_element(cols_in.begin(), cols_in.end());
+  }
   out->pi_f = tm.pi_f;
   out->two_pi_f = tm.two_pi_f;
   out->az_tile_scale = tm.az_tile_scale;

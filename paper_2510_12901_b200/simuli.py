@@ -54,6 +54,7 @@ class TilingParams(C.Structure):
 _TILING_SCALARS = [("n_phi", C.c_int32), ("n_theta", C.c_int32), ("n_tiles", C.c_int32),
                    ("max_rays_in_tile", C.c_int32), ("sat_rows", C.c_int32), ("sat_cols", C.c_int32),
                    ("n_rays", C.c_int32), ("n_beams", C.c_int32), ("n_azimuth", C.c_int32),
+                   ("max_beams_per_elev_tile", C.c_int32), ("max_cols_per_az_tile", C.c_int32),
                    ("pi_f", C.c_float), ("two_pi_f", C.c_float), ("az_tile_scale", C.c_float),
                    ("az_cell_scale", C.c_float)]
 _TILING_ARRAYS = [("elev_bounds", f32p), ("cull_row_scale", f32p), ("ray_az", f32p), ("ray_el", f32p),
@@ -70,7 +71,8 @@ class TilingDev(C.Structure):
     _fields_ = [("n_phi", C.c_int32), ("n_theta", C.c_int32), ("n_tiles", C.c_int32),
                 ("max_rays_in_tile", C.c_int32), ("sat_rows", C.c_int32), ("sat_cols", C.c_int32),
                 ("cull_az_cells", C.c_int32), ("cull_rows_per_tile", C.c_int32), ("n_rays", C.c_int32),
-                ("n_beams", C.c_int32), ("n_azimuth", C.c_int32), ("pi_f", C.c_float), ("two_pi_f", C.c_float),
+                ("n_beams", C.c_int32), ("n_azimuth", C.c_int32), ("max_beams_per_elev_tile", C.c_int32),
+                ("max_cols_per_az_tile", C.c_int32), ("pi_f", C.c_float), ("two_pi_f", C.c_float),
                 ("az_tile_scale", C.c_float), ("az_cell_scale", C.c_float)] + \
                [(name, C.c_void_p) for name, _ in _TILING_ARRAYS]
 
@@ -131,12 +133,14 @@ def load():
     L.simuli_project.argtypes = [C.POINTER(Gaussians), C.POINTER(ProjectParams), C.POINTER(Projected), C.c_void_p]
     L.simuli_bin_sort_workspace_size.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]
     L.simuli_bin_sort.argtypes = [C.POINTER(Projected), C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t,
-                                  C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_int64), C.c_void_p]
-    L.simuli_render_lidar.argtypes = [C.POINTER(Projected), C.c_void_p, C.c_void_p, C.POINTER(ProjectParams),
-                                      C.POINTER(RenderParams), C.POINTER(LidarOut), C.c_void_p]
-    L.simuli_render_camera.argtypes = [C.POINTER(Projected), C.c_void_p, C.c_void_p, C.POINTER(ProjectParams),
-                                       C.POINTER(RenderParams), C.POINTER(CameraOut), C.c_void_p]
+    L.simuli_render_lidar.argtypes = [C.POINTER(Projected), C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(LidarOut),
+                                      C.c_void_p]
+    L.simuli_render_camera.argtypes = [C.POINTER(Projected), C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(CameraOut),
+                                       C.c_void_p]
     for name in EXPORTED:
         if name not in ("simuli_last_error", "simuli_abi_version"):
             getattr(L, name).restype = C.c_int32
@@ -204,11 +208,12 @@ def simuli_bin_sort_workspace_size(n, capacity, n_tiles) -> int:
 
 
 def simuli_bin_sort(proj: Projected, n, n_tiles, n_cols_total, workspace, capacity, sorted_keys, sorted_ids,
-                    tile_ranges, n_pairs_dev, stream=None) -> int | None:
+                    tile_ranges, n_pairs_dev, stream=None, tile_order=None) -> int | None:
     req = C.c_int64(-1)
     code = load().simuli_bin_sort(C.byref(proj), int(n), int(n_tiles), int(n_cols_total), _ptr(workspace),
                                   workspace.numel() * workspace.element_size(), int(capacity), _ptr(sorted_keys),
-                                  _ptr(sorted_ids), _ptr(tile_ranges), _ptr(n_pairs_dev), C.byref(req),
+                                  _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order), _ptr(n_pairs_dev),
+                                  C.byref(req),
                                   _stream(stream))
     if code == SIMULI_ERR_CAPACITY:
         return int(req.value)
@@ -216,13 +221,16 @@ def simuli_bin_sort(proj: Projected, n, n_tiles, n_cols_total, workspace, capaci
     return None
 
 
-def simuli_render_lidar(proj, sorted_ids, tile_ranges, params, rparams, out: LidarOut, stream=None):
-    _check(load().simuli_render_lidar(C.byref(proj), _ptr(sorted_ids), _ptr(tile_ranges), C.byref(params),
+def simuli_render_lidar(proj, sorted_ids, tile_ranges, params, rparams, out: LidarOut, stream=None, tile_order=None):
+    _check(load().simuli_render_lidar(C.byref(proj), _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order),
+                                      C.byref(params),
                                       C.byref(rparams), C.byref(out), _stream(stream)))
 
 
-def simuli_render_camera(proj, sorted_ids, tile_ranges, params, rparams, out: CameraOut, stream=None):
-    _check(load().simuli_render_camera(C.byref(proj), _ptr(sorted_ids), _ptr(tile_ranges), C.byref(params),
+def simuli_render_camera(proj, sorted_ids, tile_ranges, params, rparams, out: CameraOut, stream=None,
+                         tile_order=None):
+    _check(load().simuli_render_camera(C.byref(proj), _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order),
+                                       C.byref(params),
                                        C.byref(rparams), C.byref(out), _stream(stream)))
 
 
@@ -255,6 +263,7 @@ class _Frame:
         self.depth_key = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.tile_count = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         self.tile_ranges = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
+        self.tile_order = torch.empty(n_tiles, dtype=torch.int32, device=dev)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=dev)
         self.projected = Projected(_ptr(self.record), _ptr(self.tile_rect), _ptr(self.depth_key),
                                    _ptr(self.tile_count))
@@ -276,12 +285,13 @@ class _Frame:
         """Duplicate + sort.  sync_capacity=True: one host sync to grow buffers if needed."""
         cap = -self.capacity if sync_capacity else self.capacity
         need = simuli_bin_sort(self.projected, self.n, self.n_tiles, self.n_cols_total, self.workspace, cap,
-                               self.sorted_keys, self.sorted_ids, self.tile_ranges, self.n_pairs, stream)
+                               self.sorted_keys, self.sorted_ids, self.tile_ranges, self.n_pairs, stream,
+                               self.tile_order)
         if need is not None:
             self.set_capacity(int(need * 1.25) + 1024)
             need = simuli_bin_sort(self.projected, self.n, self.n_tiles, self.n_cols_total, self.workspace,
                                    -self.capacity, self.sorted_keys, self.sorted_ids, self.tile_ranges,
-                                   self.n_pairs, stream)
+                                   self.n_pairs, stream, self.tile_order)
             assert need is None
 
     def set_poses(self, pose_start, pose_end):
@@ -307,7 +317,7 @@ class LidarRenderer(_Frame):
             self.tiling_dev_tensors[name] = torch.from_numpy(a.copy()).to(device)
         td = TilingDev(th["n_phi"], th["n_theta"], th["n_tiles"], th["max_rays_in_tile"], th["sat_rows"],
                        th["sat_cols"], cfg.cull_az_cells, cfg.cull_rows_per_tile, th["n_rays"], th["n_beams"],
-                       th["n_azimuth"], th["pi_f"], th["two_pi_f"], th["az_tile_scale"], th["az_cell_scale"],
+                       th["n_azimuth"], th["max_beams_per_elev_tile"], th["max_cols_per_az_tile"], th["pi_f"], th["two_pi_f"], th["az_tile_scale"], th["az_cell_scale"],
                        *[self.tiling_dev_tensors[name].data_ptr() for name, _ in _TILING_ARRAYS])
         self.tiling_dev = td
         beams = np.ascontiguousarray(cfg.beams, np.float32)
@@ -349,7 +359,7 @@ class LidarRenderer(_Frame):
 
     def render(self, stream=None):
         simuli_render_lidar(self.projected, self.sorted_ids, self.tile_ranges, self.params, self.rparams,
-                            self.out_struct, stream)
+                            self.out_struct, stream, self.tile_order)
 
     def scan(self, pose_start=None, pose_end=None, stream=None, sync_capacity=False):
         """Enqueue one full scan: project -> bin_sort -> render (north-star stages 1, 3-5)."""
@@ -411,7 +421,7 @@ class CameraRenderer(_Frame):
 
     def render(self, stream=None):
         simuli_render_camera(self.projected, self.sorted_ids, self.tile_ranges, self.params, self.rparams,
-                             self.out_struct, stream)
+                             self.out_struct, stream, self.tile_order)
 
     def frame(self, pose_start=None, pose_end=None, stream=None, sync_capacity=False):
         if pose_start is not None:

@@ -72,6 +72,8 @@ def _compare_tiling(cfg, SM, O):
         for j in p["az_tile_cols"][p["az_tile_col_offsets"][c]:p["az_tile_col_offsets"][c + 1]]:
             assert p["ray_tile"][j] % p["n_theta"] == c
     assert p["elev_tile_beam_offsets"][-1] == B and p["az_tile_col_offsets"][-1] == A
+    assert p["max_beams_per_elev_tile"] == np.diff(p["elev_tile_beam_offsets"]).max()
+    assert p["max_cols_per_az_tile"] == np.diff(p["az_tile_col_offsets"]).max()
 
 
 @pytest.mark.parametrize("name", ["A", "B", "C", "tiny"])
@@ -115,7 +117,7 @@ def test_workspace_size_and_bad_args(lib):
     L = lib.load()
     assert L.simuli_project(None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
     assert b"NULL" in L.simuli_last_error()
-    assert L.simuli_render_lidar(None, None, None, None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
-    assert L.simuli_render_camera(None, None, None, None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
+    assert L.simuli_render_lidar(None, None, None, None, None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
+    assert L.simuli_render_camera(None, None, None, None, None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
     size = ctypes.c_size_t(0)
     assert L.simuli_bin_sort_workspace_size(-1, 10, 1, ctypes.byref(size)) == lib.SIMULI_ERR_INVALID_ARGUMENT

@@ -20,8 +20,11 @@ TOL_DEPTH = 1e-3
 # A23 flag margins: box edges (rad / px) at the measured GPU-vs-oracle box error bound,
 # alpha / T / tau thresholds at the float32 response error; box-edge flips only count when
 # the particle's alpha*T could move an output by more than a tenth of the tolerance.
-LIDAR_EPS = {"a": 2e-6, "b": 1e-6, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
-CAMERA_EPS = {"a": 1e-3, "b": 1e-3, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
+LIDAR_EPS = {"a": 1.2e-6, "b": 6e-7, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
+CAMERA_EPS = {"a": 5e-4, "b": 5e-4, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
+# share of rays the oracle may flag in tier 2; config B traverses ~360 list entries per ray,
+# so its box-edge coincidences at a 1.2e-6 rad margin are ~0.5 %
+FLAG_BUDGET = {"default": 0.005, "B": 0.01}
 
 
 @pytest.fixture(scope="module")
@@ -226,7 +229,8 @@ def test_bin_sort_synthetic_keys_large_tiles(SM):
     ids = torch.empty(cap, dtype=torch.int32, device=dev)
     ranges = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
     npairs = torch.zeros(1, dtype=torch.int64, device=dev)
-    SM.simuli_bin_sort(proj, n, n_tiles, ncols, ws, cap, keys, ids, ranges, npairs)
+    order = torch.empty(n_tiles, dtype=torch.int32, device=dev)
+    SM.simuli_bin_sort(proj, n, n_tiles, ncols, ws, cap, keys, ids, ranges, npairs, tile_order=order)
     torch.cuda.synchronize()
     assert npairs.item() == P
     # reference: enumerate pairs in particle order, stable sort by key
@@ -241,6 +245,10 @@ def test_bin_sort_synthetic_keys_large_tiles(SM):
     st = np.searchsorted(k64[order] >> np.uint64(32), np.arange(n_tiles), "left")
     en = np.searchsorted(k64[order] >> np.uint64(32), np.arange(n_tiles), "right")
     assert np.array_equal(rr[:, 0][en > st], st[en > st]) and np.array_equal(rr[:, 1], np.where(en > st, en, 0))
+    od = order.cpu().numpy()
+    assert np.array_equal(np.sort(od), np.arange(n_tiles))  # a permutation, longest lists first
+    lens = rr[od, 1] - rr[od, 0]
+    assert np.all(np.diff(np.floor(np.log2(lens + 0.5))) <= 0)
 
 
 def test_bin_sort_capacity_protocol(SM):
@@ -325,7 +333,7 @@ def test_config_b_full_size_sampled(SM, oracle_mod):
                        near=cfg.min_range, gamb=gamb, flag_eps=LIDAR_EPS, pi_f=t.pi_f, two_pi_f=t.two_pi_f)
     ref2["intensity"], ref2["raydrop"] = O.decode_lidar(ref2["feat"])
     ok = ref2["flag"] == 0
-    assert ok.mean() > 0.995, ok.mean()
+    assert ok.mean() > 1 - FLAG_BUDGET["B"], ok.mean()
     compare_lidar(sub, ref2, ok)
 
 
@@ -342,7 +350,7 @@ def camera_run(SM, cam, scene, **kw):
 def test_camera_tier1_and_tier2(SM, oracle_mod, name):
     O = oracle_mod
     cam = S.camera_config(name)
-    scene = S.corridor_scene(21, 20000, x_range=(0.0, 60.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    scene = S.corridor_scene(21, 40000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6))
     c = camera_run(SM, cam, scene, write_all_records=True)
     rec = c.record.cpu().numpy()
     proj = O.project_camera(scene, cam)
@@ -377,4 +385,4 @@ def test_camera_tier1_and_tier2(SM, oracle_mod, name):
     assert np.abs(rgb - ref2["feat"])[ok2].max() < TOL_FEAT
     dm = ok2 & (ref2["opacity"] >= 0.5)
     assert np.abs(c.out["depth"].cpu().numpy() - ref2["depth"])[dm].max() < TOL_DEPTH
-    assert (c.out["opacity"].cpu().numpy() > 0.5).mean() > 0.05
+    assert (c.out["opacity"].cpu().numpy() > 0.1).mean() > 0.05
