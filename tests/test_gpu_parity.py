@@ -229,8 +229,8 @@ def test_bin_sort_synthetic_keys_large_tiles(SM):
     ids = torch.empty(cap, dtype=torch.int32, device=dev)
     ranges = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
     npairs = torch.zeros(1, dtype=torch.int64, device=dev)
-    order = torch.empty(n_tiles, dtype=torch.int32, device=dev)
-    SM.simuli_bin_sort(proj, n, n_tiles, ncols, ws, cap, keys, ids, ranges, npairs, tile_order=order)
+    torder = torch.empty(n_tiles, dtype=torch.int32, device=dev)
+    SM.simuli_bin_sort(proj, n, n_tiles, ncols, ws, cap, keys, ids, ranges, npairs, tile_order=torder)
     torch.cuda.synchronize()
     assert npairs.item() == P
     # reference: enumerate pairs in particle order, stable sort by key
@@ -245,7 +245,7 @@ def test_bin_sort_synthetic_keys_large_tiles(SM):
     st = np.searchsorted(k64[order] >> np.uint64(32), np.arange(n_tiles), "left")
     en = np.searchsorted(k64[order] >> np.uint64(32), np.arange(n_tiles), "right")
     assert np.array_equal(rr[:, 0][en > st], st[en > st]) and np.array_equal(rr[:, 1], np.where(en > st, en, 0))
-    od = order.cpu().numpy()
+    od = torder.cpu().numpy()
     assert np.array_equal(np.sort(od), np.arange(n_tiles))  # a permutation, longest lists first
     lens = rr[od, 1] - rr[od, 0]
     assert np.all(np.diff(np.floor(np.log2(lens + 0.5))) <= 0)
