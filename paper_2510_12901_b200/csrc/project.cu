@@ -88,6 +88,8 @@ struct ProjArgs {
   // LiDAR
   float az_start, r_min;
   int dir;
+  float R0[9], t0w[3], dtw[3], v[3], axis[3], theta;  // start pose, motion, rotation axis / angle
+  int small_rot;
   int n_phi, n_theta, rows_per_tile, az_cells, sat_cols, enable_cull;
   float pi_f, two_pi_f, az_tile_scale, az_cell_scale;
   const float *bounds, *row_scale;
@@ -125,30 +127,102 @@ __device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c
          __ldg(A.sat + (r1 + 1) * sc + c0) + __ldg(A.sat + r0 * sc + c0);
 }
 
-// Eq. 3 with the firing-time fixed point; returns (phi, omega, r), s = final firing time
-__device__ __forceinline__ void lidar_point(const ProjArgs& A, const float x[3], float* phi, float* om, float* r,
-                                            float* s_out) {
+// ---- LiDAR sensor model (Eq. 3) with the firing-time fixed point (A3, A5).
+// A point's sensor-frame position at firing time s is
+//   p(s) = R(s)^T (x - t(s)) = E(s)^T (q - s v),   q = R0^T (x - t0), v = R0^T (t1 - t0),
+// with R(s) = R0 E(s), E(s) = Exp(s theta k) (k the unit axis of R0^T R1), so per sigma point
+// only E(s)^T y = y - sin(a) (k x y) + (1 - cos a)(k (k.y) - y), a = s theta, is evaluated
+// (the start pose R0, t0 and v are launch constants).
+__device__ __forceinline__ void rot_apply_t(const ProjArgs& A, float s, const float y[3], float p[3]) {
+  const float a = s * A.theta;
+  float sn, omc;
+  if (A.small_rot) {  // |a| <= 0.5: Taylor to a^9 / a^10 (error < 1e-10)
+    const float a2 = a * a;
+    sn = a * (1.f - a2 * (1.f / 6.f) * (1.f - a2 * (1.f / 20.f) * (1.f - a2 * (1.f / 42.f))));
+    omc = 0.5f * a2 * (1.f - a2 * (1.f / 12.f) * (1.f - a2 * (1.f / 30.f) * (1.f - a2 * (1.f / 56.f))));
+  } else {
+    float sh, ch;
+    sincosf(0.5f * a, &sh, &ch);
+    sn = 2.f * sh * ch;
+    omc = 2.f * sh * sh;
+  }
+  const float* k = A.axis;
+  const float cx = k[1] * y[2] - k[2] * y[1], cy = k[2] * y[0] - k[0] * y[2], cz = k[0] * y[1] - k[1] * y[0];
+  const float kd = k[0] * y[0] + k[1] * y[1] + k[2] * y[2];
+  p[0] = y[0] - sn * cx + omc * (k[0] * kd - y[0]);
+  p[1] = y[1] - sn * cy + omc * (k[1] * kd - y[1]);
+  p[2] = y[2] - sn * cz + omc * (k[2] * kd - y[2]);
+}
+
+// sensor-frame position of the sigma point with start-pose coordinates q at its own firing
+// time (K fixed-point updates of s from s = 0); *s_out = the firing time used
+__device__ __forceinline__ void lidar_fire(const ProjArgs& A, const float q[3], float p[3], float* s_out) {
+  p[0] = q[0];
+  p[1] = q[1];
+  p[2] = q[2];
   float s = 0.f;
-  const int K = A.pose.same ? 0 : A.K;
-  const float inv2pi = 0.15915494309189535f;
-  for (int it = 0; it <= K; ++it) {
-    float R[9], t[3];
-    pose_at(A.pose, s, R, t);
-    const float d0 = x[0] - t[0], d1 = x[1] - t[1], d2 = x[2] - t[2];
-    const float px = R[0] * d0 + R[3] * d1 + R[6] * d2;
-    const float py = R[1] * d0 + R[4] * d1 + R[7] * d2;
-    const float pz = R[2] * d0 + R[5] * d1 + R[8] * d2;
-    *r = sqrtf(px * px + py * py + pz * pz);
-    *phi = atan2f(py, px);
-    const float z = *r > 0.f ? fminf(1.f, fmaxf(-1.f, pz / *r)) : 0.f;
-    *om = asinf(z);
-    if (it < K) {
-      float a = (float)A.dir * (*phi - A.az_start);
+  if (!A.pose.same) {
+    const float inv2pi = 0.15915494309189535f;
+    for (int it = 0; it < A.K; ++it) {
+      const float phi = atan2f(p[1], p[0]);
+      float a = (float)A.dir * (phi - A.az_start);
       a = a - 6.283185307179586f * floorf(a * inv2pi);
       s = fminf(fmaxf(a * inv2pi, 0.f), 1.f);
+      const float y[3] = {q[0] - s * A.v[0], q[1] - s * A.v[1], q[2] - s * A.v[2]};
+      rot_apply_t(A, s, y, p);
     }
   }
   *s_out = s;
+}
+
+// UT moments of the 7 projected sigma points in (azimuth, elevation) (Eq. 3), online.
+// Azimuths are taken relative to sigma point 0 as atan2(p0 x p_i, p0 . p_i) (the unwrap of
+// A21, cancellation-free); *a0 = azimuth of sigma point 0; ma, mb = UT mean offsets
+// (mb absolute); caa, cab, cbb = UT covariance; s0 = firing time of sigma point 0.
+__device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[3], const float L[3][3], float* a0,
+                                              float* ma, float* mb, float* caa, float* cab, float* cbb, float* s0,
+                                              bool* valid) {
+  const float* R0 = A.R0;
+  const float d0 = mu[0] - A.t0w[0], d1 = mu[1] - A.t0w[1], d2 = mu[2] - A.t0w[2];
+  const float c[3] = {R0[0] * d0 + R0[3] * d1 + R0[6] * d2, R0[1] * d0 + R0[4] * d1 + R0[7] * d2,
+                      R0[2] * d0 + R0[5] * d1 + R0[8] * d2};
+  float p0[3];
+  lidar_fire(A, c, p0, s0);
+  const float r0 = sqrtf(p0[0] * p0[0] + p0[1] * p0[1] + p0[2] * p0[2]);
+  bool ok = r0 >= A.r_min;
+  *a0 = atan2f(p0[1], p0[0]);
+  const float om0 = asinf(fminf(1.f, fmaxf(-1.f, p0[2] / r0)));
+  float Sd = 0.f, Se = 0.f, Sdd = 0.f, See = 0.f, Sde = 0.f;
+#pragma unroll 1
+  for (int k = 0; k < 3; ++k) {
+    const float lr[3] = {R0[0] * L[k][0] + R0[3] * L[k][1] + R0[6] * L[k][2],
+                         R0[1] * L[k][0] + R0[4] * L[k][1] + R0[7] * L[k][2],
+                         R0[2] * L[k][0] + R0[5] * L[k][1] + R0[8] * L[k][2]};
+#pragma unroll
+    for (int sg = 0; sg < 2; ++sg) {
+      const float q[3] = {sg ? c[0] - lr[0] : c[0] + lr[0], sg ? c[1] - lr[1] : c[1] + lr[1],
+                          sg ? c[2] - lr[2] : c[2] + lr[2]};
+      float p[3], s;
+      lidar_fire(A, q, p, &s);
+      const float r = sqrtf(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
+      ok = ok && r >= A.r_min;
+      const float d = atan2f(p0[0] * p[1] - p0[1] * p[0], p0[0] * p[0] + p0[1] * p[1]);
+      const float e = asinf(fminf(1.f, fmaxf(-1.f, p[2] / r))) - om0;
+      Sd += d;
+      Se += e;
+      Sdd = fmaf(d, d, Sdd);
+      See = fmaf(e, e, See);
+      Sde = fmaf(d, e, Sde);
+    }
+  }
+  // sigma point 0 has offset 0; w_m = (wm0, wmi x 6), w_c = (wc0, wci x 6)
+  const float m_a = A.ut.wmi * Sd, m_e = A.ut.wmi * Se;
+  *ma = m_a;
+  *mb = om0 + m_e;
+  *caa = A.ut.wc0 * m_a * m_a + A.ut.wci * (Sdd - 2.f * m_a * Sd + 6.f * m_a * m_a);
+  *cbb = A.ut.wc0 * m_e * m_e + A.ut.wci * (See - 2.f * m_e * Se + 6.f * m_e * m_e);
+  *cab = A.ut.wc0 * m_a * m_e + A.ut.wci * (Sde - m_a * Se - m_e * Sd + 6.f * m_a * m_e);
+  *valid = ok;
 }
 
 // lens projection of a camera-frame point; returns 1 valid, 0 invalid, -1 not computable
@@ -235,9 +309,13 @@ __global__ void __launch_bounds__(256) k_project(const ProjArgs A) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) L[k][c] = A.ut.spread * sc[k] * R[3 * c + k];
 
-    // ---- 7 sigma points through the sensor model
-    float ya[7], yb[7], s0 = 0.f;
+    float ma, mb, caa, cab, cbb, a0, s0 = 0.f;
     bool valid = true, computable = true;
+    if (KIND == SIMULI_SENSOR_LIDAR) {
+      lidar_moments(A, mu, L, &a0, &ma, &mb, &caa, &cab, &cbb, &s0, &valid);
+    } else {
+    // ---- 7 sigma points through the sensor model
+    float ya[7], yb[7];
 #pragma unroll 1
     for (int i = 0; i < 7; ++i) {
       float x[3] = {mu[0], mu[1], mu[2]};
@@ -249,43 +327,29 @@ __global__ void __launch_bounds__(256) k_project(const ProjArgs A) {
         x[2] += sg * L[k][2];
       }
       float s;
-      if (KIND == SIMULI_SENSOR_LIDAR) {
-        float r;
-        lidar_point(A, x, &ya[i], &yb[i], &r, &s);
-        valid = valid && (r >= A.r_min);
-      } else {
-        const int st = camera_point(A, x, &ya[i], &yb[i], &s);
-        computable = computable && st >= 0;
-        valid = valid && st == 1;
-      }
+      const int st = camera_point(A, x, &ya[i], &yb[i], &s);
+      computable = computable && st >= 0;
+      valid = valid && st == 1;
       if (i == 0) s0 = s;
     }
-    // ---- UT moments (azimuth unwrapped about sigma point 0, A21)
-    float da[7];
-    const float a0 = ya[0];
-#pragma unroll
-    for (int i = 0; i < 7; ++i) {
-      float d = ya[i] - a0;
-      if (KIND == SIMULI_SENSOR_LIDAR) {
-        if (d > 3.14159265f) d -= 6.28318531f;
-        else if (d <= -3.14159265f) d += 6.28318531f;
-      }
-      da[i] = d;
-    }
-    float ma = A.ut.wm0 * da[0], mb = A.ut.wm0 * yb[0];
+    // ---- UT moments
+    a0 = 0.f;
+    ma = A.ut.wm0 * ya[0];
+    mb = A.ut.wm0 * yb[0];
 #pragma unroll
     for (int i = 1; i < 7; ++i) {
-      ma += A.ut.wmi * da[i];
+      ma += A.ut.wmi * ya[i];
       mb += A.ut.wmi * yb[i];
     }
-    float caa = 0.f, cab = 0.f, cbb = 0.f;
+    caa = 0.f; cab = 0.f; cbb = 0.f;
 #pragma unroll
     for (int i = 0; i < 7; ++i) {
       const float w = i == 0 ? A.ut.wc0 : A.ut.wci;
-      const float ea = da[i] - ma, eb = yb[i] - mb;
+      const float ea = ya[i] - ma, eb = yb[i] - mb;
       caa += w * ea * ea;
       cab += w * ea * eb;
       cbb += w * eb * eb;
+    }
     }
     float ya_bar = a0 + ma;
     const float det = caa * cbb - cab * cab;
@@ -347,7 +411,13 @@ __global__ void __launch_bounds__(256) k_project(const ProjArgs A) {
         for (int c = 0; c < 3; ++c) M[3 * k + c] = R[3 * c + k] * is;
       }
       float Rs[9], ts[3];
-      pose_at(A.pose, s0, Rs, ts);
+      if (KIND == SIMULI_SENSOR_LIDAR) {
+        ts[0] = A.t0w[0] + s0 * A.dtw[0];
+        ts[1] = A.t0w[1] + s0 * A.dtw[1];
+        ts[2] = A.t0w[2] + s0 * A.dtw[2];
+      } else {
+        pose_at(A.pose, s0, Rs, ts);
+      }
       float vx = mu[0] - ts[0], vy = mu[1] - ts[1], vz = mu[2] - ts[2];
       const float vn = rsqrtf(vx * vx + vy * vy + vz * vz);
       vx *= vn; vy *= vn; vz *= vn;
@@ -435,6 +505,28 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.az_start = P->lidar->azimuth_start_rad;
     A.dir = P->lidar->spin_direction;
     A.r_min = P->lidar->min_range_m;
+    {
+      // launch constants of the sensor model: R0 = R(q0), t0, dt = t1 - t0, v = R0^T dt,
+      // rotation axis k (in the start frame) and angle theta of R0^T R1 (host, double)
+      const PoseInterpD pd = make_pose_interp_d(P->pose_start, P->pose_end);
+      double R0d[9];
+      {
+        const double w = pd.q0[0], x = pd.q0[1], y = pd.q0[2], z = pd.q0[3];
+        const double Rr[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                              2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                              2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+        for (int i = 0; i < 9; ++i) R0d[i] = Rr[i];
+      }
+      for (int i = 0; i < 9; ++i) A.R0[i] = static_cast<float>(R0d[i]);
+      for (int i = 0; i < 3; ++i) {
+        A.t0w[i] = P->pose_start.t[i];
+        A.dtw[i] = static_cast<float>(pd.dt[i]);
+        A.axis[i] = static_cast<float>(pd.axis[i]);
+        A.v[i] = static_cast<float>(R0d[0 * 3 + i] * pd.dt[0] + R0d[1 * 3 + i] * pd.dt[1] + R0d[2 * 3 + i] * pd.dt[2]);
+      }
+      A.theta = static_cast<float>(2.0 * pd.half_theta);
+      A.small_rot = std::fabs(2.0 * pd.half_theta) <= 0.5 ? 1 : 0;
+    }
     A.n_phi = T.n_phi; A.n_theta = T.n_theta; A.rows_per_tile = T.cull_rows_per_tile;
     A.az_cells = T.cull_az_cells; A.sat_cols = T.sat_cols; A.enable_cull = P->enable_culling;
     A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f; A.az_tile_scale = T.az_tile_scale; A.az_cell_scale = T.az_cell_scale;
