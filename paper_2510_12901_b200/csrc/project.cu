@@ -273,9 +273,30 @@ __device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3],
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(256) k_project(const ProjArgs A) {
+__global__ void __launch_bounds__(256, 3) k_project(const ProjArgs A) {
+  // degree-3 SH of the warp's 32 particles (32 x 192 B contiguous) staged into shared memory
+  // by coalesced 16-byte cp.async at kernel start, overlapping the projection arithmetic;
+  // layout [chunk][particle] so each lane's later reads are conflict-free
+  __shared__ float4 s_sh[8][12][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= A.n) return;
+  const bool stage_sh = A.sh_degree == 3;
+  if (stage_sh) {
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + wid * 32;
+    const float4* src = reinterpret_cast<const float4*>(A.sh) + g0 * 12;
+    for (int j = lane; j < 32 * 12; j += 32) {
+      const int p = j / 12, c = j - p * 12;
+      if (g0 + p < A.n) {
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&s_sh[wid][c][p]));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + j) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  if (g >= A.n) {
+    if (stage_sh) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    return;
+  }
   // ---- loads (SoA; quaternion as one 16-byte load)
   float mu[3] = {__ldg(A.means + 3 * g), __ldg(A.means + 3 * g + 1), __ldg(A.means + 3 * g + 2)};
   const float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + g);
@@ -421,7 +442,20 @@ __global__ void __launch_bounds__(256) k_project(const ProjArgs A) {
       float vx = mu[0] - ts[0], vy = mu[1] - ts[1], vz = mu[2] - ts[2];
       const float vn = rsqrtf(vx * vx + vy * vy + vz * vz);
       vx *= vn; vy *= vn; vz *= vn;
-      if (isfinite(vn)) sh_eval(A.sh + g * A.n_coef * 3, A.sh_degree, vx, vy, vz, f);
+      if (isfinite(vn)) {
+        if (stage_sh) {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+          float shl[48];
+#pragma unroll
+          for (int c = 0; c < 12; ++c) {
+            const float4 v4 = s_sh[wid][c][lane];
+            shl[4 * c] = v4.x; shl[4 * c + 1] = v4.y; shl[4 * c + 2] = v4.z; shl[4 * c + 3] = v4.w;
+          }
+          sh_eval_regs(shl, vx, vy, vz, f);
+        } else {
+          sh_eval(A.sh + g * A.n_coef * 3, A.sh_degree, vx, vy, vz, f);
+        }
+      }
     }
   }
   A.count[g] = count;

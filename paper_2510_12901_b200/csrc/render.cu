@@ -562,9 +562,10 @@ __global__ void __launch_bounds__(32 * kV2Warps) k_render_lidar_v2(const LidarV2
 // (consumer arrives, producers sync).  The consumer's stop decision for round r is
 // published with EMPTY(b) and read by the producers before round r+2, so both sides
 // agree on the number of rounds and every barrier phase is matched.
+constexpr int kV3Stages = 3;
 template <int NP>
 struct V3Smem {
-  float4 rec[2][32 * NP][5];
+  float4 rec[kV3Stages][32 * NP][5];
   float2 at[2][32 * NP][32];
   float4 feat[2][32 * NP];
   uint32_t memb[2][NP][32];
@@ -718,32 +719,41 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v3(const LidarV2
   }
 
   // ================= producers: thread = list entry of the round
-  auto issue = [&](int buf, int start) {
-    const int e = start + tid;
-    if (e < rg.y) {
-      const float4* src = A.record + (size_t)__ldg(A.ids + e) * 5;
+  // Records of round r+2 are in flight (cp.async, NS = 3 stages) while round r is
+  // processed; the list ids they need were loaded one round earlier still.
+  auto issue = [&](int stage, int start, uint32_t id) {
+    if (start + tid < rg.y) {
+      const float4* src = A.record + (size_t)id * 5;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[buf][tid][c], src + c);
+      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[stage][tid][c], src + c);
     }
     cp_async_commit();
   };
-  if (n_rounds > 0) issue(0, rg.x);
+  auto load_id = [&](int round) -> uint32_t {
+    const int e = rg.x + round * E + tid;
+    return (round < n_rounds && e < rg.y) ? __ldg(A.ids + e) : 0u;
+  };
+  issue(0, rg.x, load_id(0));
+  issue(1, rg.x + E, load_id(1));
+  uint32_t id_pf = load_id(2);
   named_sync(BAR_PROD + 5, NT);  // rays ready
   for (int r = 0; r < n_rounds; ++r) {
     const int b = r & 1;
+    const int rs = r % kV3Stages;
     if (r >= 2) {
       named_sync(BAR_EMPTY + b, NT);
       if (S.stop_at[b]) break;
     }
     const int start = rg.x + r * E;
-    cp_async_wait0();
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // round r landed (r+1 may be in flight)
     named_sync(BAR_PROD, E);
-    if (r + 1 < n_rounds) issue(b ^ 1, start + E);
+    issue((r + 2) % kV3Stages, start + 2 * E, id_pf);
+    id_pf = load_id(r + 3);
     const bool valid = start + tid < rg.y;
     uint32_t m = 0;
     if (valid) {
-      const float4 bx = S.rec[b][tid][4];
-      S.feat[b][tid] = S.rec[b][tid][3];
+      const float4 bx = S.rec[rs][tid][4];
+      S.feat[b][tid] = S.rec[rs][tid][3];
       uint32_t colbits = 0;
       if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
         colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
@@ -789,7 +799,7 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v3(const LidarV2
       const uint32_t mo = S.wmask[warp][lo];
       const int rr = __fns(mo, 0, idx - S.wex[warp][lo] + 1);
       const int e = warp * 32 + lo;
-      const float4 r0 = S.rec[b][e][0], r1 = S.rec[b][e][1], r2 = S.rec[b][e][2], r3 = S.rec[b][e][3];
+      const float4 r0 = S.rec[rs][e][0], r1 = S.rec[rs][e][1], r2 = S.rec[rs][e][2], r3 = S.rec[rs][e][3];
       const float mu[3] = {r0.x, r0.y, r0.z};
       const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
       RayF rf;
