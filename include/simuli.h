@@ -220,13 +220,15 @@ int32_t simuli_project(const simuli_gaussians* gaussians, const simuli_project_p
 /* Scratch bytes simuli_bin_sort needs for n particles, pair_capacity pairs, n_tiles. */
 int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t n_tiles, size_t* bytes);
 
-/* Tile-Gaussian duplication and sort "as in 3DGS": exclusive scan of tile_count,
- * one pair (key = tile << 32 | bits(depth_key), id = g) per (tile, particle), a stable
- * LSD radix sort of the keys (onesweep, 8-bit digits over the 32 + ceil(log2 n_tiles)
- * significant bits), and tile_ranges[t] = [begin, end) of tile t in the sorted arrays
- * (0,0 if empty).  The order is (tile, depth key bits, id) -- unique, deterministic.
+/* Tile-Gaussian duplication and sort "as in 3DGS": one pair per (tile, particle)
+ * overlap, ordered by (tile, bits(depth_key), particle id) -- unique and deterministic --
+ * and tile_ranges[t] = [begin, end) of tile t in the sorted arrays (0,0 if empty).
+ * Implementation: stable LSD onesweep radix sorts (8-bit digits) -- the visible particles
+ * by depth key, then the pairs (emitted in that depth order) by tile.
  * n_cols_total: N_theta (LiDAR) or ceil(W / tile_px) (camera).
- * sorted_keys / sorted_ids: device [pair_capacity]; tile_ranges: device [n_tiles][2];
+ * sorted_ids: device [pair_capacity] (u32 particle ids); sorted_keys: device
+ *   [pair_capacity] u64 (tile << 32 | depth bits) or NULL to skip; tile_ranges: device
+ *   [n_tiles][2];
  * tile_order: device [n_tiles] or NULL -- the tiles ordered by decreasing list length
  *   (power-of-two buckets; a longest-first schedule for the render kernels, which is a
  *   performance hint only: results do not depend on it);

@@ -281,16 +281,19 @@ class _Frame:
     def project(self, stream=None):
         simuli_project(self.gauss, self.params, self.projected, stream)
 
+    keep_keys = True  # also write the u64 (tile | depth) keys (tests); the renderer needs only ids
+
     def bin_sort(self, stream=None, sync_capacity=False):
         """Duplicate + sort.  sync_capacity=True: one host sync to grow buffers if needed."""
         cap = -self.capacity if sync_capacity else self.capacity
+        keys = self.sorted_keys if self.keep_keys else None
         need = simuli_bin_sort(self.projected, self.n, self.n_tiles, self.n_cols_total, self.workspace, cap,
-                               self.sorted_keys, self.sorted_ids, self.tile_ranges, self.n_pairs, stream,
+                               keys, self.sorted_ids, self.tile_ranges, self.n_pairs, stream,
                                self.tile_order)
         if need is not None:
             self.set_capacity(int(need * 1.25) + 1024)
             need = simuli_bin_sort(self.projected, self.n, self.n_tiles, self.n_cols_total, self.workspace,
-                                   -self.capacity, self.sorted_keys, self.sorted_ids, self.tile_ranges,
+                                   -self.capacity, keys, self.sorted_ids, self.tile_ranges,
                                    self.n_pairs, stream, self.tile_order)
             assert need is None
 
