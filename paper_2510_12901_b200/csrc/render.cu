@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "abi_util.h"
 #include "common.cuh"
@@ -1178,24 +1179,26 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
         attr2 = true;
       }
       k_render_lidar_v2<<<(unsigned)A.n_items, 32 * kV2Warps, sizeof(V2Smem), st>>>(A);
-    } else if (getenv("SIMULI_LIDAR_KERNEL") && std::string(getenv("SIMULI_LIDAR_KERNEL")) == "v3") {
-      constexpr int NP = 4;
-      static bool attr3 = false;
-      if (!attr3) {
+    } else {
+      const char* kv = getenv("SIMULI_LIDAR_KERNEL");
+      const std::string kind = kv ? kv : "v5_4";
+      auto launch_v3 = [&](auto np_tag) {
+        constexpr int NP = decltype(np_tag)::value;
         cudaFuncSetAttribute(k_render_lidar_v3<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(V3Smem<NP>));
-        attr3 = true;
-      }
-      k_render_lidar_v3<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V3Smem<NP>), st>>>(A);
-    } else {
-      constexpr int NP = 8;
-      static bool attr5 = false;
-      if (!attr5) {
+        k_render_lidar_v3<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V3Smem<NP>), st>>>(A);
+      };
+      auto launch_v5 = [&](auto np_tag) {
+        constexpr int NP = decltype(np_tag)::value;
         cudaFuncSetAttribute(k_render_lidar_v5<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(V5Smem<NP>));
-        attr5 = true;
-      }
-      k_render_lidar_v5<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V5Smem<NP>), st>>>(A);
+        k_render_lidar_v5<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V5Smem<NP>), st>>>(A);
+      };
+      if (kind == "v3") launch_v3(std::integral_constant<int, 4>{});
+      else if (kind == "v3_2") launch_v3(std::integral_constant<int, 2>{});
+      else if (kind == "v5_8") launch_v5(std::integral_constant<int, 8>{});
+      else if (kind == "v5_2") launch_v5(std::integral_constant<int, 2>{});
+      else launch_v5(std::integral_constant<int, 4>{});
     }
     return launch_check("simuli_render_lidar");
   }
