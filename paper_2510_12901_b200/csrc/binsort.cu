@@ -1,30 +1,31 @@
-// simuli_bin_sort: tile-Gaussian duplication + radix sort + tile ranges (sm_100a).
+// simuli_bin_sort: tile-Gaussian duplication + onesweep radix sort + tile ranges (sm_100a).
 //
 // "we ... estimate a 2D conic before applying tiling and culling as in 3DGS": one
 // (tile, particle) pair per render tile a particle's box overlaps, ordered so that every
 // tile's list runs front to back by the float32 depth key, ties by particle id (A19) --
 // the "Sort" kernel of tab:culling.
 //
-// B200 design: instead of sorting P 64-bit (tile | depth) keys over 6 digit passes, the
-// order is built in two stable LSD stages that move 8 bytes per element:
-//   1. depth sort of the V visible particles (32-bit depth bits + 32-bit id, 4 passes);
-//   2. duplication in that depth order into (tile, id) pairs, then a stable sort of the
-//      P pairs by tile (ceil(log2 n_tiles / 8) passes: 2 for up to 65536 tiles).
-// Stability makes the result identical to sorting (tile << 32 | depth bits, id).
-// Every pass is a hand-written onesweep: per partition a warp-level ballot multisplit
-// ranks the keys, a decoupled look-back over partitions (dynamic partition ids for
-// forward progress) gives the global digit offsets, keys are staged in shared memory in
-// digit order and written out coalesced.  Digit histograms of all passes are accumulated
-// by the kernels that produce the keys (no separate histogram sweep).
-//
-// Launches (caller's stream; no host sync when pair_capacity >= 0):
-//   k_count_reduce, k_count_top        scan of tile counts and of visibility (id order)
-//   k_compact                          visible (depth bits, id) in id order + depth histograms
-//   k_onesweep<u32> x 4                depth sort
-//   k_vcount_reduce, k_vcount_top      scan of tile counts in depth order
-//   k_duplicate                        balanced, coalesced pair emission + tile histograms
-//   k_onesweep<u32> x ceil(tile bits / 8)   stable tile sort
-//   k_ranges, [k_keys64], [k_tile_order]
+// Launch sequence (caller's stream; no host sync when pair_capacity >= 0):
+//   k_count_reduce  per-1024-particle tile-count sums + min / max depth-key bits of the
+//                   particles that emit pairs
+//   k_count_top     exclusive scan of the block sums (1 CTA) -> P; key width
+//                   b = bits(max - min) and the pass count ceil((b + tile bits) / 8)
+//   k_duplicate     balanced, coalesced pair emission (each thread emits pairs k = tid,
+//                   tid+256, ... binary-searching its owner in shared memory) of the
+//                   trimmed key (tile << b) | (depth bits - min) -- an order-preserving
+//                   map of (tile, depth bits) -- plus the digit histograms of every pass
+//                   and the per-tile pair counts
+//   k_onesweep x 6  stable LSD onesweep, 8-bit digits; passes beyond the device-side pass
+//                   count exit at once (buffer parity is chosen on the device so the
+//                   last real pass lands in the caller's arrays).  Per 3072-key partition
+//                   a warp-level ballot multisplit ranks the keys, a decoupled look-back
+//                   over partitions (dynamic partition ids for forward progress) yields
+//                   the global digit offsets, keys are staged in shared memory in digit
+//                   order and written out coalesced.
+//   k_tile_meta     tile ranges = exclusive scan of the per-tile pair counts (the sort is
+//                   stable, so tile t occupies [start_t, start_t + count_t)); longest-first
+//                   tile order
+//   [k_keys64]      the u64 (tile << 32 | depth bits) keys, only if the caller wants them
 #include <cstdint>
 
 #include "abi_util.h"
@@ -33,46 +34,46 @@
 namespace simuli {
 namespace {
 
-constexpr int kBlkThreads = 256;
-constexpr int kBlkItems = 4;
-constexpr int kBlk = kBlkThreads * kBlkItems;  // elements per scan / duplication block
+constexpr int kDupThreads = 256;
+constexpr int kDupItems = 4;
+constexpr int kDupBlock = kDupThreads * kDupItems;
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kPart = kSortThreads * kSortItems;  // keys per onesweep partition
-constexpr int kDepthPasses = 4;
-constexpr int kMaxPasses = 8;  // 4 depth + up to 4 tile passes
+constexpr int kSortItems = 12;
+constexpr int kPart = kSortThreads * kSortItems;
+constexpr int kMaxPasses = 6;  // 48 key bits: 16 tile bits + 32 depth bits at most
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
+
+// device scalars: [0] P, [1] key-min bits, [2] key-max bits, [3] depth bits b,
+// [4] passes, [5] tile bits
+enum { S_P = 0, S_KMIN, S_KMAX, S_B, S_PASSES, S_TBITS, S_N };
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-int tile_passes(int32_t n_tiles) {
+int tile_bits_of(int32_t n_tiles) {
   int bits = 0;
   while (bits < 31 && (1ll << bits) < (int64_t)n_tiles) ++bits;
-  return (bits + 7) / 8;
+  return bits;
 }
 
 struct Workspace {
-  int64_t* blk_pairs;  // [nb+1] tile-count block sums -> offsets (id order)
-  int32_t* blk_vis;    // [nb+1] visible-count block sums -> offsets
-  int64_t* vblk;       // [nb+1] tile-count block sums in depth order
-  int64_t* scal;       // [0] = P, [1] = V
-  uint32_t* hist;      // [kMaxPasses][256]
-  uint32_t* counters;  // [kMaxPasses]
-  uint32_t* status;    // [kMaxPasses][max parts][256]
-  uint32_t* vk[2];     // [n] depth bits
-  uint32_t* vi[2];     // [n] particle ids
-  uint32_t* tk[2];     // [cap] tile keys
-  uint32_t* ti_alt;    // [cap] ids (ping-pong partner of sorted_ids)
-  int64_t max_parts;
+  int64_t* block_sums;  // [nb+1]
+  uint32_t* block_kmin; // [nb]
+  uint32_t* block_kmax; // [nb]
+  int64_t* scal;        // [S_N]
+  uint32_t* hist;       // [kMaxPasses][256]
+  uint32_t* status;     // [kMaxPasses][n_parts][256]
+  uint32_t* counters;   // [kMaxPasses]
+  int32_t* tile_cnt;    // [n_tiles]
+  uint64_t* keys[2];    // [cap]
+  uint32_t* vals_alt;   // [cap]
+  int64_t parts;
   size_t bytes;
 };
 
-Workspace carve(void* base, int64_t n, int64_t cap) {
+Workspace carve(void* base, int64_t n, int64_t cap, int32_t n_tiles) {
   Workspace w{};
-  const int64_t nb = (n + kBlk - 1) / kBlk;
-  const int64_t parts_v = (n + kPart - 1) / kPart, parts_p = (cap + kPart - 1) / kPart;
-  w.max_parts = parts_v > parts_p ? parts_v : parts_p;
-  if (w.max_parts < 1) w.max_parts = 1;
+  const int64_t nb = (n + kDupBlock - 1) / kDupBlock;
+  w.parts = (cap + kPart - 1) / kPart;
   char* p = static_cast<char*>(base);
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -80,17 +81,16 @@ Workspace carve(void* base, int64_t n, int64_t cap) {
     off += align_up(bytes > 0 ? bytes : 1);
     return r;
   };
-  w.blk_pairs = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * (nb + 1)));
-  w.blk_vis = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (nb + 1)));
-  w.vblk = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * (nb + 1)));
-  w.scal = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * 4));
+  w.block_sums = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * (nb + 1)));
+  w.block_kmin = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (nb + 1)));
+  w.block_kmax = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (nb + 1)));
+  w.scal = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * S_N));
   w.hist = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses * 256));
   w.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses));
-  w.status = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses * w.max_parts * 256));
-  for (int i = 0; i < 2; ++i) w.vk[i] = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * n));
-  for (int i = 0; i < 2; ++i) w.vi[i] = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * n));
-  for (int i = 0; i < 2; ++i) w.tk[i] = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * cap));
-  w.ti_alt = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * cap));
+  w.status = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses * (w.parts > 0 ? w.parts : 1) * 256));
+  w.tile_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * n_tiles));
+  for (int i = 0; i < 2; ++i) w.keys[i] = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * cap));
+  w.vals_alt = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * cap));
   w.bytes = off;
   return w;
 }
@@ -107,7 +107,6 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 }
 
 // exclusive scan of one value per thread over a 256-thread block; *total = block sum.
-// scratch: >= 8 ints of shared memory.
 __device__ __forceinline__ int block_excl_scan256(int v, int* scratch, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int inc = warp_incl_scan(v);
@@ -125,18 +124,77 @@ __device__ __forceinline__ int block_excl_scan256(int v, int* scratch, int* tota
   return wpre + inc - v;
 }
 
-// single-CTA exclusive scan of nb int64 (or int32) block sums in place; writes the total
-// to sums[nb] and to *total_out.
-template <typename T>
-__device__ void cta_scan_inplace(T* sums, int64_t nb, int64_t* total_out) {
+// ------------------------------------------------------------------ counts, key range
+__global__ void __launch_bounds__(kDupThreads) k_count_reduce(const int* __restrict__ count,
+                                                              const float* __restrict__ key, int64_t n,
+                                                              int64_t* __restrict__ block_sums,
+                                                              uint32_t* __restrict__ block_kmin,
+                                                              uint32_t* __restrict__ block_kmax) {
+  __shared__ int scratch[8];
+  __shared__ uint32_t s_min[8], s_max[8];
+  const int64_t base = (int64_t)blockIdx.x * kDupBlock;
+  int s = 0;
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll
+  for (int i = 0; i < kDupItems; ++i) {
+    const int64_t g = base + i * kDupThreads + threadIdx.x;
+    if (g < n) {
+      const int c = __ldg(count + g);
+      s += c;
+      if (c > 0) {
+        const uint32_t kb = __float_as_uint(__ldg(key + g));
+        kmin = min(kmin, kb);
+        kmax = max(kmax, kb);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_min[threadIdx.x >> 5] = kmin;
+    s_max[threadIdx.x >> 5] = kmax;
+  }
+  int tot;
+  block_excl_scan256(s, scratch, &tot);
+  if (threadIdx.x == 0) {
+    block_sums[blockIdx.x] = tot;
+    for (int w = 0; w < 8; ++w) {
+      kmin = min(kmin, s_min[w]);
+      kmax = max(kmax, s_max[w]);
+    }
+    block_kmin[blockIdx.x] = kmin;
+    block_kmax[blockIdx.x] = kmax;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_count_top(int64_t* __restrict__ block_sums,
+                                                    const uint32_t* __restrict__ block_kmin,
+                                                    const uint32_t* __restrict__ block_kmax, int64_t nb,
+                                                    int tile_bits, int64_t* __restrict__ scal,
+                                                    int64_t* __restrict__ n_pairs, uint32_t* __restrict__ hist,
+                                                    uint32_t* __restrict__ counters, int32_t* __restrict__ tile_cnt,
+                                                    int n_tiles) {
   __shared__ int64_t warp_tot[32];
+  __shared__ uint32_t w_min[32], w_max[32];
   __shared__ int64_t carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry = 0;
+  for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) hist[i] = 0;
+  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) tile_cnt[i] = 0;
+  if (threadIdx.x < kMaxPasses) counters[threadIdx.x] = 0;
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
   __syncthreads();
-  for (int64_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+  for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
     const int64_t i = b0 + threadIdx.x;
-    const int64_t v = i < nb ? (int64_t)sums[i] : 0;
+    int64_t v = 0;
+    if (i < nb) {
+      v = block_sums[i];
+      kmin = min(kmin, block_kmin[i]);
+      kmax = max(kmax, block_kmax[i]);
+    }
     int64_t inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -146,170 +204,100 @@ __device__ void cta_scan_inplace(T* sums, int64_t nb, int64_t* total_out) {
     if (lane == 31) warp_tot[warp] = inc;
     __syncthreads();
     int64_t wpre = 0, tot = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      if (w < warp) wpre += warp_tot[w];
-      tot += warp_tot[w];
+    for (int w = 0; w < 32; ++w) {
+      const int64_t x = warp_tot[w];
+      wpre += (w < warp) ? x : 0;
+      tot += x;
     }
-    if (i < nb) sums[i] = (T)(carry + wpre + inc - v);
+    if (i < nb) block_sums[i] = carry + wpre + inc - v;
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    sums[nb] = (T)carry;
-    *total_out = carry;
-  }
-}
-
-// ------------------------------------------------------------------ stage 0: counts
-__global__ void __launch_bounds__(kBlkThreads) k_count_reduce(const int* __restrict__ count, int64_t n,
-                                                              int64_t* __restrict__ blk_pairs,
-                                                              int32_t* __restrict__ blk_vis) {
-  __shared__ int scratch[8];
-  const int64_t base = (int64_t)blockIdx.x * kBlk;
-  int s = 0, v = 0;
 #pragma unroll
-  for (int i = 0; i < kBlkItems; ++i) {
-    const int64_t g = base + i * kBlkThreads + threadIdx.x;
-    if (g < n) {
-      const int c = __ldg(count + g);
-      s += c;
-      v += c > 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) {
+    w_min[warp] = kmin;
+    w_max[warp] = kmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < 32; ++w) {
+      kmin = min(kmin, w_min[w]);
+      kmax = max(kmax, w_max[w]);
     }
-  }
-  int tot, totv;
-  block_excl_scan256(s, scratch, &tot);
-  block_excl_scan256(v, scratch, &totv);
-  if (threadIdx.x == 0) {
-    blk_pairs[blockIdx.x] = tot;
-    blk_vis[blockIdx.x] = totv;
+    block_sums[nb] = carry;
+    *n_pairs = carry;
+    int b = 0;
+    if (carry > 0 && kmax > kmin) b = 32 - __clz(kmax - kmin);
+    if (carry == 0) kmin = 0;
+    scal[S_P] = carry;
+    scal[S_KMIN] = kmin;
+    scal[S_KMAX] = kmax;
+    scal[S_B] = b;
+    scal[S_PASSES] = carry > 0 ? (b + tile_bits + 7) / 8 : 0;
+    scal[S_TBITS] = tile_bits;
   }
 }
 
-__global__ void __launch_bounds__(1024) k_count_top(int64_t* __restrict__ blk_pairs, int32_t* __restrict__ blk_vis,
-                                                    int64_t nb, int64_t* __restrict__ scal,
-                                                    int64_t* __restrict__ n_pairs, uint32_t* __restrict__ hist,
-                                                    uint32_t* __restrict__ counters) {
-  for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) hist[i] = 0;
-  if (threadIdx.x < kMaxPasses) counters[threadIdx.x] = 0;
-  cta_scan_inplace(blk_pairs, nb, &scal[0]);
-  __syncthreads();
-  cta_scan_inplace(blk_vis, nb, &scal[1]);
-  __syncthreads();
-  if (threadIdx.x == 0) *n_pairs = scal[0];
-}
-
-// visible particles (count > 0) in id order -> (depth bits, id); depth-pass histograms
-__global__ void __launch_bounds__(kBlkThreads) k_compact(const int* __restrict__ count, const float* __restrict__ key,
-                                                         int64_t n, const int32_t* __restrict__ blk_vis,
-                                                         uint32_t* __restrict__ vk, uint32_t* __restrict__ vi,
-                                                         uint32_t* __restrict__ hist) {
-  __shared__ uint32_t s_hist[kDepthPasses * 256];
-  __shared__ int scratch[8];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < kDepthPasses * 256; i += kBlkThreads) s_hist[i] = 0;
-  const int64_t g0 = (int64_t)blockIdx.x * kBlk + tid * kBlkItems;  // blocked: thread owns 4 consecutive
-  int flag[kBlkItems], v = 0;
-#pragma unroll
-  for (int i = 0; i < kBlkItems; ++i) {
-    const int64_t g = g0 + i;
-    flag[i] = (g < n && __ldg(count + g) > 0) ? 1 : 0;
-    v += flag[i];
-  }
-  int tot;
-  int ex = block_excl_scan256(v, scratch, &tot) + blk_vis[blockIdx.x];
-#pragma unroll
-  for (int i = 0; i < kBlkItems; ++i) {
-    if (!flag[i]) continue;
-    const int64_t g = g0 + i;
-    const uint32_t kb = __float_as_uint(__ldg(key + g));
-    vk[ex] = kb;
-    vi[ex] = (uint32_t)g;
-    ++ex;
-#pragma unroll
-    for (int p = 0; p < kDepthPasses; ++p) atomicAdd(&s_hist[p * 256 + ((kb >> (8 * p)) & 0xFF)], 1u);
-  }
-  __syncthreads();
-  for (int i = tid; i < kDepthPasses * 256; i += kBlkThreads)
-    if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
-}
-
-// tile counts of the depth-sorted visible particles, per 1024-block
-__global__ void __launch_bounds__(kBlkThreads) k_vcount_reduce(const int* __restrict__ count,
-                                                               const uint32_t* __restrict__ vi,
-                                                               const int64_t* __restrict__ scal,
-                                                               int64_t* __restrict__ vblk) {
-  __shared__ int scratch[8];
-  const int64_t V = scal[1];
-  const int64_t base = (int64_t)blockIdx.x * kBlk;
-  if (base >= V && blockIdx.x > 0) return;
-  int s = 0;
-#pragma unroll
-  for (int i = 0; i < kBlkItems; ++i) {
-    const int64_t j = base + i * kBlkThreads + threadIdx.x;
-    if (j < V) s += __ldg(count + vi[j]);
-  }
-  int tot;
-  block_excl_scan256(s, scratch, &tot);
-  if (threadIdx.x == 0) vblk[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) k_vcount_top(int64_t* __restrict__ vblk, const int64_t* __restrict__ scal,
-                                                     int64_t* __restrict__ scratch_total) {
-  const int64_t nvb = (scal[1] + kBlk - 1) / kBlk;
-  cta_scan_inplace(vblk, nvb, scratch_total);
-}
-
-// ------------------------------------------------------------------ duplication (depth order)
+// ------------------------------------------------------------------ duplication
 struct DupArgs {
   const int* count;
   const int4* rect;
-  const uint32_t* vi;
+  const float* key;
+  int64_t n, capacity;
+  const int64_t* block_offsets;
   const int64_t* scal;
-  const int64_t* vblk;
-  int64_t capacity;
-  int n_cols_total, passes;
-  uint32_t* tk_out;
-  uint32_t* ti_out;
-  uint32_t* hist;  // [passes][256] of the tile passes
+  int n_cols_total;
+  uint64_t* keys[2];
+  uint32_t* vals[2];
+  uint32_t* hist;      // [kMaxPasses][256]
+  int32_t* tile_cnt;   // [n_tiles]
 };
 
-__global__ void __launch_bounds__(kBlkThreads) k_duplicate(const DupArgs A) {
-  __shared__ int s_excl[kBlk + 1];
-  __shared__ int4 s_rect[kBlk];
-  __shared__ uint32_t s_id[kBlk];
-  __shared__ uint32_t s_hist[4 * 256];
+__global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
+  __shared__ int s_excl[kDupBlock + 1];
+  __shared__ int4 s_rect[kDupBlock];
+  __shared__ uint32_t s_key[kDupBlock];
+  __shared__ uint32_t s_hist[kMaxPasses * 256];
   __shared__ int scratch[8];
   const int tid = threadIdx.x;
-  const int64_t V = A.scal[1];
-  const int64_t j0 = (int64_t)blockIdx.x * kBlk;
-  if (j0 >= V) return;  // block-uniform
-  for (int i = tid; i < A.passes * 256; i += kBlkThreads) s_hist[i] = 0;
-  int c[kBlkItems], run = 0;
+  const int64_t g0 = (int64_t)blockIdx.x * kDupBlock;
+  const int passes = (int)A.scal[S_PASSES];
+  const int b = (int)A.scal[S_B];
+  const uint32_t kmin = (uint32_t)A.scal[S_KMIN];
+  const int s0 = passes & 1;  // output buffer parity so the last pass lands in buffer 0
+  uint64_t* kout = A.keys[s0];
+  uint32_t* vout = A.vals[s0];
+  for (int i = tid; i < passes * 256; i += kDupThreads) s_hist[i] = 0;
+  int c[kDupItems], run = 0;
 #pragma unroll
-  for (int i = 0; i < kBlkItems; ++i) {
-    const int64_t j = j0 + tid * kBlkItems + i;
-    c[i] = 0;
-    if (j < V) {
-      const uint32_t g = A.vi[j];
-      c[i] = __ldg(A.count + g);
-      s_id[tid * kBlkItems + i] = g;
-      s_rect[tid * kBlkItems + i] = __ldg(A.rect + g);
-    }
+  for (int i = 0; i < kDupItems; ++i) {
+    const int64_t g = g0 + tid * kDupItems + i;
+    c[i] = g < A.n ? __ldg(A.count + g) : 0;
     run += c[i];
   }
   int tot;
   int ex = block_excl_scan256(run, scratch, &tot);
 #pragma unroll
-  for (int i = 0; i < kBlkItems; ++i) {
-    s_excl[tid * kBlkItems + i] = ex;
+  for (int i = 0; i < kDupItems; ++i) {
+    const int li = tid * kDupItems + i;
+    const int64_t g = g0 + li;
+    s_excl[li] = ex;
     ex += c[i];
+    if (c[i] > 0) {
+      s_rect[li] = __ldg(A.rect + g);
+      s_key[li] = __float_as_uint(__ldg(A.key + g)) - kmin;
+    }
   }
-  if (tid == 0) s_excl[kBlk] = tot;
+  if (tid == 0) s_excl[kDupBlock] = tot;
   __syncthreads();
-  const int64_t out0 = A.vblk[blockIdx.x];
-  for (int k = tid; k < tot; k += kBlkThreads) {
-    int lo = 0, hi = kBlk;  // last li with s_excl[li] <= k
+  const int64_t out0 = A.block_offsets[blockIdx.x];
+  for (int k = tid; k < tot; k += kDupThreads) {
+    int lo = 0, hi = kDupBlock;  // last li with s_excl[li] <= k
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (s_excl[mid] <= k) lo = mid;
@@ -321,27 +309,27 @@ __global__ void __launch_bounds__(kBlkThreads) k_duplicate(const DupArgs A) {
     int col = r.z + j % r.w;
     if (col >= A.n_cols_total) col -= A.n_cols_total;
     const uint32_t tile = (uint32_t)row * (uint32_t)A.n_cols_total + (uint32_t)col;
+    const uint64_t key = ((uint64_t)tile << b) | (uint64_t)s_key[lo];
     const int64_t pos = out0 + k;
     if (pos < A.capacity) {
-      A.tk_out[pos] = tile;
-      A.ti_out[pos] = s_id[lo];
-      for (int p = 0; p < A.passes; ++p) atomicAdd(&s_hist[p * 256 + ((tile >> (8 * p)) & 0xFF)], 1u);
+      kout[pos] = key;
+      vout[pos] = (uint32_t)(g0 + lo);
+      atomicAdd(A.tile_cnt + tile, 1);
+      for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * 256 + (int)((key >> (8 * p)) & 0xFF)], 1u);
     }
   }
   __syncthreads();
-  for (int i = tid; i < A.passes * 256; i += kBlkThreads)
+  for (int i = tid; i < passes * 256; i += kDupThreads)
     if (s_hist[i]) atomicAdd(&A.hist[i], s_hist[i]);
 }
 
-// ------------------------------------------------------------------ onesweep pass (u32 keys)
+// ------------------------------------------------------------------ onesweep pass
 struct SweepArgs {
-  const uint32_t* keys_in;
-  const uint32_t* vals_in;
-  uint32_t* keys_out;
-  uint32_t* vals_out;
-  const int64_t* count;  // device element count (P or V)
+  uint64_t* keys[2];
+  uint32_t* vals[2];
+  const int64_t* scal;
   int64_t capacity;
-  int shift;
+  int pass;
   const uint32_t* hist;  // [256] of this pass
   uint32_t* status;      // [n_parts][256] of this pass
   uint32_t* counter;
@@ -361,42 +349,52 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const SweepArgs A) {
   __shared__ uint32_t s_warp_hist[8][256];
   __shared__ uint32_t s_digit_excl[256];
   __shared__ uint32_t s_global[256];
-  __shared__ uint32_t s_keys[kPart];
+  __shared__ uint64_t s_keys[kPart];
   __shared__ uint32_t s_vals[kPart];
   __shared__ int scratch[8];
+  const int passes = (int)A.scal[S_PASSES];
+  if (A.pass >= passes) return;  // grid-uniform: this digit is beyond the key width
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_part = atomicAdd(A.counter, 1u);
   for (int i = tid; i < 8 * 256; i += kSortThreads) (&s_warp_hist[0][0])[i] = 0;
   __syncthreads();
-  const int64_t P = min(*A.count, A.capacity);
+  const int64_t P = min(A.scal[S_P], A.capacity);
   const int64_t n_parts = (P + kPart - 1) / kPart;
   const int64_t part = s_part;
   if (part >= n_parts) return;
+  const int in = ((passes & 1) + A.pass) & 1;
+  const uint64_t* keys_in = A.keys[in];
+  const uint32_t* vals_in = A.vals[in];
+  uint64_t* keys_out = A.keys[in ^ 1];
+  uint32_t* vals_out = A.vals[in ^ 1];
+  const int shift = 8 * A.pass;
   const int64_t base = part * kPart;
   const int valid = (int)min((int64_t)kPart, P - base);
 
-  uint32_t k[kSortItems], v[kSortItems], rank[kSortItems];
+  uint64_t k[kSortItems];
+  uint32_t v[kSortItems];
+  uint32_t rank[kSortItems];
   const int64_t wbase = base + warp * (32 * kSortItems);
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = wbase + i * 32 + lane;
     if (idx < P) {
-      k[i] = A.keys_in[idx];
-      v[i] = A.vals_in[idx];
+      k[i] = keys_in[idx];
+      v[i] = vals_in[idx];
     } else {
-      k[i] = 0xffffffffu;  // padding: digit 0xFF, ranked after every real key
+      k[i] = ~0ull;  // padding: digit 0xFF, ranked after every real key of the partition
       v[i] = 0;
     }
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
-    const uint32_t d = (k[i] >> A.shift) & 0xFFu;
+    const uint32_t d = (uint32_t)(k[i] >> shift) & 0xFFu;
     uint32_t peers = 0xffffffffu;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-      peers &= ((d >> b) & 1u) ? bal : ~bal;
+    for (int bb = 0; bb < 8; ++bb) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (d >> bb) & 1u);
+      peers &= ((d >> bb) & 1u) ? bal : ~bal;
     }
     const uint32_t before = __popc(peers & lt_mask);
     const uint32_t prev = s_warp_hist[warp][d];
@@ -439,67 +437,85 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const SweepArgs A) {
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
-    const uint32_t dd = (k[i] >> A.shift) & 0xFFu;
+    const uint32_t dd = (uint32_t)(k[i] >> shift) & 0xFFu;
     const uint32_t pos = s_digit_excl[dd] + s_warp_hist[warp][dd] + rank[i];
     s_keys[pos] = k[i];
     s_vals[pos] = v[i];
   }
   __syncthreads();
   for (int j = tid; j < valid; j += kSortThreads) {
-    const uint32_t key = s_keys[j];
-    const uint32_t dd = (key >> A.shift) & 0xFFu;
+    const uint64_t key = s_keys[j];
+    const uint32_t dd = (uint32_t)(key >> shift) & 0xFFu;
     const int64_t out = (int64_t)s_global[dd] + (j - (int64_t)s_digit_excl[dd]);
-    A.keys_out[out] = key;
-    A.vals_out[out] = s_vals[j];
+    keys_out[out] = key;
+    vals_out[out] = s_vals[j];
   }
 }
 
-// ------------------------------------------------------------------ ranges, keys, order
-__global__ void k_ranges(const uint32_t* __restrict__ tk, const int64_t* __restrict__ n_pairs, int64_t capacity,
-                         int2* __restrict__ ranges) {
-  const int64_t P = min(*n_pairs, capacity);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t t = tk[i];
-    if (i == 0 || tk[i - 1] != t) ranges[t].x = (int)i;
-    if (i == P - 1 || tk[i + 1] != t) ranges[t].y = (int)(i + 1);
-  }
-}
-
-__global__ void k_keys64(const uint32_t* __restrict__ tk, const uint32_t* __restrict__ ids,
-                         const float* __restrict__ key, const int64_t* __restrict__ n_pairs, int64_t capacity,
-                         uint64_t* __restrict__ out) {
-  const int64_t P = min(*n_pairs, capacity);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = ((uint64_t)tk[i] << 32) | (uint64_t)__float_as_uint(__ldg(key + ids[i]));
-}
-
-// Longest-first schedule: tiles bucketed by floor(log2(list length)), decreasing (a
-// counting sort; order inside a bucket is whatever the atomics give -- it only affects
-// scheduling, never results).  One CTA.
-__global__ void __launch_bounds__(1024) k_tile_order(const int2* __restrict__ ranges, int n_tiles,
-                                                     int* __restrict__ order) {
-  __shared__ int s_hist[33];
-  __shared__ int s_off[33];
-  for (int i = threadIdx.x; i < 33; i += blockDim.x) s_hist[i] = 0;
+// ------------------------------------------------------------------ tile metadata
+// ranges = exclusive scan of the per-tile pair counts; longest-first order by
+// power-of-two buckets of the list length (scheduling hint).  One CTA.
+__global__ void __launch_bounds__(1024) k_tile_meta(const int32_t* __restrict__ tile_cnt, int n_tiles,
+                                                    const int64_t* __restrict__ scal, int64_t capacity,
+                                                    int2* __restrict__ ranges, int* __restrict__ order) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  __shared__ int s_hist[33], s_off[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x < 33) s_hist[threadIdx.x] = 0;
+  const bool complete = scal[S_P] <= capacity;
   __syncthreads();
-  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const int2 r = ranges[t];
-    const int len = r.y - r.x;
-    atomicAdd(&s_hist[len > 0 ? 32 - __clz(len) : 0], 1);
+  for (int t0 = 0; t0 < n_tiles; t0 += 1024) {
+    const int t = t0 + threadIdx.x;
+    const int v = (t < n_tiles && complete) ? tile_cnt[t] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += x;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) {
+      wpre += (w < warp) ? warp_tot[w] : 0;
+      tot += warp_tot[w];
+    }
+    if (t < n_tiles) {
+      const int start = carry + wpre + inc - v;
+      ranges[t] = v > 0 ? make_int2(start, start + v) : make_int2(0, 0);
+      if (order) atomicAdd(&s_hist[v > 0 ? 32 - __clz(v) : 0], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
   }
-  __syncthreads();
+  if (!order) return;
   if (threadIdx.x == 0) {
     int run = 0;
-    for (int b = 32; b >= 0; --b) {
-      s_off[b] = run;
-      run += s_hist[b];
+    for (int bb = 32; bb >= 0; --bb) {
+      s_off[bb] = run;
+      run += s_hist[bb];
     }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const int2 r = ranges[t];
-    const int len = r.y - r.x;
-    order[atomicAdd(&s_off[len > 0 ? 32 - __clz(len) : 0], 1)] = t;
+    const int v = complete ? tile_cnt[t] : 0;
+    order[atomicAdd(&s_off[v > 0 ? 32 - __clz(v) : 0], 1)] = t;
+  }
+}
+
+// (tile << 32 | depth bits) from the trimmed keys
+__global__ void k_keys64(const uint64_t* __restrict__ keys, const int64_t* __restrict__ scal, int64_t capacity,
+                         uint64_t* __restrict__ out) {
+  const int64_t P = min(scal[S_P], capacity);
+  const int b = (int)scal[S_B];
+  const uint32_t kmin = (uint32_t)scal[S_KMIN];
+  const uint64_t mask = b >= 64 ? ~0ull : ((1ull << b) - 1ull);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    out[i] = ((k >> b) << 32) | (uint64_t)((uint32_t)(k & mask) + kmin);
   }
 }
 
@@ -511,7 +527,7 @@ extern "C" int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t cap, int32_
   clear_error();
   SIMULI_REQUIRE(bytes && n >= 0 && n_tiles >= 1, "simuli_bin_sort_workspace_size: bad argument");
   if (cap < 0) cap = -cap;
-  *bytes = carve(nullptr, n, cap).bytes;
+  *bytes = carve(nullptr, n, cap, n_tiles).bytes;
   return SIMULI_OK;
 }
 
@@ -529,12 +545,13 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
   const bool sync_mode = pair_capacity < 0;
   const int64_t cap = sync_mode ? -pair_capacity : pair_capacity;
   SIMULI_REQUIRE(cap < (1ll << 30), "pair capacity must be < 2^30");
-  const Workspace need = carve(nullptr, n, cap);
+  const int tbits = tile_bits_of(n_tiles);
+  SIMULI_REQUIRE(tbits <= 16, "n_tiles must be <= 65536");
+  const Workspace need = carve(nullptr, n, cap, n_tiles);
   SIMULI_REQUIRE(workspace && ws_bytes >= need.bytes, "workspace too small: need %zu bytes", need.bytes);
-  Workspace w = carve(workspace, n, cap);
+  Workspace w = carve(workspace, n, cap, n_tiles);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int tpasses = tile_passes(n_tiles);
-  const int64_t nb = (n + kBlk - 1) / kBlk;
+  const int64_t nb = (n + kDupBlock - 1) / kDupBlock;
   auto check = [&](const char* what) -> int32_t {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -543,11 +560,11 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     }
     return SIMULI_OK;
   };
-  if (cudaMemsetAsync(tile_ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, st) != cudaSuccess)
-    return check("memset ranges");
   if (nb > 0)
-    k_count_reduce<<<(unsigned)nb, kBlkThreads, 0, st>>>(proj->tile_count, n, w.blk_pairs, w.blk_vis);
-  k_count_top<<<1, 1024, 0, st>>>(w.blk_pairs, w.blk_vis, nb, w.scal, n_pairs_dev, w.hist, w.counters);
+    k_count_reduce<<<(unsigned)nb, kDupThreads, 0, st>>>(proj->tile_count, proj->depth_key, n, w.block_sums,
+                                                          w.block_kmin, w.block_kmax);
+  k_count_top<<<1, 1024, 0, st>>>(w.block_sums, w.block_kmin, w.block_kmax, nb, tbits, w.scal, n_pairs_dev, w.hist,
+                                  w.counters, w.tile_cnt, n_tiles);
   if (int32_t e = check("scan")) return e;
   if (sync_mode) {
     int64_t P = 0;
@@ -560,47 +577,24 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
       return SIMULI_ERR_CAPACITY;
     }
   }
-  if (cudaMemsetAsync(w.status, 0, sizeof(uint32_t) * (kDepthPasses + tpasses) * w.max_parts * 256, st) !=
-      cudaSuccess)
+  const int max_passes = (32 + tbits + 7) / 8;
+  if (w.parts > 0 &&
+      cudaMemsetAsync(w.status, 0, sizeof(uint32_t) * (size_t)max_passes * w.parts * 256, st) != cudaSuccess)
     return check("memset status");
-  auto sweep = [&](int pass_slot, const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
-                   const int64_t* count, int64_t capacity, int shift) {
-    const int64_t parts = (capacity + kPart - 1) / kPart;
-    if (parts <= 0) return;
-    SweepArgs S{kin, vin, kout, vout, count, capacity, shift, w.hist + pass_slot * 256,
-                w.status + (size_t)pass_slot * w.max_parts * 256, w.counters + pass_slot};
-    k_onesweep<<<(unsigned)parts, kSortThreads, 0, st>>>(S);
-  };
-  // ---- stage 1: depth sort of the visible particles (result back in vk[0] / vi[0])
-  if (nb > 0) {
-    k_compact<<<(unsigned)nb, kBlkThreads, 0, st>>>(proj->tile_count, proj->depth_key, n, w.blk_vis, w.vk[0],
-                                                    w.vi[0], w.hist);
-    for (int p = 0; p < kDepthPasses; ++p)
-      sweep(p, w.vk[p & 1], w.vi[p & 1], w.vk[(p + 1) & 1], w.vi[(p + 1) & 1], w.scal + 1, n, 8 * p);
-    if (int32_t e = check("depth sort")) return e;
-    // ---- stage 2: duplication in depth order, stable tile sort
-    k_vcount_reduce<<<(unsigned)nb, kBlkThreads, 0, st>>>(proj->tile_count, w.vi[0], w.scal, w.vblk);
-    k_vcount_top<<<1, 1024, 0, st>>>(w.vblk, w.scal, w.scal + 2);
-    uint32_t* ti[2] = {sorted_ids, w.ti_alt};
-    int cur = (tpasses % 2 == 0) ? 0 : 1;  // the last pass must land in sorted_ids
-    if (cap > 0) {
-      DupArgs D{proj->tile_count, reinterpret_cast<const int4*>(proj->tile_rect), w.vi[0], w.scal, w.vblk, cap,
-                n_cols_total, tpasses, w.tk[cur], ti[cur], w.hist + kDepthPasses * 256};
-      k_duplicate<<<(unsigned)nb, kBlkThreads, 0, st>>>(D);
-      for (int p = 0; p < tpasses; ++p) {
-        sweep(kDepthPasses + p, w.tk[cur], ti[cur], w.tk[cur ^ 1], ti[cur ^ 1], w.scal, cap, 8 * p);
-        cur ^= 1;
-      }
-      if (int32_t e = check("tile sort")) return e;
-      k_ranges<<<148 * 4, 256, 0, st>>>(w.tk[cur], n_pairs_dev, cap, reinterpret_cast<int2*>(tile_ranges));
-      if (sorted_keys)
-        k_keys64<<<148 * 4, 256, 0, st>>>(w.tk[cur], sorted_ids, proj->depth_key, n_pairs_dev, cap, sorted_keys);
-      if (int32_t e = check("ranges")) return e;
+  uint32_t* vals[2] = {sorted_ids, w.vals_alt};
+  if (nb > 0 && cap > 0) {
+    DupArgs D{proj->tile_count, reinterpret_cast<const int4*>(proj->tile_rect), proj->depth_key, n, cap,
+              w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, w.tile_cnt};
+    k_duplicate<<<(unsigned)nb, kDupThreads, 0, st>>>(D);
+    if (int32_t e = check("duplicate")) return e;
+    for (int p = 0; p < max_passes; ++p) {
+      SweepArgs S{{w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.scal, cap, p, w.hist + p * 256,
+                  w.status + (size_t)p * w.parts * 256, w.counters + p};
+      k_onesweep<<<(unsigned)w.parts, kSortThreads, 0, st>>>(S);
     }
+    if (int32_t e = check("onesweep")) return e;
   }
-  if (tile_order) {
-    k_tile_order<<<1, 1024, 0, st>>>(reinterpret_cast<const int2*>(tile_ranges), n_tiles, tile_order);
-    if (int32_t e = check("tile order")) return e;
-  }
-  return SIMULI_OK;
+  k_tile_meta<<<1, 1024, 0, st>>>(w.tile_cnt, n_tiles, w.scal, cap, reinterpret_cast<int2*>(tile_ranges), tile_order);
+  if (sorted_keys && cap > 0) k_keys64<<<148 * 4, 256, 0, st>>>(w.keys[0], w.scal, cap, sorted_keys);
+  return check("tile metadata");
 }

@@ -292,6 +292,7 @@ class _Frame:
                                self.tile_order)
         if need is not None:
             self.set_capacity(int(need * 1.25) + 1024)
+            keys = self.sorted_keys if self.keep_keys else None
             need = simuli_bin_sort(self.projected, self.n, self.n_tiles, self.n_cols_total, self.workspace,
                                    -self.capacity, keys, self.sorted_ids, self.tile_ranges,
                                    self.n_pairs, stream, self.tile_order)
