@@ -14,7 +14,6 @@
 //                   tid+256, ... binary-searching its owner in shared memory) of the
 //                   trimmed key (tile << b) | (depth bits - min) -- an order-preserving
 //                   map of (tile, depth bits) -- plus the digit histograms of every pass
-//                   and the per-tile pair counts
 //   k_onesweep x 6  stable LSD onesweep, 8-bit digits; passes beyond the device-side pass
 //                   count exit at once (buffer parity is chosen on the device so the
 //                   last real pass lands in the caller's arrays).  Per 3072-key partition
@@ -22,9 +21,8 @@
 //                   over partitions (dynamic partition ids for forward progress) yields
 //                   the global digit offsets, keys are staged in shared memory in digit
 //                   order and written out coalesced.
-//   k_tile_meta     tile ranges = exclusive scan of the per-tile pair counts (the sort is
-//                   stable, so tile t occupies [start_t, start_t + count_t)); longest-first
-//                   tile order
+//   k_ranges        [begin, end) per tile from tile changes of the sorted keys
+//   k_tile_order    longest-first tile order
 //   [k_keys64]      the u64 (tile << 32 | depth bits) keys, only if the caller wants them
 #include <cstdint>
 
@@ -314,7 +312,6 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
     if (pos < A.capacity) {
       kout[pos] = key;
       vout[pos] = (uint32_t)(g0 + lo);
-      atomicAdd(A.tile_cnt + tile, 1);
       for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * 256 + (int)((key >> (8 * p)) & 0xFF)], 1u);
     }
   }
@@ -344,7 +341,7 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const SweepArgs A) {
+__global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A) {
   __shared__ uint32_t s_part;
   __shared__ uint32_t s_warp_hist[8][256];
   __shared__ uint32_t s_digit_excl[256];
@@ -389,19 +386,15 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const SweepArgs A) {
   const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
+    // warp multisplit: lanes with equal digits (match.any), the highest of them bumps the
+    // warp's digit counter once and broadcasts the previous value
     const uint32_t d = (uint32_t)(k[i] >> shift) & 0xFFu;
-    uint32_t peers = 0xffffffffu;
-#pragma unroll
-    for (int bb = 0; bb < 8; ++bb) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, (d >> bb) & 1u);
-      peers &= ((d >> bb) & 1u) ? bal : ~bal;
-    }
-    const uint32_t before = __popc(peers & lt_mask);
-    const uint32_t prev = s_warp_hist[warp][d];
-    __syncwarp();
-    if (before == 0) s_warp_hist[warp][d] = prev + __popc(peers);
-    __syncwarp();
-    rank[i] = prev + before;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = 31 - __clz(peers);
+    uint32_t prev = 0;
+    if (lane == leader) prev = atomicAdd(&s_warp_hist[warp][d], (uint32_t)__popc(peers));
+    prev = __shfl_sync(0xffffffffu, prev, leader);
+    rank[i] = prev + __popc(peers & lt_mask);
   }
   __syncthreads();
   const int d = tid;
@@ -453,45 +446,33 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const SweepArgs A) {
 }
 
 // ------------------------------------------------------------------ tile metadata
-// ranges = exclusive scan of the per-tile pair counts; longest-first order by
-// power-of-two buckets of the list length (scheduling hint).  One CTA.
-__global__ void __launch_bounds__(1024) k_tile_meta(const int32_t* __restrict__ tile_cnt, int n_tiles,
-                                                    const int64_t* __restrict__ scal, int64_t capacity,
-                                                    int2* __restrict__ ranges, int* __restrict__ order) {
-  __shared__ int warp_tot[32];
-  __shared__ int carry;
-  __shared__ int s_hist[33], s_off[33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  if (threadIdx.x < 33) s_hist[threadIdx.x] = 0;
-  const bool complete = scal[S_P] <= capacity;
-  __syncthreads();
-  for (int t0 = 0; t0 < n_tiles; t0 += 1024) {
-    const int t = t0 + threadIdx.x;
-    const int v = (t < n_tiles && complete) ? tile_cnt[t] : 0;
-    int inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int x = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += x;
-    }
-    if (lane == 31) warp_tot[warp] = inc;
-    __syncthreads();
-    int wpre = 0, tot = 0;
-    for (int w = 0; w < 32; ++w) {
-      wpre += (w < warp) ? warp_tot[w] : 0;
-      tot += warp_tot[w];
-    }
-    if (t < n_tiles) {
-      const int start = carry + wpre + inc - v;
-      ranges[t] = v > 0 ? make_int2(start, start + v) : make_int2(0, 0);
-      if (order) atomicAdd(&s_hist[v > 0 ? 32 - __clz(v) : 0], 1);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
+// [begin, end) of every tile from the tile changes of the sorted keys (tile = key >> b)
+__global__ void k_ranges(const uint64_t* __restrict__ keys, const int64_t* __restrict__ scal, int64_t capacity,
+                         int2* __restrict__ ranges) {
+  const int64_t P = min(scal[S_P], capacity);
+  const int b = (int)scal[S_B];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(keys[i] >> b);
+    if (i == 0 || (uint32_t)(keys[i - 1] >> b) != t) ranges[t].x = (int)i;
+    if (i == P - 1 || (uint32_t)(keys[i + 1] >> b) != t) ranges[t].y = (int)(i + 1);
   }
-  if (!order) return;
+}
+
+// Longest-first schedule: tiles bucketed by floor(log2(list length)), decreasing (a
+// counting sort; the order inside a bucket is whatever the atomics give -- it only affects
+// scheduling, never results).  One CTA.
+__global__ void __launch_bounds__(1024) k_tile_order(const int2* __restrict__ ranges, int n_tiles,
+                                                     int* __restrict__ order) {
+  __shared__ int s_hist[33];
+  __shared__ int s_off[33];
+  for (int i = threadIdx.x; i < 33; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+    const int2 r = ranges[t];
+    const int len = r.y - r.x;
+    atomicAdd(&s_hist[len > 0 ? 32 - __clz(len) : 0], 1);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     int run = 0;
     for (int bb = 32; bb >= 0; --bb) {
@@ -501,8 +482,9 @@ __global__ void __launch_bounds__(1024) k_tile_meta(const int32_t* __restrict__ 
   }
   __syncthreads();
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-    const int v = complete ? tile_cnt[t] : 0;
-    order[atomicAdd(&s_off[v > 0 ? 32 - __clz(v) : 0], 1)] = t;
+    const int2 r = ranges[t];
+    const int len = r.y - r.x;
+    order[atomicAdd(&s_off[len > 0 ? 32 - __clz(len) : 0], 1)] = t;
   }
 }
 
@@ -594,7 +576,11 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     }
     if (int32_t e = check("onesweep")) return e;
   }
-  k_tile_meta<<<1, 1024, 0, st>>>(w.tile_cnt, n_tiles, w.scal, cap, reinterpret_cast<int2*>(tile_ranges), tile_order);
+  if (cudaMemsetAsync(tile_ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, st) != cudaSuccess)
+    return check("memset ranges");
+  if (cap > 0) k_ranges<<<148 * 8, 256, 0, st>>>(w.keys[0], w.scal, cap, reinterpret_cast<int2*>(tile_ranges));
+  if (tile_order)
+    k_tile_order<<<1, 1024, 0, st>>>(reinterpret_cast<const int2*>(tile_ranges), n_tiles, tile_order);
   if (sorted_keys && cap > 0) k_keys64<<<148 * 4, 256, 0, st>>>(w.keys[0], w.scal, cap, sorted_keys);
   return check("tile metadata");
 }

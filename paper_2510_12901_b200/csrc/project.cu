@@ -154,6 +154,21 @@ __device__ __forceinline__ void rot_apply_t(const ProjArgs& A, float s, const fl
   p[2] = y[2] - sn * cz + omc * (k[2] * kd - y[2]);
 }
 
+// Azimuth of b relative to a, atan2(a x b, a . b) in (-pi, pi] (the A21 unwrap about a).
+// Small relative angles (all but the largest / nearest particles) use the odd series of
+// atan to t^11 (|t| <= 0.2: truncation < 1e-10 rad); the rest fall back to atan2f.
+__device__ __forceinline__ float rel_azimuth(const float a[3], const float b[3]) {
+  const float cr = a[0] * b[1] - a[1] * b[0];
+  const float dt = a[0] * b[0] + a[1] * b[1];
+  if (dt > 0.f && fabsf(cr) <= 0.2f * dt) {
+    const float t = __fdividef(cr, dt), t2 = t * t;
+    return t * (1.f - t2 * (1.f / 3.f - t2 * (1.f / 5.f - t2 * (1.f / 7.f - t2 * (1.f / 9.f - t2 * (1.f / 11.f))))));
+  }
+  return atan2f(cr, dt);
+}
+
+__device__ __forceinline__ float wrap01(float s) { return s < 0.f ? s + 1.f : (s >= 1.f ? s - 1.f : s); }
+
 // sensor-frame position of the sigma point with start-pose coordinates q at its own firing
 // time (K fixed-point updates of s from s = 0); *s_out = the firing time used
 __device__ __forceinline__ void lidar_fire(const ProjArgs& A, const float q[3], float p[3], float* s_out) {
@@ -186,12 +201,38 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
   const float d0 = mu[0] - A.t0w[0], d1 = mu[1] - A.t0w[1], d2 = mu[2] - A.t0w[2];
   const float c[3] = {R0[0] * d0 + R0[3] * d1 + R0[6] * d2, R0[1] * d0 + R0[4] * d1 + R0[7] * d2,
                       R0[2] * d0 + R0[5] * d1 + R0[8] * d2};
+  // firing times: K = 1 fixed-point step from s = 0 evaluated in the start frame, with the
+  // sigma points' azimuths taken relative to sigma point 0 (one atan2f per particle)
+  const bool moving = !A.pose.same && A.K >= 1;
+  const float inv2pi = 0.15915494309189535f;
+  float s_c = 0.f;
+  if (moving) {
+    float a = (float)A.dir * (atan2f(c[1], c[0]) - A.az_start);
+    a = a - 6.283185307179586f * floorf(a * inv2pi);
+    s_c = fminf(fmaxf(a * inv2pi, 0.f), 1.f);
+  }
+  auto fire = [&](const float q[3], float s, float p[3]) {
+    if (!moving) {
+      p[0] = q[0]; p[1] = q[1]; p[2] = q[2];
+      return;
+    }
+    const float y[3] = {q[0] - s * A.v[0], q[1] - s * A.v[1], q[2] - s * A.v[2]};
+    rot_apply_t(A, s, y, p);
+    for (int it = 1; it < A.K; ++it) {  // further fixed-point steps (K > 1)
+      float a = (float)A.dir * (atan2f(p[1], p[0]) - A.az_start);
+      a = a - 6.283185307179586f * floorf(a * inv2pi);
+      s = fminf(fmaxf(a * inv2pi, 0.f), 1.f);
+      const float y2[3] = {q[0] - s * A.v[0], q[1] - s * A.v[1], q[2] - s * A.v[2]};
+      rot_apply_t(A, s, y2, p);
+    }
+  };
   float p0[3];
-  lidar_fire(A, c, p0, s0);
-  const float r0 = sqrtf(p0[0] * p0[0] + p0[1] * p0[1] + p0[2] * p0[2]);
-  bool ok = r0 >= A.r_min;
+  fire(c, s_c, p0);
+  *s0 = s_c;
+  const float r02 = p0[0] * p0[0] + p0[1] * p0[1] + p0[2] * p0[2];
+  bool ok = r02 >= A.r_min * A.r_min;
   *a0 = atan2f(p0[1], p0[0]);
-  const float om0 = asinf(fminf(1.f, fmaxf(-1.f, p0[2] / r0)));
+  const float om0 = asinf(fminf(1.f, fmaxf(-1.f, p0[2] * rsqrtf(r02))));
   float Sd = 0.f, Se = 0.f, Sdd = 0.f, See = 0.f, Sde = 0.f;
 #pragma unroll 1
   for (int k = 0; k < 3; ++k) {
@@ -202,12 +243,13 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
     for (int sg = 0; sg < 2; ++sg) {
       const float q[3] = {sg ? c[0] - lr[0] : c[0] + lr[0], sg ? c[1] - lr[1] : c[1] + lr[1],
                           sg ? c[2] - lr[2] : c[2] + lr[2]};
-      float p[3], s;
-      lidar_fire(A, q, p, &s);
-      const float r = sqrtf(p[0] * p[0] + p[1] * p[1] + p[2] * p[2]);
-      ok = ok && r >= A.r_min;
-      const float d = atan2f(p0[0] * p[1] - p0[1] * p[0], p0[0] * p[0] + p0[1] * p[1]);
-      const float e = asinf(fminf(1.f, fmaxf(-1.f, p[2] / r))) - om0;
+      const float s = moving ? wrap01(s_c + (float)A.dir * rel_azimuth(c, q) * inv2pi) : 0.f;
+      float p[3];
+      fire(q, s, p);
+      const float r2 = p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
+      ok = ok && r2 >= A.r_min * A.r_min;
+      const float d = rel_azimuth(p0, p);
+      const float e = asinf(fminf(1.f, fmaxf(-1.f, p[2] * rsqrtf(r2)))) - om0;
       Sd += d;
       Se += e;
       Sdd = fmaf(d, d, Sdd);
