@@ -1111,6 +1111,318 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v5(const LidarV2
   cp_async_wait0();
 }
 
+// ------------------------------------------------------------------ LiDAR v6
+// v5 with a latency-free consumer: the producers place every member pair's (alpha, tau)
+// and entry index ray-major -- slot k of ray r holds the k-th member of r in list order,
+// k = (members of r in earlier producer warps) + popc(r's member word & entries below) --
+// so the compositing warp streams its ray's members with no index arithmetic or
+// dependent shared-memory lookups on the transmittance chain.  Rays with more than
+// kV6Cap members in one round take the rare slow path (walk the member words, response
+// from the record in global memory).
+constexpr int kV6Cap = 48;
+
+template <int NP>
+struct V6Smem {
+  float4 rec[2][32 * NP][5];
+  float2 at[2][32][kV6Cap];     // ray-major (alpha, tau)
+  uint8_t ent[2][32][kV6Cap];   // ray-major entry index within the round
+  float4 feat[2][32 * NP];
+  uint32_t memb[2][NP][32];     // [warp][ray] member entries of the warp's 32
+  int rowoff[NP][32];           // members of ray r in warps before w (current round)
+  uint32_t wmask[NP][32];
+  int wex[NP][32];
+  uint16_t plist[NP][1024];
+  float ray_oh[32][3], ray_ol[32][3], ray_dh[32][3], ray_dl[32][3];
+  float col_phi[32], beam_el[32];
+  int col_id[32], beam_id[32];
+  int stop_at[2];
+};
+
+template <int NP>
+__global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v6(const LidarV2Args A) {
+  constexpr int E = 32 * NP;
+  constexpr int NT = 32 * (NP + 1);
+  constexpr int BAR_PROD = 1, BAR_FULL = 2, BAR_EMPTY = 4, BAR_RAYS = 6;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V6Smem<NP>& S = *reinterpret_cast<V6Smem<NP>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t item = blockIdx.x;
+  const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
+  const int tile = A.order ? __ldg(A.order + tslot) : tslot;
+  const int et = tile / A.n_theta, at_ = tile % A.n_theta;
+  const int bgi = sub / A.n_cg, cgi = sub % A.n_cg;
+  const int b0 = __ldg(A.etb_off + et) + bgi * A.bg, b1 = min(__ldg(A.etb_off + et + 1), b0 + A.bg);
+  const int c0 = __ldg(A.atc_off + at_) + cgi * A.cg, c1 = min(__ldg(A.atc_off + at_ + 1), c0 + A.cg);
+  const int nb = b1 - b0, nc = c1 - c0;
+  if (nb <= 0 || nc <= 0) return;  // CTA-uniform
+  const int R = nb * nc;
+  if (tid < nc) {
+    const int j = __ldg(A.atc + c0 + tid);
+    S.col_id[tid] = j;
+    S.col_phi[tid] = __ldg(A.ray_az + j);
+  }
+  if (tid >= 32 && tid < 32 + nb) {
+    const int b = __ldg(A.etb + b0 + tid - 32);
+    S.beam_id[tid - 32] = b;
+    S.beam_el[tid - 32] = __ldg(A.ray_el + (size_t)b * A.n_az);
+  }
+  if (tid < 2) S.stop_at[tid] = 0;
+  __syncthreads();
+  const int2 rg = __ldg(A.ranges + tile);
+  const int n_rounds = (rg.y - rg.x + E - 1) / E;
+
+  if (warp == NP) {
+    // ================= consumer: lane = ray
+    int ray = 0;
+    double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
+    RayF rf;
+    if (lane < R) {
+      const int bi = lane / nc, ci = lane % nc;
+      const int j = S.col_id[ci];
+      ray = S.beam_id[bi] * A.n_az + j;
+      double Rm[9];
+      pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
+      double sa, ca, se, ce;
+      sincos((double)S.col_phi[ci], &sa, &ca);
+      sincos((double)S.beam_el[bi], &se, &ce);
+      const double u[3] = {ce * ca, ce * sa, se};
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
+    }
+    split_ray(o, dd, rf);
+    if (lane < R) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        S.ray_oh[lane][i] = rf.o_hi[i];
+        S.ray_ol[lane][i] = rf.o_lo[i];
+        S.ray_dh[lane][i] = rf.d_hi[i];
+        S.ray_dl[lane][i] = rf.d_lo[i];
+      }
+    }
+    __threadfence_block();
+    named_arrive(BAR_RAYS, NT);
+    float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
+    int ncontrib = 0, nv = 0, ni = 0;
+    bool done = lane >= R;
+    for (int r = 0; r < n_rounds; ++r) {
+      const int b = r & 1;
+      named_sync(BAR_FULL + b, NT);
+      const int start = rg.x + r * E;
+      if (!done) {
+        const int n_in = min(E, rg.y - start);
+        int cnt = 0;
+#pragma unroll
+        for (int w = 0; w < NP; ++w) cnt += __popc(S.memb[b][w][lane]);
+        bool stopped = false;
+        const int fast = min(cnt, kV6Cap);
+        int k = 0;
+        for (; k < fast; ++k) {
+          const float2 a = S.at[b][lane][k];
+          if (a.y < A.near_tau || a.x < A.alpha_min) continue;
+          const float Tn = T * (1.f - a.x);
+          if (Tn < A.T_min) {
+            stopped = true;
+            nv += S.ent[b][lane][k] + 1;
+            ni += k + 1;
+            break;
+          }
+          const float4 f = S.feat[b][S.ent[b][lane][k]];
+          const float wgt = a.x * T;
+          acc0 = fmaf(wgt, f.y, acc0);
+          acc1 = fmaf(wgt, f.z, acc1);
+          acc2 = fmaf(wgt, f.w, acc2);
+          D = fmaf(wgt, a.y, D);
+          W += wgt;
+          ++ncontrib;
+          T = Tn;
+        }
+        if (!stopped && cnt > kV6Cap) {
+          // slow path: members beyond the ray's slot capacity, in list order
+          int seen = 0;
+          for (int w = 0; w < NP && !stopped; ++w) {
+            uint32_t bits = S.memb[b][w][lane];
+            while (bits) {
+              const int oo = __ffs(bits) - 1;
+              bits &= bits - 1u;
+              if (seen++ < kV6Cap) continue;
+              const int e = w * 32 + oo;
+              const float4* src = A.record + (size_t)__ldg(A.ids + start + e) * 5;
+              const float4 r0 = __ldg(src), r1 = __ldg(src + 1), r2 = __ldg(src + 2), r3 = __ldg(src + 3);
+              const float mu[3] = {r0.x, r0.y, r0.z};
+              const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
+              float tau, d2;
+              response(rf, mu, M, &tau, &d2);
+              const float alpha = fminf(A.alpha_max, r3.x * expf(-0.5f * d2));
+              if (tau < A.near_tau || alpha < A.alpha_min) continue;
+              const float Tn = T * (1.f - alpha);
+              if (Tn < A.T_min) {
+                stopped = true;
+                nv += e + 1;
+                ni += seen;
+                break;
+              }
+              const float wgt = alpha * T;
+              acc0 = fmaf(wgt, r3.y, acc0);
+              acc1 = fmaf(wgt, r3.z, acc1);
+              acc2 = fmaf(wgt, r3.w, acc2);
+              D = fmaf(wgt, tau, D);
+              W += wgt;
+              ++ncontrib;
+              T = Tn;
+            }
+          }
+        }
+        if (stopped) done = true;
+        else {
+          nv += n_in;
+          ni += cnt;
+        }
+      }
+      const bool all = __all_sync(0xffffffffu, done);
+      if (r + 2 < n_rounds) {
+        if (lane == 0) S.stop_at[b] = all ? 1 : 0;
+        __threadfence_block();
+        named_arrive(BAR_EMPTY + b, NT);
+      }
+      if (all) {
+        if (r + 1 < n_rounds) named_sync(BAR_FULL + (b ^ 1), NT);  // drain the round in flight
+        break;
+      }
+    }
+    if (lane >= R) return;
+    if (A.zeta) {
+      A.zeta[3 * (size_t)ray] = acc0;
+      A.zeta[3 * (size_t)ray + 1] = acc1;
+      A.zeta[3 * (size_t)ray + 2] = acc2;
+    }
+    if (A.opacity) A.opacity[ray] = W;
+    if (A.depth_accum) A.depth_accum[ray] = D;
+    if (A.depth) A.depth[ray] = W > 0.f ? D / W : 0.f;
+    if (A.intensity) A.intensity[ray] = acc0;
+    if (A.raydrop) A.raydrop[ray] = raydrop_prob(acc1, acc2);
+    if (A.final_T) A.final_T[ray] = T;
+    if (A.n_contrib) A.n_contrib[ray] = ncontrib;
+    if (A.n_visited) A.n_visited[ray] = nv;
+    if (A.n_inbox) A.n_inbox[ray] = ni;
+    if (A.ray_od) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        A.ray_od[6 * (size_t)ray + i] = o[i];
+        A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
+      }
+    }
+    return;
+  }
+
+  // ================= producers: thread = list entry of the round
+  auto issue = [&](int stage, int start, uint32_t id) {
+    if (start + tid < rg.y) {
+      const float4* src = A.record + (size_t)id * 5;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[stage][tid][c], src + c);
+    }
+    cp_async_commit();
+  };
+  auto load_id = [&](int round) -> uint32_t {
+    const int e = rg.x + round * E + tid;
+    return (round < n_rounds && e < rg.y) ? __ldg(A.ids + e) : 0u;
+  };
+  issue(0, rg.x, load_id(0));
+  uint32_t id_pf = load_id(1);
+  named_sync(BAR_RAYS, NT);
+  for (int r = 0; r < n_rounds; ++r) {
+    const int b = r & 1;
+    if (r >= 2) {
+      named_sync(BAR_EMPTY + b, NT);
+      if (S.stop_at[b]) break;
+    }
+    const int start = rg.x + r * E;
+    cp_async_wait0();
+    named_sync(BAR_PROD, E);  // round r's records visible; stage b^1 and rowoff free
+    issue(b ^ 1, start + E, id_pf);
+    id_pf = load_id(r + 2);
+    const bool valid = start + tid < rg.y;
+    uint32_t m = 0;
+    if (valid) {
+      const float4 bx = S.rec[b][tid][4];
+      S.feat[b][tid] = S.rec[b][tid][3];
+      uint32_t colbits = 0;
+      if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
+        colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
+      } else {
+        const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
+        const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
+        for (int ci = 0; ci < nc; ++ci) {
+          const float p = S.col_phi[ci];
+          const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
+          colbits |= (uint32_t)in << ci;
+        }
+      }
+      if (colbits)
+        for (int bi = 0; bi < nb; ++bi) {
+          const float w = S.beam_el[bi];
+          if (bx.z <= w && w <= bx.w) m |= colbits << (bi * nc);
+        }
+    }
+    const uint32_t my = warp_transpose32(m, lane);  // lane r: entries of this warp holding ray r
+    S.memb[b][warp][lane] = my;
+    const int k = __popc(m);
+    int inc = k;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += t;
+    }
+    const int K = __shfl_sync(0xffffffffu, inc, 31);
+    const int ex = inc - k;
+    S.wex[warp][lane] = ex;
+    S.wmask[warp][lane] = m;
+    {
+      int pos = ex;
+      uint32_t mm = m;
+      while (mm) {
+        const int rr = __ffs(mm) - 1;
+        mm &= mm - 1u;
+        S.plist[warp][pos++] = (uint16_t)((lane << 5) | rr);
+      }
+    }
+    named_sync(BAR_PROD, E);  // every producer warp's member words are in
+    {
+      int off = 0;
+#pragma unroll
+      for (int w = 0; w < NP; ++w)
+        if (w < warp) off += __popc(S.memb[b][w][lane]);
+      S.rowoff[warp][lane] = off;
+    }
+    __syncwarp();
+    for (int idx = lane; idx < K; idx += 32) {
+      const int v = S.plist[warp][idx];
+      const int rr = v & 31, el = v >> 5, e = warp * 32 + el;
+      const int slot = S.rowoff[warp][rr] + __popc(S.memb[b][warp][rr] & ((1u << el) - 1u));
+      if (slot >= kV6Cap) continue;  // consumer's slow path
+      const float4 r0 = S.rec[b][e][0], r1 = S.rec[b][e][1], r2 = S.rec[b][e][2], r3 = S.rec[b][e][3];
+      const float mu[3] = {r0.x, r0.y, r0.z};
+      const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
+      RayF rf;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        rf.o_hi[i] = S.ray_oh[rr][i];
+        rf.o_lo[i] = S.ray_ol[rr][i];
+        rf.d_hi[i] = S.ray_dh[rr][i];
+        rf.d_lo[i] = S.ray_dl[rr][i];
+      }
+      float tau, d2;
+      response(rf, mu, M, &tau, &d2);
+      S.at[b][rr][slot] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
+      S.ent[b][rr][slot] = (uint8_t)e;
+    }
+    __syncwarp();
+    __threadfence_block();
+    named_arrive(BAR_FULL + b, NT);
+  }
+  cp_async_wait0();
+}
+
 int32_t launch_check(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -1181,7 +1493,7 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
       k_render_lidar_v2<<<(unsigned)A.n_items, 32 * kV2Warps, sizeof(V2Smem), st>>>(A);
     } else {
       const char* kv = getenv("SIMULI_LIDAR_KERNEL");
-      const std::string kind = kv ? kv : "v5_4";
+      const std::string kind = kv ? kv : "v6_4";
       auto launch_v3 = [&](auto np_tag) {
         constexpr int NP = decltype(np_tag)::value;
         cudaFuncSetAttribute(k_render_lidar_v3<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1194,7 +1506,16 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
                              (int)sizeof(V5Smem<NP>));
         k_render_lidar_v5<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V5Smem<NP>), st>>>(A);
       };
-      if (kind == "v3") launch_v3(std::integral_constant<int, 4>{});
+      auto launch_v6 = [&](auto np_tag) {
+        constexpr int NP = decltype(np_tag)::value;
+        cudaFuncSetAttribute(k_render_lidar_v6<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(V6Smem<NP>));
+        k_render_lidar_v6<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V6Smem<NP>), st>>>(A);
+      };
+      if (kind == "v6_4") launch_v6(std::integral_constant<int, 4>{});
+      else if (kind == "v6_2") launch_v6(std::integral_constant<int, 2>{});
+      else if (kind == "v6_8") launch_v6(std::integral_constant<int, 8>{});
+      else if (kind == "v3") launch_v3(std::integral_constant<int, 4>{});
       else if (kind == "v3_2") launch_v3(std::integral_constant<int, 2>{});
       else if (kind == "v5_8") launch_v5(std::integral_constant<int, 8>{});
       else if (kind == "v5_2") launch_v5(std::integral_constant<int, 2>{});
