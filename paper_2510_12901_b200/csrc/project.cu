@@ -109,10 +109,15 @@ __device__ __forceinline__ int elev_tile(const ProjArgs& A, float w) {
   int lo = 1, hi = A.n_phi;  // first index in [1, n_phi) with bound > w
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (__ldg(A.bounds + mid) <= w) lo = mid + 1;
+    if (A.bounds[mid] <= w) lo = mid + 1;
     else hi = mid;
   }
   return lo - 1;
+}
+
+__device__ __forceinline__ int dense_row_e(const ProjArgs& A, float w, int e) {
+  const float u = __fmul_rn(__fsub_rn(w, A.bounds[e]), A.row_scale[e]);
+  return e * A.rows_per_tile + clamp_floor(u, A.rows_per_tile);
 }
 
 __device__ __forceinline__ int dense_row(const ProjArgs& A, float w) {
@@ -314,12 +319,28 @@ __device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3],
   return valid;
 }
 
+constexpr int kSmemBounds = 264;
+constexpr int kShSmem = 8 * 12 * 32 * 16;
+
 template <int KIND>
-__global__ void __launch_bounds__(256, 3) k_project(const ProjArgs A) {
+__global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
+  // tiling boundaries / row scales staged in shared memory (binary searches hit smem)
+  __shared__ float s_bounds[kSmemBounds], s_rscale[kSmemBounds];
+  ProjArgs A = Ain;
+  if (KIND == SIMULI_SENSOR_LIDAR && Ain.n_phi + 1 <= kSmemBounds) {
+    for (int i = threadIdx.x; i <= Ain.n_phi; i += blockDim.x) {
+      s_bounds[i] = __ldg(Ain.bounds + i);
+      if (i < Ain.n_phi) s_rscale[i] = __ldg(Ain.row_scale + i);
+    }
+    __syncthreads();
+    A.bounds = s_bounds;
+    A.row_scale = s_rscale;
+  }
   // degree-3 SH of the warp's 32 particles (32 x 192 B contiguous) staged into shared memory
   // by coalesced 16-byte cp.async at kernel start, overlapping the projection arithmetic;
   // layout [chunk][particle] so each lane's later reads are conflict-free
-  __shared__ float4 s_sh[8][12][32];
+  extern __shared__ float4 s_sh_raw[];  // [8 warps][12 chunks][32 lanes] (48 KB, dynamic)
+  float4 (*s_sh)[12][32] = reinterpret_cast<float4 (*)[12][32]>(s_sh_raw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool stage_sh = A.sh_degree == 3;
@@ -435,8 +456,9 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs A) {
       if (KIND == SIMULI_SENSOR_LIDAR) {
         const float b0 = __ldg(A.bounds), bl = __ldg(A.bounds + A.n_phi);
         bool keep = !(box[3] < b0 || box[2] > bl);
+        const int e0 = elev_tile(A, box[2]), e1 = elev_tile(A, box[3]);
         if (keep && A.enable_cull) {
-          const int r0 = dense_row(A, box[2]), r1 = dense_row(A, box[3]);
+          const int r0 = dense_row_e(A, box[2], e0), r1 = dense_row_e(A, box[3], e1);
           int cs, cl;
           az_run(box[0], box[1], A.pi_f, A.two_pi_f, A.az_cell_scale, A.az_cells, &cs, &cl);
           const int ce = cs + cl - 1;
@@ -446,7 +468,6 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs A) {
           keep = occ > 0;
         }
         if (keep) {
-          const int e0 = elev_tile(A, box[2]), e1 = elev_tile(A, box[3]);
           int cs, cl;
           az_run(box[0], box[1], A.pi_f, A.two_pi_f, A.az_tile_scale, A.n_theta, &cs, &cl);
           rect[0] = e0; rect[1] = e1; rect[2] = cs; rect[3] = cl;
@@ -607,7 +628,8 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.az_cells = T.cull_az_cells; A.sat_cols = T.sat_cols; A.enable_cull = P->enable_culling;
     A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f; A.az_tile_scale = T.az_tile_scale; A.az_cell_scale = T.az_cell_scale;
     A.bounds = T.elev_bounds; A.row_scale = T.cull_row_scale; A.sat = T.sat;
-    k_project<SIMULI_SENSOR_LIDAR><<<blocks, threads, 0, st>>>(A);
+    cudaFuncSetAttribute(k_project<SIMULI_SENSOR_LIDAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
+    k_project<SIMULI_SENSOR_LIDAR><<<blocks, threads, kShSmem, st>>>(A);
   } else if (P->kind == SIMULI_SENSOR_CAMERA) {
     SIMULI_REQUIRE(P->camera, "camera projection needs camera");
     const simuli_camera& C = *P->camera;
@@ -620,7 +642,8 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.fx = C.fx; A.fy = C.fy; A.cx = C.cx; A.cy = C.cy;
     for (int i = 0; i < 5; ++i) A.k[i] = C.k[i];
     A.near_m = C.near_m; A.max_theta = C.max_theta_rad; A.inv_tile = 1.0f / (float)C.tile_px;
-    k_project<SIMULI_SENSOR_CAMERA><<<blocks, threads, 0, st>>>(A);
+    cudaFuncSetAttribute(k_project<SIMULI_SENSOR_CAMERA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
+    k_project<SIMULI_SENSOR_CAMERA><<<blocks, threads, kShSmem, st>>>(A);
   } else {
     set_error("simuli_project: unknown sensor kind %d", P->kind);
     return SIMULI_ERR_INVALID_ARGUMENT;
