@@ -222,9 +222,20 @@ static void to_sensor(const double R[9], const double t[3], const double x[3], d
  *     firing time depends on the azimuth: K fixed-point iterations from s = 0 (A3, A5):
  *     s <- wrap_[0,2pi)(dir (phi - phi_start)) / 2pi.   out = (phi, omega, r, s).
  * ---------------------------------------------------------------------------------- */
+/* seam_dist (optional): smallest angular distance of a firing-time update's azimuth to
+ * the start of the sweep, where s jumps between 0 and 1 (an A23 threshold event) */
+static void lidar_point_seam(const double x[3], const or_lidar* L, const double pose0[7], const double pose1[7],
+                             int K, double out[4], double* seam_dist);
+
 void or_lidar_point(const double x[3], const or_lidar* L, const double pose0[7], const double pose1[7],
                     int K, double out[4]) {
+  lidar_point_seam(x, L, pose0, pose1, K, out, NULL);
+}
+
+static void lidar_point_seam(const double x[3], const or_lidar* L, const double pose0[7], const double pose1[7],
+                             int K, double out[4], double* seam_dist) {
   double s = 0.0, R[9], t[3], p[3], r = 0, phi = 0, om = 0;
+  if (seam_dist) *seam_dist = INFINITY;
   for (int i = 0; i <= K; ++i) {
     or_pose_at(pose0, pose1, s, R, t);
     to_sensor(R, t, x, p);
@@ -238,6 +249,10 @@ void or_lidar_point(const double x[3], const or_lidar* L, const double pose0[7],
       double a = (double)L->dir * (phi - L->az_start);
       a = a - OR_TWO_PI * floor(a / OR_TWO_PI);
       s = a / OR_TWO_PI;
+      if (seam_dist) {
+        const double dseam = a < OR_TWO_PI - a ? a : OR_TWO_PI - a;
+        if (dseam < *seam_dist) *seam_dist = dseam;
+      }
     }
   }
   out[0] = phi;
@@ -708,8 +723,11 @@ typedef int (*point_fn)(const double x[3], const void* sensor, const double p0[7
 static int lidar_point_fn(const double x[3], const void* sensor, const double p0[7], const double p1[7], int K,
                           double out[4], int* edge) {
   const or_lidar* L = (const or_lidar*)sensor;
-  or_lidar_point(x, L, p0, p1, K, out);
+  double seam = INFINITY;
+  const int moving = memcmp(p0, p1, 7 * sizeof(double)) != 0;
+  lidar_point_seam(x, L, p0, p1, K, out, &seam);
   if (fabs(out[2] - L->r_min) < 1e-4) *edge = 1;
+  if (moving && seam < 1e-5) *edge = 1; /* firing time s ~ 0 vs ~ 1: float32 may decide otherwise */
   return out[2] >= L->r_min;
 }
 
@@ -1045,14 +1063,17 @@ int or_composite(int64_t n_gauss, const double* mu, const double* Mrows, const d
                       (double)bx[2] - p->eps_b <= xb && xb <= (double)bx[3] + p->eps_b;
           int strict = in_interval_a_d(bx[0], bx[1], xa, p->wrap, -p->eps_a) &&
                        (double)bx[2] + p->eps_b <= xb && xb <= (double)bx[3] - p->eps_b;
-          if (loose != strict || (gamb && gamb[g] && loose)) {
+          /* validity-ambiguous particles (gamb) flag every live ray of the tiles they are
+           * listed in (their lists come from generously grown boxes) */
+          if (gamb && gamb[g]) flag |= 8;
+          if (loose != strict) {
             /* ambiguous membership matters only if this particle could composite with a
              * weight alpha T above the impact threshold (its alpha if it were a member) */
             double rs0[2];
             or_response(&mu[(int64_t)g * 3], &Mrows[(int64_t)g * 9], o, d, rs0);
             double a0 = sigma[g] * exp(-0.5 * rs0[1]);
             if (!(isfinite(a0)) || (a0 >= p->alpha_min - p->eps_alpha && a0 * T > p->eps_impact))
-              flag |= (loose != strict) ? 1 : 8;
+              flag |= 1;
           }
         }
         if (gamb && gamb[g] == 2) continue; /* listed for flagging only (oracle-invalid) */

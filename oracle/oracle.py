@@ -398,6 +398,9 @@ def records_from_projection(proj, scene):
 # whole-path oracle renders (tier 2)
 # ------------------------------------------------------------------------------------
 
+AMBIGUOUS_MARGIN = (0.1, 0.02)  # rad: listing margin of validity-ambiguous particles (flag mode)
+
+
 def expand_box(box, ea, eb):
     """Grow float32 boxes outward by (ea, eb) (flag-mode list construction)."""
     b = box.astype(np.float64)
@@ -427,11 +430,13 @@ def render_lidar(scene, cfg, tiling: Tiling | None = None, pose0=None, pose1=Non
         gamb = np.where(proj["ambiguous"] != 0, np.where(valid != 0, 1, 2), 0).astype(np.int32)
         listed = ((valid != 0) | (proj["ambiguous"] != 0)) & np.isfinite(proj["box"]).all(1)
         lbox = expand_box(proj["box"], flag_eps["a"], flag_eps["b"])
+        amb = proj["ambiguous"] != 0  # e.g. a sigma point at the sweep seam: the float32 box may differ a lot
+        lbox[amb] = expand_box(proj["box"][amb], AMBIGUOUS_MARGIN[0], AMBIGUOUS_MARGIN[1])
     else:
         listed = valid != 0
         lbox = proj["box"]
     if mode == "tiled":
-        count, rect = cull_lidar(listed.astype(np.int32), lbox, tiling, enable_cull)
+        count, rect = cull_lidar(listed.astype(np.int32), lbox, tiling, enable_cull and flag_eps is None)
         _, ids, ranges = bin_pairs(count, rect, proj["key"], tiling.n_tiles, tiling.n_theta)
         ray_tile = tiling.ray_tile
     else:

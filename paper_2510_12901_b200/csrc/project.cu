@@ -120,12 +120,6 @@ __device__ __forceinline__ int dense_row_e(const ProjArgs& A, float w, int e) {
   return e * A.rows_per_tile + clamp_floor(u, A.rows_per_tile);
 }
 
-__device__ __forceinline__ int dense_row(const ProjArgs& A, float w) {
-  const int e = elev_tile(A, w);
-  const float u = __fmul_rn(__fsub_rn(w, __ldg(A.bounds + e)), __ldg(A.row_scale + e));
-  return e * A.rows_per_tile + clamp_floor(u, A.rows_per_tile);
-}
-
 __device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c0, int c1) {
   const int sc = A.sat_cols;
   return __ldg(A.sat + (r1 + 1) * sc + (c1 + 1)) - __ldg(A.sat + r0 * sc + (c1 + 1)) -
@@ -454,7 +448,7 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
     if (ok) {
       // ---- culling + render-tile rectangle
       if (KIND == SIMULI_SENSOR_LIDAR) {
-        const float b0 = __ldg(A.bounds), bl = __ldg(A.bounds + A.n_phi);
+        const float b0 = A.bounds[0], bl = A.bounds[A.n_phi];
         bool keep = !(box[3] < b0 || box[2] > bl);
         const int e0 = elev_tile(A, box[2]), e1 = elev_tile(A, box[3]);
         if (keep && A.enable_cull) {

@@ -86,7 +86,7 @@ def test_project_lidar_tier1(SM, oracle_mod, config):
     ov = proj["valid"] != 0
     amb = proj["ambiguous"] != 0
     assert np.array_equal(gv[~amb], ov[~amb]), np.nonzero(gv[~amb] != ov[~amb])[0][:10]
-    both = gv & ov
+    both = gv & ov & ~amb
     # depth keys: bit-exact float32 (A19)
     assert np.array_equal(r.depth_key.cpu().numpy().view(np.uint32), proj["key"].view(np.uint32))
     db = np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both].astype(np.float64))
@@ -325,7 +325,9 @@ def test_config_b_full_size_sampled(SM, oracle_mod):
     rec2 = O.records_from_projection(proj, scene)
     listed = ((proj["valid"] != 0) | (proj["ambiguous"] != 0)) & np.isfinite(proj["box"]).all(1)
     lbox = O.expand_box(proj["box"], LIDAR_EPS["a"], LIDAR_EPS["b"])
-    count, rect = O.cull_lidar(listed.astype(np.int32), lbox, t, True)
+    amb = proj["ambiguous"] != 0
+    lbox[amb] = O.expand_box(proj["box"][amb], *O.AMBIGUOUS_MARGIN)
+    count, rect = O.cull_lidar(listed.astype(np.int32), lbox, t, False)
     _, ids2, ranges2 = O.bin_pairs(count, rect, proj["key"], t.n_tiles, t.n_theta)
     od2 = O.lidar_rays(t, cfg.pose_start, cfg.pose_end)[rays]
     gamb = np.where(proj["ambiguous"] != 0, np.where(proj["valid"] != 0, 1, 2), 0).astype(np.int32)
