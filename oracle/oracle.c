@@ -1063,9 +1063,11 @@ int or_composite(int64_t n_gauss, const double* mu, const double* Mrows, const d
                       (double)bx[2] - p->eps_b <= xb && xb <= (double)bx[3] + p->eps_b;
           int strict = in_interval_a_d(bx[0], bx[1], xa, p->wrap, -p->eps_a) &&
                        (double)bx[2] + p->eps_b <= xb && xb <= (double)bx[3] - p->eps_b;
-          /* validity-ambiguous particles (gamb) flag every live ray of the tiles they are
-           * listed in (their lists come from generously grown boxes) */
-          if (gamb && gamb[g]) flag |= 8;
+          /* validity-ambiguous particles (gamb): the float32 box may differ a lot (e.g. a
+           * sigma point at the sweep seam) -> flag live rays inside a generously grown box */
+          if (gamb && gamb[g] && in_interval_a_d(bx[0], bx[1], xa, p->wrap, p->eps_amb_a) &&
+              (double)bx[2] - p->eps_amb_b <= xb && xb <= (double)bx[3] + p->eps_amb_b)
+            flag |= 8;
           if (loose != strict) {
             /* ambiguous membership matters only if this particle could composite with a
              * weight alpha T above the impact threshold (its alpha if it were a member) */

@@ -126,6 +126,7 @@ typedef struct {
   double eps_a, eps_b;       /* box-edge ambiguity margins (coordinate units)           */
   double eps_alpha, eps_T_rel, eps_tau;
   double eps_impact;         /* box-edge flags only when alpha*T of the particle > this  */
+  double eps_amb_a, eps_amb_b; /* margins around validity-ambiguous particles' boxes       */
 } or_render_params;
 
 typedef struct {

@@ -74,7 +74,7 @@ class OrRenderParams(C.Structure):
                 ("T_min", C.c_double), ("wrap", C.c_int32), ("pi_f", C.c_float), ("two_pi_f", C.c_float),
                 ("flag_mode", C.c_int32), ("eps_a", C.c_double), ("eps_b", C.c_double),
                 ("eps_alpha", C.c_double), ("eps_T_rel", C.c_double), ("eps_tau", C.c_double),
-                ("eps_impact", C.c_double)]
+                ("eps_impact", C.c_double), ("eps_amb_a", C.c_double), ("eps_amb_b", C.c_double)]
 
 
 class OrRenderOut(C.Structure):
@@ -367,7 +367,8 @@ def composite(records, ids, ranges, ray_tile, ray_a, ray_b, ray_od, *, wrap, nea
     prm = OrRenderParams(float(np.float32(near)), float(np.float32(alpha_min)), float(np.float32(alpha_max)),
                          float(np.float32(T_min)), int(wrap), pf, tpf, int(flag_eps is not None),
                          fe.get("a", 0.0), fe.get("b", 0.0), fe.get("alpha", 0.0), fe.get("T_rel", 0.0),
-                         fe.get("tau", 0.0), fe.get("impact", 0.0))
+                         fe.get("tau", 0.0), fe.get("impact", 0.0), fe.get("amb_a", AMBIGUOUS_MARGIN[0]),
+                         fe.get("amb_b", AMBIGUOUS_MARGIN[1]))
     out = {"feat": np.zeros((R, 3)), "opacity": np.zeros(R), "depth_accum": np.zeros(R), "depth": np.zeros(R),
            "T_final": np.zeros(R), "n_contrib": np.zeros(R, np.int32), "flag": np.zeros(R, np.int32),
            "scanned": np.zeros(R, np.int64), "inbox": np.zeros(R, np.int64)}
@@ -431,7 +432,8 @@ def render_lidar(scene, cfg, tiling: Tiling | None = None, pose0=None, pose1=Non
         listed = ((valid != 0) | (proj["ambiguous"] != 0)) & np.isfinite(proj["box"]).all(1)
         lbox = expand_box(proj["box"], flag_eps["a"], flag_eps["b"])
         amb = proj["ambiguous"] != 0  # e.g. a sigma point at the sweep seam: the float32 box may differ a lot
-        lbox[amb] = expand_box(proj["box"][amb], AMBIGUOUS_MARGIN[0], AMBIGUOUS_MARGIN[1])
+        lbox[amb] = expand_box(proj["box"][amb], flag_eps.get("amb_a", AMBIGUOUS_MARGIN[0]),
+                               flag_eps.get("amb_b", AMBIGUOUS_MARGIN[1]))
     else:
         listed = valid != 0
         lbox = proj["box"]
@@ -467,6 +469,8 @@ def render_camera(scene, cam, pose0=None, pose1=None, mode="tiled", flag_eps=Non
         gamb = np.where(proj["ambiguous"] != 0, np.where(valid != 0, 1, 2), 0).astype(np.int32)
         listed = ((valid != 0) | (proj["ambiguous"] != 0)) & np.isfinite(proj["box"]).all(1)
         lbox = expand_box(proj["box"], flag_eps["a"], flag_eps["b"])
+        amb = proj["ambiguous"] != 0
+        lbox[amb] = expand_box(proj["box"][amb], flag_eps.get("amb_a", 20.0), flag_eps.get("amb_b", 20.0))
     else:
         listed = valid != 0
         lbox = proj["box"]

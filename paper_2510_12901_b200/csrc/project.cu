@@ -231,7 +231,7 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
   const float r02 = p0[0] * p0[0] + p0[1] * p0[1] + p0[2] * p0[2];
   bool ok = r02 >= A.r_min * A.r_min;
   *a0 = atan2f(p0[1], p0[0]);
-  const float om0 = asinf(fminf(1.f, fmaxf(-1.f, p0[2] * rsqrtf(r02))));
+  const float om0 = asinf(fminf(1.f, fmaxf(-1.f, p0[2] / sqrtf(r02))));
   float Sd = 0.f, Se = 0.f, Sdd = 0.f, See = 0.f, Sde = 0.f;
 #pragma unroll 1
   for (int k = 0; k < 3; ++k) {

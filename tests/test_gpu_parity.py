@@ -20,8 +20,9 @@ TOL_DEPTH = 1e-3
 # A23 flag margins: box edges (rad / px) at the measured GPU-vs-oracle box error bound,
 # alpha / T / tau thresholds at the float32 response error; box-edge flips only count when
 # the particle's alpha*T could move an output by more than a tenth of the tolerance.
-LIDAR_EPS = {"a": 1.2e-6, "b": 6e-7, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
-CAMERA_EPS = {"a": 5e-4, "b": 5e-4, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
+LIDAR_EPS = {"a": 1.2e-6, "b": 1e-6, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
+CAMERA_EPS = {"a": 5e-4, "b": 5e-4, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6, "amb_a": 20.0,
+              "amb_b": 20.0}
 # share of rays the oracle may flag in tier 2; config B traverses ~360 list entries per ray,
 # so its box-edge coincidences at a 1.2e-6 rad margin are ~0.5 %
 FLAG_BUDGET = {"default": 0.005, "B": 0.01}
