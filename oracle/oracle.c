@@ -1064,18 +1064,18 @@ int or_composite(int64_t n_gauss, const double* mu, const double* Mrows, const d
           int strict = in_interval_a_d(bx[0], bx[1], xa, p->wrap, -p->eps_a) &&
                        (double)bx[2] + p->eps_b <= xb && xb <= (double)bx[3] - p->eps_b;
           /* validity-ambiguous particles (gamb): the float32 box may differ a lot (e.g. a
-           * sigma point at the sweep seam) -> flag live rays inside a generously grown box */
-          if (gamb && gamb[g] && in_interval_a_d(bx[0], bx[1], xa, p->wrap, p->eps_amb_a) &&
-              (double)bx[2] - p->eps_amb_b <= xb && xb <= (double)bx[3] + p->eps_amb_b)
-            flag |= 8;
-          if (loose != strict) {
+           * sigma point at the sweep seam) -> candidates are the live rays inside a
+           * generously grown box; like box-edge flips they only count if they could matter */
+          const int amb_box = gamb && gamb[g] && in_interval_a_d(bx[0], bx[1], xa, p->wrap, p->eps_amb_a) &&
+                              (double)bx[2] - p->eps_amb_b <= xb && xb <= (double)bx[3] + p->eps_amb_b;
+          if (loose != strict || amb_box) {
             /* ambiguous membership matters only if this particle could composite with a
              * weight alpha T above the impact threshold (its alpha if it were a member) */
             double rs0[2];
             or_response(&mu[(int64_t)g * 3], &Mrows[(int64_t)g * 9], o, d, rs0);
             double a0 = sigma[g] * exp(-0.5 * rs0[1]);
             if (!(isfinite(a0)) || (a0 >= p->alpha_min - p->eps_alpha && a0 * T > p->eps_impact))
-              flag |= 1;
+              flag |= (loose != strict) ? 1 : 8;
           }
         }
         if (gamb && gamb[g] == 2) continue; /* listed for flagging only (oracle-invalid) */

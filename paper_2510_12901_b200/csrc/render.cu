@@ -1215,26 +1215,38 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v6(const LidarV2
         for (int w = 0; w < NP; ++w) cnt += __popc(S.memb[b][w][lane]);
         bool stopped = false;
         const int fast = min(cnt, kV6Cap);
-        int k = 0;
-        for (; k < fast; ++k) {
+        // phase 1: the transmittance chain only (weights written back in place); branch-free
+        // so the slot loads of later members are issued ahead of the chain
+        int stop_k = -1;
+#pragma unroll 4
+        for (int k = 0; k < fast; ++k) {
           const float2 a = S.at[b][lane][k];
-          if (a.y < A.near_tau || a.x < A.alpha_min) continue;
+          const bool take = !(a.y < A.near_tau || a.x < A.alpha_min) && stop_k < 0;
           const float Tn = T * (1.f - a.x);
-          if (Tn < A.T_min) {
-            stopped = true;
-            nv += S.ent[b][lane][k] + 1;
-            ni += k + 1;
-            break;
-          }
+          const bool term = take && Tn < A.T_min;
+          stop_k = term ? k : stop_k;
+          const bool comp = take && !term;
+          S.at[b][lane][k].x = comp ? a.x * T : 0.f;
+          T = comp ? Tn : T;
+        }
+        // phase 2: accumulate the weighted features / depths in member order
+        const int kend = stop_k >= 0 ? stop_k : fast;
+#pragma unroll 4
+        for (int k = 0; k < kend; ++k) {
+          const float2 wt = S.at[b][lane][k];
+          if (wt.x == 0.f) continue;  // skipped member (alpha < alpha_min or behind the origin)
           const float4 f = S.feat[b][S.ent[b][lane][k]];
-          const float wgt = a.x * T;
-          acc0 = fmaf(wgt, f.y, acc0);
-          acc1 = fmaf(wgt, f.z, acc1);
-          acc2 = fmaf(wgt, f.w, acc2);
-          D = fmaf(wgt, a.y, D);
-          W += wgt;
+          acc0 = fmaf(wt.x, f.y, acc0);
+          acc1 = fmaf(wt.x, f.z, acc1);
+          acc2 = fmaf(wt.x, f.w, acc2);
+          D = fmaf(wt.x, wt.y, D);
+          W += wt.x;
           ++ncontrib;
-          T = Tn;
+        }
+        if (stop_k >= 0) {
+          stopped = true;
+          nv += S.ent[b][lane][stop_k] + 1;
+          ni += stop_k + 1;
         }
         if (!stopped && cnt > kV6Cap) {
           // slow path: members beyond the ray's slot capacity, in list order
