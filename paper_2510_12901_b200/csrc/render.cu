@@ -1119,7 +1119,7 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v5(const LidarV2
 // dependent shared-memory lookups on the transmittance chain.  Rays with more than
 // kV6Cap members in one round take the rare slow path (walk the member words, response
 // from the record in global memory).
-constexpr int kV6Cap = 48;
+constexpr int kV6Cap = 32;
 
 template <int NP>
 struct V6Smem {
@@ -1136,6 +1136,7 @@ struct V6Smem {
   float col_phi[32], beam_el[32];
   int col_id[32], beam_id[32];
   int stop_at[2];
+  uint32_t done_mask[2];  // rays terminated by the end of the round that released buffer b
 };
 
 template <int NP>
@@ -1290,9 +1291,13 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v6(const LidarV2
           ni += cnt;
         }
       }
-      const bool all = __all_sync(0xffffffffu, done);
+      const uint32_t dmask = __ballot_sync(0xffffffffu, done);
+      const bool all = dmask == 0xffffffffu;
       if (r + 2 < n_rounds) {
-        if (lane == 0) S.stop_at[b] = all ? 1 : 0;
+        if (lane == 0) {
+          S.stop_at[b] = all ? 1 : 0;
+          S.done_mask[b] = dmask;
+        }
         __threadfence_block();
         named_arrive(BAR_EMPTY + b, NT);
       }
@@ -1342,11 +1347,13 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v6(const LidarV2
   issue(0, rg.x, load_id(0));
   uint32_t id_pf = load_id(1);
   named_sync(BAR_RAYS, NT);
+  uint32_t alive = 0xffffffffu;  // rays the consumer has not terminated (2 rounds behind)
   for (int r = 0; r < n_rounds; ++r) {
     const int b = r & 1;
     if (r >= 2) {
       named_sync(BAR_EMPTY + b, NT);
       if (S.stop_at[b]) break;
+      alive = ~S.done_mask[b];
     }
     const int start = rg.x + r * E;
     cp_async_wait0();
@@ -1376,6 +1383,7 @@ __global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v6(const LidarV2
           if (bx.z <= w && w <= bx.w) m |= colbits << (bi * nc);
         }
     }
+    m &= alive;  // no member pairs for terminated rays
     const uint32_t my = warp_transpose32(m, lane);  // lane r: entries of this warp holding ray r
     S.memb[b][warp][lane] = my;
     const int k = __popc(m);
