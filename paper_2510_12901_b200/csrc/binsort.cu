@@ -254,6 +254,7 @@ struct DupArgs {
   uint32_t* vals[2];
   uint32_t* hist;      // [kMaxPasses][256]
   int32_t* tile_cnt;   // [n_tiles]
+  int id_bits, packed; // packed: one u64 word = (key << id_bits) | id
 };
 
 __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
@@ -310,8 +311,12 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
     const uint64_t key = ((uint64_t)tile << b) | (uint64_t)s_key[lo];
     const int64_t pos = out0 + k;
     if (pos < A.capacity) {
-      kout[pos] = key;
-      vout[pos] = (uint32_t)(g0 + lo);
+      if (A.packed) {
+        kout[pos] = (key << A.id_bits) | (uint64_t)(g0 + lo);
+      } else {
+        kout[pos] = key;
+        vout[pos] = (uint32_t)(g0 + lo);
+      }
       for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * 256 + (int)((key >> (8 * p)) & 0xFF)], 1u);
     }
   }
@@ -327,6 +332,8 @@ struct SweepArgs {
   const int64_t* scal;
   int64_t capacity;
   int pass;
+  int id_bits;          // packed mode: low id_bits of every word are the particle id
+  uint32_t* ids_final;  // packed mode: the last pass also writes the ids here
   const uint32_t* hist;  // [256] of this pass
   uint32_t* status;      // [n_parts][256] of this pass
   uint32_t* counter;
@@ -341,13 +348,14 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A) {
+template <bool Packed>
+__global__ void __launch_bounds__(kSortThreads, Packed ? 5 : 4) k_onesweep(const SweepArgs A) {
   __shared__ uint32_t s_part;
   __shared__ uint32_t s_warp_hist[8][256];
   __shared__ uint32_t s_digit_excl[256];
   __shared__ uint32_t s_global[256];
   __shared__ uint64_t s_keys[kPart];
-  __shared__ uint32_t s_vals[kPart];
+  __shared__ uint32_t s_vals[Packed ? 1 : kPart];
   __shared__ int scratch[8];
   const int passes = (int)A.scal[S_PASSES];
   if (A.pass >= passes) return;  // grid-uniform: this digit is beyond the key width
@@ -364,7 +372,8 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A)
   const uint32_t* vals_in = A.vals[in];
   uint64_t* keys_out = A.keys[in ^ 1];
   uint32_t* vals_out = A.vals[in ^ 1];
-  const int shift = 8 * A.pass;
+  const int shift = 8 * A.pass + (Packed ? A.id_bits : 0);
+  const bool last = A.pass == passes - 1;
   const int64_t base = part * kPart;
   const int valid = (int)min((int64_t)kPart, P - base);
 
@@ -377,10 +386,10 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A)
     const int64_t idx = wbase + i * 32 + lane;
     if (idx < P) {
       k[i] = keys_in[idx];
-      v[i] = vals_in[idx];
+      if (!Packed) v[i] = vals_in[idx];
     } else {
       k[i] = ~0ull;  // padding: digit 0xFF, ranked after every real key of the partition
-      v[i] = 0;
+      if (!Packed) v[i] = 0;
     }
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -433,7 +442,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A)
     const uint32_t dd = (uint32_t)(k[i] >> shift) & 0xFFu;
     const uint32_t pos = s_digit_excl[dd] + s_warp_hist[warp][dd] + rank[i];
     s_keys[pos] = k[i];
-    s_vals[pos] = v[i];
+    if (!Packed) s_vals[pos] = v[i];
   }
   __syncthreads();
   for (int j = tid; j < valid; j += kSortThreads) {
@@ -441,16 +450,17 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A)
     const uint32_t dd = (uint32_t)(key >> shift) & 0xFFu;
     const int64_t out = (int64_t)s_global[dd] + (j - (int64_t)s_digit_excl[dd]);
     keys_out[out] = key;
-    vals_out[out] = s_vals[j];
+    if (!Packed) vals_out[out] = s_vals[j];
+    else if (last) A.ids_final[out] = (uint32_t)(key & ((1ull << A.id_bits) - 1ull));
   }
 }
 
 // ------------------------------------------------------------------ tile metadata
 // [begin, end) of every tile from the tile changes of the sorted keys (tile = key >> b)
 __global__ void k_ranges(const uint64_t* __restrict__ keys, const int64_t* __restrict__ scal, int64_t capacity,
-                         int2* __restrict__ ranges) {
+                         int id_bits, int2* __restrict__ ranges) {
   const int64_t P = min(scal[S_P], capacity);
-  const int b = (int)scal[S_B];
+  const int b = (int)scal[S_B] + id_bits;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t t = (uint32_t)(keys[i] >> b);
     if (i == 0 || (uint32_t)(keys[i - 1] >> b) != t) ranges[t].x = (int)i;
@@ -490,13 +500,13 @@ __global__ void __launch_bounds__(1024) k_tile_order(const int2* __restrict__ ra
 
 // (tile << 32 | depth bits) from the trimmed keys
 __global__ void k_keys64(const uint64_t* __restrict__ keys, const int64_t* __restrict__ scal, int64_t capacity,
-                         uint64_t* __restrict__ out) {
+                         int id_bits, uint64_t* __restrict__ out) {
   const int64_t P = min(scal[S_P], capacity);
   const int b = (int)scal[S_B];
   const uint32_t kmin = (uint32_t)scal[S_KMIN];
   const uint64_t mask = b >= 64 ? ~0ull : ((1ull << b) - 1ull);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
+    const uint64_t k = keys[i] >> id_bits;
     out[i] = ((k >> b) << 32) | (uint64_t)((uint32_t)(k & mask) + kmin);
   }
 }
@@ -564,23 +574,32 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
       cudaMemsetAsync(w.status, 0, sizeof(uint32_t) * (size_t)max_passes * w.parts * 256, st) != cudaSuccess)
     return check("memset status");
   uint32_t* vals[2] = {sorted_ids, w.vals_alt};
+  // packed mode: depth-key span b <= 31 bits (positive floats), so one u64 word holds
+  // (tile << b | depth - min) << id_bits | id whenever 31 + tile bits + id bits <= 64
+  int id_bits = 1;
+  while (id_bits < 31 && (1ll << id_bits) < n) ++id_bits;
+  const bool packed = 31 + tbits + id_bits <= 64;
   if (nb > 0 && cap > 0) {
     DupArgs D{proj->tile_count, reinterpret_cast<const int4*>(proj->tile_rect), proj->depth_key, n, cap,
-              w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, w.tile_cnt};
+              w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, w.tile_cnt,
+              id_bits, packed ? 1 : 0};
     k_duplicate<<<(unsigned)nb, kDupThreads, 0, st>>>(D);
     if (int32_t e = check("duplicate")) return e;
     for (int p = 0; p < max_passes; ++p) {
-      SweepArgs S{{w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.scal, cap, p, w.hist + p * 256,
-                  w.status + (size_t)p * w.parts * 256, w.counters + p};
-      k_onesweep<<<(unsigned)w.parts, kSortThreads, 0, st>>>(S);
+      SweepArgs S{{w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.scal, cap, p, id_bits, sorted_ids,
+                  w.hist + p * 256, w.status + (size_t)p * w.parts * 256, w.counters + p};
+      if (packed) k_onesweep<true><<<(unsigned)w.parts, kSortThreads, 0, st>>>(S);
+      else k_onesweep<false><<<(unsigned)w.parts, kSortThreads, 0, st>>>(S);
     }
     if (int32_t e = check("onesweep")) return e;
   }
+  const int key_shift = packed ? id_bits : 0;
   if (cudaMemsetAsync(tile_ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, st) != cudaSuccess)
     return check("memset ranges");
-  if (cap > 0) k_ranges<<<148 * 8, 256, 0, st>>>(w.keys[0], w.scal, cap, reinterpret_cast<int2*>(tile_ranges));
+  if (cap > 0)
+    k_ranges<<<148 * 8, 256, 0, st>>>(w.keys[0], w.scal, cap, key_shift, reinterpret_cast<int2*>(tile_ranges));
   if (tile_order)
     k_tile_order<<<1, 1024, 0, st>>>(reinterpret_cast<const int2*>(tile_ranges), n_tiles, tile_order);
-  if (sorted_keys && cap > 0) k_keys64<<<148 * 4, 256, 0, st>>>(w.keys[0], w.scal, cap, sorted_keys);
+  if (sorted_keys && cap > 0) k_keys64<<<148 * 4, 256, 0, st>>>(w.keys[0], w.scal, cap, key_shift, sorted_keys);
   return check("tile metadata");
 }
