@@ -230,6 +230,7 @@ def run_gpu(args):
     scene_np = synth.scene_for("B")  # same seed on every rank: replicated scene
     scene = SM.to_device_scene(scene_np, dev)
     r = SM.LidarRenderer(cfg, scene, device=dev)
+    r.keep_keys = False  # the renderer reads only the sorted ids
     n_total = (args.steps + args.warmup) * ws
     my = shard_poses(n_total, ws, rank)
     # size the pair buffers once (one sync), with head room for every pose of the shard

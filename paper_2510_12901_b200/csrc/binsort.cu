@@ -37,6 +37,8 @@ constexpr int kDupItems = 4;
 constexpr int kDupBlock = kDupThreads * kDupItems;
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 12;
+constexpr int kLookW = 8;      // look-back window (predecessor partitions loaded per round trip)
+constexpr int kRankBatch = 4;  // ranking items whose match.any latencies overlap
 constexpr int kPart = kSortThreads * kSortItems;
 constexpr int kMaxPasses = 6;  // 48 key bits: 16 tile bits + 32 depth bits at most
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
@@ -269,8 +271,8 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
   const int b = (int)A.scal[S_B];
   const uint32_t kmin = (uint32_t)A.scal[S_KMIN];
   const int s0 = passes & 1;  // output buffer parity so the last pass lands in buffer 0
-  uint64_t* kout = A.keys[s0];
-  uint32_t* vout = A.vals[s0];
+  uint64_t* kout = s0 ? A.keys[1] : A.keys[0];
+  uint32_t* vout = s0 ? A.vals[1] : A.vals[0];
   for (int i = tid; i < passes * 256; i += kDupThreads) s_hist[i] = 0;
   int c[kDupItems], run = 0;
 #pragma unroll
@@ -349,7 +351,7 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
 }
 
 template <bool Packed>
-__global__ void __launch_bounds__(kSortThreads, Packed ? 5 : 4) k_onesweep(const SweepArgs A) {
+__global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A) {
   __shared__ uint32_t s_part;
   __shared__ uint32_t s_warp_hist[8][256];
   __shared__ uint32_t s_digit_excl[256];
@@ -360,18 +362,22 @@ __global__ void __launch_bounds__(kSortThreads, Packed ? 5 : 4) k_onesweep(const
   const int passes = (int)A.scal[S_PASSES];
   if (A.pass >= passes) return;  // grid-uniform: this digit is beyond the key width
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t P = min(A.scal[S_P], A.capacity);
+  const int64_t n_parts = (P + kPart - 1) / kPart;
+  // the grid is sized for the capacity; exactly the first n_parts CTAs take a partition
+  // number from the counter, so every partition is claimed once
+  if ((int64_t)blockIdx.x >= n_parts) return;
   if (tid == 0) s_part = atomicAdd(A.counter, 1u);
   for (int i = tid; i < 8 * 256; i += kSortThreads) (&s_warp_hist[0][0])[i] = 0;
   __syncthreads();
-  const int64_t P = min(A.scal[S_P], A.capacity);
-  const int64_t n_parts = (P + kPart - 1) / kPart;
   const int64_t part = s_part;
-  if (part >= n_parts) return;
   const int in = ((passes & 1) + A.pass) & 1;
-  const uint64_t* keys_in = A.keys[in];
-  const uint32_t* vals_in = A.vals[in];
-  uint64_t* keys_out = A.keys[in ^ 1];
-  uint32_t* vals_out = A.vals[in ^ 1];
+  // selects, not A.keys[in]: a dynamic index into the parameter struct would copy it to
+  // local memory
+  const uint64_t* keys_in = in ? A.keys[1] : A.keys[0];
+  const uint32_t* vals_in = in ? A.vals[1] : A.vals[0];
+  uint64_t* keys_out = in ? A.keys[0] : A.keys[1];
+  uint32_t* vals_out = in ? A.vals[0] : A.vals[1];
   const int shift = 8 * A.pass + (Packed ? A.id_bits : 0);
   const bool last = A.pass == passes - 1;
   const int64_t base = part * kPart;
@@ -393,17 +399,28 @@ __global__ void __launch_bounds__(kSortThreads, Packed ? 5 : 4) k_onesweep(const
     }
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
+  // warp multisplit: lanes with equal digits (match.any), the highest of them bumps the
+  // warp's digit counter once and broadcasts the previous value.  Items go in batches of
+  // kRankBatch so the match latencies overlap; the counter updates stay in item order
+  // (one warp's shared-memory atomics execute in program order), which keeps the sort stable.
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
-    // warp multisplit: lanes with equal digits (match.any), the highest of them bumps the
-    // warp's digit counter once and broadcasts the previous value
-    const uint32_t d = (uint32_t)(k[i] >> shift) & 0xFFu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const int leader = 31 - __clz(peers);
-    uint32_t prev = 0;
-    if (lane == leader) prev = atomicAdd(&s_warp_hist[warp][d], (uint32_t)__popc(peers));
-    prev = __shfl_sync(0xffffffffu, prev, leader);
-    rank[i] = prev + __popc(peers & lt_mask);
+  for (int i0 = 0; i0 < kSortItems; i0 += kRankBatch) {
+    uint32_t peers[kRankBatch], dg[kRankBatch], prev[kRankBatch];
+#pragma unroll
+    for (int j = 0; j < kRankBatch; ++j) {
+      dg[j] = (uint32_t)(k[i0 + j] >> shift) & 0xFFu;
+      peers[j] = __match_any_sync(0xffffffffu, dg[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < kRankBatch; ++j) {
+      prev[j] = 0;
+      if (lane == 31 - __clz(peers[j])) prev[j] = atomicAdd(&s_warp_hist[warp][dg[j]], (uint32_t)__popc(peers[j]));
+    }
+#pragma unroll
+    for (int j = 0; j < kRankBatch; ++j) {
+      prev[j] = __shfl_sync(0xffffffffu, prev[j], 31 - __clz(peers[j]));
+      rank[i0 + j] = prev[j] + __popc(peers[j] & lt_mask);
+    }
   }
   __syncthreads();
   const int d = tid;
@@ -425,13 +442,29 @@ __global__ void __launch_bounds__(kSortThreads, Packed ? 5 : 4) k_onesweep(const
   const int hex = block_excl_scan256((int)A.hist[d], scratch, &htot);
   uint32_t excl = 0;
   if (part > 0) {
+    // windowed look-back: kLookW predecessors are loaded at once (independent loads, one
+    // round trip), then consumed in order up to the first inclusive prefix or the first
+    // partition that has not published yet (retried from there)
     int64_t p = part - 1;
     while (true) {
-      const uint32_t s = ld_relaxed(A.status + p * 256 + d);
-      if ((s & ~kValMask) == 0) continue;  // not yet published
-      excl += s & kValMask;
-      if ((s & ~kValMask) == kFlagInc) break;
-      --p;
+      uint32_t s[kLookW];
+#pragma unroll
+      for (int w = 0; w < kLookW; ++w) s[w] = (p - w >= 0) ? ld_relaxed(A.status + (p - w) * 256 + d) : 0u;
+      int adv = 0;
+      bool done = false;
+#pragma unroll
+      for (int w = 0; w < kLookW; ++w) {
+        if (adv == w && !done) {
+          const uint32_t f = s[w] & ~kValMask;
+          if (f != 0) {
+            excl += s[w] & kValMask;
+            ++adv;
+            done = (f == kFlagInc);
+          }
+        }
+      }
+      if (done) break;
+      p -= adv;
     }
     st_relaxed(st, kFlagInc | (excl + cnt_pub));
   }
