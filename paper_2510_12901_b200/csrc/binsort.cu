@@ -238,7 +238,8 @@ __global__ void __launch_bounds__(1024) k_count_top(int64_t* __restrict__ block_
     scal[S_KMIN] = kmin;
     scal[S_KMAX] = kmax;
     scal[S_B] = b;
-    scal[S_PASSES] = carry > 0 ? (b + tile_bits + 7) / 8 : 0;
+    // at least one pass whenever there are pairs: it also writes the ids
+    scal[S_PASSES] = carry > 0 ? max(1, (b + tile_bits + 7) / 8) : 0;
     scal[S_TBITS] = tile_bits;
   }
 }

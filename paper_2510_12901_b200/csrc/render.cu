@@ -1140,7 +1140,7 @@ struct V6Smem {
 };
 
 template <int NP>
-__global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v6(const LidarV2Args A) {
+__global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lidar_v6(const LidarV2Args A) {
   constexpr int E = 32 * NP;
   constexpr int NT = 32 * (NP + 1);
   constexpr int BAR_PROD = 1, BAR_FULL = 2, BAR_EMPTY = 4, BAR_RAYS = 6;
