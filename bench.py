@@ -56,57 +56,74 @@ def read_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML thread polling
+    every 2 ms (the timed region of a default run is a few hundred ms, too short for
+    ``nvidia-smi -lms``); falls back to ``nvidia-smi -lms 100`` if NVML is unavailable."""
 
-    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap", "clocks_event_reasons.gpu_idle"]
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.stop_ev = threading.Event()
+        self.thread = None
+        self.nvml = None
+
+    def _poll(self):
+        n, h = self.nvml
+        smax = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append((n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM), smax,
+                                     n.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            import pynvml as n
+            n.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
+            self.nvml = (n, n.nvmlDeviceGetHandleByIndex(idx))
+            self.thread = threading.Thread(target=self._poll, daemon=True)
         except Exception:
-            self.proc = None
+            self.nvml = None
+            self.thread = threading.Thread(target=self._smi, daemon=True)
+        self.thread.start()
+        time.sleep(0.01)
 
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
-
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        time.sleep(0.25)
-        self.proc.terminate()
+    def _smi(self):
         try:
-            self.proc.wait(timeout=2)
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                                  "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "100"],
+                                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
-            self.proc.kill()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap", "gpu_idle"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
+            return
+        while not self.stop_ev.is_set():
+            ln = p.stdout.readline()
+            if not ln:
+                break
             try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
+                a, b, c = [x.strip() for x in ln.split(",")]
+                self.samples.append((float(a), float(b), int(c, 16)))
             except ValueError:
                 continue
-            for name, val in zip(names, parts[2:]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
-        busy = [s for s in sm] or [float("nan")]
-        return {"sm_mhz": statistics.median(busy) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        p.terminate()
+
+    def stop(self):
+        self.stop_ev.set()
+        if self.thread is not None:
+            self.thread.join(timeout=3)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for _, _, m in self.samples for name, bit in self.REASONS if m & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "sm_mhz_min": min(sm), "reasons": reasons, "samples": len(sm),
+                "source": "nvml 2 ms" if self.nvml else "nvidia-smi 100 ms"}
 
 
 def dist_env():
@@ -345,8 +362,7 @@ def run_gpu(args):
             "scans_per_s": value / r.n_rays,
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "stages": roof, "counters": counters, "job_counters": job_counters,
-            "clocks": {"sm_mhz": clk["sm_mhz"], "sm_max_mhz": clk["sm_max_mhz"], "reasons": clk["reasons"],
-                       "samples": clk["samples"]},
+            "clocks": clk,
             "wall_s_timed_region": wall}
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene_np, cfg)
@@ -372,8 +388,8 @@ def cpu_baseline(scene_np, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

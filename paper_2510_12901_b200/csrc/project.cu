@@ -89,6 +89,7 @@ struct ProjArgs {
   float az_start, r_min;
   int dir;
   float R0[9], t0w[3], dtw[3], v[3], axis[3], theta;  // start pose, motion, rotation axis / angle
+  double R0d[9], t0d[3], vd[3], axis_d[3], theta_d;  // the same in double (sigma point 0)
   int small_rot;
   int n_phi, n_theta, rows_per_tile, az_cells, sat_cols, enable_cull;
   float pi_f, two_pi_f, az_tile_scale, az_cell_scale;
@@ -129,126 +130,182 @@ __device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c
 // ---- LiDAR sensor model (Eq. 3) with the firing-time fixed point (A3, A5).
 // A point's sensor-frame position at firing time s is
 //   p(s) = R(s)^T (x - t(s)) = E(s)^T (q - s v),   q = R0^T (x - t0), v = R0^T (t1 - t0),
-// with R(s) = R0 E(s), E(s) = Exp(s theta k) (k the unit axis of R0^T R1), so per sigma point
-// only E(s)^T y = y - sin(a) (k x y) + (1 - cos a)(k (k.y) - y), a = s theta, is evaluated
-// (the start pose R0, t0 and v are launch constants).
-__device__ __forceinline__ void rot_apply_t(const ProjArgs& A, float s, const float y[3], float p[3]) {
+// with R(s) = R0 E(s), E(s) = Exp(s theta k) (k the unit axis of R0^T R1); the start pose
+// R0, t0 and v are launch constants, and
+//   E(s)^T y = y - sin(a) (k x y) + (1 - cos a)(k (k.y) - y),   a = s theta.
+//
+// Precision split.  The box edges are the interface values every membership
+// decision compares against, so their ABSOLUTE position must match the double oracle to well
+// under one float32 ulp: sigma point 0 (the particle mean) is carried in double -- start-frame
+// coordinates, the rotation to its firing time, its azimuth and elevation.  The other six
+// sigma points are carried as float32 OFFSETS from sigma point 0,
+//   p_i = E(ds)^T (p0 + w),  w = E(s0)^T (l_i - ds v),  ds = s_i - s0,
+//   p_i - p0 = w + G(ds)(p0 + w),  G(a) y = -sin(a theta)(k x y) + (1 - cos a theta)(k (k.y) - y),
+// which never forms the difference of two rounded 100 m positions, and their azimuth /
+// elevation offsets are taken from the offsets directly (atan of a cancellation-free ratio).
+// Firing times are decisions of float32 accuracy only (an error of 1e-7 in s moves a point by
+// < 1e-9 rad), so they stay in float32.
+
+// sin(a theta), 1 - cos(a theta) in double (Taylor for |a theta| <= 0.5: truncation < 1e-16)
+__device__ __forceinline__ void rot_sc_d(const ProjArgs& A, double s, double* sn, double* omc) {
+  const double a = s * A.theta_d;
+  if (A.small_rot) {
+    const double a2 = a * a;
+    *sn = a * (1. - a2 * (1. / 6.) * (1. - a2 * (1. / 20.) * (1. - a2 * (1. / 42.) * (1. - a2 * (1. / 72.) *
+                                                 (1. - a2 * (1. / 110.) * (1. - a2 * (1. / 156.)))))));
+    *omc = 0.5 * a2 * (1. - a2 * (1. / 12.) * (1. - a2 * (1. / 30.) * (1. - a2 * (1. / 56.) * (1. - a2 * (1. / 90.) *
+                                                 (1. - a2 * (1. / 132.) * (1. - a2 * (1. / 182.)))))));
+  } else {
+    double sh, ch;
+    sincos(0.5 * a, &sh, &ch);
+    *sn = 2. * sh * ch;
+    *omc = 2. * sh * sh;
+  }
+}
+
+// sin(a theta), 1 - cos(a theta) in float (Taylor for |a theta| <= 0.5: error < 1e-10)
+__device__ __forceinline__ void rot_sc_f(const ProjArgs& A, float s, float* sn, float* omc) {
   const float a = s * A.theta;
-  float sn, omc;
-  if (A.small_rot) {  // |a| <= 0.5: Taylor to a^9 / a^10 (error < 1e-10)
+  if (fabsf(a) <= 0.5f) {
     const float a2 = a * a;
-    sn = a * (1.f - a2 * (1.f / 6.f) * (1.f - a2 * (1.f / 20.f) * (1.f - a2 * (1.f / 42.f))));
-    omc = 0.5f * a2 * (1.f - a2 * (1.f / 12.f) * (1.f - a2 * (1.f / 30.f) * (1.f - a2 * (1.f / 56.f))));
+    *sn = a * (1.f - a2 * (1.f / 6.f) * (1.f - a2 * (1.f / 20.f) * (1.f - a2 * (1.f / 42.f))));
+    *omc = 0.5f * a2 * (1.f - a2 * (1.f / 12.f) * (1.f - a2 * (1.f / 30.f) * (1.f - a2 * (1.f / 56.f))));
   } else {
     float sh, ch;
     sincosf(0.5f * a, &sh, &ch);
-    sn = 2.f * sh * ch;
-    omc = 2.f * sh * sh;
+    *sn = 2.f * sh * ch;
+    *omc = 2.f * sh * sh;
   }
-  const float* k = A.axis;
-  const float cx = k[1] * y[2] - k[2] * y[1], cy = k[2] * y[0] - k[0] * y[2], cz = k[0] * y[1] - k[1] * y[0];
-  const float kd = k[0] * y[0] + k[1] * y[1] + k[2] * y[2];
+}
+
+// y - sn (k x y) + omc (k (k.y) - y), k = rotation axis  (E^T y for (sn, omc) of +a)
+template <typename T>
+__device__ __forceinline__ void rot_apply(const T k[3], T sn, T omc, const T y[3], T p[3]) {
+  const T cx = k[1] * y[2] - k[2] * y[1], cy = k[2] * y[0] - k[0] * y[2], cz = k[0] * y[1] - k[1] * y[0];
+  const T kd = k[0] * y[0] + k[1] * y[1] + k[2] * y[2];
   p[0] = y[0] - sn * cx + omc * (k[0] * kd - y[0]);
   p[1] = y[1] - sn * cy + omc * (k[1] * kd - y[1]);
   p[2] = y[2] - sn * cz + omc * (k[2] * kd - y[2]);
 }
 
-// Azimuth of b relative to a, atan2(a x b, a . b) in (-pi, pi] (the A21 unwrap about a).
-// Small relative angles (all but the largest / nearest particles) use the odd series of
-// atan to t^11 (|t| <= 0.2: truncation < 1e-10 rad); the rest fall back to atan2f.
-__device__ __forceinline__ float rel_azimuth(const float a[3], const float b[3]) {
-  const float cr = a[0] * b[1] - a[1] * b[0];
-  const float dt = a[0] * b[0] + a[1] * b[1];
-  if (dt > 0.f && fabsf(cr) <= 0.2f * dt) {
-    const float t = __fdividef(cr, dt), t2 = t * t;
+// atan(t) for |t| <= 0.2 by the odd series to t^11 (truncation < 1e-10); else atan2f
+__device__ __forceinline__ float atan_ratio(float num, float den) {
+  if (den > 0.f && fabsf(num) <= 0.2f * den) {
+    const float t = __fdividef(num, den), t2 = t * t;
     return t * (1.f - t2 * (1.f / 3.f - t2 * (1.f / 5.f - t2 * (1.f / 7.f - t2 * (1.f / 9.f - t2 * (1.f / 11.f))))));
   }
-  return atan2f(cr, dt);
+  return atan2f(num, den);
 }
 
 __device__ __forceinline__ float wrap01(float s) { return s < 0.f ? s + 1.f : (s >= 1.f ? s - 1.f : s); }
 
-// sensor-frame position of the sigma point with start-pose coordinates q at its own firing
-// time (K fixed-point updates of s from s = 0); *s_out = the firing time used
-__device__ __forceinline__ void lidar_fire(const ProjArgs& A, const float q[3], float p[3], float* s_out) {
-  p[0] = q[0];
-  p[1] = q[1];
-  p[2] = q[2];
-  float s = 0.f;
-  if (!A.pose.same) {
-    const float inv2pi = 0.15915494309189535f;
-    for (int it = 0; it < A.K; ++it) {
-      const float phi = atan2f(p[1], p[0]);
-      float a = (float)A.dir * (phi - A.az_start);
-      a = a - 6.283185307179586f * floorf(a * inv2pi);
-      s = fminf(fmaxf(a * inv2pi, 0.f), 1.f);
-      const float y[3] = {q[0] - s * A.v[0], q[1] - s * A.v[1], q[2] - s * A.v[2]};
-      rot_apply_t(A, s, y, p);
-    }
-  }
-  *s_out = s;
+// firing time of a sensor-frame position (A5): wrap(dir (phi - phi_start)) / 2 pi, clamped
+__device__ __forceinline__ float fire_time(const ProjArgs& A, float px, float py) {
+  const float inv2pi = 0.15915494309189535f;
+  float a = (float)A.dir * (atan2f(py, px) - A.az_start);
+  a = a - 6.283185307179586f * floorf(a * inv2pi);
+  return fminf(fmaxf(a * inv2pi, 0.f), 1.f);
 }
 
-// UT moments of the 7 projected sigma points in (azimuth, elevation) (Eq. 3), online.
-// Azimuths are taken relative to sigma point 0 as atan2(p0 x p_i, p0 . p_i) (the unwrap of
-// A21, cancellation-free); *a0 = azimuth of sigma point 0; ma, mb = UT mean offsets
-// (mb absolute); caa, cab, cbb = UT covariance; s0 = firing time of sigma point 0.
-__device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[3], const float L[3][3], float* a0,
-                                              float* ma, float* mb, float* caa, float* cab, float* cbb, float* s0,
-                                              bool* valid) {
-  const float* R0 = A.R0;
-  const float d0 = mu[0] - A.t0w[0], d1 = mu[1] - A.t0w[1], d2 = mu[2] - A.t0w[2];
-  const float c[3] = {R0[0] * d0 + R0[3] * d1 + R0[6] * d2, R0[1] * d0 + R0[4] * d1 + R0[7] * d2,
-                      R0[2] * d0 + R0[5] * d1 + R0[8] * d2};
-  // firing times: K = 1 fixed-point step from s = 0 evaluated in the start frame, with the
-  // sigma points' azimuths taken relative to sigma point 0 (one atan2f per particle)
+// UT moments of the 7 projected sigma points in (azimuth, elevation) (Eq. 3).
+// Outputs: *a0, *e0 = azimuth / elevation of sigma point 0 (double); ma, me = UT mean offsets
+// from them (azimuth unwrapped about sigma point 0, A21); caa, cab, cbb = UT covariance;
+// s0 = firing time of sigma point 0.
+__device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[3], const float L[3][3], double* a0,
+                                              double* e0, float* ma, float* me, float* caa, float* cab, float* cbb,
+                                              float* s0, bool* valid) {
+  const double* R0 = A.R0d;
+  const double d0 = (double)mu[0] - A.t0d[0], d1 = (double)mu[1] - A.t0d[1], d2 = (double)mu[2] - A.t0d[2];
+  const double cd[3] = {R0[0] * d0 + R0[3] * d1 + R0[6] * d2, R0[1] * d0 + R0[4] * d1 + R0[7] * d2,
+                        R0[2] * d0 + R0[5] * d1 + R0[8] * d2};
+  const float c[3] = {(float)cd[0], (float)cd[1], (float)cd[2]};
   const bool moving = !A.pose.same && A.K >= 1;
-  const float inv2pi = 0.15915494309189535f;
+  // ---- firing time of sigma point 0 (float32 decisions; K fixed-point steps from s = 0)
   float s_c = 0.f;
   if (moving) {
-    float a = (float)A.dir * (atan2f(c[1], c[0]) - A.az_start);
-    a = a - 6.283185307179586f * floorf(a * inv2pi);
-    s_c = fminf(fmaxf(a * inv2pi, 0.f), 1.f);
+    s_c = fire_time(A, c[0], c[1]);
+    for (int it = 1; it < A.K; ++it) {
+      float sn, omc, p[3];
+      rot_sc_f(A, s_c, &sn, &omc);
+      const float y[3] = {c[0] - s_c * A.v[0], c[1] - s_c * A.v[1], c[2] - s_c * A.v[2]};
+      rot_apply(A.axis, sn, omc, y, p);
+      s_c = fire_time(A, p[0], p[1]);
+    }
   }
-  auto fire = [&](const float q[3], float s, float p[3]) {
-    if (!moving) {
-      p[0] = q[0]; p[1] = q[1]; p[2] = q[2];
-      return;
-    }
-    const float y[3] = {q[0] - s * A.v[0], q[1] - s * A.v[1], q[2] - s * A.v[2]};
-    rot_apply_t(A, s, y, p);
-    for (int it = 1; it < A.K; ++it) {  // further fixed-point steps (K > 1)
-      float a = (float)A.dir * (atan2f(p[1], p[0]) - A.az_start);
-      a = a - 6.283185307179586f * floorf(a * inv2pi);
-      s = fminf(fmaxf(a * inv2pi, 0.f), 1.f);
-      const float y2[3] = {q[0] - s * A.v[0], q[1] - s * A.v[1], q[2] - s * A.v[2]};
-      rot_apply_t(A, s, y2, p);
-    }
-  };
-  float p0[3];
-  fire(c, s_c, p0);
   *s0 = s_c;
-  const float r02 = p0[0] * p0[0] + p0[1] * p0[1] + p0[2] * p0[2];
-  bool ok = r02 >= A.r_min * A.r_min;
-  *a0 = atan2f(p0[1], p0[0]);
-  const float om0 = asinf(fminf(1.f, fmaxf(-1.f, p0[2] / sqrtf(r02))));
+  // ---- sigma point 0 in double
+  double p0d[3] = {cd[0], cd[1], cd[2]};
+  float E[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};  // E(s0)^T, row-major
+  if (moving) {
+    double sn, omc;
+    rot_sc_d(A, (double)s_c, &sn, &omc);
+    const double y[3] = {cd[0] - (double)s_c * A.vd[0], cd[1] - (double)s_c * A.vd[1],
+                         cd[2] - (double)s_c * A.vd[2]};
+    rot_apply(A.axis_d, sn, omc, y, p0d);
+    const float* k = A.axis;
+    const float fs = (float)sn, fo = (float)omc;
+    // E^T = I - sn [k]x + omc (k k^T - I)
+    E[0] = 1.f + fo * (k[0] * k[0] - 1.f); E[1] = fs * k[2] + fo * k[0] * k[1]; E[2] = -fs * k[1] + fo * k[0] * k[2];
+    E[3] = -fs * k[2] + fo * k[1] * k[0]; E[4] = 1.f + fo * (k[1] * k[1] - 1.f); E[5] = fs * k[0] + fo * k[1] * k[2];
+    E[6] = fs * k[1] + fo * k[2] * k[0]; E[7] = -fs * k[0] + fo * k[2] * k[1]; E[8] = 1.f + fo * (k[2] * k[2] - 1.f);
+  }
+  const double rho0d = sqrt(p0d[0] * p0d[0] + p0d[1] * p0d[1]);
+  *a0 = atan2(p0d[1], p0d[0]);
+  *e0 = atan2(p0d[2], rho0d);
+  const float p0[3] = {(float)p0d[0], (float)p0d[1], (float)p0d[2]};
+  const float rho0 = (float)rho0d, rho02 = (float)(rho0d * rho0d);
+  bool ok = rho0d * rho0d + p0d[2] * p0d[2] >= (double)A.r_min * (double)A.r_min;
   float Sd = 0.f, Se = 0.f, Sdd = 0.f, See = 0.f, Sde = 0.f;
 #pragma unroll 1
   for (int k = 0; k < 3; ++k) {
-    const float lr[3] = {R0[0] * L[k][0] + R0[3] * L[k][1] + R0[6] * L[k][2],
-                         R0[1] * L[k][0] + R0[4] * L[k][1] + R0[7] * L[k][2],
-                         R0[2] * L[k][0] + R0[5] * L[k][1] + R0[8] * L[k][2]};
+    // l_k in the start frame
+    const float lr[3] = {A.R0[0] * L[k][0] + A.R0[3] * L[k][1] + A.R0[6] * L[k][2],
+                         A.R0[1] * L[k][0] + A.R0[4] * L[k][1] + A.R0[7] * L[k][2],
+                         A.R0[2] * L[k][0] + A.R0[5] * L[k][1] + A.R0[8] * L[k][2]};
 #pragma unroll
     for (int sg = 0; sg < 2; ++sg) {
-      const float q[3] = {sg ? c[0] - lr[0] : c[0] + lr[0], sg ? c[1] - lr[1] : c[1] + lr[1],
-                          sg ? c[2] - lr[2] : c[2] + lr[2]};
-      const float s = moving ? wrap01(s_c + (float)A.dir * rel_azimuth(c, q) * inv2pi) : 0.f;
-      float p[3];
-      fire(q, s, p);
-      const float r2 = p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
-      ok = ok && r2 >= A.r_min * A.r_min;
-      const float d = rel_azimuth(p0, p);
-      const float e = asinf(fminf(1.f, fmaxf(-1.f, p[2] * rsqrtf(r2)))) - om0;
+      const float l[3] = {sg ? -lr[0] : lr[0], sg ? -lr[1] : lr[1], sg ? -lr[2] : lr[2]};
+      float D[3];  // p_i - p0
+      if (!moving) {
+        D[0] = l[0]; D[1] = l[1]; D[2] = l[2];
+      } else {
+        // firing time of sigma point i (float32): start-frame azimuth relative to sigma point 0's
+        const float q[3] = {c[0] + l[0], c[1] + l[1], c[2] + l[2]};
+        float s = wrap01(s_c + (float)A.dir * atan_ratio(c[0] * q[1] - c[1] * q[0], c[0] * q[0] + c[1] * q[1]) *
+                                   0.15915494309189535f);
+        for (int it = 1; it < A.K; ++it) {
+          float sn, omc, p[3];
+          rot_sc_f(A, s, &sn, &omc);
+          const float y[3] = {q[0] - s * A.v[0], q[1] - s * A.v[1], q[2] - s * A.v[2]};
+          rot_apply(A.axis, sn, omc, y, p);
+          s = fire_time(A, p[0], p[1]);
+        }
+        const float ds = s - s_c;
+        const float y[3] = {l[0] - ds * A.v[0], l[1] - ds * A.v[1], l[2] - ds * A.v[2]};
+        const float w[3] = {E[0] * y[0] + E[1] * y[1] + E[2] * y[2], E[3] * y[0] + E[4] * y[1] + E[5] * y[2],
+                            E[6] * y[0] + E[7] * y[1] + E[8] * y[2]};
+        float sn, omc;
+        rot_sc_f(A, ds, &sn, &omc);
+        const float z[3] = {p0[0] + w[0], p0[1] + w[1], p0[2] + w[2]};
+        const float* kk = A.axis;
+        const float cx = kk[1] * z[2] - kk[2] * z[1], cy = kk[2] * z[0] - kk[0] * z[2], cz = kk[0] * z[1] - kk[1] * z[0];
+        const float kd = kk[0] * z[0] + kk[1] * z[1] + kk[2] * z[2];
+        D[0] = w[0] - sn * cx + omc * (kk[0] * kd - z[0]);
+        D[1] = w[1] - sn * cy + omc * (kk[1] * kd - z[1]);
+        D[2] = w[2] - sn * cz + omc * (kk[2] * kd - z[2]);
+      }
+      const float pz = p0[2] + D[2];
+      const float xy = p0[0] * D[0] + p0[1] * D[1];
+      const float dxy2 = D[0] * D[0] + D[1] * D[1];
+      const float rho2 = rho02 + (2.f * xy + dxy2);
+      ok = ok && rho2 + pz * pz >= A.r_min * A.r_min;
+      // azimuth offset: atan2(p0 x p_i, p0 . p_i) in the xy plane (A21 unwrap about p0)
+      const float d = atan_ratio(p0[0] * D[1] - p0[1] * D[0], rho02 + xy);
+      // elevation offset: atan2(pz_i rho0 - pz0 rho_i, rho_i rho0 + pz_i pz0) with
+      // rho_i - rho0 = (2 p0.D + |D|^2) / (rho_i + rho0)
+      const float rho = sqrtf(rho2);
+      const float drho = __fdividef(2.f * xy + dxy2, rho + rho0);
+      const float e = atan_ratio(D[2] * rho0 - p0[2] * drho, rho * rho0 + pz * p0[2]);
       Sd += d;
       Se += e;
       Sdd = fmaf(d, d, Sdd);
@@ -259,7 +316,7 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
   // sigma point 0 has offset 0; w_m = (wm0, wmi x 6), w_c = (wc0, wci x 6)
   const float m_a = A.ut.wmi * Sd, m_e = A.ut.wmi * Se;
   *ma = m_a;
-  *mb = om0 + m_e;
+  *me = m_e;
   *caa = A.ut.wc0 * m_a * m_a + A.ut.wci * (Sdd - 2.f * m_a * Sd + 6.f * m_a * m_a);
   *cbb = A.ut.wc0 * m_e * m_e + A.ut.wci * (See - 2.f * m_e * Se + 6.f * m_e * m_e);
   *cab = A.ut.wc0 * m_a * m_e + A.ut.wci * (Sde - m_a * Se - m_e * Sd + 6.f * m_a * m_e);
@@ -313,6 +370,7 @@ __device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3],
   return valid;
 }
 
+constexpr double kPiD = 3.141592653589793;
 constexpr int kSmemBounds = 264;
 constexpr int kShSmem = 8 * 12 * 32 * 16;
 
@@ -387,10 +445,11 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) L[k][c] = A.ut.spread * sc[k] * R[3 * c + k];
 
-    float ma, mb, caa, cab, cbb, a0, s0 = 0.f;
+    float ma, mb, caa, cab, cbb, s0 = 0.f;
+    double a0 = 0.0, e0 = 0.0;
     bool valid = true, computable = true;
     if (KIND == SIMULI_SENSOR_LIDAR) {
-      lidar_moments(A, mu, L, &a0, &ma, &mb, &caa, &cab, &cbb, &s0, &valid);
+      lidar_moments(A, mu, L, &a0, &e0, &ma, &mb, &caa, &cab, &cbb, &s0, &valid);
     } else {
     // ---- 7 sigma points through the sensor model
     float ya[7], yb[7];
@@ -411,7 +470,6 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
       if (i == 0) s0 = s;
     }
     // ---- UT moments
-    a0 = 0.f;
     ma = A.ut.wm0 * ya[0];
     mb = A.ut.wm0 * yb[0];
 #pragma unroll
@@ -429,21 +487,23 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
       cbb += w * eb * eb;
     }
     }
-    float ya_bar = a0 + ma;
+    // UT mean: sigma point 0 (double, LiDAR) + float32 offset; the azimuth wrapped into
+    // [-pi, pi) (A11); box edges rounded outward from double (A11)
+    double ya_bar = a0 + (double)ma, yb_bar = e0 + (double)mb;
     const float det = caa * cbb - cab * cab;
-    const bool boxok = computable && isfinite(ya_bar) && isfinite(mb) && caa > 0.f && cbb > 0.f && det > 0.f &&
+    const bool boxok = computable && isfinite(ya_bar) && isfinite(yb_bar) && caa > 0.f && cbb > 0.f && det > 0.f &&
                        isfinite(det);
     ok = boxok && valid;
     if (boxok) {
       if (KIND == SIMULI_SENSOR_LIDAR) {
-        if (ya_bar >= A.pi_f) ya_bar = __fsub_rn(ya_bar, A.two_pi_f);
-        else if (ya_bar < -A.pi_f) ya_bar = __fadd_rn(ya_bar, A.two_pi_f);
+        if (ya_bar >= kPiD) ya_bar -= 2.0 * kPiD;
+        else if (ya_bar < -kPiD) ya_bar += 2.0 * kPiD;
       }
-      const float ha = A.ks * sqrtf(caa), hb = A.ks * sqrtf(cbb);
-      box[0] = __fsub_rd(ya_bar, ha);
-      box[1] = __fadd_ru(ya_bar, ha);
-      box[2] = __fsub_rd(mb, hb);
-      box[3] = __fadd_ru(mb, hb);
+      const double ha = (double)A.ks * sqrt((double)caa), hb = (double)A.ks * sqrt((double)cbb);
+      box[0] = __double2float_rd(ya_bar - ha);
+      box[1] = __double2float_ru(ya_bar + ha);
+      box[2] = __double2float_rd(yb_bar - hb);
+      box[3] = __double2float_ru(yb_bar + hb);
     }
     if (ok) {
       // ---- culling + render-tile rectangle
@@ -616,6 +676,13 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
         A.v[i] = static_cast<float>(R0d[0 * 3 + i] * pd.dt[0] + R0d[1 * 3 + i] * pd.dt[1] + R0d[2 * 3 + i] * pd.dt[2]);
       }
       A.theta = static_cast<float>(2.0 * pd.half_theta);
+      A.theta_d = 2.0 * pd.half_theta;
+      for (int i = 0; i < 9; ++i) A.R0d[i] = R0d[i];
+      for (int i = 0; i < 3; ++i) {
+        A.t0d[i] = pd.t0[i];
+        A.axis_d[i] = pd.axis[i];
+        A.vd[i] = R0d[0 * 3 + i] * pd.dt[0] + R0d[1 * 3 + i] * pd.dt[1] + R0d[2 * 3 + i] * pd.dt[2];
+      }
       A.small_rot = std::fabs(2.0 * pd.half_theta) <= 0.5 ? 1 : 0;
     }
     A.n_phi = T.n_phi; A.n_theta = T.n_theta; A.rows_per_tile = T.cull_rows_per_tile;

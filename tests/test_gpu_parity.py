@@ -17,15 +17,17 @@ pytestmark = pytest.mark.gpu
 
 TOL_FEAT = 1e-4
 TOL_DEPTH = 1e-3
-# A23 flag margins: box edges (rad / px) at the measured GPU-vs-oracle box error bound,
+# A23 flag margins: box edges (rad / px) at the measured GPU-vs-oracle box error bound
+# (LiDAR: sigma point 0 in double, offsets in float32 -> <= 1 float32 ulp at |phi| ~ pi,
+# measured max 2.38e-7 rad azimuth / 1.8e-7 rad elevation),
 # alpha / T / tau thresholds at the float32 response error; box-edge flips only count when
 # the particle's alpha*T could move an output by more than a tenth of the tolerance.
-LIDAR_EPS = {"a": 1.2e-6, "b": 1e-6, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
+LIDAR_EPS = {"a": 3e-7, "b": 2e-7, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
 CAMERA_EPS = {"a": 5e-4, "b": 5e-4, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6, "amb_a": 20.0,
               "amb_b": 20.0}
-# share of rays the oracle may flag in tier 2; config B traverses ~360 list entries per ray,
-# so its box-edge coincidences at a 1.2e-6 rad margin are ~0.5 %
-FLAG_BUDGET = {"default": 0.005, "B": 0.01}
+# share of rays the oracle may flag in tier 2; config B's rays traverse ~360
+# list entries each, its flag rate at the margins above is ~0.3 %
+FLAG_BUDGET = {"default": 0.005, "B": 0.005}
 
 
 @pytest.fixture(scope="module")
