@@ -206,10 +206,12 @@ def run_reference(args):
 def roofline_entries(stage_ms, counters, peaks, clocks_mhz):
     """Roofline of every stage from ALGORITHMIC bytes / instructions per launch."""
     hbm = peaks["hbm_gbs"]
-    n, n_vis, P, R, passes, n_tiles = (counters[k] for k in ("n", "n_vis", "P", "R", "passes", "n_tiles"))
+    n, n_vis, P, R, n_tiles = (counters[k] for k in ("n", "n_vis", "P", "R", "n_tiles"))
     # stage bytes: inputs the method must read + outputs it must write (SURVEY §8(d))
     b_project = n * (12 + 16 + 12 + 4) + n * (4 + 16 + 4) + n_vis * (192 + 80)
-    b_sort = n * (4 + 16 + 4) + 12 * P + passes * 24 * P + 8 * P + 8 * n_tiles
+    # sort: read each particle's count, rect and key once, write each pair's id once, plus the
+    # tile ranges and order (the radix passes of the implementation are not algorithmic)
+    b_sort = n * (4 + 16 + 4) + 4 * P + 12 * n_tiles
     lane_instr = (C_BOX * counters["visited"] + C_RESP * counters["inbox"] + C_ACC * counters["contrib"] +
                   C_RAY * R)
     b_render = n_vis * 80 + P * 4 + R * (40 + 12)
@@ -259,7 +261,6 @@ def run_gpu(args):
     r.set_capacity(int(need * 1.3) + 4096)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    passes = 4 + (1 if r.n_tiles > 1 else 0) + (1 if r.n_tiles > 256 else 0) + (1 if r.n_tiles > 65536 else 0)
 
     def scan(p0, p1):
         r.set_poses(p0, p1)
@@ -275,7 +276,7 @@ def run_gpu(args):
     scan(*my[args.warmup])
     torch.cuda.synchronize()
     counters = {"n": r.n, "n_vis": int((r.tile_count > 0).sum().item()), "P": int(r.n_pairs.item()),
-                "R": r.n_rays, "passes": passes, "n_tiles": r.n_tiles,
+                "R": r.n_rays, "n_tiles": r.n_tiles,
                 "visited": int(r.out["n_visited"].sum().item()), "inbox": int(r.out["n_inbox"].sum().item()),
                 "contrib": int(r.out["n_contrib"].sum().item())}
     r.want_counters(False)
@@ -352,7 +353,9 @@ def run_gpu(args):
         dist.destroy_process_group()
         return 0
     value = ws * args.steps * r.n_rays / (max_ms * 1e-3)
-    launches_per_step = 1 + (3 + passes + 1) + 1
+    # k_project; k_count_reduce, k_count_top, k_duplicate, 6 x k_onesweep (passes beyond the
+    # device-side pass count exit at once), k_ranges, k_tile_order; k_render
+    launches_per_step = 1 + (3 + 6 + 2) + 1
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",

@@ -19,10 +19,10 @@ TOL_FEAT = 1e-4
 TOL_DEPTH = 1e-3
 # A23 flag margins: box edges (rad / px) at the measured GPU-vs-oracle box error bound
 # (LiDAR: sigma point 0 in double, offsets in float32 -> <= 1 float32 ulp at |phi| ~ pi,
-# measured max 2.38e-7 rad azimuth / 1.8e-7 rad elevation),
+# measured max 2.38e-7 rad in azimuth and elevation),
 # alpha / T / tau thresholds at the float32 response error; box-edge flips only count when
 # the particle's alpha*T could move an output by more than a tenth of the tolerance.
-LIDAR_EPS = {"a": 3e-7, "b": 2e-7, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
+LIDAR_EPS = {"a": 3e-7, "b": 3e-7, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6}
 CAMERA_EPS = {"a": 5e-4, "b": 5e-4, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4, "impact": 5e-6, "amb_a": 20.0,
               "amb_b": 20.0}
 # share of rays the oracle may flag in tier 2; config B's rays traverse ~360
@@ -204,8 +204,10 @@ def test_culling_reduces_pairs(SM):
 
 
 # ------------------------------------------------------------------ sort + edge cases
-def test_bin_sort_synthetic_keys_large_tiles(SM):
-    """Stable sort of many pairs over 8160 tiles (13 tile bits, 6 passes), ragged partition."""
+@pytest.mark.parametrize("skew", [False, True])
+def test_bin_sort_synthetic_keys_large_tiles(SM, skew):
+    """Stable sort of many pairs over 8160 tiles (13 tile bits) with many equal depth keys
+    (ties by id), ragged last partition.  skew: ~60k pairs in one tile and ~3k in another."""
     dev = "cuda"
     rng = np.random.default_rng(17)
     n = 123_457
@@ -215,6 +217,10 @@ def test_bin_sort_synthetic_keys_large_tiles(SM):
     rows = n_tiles // ncols
     r0 = rng.integers(0, rows, n)
     c0 = rng.integers(0, ncols, n)
+    if skew:
+        hot = rng.uniform(size=n)
+        r0[hot < 0.5], c0[hot < 0.5] = 3, 7
+        r0[(hot >= 0.5) & (hot < 0.525)], c0[(hot >= 0.5) & (hot < 0.525)] = 40, 119
     for i in range(n):
         h = int(rng.integers(1, 3))
         rect[i] = [r0[i], min(rows - 1, r0[i] + h - 1), c0[i], 1]
@@ -252,6 +258,8 @@ def test_bin_sort_synthetic_keys_large_tiles(SM):
     assert np.array_equal(np.sort(od), np.arange(n_tiles))  # a permutation, longest lists first
     lens = rr[od, 1] - rr[od, 0]
     assert np.all(np.diff(np.floor(np.log2(lens + 0.5))) <= 0)
+    if skew:
+        assert lens.max() > 16 * 2048
 
 
 def test_bin_sort_capacity_protocol(SM):
