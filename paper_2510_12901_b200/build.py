@@ -49,6 +49,8 @@ def _compile(src: str, verbose: bool) -> str:
     if src.endswith(".cu"):
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-c", path, "-o", obj]
+        # profiling builds only (e.g. SIMULI_EXTRA_NVCC=-DSIMULI_RENDER_PROFILE, with build(force=True))
+        cmd += os.environ.get("SIMULI_EXTRA_NVCC", "").split()
     else:
         cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
                "-I", INCLUDE, "-I", "/usr/local/cuda/include", "-c", path, "-o", obj]

@@ -6,141 +6,36 @@
 // softmax(zeta_1, zeta_2).  A listed particle contributes to a ray only if its box
 // contains the ray (A12), which makes the result independent of tiling and culling.
 //
-// LiDAR: one warp per (tile, chunk of <= 32 rays), lane = ray.  Each warp stages batches of
-// 32 records (32 x 80 B) of its tile's sorted list in shared memory, every lane walks the
-// batch front to back, and the warp leaves the list once every ray has terminated
-// (T (1 - alpha) < T_min; warp vote).  Rays are generated in double (pose at the column's
-// firing time) and split into float hi/lo parts for the compensated response.
-// Camera: one CTA of tile_px^2 threads per tile (pixel per thread), 256-record batches in
-// shared memory, CTA-wide early exit; pixel rays by the inverse lens model in double.
+// LiDAR (k_render_lidar): one CTA per work item = (tile, beam group, column group) of <= 32
+// rays, items scheduled longest-list-first.  Warp-specialised pipeline over rounds of
+// E = 32 NP list entries:
+//  * producers (NP warps, thread = list entry): the round's 80-byte records arrive by
+//    cp.async, issued STAGES - 1 rounds ahead (a ring of record stages); each entry's
+//    exact A12 ray mask, factorised as (columns inside the azimuth interval) x (beams inside
+//    the elevation interval); a 32x32 bit transpose gives every ray its member entries; the
+//    member pairs are compacted and their responses (alpha, tau) computed with every lane
+//    busy, written ray-major (slot k of ray r = the k-th member of r in list order; E slots
+//    per ray, so no member ever overflows);
+//  * consumer (one warp, lane = ray): streams its ray's slots front to back -- first the
+//    transmittance chain, then the weighted sums -- and reports terminated rays, whose
+//    member pairs the producers skip from then on; the item ends once every ray has
+//    terminated.
+// The per-ray arithmetic (order and operands) does not depend on the tiling, on culling or
+// on the round structure, so results are bit-identical across (N_phi, M) and culling on/off.
+// Rays are generated in double (pose at the column's firing time) and split into float
+// hi / lo parts for the compensated response (common.cuh).
+// Camera (k_render_camera): one CTA of tile_px^2 threads per tile (pixel per thread),
+// 256-record batches in shared memory, CTA-wide early exit; pixel rays by the inverse lens
+// model in double.
 #include <cstdint>
 #include <cstdlib>
 #include <string>
-#include <type_traits>
 
 #include "abi_util.h"
 #include "common.cuh"
 
 namespace simuli {
 namespace {
-
-constexpr int kWarpsPerCta = 4;
-
-struct LidarArgs {
-  const float4* record;
-  const uint32_t* ids;
-  const int2* ranges;
-  const int* tile_ray_offsets;
-  const int* tile_rays;
-  const float *ray_az, *ray_el, *ray_s;
-  int n_tiles, chunks_per_tile;
-  PoseInterpD pose;
-  float pi_f, two_pi_f, near_tau, alpha_min, alpha_max, T_min;
-  float *zeta, *opacity, *depth_accum, *depth, *intensity, *raydrop, *final_T;
-  int* n_contrib;
-  double* ray_od;
-  int *n_visited, *n_inbox;
-};
-
-__global__ void __launch_bounds__(32 * kWarpsPerCta) k_render_lidar(const LidarArgs A) {
-  __shared__ float4 s_rec[kWarpsPerCta][32][5];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wg = (int64_t)blockIdx.x * kWarpsPerCta + warp;
-  const int tile = (int)(wg / A.chunks_per_tile);
-  const int chunk = (int)(wg % A.chunks_per_tile);
-  if (tile >= A.n_tiles) return;
-  const int r_begin = __ldg(A.tile_ray_offsets + tile) + chunk * 32;
-  const int r_end = __ldg(A.tile_ray_offsets + tile + 1);
-  if (r_begin >= r_end) return;  // warp-uniform
-  const bool active = r_begin + lane < r_end;
-  const int ray = active ? __ldg(A.tile_rays + r_begin + lane) : 0;
-
-  // ---- ray o(s_j), d(s_j) in double (A5): pose at the column firing time
-  RayF rf;
-  float ra = 0.f, rb = 0.f;
-  double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
-  if (active) {
-    ra = __ldg(A.ray_az + ray);
-    rb = __ldg(A.ray_el + ray);
-    double R[9];
-    pose_at_d(A.pose, (double)__ldg(A.ray_s + ray), R, o);
-    double sa, ca, se, ce;
-    sincos((double)ra, &sa, &ca);
-    sincos((double)rb, &se, &ce);
-    const double u[3] = {ce * ca, ce * sa, se};
-#pragma unroll
-    for (int i = 0; i < 3; ++i) dd[i] = R[3 * i] * u[0] + R[3 * i + 1] * u[1] + R[3 * i + 2] * u[2];
-  }
-  split_ray(o, dd, rf);
-
-  float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
-  int nc = 0, nv = 0, ni = 0;
-  bool done = !active;
-  const int2 rg = __ldg(A.ranges + tile);
-  for (int b = rg.x; b < rg.y; b += 32) {
-    const int nb = min(32, rg.y - b);
-    if (lane < nb) {
-      const uint32_t g = __ldg(A.ids + b + lane);
-      const float4* src = A.record + (size_t)g * 5;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) s_rec[warp][lane][c] = __ldg(src + c);
-    }
-    __syncwarp();
-    if (!done) {
-      for (int j = 0; j < nb; ++j) {
-        const float4 bx = s_rec[warp][j][4];
-        ++nv;
-        if (!in_box_wrap(bx.x, bx.y, bx.z, bx.w, ra, rb, A.pi_f, A.two_pi_f)) continue;
-        ++ni;
-        const float4 r0 = s_rec[warp][j][0], r1 = s_rec[warp][j][1], r2 = s_rec[warp][j][2],
-                     r3 = s_rec[warp][j][3];
-        const float mu[3] = {r0.x, r0.y, r0.z};
-        const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-        float tau, d2;
-        response(rf, mu, M, &tau, &d2);
-        const float alpha = fminf(A.alpha_max, r3.x * expf(-0.5f * d2));
-        if (tau < A.near_tau || alpha < A.alpha_min) continue;
-        const float Tn = T * (1.f - alpha);
-        if (Tn < A.T_min) {
-          done = true;
-          break;
-        }
-        const float w = alpha * T;
-        acc0 = fmaf(w, r3.y, acc0);
-        acc1 = fmaf(w, r3.z, acc1);
-        acc2 = fmaf(w, r3.w, acc2);
-        D = fmaf(w, tau, D);
-        W += w;
-        ++nc;
-        T = Tn;
-      }
-    }
-    if (__all_sync(0xffffffffu, done)) break;
-    __syncwarp();
-  }
-  if (!active) return;
-  if (A.zeta) {
-    A.zeta[3 * (size_t)ray] = acc0;
-    A.zeta[3 * (size_t)ray + 1] = acc1;
-    A.zeta[3 * (size_t)ray + 2] = acc2;
-  }
-  if (A.opacity) A.opacity[ray] = W;
-  if (A.depth_accum) A.depth_accum[ray] = D;
-  if (A.depth) A.depth[ray] = W > 0.f ? D / W : 0.f;
-  if (A.intensity) A.intensity[ray] = acc0;
-  if (A.raydrop) A.raydrop[ray] = raydrop_prob(acc1, acc2);
-  if (A.final_T) A.final_T[ray] = T;
-  if (A.n_contrib) A.n_contrib[ray] = nc;
-  if (A.n_visited) A.n_visited[ray] = nv;
-  if (A.n_inbox) A.n_inbox[ray] = ni;
-  if (A.ray_od) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      A.ray_od[6 * (size_t)ray + i] = o[i];
-      A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
-    }
-  }
-}
 
 // ------------------------------------------------------------------ camera
 struct CameraArgs {
@@ -295,37 +190,9 @@ __global__ void __launch_bounds__(TP* TP) k_render_camera(const CameraArgs A) {
     }
 }
 
-// ------------------------------------------------------------------ LiDAR v2
-// One CTA of kV2Warps warps per work item = (tile, beam group, column group) with <= 32
-// rays; items are scheduled longest-list-first (tile_order).  Each round stages kV2E list
-// entries' records in shared memory with cp.async (double buffered, the next round's
-// copies in flight while the current one is processed), then:
-//  * producer (all warps, lane = list entry): the entry's ray mask over the item's rays,
-//    factorised as (columns inside the azimuth interval) x (beams inside the elevation
-//    interval) -- the exact A12 membership, ~6 instructions per column / beam; a ballot
-//    transpose gives each ray its member entries; the (entry, ray) member pairs are
-//    compacted and their responses (alpha, tau) computed with every lane busy;
-//  * consumer (warp 0, lane = ray): walks its member entries of the round in list order
-//    and composites front to back exactly as Eq. 1; a warp vote ends the item once every
-//    ray has terminated.
-// The per-ray arithmetic (order and operands) is independent of the tiling and of
-// culling, so results are bit-identical across (N_phi, M) and culling on/off.
-constexpr int kV2Warps = 8;
-constexpr int kV2E = 32 * kV2Warps;
 
-struct V2Smem {
-  float4 rec[2][kV2E][5];       // staged records (double buffer)
-  float2 at[kV2E][32];          // (alpha, tau) of member pairs [entry][ray]
-  uint32_t memb[kV2Warps][32];  // per warp, per ray: member entries of the warp's 32
-  uint32_t wmask[kV2Warps][32]; // per entry ray mask
-  int wex[kV2Warps][32];        // per warp exclusive pair offsets
-  float ray_oh[32][3], ray_ol[32][3], ray_dh[32][3], ray_dl[32][3];
-  float col_phi[32], beam_el[32];
-  int col_id[32], beam_id[32];
-  int all_done;
-};
-
-struct LidarV2Args {
+// ------------------------------------------------------------------ LiDAR
+struct LidarArgs {
   const float4* record;
   const uint32_t* ids;
   const int2* ranges;
@@ -347,496 +214,15 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-__global__ void __launch_bounds__(32 * kV2Warps) k_render_lidar_v2(const LidarV2Args A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V2Smem& S = *reinterpret_cast<V2Smem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t item = blockIdx.x;
-  const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
-  const int tile = A.order ? __ldg(A.order + tslot) : tslot;
-  const int et = tile / A.n_theta, at_ = tile % A.n_theta;
-  const int bgi = sub / A.n_cg, cgi = sub % A.n_cg;
-  const int b0 = __ldg(A.etb_off + et) + bgi * A.bg, b1 = min(__ldg(A.etb_off + et + 1), b0 + A.bg);
-  const int c0 = __ldg(A.atc_off + at_) + cgi * A.cg, c1 = min(__ldg(A.atc_off + at_ + 1), c0 + A.cg);
-  const int nb = b1 - b0, nc = c1 - c0;
-  if (nb <= 0 || nc <= 0) return;  // CTA-uniform
-  const int R = nb * nc;            // <= 32 by construction of (bg, cg)
-
-  // ---- item setup: column azimuths, beam elevations, rays in double (warp 0)
-  if (tid < nc) {
-    const int j = __ldg(A.atc + c0 + tid);
-    S.col_id[tid] = j;
-    S.col_phi[tid] = __ldg(A.ray_az + j);
-  }
-  if (tid >= 32 && tid < 32 + nb) {
-    const int b = __ldg(A.etb + b0 + tid - 32);
-    S.beam_id[tid - 32] = b;
-    S.beam_el[tid - 32] = __ldg(A.ray_el + (size_t)b * A.n_az);
-  }
-  if (tid == 0) S.all_done = 0;
-  __syncthreads();
-  int ray = 0;
-  double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
-  if (warp == 0 && lane < R) {
-    const int bi = lane / nc, ci = lane % nc;
-    const int j = S.col_id[ci];
-    ray = S.beam_id[bi] * A.n_az + j;
-    double Rm[9];
-    pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
-    double sa, ca, se, ce;
-    sincos((double)S.col_phi[ci], &sa, &ca);
-    sincos((double)S.beam_el[bi], &se, &ce);
-    const double u[3] = {ce * ca, ce * sa, se};
-#pragma unroll
-    for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
-    RayF rf;
-    split_ray(o, dd, rf);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      S.ray_oh[lane][i] = rf.o_hi[i];
-      S.ray_ol[lane][i] = rf.o_lo[i];
-      S.ray_dh[lane][i] = rf.d_hi[i];
-      S.ray_dl[lane][i] = rf.d_lo[i];
-    }
-  }
-  const int2 rg = __ldg(A.ranges + tile);
-
-  auto issue = [&](int buf, int start) {
-    const int e = start + tid;
-    if (e < rg.y) {
-      const float4* src = A.record + (size_t)__ldg(A.ids + e) * 5;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[buf][tid][c], src + c);
-    }
-    cp_async_commit();
-  };
-
-  // consumer state (warp 0, lane = ray)
-  float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
-  int nc_ = 0, nv = 0, ni = 0;
-  bool done = !(warp == 0 && lane < R);
-
-  issue(0, rg.x);
-  for (int round = 0;; ++round) {
-    const int cur = round & 1;
-    const int start = rg.x + round * kV2E;
-    if (start >= rg.y) break;  // CTA-uniform
-    issue(cur ^ 1, start + kV2E);
-    cp_async_wait1();
-    __syncthreads();
-    // ---- producer: ray mask of entry `tid`
-    const bool valid = start + tid < rg.y;
-    uint32_t m = 0;
-    if (valid) {
-      const float4 bx = S.rec[cur][tid][4];
-      uint32_t colbits = 0;
-      if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
-        colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
-      } else {
-        const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
-        const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
-        for (int ci = 0; ci < nc; ++ci) {
-          const float p = S.col_phi[ci];
-          const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
-          colbits |= (uint32_t)in << ci;
-        }
-      }
-      if (colbits)
-        for (int bi = 0; bi < nb; ++bi) {
-          const float w = S.beam_el[bi];
-          if (bx.z <= w && w <= bx.w) m |= colbits << (bi * nc);
-        }
-    }
-    // ballot transpose: lane r of warp w gets the warp's entries containing ray r
-    uint32_t my = 0;
-    for (int r = 0; r < R; ++r) {
-      const uint32_t b = __ballot_sync(0xffffffffu, (m >> r) & 1u);
-      if (lane == r) my = b;
-    }
-    S.memb[warp][lane] = my;
-    // compaction of member pairs and their responses
-    const int k = __popc(m);
-    int inc = k;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= off) inc += t;
-    }
-    const int K = __shfl_sync(0xffffffffu, inc, 31);
-    S.wex[warp][lane] = inc - k;
-    S.wmask[warp][lane] = m;
-    __syncwarp();
-    for (int idx = lane; idx < K; idx += 32) {
-      int lo = 0, hi = 32;  // last owner with wex <= idx
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (S.wex[warp][mid] <= idx) lo = mid;
-        else hi = mid;
-      }
-      const uint32_t mo = S.wmask[warp][lo];
-      const int r = __fns(mo, 0, idx - S.wex[warp][lo] + 1);
-      const int e = warp * 32 + lo;
-      const float4 r0 = S.rec[cur][e][0], r1 = S.rec[cur][e][1], r2 = S.rec[cur][e][2], r3 = S.rec[cur][e][3];
-      const float mu[3] = {r0.x, r0.y, r0.z};
-      const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-      RayF rf;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        rf.o_hi[i] = S.ray_oh[r][i];
-        rf.o_lo[i] = S.ray_ol[r][i];
-        rf.d_hi[i] = S.ray_dh[r][i];
-        rf.d_lo[i] = S.ray_dl[r][i];
-      }
-      float tau, d2;
-      response(rf, mu, M, &tau, &d2);
-      S.at[e][r] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
-    }
-    __syncthreads();
-    // ---- consumer: warp 0 composites its rays' members in list order
-    if (warp == 0) {
-      if (!done) {
-        const int n_in_round = min(kV2E, rg.y - start);
-        for (int w = 0; w < kV2Warps && !done; ++w) {
-          uint32_t bits = S.memb[w][lane];
-          while (bits) {
-            const int o = __ffs(bits) - 1;
-            bits &= bits - 1u;
-            const int e = w * 32 + o;
-            ++ni;
-            const float2 a = S.at[e][lane];
-            if (a.y < A.near_tau || a.x < A.alpha_min) continue;
-            const float Tn = T * (1.f - a.x);
-            if (Tn < A.T_min) {
-              done = true;
-              nv += e + 1;  // entries examined this round up to the stopping one
-              break;
-            }
-            const float4 r3 = S.rec[cur][e][3];
-            const float wgt = a.x * T;
-            acc0 = fmaf(wgt, r3.y, acc0);
-            acc1 = fmaf(wgt, r3.z, acc1);
-            acc2 = fmaf(wgt, r3.w, acc2);
-            D = fmaf(wgt, a.y, D);
-            W += wgt;
-            ++nc_;
-            T = Tn;
-          }
-        }
-        if (!done) nv += n_in_round;
-      }
-      const bool all = __all_sync(0xffffffffu, done);
-      if (lane == 0) S.all_done = all ? 1 : 0;
-    }
-    __syncthreads();
-    if (S.all_done) break;
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (warp != 0 || lane >= R) return;
-  if (A.zeta) {
-    A.zeta[3 * (size_t)ray] = acc0;
-    A.zeta[3 * (size_t)ray + 1] = acc1;
-    A.zeta[3 * (size_t)ray + 2] = acc2;
-  }
-  if (A.opacity) A.opacity[ray] = W;
-  if (A.depth_accum) A.depth_accum[ray] = D;
-  if (A.depth) A.depth[ray] = W > 0.f ? D / W : 0.f;
-  if (A.intensity) A.intensity[ray] = acc0;
-  if (A.raydrop) A.raydrop[ray] = raydrop_prob(acc1, acc2);
-  if (A.final_T) A.final_T[ray] = T;
-  if (A.n_contrib) A.n_contrib[ray] = nc_;
-  if (A.n_visited) A.n_visited[ray] = nv;
-  if (A.n_inbox) A.n_inbox[ray] = ni;
-  if (A.ray_od) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      A.ray_od[6 * (size_t)ray + i] = o[i];
-      A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
-    }
-  }
-}
-
-// ------------------------------------------------------------------ LiDAR v3 (warp specialised)
-// Same per-ray arithmetic as v2, but the compositing warp no longer serialises the CTA:
-// NP producer warps fill round r+1's member masks / (alpha, tau) / features into one of two
-// shared-memory buffers while the consumer warp composites round r from the other.
-// Hand-off by named barriers: FULL(b) (producers arrive, consumer syncs) and EMPTY(b)
-// (consumer arrives, producers sync).  The consumer's stop decision for round r is
-// published with EMPTY(b) and read by the producers before round r+2, so both sides
-// agree on the number of rounds and every barrier phase is matched.
-constexpr int kV3Stages = 3;
-template <int NP>
-struct V3Smem {
-  float4 rec[kV3Stages][32 * NP][5];
-  float2 at[2][32 * NP][32];
-  float4 feat[2][32 * NP];
-  uint32_t memb[2][NP][32];
-  uint32_t wmask[NP][32];
-  int wex[NP][32];
-  float ray_oh[32][3], ray_ol[32][3], ray_dh[32][3], ray_dl[32][3];
-  float col_phi[32], beam_el[32];
-  int col_id[32], beam_id[32];
-  int stop_at[2];
-};
-
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-template <int NP>
-__global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v3(const LidarV2Args A) {
-  constexpr int E = 32 * NP;
-  constexpr int NT = 32 * (NP + 1);
-  constexpr int BAR_PROD = 1, BAR_FULL = 2, BAR_EMPTY = 4;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V3Smem<NP>& S = *reinterpret_cast<V3Smem<NP>*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t item = blockIdx.x;
-  const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
-  const int tile = A.order ? __ldg(A.order + tslot) : tslot;
-  const int et = tile / A.n_theta, at_ = tile % A.n_theta;
-  const int bgi = sub / A.n_cg, cgi = sub % A.n_cg;
-  const int b0 = __ldg(A.etb_off + et) + bgi * A.bg, b1 = min(__ldg(A.etb_off + et + 1), b0 + A.bg);
-  const int c0 = __ldg(A.atc_off + at_) + cgi * A.cg, c1 = min(__ldg(A.atc_off + at_ + 1), c0 + A.cg);
-  const int nb = b1 - b0, nc = c1 - c0;
-  if (nb <= 0 || nc <= 0) return;  // CTA-uniform
-  const int R = nb * nc;
-  if (tid < nc) {
-    const int j = __ldg(A.atc + c0 + tid);
-    S.col_id[tid] = j;
-    S.col_phi[tid] = __ldg(A.ray_az + j);
-  }
-  if (tid >= 32 && tid < 32 + nb) {
-    const int b = __ldg(A.etb + b0 + tid - 32);
-    S.beam_id[tid - 32] = b;
-    S.beam_el[tid - 32] = __ldg(A.ray_el + (size_t)b * A.n_az);
-  }
-  if (tid < 2) S.stop_at[tid] = 0;
-  __syncthreads();
-  const int2 rg = __ldg(A.ranges + tile);
-  const int n_rounds = (rg.y - rg.x + E - 1) / E;
-
-  if (warp == NP) {
-    // ================= consumer: lane = ray
-    int ray = 0;
-    double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
-    if (lane < R) {
-      const int bi = lane / nc, ci = lane % nc;
-      const int j = S.col_id[ci];
-      ray = S.beam_id[bi] * A.n_az + j;
-      double Rm[9];
-      pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
-      double sa, ca, se, ce;
-      sincos((double)S.col_phi[ci], &sa, &ca);
-      sincos((double)S.beam_el[bi], &se, &ce);
-      const double u[3] = {ce * ca, ce * sa, se};
-#pragma unroll
-      for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
-      RayF rf;
-      split_ray(o, dd, rf);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        S.ray_oh[lane][i] = rf.o_hi[i];
-        S.ray_ol[lane][i] = rf.o_lo[i];
-        S.ray_dh[lane][i] = rf.d_hi[i];
-        S.ray_dl[lane][i] = rf.d_lo[i];
-      }
-    }
-    named_arrive(BAR_PROD + 5, NT);  // rays ready
-    float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
-    int ncontrib = 0, nv = 0, ni = 0;
-    bool done = lane >= R;
-    for (int r = 0; r < n_rounds; ++r) {
-      const int b = r & 1;
-      named_sync(BAR_FULL + b, NT);
-      const int start = rg.x + r * E;
-      if (!done) {
-        const int n_in = min(E, rg.y - start);
-        bool stopped = false;
-        for (int w = 0; w < NP && !stopped; ++w) {
-          uint32_t bits = S.memb[b][w][lane];
-          while (bits) {
-            const int oo = __ffs(bits) - 1;
-            bits &= bits - 1u;
-            const int e = w * 32 + oo;
-            ++ni;
-            const float2 a = S.at[b][e][lane];
-            if (a.y < A.near_tau || a.x < A.alpha_min) continue;
-            const float Tn = T * (1.f - a.x);
-            if (Tn < A.T_min) {
-              stopped = true;
-              nv += e + 1;
-              break;
-            }
-            const float4 f = S.feat[b][e];
-            const float wgt = a.x * T;
-            acc0 = fmaf(wgt, f.y, acc0);
-            acc1 = fmaf(wgt, f.z, acc1);
-            acc2 = fmaf(wgt, f.w, acc2);
-            D = fmaf(wgt, a.y, D);
-            W += wgt;
-            ++ncontrib;
-            T = Tn;
-          }
-        }
-        if (stopped) done = true;
-        else nv += n_in;
-      }
-      const bool all = __all_sync(0xffffffffu, done);
-      if (r + 2 < n_rounds) {
-        if (lane == 0) S.stop_at[b] = all ? 1 : 0;
-        __threadfence_block();
-        named_arrive(BAR_EMPTY + b, NT);
-      }
-      if (all) {
-        if (r + 1 < n_rounds) named_sync(BAR_FULL + (b ^ 1), NT);  // drain the round in flight
-        break;
-      }
-    }
-    if (lane >= R) return;
-    if (A.zeta) {
-      A.zeta[3 * (size_t)ray] = acc0;
-      A.zeta[3 * (size_t)ray + 1] = acc1;
-      A.zeta[3 * (size_t)ray + 2] = acc2;
-    }
-    if (A.opacity) A.opacity[ray] = W;
-    if (A.depth_accum) A.depth_accum[ray] = D;
-    if (A.depth) A.depth[ray] = W > 0.f ? D / W : 0.f;
-    if (A.intensity) A.intensity[ray] = acc0;
-    if (A.raydrop) A.raydrop[ray] = raydrop_prob(acc1, acc2);
-    if (A.final_T) A.final_T[ray] = T;
-    if (A.n_contrib) A.n_contrib[ray] = ncontrib;
-    if (A.n_visited) A.n_visited[ray] = nv;
-    if (A.n_inbox) A.n_inbox[ray] = ni;
-    if (A.ray_od) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        A.ray_od[6 * (size_t)ray + i] = o[i];
-        A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
-      }
-    }
-    return;
-  }
-
-  // ================= producers: thread = list entry of the round
-  // Records of round r+2 are in flight (cp.async, NS = 3 stages) while round r is
-  // processed; the list ids they need were loaded one round earlier still.
-  auto issue = [&](int stage, int start, uint32_t id) {
-    if (start + tid < rg.y) {
-      const float4* src = A.record + (size_t)id * 5;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[stage][tid][c], src + c);
-    }
-    cp_async_commit();
-  };
-  auto load_id = [&](int round) -> uint32_t {
-    const int e = rg.x + round * E + tid;
-    return (round < n_rounds && e < rg.y) ? __ldg(A.ids + e) : 0u;
-  };
-  issue(0, rg.x, load_id(0));
-  issue(1, rg.x + E, load_id(1));
-  uint32_t id_pf = load_id(2);
-  named_sync(BAR_PROD + 5, NT);  // rays ready
-  for (int r = 0; r < n_rounds; ++r) {
-    const int b = r & 1;
-    const int rs = r % kV3Stages;
-    if (r >= 2) {
-      named_sync(BAR_EMPTY + b, NT);
-      if (S.stop_at[b]) break;
-    }
-    const int start = rg.x + r * E;
-    asm volatile("cp.async.wait_group 1;" ::: "memory");  // round r landed (r+1 may be in flight)
-    named_sync(BAR_PROD, E);
-    issue((r + 2) % kV3Stages, start + 2 * E, id_pf);
-    id_pf = load_id(r + 3);
-    const bool valid = start + tid < rg.y;
-    uint32_t m = 0;
-    if (valid) {
-      const float4 bx = S.rec[rs][tid][4];
-      S.feat[b][tid] = S.rec[rs][tid][3];
-      uint32_t colbits = 0;
-      if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
-        colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
-      } else {
-        const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
-        const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
-        for (int ci = 0; ci < nc; ++ci) {
-          const float p = S.col_phi[ci];
-          const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
-          colbits |= (uint32_t)in << ci;
-        }
-      }
-      if (colbits)
-        for (int bi = 0; bi < nb; ++bi) {
-          const float w = S.beam_el[bi];
-          if (bx.z <= w && w <= bx.w) m |= colbits << (bi * nc);
-        }
-    }
-    uint32_t my = 0;
-    for (int rr = 0; rr < R; ++rr) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, (m >> rr) & 1u);
-      if (lane == rr) my = bal;
-    }
-    S.memb[b][warp][lane] = my;
-    const int k = __popc(m);
-    int inc = k;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= off) inc += t;
-    }
-    const int K = __shfl_sync(0xffffffffu, inc, 31);
-    S.wex[warp][lane] = inc - k;
-    S.wmask[warp][lane] = m;
-    __syncwarp();
-    for (int idx = lane; idx < K; idx += 32) {
-      int lo = 0, hi = 32;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (S.wex[warp][mid] <= idx) lo = mid;
-        else hi = mid;
-      }
-      const uint32_t mo = S.wmask[warp][lo];
-      const int rr = __fns(mo, 0, idx - S.wex[warp][lo] + 1);
-      const int e = warp * 32 + lo;
-      const float4 r0 = S.rec[rs][e][0], r1 = S.rec[rs][e][1], r2 = S.rec[rs][e][2], r3 = S.rec[rs][e][3];
-      const float mu[3] = {r0.x, r0.y, r0.z};
-      const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-      RayF rf;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        rf.o_hi[i] = S.ray_oh[rr][i];
-        rf.o_lo[i] = S.ray_ol[rr][i];
-        rf.d_hi[i] = S.ray_dh[rr][i];
-        rf.d_lo[i] = S.ray_dl[rr][i];
-      }
-      float tau, d2;
-      response(rf, mu, M, &tau, &d2);
-      S.at[b][e][rr] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
-    }
-    __syncwarp();
-    __threadfence_block();
-    named_arrive(BAR_FULL + b, NT);
-  }
-  cp_async_wait0();
-}
-
-// ------------------------------------------------------------------ LiDAR v5
-// v3's warp-specialised pipeline with the producer's bookkeeping cut to O(log) per warp:
-//  * ray-major member words by a 5-stage shuffle butterfly transpose of the 32x32 bit
-//    matrix (30 instructions instead of 32 ballots);
-//  * member pairs listed in shared memory by each entry's own bit loop, then their
-//    responses computed over the list with every lane busy (no per-pair search);
-//  * (alpha, tau) stored compactly per producer warp (capacity kV5Cap pairs; the consumer
-//    recomputes the rare overflow pairs itself from the record in global memory); the
-//    consumer finds a member's pair index as excl[entry] + popc(mask[entry] & lanes below).
-constexpr int kV5Cap = 384;
 
 // 32x32 bit-matrix transpose across a warp: in: lane i holds row i; out: lane r holds
-// the word whose bit e is bit r of row e.
+// the word whose bit e is bit r of row e (5-stage shuffle butterfly).
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
   const uint32_t lm[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
@@ -848,290 +234,15 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
   return x;
 }
 
-template <int NP>
-struct V5Smem {
-  float4 rec[2][32 * NP][5];
-  float2 at[2][NP][kV5Cap];
-  float4 feat[2][32 * NP];
-  uint32_t memb[2][NP][32];
-  uint32_t wmask[2][NP][32];
-  int wex[2][NP][32];
-  uint16_t plist[NP][kV5Cap];
-  float ray_oh[32][3], ray_ol[32][3], ray_dh[32][3], ray_dl[32][3];
-  float col_phi[32], beam_el[32];
-  int col_id[32], beam_id[32];
-  int stop_at[2];
-};
-
-template <int NP>
-__global__ void __launch_bounds__(32 * (NP + 1)) k_render_lidar_v5(const LidarV2Args A) {
-  constexpr int E = 32 * NP;
-  constexpr int NT = 32 * (NP + 1);
-  constexpr int BAR_PROD = 1, BAR_FULL = 2, BAR_EMPTY = 4, BAR_RAYS = 6;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V5Smem<NP>& S = *reinterpret_cast<V5Smem<NP>*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t item = blockIdx.x;
-  const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
-  const int tile = A.order ? __ldg(A.order + tslot) : tslot;
-  const int et = tile / A.n_theta, at_ = tile % A.n_theta;
-  const int bgi = sub / A.n_cg, cgi = sub % A.n_cg;
-  const int b0 = __ldg(A.etb_off + et) + bgi * A.bg, b1 = min(__ldg(A.etb_off + et + 1), b0 + A.bg);
-  const int c0 = __ldg(A.atc_off + at_) + cgi * A.cg, c1 = min(__ldg(A.atc_off + at_ + 1), c0 + A.cg);
-  const int nb = b1 - b0, nc = c1 - c0;
-  if (nb <= 0 || nc <= 0) return;  // CTA-uniform
-  const int R = nb * nc;
-  if (tid < nc) {
-    const int j = __ldg(A.atc + c0 + tid);
-    S.col_id[tid] = j;
-    S.col_phi[tid] = __ldg(A.ray_az + j);
-  }
-  if (tid >= 32 && tid < 32 + nb) {
-    const int b = __ldg(A.etb + b0 + tid - 32);
-    S.beam_id[tid - 32] = b;
-    S.beam_el[tid - 32] = __ldg(A.ray_el + (size_t)b * A.n_az);
-  }
-  if (tid < 2) S.stop_at[tid] = 0;
-  __syncthreads();
-  const int2 rg = __ldg(A.ranges + tile);
-  const int n_rounds = (rg.y - rg.x + E - 1) / E;
-
-  if (warp == NP) {
-    // ================= consumer: lane = ray
-    int ray = 0;
-    double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
-    RayF rf;
-    if (lane < R) {
-      const int bi = lane / nc, ci = lane % nc;
-      const int j = S.col_id[ci];
-      ray = S.beam_id[bi] * A.n_az + j;
-      double Rm[9];
-      pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
-      double sa, ca, se, ce;
-      sincos((double)S.col_phi[ci], &sa, &ca);
-      sincos((double)S.beam_el[bi], &se, &ce);
-      const double u[3] = {ce * ca, ce * sa, se};
-#pragma unroll
-      for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
-    }
-    split_ray(o, dd, rf);
-    if (lane < R) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        S.ray_oh[lane][i] = rf.o_hi[i];
-        S.ray_ol[lane][i] = rf.o_lo[i];
-        S.ray_dh[lane][i] = rf.d_hi[i];
-        S.ray_dl[lane][i] = rf.d_lo[i];
-      }
-    }
-    __threadfence_block();
-    named_arrive(BAR_RAYS, NT);
-    const uint32_t below = (1u << lane) - 1u;
-    float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
-    int ncontrib = 0, nv = 0, ni = 0;
-    bool done = lane >= R;
-    for (int r = 0; r < n_rounds; ++r) {
-      const int b = r & 1;
-      named_sync(BAR_FULL + b, NT);
-      const int start = rg.x + r * E;
-      if (!done) {
-        const int n_in = min(E, rg.y - start);
-        bool stopped = false;
-        for (int w = 0; w < NP && !stopped; ++w) {
-          uint32_t bits = S.memb[b][w][lane];
-          while (bits) {
-            const int oo = __ffs(bits) - 1;
-            bits &= bits - 1u;
-            const int e = w * 32 + oo;
-            ++ni;
-            const int pidx = S.wex[b][w][oo] + __popc(S.wmask[b][w][oo] & below);
-            float2 a;
-            if (pidx < kV5Cap) {
-              a = S.at[b][w][pidx];
-            } else {  // overflow pair: response from the record in global memory
-              const float4* src = A.record + (size_t)__ldg(A.ids + start + e) * 5;
-              const float4 r0 = __ldg(src), r1 = __ldg(src + 1), r2 = __ldg(src + 2), r3 = __ldg(src + 3);
-              const float mu[3] = {r0.x, r0.y, r0.z};
-              const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-              float tau, d2;
-              response(rf, mu, M, &tau, &d2);
-              a = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
-            }
-            if (a.y < A.near_tau || a.x < A.alpha_min) continue;
-            const float Tn = T * (1.f - a.x);
-            if (Tn < A.T_min) {
-              stopped = true;
-              nv += e + 1;
-              break;
-            }
-            const float4 f = S.feat[b][e];
-            const float wgt = a.x * T;
-            acc0 = fmaf(wgt, f.y, acc0);
-            acc1 = fmaf(wgt, f.z, acc1);
-            acc2 = fmaf(wgt, f.w, acc2);
-            D = fmaf(wgt, a.y, D);
-            W += wgt;
-            ++ncontrib;
-            T = Tn;
-          }
-        }
-        if (stopped) done = true;
-        else nv += n_in;
-      }
-      const bool all = __all_sync(0xffffffffu, done);
-      if (r + 2 < n_rounds) {
-        if (lane == 0) S.stop_at[b] = all ? 1 : 0;
-        __threadfence_block();
-        named_arrive(BAR_EMPTY + b, NT);
-      }
-      if (all) {
-        if (r + 1 < n_rounds) named_sync(BAR_FULL + (b ^ 1), NT);  // drain the round in flight
-        break;
-      }
-    }
-    if (lane >= R) return;
-    if (A.zeta) {
-      A.zeta[3 * (size_t)ray] = acc0;
-      A.zeta[3 * (size_t)ray + 1] = acc1;
-      A.zeta[3 * (size_t)ray + 2] = acc2;
-    }
-    if (A.opacity) A.opacity[ray] = W;
-    if (A.depth_accum) A.depth_accum[ray] = D;
-    if (A.depth) A.depth[ray] = W > 0.f ? D / W : 0.f;
-    if (A.intensity) A.intensity[ray] = acc0;
-    if (A.raydrop) A.raydrop[ray] = raydrop_prob(acc1, acc2);
-    if (A.final_T) A.final_T[ray] = T;
-    if (A.n_contrib) A.n_contrib[ray] = ncontrib;
-    if (A.n_visited) A.n_visited[ray] = nv;
-    if (A.n_inbox) A.n_inbox[ray] = ni;
-    if (A.ray_od) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        A.ray_od[6 * (size_t)ray + i] = o[i];
-        A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
-      }
-    }
-    return;
-  }
-
-  // ================= producers: thread = list entry of the round
-  auto issue = [&](int stage, int start, uint32_t id) {
-    if (start + tid < rg.y) {
-      const float4* src = A.record + (size_t)id * 5;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[stage][tid][c], src + c);
-    }
-    cp_async_commit();
-  };
-  auto load_id = [&](int round) -> uint32_t {
-    const int e = rg.x + round * E + tid;
-    return (round < n_rounds && e < rg.y) ? __ldg(A.ids + e) : 0u;
-  };
-  issue(0, rg.x, load_id(0));
-  uint32_t id_pf = load_id(1);
-  named_sync(BAR_RAYS, NT);
-  for (int r = 0; r < n_rounds; ++r) {
-    const int b = r & 1;
-    if (r >= 2) {
-      named_sync(BAR_EMPTY + b, NT);
-      if (S.stop_at[b]) break;
-    }
-    const int start = rg.x + r * E;
-    cp_async_wait0();
-    named_sync(BAR_PROD, E);  // round r's records visible; stage b^1 free (round r-1 done)
-    issue(b ^ 1, start + E, id_pf);
-    id_pf = load_id(r + 2);
-    const bool valid = start + tid < rg.y;
-    uint32_t m = 0;
-    if (valid) {
-      const float4 bx = S.rec[b][tid][4];
-      S.feat[b][tid] = S.rec[b][tid][3];
-      uint32_t colbits = 0;
-      if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
-        colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
-      } else {
-        const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
-        const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
-        for (int ci = 0; ci < nc; ++ci) {
-          const float p = S.col_phi[ci];
-          const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
-          colbits |= (uint32_t)in << ci;
-        }
-      }
-      if (colbits)
-        for (int bi = 0; bi < nb; ++bi) {
-          const float w = S.beam_el[bi];
-          if (bx.z <= w && w <= bx.w) m |= colbits << (bi * nc);
-        }
-    }
-    S.memb[b][warp][lane] = warp_transpose32(m, lane);
-    const int k = __popc(m);
-    int inc = k;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= off) inc += t;
-    }
-    const int K = min(__shfl_sync(0xffffffffu, inc, 31), kV5Cap);
-    const int ex = inc - k;
-    S.wex[b][warp][lane] = ex;
-    S.wmask[b][warp][lane] = m;
-    {
-      int pos = ex;
-      uint32_t mm = m;
-      while (mm && pos < kV5Cap) {
-        const int rr = __ffs(mm) - 1;
-        mm &= mm - 1u;
-        S.plist[warp][pos++] = (uint16_t)((lane << 5) | rr);
-      }
-    }
-    __syncwarp();
-    for (int idx = lane; idx < K; idx += 32) {
-      const int v = S.plist[warp][idx];
-      const int rr = v & 31, e = warp * 32 + (v >> 5);
-      const float4 r0 = S.rec[b][e][0], r1 = S.rec[b][e][1], r2 = S.rec[b][e][2], r3 = S.rec[b][e][3];
-      const float mu[3] = {r0.x, r0.y, r0.z};
-      const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-      RayF rf;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        rf.o_hi[i] = S.ray_oh[rr][i];
-        rf.o_lo[i] = S.ray_ol[rr][i];
-        rf.d_hi[i] = S.ray_dh[rr][i];
-        rf.d_lo[i] = S.ray_dl[rr][i];
-      }
-      float tau, d2;
-      response(rf, mu, M, &tau, &d2);
-      S.at[b][warp][idx] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
-    }
-    __syncwarp();
-    __threadfence_block();
-    named_arrive(BAR_FULL + b, NT);
-  }
-  cp_async_wait0();
-}
-
-// ------------------------------------------------------------------ LiDAR v6
-// v5 with a latency-free consumer: the producers place every member pair's (alpha, tau)
-// and entry index ray-major -- slot k of ray r holds the k-th member of r in list order,
-// k = (members of r in earlier producer warps) + popc(r's member word & entries below) --
-// so the compositing warp streams its ray's members with no index arithmetic or
-// dependent shared-memory lookups on the transmittance chain.  Rays with more than
-// kV6Cap members in one round take the rare slow path (walk the member words, response
-// from the record in global memory).
-constexpr int kV6Cap = 32;
-
-template <int NP>
-struct V6Smem {
-  float4 rec[2][32 * NP][5];
-  float2 at[2][32][kV6Cap];     // ray-major (alpha, tau)
-  uint8_t ent[2][32][kV6Cap];   // ray-major entry index within the round
-  float4 feat[2][32 * NP];
-  uint32_t memb[2][NP][32];     // [warp][ray] member entries of the warp's 32
-  int rowoff[NP][32];           // members of ray r in warps before w (current round)
-  uint32_t wmask[NP][32];
-  int wex[NP][32];
-  uint16_t plist[NP][1024];
+template <int NP, int STAGES>
+struct LidarSmem {
+  float4 rec[STAGES][32 * NP][5];  // record ring (cp.async, STAGES - 1 rounds ahead)
+  float2 at[2][32][32 * NP];       // ray-major (alpha, tau) of member pairs, per slot buffer
+  uint8_t ent[2][32][32 * NP];     // ray-major entry index within the round
+  float4 feat[2][32 * NP];         // (sigma, features) of the round's entries
+  uint32_t memb[2][NP][32];        // [warp][ray] member entries of the warp's 32
+  int rowoff[NP][32];              // members of ray r in warps before w (current round)
+  uint16_t plist[NP][1024];        // the warp's member pairs (entry << 5 | ray)
   float ray_oh[32][3], ray_ol[32][3], ray_dh[32][3], ray_dl[32][3];
   float col_phi[32], beam_el[32];
   int col_id[32], beam_id[32];
@@ -1139,14 +250,33 @@ struct V6Smem {
   uint32_t done_mask[2];  // rays terminated by the end of the round that released buffer b
 };
 
-template <int NP>
-__global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lidar_v6(const LidarV2Args A) {
+#ifdef SIMULI_RENDER_PROFILE
+__device__ long long g_render_prof[1 << 20];  // per item: start ns, end ns, rounds run, list length | smid << 32
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
+// LiDAR pipeline shape: 2 producer warps (64 list entries per round), 2 record stages
+// (prefetch 1 round ahead); ~54 KB shared memory -> 4 CTAs per SM.  Measured on config B
+// (render only, L2 flushed): (NP, stages) = (2, 2) 200 us, (2, 3) 238, (2, 4) 240, (1, 2) 281,
+// (3, 2) 295 -- residency beats prefetch depth (the deeper ring costs a CTA per SM).
+constexpr int kLidarNP = 2, kLidarStages = 2;
+
+template <int NP, int STAGES>
+__global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarArgs A) {
   constexpr int E = 32 * NP;
   constexpr int NT = 32 * (NP + 1);
   constexpr int BAR_PROD = 1, BAR_FULL = 2, BAR_EMPTY = 4, BAR_RAYS = 6;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  V6Smem<NP>& S = *reinterpret_cast<V6Smem<NP>*>(smem_raw);
+  LidarSmem<NP, STAGES>& S = *reinterpret_cast<LidarSmem<NP, STAGES>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef SIMULI_RENDER_PROFILE
+  const long long t_start = gtime();
+  int rounds_run = 0;
+#endif
   const int64_t item = blockIdx.x;
   const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
   const int tile = A.order ? __ldg(A.order + tslot) : tslot;
@@ -1215,12 +345,11 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
 #pragma unroll
         for (int w = 0; w < NP; ++w) cnt += __popc(S.memb[b][w][lane]);
         bool stopped = false;
-        const int fast = min(cnt, kV6Cap);
         // phase 1: the transmittance chain only (weights written back in place); branch-free
         // so the slot loads of later members are issued ahead of the chain
         int stop_k = -1;
 #pragma unroll 4
-        for (int k = 0; k < fast; ++k) {
+        for (int k = 0; k < cnt; ++k) {
           const float2 a = S.at[b][lane][k];
           const bool take = !(a.y < A.near_tau || a.x < A.alpha_min) && stop_k < 0;
           const float Tn = T * (1.f - a.x);
@@ -1231,7 +360,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
           T = comp ? Tn : T;
         }
         // phase 2: accumulate the weighted features / depths in member order
-        const int kend = stop_k >= 0 ? stop_k : fast;
+        const int kend = stop_k >= 0 ? stop_k : cnt;
 #pragma unroll 4
         for (int k = 0; k < kend; ++k) {
           const float2 wt = S.at[b][lane][k];
@@ -1249,42 +378,6 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
           nv += S.ent[b][lane][stop_k] + 1;
           ni += stop_k + 1;
         }
-        if (!stopped && cnt > kV6Cap) {
-          // slow path: members beyond the ray's slot capacity, in list order
-          int seen = 0;
-          for (int w = 0; w < NP && !stopped; ++w) {
-            uint32_t bits = S.memb[b][w][lane];
-            while (bits) {
-              const int oo = __ffs(bits) - 1;
-              bits &= bits - 1u;
-              if (seen++ < kV6Cap) continue;
-              const int e = w * 32 + oo;
-              const float4* src = A.record + (size_t)__ldg(A.ids + start + e) * 5;
-              const float4 r0 = __ldg(src), r1 = __ldg(src + 1), r2 = __ldg(src + 2), r3 = __ldg(src + 3);
-              const float mu[3] = {r0.x, r0.y, r0.z};
-              const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-              float tau, d2;
-              response(rf, mu, M, &tau, &d2);
-              const float alpha = fminf(A.alpha_max, r3.x * expf(-0.5f * d2));
-              if (tau < A.near_tau || alpha < A.alpha_min) continue;
-              const float Tn = T * (1.f - alpha);
-              if (Tn < A.T_min) {
-                stopped = true;
-                nv += e + 1;
-                ni += seen;
-                break;
-              }
-              const float wgt = alpha * T;
-              acc0 = fmaf(wgt, r3.y, acc0);
-              acc1 = fmaf(wgt, r3.z, acc1);
-              acc2 = fmaf(wgt, r3.w, acc2);
-              D = fmaf(wgt, tau, D);
-              W += wgt;
-              ++ncontrib;
-              T = Tn;
-            }
-          }
-        }
         if (stopped) done = true;
         else {
           nv += n_in;
@@ -1293,6 +386,9 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
       }
       const uint32_t dmask = __ballot_sync(0xffffffffu, done);
       const bool all = dmask == 0xffffffffu;
+#ifdef SIMULI_RENDER_PROFILE
+      rounds_run = r + 1;
+#endif
       if (r + 2 < n_rounds) {
         if (lane == 0) {
           S.stop_at[b] = all ? 1 : 0;
@@ -1306,6 +402,16 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
         break;
       }
     }
+#ifdef SIMULI_RENDER_PROFILE
+    if (lane == 0 && item < (1 << 18)) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_render_prof[4 * item] = t_start;
+      g_render_prof[4 * item + 1] = gtime();
+      g_render_prof[4 * item + 2] = rounds_run;
+      g_render_prof[4 * item + 3] = (long long)(rg.y - rg.x) | ((long long)smid << 32);
+    }
+#endif
     if (lane >= R) return;
     if (A.zeta) {
       A.zeta[3 * (size_t)ray] = acc0;
@@ -1332,39 +438,46 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
   }
 
   // ================= producers: thread = list entry of the round
-  auto issue = [&](int stage, int start, uint32_t id) {
-    if (start + tid < rg.y) {
+  constexpr int D = STAGES - 1;  // record prefetch distance (rounds)
+  auto issue = [&](int round, uint32_t id) {
+    if (round < n_rounds && rg.x + round * E + tid < rg.y) {
       const float4* src = A.record + (size_t)id * 5;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[stage][tid][c], src + c);
+      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[round % STAGES][tid][c], src + c);
     }
-    cp_async_commit();
+    cp_async_commit();  // one group per round, empty or not (keeps the wait_group count exact)
   };
   auto load_id = [&](int round) -> uint32_t {
     const int e = rg.x + round * E + tid;
     return (round < n_rounds && e < rg.y) ? __ldg(A.ids + e) : 0u;
   };
-  issue(0, rg.x, load_id(0));
-  uint32_t id_pf = load_id(1);
+  {
+    uint32_t ids[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) ids[q] = load_id(q);
+#pragma unroll
+    for (int q = 0; q < D; ++q) issue(q, ids[q]);
+  }
+  uint32_t id_pf = load_id(D);
   named_sync(BAR_RAYS, NT);
   uint32_t alive = 0xffffffffu;  // rays the consumer has not terminated (2 rounds behind)
   for (int r = 0; r < n_rounds; ++r) {
-    const int b = r & 1;
+    const int b = r & 1, st = r % STAGES;
     if (r >= 2) {
       named_sync(BAR_EMPTY + b, NT);
       if (S.stop_at[b]) break;
       alive = ~S.done_mask[b];
     }
     const int start = rg.x + r * E;
-    cp_async_wait0();
-    named_sync(BAR_PROD, E);  // round r's records visible; stage b^1 and rowoff free
-    issue(b ^ 1, start + E, id_pf);
-    id_pf = load_id(r + 2);
+    cp_async_wait<D - 1>();   // this thread's copies of round r have landed
+    named_sync(BAR_PROD, E);  // everyone's: round r's records visible; stage of round r - 1 and rowoff free
+    issue(r + D, id_pf);
+    id_pf = load_id(r + D + 1);
     const bool valid = start + tid < rg.y;
     uint32_t m = 0;
     if (valid) {
-      const float4 bx = S.rec[b][tid][4];
-      S.feat[b][tid] = S.rec[b][tid][3];
+      const float4 bx = S.rec[st][tid][4];
+      S.feat[b][tid] = S.rec[st][tid][3];
       uint32_t colbits = 0;
       if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
         colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
@@ -1395,8 +508,6 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
     }
     const int K = __shfl_sync(0xffffffffu, inc, 31);
     const int ex = inc - k;
-    S.wex[warp][lane] = ex;
-    S.wmask[warp][lane] = m;
     {
       int pos = ex;
       uint32_t mm = m;
@@ -1419,8 +530,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
       const int v = S.plist[warp][idx];
       const int rr = v & 31, el = v >> 5, e = warp * 32 + el;
       const int slot = S.rowoff[warp][rr] + __popc(S.memb[b][warp][rr] & ((1u << el) - 1u));
-      if (slot >= kV6Cap) continue;  // consumer's slow path
-      const float4 r0 = S.rec[b][e][0], r1 = S.rec[b][e][1], r2 = S.rec[b][e][2], r3 = S.rec[b][e][3];
+      const float4 r0 = S.rec[st][e][0], r1 = S.rec[st][e][1], r2 = S.rec[st][e][2], r3 = S.rec[st][e][3];
       const float mu[3] = {r0.x, r0.y, r0.z};
       const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
       RayF rf;
@@ -1440,7 +550,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), (NP <= 4 ? 4 : 2)) k_render_lid
     __threadfence_block();
     named_arrive(BAR_FULL + b, NT);
   }
-  cp_async_wait0();
+  cp_async_wait<0>();
 }
 
 int32_t launch_check(const char* what) {
@@ -1467,104 +577,55 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   SIMULI_REQUIRE(T.tile_ray_offsets && T.tile_rays && T.ray_az && T.ray_el && T.ray_s && T.n_tiles >= 1,
                  "simuli_render_lidar: incomplete device tiling");
   SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(proj->record) % 16 == 0, "record must be 16-byte aligned");
-  static const bool use_v1 = [] {
-    const char* v = getenv("SIMULI_LIDAR_KERNEL");
-    return v && v[0] == 'v' && v[1] == '1';
-  }();
-  if (!use_v1) {
-    SIMULI_REQUIRE(T.elev_tile_beam_offsets && T.elev_tile_beams && T.az_tile_col_offsets && T.az_tile_cols,
-                   "simuli_render_lidar: device tiling lacks the beam / column CSR");
-    LidarV2Args A{};
-    A.record = reinterpret_cast<const float4*>(proj->record);
-    A.ids = sorted_ids;
-    A.ranges = reinterpret_cast<const int2*>(tile_ranges);
-    A.order = tile_order;
-    A.etb_off = T.elev_tile_beam_offsets; A.etb = T.elev_tile_beams;
-    A.atc_off = T.az_tile_col_offsets; A.atc = T.az_tile_cols;
-    A.ray_az = T.ray_az; A.ray_el = T.ray_el; A.ray_s = T.ray_s;
-    A.n_theta = T.n_theta; A.n_az = T.n_azimuth;
-    // work items: beam groups x column groups of <= 32 rays per tile, uniform over tiles
-    SIMULI_REQUIRE(T.max_beams_per_elev_tile >= 1 && T.max_cols_per_az_tile >= 1,
-                   "simuli_render_lidar: tiling maxima missing");
-    A.cg = T.max_cols_per_az_tile < 32 ? T.max_cols_per_az_tile : 32;
-    A.bg = 32 / A.cg;
-    A.n_cg = (T.max_cols_per_az_tile + A.cg - 1) / A.cg;
-    const int nbg = (T.max_beams_per_elev_tile + A.bg - 1) / A.bg;
-    A.items_per_tile = A.n_cg * nbg;
-    A.n_items = (int64_t)T.n_tiles * A.items_per_tile;
-    A.pose = make_pose_interp_d(P->pose_start, P->pose_end);
-    A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f;
-    A.near_tau = P->lidar->min_range_m;
-    A.alpha_min = rp->alpha_min; A.alpha_max = rp->alpha_max; A.T_min = rp->T_min;
-    A.zeta = out->zeta; A.opacity = out->opacity; A.depth_accum = out->depth_accum; A.depth = out->depth;
-    A.intensity = out->intensity; A.raydrop = out->raydrop; A.final_T = out->final_T; A.n_contrib = out->n_contrib;
-    A.ray_od = out->ray_od; A.n_visited = out->n_visited; A.n_inbox = out->n_inbox;
-    static const bool use_v2 = [] {
-      const char* v = getenv("SIMULI_LIDAR_KERNEL");
-      return v && v[0] == 'v' && v[1] == '2';
-    }();
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (use_v2) {
-      static bool attr2 = false;
-      if (!attr2) {
-        cudaFuncSetAttribute(k_render_lidar_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(V2Smem));
-        attr2 = true;
-      }
-      k_render_lidar_v2<<<(unsigned)A.n_items, 32 * kV2Warps, sizeof(V2Smem), st>>>(A);
-    } else {
-      const char* kv = getenv("SIMULI_LIDAR_KERNEL");
-      const std::string kind = kv ? kv : "v6_4";
-      auto launch_v3 = [&](auto np_tag) {
-        constexpr int NP = decltype(np_tag)::value;
-        cudaFuncSetAttribute(k_render_lidar_v3<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(V3Smem<NP>));
-        k_render_lidar_v3<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V3Smem<NP>), st>>>(A);
-      };
-      auto launch_v5 = [&](auto np_tag) {
-        constexpr int NP = decltype(np_tag)::value;
-        cudaFuncSetAttribute(k_render_lidar_v5<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(V5Smem<NP>));
-        k_render_lidar_v5<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V5Smem<NP>), st>>>(A);
-      };
-      auto launch_v6 = [&](auto np_tag) {
-        constexpr int NP = decltype(np_tag)::value;
-        cudaFuncSetAttribute(k_render_lidar_v6<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(V6Smem<NP>));
-        k_render_lidar_v6<NP><<<(unsigned)A.n_items, 32 * (NP + 1), sizeof(V6Smem<NP>), st>>>(A);
-      };
-      if (kind == "v6_4") launch_v6(std::integral_constant<int, 4>{});
-      else if (kind == "v6_2") launch_v6(std::integral_constant<int, 2>{});
-      else if (kind == "v6_8") launch_v6(std::integral_constant<int, 8>{});
-      else if (kind == "v3") launch_v3(std::integral_constant<int, 4>{});
-      else if (kind == "v3_2") launch_v3(std::integral_constant<int, 2>{});
-      else if (kind == "v5_8") launch_v5(std::integral_constant<int, 8>{});
-      else if (kind == "v5_2") launch_v5(std::integral_constant<int, 2>{});
-      else launch_v5(std::integral_constant<int, 4>{});
-    }
-    return launch_check("simuli_render_lidar");
-  }
+  SIMULI_REQUIRE(T.elev_tile_beam_offsets && T.elev_tile_beams && T.az_tile_col_offsets && T.az_tile_cols,
+                 "simuli_render_lidar: device tiling lacks the beam / column CSR");
+  SIMULI_REQUIRE(T.max_beams_per_elev_tile >= 1 && T.max_cols_per_az_tile >= 1,
+                 "simuli_render_lidar: tiling maxima missing");
   LidarArgs A{};
   A.record = reinterpret_cast<const float4*>(proj->record);
   A.ids = sorted_ids;
   A.ranges = reinterpret_cast<const int2*>(tile_ranges);
-  A.tile_ray_offsets = T.tile_ray_offsets;
-  A.tile_rays = T.tile_rays;
+  A.order = tile_order;
+  A.etb_off = T.elev_tile_beam_offsets; A.etb = T.elev_tile_beams;
+  A.atc_off = T.az_tile_col_offsets; A.atc = T.az_tile_cols;
   A.ray_az = T.ray_az; A.ray_el = T.ray_el; A.ray_s = T.ray_s;
-  A.n_tiles = T.n_tiles;
-  A.chunks_per_tile = (T.max_rays_in_tile + 31) / 32;
-  if (A.chunks_per_tile < 1) A.chunks_per_tile = 1;
+  A.n_theta = T.n_theta; A.n_az = T.n_azimuth;
+  // work items: beam groups x column groups of <= 32 rays per tile, uniform over tiles
+  A.cg = T.max_cols_per_az_tile < 32 ? T.max_cols_per_az_tile : 32;
+  A.bg = 32 / A.cg;
+  A.n_cg = (T.max_cols_per_az_tile + A.cg - 1) / A.cg;
+  const int nbg = (T.max_beams_per_elev_tile + A.bg - 1) / A.bg;
+  A.items_per_tile = A.n_cg * nbg;
+  A.n_items = (int64_t)T.n_tiles * A.items_per_tile;
   A.pose = make_pose_interp_d(P->pose_start, P->pose_end);
   A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f;
   A.near_tau = P->lidar->min_range_m;
   A.alpha_min = rp->alpha_min; A.alpha_max = rp->alpha_max; A.T_min = rp->T_min;
   A.zeta = out->zeta; A.opacity = out->opacity; A.depth_accum = out->depth_accum; A.depth = out->depth;
   A.intensity = out->intensity; A.raydrop = out->raydrop; A.final_T = out->final_T; A.n_contrib = out->n_contrib;
-  A.ray_od = out->ray_od;
-  A.n_visited = out->n_visited;
-  A.n_inbox = out->n_inbox;
-  const int64_t warps = (int64_t)T.n_tiles * A.chunks_per_tile;
-  const unsigned blocks = (unsigned)((warps + kWarpsPerCta - 1) / kWarpsPerCta);
-  k_render_lidar<<<blocks, 32 * kWarpsPerCta, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A);
+  A.ray_od = out->ray_od; A.n_visited = out->n_visited; A.n_inbox = out->n_inbox;
+  if (A.n_items == 0) return SIMULI_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto launch = [&](auto np_tag, auto stages_tag) {
+    constexpr int NP = decltype(np_tag)::value, STG = decltype(stages_tag)::value;
+    constexpr size_t smem = sizeof(LidarSmem<NP, STG>);
+    cudaFuncSetAttribute(k_render_lidar<NP, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_render_lidar<NP, STG><<<(unsigned)A.n_items, 32 * (NP + 1), smem, st>>>(A);
+  };
+  using std::integral_constant;
+  static const int variant = [] {
+    const char* v = getenv("SIMULI_LIDAR_VARIANT");  // tuning only: NP * 10 + STAGES
+    return v ? atoi(v) : 0;
+  }();
+  switch (variant) {
+    case 12: launch(integral_constant<int, 1>{}, integral_constant<int, 2>{}); break;
+    case 13: launch(integral_constant<int, 1>{}, integral_constant<int, 3>{}); break;
+    case 22: launch(integral_constant<int, 2>{}, integral_constant<int, 2>{}); break;
+    case 23: launch(integral_constant<int, 2>{}, integral_constant<int, 3>{}); break;
+    case 24: launch(integral_constant<int, 2>{}, integral_constant<int, 4>{}); break;
+    case 32: launch(integral_constant<int, 3>{}, integral_constant<int, 2>{}); break;
+    default: launch(integral_constant<int, kLidarNP>{}, integral_constant<int, kLidarStages>{}); break;
+  }
   return launch_check("simuli_render_lidar");
 }
 
@@ -1607,3 +668,9 @@ extern "C" int32_t simuli_render_camera(const simuli_projected* proj, const uint
   }
   return launch_check("simuli_render_camera");
 }
+
+#ifdef SIMULI_RENDER_PROFILE
+extern "C" int32_t simuli_debug_render_prof(long long* host, int64_t n) {
+  return cudaMemcpyFromSymbol(host, simuli::g_render_prof, sizeof(long long) * 4 * n) == cudaSuccess ? 0 : 3;
+}
+#endif

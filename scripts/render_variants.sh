@@ -1,0 +1,13 @@
+#!/bin/bash
+python -c "import __graft_entry__ as g; g.build()" >/dev/null || exit 1
+rm -f /tmp/rv_*.npz
+for k in ${@:-0}; do
+  SIMULI_LIDAR_VARIANT=$k SIMULI_LIDAR_KERNEL=$k python scripts/bench_render.py B /tmp/rv_$k.npz
+done
+python - <<'PY'
+import numpy as np, glob
+fs = sorted(glob.glob("/tmp/rv_*.npz")); base = np.load(fs[0])
+for f in fs[1:]:
+    d = np.load(f)
+    print(f, {k: float(np.abs(d[k].astype(np.float64) - base[k]).max()) for k in ("opacity", "depth", "zeta")})
+PY
