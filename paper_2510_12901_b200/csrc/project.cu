@@ -255,6 +255,7 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
   const float p0[3] = {(float)p0d[0], (float)p0d[1], (float)p0d[2]};
   const float rho0 = (float)rho0d, rho02 = (float)(rho0d * rho0d);
   bool ok = rho0d * rho0d + p0d[2] * p0d[2] >= (double)A.r_min * (double)A.r_min;
+  const float cxy2 = c[0] * c[0] + c[1] * c[1];
   float Sd = 0.f, Se = 0.f, Sdd = 0.f, See = 0.f, Sde = 0.f;
 #pragma unroll 1
   for (int k = 0; k < 3; ++k) {
@@ -270,8 +271,10 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
         D[0] = l[0]; D[1] = l[1]; D[2] = l[2];
       } else {
         // firing time of sigma point i (float32): start-frame azimuth relative to sigma point 0's
+        // (c x q, c . q) with q = c + l, written without the cancellation: (c x l, |c|^2 + c . l)
         const float q[3] = {c[0] + l[0], c[1] + l[1], c[2] + l[2]};
-        float s = wrap01(s_c + (float)A.dir * atan_ratio(c[0] * q[1] - c[1] * q[0], c[0] * q[0] + c[1] * q[1]) *
+        float s = wrap01(s_c + (float)A.dir *
+                                   atan_ratio(c[0] * l[1] - c[1] * l[0], cxy2 + c[0] * l[0] + c[1] * l[1]) *
                                    0.15915494309189535f);
         for (int it = 1; it < A.K; ++it) {
           float sn, omc, p[3];
