@@ -369,10 +369,57 @@ def run_gpu(args):
             "wall_s_timed_region": wall}
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene_np, cfg)
+    if ws == 1 and not args.no_secondary:
+        del r
+        torch.cuda.empty_cache()
+        line["secondary"] = secondary_configs(dev)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def secondary_configs(dev, steps=20, warmup=3):
+    """The other full-size BASELINE.json configs, device time per scan / frame with the L2
+    flushed between scans (not the headline): C = Waymo-top-like LiDAR, 64 x 2650 rays,
+    4M particles; D = KB fisheye rolling-shutter camera 1920 x 1080, 2M particles."""
+    import torch
+
+    from paper_2510_12901_b200 import simuli as SM
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    out = {}
+
+    def timed(obj, n_units, unit):
+        obj.keep_keys = False
+        for _ in range(warmup):
+            obj.project(); obj.bin_sort(sync_capacity=True); obj.render()
+        torch.cuda.synchronize()
+        st = {"project": [], "bin_sort": [], "render": []}
+        for _ in range(steps):
+            flush.zero_()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record(); obj.project(); ev[1].record(); obj.bin_sort(); ev[2].record(); obj.render(); ev[3].record()
+            torch.cuda.synchronize()
+            for k, (a, b) in zip(st, ((0, 1), (1, 2), (2, 3))):
+                st[k].append(ev[a].elapsed_time(ev[b]))
+        ms = sum(statistics.median(v) for v in st.values())
+        return {"value": n_units / (ms * 1e-3), "unit": unit, "ms_per_step": ms,
+                "stages_ms": {k: statistics.median(v) for k, v in st.items()}, "pairs": int(obj.n_pairs.item()),
+                "steps": steps}
+
+    cfg = synth.lidar_config("C")
+    r = SM.LidarRenderer(cfg, SM.to_device_scene(synth.scene_for("C"), dev), device=dev)
+    out["C"] = dict(timed(r, r.n_rays, "rays/s"), workload="C: Waymo-top-like 64x2650 rays (non-uniform beams), "
+                    "4M particles, rolling shutter (1.5 m, 0.02 rad)")
+    del r
+    torch.cuda.empty_cache()
+    cam = synth.camera_config("D")
+    c = SM.CameraRenderer(cam, SM.to_device_scene(synth.scene_for("D"), dev), device=dev)
+    out["D"] = dict(timed(c, cam.width * cam.height, "pixels/s"), workload="D: KB fisheye 1920x1080, rolling "
+                    "shutter (30 ms, 0.3 m, 0.009 rad), 2M camera particles, 16x16 px tiles")
+    del c
+    torch.cuda.empty_cache()
+    return out
 
 
 def cpu_baseline(scene_np, cfg):
@@ -395,6 +442,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the configs C and D lines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -14,4 +14,4 @@ timeout 600 python bench.py > $out/bench.json 2> $out/bench.err; echo "bench rc=
 cat $out/bench.json | head -c 3000; echo
 tail -5 $out/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $out/ncu_launch.log 2>&1; echo "ncu rc=$?"
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-secondary > $out/ncu_launch.log 2>&1; echo "ncu rc=$?"
