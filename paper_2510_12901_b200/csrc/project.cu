@@ -256,6 +256,7 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
   const float rho0 = (float)rho0d, rho02 = (float)(rho0d * rho0d);
   bool ok = rho0d * rho0d + p0d[2] * p0d[2] >= (double)A.r_min * (double)A.r_min;
   const float cxy2 = c[0] * c[0] + c[1] * c[1];
+  const bool pax = rho0d > 0.0, pnz = pax || p0d[2] != 0.0;  // sigma point 0 off the sensor axis / origin
   float Sd = 0.f, Se = 0.f, Sdd = 0.f, See = 0.f, Sde = 0.f;
 #pragma unroll 1
   for (int k = 0; k < 3; ++k) {
@@ -273,11 +274,13 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
         // firing time of sigma point i (float32): start-frame azimuth relative to sigma point 0's
         // (c x q, c . q) with q = c + l, written without the cancellation: (c x l, |c|^2 + c . l);
         // c on the z axis: sigma point 0's azimuth is atan2(0, 0) = 0 (A21), so q's own azimuth
+        // (atan_ratio(y, x) is atan2(y, x) for any arguments)
         const float q[3] = {c[0] + l[0], c[1] + l[1], c[2] + l[2]};
-        float s = cxy2 > 0.f ? wrap01(s_c + (float)A.dir *
-                                                atan_ratio(c[0] * l[1] - c[1] * l[0], cxy2 + c[0] * l[0] + c[1] * l[1]) *
-                                                0.15915494309189535f)
-                             : fire_time(A, q[0], q[1]);
+        const bool cax = cxy2 > 0.f;
+        float s = wrap01(s_c + (float)A.dir *
+                                   atan_ratio(cax ? c[0] * l[1] - c[1] * l[0] : q[1],
+                                              cax ? cxy2 + c[0] * l[0] + c[1] * l[1] : q[0]) *
+                                   0.15915494309189535f);
         for (int it = 1; it < A.K; ++it) {
           float sn, omc, p[3];
           rot_sc_f(A, s, &sn, &omc);
@@ -306,14 +309,13 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
       ok = ok && rho2 + pz * pz >= A.r_min * A.r_min;
       // azimuth offset: atan2(p0 x p_i, p0 . p_i) in the xy plane (A21 unwrap about p0); p0 on
       // the z axis has azimuth atan2(0, 0) = 0 (A21), so the offset is p_i's own azimuth
-      const float d = rho0d > 0.0 ? atan_ratio(p0[0] * D[1] - p0[1] * D[0], rho02 + xy) : atan2f(D[1], D[0]);
+      const float d = atan_ratio(pax ? p0[0] * D[1] - p0[1] * D[0] : D[1], pax ? rho02 + xy : D[0]);
       // elevation offset: atan2(pz_i rho0 - pz0 rho_i, rho_i rho0 + pz_i pz0) with
       // rho_i - rho0 = (2 p0.D + |D|^2) / (rho_i + rho0)
       const float rho = sqrtf(rho2);
       const float drho = __fdividef(2.f * xy + dxy2, rho + rho0);
       // (p0 = 0: elevation atan2(0, 0) = 0, the offset is p_i's own elevation)
-      const float e = (rho0d > 0.0 || p0d[2] != 0.0) ? atan_ratio(D[2] * rho0 - p0[2] * drho, rho * rho0 + pz * p0[2])
-                                                      : atan2f(D[2], rho);
+      const float e = atan_ratio(pnz ? D[2] * rho0 - p0[2] * drho : D[2], pnz ? rho * rho0 + pz * p0[2] : rho);
       Sd += d;
       Se += e;
       Sdd = fmaf(d, d, Sdd);
