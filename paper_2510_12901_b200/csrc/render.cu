@@ -8,7 +8,7 @@
 //
 // LiDAR (k_render_lidar): one CTA per work item = (tile, beam group, column group) of <= 32
 // rays, items scheduled longest-list-first.  Warp-specialised pipeline over rounds of
-// E = 32 NP list entries:
+// E = 32 NP list entries (NP = 4 producer warps, one consumer warp):
 //  * producers (NP warps, thread = list entry): the round's 80-byte records arrive by
 //    cp.async, issued STAGES - 1 rounds ahead (a ring of record stages); each entry's
 //    exact A12 ray mask, factorised as (columns inside the azimuth interval) x (beams inside
@@ -234,13 +234,13 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
   return x;
 }
 
-template <int NP, int STAGES>
+template <int NP, int STAGES, int SLOTB>
 struct LidarSmem {
   float4 rec[STAGES][32 * NP][5];  // record ring (cp.async, STAGES - 1 rounds ahead)
-  float2 at[2][32][32 * NP];       // ray-major (alpha, tau) of member pairs, per slot buffer
-  uint8_t ent[2][32][32 * NP];     // ray-major entry index within the round
-  float4 feat[2][32 * NP];         // (sigma, features) of the round's entries
-  uint32_t memb[2][NP][32];        // [warp][ray] member entries of the warp's 32
+  float2 at[SLOTB][32][32 * NP];   // ray-major (alpha, tau) of member pairs, per slot buffer
+  uint8_t ent[SLOTB][32][32 * NP]; // ray-major entry index within the round
+  float4 feat[SLOTB][32 * NP];     // (sigma, features) of the round's entries
+  uint32_t memb[SLOTB][NP][32];    // [warp][ray] member entries of the warp's 32
   int rowoff[NP][32];              // members of ray r in warps before w (current round)
   uint16_t plist[NP][1024];        // the warp's member pairs (entry << 5 | ray)
   float ray_oh[32][3], ray_ol[32][3], ray_dh[32][3], ray_dl[32][3];
@@ -259,19 +259,25 @@ __device__ __forceinline__ long long gtime() {
 }
 #endif
 
-// LiDAR pipeline shape: 2 producer warps (64 list entries per round), 2 record stages
-// (prefetch 1 round ahead); ~54 KB shared memory -> 4 CTAs per SM.  Measured on config B
-// (render only, L2 flushed): (NP, stages) = (2, 2) 200 us, (2, 3) 238, (2, 4) 240, (1, 2) 281,
-// (3, 2) 295 -- residency beats prefetch depth (the deeper ring costs a CTA per SM).
-constexpr int kLidarNP = 2, kLidarStages = 2;
+// LiDAR pipeline shape: 4 producer warps (128 list entries per round), 2 record stages, one
+// slot buffer (~69 KB shared memory, 3 CTAs per SM).  Render-only means over 10 poses of the
+// B-batch trajectory, L2 flushed (NP, stages, slot buffers):
+//   config B: (4,2,1) 260 us [252-275], (3,2,1) 254 [215-305], (2,2,2) 266 [211-324],
+//             (2,2,1) 296, (2,3,1) 295, (4,2,2) 298;
+//   config C: (4,2,1) 489 us, (3,2,1) 554, (2,2,2) 664.
+// Fewer, larger rounds keep the long near-field lists off the critical path.
+constexpr int kLidarNP = 4, kLidarStages = 2, kLidarSlotBuffers = 1;
 
-template <int NP, int STAGES>
+// SLOTB = 2: double-buffered slots, producers up to two rounds ahead of the consumer;
+// SLOTB = 1: one slot buffer (less shared memory, more CTAs per SM), producers wait for the
+// consumer's previous round after their box tests, before writing the slots.
+template <int NP, int STAGES, int SLOTB>
 __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarArgs A) {
   constexpr int E = 32 * NP;
   constexpr int NT = 32 * (NP + 1);
   constexpr int BAR_PROD = 1, BAR_FULL = 2, BAR_EMPTY = 4, BAR_RAYS = 6;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LidarSmem<NP, STAGES>& S = *reinterpret_cast<LidarSmem<NP, STAGES>*>(smem_raw);
+  LidarSmem<NP, STAGES, SLOTB>& S = *reinterpret_cast<LidarSmem<NP, STAGES, SLOTB>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef SIMULI_RENDER_PROFILE
   const long long t_start = gtime();
@@ -336,36 +342,36 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
     int ncontrib = 0, nv = 0, ni = 0;
     bool done = lane >= R;
     for (int r = 0; r < n_rounds; ++r) {
-      const int b = r & 1;
+      const int b = r & 1, sb = SLOTB == 2 ? b : 0;
       named_sync(BAR_FULL + b, NT);
       const int start = rg.x + r * E;
       if (!done) {
         const int n_in = min(E, rg.y - start);
         int cnt = 0;
 #pragma unroll
-        for (int w = 0; w < NP; ++w) cnt += __popc(S.memb[b][w][lane]);
+        for (int w = 0; w < NP; ++w) cnt += __popc(S.memb[sb][w][lane]);
         bool stopped = false;
         // phase 1: the transmittance chain only (weights written back in place); branch-free
         // so the slot loads of later members are issued ahead of the chain
         int stop_k = -1;
 #pragma unroll 4
         for (int k = 0; k < cnt; ++k) {
-          const float2 a = S.at[b][lane][k];
+          const float2 a = S.at[sb][lane][k];
           const bool take = !(a.y < A.near_tau || a.x < A.alpha_min) && stop_k < 0;
           const float Tn = T * (1.f - a.x);
           const bool term = take && Tn < A.T_min;
           stop_k = term ? k : stop_k;
           const bool comp = take && !term;
-          S.at[b][lane][k].x = comp ? a.x * T : 0.f;
+          S.at[sb][lane][k].x = comp ? a.x * T : 0.f;
           T = comp ? Tn : T;
         }
         // phase 2: accumulate the weighted features / depths in member order
         const int kend = stop_k >= 0 ? stop_k : cnt;
 #pragma unroll 4
         for (int k = 0; k < kend; ++k) {
-          const float2 wt = S.at[b][lane][k];
+          const float2 wt = S.at[sb][lane][k];
           if (wt.x == 0.f) continue;  // skipped member (alpha < alpha_min or behind the origin)
-          const float4 f = S.feat[b][S.ent[b][lane][k]];
+          const float4 f = S.feat[sb][S.ent[sb][lane][k]];
           acc0 = fmaf(wt.x, f.y, acc0);
           acc1 = fmaf(wt.x, f.z, acc1);
           acc2 = fmaf(wt.x, f.w, acc2);
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
         }
         if (stop_k >= 0) {
           stopped = true;
-          nv += S.ent[b][lane][stop_k] + 1;
+          nv += S.ent[sb][lane][stop_k] + 1;
           ni += stop_k + 1;
         }
         if (stopped) done = true;
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
 #ifdef SIMULI_RENDER_PROFILE
       rounds_run = r + 1;
 #endif
-      if (r + 2 < n_rounds) {
+      if (r + SLOTB < n_rounds) {
         if (lane == 0) {
           S.stop_at[b] = all ? 1 : 0;
           S.done_mask[b] = dmask;
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
         named_arrive(BAR_EMPTY + b, NT);
       }
       if (all) {
-        if (r + 1 < n_rounds) named_sync(BAR_FULL + (b ^ 1), NT);  // drain the round in flight
+        if (SLOTB == 2 && r + 1 < n_rounds) named_sync(BAR_FULL + (b ^ 1), NT);  // drain the round in flight
         break;
       }
     }
@@ -462,8 +468,8 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
   named_sync(BAR_RAYS, NT);
   uint32_t alive = 0xffffffffu;  // rays the consumer has not terminated (2 rounds behind)
   for (int r = 0; r < n_rounds; ++r) {
-    const int b = r & 1, st = r % STAGES;
-    if (r >= 2) {
+    const int b = r & 1, st = r % STAGES, sb = SLOTB == 2 ? b : 0;
+    if (SLOTB == 2 && r >= 2) {
       named_sync(BAR_EMPTY + b, NT);
       if (S.stop_at[b]) break;
       alive = ~S.done_mask[b];
@@ -477,7 +483,6 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
     uint32_t m = 0;
     if (valid) {
       const float4 bx = S.rec[st][tid][4];
-      S.feat[b][tid] = S.rec[st][tid][3];
       uint32_t colbits = 0;
       if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
         colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
@@ -496,9 +501,15 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
           if (bx.z <= w && w <= bx.w) m |= colbits << (bi * nc);
         }
     }
+    if (SLOTB == 1 && r >= 1) {  // the consumer is done with round r - 1's slots
+      named_sync(BAR_EMPTY + (b ^ 1), NT);
+      if (S.stop_at[b ^ 1]) break;
+      alive = ~S.done_mask[b ^ 1];
+    }
+    if (valid) S.feat[sb][tid] = S.rec[st][tid][3];
     m &= alive;  // no member pairs for terminated rays
     const uint32_t my = warp_transpose32(m, lane);  // lane r: entries of this warp holding ray r
-    S.memb[b][warp][lane] = my;
+    S.memb[sb][warp][lane] = my;
     const int k = __popc(m);
     int inc = k;
 #pragma unroll
@@ -522,14 +533,14 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
       int off = 0;
 #pragma unroll
       for (int w = 0; w < NP; ++w)
-        if (w < warp) off += __popc(S.memb[b][w][lane]);
+        if (w < warp) off += __popc(S.memb[sb][w][lane]);
       S.rowoff[warp][lane] = off;
     }
     __syncwarp();
     for (int idx = lane; idx < K; idx += 32) {
       const int v = S.plist[warp][idx];
       const int rr = v & 31, el = v >> 5, e = warp * 32 + el;
-      const int slot = S.rowoff[warp][rr] + __popc(S.memb[b][warp][rr] & ((1u << el) - 1u));
+      const int slot = S.rowoff[warp][rr] + __popc(S.memb[sb][warp][rr] & ((1u << el) - 1u));
       const float4 r0 = S.rec[st][e][0], r1 = S.rec[st][e][1], r2 = S.rec[st][e][2], r3 = S.rec[st][e][3];
       const float mu[3] = {r0.x, r0.y, r0.z};
       const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
@@ -543,8 +554,8 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
       }
       float tau, d2;
       response(rf, mu, M, &tau, &d2);
-      S.at[b][rr][slot] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
-      S.ent[b][rr][slot] = (uint8_t)e;
+      S.at[sb][rr][slot] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
+      S.ent[sb][rr][slot] = (uint8_t)e;
     }
     __syncwarp();
     __threadfence_block();
@@ -606,25 +617,30 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   A.ray_od = out->ray_od; A.n_visited = out->n_visited; A.n_inbox = out->n_inbox;
   if (A.n_items == 0) return SIMULI_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  auto launch = [&](auto np_tag, auto stages_tag) {
-    constexpr int NP = decltype(np_tag)::value, STG = decltype(stages_tag)::value;
-    constexpr size_t smem = sizeof(LidarSmem<NP, STG>);
-    cudaFuncSetAttribute(k_render_lidar<NP, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_render_lidar<NP, STG><<<(unsigned)A.n_items, 32 * (NP + 1), smem, st>>>(A);
+  auto launch = [&](auto np_tag, auto stages_tag, auto slot_tag) {
+    constexpr int NP = decltype(np_tag)::value, STG = decltype(stages_tag)::value, SB = decltype(slot_tag)::value;
+    constexpr size_t smem = sizeof(LidarSmem<NP, STG, SB>);
+    cudaFuncSetAttribute(k_render_lidar<NP, STG, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_render_lidar<NP, STG, SB><<<(unsigned)A.n_items, 32 * (NP + 1), smem, st>>>(A);
   };
   using std::integral_constant;
   static const int variant = [] {
-    const char* v = getenv("SIMULI_LIDAR_VARIANT");  // tuning only: NP * 10 + STAGES
+    const char* v = getenv("SIMULI_LIDAR_VARIANT");  // tuning only
     return v ? atoi(v) : 0;
   }();
-  switch (variant) {
-    case 12: launch(integral_constant<int, 1>{}, integral_constant<int, 2>{}); break;
-    case 13: launch(integral_constant<int, 1>{}, integral_constant<int, 3>{}); break;
-    case 22: launch(integral_constant<int, 2>{}, integral_constant<int, 2>{}); break;
-    case 23: launch(integral_constant<int, 2>{}, integral_constant<int, 3>{}); break;
-    case 24: launch(integral_constant<int, 2>{}, integral_constant<int, 4>{}); break;
-    case 32: launch(integral_constant<int, 3>{}, integral_constant<int, 2>{}); break;
-    default: launch(integral_constant<int, kLidarNP>{}, integral_constant<int, kLidarStages>{}); break;
+  using I1 = integral_constant<int, 1>;
+  using I2 = integral_constant<int, 2>;
+  using I3 = integral_constant<int, 3>;
+  using I4 = integral_constant<int, 4>;
+  switch (variant) {  // NP * 100 + STAGES * 10 + SLOTB
+    case 221: launch(I2{}, I2{}, I1{}); break;
+    case 231: launch(I2{}, I3{}, I1{}); break;
+    case 421: launch(I4{}, I2{}, I1{}); break;
+    case 321: launch(I3{}, I2{}, I1{}); break;
+    case 422: launch(I4{}, I2{}, I2{}); break;
+    case 222: launch(I2{}, I2{}, I2{}); break;
+    default: launch(integral_constant<int, kLidarNP>{}, integral_constant<int, kLidarStages>{},
+                    integral_constant<int, kLidarSlotBuffers>{}); break;
   }
   return launch_check("simuli_render_lidar");
 }

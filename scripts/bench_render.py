@@ -10,7 +10,7 @@ cfg, scene = synth.lidar_config(name), synth.scene_for(name)
 r = SM.LidarRenderer(cfg, SM.to_device_scene(scene))
 r.keep_keys = False
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-poses = synth.batch_poses(210)[::21] if name == "B" else [(cfg.pose_start, cfg.pose_end)]
+poses = synth.batch_poses(210)[::21] if name in ("B", "C") else [(cfg.pose_start, cfg.pose_end)]
 per_pose = []
 for p0, p1 in poses:  # the B-batch trajectory (bench.py's workload), 10 poses across it
     r.scan(p0, p1, sync_capacity=True)

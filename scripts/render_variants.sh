@@ -2,7 +2,7 @@
 python -c "import __graft_entry__ as g; g.build()" >/dev/null || exit 1
 rm -f /tmp/rv_*.npz
 for k in ${@:-0}; do
-  SIMULI_LIDAR_VARIANT=$k SIMULI_LIDAR_KERNEL=$k python scripts/bench_render.py B /tmp/rv_$k.npz
+  SIMULI_LIDAR_VARIANT=$k python scripts/bench_render.py ${CFG:-B} /tmp/rv_$k.npz
 done
 python - <<'PY'
 import numpy as np, glob
