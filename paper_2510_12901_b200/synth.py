@@ -341,12 +341,31 @@ def scene_for(config: str, seed: int | None = None, n: int | None = None) -> dic
         return corridor_scene(1003 if seed is None else seed, n or 4_000_000, x_range=(-200.0, 200.0))
     if config == "D":
         return corridor_scene(1004 if seed is None else seed, n or 2_000_000, kind="camera", ego=(1.5, 0.0, 1.6))
+    if config == "E-lidar":  # config E: one 4M G_l + 4M G_c corridor scene, x in [-200, 200]
+        return corridor_scene(1005 if seed is None else seed, n or 4_000_000, x_range=(-200.0, 200.0))
+    if config == "E-camera":
+        return corridor_scene(1006 if seed is None else seed, n or 4_000_000, x_range=(-200.0, 200.0),
+                              kind="camera", ego=(1.5, 0.0, 1.6))
     if config == "tiny":
         s = 0 if seed is None else seed
         rng = np.random.default_rng(10_000 + s)
         return random_shell_scene(s, n or int(rng.integers(50, 500)), r_lo=1.0, r_hi=12.0,
                                   el_lo=-30.0, el_hi=20.0, s_lo=0.03, s_hi=0.6)
     raise ValueError(config)
+
+
+def e_poses(n: int = 64):
+    """Config E: n poses along x = -32 .. +31 m (1 m steps, yaw +-0.02
+    alternating); scan i is C-type with 1.5 m / 0.02 rad of intra-scan motion, frame i is
+    D-type (rolling shutter over 30 ms: +0.3 m, +0.009 rad) from the same pose."""
+    scans, frames = [], []
+    for i in range(n):
+        x = -32.0 + i
+        yaw = 0.02 * (1 if i % 2 else -1)
+        scans.append((pose(yaw_quat(yaw), [x, 0.0, 1.8]), pose(yaw_quat(yaw + 0.02), [x + 1.5, 0.0, 1.8])))
+        frames.append((pose(yaw_quat(yaw, CAM_FORWARD_Q), [x + 1.5, 0.0, 1.6]),
+                       pose(yaw_quat(yaw + 0.009, CAM_FORWARD_Q), [x + 1.8, 0.0, 1.6])))
+    return scans, frames
 
 
 def batch_poses(n_scans: int, x_lo: float = -51.0, step: float = 0.2, motion: float = 1.0,
