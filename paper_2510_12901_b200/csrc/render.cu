@@ -237,8 +237,11 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 template <int NP, int STAGES, int SLOTB>
 struct LidarSmem {
   float4 rec[STAGES][32 * NP][5];  // record ring (cp.async, STAGES - 1 rounds ahead)
-  float2 at[SLOTB][32][32 * NP];   // ray-major (alpha, tau) of member pairs, per slot buffer
-  uint8_t ent[SLOTB][32][32 * NP]; // ray-major entry index within the round
+  // ray-major slots, rows padded so that the consumer's lane-per-ray accesses (lane r reads
+  // row r) hit distinct banks: without the pad every row starts in the same bank and each
+  // consumer load / store was a 32-way conflict
+  float2 at[SLOTB][32][32 * NP + 1];   // (alpha, tau) of member pairs, per slot buffer
+  uint8_t ent[SLOTB][32][32 * NP + 4]; // entry index within the round
   float4 feat[SLOTB][32 * NP];     // (sigma, features) of the round's entries
   uint32_t memb[SLOTB][NP][32];    // [warp][ray] member entries of the warp's 32
   int rowoff[NP][32];              // members of ray r in warps before w (current round)
@@ -252,11 +255,21 @@ struct LidarSmem {
 
 #ifdef SIMULI_RENDER_PROFILE
 __device__ long long g_render_prof[1 << 20];  // per item: start ns, end ns, rounds run, list length | smid << 32
+__device__ long long g_render_trace[64][16];  // item traced: clock64 marks per round (see RMARK)
+__device__ int g_render_trace_item;
+#define RMARK(r, k)                                                                                  \
+  do {                                                                                               \
+    if (blockIdx.x == (unsigned)g_render_trace_item && (r) < 64 && (threadIdx.x & 31) == 0) g_render_trace[(r)][(k)] = clock64(); \
+  } while (0)
 __device__ __forceinline__ long long gtime() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#else
+#define RMARK(r, k) \
+  do {              \
+  } while (0)
 #endif
 
 // LiDAR pipeline shape: 4 producer warps (128 list entries per round), 2 record stages, one
@@ -343,7 +356,9 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
     bool done = lane >= R;
     for (int r = 0; r < n_rounds; ++r) {
       const int b = r & 1, sb = SLOTB == 2 ? b : 0;
+      RMARK(r, 8);
       named_sync(BAR_FULL + b, NT);
+      RMARK(r, 9);
       const int start = rg.x + r * E;
       if (!done) {
         const int n_in = min(E, rg.y - start);
@@ -351,37 +366,49 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
 #pragma unroll
         for (int w = 0; w < NP; ++w) cnt += __popc(S.memb[sb][w][lane]);
         bool stopped = false;
-        // phase 1: the transmittance chain only (weights written back in place); branch-free
-        // so the slot loads of later members are issued ahead of the chain
-        int stop_k = -1;
-#pragma unroll 4
-        for (int k = 0; k < cnt; ++k) {
-          const float2 a = S.at[sb][lane][k];
-          const bool take = !(a.y < A.near_tau || a.x < A.alpha_min) && stop_k < 0;
-          const float Tn = T * (1.f - a.x);
-          const bool term = take && Tn < A.T_min;
-          stop_k = term ? k : stop_k;
-          const bool comp = take && !term;
-          S.at[sb][lane][k].x = comp ? a.x * T : 0.f;
-          T = comp ? Tn : T;
+        // one pass over the ray's slots in list order; the slot loads run two members ahead
+        // and the feature load (indexed by the entry) one ahead, off the transmittance chain
+        int stop_k = -1, stop_e = 0;
+        if (cnt > 0) {
+          float2 a1 = S.at[sb][lane][0], a2 = make_float2(0.f, 0.f);
+          int e1 = S.ent[sb][lane][0], e2 = 0;
+          if (cnt > 1) {
+            a2 = S.at[sb][lane][1];
+            e2 = S.ent[sb][lane][1];
+          }
+          float4 f1 = S.feat[sb][e1];
+          for (int k = 0; k < cnt; ++k) {
+            const float2 a = a1;
+            const float4 f = f1;
+            const int e = e1;
+            a1 = a2;
+            e1 = e2;
+            if (k + 2 < cnt) {
+              a2 = S.at[sb][lane][k + 2];
+              e2 = S.ent[sb][lane][k + 2];
+            }
+            if (k + 1 < cnt) f1 = S.feat[sb][e1];
+            if (a.y < A.near_tau || a.x < A.alpha_min) continue;  // skipped member
+            const float Tn = T * (1.f - a.x);
+            if (Tn < A.T_min) {  // terminated: this member is not composited (A14)
+              stop_k = k;
+              stop_e = e;
+              break;
+            }
+            const float w = a.x * T;
+            acc0 = fmaf(w, f.y, acc0);
+            acc1 = fmaf(w, f.z, acc1);
+            acc2 = fmaf(w, f.w, acc2);
+            D = fmaf(w, a.y, D);
+            W += w;
+            ++ncontrib;
+            T = Tn;
+          }
         }
-        // phase 2: accumulate the weighted features / depths in member order
-        const int kend = stop_k >= 0 ? stop_k : cnt;
-#pragma unroll 4
-        for (int k = 0; k < kend; ++k) {
-          const float2 wt = S.at[sb][lane][k];
-          if (wt.x == 0.f) continue;  // skipped member (alpha < alpha_min or behind the origin)
-          const float4 f = S.feat[sb][S.ent[sb][lane][k]];
-          acc0 = fmaf(wt.x, f.y, acc0);
-          acc1 = fmaf(wt.x, f.z, acc1);
-          acc2 = fmaf(wt.x, f.w, acc2);
-          D = fmaf(wt.x, wt.y, D);
-          W += wt.x;
-          ++ncontrib;
-        }
+        RMARK(r, 10);
         if (stop_k >= 0) {
           stopped = true;
-          nv += S.ent[sb][lane][stop_k] + 1;
+          nv += stop_e + 1;
           ni += stop_k + 1;
         }
         if (stopped) done = true;
@@ -392,6 +419,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
       }
       const uint32_t dmask = __ballot_sync(0xffffffffu, done);
       const bool all = dmask == 0xffffffffu;
+      RMARK(r, 11);
 #ifdef SIMULI_RENDER_PROFILE
       rounds_run = r + 1;
 #endif
@@ -469,6 +497,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
   uint32_t alive = 0xffffffffu;  // rays the consumer has not terminated (2 rounds behind)
   for (int r = 0; r < n_rounds; ++r) {
     const int b = r & 1, st = r % STAGES, sb = SLOTB == 2 ? b : 0;
+    if (warp == 0) RMARK(r, 0);
     if (SLOTB == 2 && r >= 2) {
       named_sync(BAR_EMPTY + b, NT);
       if (S.stop_at[b]) break;
@@ -476,7 +505,9 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
     }
     const int start = rg.x + r * E;
     cp_async_wait<D - 1>();   // this thread's copies of round r have landed
+    if (warp == 0) RMARK(r, 1);
     named_sync(BAR_PROD, E);  // everyone's: round r's records visible; stage of round r - 1 and rowoff free
+    if (warp == 0) RMARK(r, 2);
     issue(r + D, id_pf);
     id_pf = load_id(r + D + 1);
     const bool valid = start + tid < rg.y;
@@ -489,23 +520,41 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
       } else {
         const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
         const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
-        for (int ci = 0; ci < nc; ++ci) {
+        // the usual item has <= 8 columns and <= 4 beams: fixed-trip unrolled, independent
+        // compares (general shapes fall through to the loops)
+#pragma unroll
+        for (int ci = 0; ci < 8; ++ci) {
+          const float p = S.col_phi[ci];
+          const bool in = ci < nc && ((bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2);
+          colbits |= (uint32_t)in << ci;
+        }
+        for (int ci = 8; ci < nc; ++ci) {
           const float p = S.col_phi[ci];
           const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
           colbits |= (uint32_t)in << ci;
         }
       }
-      if (colbits)
-        for (int bi = 0; bi < nb; ++bi) {
+      if (colbits) {
+        uint32_t beambits = 0;
+#pragma unroll
+        for (int bi = 0; bi < 4; ++bi) {
           const float w = S.beam_el[bi];
-          if (bx.z <= w && w <= bx.w) m |= colbits << (bi * nc);
+          beambits |= (uint32_t)(bi < nb && bx.z <= w && w <= bx.w) << bi;
         }
+        for (int bi = 4; bi < nb; ++bi) {
+          const float w = S.beam_el[bi];
+          beambits |= (uint32_t)(bx.z <= w && w <= bx.w) << bi;
+        }
+        for (uint32_t bb = beambits; bb; bb &= bb - 1u) m |= colbits << ((__ffs(bb) - 1) * nc);
+      }
     }
+    if (warp == 0) RMARK(r, 3);
     if (SLOTB == 1 && r >= 1) {  // the consumer is done with round r - 1's slots
       named_sync(BAR_EMPTY + (b ^ 1), NT);
       if (S.stop_at[b ^ 1]) break;
       alive = ~S.done_mask[b ^ 1];
     }
+    if (warp == 0) RMARK(r, 4);
     if (valid) S.feat[sb][tid] = S.rec[st][tid][3];
     m &= alive;  // no member pairs for terminated rays
     const uint32_t my = warp_transpose32(m, lane);  // lane r: entries of this warp holding ray r
@@ -528,7 +577,9 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
         S.plist[warp][pos++] = (uint16_t)((lane << 5) | rr);
       }
     }
+    if (warp == 0) RMARK(r, 5);
     named_sync(BAR_PROD, E);  // every producer warp's member words are in
+    if (warp == 0) RMARK(r, 6);
     {
       int off = 0;
 #pragma unroll
@@ -559,6 +610,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
     }
     __syncwarp();
     __threadfence_block();
+    if (warp == 0) RMARK(r, 7);
     named_arrive(BAR_FULL + b, NT);
   }
   cp_async_wait<0>();
@@ -686,6 +738,10 @@ extern "C" int32_t simuli_render_camera(const simuli_projected* proj, const uint
 }
 
 #ifdef SIMULI_RENDER_PROFILE
+extern "C" int32_t simuli_debug_render_trace(long long* host, int item) {
+  cudaMemcpyToSymbol(simuli::g_render_trace_item, &item, sizeof(int));
+  return cudaMemcpyFromSymbol(host, simuli::g_render_trace, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 3;
+}
 extern "C" int32_t simuli_debug_render_prof(long long* host, int64_t n) {
   return cudaMemcpyFromSymbol(host, simuli::g_render_prof, sizeof(long long) * 4 * n) == cudaSuccess ? 0 : 3;
 }

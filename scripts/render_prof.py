@@ -38,3 +38,23 @@ busy = np.zeros(200)
 for s_, e_, m in zip(st, en, sm):
     busy[m] += e_ - s_
 print(f"per-SM busy (sum of item durations): mean {busy[:148].mean():.1f} max {busy[:148].max():.1f} us")
+
+# per-round phase trace of one long item (clock64 marks, RMARK in render.cu)
+item = int(np.argmax(dur))  # the longest item of the timeline above
+tr = np.zeros(64 * 16, np.int64)
+L.simuli_debug_render_trace(tr.ctypes.data_as(C.c_void_p), C.c_int(int(item)))  # select the item
+flush.zero_(); r.render(); torch.cuda.synchronize()
+L.simuli_debug_render_trace(tr.ctypes.data_as(C.c_void_p), C.c_int(int(item)))
+tr = tr.reshape(64, 16).astype(np.float64)
+names = ["p:start", "p:cp.wait", "p:BAR_PROD1", "p:boxtest", "p:EMPTY", "p:plist", "p:BAR_PROD2", "p:resp",
+         "c:start", "c:FULL", "c:phase1", "c:end"]
+print(f"item {item}: per-round phase durations (cycles), rounds 2..12:")
+for rr in range(2, 13):
+    row = tr[rr]
+    if row[0] == 0:
+        break
+    p = [row[k + 1] - row[k] for k in range(0, 7)]
+    c = [row[k + 1] - row[k] for k in range(8, 11)]
+    print(f"  r{rr:2d} prod " + " ".join(f"{names[k+1]}={v:6.0f}" for k, v in enumerate(p)) +
+          " | cons " + " ".join(f"{names[8 + k + 1]}={v:6.0f}" for k, v in enumerate(c)) +
+          f" | round {tr[rr + 1][0] - row[0] if tr[rr + 1][0] else 0:6.0f}")
