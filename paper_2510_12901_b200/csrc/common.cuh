@@ -175,6 +175,27 @@ __device__ __forceinline__ void sh_eval(const float* __restrict__ sh, int degree
   out[0] = r0; out[1] = r1; out[2] = r2;
 }
 
+// The 16 real SH basis values of degree <= 3 at the unit direction (x, y, z)
+__device__ __forceinline__ void sh_basis3(float x, float y, float z, float b[16]) {
+  const float xx = x * x, yy = y * y, zz = z * z;
+  b[0] = 0.28209479177387814f;
+  b[1] = -0.4886025119029199f * y;
+  b[2] = 0.4886025119029199f * z;
+  b[3] = -0.4886025119029199f * x;
+  b[4] = 1.0925484305920792f * x * y;
+  b[5] = -1.0925484305920792f * y * z;
+  b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+  b[7] = -1.0925484305920792f * x * z;
+  b[8] = 0.5462742152960396f * (xx - yy);
+  b[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+  b[10] = 2.890611442640554f * x * y * z;
+  b[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+  b[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+  b[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+  b[14] = 1.445305721320277f * z * (xx - yy);
+  b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+}
+
 // Degree-3 SH with the 48 coefficients already in registers
 __device__ __forceinline__ void sh_eval_regs(const float sh[48], float x, float y, float z, float out[3]) {
   const float xx = x * x, yy = y * y, zz = z * z;

@@ -572,13 +572,19 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
       if (isfinite(vn)) {
         if (stage_sh) {
           asm volatile("cp.async.wait_group 0;" ::: "memory");
-          float shl[48];
+          // coefficients streamed from shared memory one float4 at a time (coefficient
+          // i = 4c + j belongs to basis function i / 3, channel i % 3)
+          float bsh[16];
+          sh_basis3(vx, vy, vz, bsh);
+          float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
           for (int c = 0; c < 12; ++c) {
             const float4 v4 = s_sh[wid][c][lane];
-            shl[4 * c] = v4.x; shl[4 * c + 1] = v4.y; shl[4 * c + 2] = v4.z; shl[4 * c + 3] = v4.w;
+            const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[(4 * c + j) % 3] = fmaf(bsh[(4 * c + j) / 3], v[j], acc[(4 * c + j) % 3]);
           }
-          sh_eval_regs(shl, vx, vy, vz, f);
+          f[0] = acc[0]; f[1] = acc[1]; f[2] = acc[2];
         } else {
           sh_eval(A.sh + g * A.n_coef * 3, A.sh_degree, vx, vy, vz, f);
         }
