@@ -133,10 +133,15 @@ def dist_env():
     return ws, rank, local
 
 
+B_BATCH = 512  # scans in the B-batch trajectory (poses 0.2 m apart, x in [-51, +51] m)
+
+
 def shard_poses(n_total: int, world: int, rank: int):
-    """Round-robin shard of the B-batch trajectory: scan i -> rank i mod world."""
-    poses = synth.batch_poses(n_total)
-    return [poses[i] for i in batch.shard_indices(n_total, world, rank)]
+    """Round-robin shard of the B-batch trajectory: scan i -> rank i mod world,
+    scan i at pose i mod 512 (the trajectory repeats, so every rank count sees the same mix
+    of poses however many scans a run takes)."""
+    poses = synth.batch_poses(B_BATCH)
+    return [poses[i % B_BATCH] for i in batch.shard_indices(n_total, world, rank)]
 
 
 def cpu_count():
