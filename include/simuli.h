@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 1
+#define SIMULI_ABI_VERSION 2
 
 enum {
   SIMULI_OK = 0,
@@ -80,6 +80,13 @@ typedef struct {
   float azimuth_start_rad;         /* phi_start in [-pi, pi)                              */
   int32_t spin_direction;          /* +1: azimuth increases with time, -1: decreases      */
   float min_range_m;               /* minimum range r_min (> 0)                           */
+  float beam_divergence_rad;       /* theta_div >= 0 (App. C): every particle's
+                                      covariance becomes Sigma_hat = Sigma + (theta r)^2
+                                      (I - d d^T), d / r the direction / range from the sensor
+                                      position at the mean's firing time (A27), used for the
+                                      projection (sigma points from chol(Sigma_hat)) and the
+                                      response, WITHOUT opacity compensation; 0 = off (the
+                                      bitwise default path)                                 */
 } simuli_lidar;
 
 /* Tiling parameters: n_phi elevation tiles N_phi, M = max rays per tile,

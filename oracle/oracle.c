@@ -107,6 +107,70 @@ int or_sigma_points(const double mu[3], const double q[4], const double s[3], co
   return 0;
 }
 
+/* Sigma points from an arbitrary square root Lsq of the covariance (Lsq Lsq^T = Sigma):
+ * mu, mu +- spread * (column k of Lsq).  Used with the Cholesky factor of the beam-
+ * divergence covariance Sigma_hat (App. C; reading A27). */
+int or_sigma_points_sqrt(const double mu[3], const double Lsq[9], const double ut[3], double pts[21], double wm[7],
+                         double wc[7]) {
+  double spread;
+  if (or_ut_weights(ut, &spread, wm, wc)) return -1;
+  for (int c = 0; c < 3; ++c) pts[c] = mu[c];
+  for (int k = 0; k < 3; ++k)
+    for (int c = 0; c < 3; ++c) {
+      pts[(1 + k) * 3 + c] = mu[c] + spread * Lsq[c * 3 + k];
+      pts[(4 + k) * 3 + c] = mu[c] - spread * Lsq[c * 3 + k];
+    }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------
+ * O2b Beam divergence (App. C): a 3D smoothing filter that widens
+ *     each LiDAR particle by the beam footprint orthogonal to the viewing direction,
+ *       Sigma_hat = Sigma + (theta_div r)^2 (I - d d^T),  d = (mu - o)/r,  r = |mu - o|,
+ *     and the response uses Sigma_hat WITHOUT the opacity factor sqrt(|Sigma_perp| /
+ *     |Sigma_hat_perp|) of AAA-Gaussians (the paper's modification).  o = sensor position
+ *     at the firing time of the particle mean (the sigma-point-0 time of A17; reading A27).
+ * ---------------------------------------------------------------------------------- */
+void or_divergence_cov(const double Sigma[9], const double mu[3], const double o[3], double theta, double Sh[9]) {
+  double d[3] = {mu[0] - o[0], mu[1] - o[1], mu[2] - o[2]};
+  double r2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+  double r = sqrt(r2);
+  double w = (theta * r) * (theta * r);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double dd = r > 0.0 ? (d[i] / r) * (d[j] / r) : 0.0;
+      Sh[i * 3 + j] = Sigma[i * 3 + j] + w * ((i == j ? 1.0 : 0.0) - dd);
+    }
+}
+
+/* Cholesky factor of a symmetric positive definite 3x3 (textbook, row by row). */
+int or_cholesky3(const double S[9], double L[9]) {
+  for (int i = 0; i < 9; ++i) L[i] = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j <= i; ++j) {
+      double acc = S[i * 3 + j];
+      for (int k = 0; k < j; ++k) acc -= L[i * 3 + k] * L[j * 3 + k];
+      if (i == j) {
+        if (!(acc > 0.0)) return -1;
+        L[i * 3 + i] = sqrt(acc);
+      } else {
+        L[i * 3 + j] = acc / L[j * 3 + j];
+      }
+    }
+  }
+  return 0;
+}
+
+/* Inverse of a lower-triangular 3x3 by forward substitution on the identity columns. */
+void or_lower_inverse3(const double L[9], double M[9]) {
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 3; ++i) {
+      double acc = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) acc -= L[i * 3 + k] * M[k * 3 + c];
+      M[i * 3 + c] = acc / L[i * 3 + i];
+    }
+}
+
 /* UT moments of 7 projected 2-vectors ("estimate a 2D conic").  If wrap_a, the
  * first coordinate is an azimuth, unwrapped about sigma point 0 (A21). */
 static void ut_moments(const double y[7][2], const double wm[7], const double wc[7], int wrap_a,
@@ -764,7 +828,26 @@ static int project_common(const or_gaussians* G, const void* sensor, int wrap_a,
     }
     or_quat_to_rot(q, R);
     double pts[21], w1[7], w2[7];
-    or_sigma_points(mu, q, s, ut, pts, w1, w2);
+    /* beam divergence (LiDAR, App. C): Sigma_hat, its Cholesky factor as the sigma-point
+     * square root and M_hat = L_hat^-1 as the canonical transform (Sigma_hat^-1 = M^T M) */
+    const double theta = wrap_a ? ((const or_lidar*)sensor)->beam_div : 0.0;
+    double Mdiv[9];
+    if (theta > 0.0) {
+      double o4[4], Rs0[9], ts0[3], Sig[9], Sh[9], Lh[9];
+      int e_unused = 0;
+      fn(mu, sensor, pose0, pose1, K, o4, &e_unused); /* firing time of the mean */
+      or_pose_at(pose0, pose1, o4[3], Rs0, ts0);
+      or_covariance(q, s, Sig);
+      or_divergence_cov(Sig, mu, ts0, theta, Sh);
+      if (or_cholesky3(Sh, Lh)) {
+        write_invalid(out, g);
+        continue;
+      }
+      or_sigma_points_sqrt(mu, Lh, ut, pts, w1, w2);
+      or_lower_inverse3(Lh, Mdiv);
+    } else {
+      or_sigma_points(mu, q, s, ut, pts, w1, w2);
+    }
     double y[7][2], s0 = 0.0, minr = INFINITY;
     int valid = 1, edge = 0, computable = 1;
     for (int i = 0; i < 7; ++i) {
@@ -803,8 +886,12 @@ static int project_common(const or_gaussians* G, const void* sensor, int wrap_a,
     out->box[g * 4 + 1] = round_up_f(mean[0] + ha);
     out->box[g * 4 + 2] = round_down_f(mean[1] - hb);
     out->box[g * 4 + 3] = round_up_f(mean[1] + hb);
-    for (int k = 0; k < 3; ++k) /* M = diag(1/s) R^T : row k = (column k of R)/s_k */
-      for (int i = 0; i < 3; ++i) out->Mrows[g * 9 + k * 3 + i] = R[i * 3 + k] / s[k];
+    if (theta > 0.0) {
+      for (int i = 0; i < 9; ++i) out->Mrows[g * 9 + i] = Mdiv[i];
+    } else {
+      for (int k = 0; k < 3; ++k) /* M = diag(1/s) R^T : row k = (column k of R)/s_k */
+        for (int i = 0; i < 3; ++i) out->Mrows[g * 9 + k * 3 + i] = R[i * 3 + k] / s[k];
+    }
     /* O9: SH features, direction from the sensor position at sigma point 0's firing time (A17) */
     double Rs[9], ts[3], v[3], shd[48];
     or_pose_at(pose0, pose1, s0, Rs, ts);

@@ -29,6 +29,7 @@ typedef struct {
   double az_start;          /* phi_start (rad)                                      */
   int32_t dir;              /* +1 ccw, -1 cw                                        */
   double r_min;             /* minimum range (m)                                    */
+  double beam_div;          /* beam divergence theta_div (rad), App. C; 0 = off (A24) */
 } or_lidar;
 
 /* Camera (A22). model 0 = pinhole + radtan, 1 = KB fisheye. */
@@ -58,6 +59,12 @@ typedef struct {
 
 /* ---- primitives (exposed for pins) ---- */
 void or_quat_to_rot(const double q[4], double R[9]);
+/* App. C: Sigma_hat = Sigma + (theta r)^2 (I - d d^T), d = (mu - o)/r, r = |mu - o| */
+void or_divergence_cov(const double Sigma[9], const double mu[3], const double o[3], double theta, double Sh[9]);
+int  or_cholesky3(const double S[9], double L[9]);          /* S = L L^T, L lower; -1 if not SPD */
+void or_lower_inverse3(const double L[9], double M[9]);      /* M = L^-1 (lower)                   */
+int  or_sigma_points_sqrt(const double mu[3], const double Lsq[9], const double ut[3], double pts[21],
+                          double wm[7], double wc[7]);        /* sigma points from the columns of Lsq */
 void or_covariance(const double q[4], const double s[3], double Sigma[9]);
 int  or_ut_weights(const double ut[3], double* spread, double wm[7], double wc[7]);
 int  or_sigma_points(const double mu[3], const double q[4], const double s[3], const double ut[3],

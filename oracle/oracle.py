@@ -39,7 +39,7 @@ u32p = C.POINTER(C.c_uint32)
 
 class OrLidar(C.Structure):
     _fields_ = [("n_beams", C.c_int32), ("elev", f32p), ("n_az", C.c_int32), ("az_start", C.c_double),
-                ("dir", C.c_int32), ("r_min", C.c_double)]
+                ("dir", C.c_int32), ("r_min", C.c_double), ("beam_div", C.c_double)]
 
 
 class OrCamera(C.Structure):
@@ -112,6 +112,10 @@ def lib():
         L.or_sh_eval.argtypes = [f64p, C.c_int, f64p, f64p]
         L.or_response.argtypes = [f64p, f64p, f64p, f64p, f64p]
         L.or_ut_affine.argtypes = [f64p, f64p, f64p, f64p, f64p, f64p, f64p, f64p]
+        L.or_divergence_cov.argtypes = [f64p, f64p, f64p, C.c_double, f64p]
+        L.or_cholesky3.argtypes = [f64p, f64p]
+        L.or_lower_inverse3.argtypes = [f64p, f64p]
+        L.or_sigma_points_sqrt.argtypes = [f64p, f64p, f64p, f64p, f64p, f64p]
         L.or_sat_query.argtypes = [i32p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]
         L.or_decode_lidar.argtypes = [f64p, f64p]
         L.or_elev_tile.argtypes = [C.POINTER(OrTiling), C.c_float]
@@ -151,7 +155,8 @@ def pose7(p) -> np.ndarray:
 def make_lidar(cfg):
     beams = np.ascontiguousarray(cfg.beams, np.float32)
     L = OrLidar(int(beams.shape[0]), _p(beams, f32p), int(cfg.n_azimuth), float(np.float32(cfg.azimuth_start)),
-                int(cfg.spin_direction), float(np.float32(cfg.min_range)))
+                int(cfg.spin_direction), float(np.float32(cfg.min_range)),
+                float(np.float32(getattr(cfg, "beam_divergence", 0.0))))
     L._keep = beams
     return L
 
@@ -511,6 +516,33 @@ def sigma_points(mu, q, s, ut=None):
     pts, wm, wc = np.zeros(21), np.zeros(7), np.zeros(7)
     rc = lib().or_sigma_points(_p(_d(mu), f64p), _p(_d(q), f64p), _p(_d(s), f64p), _p(_ut(ut), f64p),
                                _p(pts, f64p), _p(wm, f64p), _p(wc, f64p))
+    assert rc == 0
+    return pts.reshape(7, 3), wm, wc
+
+
+def divergence_cov(Sigma, mu, o, theta):
+    """App. C: Sigma_hat = Sigma + (theta r)^2 (I - d d^T)."""
+    Sh = np.zeros(9)
+    lib().or_divergence_cov(_p(_d(Sigma), f64p), _p(_d(mu), f64p), _p(_d(o), f64p), float(theta), _p(Sh, f64p))
+    return Sh.reshape(3, 3)
+
+
+def cholesky3(S):
+    L = np.zeros(9)
+    rc = lib().or_cholesky3(_p(_d(S), f64p), _p(L, f64p))
+    return None if rc else L.reshape(3, 3)
+
+
+def lower_inverse3(L):
+    M = np.zeros(9)
+    lib().or_lower_inverse3(_p(_d(L), f64p), _p(M, f64p))
+    return M.reshape(3, 3)
+
+
+def sigma_points_sqrt(mu, Lsq, ut=None):
+    pts, wm, wc = np.zeros(21), np.zeros(7), np.zeros(7)
+    rc = lib().or_sigma_points_sqrt(_p(_d(mu), f64p), _p(_d(Lsq), f64p), _p(_ut(ut), f64p), _p(pts, f64p),
+                                    _p(wm, f64p), _p(wc, f64p))
     assert rc == 0
     return pts.reshape(7, 3), wm, wc
 

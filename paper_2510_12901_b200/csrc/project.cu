@@ -89,6 +89,7 @@ struct ProjArgs {
   float az_start, r_min;
   int dir;
   float R0[9], t0w[3], dtw[3], v[3], axis[3], theta;  // start pose, motion, rotation axis / angle
+  float beam_div;                                     // theta_div (App. C), 0 = off
   double R0d[9], t0d[3], vd[3], axis_d[3], theta_d;  // the same in double (sigma point 0)
   int small_rot;
   int n_phi, n_theta, rows_per_tile, az_cells, sat_cols, enable_cull;
@@ -384,7 +385,7 @@ constexpr double kPiD = 3.141592653589793;
 constexpr int kSmemBounds = 264;
 constexpr int kShSmem = 8 * 12 * 32 * 16;
 
-template <int KIND>
+template <int KIND, bool DIV>
 __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
   // tiling boundaries / row scales staged in shared memory (binary searches hit smem)
   __shared__ float s_bounds[kSmemBounds], s_rscale[kSmemBounds];
@@ -458,6 +459,55 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
     float ma, mb, caa, cab, cbb, s0 = 0.f;
     double a0 = 0.0, e0 = 0.0;
     bool valid = true, computable = true;
+    // beam divergence (App. C; A27): Sigma_hat = Sigma + theta^2 (r^2 I - v v^T),
+    // v = mu - o, o = sensor position at the mean's firing time; its Cholesky factor is the
+    // sigma-point square root and its inverse the canonical transform (Sigma_hat^-1 = M^T M)
+    float Mh[9];
+    constexpr bool div = KIND == SIMULI_SENSOR_LIDAR && DIV;  // (A.beam_div > 0, a separate instantiation)
+    if (div) {
+      const float d0 = mu[0] - A.t0w[0], d1 = mu[1] - A.t0w[1], d2 = mu[2] - A.t0w[2];
+      const float cs[3] = {A.R0[0] * d0 + A.R0[3] * d1 + A.R0[6] * d2, A.R0[1] * d0 + A.R0[4] * d1 + A.R0[7] * d2,
+                           A.R0[2] * d0 + A.R0[5] * d1 + A.R0[8] * d2};
+      float sf = 0.f;
+      if (!A.pose.same && A.K >= 1) {
+        sf = fire_time(A, cs[0], cs[1]);
+        for (int it = 1; it < A.K; ++it) {
+          float sn, omc, p[3];
+          rot_sc_f(A, sf, &sn, &omc);
+          const float y[3] = {cs[0] - sf * A.v[0], cs[1] - sf * A.v[1], cs[2] - sf * A.v[2]};
+          rot_apply(A.axis, sn, omc, y, p);
+          sf = fire_time(A, p[0], p[1]);
+        }
+      }
+      const float v[3] = {mu[0] - (A.t0w[0] + sf * A.dtw[0]), mu[1] - (A.t0w[1] + sf * A.dtw[1]),
+                          mu[2] - (A.t0w[2] + sf * A.dtw[2])};
+      const float r2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2], t2 = A.beam_div * A.beam_div;
+      float Sh[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) acc += R[3 * i + k] * R[3 * j + k] * (sc[k] * sc[k]);
+          Sh[i][j] = acc + t2 * ((i == j ? r2 : 0.f) - v[i] * v[j]);
+        }
+      const float l00 = sqrtf(Sh[0][0]), l10 = Sh[1][0] / l00, l20 = Sh[2][0] / l00;
+      const float q11 = Sh[1][1] - l10 * l10;
+      const float l11 = sqrtf(q11), l21 = (Sh[2][1] - l20 * l10) / l11;
+      const float q22 = Sh[2][2] - l20 * l20 - l21 * l21;
+      const float l22 = sqrtf(q22);
+      computable = Sh[0][0] > 0.f && q11 > 0.f && q22 > 0.f && isfinite(l22);
+      const float sp = A.ut.spread;
+      L[0][0] = sp * l00; L[0][1] = sp * l10; L[0][2] = sp * l20;  // columns of chol(Sigma_hat)
+      L[1][0] = 0.f;      L[1][1] = sp * l11; L[1][2] = sp * l21;
+      L[2][0] = 0.f;      L[2][1] = 0.f;      L[2][2] = sp * l22;
+      const float m00 = 1.0f / l00, m11 = 1.0f / l11, m22 = 1.0f / l22;
+      const float m10 = -l10 * m00 * m11, m21 = -l21 * m11 * m22, m20 = -(l20 * m00 + l21 * m10) * m22;
+      Mh[0] = m00; Mh[1] = 0.f; Mh[2] = 0.f;
+      Mh[3] = m10; Mh[4] = m11; Mh[5] = 0.f;
+      Mh[6] = m20; Mh[7] = m21; Mh[8] = m22;
+    }
     if (KIND == SIMULI_SENSOR_LIDAR) {
       lidar_moments(A, mu, L, &a0, &e0, &ma, &mb, &caa, &cab, &cbb, &s0, &valid);
     } else {
@@ -552,11 +602,16 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
     }
     if (ok && (count > 0 || A.write_all)) {
       // ---- record: canonical transform M = diag(1/s) R^T, SH features (A17)
+      if (div) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float is = 1.0f / sc[k];
+        for (int i = 0; i < 9; ++i) M[i] = Mh[i];
+      } else {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) M[3 * k + c] = R[3 * c + k] * is;
+        for (int k = 0; k < 3; ++k) {
+          const float is = 1.0f / sc[k];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) M[3 * k + c] = R[3 * c + k] * is;
+        }
       }
       float Rs[9], ts[3];
       if (KIND == SIMULI_SENSOR_LIDAR) {
@@ -672,6 +727,8 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.az_start = P->lidar->azimuth_start_rad;
     A.dir = P->lidar->spin_direction;
     A.r_min = P->lidar->min_range_m;
+    SIMULI_REQUIRE(P->lidar->beam_divergence_rad >= 0.f, "beam_divergence_rad must be >= 0");
+    A.beam_div = P->lidar->beam_divergence_rad;
     {
       // launch constants of the sensor model: R0 = R(q0), t0, dt = t1 - t0, v = R0^T dt,
       // rotation axis k (in the start frame) and angle theta of R0^T R1 (host, double)
@@ -705,8 +762,13 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.az_cells = T.cull_az_cells; A.sat_cols = T.sat_cols; A.enable_cull = P->enable_culling;
     A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f; A.az_tile_scale = T.az_tile_scale; A.az_cell_scale = T.az_cell_scale;
     A.bounds = T.elev_bounds; A.row_scale = T.cull_row_scale; A.sat = T.sat;
-    cudaFuncSetAttribute(k_project<SIMULI_SENSOR_LIDAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
-    k_project<SIMULI_SENSOR_LIDAR><<<blocks, threads, kShSmem, st>>>(A);
+    if (A.beam_div > 0.f) {
+      cudaFuncSetAttribute(k_project<SIMULI_SENSOR_LIDAR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
+      k_project<SIMULI_SENSOR_LIDAR, true><<<blocks, threads, kShSmem, st>>>(A);
+    } else {
+      cudaFuncSetAttribute(k_project<SIMULI_SENSOR_LIDAR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
+      k_project<SIMULI_SENSOR_LIDAR, false><<<blocks, threads, kShSmem, st>>>(A);
+    }
   } else if (P->kind == SIMULI_SENSOR_CAMERA) {
     SIMULI_REQUIRE(P->camera, "camera projection needs camera");
     const simuli_camera& C = *P->camera;
@@ -719,8 +781,8 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.fx = C.fx; A.fy = C.fy; A.cx = C.cx; A.cy = C.cy;
     for (int i = 0; i < 5; ++i) A.k[i] = C.k[i];
     A.near_m = C.near_m; A.max_theta = C.max_theta_rad; A.inv_tile = 1.0f / (float)C.tile_px;
-    cudaFuncSetAttribute(k_project<SIMULI_SENSOR_CAMERA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
-    k_project<SIMULI_SENSOR_CAMERA><<<blocks, threads, kShSmem, st>>>(A);
+    cudaFuncSetAttribute(k_project<SIMULI_SENSOR_CAMERA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
+    k_project<SIMULI_SENSOR_CAMERA, false><<<blocks, threads, kShSmem, st>>>(A);
   } else {
     set_error("simuli_project: unknown sensor kind %d", P->kind);
     return SIMULI_ERR_INVALID_ARGUMENT;

@@ -43,7 +43,8 @@ class Pose(C.Structure):
 
 class Lidar(C.Structure):
     _fields_ = [("n_beams", C.c_int32), ("beam_elevation_rad", f32p), ("n_azimuth", C.c_int32),
-                ("azimuth_start_rad", C.c_float), ("spin_direction", C.c_int32), ("min_range_m", C.c_float)]
+                ("azimuth_start_rad", C.c_float), ("spin_direction", C.c_int32), ("min_range_m", C.c_float),
+                ("beam_divergence_rad", C.c_float)]
 
 
 class TilingParams(C.Structure):
@@ -327,7 +328,8 @@ class LidarRenderer(_Frame):
         beams = np.ascontiguousarray(cfg.beams, np.float32)
         self._beams = beams
         self.lidar = Lidar(int(beams.shape[0]), beams.ctypes.data_as(f32p), int(cfg.n_azimuth),
-                           float(cfg.azimuth_start), int(cfg.spin_direction), float(cfg.min_range))
+                           float(cfg.azimuth_start), int(cfg.spin_direction), float(cfg.min_range),
+                           float(getattr(cfg, "beam_divergence", 0.0)))
         self.params = ProjectParams(SENSOR_LIDAR, C.pointer(self.lidar), C.pointer(self.tiling_dev), None,
                                     make_pose(cfg.pose_start), make_pose(cfg.pose_end), int(cfg.rs_iterations),
                                     ut[0], ut[1], ut[2], extent_sigma, int(enable_culling), int(write_all_records))

@@ -89,6 +89,7 @@ class LidarConfig:
     spin_direction: int = 1
     min_range: float = 0.1
     rs_iterations: int = 1
+    beam_divergence: float = 0.0  # theta_div (rad), App. C filter; 0 = off (A24); SPEC suggests 1.5e-3
     pose_start: dict = field(default_factory=lambda: pose([1, 0, 0, 0], [0, 0, 1.8]))
     pose_end: dict = field(default_factory=lambda: pose([1, 0, 0, 0], [0, 0, 1.8]))
 

@@ -449,3 +449,46 @@ def test_camera_config_d_full_size_sampled(SM, oracle_mod):
     dm = ok2 & (ref2["opacity"] >= 0.5)
     assert np.abs(c.out["depth"].cpu().numpy()[sel] - ref2["depth"])[dm].max(initial=0) < TOL_DEPTH
     assert (c.out["opacity"].cpu().numpy() > 0.1).mean() > 0.05
+
+
+# ------------------------------------------------------------------ beam divergence (NEXT-2)
+@pytest.mark.parametrize("config", ["A", "B-sub"])
+def test_beam_divergence_parity(SM, oracle_mod, config):
+    """App. C filter (theta_div = 1.5e-3 rad, SPEC S:287's value; A24/A27) on the GPU path:
+    projection (boxes, canonical transform from chol(Sigma_hat)^-1), then compositing tier 1
+    (GPU records / lists / rays) and tier 2 (oracle from scratch, A23 flags)."""
+    O = oracle_mod
+    if config == "B-sub":
+        cfg, scene = S.lidar_config("B"), S.scene_for("B", n=200_000)
+    else:
+        cfg, scene = S.lidar_config(config), S.scene_for(config)
+    cfg.beam_divergence = 1.5e-3
+    r = lidar_run(SM, cfg, scene, write_all_records=True)
+    rec = r.record.cpu().numpy()
+    proj = O.project_lidar(scene, cfg)
+    gv, ov, amb = np.isfinite(rec[:, 16]), proj["valid"] != 0, proj["ambiguous"] != 0
+    assert np.array_equal(gv[~amb], ov[~amb])
+    both = gv & ov & ~amb
+    db = np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both])
+    assert db[:, :2].max() < LIDAR_EPS["a"] and db[:, 2:].max() < LIDAR_EPS["b"], db.max(0)
+    Mref = proj["Mrows"][both]
+    rel = np.abs(rec[both, 3:12] - Mref) / np.abs(Mref).max(1, keepdims=True)
+    assert rel.max() < 2e-5, rel.max()
+    # the filter changed the particles (not a silent no-op)
+    cfg0 = S.lidar_config("B" if config == "B-sub" else config)
+    assert not np.array_equal(O.project_lidar(scene, cfg0)["Mrows"][both], Mref)
+    t = O.Tiling(cfg)
+    _, ids, ranges = sorted_lists(r)
+    od = r.out["ray_od"].cpu().numpy()
+    ref = O.composite(gpu_records(r), ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, wrap=1, near=cfg.min_range,
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4},
+                      pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    ref["intensity"], ref["raydrop"] = O.decode_lidar(ref["feat"])
+    ok = ref["flag"] == 0
+    assert ok.mean() > 0.999
+    compare_lidar(r.out, ref, ok)
+    if config == "A":
+        ref2 = O.render_lidar(scene, cfg, tiling=t, flag_eps=LIDAR_EPS)
+        ok2 = ref2["flag"] == 0
+        assert ok2.mean() > 1 - FLAG_BUDGET["default"], ok2.mean()
+        compare_lidar(r.out, ref2, ok2)

@@ -654,3 +654,124 @@ def test_camera_tiled_equals_bruteforce(oracle_mod):
         for k in ("feat", "opacity", "depth_accum", "T_final", "n_contrib"):
             assert np.array_equal(a[k], b[k]), (name, k)
         assert (a["opacity"] > 0.01).mean() > 0.05
+
+
+# ------------------------------------------------------------------ beam divergence (App. C)
+def test_divergence_cov_directions(oracle_mod):
+    """Sigma_hat = Sigma + (theta r)^2 (I - d d^T): unchanged along the viewing
+    direction, widened by exactly (theta r)^2 across it; for an isotropic particle the
+    eigen-decomposition (numpy) is {a^2 along d, a^2 + (theta r)^2 twice}."""
+    O = oracle_mod
+    rng = np.random.default_rng(31)
+    for _ in range(20):
+        q, s = rng.normal(size=4), rng.uniform(0.02, 0.5, 3)
+        Sig = O.covariance(q, s)
+        mu, o = rng.uniform(-40, 40, 3), rng.uniform(-2, 2, 3)
+        theta = rng.uniform(1e-4, 5e-3)
+        Sh = O.divergence_cov(Sig, mu, o, theta)
+        r = np.linalg.norm(mu - o)
+        d = (mu - o) / r
+        u = np.cross(d, rng.normal(size=3))
+        u /= np.linalg.norm(u)
+        assert np.allclose(Sh @ d, Sig @ d, atol=1e-12)
+        assert abs(u @ Sh @ u - (u @ Sig @ u + (theta * r) ** 2)) < 1e-12
+        assert np.allclose(Sh, Sh.T, atol=1e-15)
+    a, theta = 0.07, 2e-3
+    mu, o = np.array([30.0, -12.0, 1.0]), np.array([0.5, 0.2, 1.8])
+    Sh = O.divergence_cov(a * a * np.eye(3), mu, o, theta)
+    w, V = np.linalg.eigh(Sh)
+    r = np.linalg.norm(mu - o)
+    assert np.allclose(w, [a * a, a * a + (theta * r) ** 2, a * a + (theta * r) ** 2], rtol=1e-12)
+    assert abs(abs(V[:, 0] @ (mu - o) / r) - 1.0) < 1e-12
+
+
+def test_cholesky_and_lower_inverse(oracle_mod):
+    """The oracle's textbook Cholesky equals numpy's; its triangular inverse inverts."""
+    O = oracle_mod
+    rng = np.random.default_rng(32)
+    for _ in range(30):
+        A = rng.normal(size=(3, 3))
+        S = A @ A.T + 1e-3 * np.eye(3)
+        L = O.cholesky3(S)
+        assert np.allclose(L, np.linalg.cholesky(S), rtol=1e-12, atol=1e-14)
+        assert np.allclose(O.lower_inverse3(L) @ L, np.eye(3), atol=1e-12)
+    assert O.cholesky3(-np.eye(3)) is None
+
+
+def test_divergence_response_closed_form_and_dense(oracle_mod):
+    """Response with Sigma_hat (M_hat = chol(Sigma_hat)^-1): (i) a dense scan of the
+    Mahalanobis distance along the ray with numpy's inv(Sigma_hat) gives the same minimum
+    and argmin; (ii) for an isotropic particle seen from the sensor at angle beta off its
+    centre, delta^2 = r^2 sin^2 b / (a^2 sin^2 b + (a^2 + (theta r)^2) cos^2 b) -- the
+    beam footprint widens the particle across the beam only."""
+    O = oracle_mod
+    rng = np.random.default_rng(33)
+    for _ in range(10):
+        q, s = rng.normal(size=4), rng.uniform(0.05, 0.4, 3)
+        mu, o = rng.uniform(-20, 20, 3), rng.uniform(-1, 1, 3)
+        theta = 3e-3
+        Sh = O.divergence_cov(O.covariance(q, s), mu, o, theta)
+        M = O.lower_inverse3(O.cholesky3(Sh))
+        d = (mu - o) + rng.normal(scale=0.3, size=3)
+        d /= np.linalg.norm(d)
+        tau, d2 = O.response(mu, M.reshape(-1), o, d)
+        Si = np.linalg.inv(Sh)
+        t = np.linspace(tau - 2.0, tau + 2.0, 200001)
+        x = o[None, :] + t[:, None] * d[None, :] - mu[None, :]
+        m = np.einsum("ni,ij,nj->n", x, Si, x)
+        k = int(np.argmin(m))
+        assert abs(m[k] - d2) < 1e-6 * max(1.0, d2) and abs(t[k] - tau) < 2e-5
+    a, theta, r = 0.05, 2e-3, 40.0
+    mu, o = np.array([r, 0.0, 0.0]), np.zeros(3)
+    Sh = O.divergence_cov(a * a * np.eye(3), mu, o, theta)
+    M = O.lower_inverse3(O.cholesky3(Sh))
+    b2 = a * a + (theta * r) ** 2
+    for beta in (0.0, 1e-4, 1e-3, 4e-3, 2e-2):
+        d = np.array([np.cos(beta), np.sin(beta), 0.0])
+        _, d2 = O.response(mu, M.reshape(-1), o, d)
+        ref = r * r * np.sin(beta) ** 2 / (a * a * np.sin(beta) ** 2 + b2 * np.cos(beta) ** 2)
+        assert abs(d2 - ref) <= 1e-9 * max(1.0, ref), (beta, d2, ref)
+
+
+def test_ut_affine_exact_with_cholesky_root(oracle_mod):
+    """UT with the Cholesky root of Sigma_hat through an affine sensor is exact:
+    mean A mu + b, covariance A Sigma_hat A^T (the UT moments written out here)."""
+    O = oracle_mod
+    rng = np.random.default_rng(34)
+    for ut in ((1.0, 2.0, 0.0), (0.6, 2.0, 0.5)):
+        Sh = O.divergence_cov(O.covariance(rng.normal(size=4), rng.uniform(0.05, 0.5, 3)),
+                              rng.uniform(-10, 10, 3), np.zeros(3), 4e-3)
+        mu = rng.uniform(-10, 10, 3)
+        pts, wm, wc = O.sigma_points_sqrt(mu, O.cholesky3(Sh), ut)
+        A, b = rng.normal(size=(2, 3)), rng.normal(size=2)
+        y = pts @ A.T + b
+        mean = wm @ y
+        cov = (wc[:, None, None] * np.einsum("ni,nj->nij", y - mean, y - mean)).sum(0)
+        assert np.allclose(mean, A @ mu + b, atol=1e-9)
+        assert np.allclose(cov, A @ Sh @ A.T, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("theta", [1.5e-3, 5e-3])
+def test_divergence_tiled_equals_bruteforce_and_widens(oracle_mod, theta):
+    """With the filter on, tiling and culling stay exact accelerations (tiled = brute force
+    on tiny scenes, A12); and since Sigma_hat - Sigma is positive semi-definite, every
+    (ray, particle) Mahalanobis distance can only shrink: delta_hat^2 <= delta^2."""
+    O = oracle_mod
+    for seed in range(6):
+        cfg = S.lidar_config("tiny")
+        scene = S.scene_for("tiny", seed=seed)
+        cfg.beam_divergence = theta
+        tiled = O.render_lidar(scene, cfg)
+        brute = O.render_lidar(scene, cfg, mode="brute")
+        for k in ("feat", "opacity", "depth_accum", "T_final"):
+            assert np.array_equal(tiled[k], brute[k]), k
+    rng = np.random.default_rng(35)
+    for _ in range(200):
+        q, s = rng.normal(size=4), rng.uniform(0.02, 0.5, 3)
+        mu, o = rng.uniform(-30, 30, 3), rng.uniform(-1, 1, 3)
+        Sig = O.covariance(q, s)
+        M = O.lower_inverse3(O.cholesky3(Sig))
+        Mh = O.lower_inverse3(O.cholesky3(O.divergence_cov(Sig, mu, o, theta)))
+        d = (mu - o) + rng.normal(scale=2.0, size=3)
+        d /= np.linalg.norm(d)
+        assert O.response(mu, Mh.reshape(-1), o, d)[1] <= O.response(mu, M.reshape(-1), o, d)[1] * (1 + 1e-9) + 1e-12
