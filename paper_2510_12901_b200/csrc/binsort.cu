@@ -260,14 +260,17 @@ struct DupArgs {
   int id_bits, packed; // packed: one u64 word = (key << id_bits) | id
 };
 
+// Warp-balanced emission: warp w of the CTA takes particles [128 w, 128 w + 128) of the
+// CTA's 1024 in groups of 32 (lane = particle); a group's pairs are enumerated 32 at a time
+// (pair k0 + lane), the owner lane found by a 5-step shuffle search over the exclusive
+// prefix of the counts (no shared-memory binary search, no bank conflicts), so a particle
+// spanning hundreds of tiles does not serialise one lane.  Pairs are written in particle
+// order (the stable sort then keeps equal keys in id order).
 __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
-  __shared__ int s_excl[kDupBlock + 1];
-  __shared__ int4 s_rect[kDupBlock];
-  __shared__ uint32_t s_key[kDupBlock];
   __shared__ uint32_t s_hist[kMaxPasses * 256];
-  __shared__ int scratch[8];
-  const int tid = threadIdx.x;
-  const int64_t g0 = (int64_t)blockIdx.x * kDupBlock;
+  __shared__ int s_wtot[kDupThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t gb = (int64_t)blockIdx.x * kDupBlock;
   const int passes = (int)A.scal[S_PASSES];
   const int b = (int)A.scal[S_B];
   const uint32_t kmin = (uint32_t)A.scal[S_KMIN];
@@ -275,53 +278,70 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
   uint64_t* kout = s0 ? A.keys[1] : A.keys[0];
   uint32_t* vout = s0 ? A.vals[1] : A.vals[0];
   for (int i = tid; i < passes * 256; i += kDupThreads) s_hist[i] = 0;
-  int c[kDupItems], run = 0;
+  constexpr int kGroups = kDupBlock / kDupThreads;  // groups of 32 particles per warp
+  const int64_t gw = gb + (int64_t)warp * 32 * kGroups;
+  int c[kGroups], wsum = 0;
 #pragma unroll
-  for (int i = 0; i < kDupItems; ++i) {
-    const int64_t g = g0 + tid * kDupItems + i;
-    c[i] = g < A.n ? __ldg(A.count + g) : 0;
-    run += c[i];
+  for (int q = 0; q < kGroups; ++q) {
+    const int64_t g = gw + q * 32 + lane;
+    c[q] = g < A.n ? __ldg(A.count + g) : 0;
+    wsum += c[q];
   }
-  int tot;
-  int ex = block_excl_scan256(run, scratch, &tot);
 #pragma unroll
-  for (int i = 0; i < kDupItems; ++i) {
-    const int li = tid * kDupItems + i;
-    const int64_t g = g0 + li;
-    s_excl[li] = ex;
-    ex += c[i];
-    if (c[i] > 0) {
-      s_rect[li] = __ldg(A.rect + g);
-      s_key[li] = __float_as_uint(__ldg(A.key + g)) - kmin;
-    }
-  }
-  if (tid == 0) s_excl[kDupBlock] = tot;
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+  if (lane == 0) s_wtot[warp] = wsum;
   __syncthreads();
-  const int64_t out0 = A.block_offsets[blockIdx.x];
-  for (int k = tid; k < tot; k += kDupThreads) {
-    int lo = 0, hi = kDupBlock;  // last li with s_excl[li] <= k
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_excl[mid] <= k) lo = mid;
-      else hi = mid;
+  int64_t base = A.block_offsets[blockIdx.x];
+  for (int w = 0; w < warp; ++w) base += s_wtot[w];
+#pragma unroll 1
+  for (int q = 0; q < kGroups; ++q) {
+    const int64_t g = gw + q * 32 + lane;
+    const int cq = c[q];
+    int4 r = make_int4(0, 0, 0, 1);
+    uint32_t kq = 0;
+    if (cq > 0) {
+      r = __ldg(A.rect + g);
+      kq = __float_as_uint(__ldg(A.key + g)) - kmin;
     }
-    const int j = k - s_excl[lo];
-    const int4 r = s_rect[lo];
-    const int row = r.x + j / r.w;
-    int col = r.z + j % r.w;
-    if (col >= A.n_cols_total) col -= A.n_cols_total;
-    const uint32_t tile = (uint32_t)row * (uint32_t)A.n_cols_total + (uint32_t)col;
-    const uint64_t key = ((uint64_t)tile << b) | (uint64_t)s_key[lo];
-    const int64_t pos = out0 + k;
-    if (pos < A.capacity) {
-      if (A.packed) {
-        kout[pos] = (key << A.id_bits) | (uint64_t)(g0 + lo);
-      } else {
-        kout[pos] = key;
-        vout[pos] = (uint32_t)(g0 + lo);
+    int incl = cq;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int excl = incl - cq;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int k0 = 0; k0 < total; k0 += 32) {
+      const int k = k0 + lane;
+      int lo = 0;  // owner: the last lane whose exclusive prefix is <= k
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, excl, lo + step);
+        if (v <= k) lo += step;
       }
-      for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * 256 + (int)((key >> (8 * p)) & 0xFF)], 1u);
+      const int j = k - __shfl_sync(0xffffffffu, excl, lo);
+      const int rx = __shfl_sync(0xffffffffu, r.x, lo), rz = __shfl_sync(0xffffffffu, r.z, lo),
+                rw = __shfl_sync(0xffffffffu, r.w, lo);
+      const uint32_t kk = __shfl_sync(0xffffffffu, kq, lo);
+      if (k >= total) continue;
+      const int row = rx + j / rw;  // rect = (row0, row1, col start, col run length)
+      int col = rz + j % rw;
+      if (col >= A.n_cols_total) col -= A.n_cols_total;
+      const uint32_t tile = (uint32_t)row * (uint32_t)A.n_cols_total + (uint32_t)col;
+      const uint64_t key = ((uint64_t)tile << b) | (uint64_t)kk;
+      const int64_t pos = base + k;
+      if (pos < A.capacity) {
+        const uint64_t id = (uint64_t)(gw + q * 32 + lo);
+        if (A.packed) {
+          kout[pos] = (key << A.id_bits) | id;
+        } else {
+          kout[pos] = key;
+          vout[pos] = (uint32_t)id;
+        }
+        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * 256 + (int)((key >> (8 * p)) & 0xFF)], 1u);
+      }
     }
+    base += total;
   }
   __syncthreads();
   for (int i = tid; i < passes * 256; i += kDupThreads)
