@@ -293,8 +293,18 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
         const float y[3] = {l[0] - ds * A.v[0], l[1] - ds * A.v[1], l[2] - ds * A.v[2]};
         const float w[3] = {E[0] * y[0] + E[1] * y[1] + E[2] * y[2], E[3] * y[0] + E[4] * y[1] + E[5] * y[2],
                             E[6] * y[0] + E[7] * y[1] + E[8] * y[2]};
+        // E(ds) - I for the small rotation between the two firing times (|ds theta| is the
+        // particle's angular size times the sweep's yaw, ~1e-3): Taylor to a^4 below 1e-2
+        // (truncation < 1e-11), the general form otherwise
         float sn, omc;
-        rot_sc_f(A, ds, &sn, &omc);
+        const float ad = ds * A.theta;
+        if (fabsf(ad) < 1e-2f) {
+          const float a2 = ad * ad;
+          sn = ad * (1.f - a2 * (1.f / 6.f));
+          omc = 0.5f * a2 * (1.f - a2 * (1.f / 12.f));
+        } else {
+          rot_sc_f(A, ds, &sn, &omc);
+        }
         const float z[3] = {p0[0] + w[0], p0[1] + w[1], p0[2] + w[2]};
         const float* kk = A.axis;
         const float cx = kk[1] * z[2] - kk[2] * z[1], cy = kk[2] * z[0] - kk[0] * z[2], cz = kk[0] * z[1] - kk[1] * z[0];
