@@ -196,35 +196,6 @@ __device__ __forceinline__ void sh_basis3(float x, float y, float z, float b[16]
   b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
 }
 
-// Degree-3 SH with the 48 coefficients already in registers
-__device__ __forceinline__ void sh_eval_regs(const float sh[48], float x, float y, float z, float out[3]) {
-  const float xx = x * x, yy = y * y, zz = z * z;
-  const float b[16] = {0.28209479177387814f,
-                       -0.4886025119029199f * y,
-                       0.4886025119029199f * z,
-                       -0.4886025119029199f * x,
-                       1.0925484305920792f * x * y,
-                       -1.0925484305920792f * y * z,
-                       0.31539156525252005f * (2.0f * zz - xx - yy),
-                       -1.0925484305920792f * x * z,
-                       0.5462742152960396f * (xx - yy),
-                       -0.5900435899266435f * y * (3.0f * xx - yy),
-                       2.890611442640554f * x * y * z,
-                       -0.4570457994644658f * y * (4.0f * zz - xx - yy),
-                       0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy),
-                       -0.4570457994644658f * x * (4.0f * zz - xx - yy),
-                       1.445305721320277f * z * (xx - yy),
-                       -0.5900435899266435f * x * (xx - 3.0f * yy)};
-  float r0 = 0.f, r1 = 0.f, r2 = 0.f;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    r0 = fmaf(b[k], sh[3 * k], r0);
-    r1 = fmaf(b[k], sh[3 * k + 1], r1);
-    r2 = fmaf(b[k], sh[3 * k + 2], r2);
-  }
-  out[0] = r0; out[1] = r1; out[2] = r2;
-}
-
 // Ray in double, split into float hi + lo parts for the compensated response.
 struct RayF {
   float o_hi[3], o_lo[3], d_hi[3], d_lo[3];
