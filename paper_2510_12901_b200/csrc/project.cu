@@ -222,9 +222,9 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
   const float c[3] = {(float)cd[0], (float)cd[1], (float)cd[2]};
   const bool moving = !A.pose.same && A.K >= 1;
   // ---- firing time of sigma point 0 (float32 decisions; K fixed-point steps from s = 0)
-  float s_c = 0.f;
+  float s_c = 0.f, s_c1 = 0.f;  // s_c1: the first step (start-frame azimuth), for the offsets below
   if (moving) {
-    s_c = fire_time(A, c[0], c[1]);
+    s_c = s_c1 = fire_time(A, c[0], c[1]);
     for (int it = 1; it < A.K; ++it) {
       float sn, omc, p[3];
       rot_sc_f(A, s_c, &sn, &omc);
@@ -278,10 +278,10 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
         // (atan_ratio(y, x) is atan2(y, x) for any arguments)
         const float q[3] = {c[0] + l[0], c[1] + l[1], c[2] + l[2]};
         const bool cax = cxy2 > 0.f;
-        float s = wrap01(s_c + (float)A.dir *
-                                   atan_ratio(cax ? c[0] * l[1] - c[1] * l[0] : q[1],
-                                              cax ? cxy2 + c[0] * l[0] + c[1] * l[1] : q[0]) *
-                                   0.15915494309189535f);
+        float s = wrap01(s_c1 + (float)A.dir *
+                                    atan_ratio(cax ? c[0] * l[1] - c[1] * l[0] : q[1],
+                                               cax ? cxy2 + c[0] * l[0] + c[1] * l[1] : q[0]) *
+                                    0.15915494309189535f);
         for (int it = 1; it < A.K; ++it) {
           float sn, omc, p[3];
           rot_sc_f(A, s, &sn, &omc);

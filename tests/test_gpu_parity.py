@@ -492,3 +492,76 @@ def test_beam_divergence_parity(SM, oracle_mod, config):
         ok2 = ref2["flag"] == 0
         assert ok2.mean() > 1 - FLAG_BUDGET["default"], ok2.mean()
         compare_lidar(r.out, ref2, ok2)
+
+
+# ------------------------------------------------------------------ sensor-model variants
+@pytest.mark.parametrize("variant", ["cw_spin", "K2", "K0", "az_start", "static_pose", "rotating_fast"])
+def test_lidar_sensor_variants(SM, oracle_mod, variant):
+    """Paths of the sensor model the BASELINE configs do not exercise: clockwise spin,
+    K = 2 and K = 0 firing-time iterations (A3), a non-default phi_start, a static pose, and
+    a fast-rotating sweep (0.6 rad of yaw: the general rotation branch instead of the
+    small-angle series).  Tier 1 projection + compositing and tier 2 end to end on config A
+    geometry (32 x 512 rays, 1k particles) moved through a 1.5 m / yawing sweep."""
+    O = oracle_mod
+    cfg, scene = S.lidar_config("A"), S.scene_for("A")
+    cfg.pose_start = S.pose(S.yaw_quat(0.1), [0.0, 0.0, 1.8])
+    cfg.pose_end = S.pose(S.yaw_quat(0.13), [1.5, 0.3, 1.8])
+    if variant == "cw_spin":
+        cfg.spin_direction = -1
+    elif variant == "K2":
+        cfg.rs_iterations = 2
+    elif variant == "K0":
+        cfg.rs_iterations = 0
+    elif variant == "az_start":
+        cfg.azimuth_start = float(np.float32(0.7))
+    elif variant == "static_pose":
+        cfg.pose_end = cfg.pose_start
+    elif variant == "rotating_fast":
+        cfg.pose_end = S.pose(S.yaw_quat(0.7), [1.5, 0.3, 1.8])
+    r = lidar_run(SM, cfg, scene, write_all_records=True)
+    rec = r.record.cpu().numpy()
+    proj = O.project_lidar(scene, cfg)
+    gv, ov, amb = np.isfinite(rec[:, 16]), proj["valid"] != 0, proj["ambiguous"] != 0
+    assert np.array_equal(gv[~amb], ov[~amb])
+    both = gv & ov & ~amb
+    db = np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both])
+    assert db[:, :2].max() < LIDAR_EPS["a"] and db[:, 2:].max() < LIDAR_EPS["b"], db.max(0)
+    assert np.array_equal(r.depth_key.cpu().numpy().view(np.uint32), proj["key"].view(np.uint32))
+    t = O.Tiling(cfg)
+    _, ids, ranges = sorted_lists(r)
+    od = r.out["ray_od"].cpu().numpy()
+    ref = O.composite(gpu_records(r), ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, wrap=1, near=cfg.min_range,
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4},
+                      pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    ref["intensity"], ref["raydrop"] = O.decode_lidar(ref["feat"])
+    ok = ref["flag"] == 0
+    assert ok.mean() > 0.999
+    compare_lidar(r.out, ref, ok)
+    ref2 = O.render_lidar(scene, cfg, tiling=t, flag_eps=LIDAR_EPS)
+    ok2 = ref2["flag"] == 0
+    assert ok2.mean() > 1 - FLAG_BUDGET["default"], ok2.mean()
+    compare_lidar(r.out, ref2, ok2)
+
+
+@pytest.mark.parametrize("variant", ["global_shutter", "K2", "kb_static", "radtan_rolling"])
+def test_camera_variants(SM, oracle_mod, variant):
+    """Camera paths beyond D: global shutter, K = 2 row fixed point, a static KB camera, and
+    pinhole-radtan with rolling shutter; tier 2 (oracle from scratch) on 320 x 180 frames."""
+    O = oracle_mod
+    cam = S.camera_config("pinhole-small" if variant == "radtan_rolling" else "D-small")
+    if variant == "global_shutter":
+        cam.rolling_shutter = 0
+    elif variant == "K2":
+        cam.rs_iterations = 2
+    elif variant == "kb_static":
+        cam.pose_end = cam.pose_start
+    scene = S.corridor_scene(23, 30000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    c = camera_run(SM, cam, scene)
+    ref = O.render_camera(scene, cam, flag_eps=CAMERA_EPS)
+    ok = ref["flag"] == 0
+    assert ok.mean() > 0.995, ok.mean()
+    rgb = c.out["rgb"].cpu().numpy()
+    assert np.abs(rgb - ref["feat"])[ok].max() < TOL_FEAT
+    assert np.abs(c.out["opacity"].cpu().numpy() - ref["opacity"])[ok].max() < TOL_FEAT
+    dm = ok & (ref["opacity"] >= 0.5)
+    assert np.abs(c.out["depth"].cpu().numpy() - ref["depth"])[dm].max(initial=0) < TOL_DEPTH
