@@ -220,8 +220,10 @@ class Tiling:
 def _gauss(scene):
     n = int(scene["means"].shape[0])
     arrs = {k: np.ascontiguousarray(scene[k], np.float32) for k in ("means", "quats", "scales", "opacity", "sh")}
+    ncoef = arrs["sh"].size // max(n, 1) // 3 if n else 16
+    deg = {1: 0, 4: 1, 9: 2, 16: 3}[ncoef]  # SH degree from the coefficient count
     G = OrGaussians(n, _p(arrs["means"], f32p), _p(arrs["quats"], f32p), _p(arrs["scales"], f32p),
-                    _p(arrs["opacity"], f32p), _p(arrs["sh"], f32p), 3)
+                    _p(arrs["opacity"], f32p), _p(arrs["sh"], f32p), deg)
     G._keep = arrs
     return G, n
 

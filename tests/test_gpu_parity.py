@@ -565,3 +565,24 @@ def test_camera_variants(SM, oracle_mod, variant):
     assert np.abs(c.out["opacity"].cpu().numpy() - ref["opacity"])[ok].max() < TOL_FEAT
     dm = ok & (ref["opacity"] >= 0.5)
     assert np.abs(c.out["depth"].cpu().numpy() - ref["depth"])[dm].max(initial=0) < TOL_DEPTH
+
+
+@pytest.mark.parametrize("degree", [0, 1, 2])
+def test_lower_sh_degrees(SM, oracle_mod, degree):
+    """SH degrees below 3 (the generic feature path): features per particle and the
+    composited outputs, tier 1, on config A with the coefficients truncated to (d+1)^2."""
+    O = oracle_mod
+    cfg, scene = S.lidar_config("A"), dict(S.scene_for("A"))
+    scene["sh"] = np.ascontiguousarray(scene["sh"][:, : (degree + 1) ** 2, :])
+    r = lidar_run(SM, cfg, scene, write_all_records=True)
+    rec = r.record.cpu().numpy()
+    proj = O.project_lidar(scene, cfg)
+    both = np.isfinite(rec[:, 16]) & (proj["valid"] != 0) & (proj["ambiguous"] == 0)
+    assert np.abs(rec[both, 13:16] - proj["feat"][both]).max() < 2e-5
+    t = O.Tiling(cfg)
+    _, ids, ranges = sorted_lists(r)
+    ref = O.composite(gpu_records(r), ids, ranges, t.ray_tile, t.ray_az, t.ray_el, r.out["ray_od"].cpu().numpy(),
+                      wrap=1, near=cfg.min_range, flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4,
+                                                            "tau": 1e-4}, pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    ref["intensity"], ref["raydrop"] = O.decode_lidar(ref["feat"])
+    compare_lidar(r.out, ref, ref["flag"] == 0)
