@@ -543,10 +543,11 @@ def test_lidar_sensor_variants(SM, oracle_mod, variant):
     compare_lidar(r.out, ref2, ok2)
 
 
-@pytest.mark.parametrize("variant", ["global_shutter", "K2", "kb_static", "radtan_rolling"])
+@pytest.mark.parametrize("variant", ["global_shutter", "K2", "kb_static", "radtan_rolling", "tile8"])
 def test_camera_variants(SM, oracle_mod, variant):
-    """Camera paths beyond D: global shutter, K = 2 row fixed point, a static KB camera, and
-    pinhole-radtan with rolling shutter; tier 2 (oracle from scratch) on 320 x 180 frames."""
+    """Camera paths beyond D: global shutter, K = 2 row fixed point, a static KB camera,
+    pinhole-radtan with rolling shutter, 8x8-pixel tiles; tier 2 (oracle from scratch) on
+    320 x 180 frames."""
     O = oracle_mod
     cam = S.camera_config("pinhole-small" if variant == "radtan_rolling" else "D-small")
     if variant == "global_shutter":
@@ -555,6 +556,8 @@ def test_camera_variants(SM, oracle_mod, variant):
         cam.rs_iterations = 2
     elif variant == "kb_static":
         cam.pose_end = cam.pose_start
+    elif variant == "tile8":
+        cam.tile_px = 8
     scene = S.corridor_scene(23, 30000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6))
     c = camera_run(SM, cam, scene)
     ref = O.render_camera(scene, cam, flag_eps=CAMERA_EPS)
