@@ -525,6 +525,13 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
     for (int q = 0; q < D; ++q) issue(q, ids[q]);
   }
   uint32_t id_pf = load_id(D);
+  // the item's first 8 column azimuths / 4 beam elevations in registers (the usual item;
+  // unused slots are masked by nc / nb below)
+  float cphi[8], bel[4];
+#pragma unroll
+  for (int ci = 0; ci < 8; ++ci) cphi[ci] = S.col_phi[ci];
+#pragma unroll
+  for (int bi = 0; bi < 4; ++bi) bel[bi] = S.beam_el[bi];
   named_sync(BAR_RAYS, NT);
   uint32_t alive = 0xffffffffu;  // rays the consumer has not terminated (2 rounds behind)
   for (int r = 0; r < n_rounds; ++r) {
@@ -556,7 +563,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
         // compares (general shapes fall through to the loops)
 #pragma unroll
         for (int ci = 0; ci < 8; ++ci) {
-          const float p = S.col_phi[ci];
+          const float p = cphi[ci];
           const bool in = ci < nc && ((bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2);
           colbits |= (uint32_t)in << ci;
         }
@@ -570,7 +577,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
         uint32_t beambits = 0;
 #pragma unroll
         for (int bi = 0; bi < 4; ++bi) {
-          const float w = S.beam_el[bi];
+          const float w = bel[bi];
           beambits |= (uint32_t)(bi < nb && bx.z <= w && w <= bx.w) << bi;
         }
         for (int bi = 4; bi < nb; ++bi) {
