@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 2
+#define SIMULI_ABI_VERSION 3
 
 enum {
   SIMULI_OK = 0,
@@ -308,6 +308,32 @@ typedef struct {
 int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorted_ids, const int32_t* tile_ranges,
                              const int32_t* tile_order, const simuli_project_params* params,
                              const simuli_render_params* rparams, simuli_camera_out* out, void* stream);
+
+/* Final camera colour, Eq. 2: c = A(omega c_f + (1 - omega) c_b(d)), with the
+ * background c_b(d) from a learned environment map and A an affine colour transform from a
+ * learned bilateral grid (readings A28):
+ *  * env_map: device [env_h][env_w][3] float, equirectangular in the world frame (z up):
+ *    longitude atan2(d_y, d_x) in [-pi, pi) -> [0, env_w), colatitude acos(d_z) in [0, pi]
+ *    -> [0, env_h), texel centres at +0.5, bilinear, wrapping in longitude, clamped in
+ *    colatitude; NULL -> c_b = 0.
+ *  * grid: device [grid_d][grid_h][grid_w][12] float, row-major 3x4 affine matrices over
+ *    (x / W, y / H, luminance), luminance = 0.299 r + 0.587 g + 0.114 b of the blended colour
+ *    clamped to [0, 1], cell centres at +0.5, trilinear, clamped at the borders;
+ *    c = M[:, :3] c_in + M[:, 3]; NULL -> A = identity.
+ * d is the pixel's ray direction (the same inverse lens model and row time as
+ * simuli_render_camera; (0, 0, 0) outside the lens validity).  rgb_fg [H*W][3] and opacity
+ * [H*W] are simuli_render_camera's rgb / opacity; rgb_out [H*W][3] (may alias rgb_fg).
+ * All device pointers, caller-owned; asynchronous on `stream`.  Errors: INVALID_ARGUMENT
+ * (NULL / non-camera params / non-positive sizes with a non-NULL table). */
+typedef struct {
+  const float* env_map;
+  int32_t env_h, env_w;
+  const float* grid;
+  int32_t grid_h, grid_w, grid_d;
+} simuli_camera_compose;
+
+int32_t simuli_compose_camera(const simuli_project_params* params, const simuli_camera_compose* compose,
+                              const float* rgb_fg, const float* opacity, float* rgb_out, void* stream);
 
 #ifdef __cplusplus
 }

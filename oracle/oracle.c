@@ -1243,3 +1243,90 @@ void or_camera_rays(const or_camera* C, const double pose0[7], const double pose
     }
   }
 }
+
+/* ------------------------------------------------------------------------------------
+ * O14 Camera final colour, Eq. 2:  c = A(omega c_f + (1 - omega) c_b(d)).
+ *     c_b: learned environment map -- reading A28: an equirectangular texture in
+ *     the world frame (z up), longitude atan2(d_y, d_x) over [-pi, pi) -> [0, W_e), colatitude
+ *     acos(d_z) over [0, pi] -> [0, H_e), texel centres at +0.5, bilinear, wrapping in
+ *     longitude, clamped in colatitude.  A: learned bilateral grid -- a grid of 3x4
+ *     affine matrices over (x / W, y / H, luminance) with luminance = 0.299 r + 0.587 g +
+ *     0.114 b of the blended colour (clamped to [0, 1]), cell centres at +0.5, trilinear,
+ *     clamped at the borders; c = M[:, :3] c_in + M[:, 3].  d = the pixel's unit ray
+ *     direction (world).  env == NULL: c_b = 0; grid == NULL: A = identity.
+ * ---------------------------------------------------------------------------------- */
+static void env_lookup(const float* env, int32_t He, int32_t We, const double d[3], double out[3]) {
+  double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  double lon = atan2(d[1], d[0]);
+  double z = n > 0.0 ? d[2] / n : 1.0;
+  if (z > 1.0) z = 1.0;
+  if (z < -1.0) z = -1.0;
+  double colat = acos(z);
+  double u = (lon + OR_PI) / OR_TWO_PI * We - 0.5;
+  double v = colat / OR_PI * He - 0.5;
+  double fu = floor(u), fv = floor(v);
+  double au = u - fu, av = v - fv;
+  int64_t u0 = (int64_t)fu, v0 = (int64_t)fv;
+  for (int c = 0; c < 3; ++c) out[c] = 0.0;
+  for (int dv = 0; dv <= 1; ++dv)
+    for (int du = 0; du <= 1; ++du) {
+      int64_t uu = ((u0 + du) % We + We) % We;
+      int64_t vv = v0 + dv;
+      if (vv < 0) vv = 0;
+      if (vv > He - 1) vv = He - 1;
+      double w = (du ? au : 1.0 - au) * (dv ? av : 1.0 - av);
+      for (int c = 0; c < 3; ++c) out[c] += w * env[(vv * We + uu) * 3 + c];
+    }
+}
+
+static void grid_apply(const float* grid, int32_t gh, int32_t gw, int32_t gd, double x, double y, const double cin[3],
+                       double out[3]) {
+  double lum = 0.299 * cin[0] + 0.587 * cin[1] + 0.114 * cin[2];
+  if (lum < 0.0) lum = 0.0;
+  if (lum > 1.0) lum = 1.0;
+  double g[3] = {x * gw - 0.5, y * gh - 0.5, lum * gd - 0.5};
+  int32_t n[3] = {gw, gh, gd};
+  int64_t i0[3];
+  double a[3];
+  for (int k = 0; k < 3; ++k) {
+    double c = g[k];
+    if (c < 0.0) c = 0.0;
+    if (c > n[k] - 1) c = n[k] - 1;
+    double f = floor(c);
+    i0[k] = (int64_t)f;
+    a[k] = c - f;
+  }
+  double M[12] = {0};
+  for (int dz = 0; dz <= 1; ++dz)
+    for (int dy = 0; dy <= 1; ++dy)
+      for (int dx = 0; dx <= 1; ++dx) {
+        int64_t xi = i0[0] + dx, yi = i0[1] + dy, zi = i0[2] + dz;
+        if (xi > gw - 1) xi = gw - 1;
+        if (yi > gh - 1) yi = gh - 1;
+        if (zi > gd - 1) zi = gd - 1;
+        double w = (dx ? a[0] : 1.0 - a[0]) * (dy ? a[1] : 1.0 - a[1]) * (dz ? a[2] : 1.0 - a[2]);
+        const float* m = &grid[((zi * gh + yi) * gw + xi) * 12];
+        for (int q = 0; q < 12; ++q) M[q] += w * m[q];
+      }
+  for (int r = 0; r < 3; ++r) out[r] = M[r * 4] * cin[0] + M[r * 4 + 1] * cin[1] + M[r * 4 + 2] * cin[2] + M[r * 4 + 3];
+}
+
+int or_compose_camera(const or_camera* C, const double* ray_od, const double* rgb_fg, const double* omega,
+                      const float* env, int32_t He, int32_t We, const float* grid, int32_t gh, int32_t gw,
+                      int32_t gd, double* rgb_out) {
+  int32_t W = C->width, H = C->height;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < (int64_t)W * H; ++r) {
+    const double* d = &ray_od[r * 6 + 3];
+    double cb[3] = {0, 0, 0}, cin[3];
+    if (env) env_lookup(env, He, We, d, cb);
+    for (int c = 0; c < 3; ++c) cin[c] = omega[r] * rgb_fg[r * 3 + c] + (1.0 - omega[r]) * cb[c];
+    if (grid) {
+      double x = ((double)(r % W) + 0.5) / W, y = ((double)(r / W) + 0.5) / H;
+      grid_apply(grid, gh, gw, gd, x, y, cin, &rgb_out[r * 3]);
+    } else {
+      for (int c = 0; c < 3; ++c) rgb_out[r * 3 + c] = cin[c];
+    }
+  }
+  return 0;
+}

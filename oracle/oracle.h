@@ -159,6 +159,11 @@ void or_camera_rays(const or_camera* C, const double pose0[7], const double pose
 void or_set_threads(int n);
 int  or_get_threads(void);
 
+/* O14: camera final colour, Eq. 2 (env map c_b + bilateral grid A; readings A28) */
+int or_compose_camera(const or_camera* C, const double* ray_od, const double* rgb_fg, const double* omega,
+                      const float* env, int32_t He, int32_t We, const float* grid, int32_t gh, int32_t gw,
+                      int32_t gd, double* rgb_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -112,6 +112,8 @@ def lib():
         L.or_sh_eval.argtypes = [f64p, C.c_int, f64p, f64p]
         L.or_response.argtypes = [f64p, f64p, f64p, f64p, f64p]
         L.or_ut_affine.argtypes = [f64p, f64p, f64p, f64p, f64p, f64p, f64p, f64p]
+        L.or_compose_camera.argtypes = [C.POINTER(OrCamera), f64p, f64p, f64p, f32p, C.c_int32, C.c_int32, f32p,
+                                        C.c_int32, C.c_int32, C.c_int32, f64p]
         L.or_divergence_cov.argtypes = [f64p, f64p, f64p, C.c_double, f64p]
         L.or_cholesky3.argtypes = [f64p, f64p]
         L.or_lower_inverse3.argtypes = [f64p, f64p]
@@ -520,6 +522,21 @@ def sigma_points(mu, q, s, ut=None):
                                _p(pts, f64p), _p(wm, f64p), _p(wc, f64p))
     assert rc == 0
     return pts.reshape(7, 3), wm, wc
+
+
+def compose_camera(cam, ray_od, rgb_fg, omega, env=None, grid=None):
+    """Eq. 2: c = A(omega c_f + (1 - omega) c_b(d)); env [He, We, 3], grid [gd, gh, gw, 12]."""
+    n = cam.width * cam.height
+    out = np.zeros((n, 3))
+    Cm = make_camera(cam)
+    e = None if env is None else np.ascontiguousarray(env, np.float32)
+    g = None if grid is None else np.ascontiguousarray(grid, np.float32)
+    lib().or_compose_camera(C.byref(Cm), _p(_d(ray_od).reshape(-1), f64p), _p(_d(rgb_fg).reshape(-1), f64p),
+                            _p(_d(omega), f64p), None if e is None else _p(e, f32p),
+                            0 if e is None else e.shape[0], 0 if e is None else e.shape[1],
+                            None if g is None else _p(g, f32p), 0 if g is None else g.shape[1],
+                            0 if g is None else g.shape[2], 0 if g is None else g.shape[0], _p(out, f64p))
+    return out
 
 
 def divergence_cov(Sigma, mu, o, theta):

@@ -786,3 +786,129 @@ extern "C" int32_t simuli_debug_render_prof(long long* host, int64_t n) {
   return cudaMemcpyFromSymbol(host, simuli::g_render_prof, sizeof(long long) * 4 * n) == cudaSuccess ? 0 : 3;
 }
 #endif
+
+namespace simuli {
+namespace {
+
+// ------------------------------------------------------------------ camera Eq. 2
+struct ComposeArgs {
+  CameraArgs cam;  // lens model + poses (ray directions)
+  const float* env;
+  int He, We;
+  const float* grid;
+  int gh, gw, gd;
+  const float* rgb_fg;
+  const float* opacity;
+  float* rgb_out;
+};
+
+__device__ void env_lookup(const ComposeArgs& A, const double d[3], float out[3]) {
+  const double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  const double lon = atan2(d[1], d[0]);
+  const double z = n > 0.0 ? fmin(1.0, fmax(-1.0, d[2] / n)) : 1.0;
+  const double colat = acos(z);
+  const double u = (lon + 3.141592653589793) / 6.283185307179586 * A.We - 0.5;
+  const double v = colat / 3.141592653589793 * A.He - 0.5;
+  const double fu = floor(u), fv = floor(v);
+  const float au = (float)(u - fu), av = (float)(v - fv);
+  const int u0 = (int)fu, v0 = (int)fv;
+  float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int dv = 0; dv <= 1; ++dv)
+#pragma unroll
+    for (int du = 0; du <= 1; ++du) {
+      const int uu = ((u0 + du) % A.We + A.We) % A.We;
+      const int vv = min(max(v0 + dv, 0), A.He - 1);
+      const float w = (du ? au : 1.f - au) * (dv ? av : 1.f - av);
+      const float* t = A.env + ((size_t)vv * A.We + uu) * 3;
+      acc[0] = fmaf(w, __ldg(t), acc[0]);
+      acc[1] = fmaf(w, __ldg(t + 1), acc[1]);
+      acc[2] = fmaf(w, __ldg(t + 2), acc[2]);
+    }
+  out[0] = acc[0]; out[1] = acc[1]; out[2] = acc[2];
+}
+
+// thread per pixel: ray direction, environment map, blend, bilateral-grid affine
+__global__ void __launch_bounds__(256) k_compose_camera(const ComposeArgs A) {
+  const int W = A.cam.width, H = A.cam.height;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)W * H) return;
+  const int i = (int)(p % W), j = (int)(p / W);
+  float cb[3] = {0.f, 0.f, 0.f};
+  if (A.env) {
+    double dc[3], d[3] = {0.0, 0.0, 0.0};
+    if (unproject(A.cam, (double)i + 0.5, (double)j + 0.5, dc)) {
+      const double s = A.cam.rolling ? ((double)j + 0.5) / (double)H : 0.0;
+      double R[9], o[3];
+      pose_at_d(A.cam.pose, s, R, o);
+      for (int k = 0; k < 3; ++k) d[k] = R[3 * k] * dc[0] + R[3 * k + 1] * dc[1] + R[3 * k + 2] * dc[2];
+    }
+    env_lookup(A, d, cb);
+  }
+  const float om = __ldg(A.opacity + p);
+  float cin[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) cin[c] = om * __ldg(A.rgb_fg + 3 * p + c) + (1.f - om) * cb[c];
+  float out[3] = {cin[0], cin[1], cin[2]};
+  if (A.grid) {
+    const float lum = fminf(1.f, fmaxf(0.f, 0.299f * cin[0] + 0.587f * cin[1] + 0.114f * cin[2]));
+    const float g[3] = {((float)i + 0.5f) / W * A.gw - 0.5f, ((float)j + 0.5f) / H * A.gh - 0.5f, lum * A.gd - 0.5f};
+    const int n[3] = {A.gw, A.gh, A.gd};
+    int i0[3];
+    float a[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float c = fminf(fmaxf(g[k], 0.f), (float)(n[k] - 1));
+      const float f = floorf(c);
+      i0[k] = (int)f;
+      a[k] = c - f;
+    }
+    float M[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) M[q] = 0.f;
+#pragma unroll
+    for (int dz = 0; dz <= 1; ++dz)
+#pragma unroll
+      for (int dy = 0; dy <= 1; ++dy)
+#pragma unroll
+        for (int dx = 0; dx <= 1; ++dx) {
+          const int xi = min(i0[0] + dx, A.gw - 1), yi = min(i0[1] + dy, A.gh - 1), zi = min(i0[2] + dz, A.gd - 1);
+          const float w = (dx ? a[0] : 1.f - a[0]) * (dy ? a[1] : 1.f - a[1]) * (dz ? a[2] : 1.f - a[2]);
+          const float* m = A.grid + (((size_t)zi * A.gh + yi) * A.gw + xi) * 12;
+#pragma unroll
+          for (int q = 0; q < 12; ++q) M[q] = fmaf(w, __ldg(m + q), M[q]);
+        }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) out[r] = M[4 * r] * cin[0] + M[4 * r + 1] * cin[1] + M[4 * r + 2] * cin[2] + M[4 * r + 3];
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) A.rgb_out[3 * p + c] = out[c];
+}
+
+}  // namespace
+}  // namespace simuli
+
+extern "C" int32_t simuli_compose_camera(const simuli_project_params* P, const simuli_camera_compose* comp,
+                                         const float* rgb_fg, const float* opacity, float* rgb_out, void* stream) {
+  using namespace simuli;
+  clear_error();
+  SIMULI_REQUIRE(P && comp && rgb_fg && opacity && rgb_out, "simuli_compose_camera: NULL argument");
+  SIMULI_REQUIRE(P->kind == SIMULI_SENSOR_CAMERA && P->camera, "simuli_compose_camera: needs camera params");
+  SIMULI_REQUIRE(!comp->env_map || (comp->env_h > 0 && comp->env_w > 0), "simuli_compose_camera: bad env map size");
+  SIMULI_REQUIRE(!comp->grid || (comp->grid_h > 0 && comp->grid_w > 0 && comp->grid_d > 0),
+                 "simuli_compose_camera: bad grid size");
+  const simuli_camera& C = *P->camera;
+  ComposeArgs A{};
+  A.cam.model = C.model; A.cam.width = C.width; A.cam.height = C.height; A.cam.rolling = C.rolling_shutter;
+  A.cam.fx = C.fx; A.cam.fy = C.fy; A.cam.cx = C.cx; A.cam.cy = C.cy;
+  for (int i = 0; i < 5; ++i) A.cam.k[i] = C.k[i];
+  A.cam.max_theta = C.max_theta_rad;
+  A.cam.pose = make_pose_interp_d(P->pose_start, P->pose_end);
+  A.env = comp->env_map; A.He = comp->env_h; A.We = comp->env_w;
+  A.grid = comp->grid; A.gh = comp->grid_h; A.gw = comp->grid_w; A.gd = comp->grid_d;
+  A.rgb_fg = rgb_fg; A.opacity = opacity; A.rgb_out = rgb_out;
+  const int64_t n = (int64_t)C.width * C.height;
+  if (n == 0) return SIMULI_OK;
+  k_compose_camera<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A);
+  return launch_check("simuli_compose_camera");
+}

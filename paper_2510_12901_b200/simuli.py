@@ -25,7 +25,8 @@ CAM_PINHOLE_RADTAN, CAM_FISHEYE_KB = 0, 1
 RECORD_FLOATS = 20
 
 EXPORTED = ["simuli_last_error", "simuli_abi_version", "simuli_build_tiles", "simuli_project",
-            "simuli_bin_sort_workspace_size", "simuli_bin_sort", "simuli_render_lidar", "simuli_render_camera"]
+            "simuli_bin_sort_workspace_size", "simuli_bin_sort", "simuli_render_lidar", "simuli_render_camera",
+            "simuli_compose_camera"]
 
 f32p, i32p, f64p = C.POINTER(C.c_float), C.POINTER(C.c_int32), C.POINTER(C.c_double)
 
@@ -81,6 +82,11 @@ class TilingDev(C.Structure):
 class Gaussians(C.Structure):
     _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("quats", C.c_void_p), ("scales", C.c_void_p),
                 ("opacity", C.c_void_p), ("sh", C.c_void_p), ("sh_degree", C.c_int32)]
+
+
+class CameraCompose(C.Structure):
+    _fields_ = [("env_map", C.c_void_p), ("env_h", C.c_int32), ("env_w", C.c_int32), ("grid", C.c_void_p),
+                ("grid_h", C.c_int32), ("grid_w", C.c_int32), ("grid_d", C.c_int32)]
 
 
 class Camera(C.Structure):
@@ -142,6 +148,8 @@ def load():
     L.simuli_render_camera.argtypes = [C.POINTER(Projected), C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(CameraOut),
                                        C.c_void_p]
+    L.simuli_compose_camera.argtypes = [C.POINTER(ProjectParams), C.POINTER(CameraCompose), C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
     for name in EXPORTED:
         if name not in ("simuli_last_error", "simuli_abi_version"):
             getattr(L, name).restype = C.c_int32
@@ -226,6 +234,16 @@ def simuli_render_lidar(proj, sorted_ids, tile_ranges, params, rparams, out: Lid
     _check(load().simuli_render_lidar(C.byref(proj), _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order),
                                       C.byref(params),
                                       C.byref(rparams), C.byref(out), _stream(stream)))
+
+
+def simuli_compose_camera(params, env, grid, rgb_fg, opacity, rgb_out, stream=None):
+    """Eq. 2 (env map + bilateral grid); env [He, We, 3] / grid [gd, gh, gw, 12] device float32 or None."""
+    comp = CameraCompose(None if env is None else env.data_ptr(), 0 if env is None else env.shape[0],
+                         0 if env is None else env.shape[1], None if grid is None else grid.data_ptr(),
+                         0 if grid is None else grid.shape[1], 0 if grid is None else grid.shape[2],
+                         0 if grid is None else grid.shape[0])
+    _check(load().simuli_compose_camera(C.byref(params), C.byref(comp), _ptr(rgb_fg), _ptr(opacity), _ptr(rgb_out),
+                                        _stream(stream)))
 
 
 def simuli_render_camera(proj, sorted_ids, tile_ranges, params, rparams, out: CameraOut, stream=None,
@@ -428,6 +446,13 @@ class CameraRenderer(_Frame):
     def render(self, stream=None):
         simuli_render_camera(self.projected, self.sorted_ids, self.tile_ranges, self.params, self.rparams,
                              self.out_struct, stream, self.tile_order)
+
+    def compose(self, env=None, grid=None, stream=None):
+        """Eq. 2 final colour from the last frame's c_f and omega (env map, bilateral grid)."""
+        import torch
+        out = torch.empty_like(self.out["rgb"])
+        simuli_compose_camera(self.params, env, grid, self.out["rgb"], self.out["opacity"], out, stream)
+        return out
 
     def frame(self, pose_start=None, pose_end=None, stream=None, sync_capacity=False):
         if pose_start is not None:

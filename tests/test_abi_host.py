@@ -38,7 +38,7 @@ def test_exports_every_header_symbol(lib):
     exported = {ln.split()[-1] for ln in nm.splitlines() if " T " in ln}
     assert set(syms) <= exported
     assert set(lib.EXPORTED) == set(syms)
-    assert L.simuli_abi_version() == 2
+    assert L.simuli_abi_version() == 3
 
 
 def test_library_is_sm100a(lib):
@@ -119,5 +119,6 @@ def test_workspace_size_and_bad_args(lib):
     assert b"NULL" in L.simuli_last_error()
     assert L.simuli_render_lidar(None, None, None, None, None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
     assert L.simuli_render_camera(None, None, None, None, None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
+    assert L.simuli_compose_camera(None, None, None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
     size = ctypes.c_size_t(0)
     assert L.simuli_bin_sort_workspace_size(-1, 10, 1, ctypes.byref(size)) == lib.SIMULI_ERR_INVALID_ARGUMENT

@@ -589,3 +589,33 @@ def test_lower_sh_degrees(SM, oracle_mod, degree):
                                                             "tau": 1e-4}, pi_f=t.pi_f, two_pi_f=t.two_pi_f)
     ref["intensity"], ref["raydrop"] = O.decode_lidar(ref["feat"])
     compare_lidar(r.out, ref, ref["flag"] == 0)
+
+
+@pytest.mark.parametrize("name", ["D-small", "pinhole-small"])
+def test_compose_camera_parity(SM, oracle_mod, name):
+    """Eq. 2 (P: camera model, A28): GPU simuli_compose_camera vs the oracle's compose on the
+    same c_f / omega (the GPU frame's), with a random environment map and a random
+    near-identity bilateral grid; also env only, grid only and neither."""
+    O = oracle_mod
+    cam = S.camera_config(name)
+    scene = S.corridor_scene(23, 20000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    c = camera_run(SM, cam, scene)
+    rng = np.random.default_rng(77)
+    env = rng.uniform(0, 1, (32, 64, 3)).astype(np.float32)
+    grid = np.zeros((8, 9, 16, 12), np.float32)
+    grid[..., 0] = grid[..., 5] = grid[..., 10] = 1.0
+    grid += rng.normal(scale=0.05, size=grid.shape).astype(np.float32)
+    rays = O.camera_rays(cam)
+    cf = c.out["rgb"].cpu().numpy().astype(np.float64)
+    om = c.out["opacity"].cpu().numpy().astype(np.float64)
+    assert (om > 0.1).mean() > 0.02 and (om < 0.9).mean() > 0.02
+    valid = rays["valid"] != 0
+    for e, g in ((env, grid), (env, None), (None, grid), (None, None)):
+        got = c.compose(None if e is None else torch.from_numpy(e).cuda(),
+                        None if g is None else torch.from_numpy(g).cuda()).cpu().numpy()
+        ref = O.compose_camera(cam, rays["od"], cf, om, e, g)
+        err = np.abs(got - ref)[valid].max()
+        print(f"{name} env={e is not None} grid={g is not None}: max |gpu - oracle| {err:.2e}")
+        assert err < 2e-5
+        if e is None:
+            assert np.abs(got - ref).max() < 2e-5  # invalid pixels: no background term at all

@@ -775,3 +775,79 @@ def test_divergence_tiled_equals_bruteforce_and_widens(oracle_mod, theta):
         d = (mu - o) + rng.normal(scale=2.0, size=3)
         d /= np.linalg.norm(d)
         assert O.response(mu, Mh.reshape(-1), o, d)[1] <= O.response(mu, M.reshape(-1), o, d)[1] * (1 + 1e-9) + 1e-12
+
+
+# ------------------------------------------------------------------ camera Eq. 2
+def _dirs(lon, colat):
+    return np.stack([np.sin(colat) * np.cos(lon), np.sin(colat) * np.sin(lon), np.cos(colat)], -1)
+
+
+def test_compose_identity_and_constant_background(oracle_mod):
+    """Eq. 2 with A = identity: c = omega c_f + (1 - omega) c_b; a constant environment gives
+    c_b = that constant for every direction; no map, no grid: c = omega c_f."""
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    rng = np.random.default_rng(41)
+    n = cam.width * cam.height
+    od = np.zeros((n, 6))
+    od[:, 3:] = rng.normal(size=(n, 3))
+    cf, om = rng.uniform(0, 1, (n, 3)), rng.uniform(0, 1, n)
+    k = np.array([0.2, 0.5, 0.9], np.float32)
+    env = np.broadcast_to(k, (7, 13, 3)).copy()
+    ident = np.zeros((3, 4, 5, 12), np.float32)
+    ident[..., 0] = ident[..., 5] = ident[..., 10] = 1.0
+    out = O.compose_camera(cam, od, cf, om, env, ident)
+    assert np.allclose(out, om[:, None] * cf + (1 - om[:, None]) * k.astype(np.float64), atol=1e-6)
+    assert np.allclose(O.compose_camera(cam, od, cf, om), om[:, None] * cf, atol=1e-15)
+
+
+def test_compose_env_bilinear(oracle_mod):
+    """The equirectangular lookup returns a texel's value at its centre direction, the mean of
+    two neighbours halfway between them, and wraps across longitude +-pi."""
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    He, We = 6, 10
+    rng = np.random.default_rng(42)
+    env = rng.uniform(0, 1, (He, We, 3)).astype(np.float32)
+    i, j = 2, 3
+    lon = (j + 0.5) / We * 2 * np.pi - np.pi
+    colat = (i + 0.5) / He * np.pi
+    lon_half = (j + 1.0) / We * 2 * np.pi - np.pi
+    lon_wrap = np.pi - 1e-12  # between the last column and the first (u = We - 0.5 ~ -0.5 wrapped)
+    d = np.array([_dirs(lon, colat), _dirs(lon_half, colat), _dirs(lon_wrap, colat)])
+    n = cam.width * cam.height
+    od = np.zeros((n, 6))
+    od[:3, 3:] = d
+    out = O.compose_camera(cam, od, np.zeros((n, 3)), np.zeros(n), env, None)
+    assert np.allclose(out[0], env[i, j], atol=1e-9)
+    assert np.allclose(out[1], 0.5 * (env[i, j] + env[i, j + 1]), atol=1e-9)
+    assert np.allclose(out[2], 0.5 * (env[i, We - 1] + env[i, 0]), atol=1e-6)
+
+
+def test_compose_grid_trilinear_exact_for_affine_fields(oracle_mod):
+    """A bilateral grid whose 12 coefficients are an affine function of the cell-centre
+    coordinates reproduces that function exactly inside the grid (trilinear interpolation
+    is exact for affine fields); checked against the field evaluated directly."""
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    W, H = cam.width, cam.height
+    gd, gh, gw = 4, 5, 6
+    rng = np.random.default_rng(43)
+    Acoef = rng.normal(scale=0.1, size=(12, 3))
+    b = rng.normal(scale=0.1, size=12)
+    zc, yc, xc = np.meshgrid((np.arange(gd) + 0.5) / gd, (np.arange(gh) + 0.5) / gh, (np.arange(gw) + 0.5) / gw,
+                             indexing="ij")
+    grid = (np.stack([xc, yc, zc], -1) @ Acoef.T + b).astype(np.float64)
+    n = W * H
+    cf = rng.uniform(0.2, 0.8, (n, 3))
+    om = np.ones(n)
+    out = O.compose_camera(cam, np.zeros((n, 6)), cf, om, None, grid.astype(np.float32))
+    px, py = (np.arange(n) % W + 0.5) / W, (np.arange(n) // W + 0.5) / H
+    lum = np.clip(0.299 * cf[:, 0] + 0.587 * cf[:, 1] + 0.114 * cf[:, 2], 0, 1)
+    inside = (px > 0.5 / gw) & (px < 1 - 0.5 / gw) & (py > 0.5 / gh) & (py < 1 - 0.5 / gh) & \
+             (lum > 0.5 / gd) & (lum < 1 - 0.5 / gd)
+    M = np.stack([px, py, lum], -1) @ Acoef.T + b  # the field itself (float64)
+    M = M.reshape(n, 3, 4)
+    ref = np.einsum("nij,nj->ni", M[:, :, :3], cf) + M[:, :, 3]
+    assert inside.mean() > 0.3
+    assert np.abs(out - ref)[inside].max() < 1e-6  # (grid stored as float32)
