@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 3
+#define SIMULI_ABI_VERSION 4
 
 enum {
   SIMULI_OK = 0,
@@ -154,7 +154,16 @@ typedef struct {
   const int32_t *elev_tile_beam_offsets, *elev_tile_beams, *az_tile_col_offsets, *az_tile_cols;
 } simuli_tiling_dev;
 
-/* Gaussian particle set G_l or G_c: device pointers. */
+/* Gaussian particle set G_l or G_c: device pointers.
+ * Scene graph (reading A29): particles of dynamic objects are stored in their
+ * object's local frame.  actor_id [n] (device, or NULL = everything is static background)
+ * gives -1 for the static background or the object index a in [0, n_actors); actor_pose
+ * [n_actors] (device) is object a's SE(3) object -> world at the frame's timestamp t (the
+ * sequence of poses + learned offsets is resolved by the caller).  simuli_project maps
+ * each object particle to world coordinates first: mu_w = float32(R_a mu + t_a) (computed
+ * in double, rounded once), q_w = q_a (x) q (so Sigma_w = R_a Sigma R_a^T), scales and SH
+ * unchanged (SH stay in the world frame, A29); everything downstream (depth key, UT,
+ * records) sees the world particle.  An id < -1 or >= n_actors makes the particle invalid. */
 typedef struct {
   int64_t n;
   const float* means;   /* [n][3]              */
@@ -163,6 +172,9 @@ typedef struct {
   const float* opacity; /* [n]                 */
   const float* sh;      /* [n][(deg+1)^2][3]   */
   int32_t sh_degree;    /* 0..3                */
+  const int32_t* actor_id;        /* [n] or NULL (A29)                 */
+  const simuli_pose* actor_pose;  /* [n_actors] object -> world at t   */
+  int32_t n_actors;
 } simuli_gaussians;
 
 /* Camera (A22).  model PINHOLE_RADTAN: k = (k1, k2, p1, p2, k3) (OpenCV);
@@ -219,7 +231,8 @@ typedef struct {
  * extent_sigma std-devs (A11), rounded outward.  LiDAR: ray-based culling by the SAT
  * rectangle count (Proc. RayOccupancyCount / ProjectParticles) and the
  * coarse tile count; camera: tiles of tile_px pixels, no culling.
- * Errors: INVALID_ARGUMENT (NULL / size mismatch / kind), UNSUPPORTED (sh_degree > 3),
+ * Errors: INVALID_ARGUMENT (NULL / size mismatch / kind; actor_id set with n_actors < 1 or
+ * actor_pose NULL), UNSUPPORTED (sh_degree > 3),
  * CUDA (launch failure).  Device pointers in `out` must hold n entries. */
 int32_t simuli_project(const simuli_gaussians* gaussians, const simuli_project_params* params,
                        simuli_projected* out, void* stream);
@@ -323,6 +336,10 @@ int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorte
  * d is the pixel's ray direction (the same inverse lens model and row time as
  * simuli_render_camera; (0, 0, 0) outside the lens validity).  rgb_fg [H*W][3] and opacity
  * [H*W] are simuli_render_camera's rgb / opacity; rgb_out [H*W][3] (may alias rgb_fg).
+ * rgb_fg is Eq. 1's sum of SH alpha T, i.e. already omega times the opacity-normalised
+ * foreground colour, so Eq. 2's "omega c_f" IS rgb_fg (A28: P:122 calls the step alpha
+ * compositing; multiplying the sum by omega again would weight the foreground by omega^2):
+ * c_in = rgb_fg + (1 - omega) c_b.
  * All device pointers, caller-owned; asynchronous on `stream`.  Errors: INVALID_ARGUMENT
  * (NULL / non-camera params / non-positive sizes with a non-NULL table). */
 typedef struct {

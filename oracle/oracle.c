@@ -1254,6 +1254,8 @@ void or_camera_rays(const or_camera* C, const double pose0[7], const double pose
  *     0.114 b of the blended colour (clamped to [0, 1]), cell centres at +0.5, trilinear,
  *     clamped at the borders; c = M[:, :3] c_in + M[:, 3].  d = the pixel's unit ray
  *     direction (world).  env == NULL: c_b = 0; grid == NULL: A = identity.
+ *     rgb_fg is Eq. 1's sum SH alpha T = omega * (normalised c_f), so "omega c_f" of Eq. 2 is
+ *     rgb_fg itself (A28: the step is alpha compositing).
  * ---------------------------------------------------------------------------------- */
 static void env_lookup(const float* env, int32_t He, int32_t We, const double d[3], double out[3]) {
   double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
@@ -1320,7 +1322,7 @@ int or_compose_camera(const or_camera* C, const double* ray_od, const double* rg
     const double* d = &ray_od[r * 6 + 3];
     double cb[3] = {0, 0, 0}, cin[3];
     if (env) env_lookup(env, He, We, d, cb);
-    for (int c = 0; c < 3; ++c) cin[c] = omega[r] * rgb_fg[r * 3 + c] + (1.0 - omega[r]) * cb[c];
+    for (int c = 0; c < 3; ++c) cin[c] = rgb_fg[r * 3 + c] + (1.0 - omega[r]) * cb[c];
     if (grid) {
       double x = ((double)(r % W) + 0.5) / W, y = ((double)(r / W) + 0.5) / H;
       grid_apply(grid, gh, gw, gd, x, y, cin, &rgb_out[r * 3]);
@@ -1329,4 +1331,65 @@ int or_compose_camera(const or_camera* C, const double* ray_od, const double* rg
     }
   }
   return 0;
+}
+
+/* ------------------------------------------------------------------------------------
+ * O0 Scene graph (reading A29): particles of a dynamic object live in the object's
+ *     local frame and are "transformed to world coordinates by applying the SE(3)
+ *     transformation corresponding to the timestamp t":  mu_w = R_a mu + t_a,
+ *     Sigma_w = R_a Sigma R_a^T, i.e. the rotation R_a R(q) = R(q_a (x) q) with S unchanged.
+ *     The world particle is a float32 particle (mu_w rounded once from double, q_w the
+ *     normalised double product rounded to float32).  actor_id -1: static (copied);
+ *     outside [-1, n_actors): the particle is made degenerate (zero quaternion -> invalid,
+ *     A20).  actor_pose [n_actors][7] = (q w,x,y,z, t), object -> world at t.
+ * ---------------------------------------------------------------------------------- */
+void or_actors_to_world(int64_t n, const float* means, const float* quats, const int32_t* actor_id,
+                        int32_t n_actors, const double* actor_pose, float* means_w, float* quats_w) {
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t a = actor_id[i];
+    if (a == -1) {
+      for (int c = 0; c < 3; ++c) means_w[3 * i + c] = means[3 * i + c];
+      for (int c = 0; c < 4; ++c) quats_w[4 * i + c] = quats[4 * i + c];
+      continue;
+    }
+    if (a < -1 || a >= n_actors) {
+      for (int c = 0; c < 3; ++c) means_w[3 * i + c] = means[3 * i + c];
+      for (int c = 0; c < 4; ++c) quats_w[4 * i + c] = 0.0f;
+      continue;
+    }
+    const double* P = actor_pose + 7 * (int64_t)a;
+    double Ra[9];
+    or_quat_to_rot(P, Ra);
+    for (int r = 0; r < 3; ++r) {
+      double acc = P[4 + r];
+      for (int c = 0; c < 3; ++c) acc += Ra[3 * r + c] * (double)means[3 * i + c];
+      means_w[3 * i + r] = (float)acc;
+    }
+    /* Hamilton product q_a (x) q of the unit quaternions */
+    double qa[4], q[4], na = 0.0, nq = 0.0;
+    for (int c = 0; c < 4; ++c) {
+      qa[c] = P[c];
+      q[c] = quats[4 * i + c];
+      na += qa[c] * qa[c];
+      nq += q[c] * q[c];
+    }
+    if (!(na > 0.0) || !(nq > 0.0)) {
+      for (int c = 0; c < 4; ++c) quats_w[4 * i + c] = 0.0f;
+      continue;
+    }
+    na = sqrt(na);
+    nq = sqrt(nq);
+    for (int c = 0; c < 4; ++c) {
+      qa[c] /= na;
+      q[c] /= nq;
+    }
+    const double w = qa[0] * q[0] - qa[1] * q[1] - qa[2] * q[2] - qa[3] * q[3];
+    const double x = qa[0] * q[1] + qa[1] * q[0] + qa[2] * q[3] - qa[3] * q[2];
+    const double y = qa[0] * q[2] - qa[1] * q[3] + qa[2] * q[0] + qa[3] * q[1];
+    const double z = qa[0] * q[3] + qa[1] * q[2] - qa[2] * q[1] + qa[3] * q[0];
+    quats_w[4 * i + 0] = (float)w;
+    quats_w[4 * i + 1] = (float)x;
+    quats_w[4 * i + 2] = (float)y;
+    quats_w[4 * i + 3] = (float)z;
+  }
 }

@@ -164,6 +164,10 @@ int or_compose_camera(const or_camera* C, const double* ray_od, const double* rg
                       const float* env, int32_t He, int32_t We, const float* grid, int32_t gh, int32_t gw,
                       int32_t gd, double* rgb_out);
 
+/* O0: scene graph, object particles -> world at the frame's timestamp (A29) */
+void or_actors_to_world(int64_t n, const float* means, const float* quats, const int32_t* actor_id,
+                        int32_t n_actors, const double* actor_pose, float* means_w, float* quats_w);
+
 #ifdef __cplusplus
 }
 #endif

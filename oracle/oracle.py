@@ -123,6 +123,7 @@ def lib():
         L.or_elev_tile.argtypes = [C.POINTER(OrTiling), C.c_float]
         L.or_az_col.argtypes = [C.POINTER(OrTiling), C.c_float]
         L.or_set_threads.argtypes = [C.c_int]
+        L.or_actors_to_world.argtypes = [C.c_int64, f32p, f32p, i32p, C.c_int32, f64p, f32p, f32p]
         _lib = L
     return _lib
 
@@ -220,6 +221,8 @@ class Tiling:
 # ------------------------------------------------------------------------------------
 
 def _gauss(scene):
+    if scene.get("actor_id") is not None:  # scene graph first (O0)
+        scene = actors_to_world(scene)
     n = int(scene["means"].shape[0])
     arrs = {k: np.ascontiguousarray(scene[k], np.float32) for k in ("means", "quats", "scales", "opacity", "sh")}
     ncoef = arrs["sh"].size // max(n, 1) // 3 if n else 16
@@ -400,6 +403,8 @@ def decode_lidar(zeta):
 
 
 def records_from_projection(proj, scene):
+    if scene.get("actor_id") is not None:  # world particles (O0)
+        scene = actors_to_world(scene)
     return {"mu": scene["means"].astype(np.float64), "Mrows": proj["Mrows"],
             "sigma": scene["opacity"].astype(np.float64), "feat": proj["feat"], "box": proj["box"]}
 
@@ -536,6 +541,27 @@ def compose_camera(cam, ray_od, rgb_fg, omega, env=None, grid=None):
                             0 if e is None else e.shape[0], 0 if e is None else e.shape[1],
                             None if g is None else _p(g, f32p), 0 if g is None else g.shape[1],
                             0 if g is None else g.shape[2], 0 if g is None else g.shape[0], _p(out, f64p))
+    return out
+
+
+def actors_to_world(scene, actor_id=None, actor_pose=None):
+    """O0 (A29): the scene with object particles mapped to world coordinates at t.
+    actor_id [n] int32 (-1 static), actor_pose [n_actors, 7] (q w,x,y,z, t); defaults to the
+    scene's own 'actor_id' / 'actor_pose' keys.  Returns a new scene dict without them."""
+    actor_id = scene.get("actor_id") if actor_id is None else actor_id
+    actor_pose = scene.get("actor_pose") if actor_pose is None else actor_pose
+    out = {k: v for k, v in scene.items() if k not in ("actor_id", "actor_pose")}
+    if actor_id is None:
+        return out
+    n = int(scene["means"].shape[0])
+    m = np.ascontiguousarray(scene["means"], np.float32)
+    q = np.ascontiguousarray(scene["quats"], np.float32)
+    ids = np.ascontiguousarray(actor_id, np.int32)
+    ap = _d(np.asarray(actor_pose, np.float32).astype(np.float64))  # the float32 poses, exactly
+    mw, qw = np.zeros((n, 3), np.float32), np.zeros((n, 4), np.float32)
+    lib().or_actors_to_world(n, _p(m, f32p), _p(q, f32p), _p(ids, i32p), int(ap.shape[0]), _p(ap, f64p),
+                             _p(mw, f32p), _p(qw, f32p))
+    out["means"], out["quats"] = mw, qw
     return out
 
 

@@ -79,6 +79,9 @@ struct ProjArgs {
   int64_t n;
   const float *means, *quats, *scales, *opacity, *sh;
   int sh_degree, n_coef;
+  const int* actor_id;      // scene graph (A29): -1 static, else object index
+  const float* actor_pose;  // [n_actors][7] (q w,x,y,z, t) object -> world at t
+  int n_actors;
   PoseInterpF pose;
   int K;
   UTW ut;
@@ -395,7 +398,7 @@ constexpr double kPiD = 3.141592653589793;
 constexpr int kSmemBounds = 264;
 constexpr int kShSmem = 8 * 12 * 32 * 16;
 
-template <int KIND, bool DIV>
+template <int KIND, bool DIV, bool ACT>
 __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
   // tiling boundaries / row scales staged in shared memory (binary searches hit smem)
   __shared__ float s_bounds[kSmemBounds], s_rscale[kSmemBounds];
@@ -435,9 +438,38 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
   }
   // ---- loads (SoA; quaternion as one 16-byte load)
   float mu[3] = {__ldg(A.means + 3 * g), __ldg(A.means + 3 * g + 1), __ldg(A.means + 3 * g + 2)};
-  const float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + g);
+  float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + g);
   const float sc[3] = {__ldg(A.scales + 3 * g), __ldg(A.scales + 3 * g + 1), __ldg(A.scales + 3 * g + 2)};
   const float sigma = __ldg(A.opacity + g);
+  bool actor_ok = true;
+  if (ACT) {
+    // scene graph (A29): object particle -> world with its object's pose at t;
+    // the mean in double, rounded once; q_w = q_a (x) q in float (normalised below)
+    const int a = __ldg(A.actor_id + g);
+    if (a >= 0 && a < A.n_actors) {
+      const float* ap = A.actor_pose + 7 * (size_t)a;
+      const float qa4[4] = {__ldg(ap), __ldg(ap + 1), __ldg(ap + 2), __ldg(ap + 3)};
+      const double qn = sqrt((double)qa4[0] * qa4[0] + (double)qa4[1] * qa4[1] + (double)qa4[2] * qa4[2] +
+                             (double)qa4[3] * qa4[3]);
+      const double w = qa4[0] / qn, x = qa4[1] / qn, y = qa4[2] / qn, z = qa4[3] / qn;
+      const double Ra[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z),     2 * (x * z + w * y),
+                            2 * (x * y + w * z),     1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                            2 * (x * z - w * y),     2 * (y * z + w * x),     1 - 2 * (x * x + y * y)};
+      const double m0 = mu[0], m1 = mu[1], m2 = mu[2];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        mu[c] = __double2float_rn(Ra[3 * c] * m0 + Ra[3 * c + 1] * m1 + Ra[3 * c + 2] * m2 + (double)__ldg(ap + 4 + c));
+      const float aw = (float)w, ax = (float)x, ay = (float)y, az = (float)z;
+      const float4 ql = q4;
+      q4.x = aw * ql.x - ax * ql.y - ay * ql.z - az * ql.w;
+      q4.y = aw * ql.y + ax * ql.x + ay * ql.w - az * ql.z;
+      q4.z = aw * ql.z - ax * ql.w + ay * ql.x + az * ql.y;
+      q4.w = aw * ql.w + ax * ql.z - ay * ql.y + az * ql.x;
+      actor_ok = qn > 0.0 && isfinite(qn);
+    } else {
+      actor_ok = a == -1;
+    }
+  }
 
   // ---- depth key (A19): exact float32 op sequence
   {
@@ -452,7 +484,7 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
   bool ok = true;
 
   const float qn2 = q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w;
-  ok = qn2 > 0.f && isfinite(qn2);
+  ok = actor_ok && qn2 > 0.f && isfinite(qn2);
 #pragma unroll
   for (int c = 0; c < 3; ++c) ok = ok && sc[c] > 0.f && isfinite(sc[c]) && isfinite(mu[c]);
   if (ok) {
@@ -691,6 +723,12 @@ static void depth_origin(const simuli_pose& a, const simuli_pose& b, float out[3
   }
 }
 
+template <int KIND, bool DIV, bool ACT>
+void launch_project(const ProjArgs& A, unsigned blocks, int threads, cudaStream_t st) {
+  cudaFuncSetAttribute(k_project<KIND, DIV, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
+  k_project<KIND, DIV, ACT><<<blocks, threads, kShSmem, st>>>(A);
+}
+
 }  // namespace simuli
 
 extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_project_params* P, simuli_projected* out,
@@ -716,6 +754,14 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
   A.means = G->means; A.quats = G->quats; A.scales = G->scales; A.opacity = G->opacity; A.sh = G->sh;
   A.sh_degree = G->sh_degree;
   A.n_coef = (G->sh_degree + 1) * (G->sh_degree + 1);
+  const bool act = G->actor_id != nullptr;
+  if (act) {
+    SIMULI_REQUIRE(G->n_actors >= 1 && G->actor_pose, "simuli_project: actor_id needs n_actors >= 1 and actor_pose");
+    static_assert(sizeof(simuli_pose) == 7 * sizeof(float), "simuli_pose must be 7 packed floats");
+    A.actor_id = G->actor_id;
+    A.actor_pose = reinterpret_cast<const float*>(G->actor_pose);
+    A.n_actors = G->n_actors;
+  }
   A.pose = make_pose_interp_f(make_pose_interp_d(P->pose_start, P->pose_end));
   A.K = P->rs_iterations;
   SIMULI_REQUIRE(ut_weights(P->ut_alpha, P->ut_beta, P->ut_kappa, &A.ut.spread, &A.ut.wm0, &A.ut.wmi, &A.ut.wc0,
@@ -773,11 +819,11 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f; A.az_tile_scale = T.az_tile_scale; A.az_cell_scale = T.az_cell_scale;
     A.bounds = T.elev_bounds; A.row_scale = T.cull_row_scale; A.sat = T.sat;
     if (A.beam_div > 0.f) {
-      cudaFuncSetAttribute(k_project<SIMULI_SENSOR_LIDAR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
-      k_project<SIMULI_SENSOR_LIDAR, true><<<blocks, threads, kShSmem, st>>>(A);
+      if (act) launch_project<SIMULI_SENSOR_LIDAR, true, true>(A, blocks, threads, st);
+      else launch_project<SIMULI_SENSOR_LIDAR, true, false>(A, blocks, threads, st);
     } else {
-      cudaFuncSetAttribute(k_project<SIMULI_SENSOR_LIDAR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
-      k_project<SIMULI_SENSOR_LIDAR, false><<<blocks, threads, kShSmem, st>>>(A);
+      if (act) launch_project<SIMULI_SENSOR_LIDAR, false, true>(A, blocks, threads, st);
+      else launch_project<SIMULI_SENSOR_LIDAR, false, false>(A, blocks, threads, st);
     }
   } else if (P->kind == SIMULI_SENSOR_CAMERA) {
     SIMULI_REQUIRE(P->camera, "camera projection needs camera");
@@ -791,8 +837,8 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.fx = C.fx; A.fy = C.fy; A.cx = C.cx; A.cy = C.cy;
     for (int i = 0; i < 5; ++i) A.k[i] = C.k[i];
     A.near_m = C.near_m; A.max_theta = C.max_theta_rad; A.inv_tile = 1.0f / (float)C.tile_px;
-    cudaFuncSetAttribute(k_project<SIMULI_SENSOR_CAMERA, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
-    k_project<SIMULI_SENSOR_CAMERA, false><<<blocks, threads, kShSmem, st>>>(A);
+    if (act) launch_project<SIMULI_SENSOR_CAMERA, false, true>(A, blocks, threads, st);
+    else launch_project<SIMULI_SENSOR_CAMERA, false, false>(A, blocks, threads, st);
   } else {
     set_error("simuli_project: unknown sensor kind %d", P->kind);
     return SIMULI_ERR_INVALID_ARGUMENT;

@@ -848,7 +848,7 @@ __global__ void __launch_bounds__(256) k_compose_camera(const ComposeArgs A) {
   const float om = __ldg(A.opacity + p);
   float cin[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) cin[c] = om * __ldg(A.rgb_fg + 3 * p + c) + (1.f - om) * cb[c];
+  for (int c = 0; c < 3; ++c) cin[c] = __ldg(A.rgb_fg + 3 * p + c) + (1.f - om) * cb[c];
   float out[3] = {cin[0], cin[1], cin[2]};
   if (A.grid) {
     const float lum = fminf(1.f, fmaxf(0.f, 0.299f * cin[0] + 0.587f * cin[1] + 0.114f * cin[2]));

@@ -81,7 +81,8 @@ class TilingDev(C.Structure):
 
 class Gaussians(C.Structure):
     _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("quats", C.c_void_p), ("scales", C.c_void_p),
-                ("opacity", C.c_void_p), ("sh", C.c_void_p), ("sh_degree", C.c_int32)]
+                ("opacity", C.c_void_p), ("sh", C.c_void_p), ("sh_degree", C.c_int32),
+                ("actor_id", C.c_void_p), ("actor_pose", C.c_void_p), ("n_actors", C.c_int32)]
 
 
 class CameraCompose(C.Structure):
@@ -255,10 +256,15 @@ def simuli_render_camera(proj, sorted_ids, tile_ranges, params, rparams, out: Ca
 
 # ------------------------------------------------------------------------------ helpers
 def to_device_scene(scene: dict, device="cuda"):
-    """Upload a synth scene (float32 numpy) to device tensors."""
+    """Upload a synth scene (float32 numpy) to device tensors; optional scene-graph keys
+    actor_id [n] int32 and actor_pose [n_actors, 7] float32 (q w,x,y,z, t) (A29)."""
     import torch
-    return {k: torch.from_numpy(np.ascontiguousarray(scene[k], np.float32)).to(device)
-            for k in ("means", "quats", "scales", "opacity", "sh")}
+    out = {k: torch.from_numpy(np.ascontiguousarray(scene[k], np.float32)).to(device)
+           for k in ("means", "quats", "scales", "opacity", "sh")}
+    if scene.get("actor_id") is not None:
+        out["actor_id"] = torch.from_numpy(np.ascontiguousarray(scene["actor_id"], np.int32)).to(device)
+        out["actor_pose"] = torch.from_numpy(np.ascontiguousarray(scene["actor_pose"], np.float32)).to(device)
+    return out
 
 
 def gaussians_struct(scene_dev) -> Gaussians:
@@ -266,8 +272,11 @@ def gaussians_struct(scene_dev) -> Gaussians:
     sh = scene_dev["sh"]
     ncoef = sh.numel() // max(n, 1) // 3 if n else 16
     deg = {1: 0, 4: 1, 9: 2, 16: 3}[ncoef]
+    act = scene_dev.get("actor_id")
     return Gaussians(n, _ptr(scene_dev["means"]), _ptr(scene_dev["quats"]), _ptr(scene_dev["scales"]),
-                     _ptr(scene_dev["opacity"]), _ptr(sh), deg)
+                     _ptr(scene_dev["opacity"]), _ptr(sh), deg, _ptr(act),
+                     _ptr(scene_dev["actor_pose"] if act is not None else None),
+                     int(scene_dev["actor_pose"].shape[0]) if act is not None else 0)
 
 
 class _Frame:

@@ -379,3 +379,54 @@ def batch_poses(n_scans: int, x_lo: float = -51.0, step: float = 0.2, motion: fl
         yaw0 = 0.01 * ((i % 2) * 2 - 1)
         out.append((pose(yaw_quat(yaw0), [x, 0.0, z]), pose(yaw_quat(yaw0 + yaw_rate), [x + motion, 0.0, z])))
     return out
+
+
+def with_actors(scene: dict, seed: int, n_actors: int = 8, per_actor: int = 1500, x_range=(5.0, 40.0),
+                kind: str = "lidar", yaw_only: bool = False) -> dict:
+    """Scene graph input (A29): appends n_actors dynamic objects (car-sized shells
+    of per_actor particles each, generated directly in the object's local frame: x forward,
+    z up, origin at the box's ground centre) plus their object -> world poses at t (on the
+    road at |y| in [3, 9], random yaw, small roll / pitch unless yaw_only).  The static
+    scene's particles get actor_id -1.  Returns a new dict with 'actor_id' [n] int32 and
+    'actor_pose' [n_actors, 7] float32 (q w,x,y,z, t).  No method arithmetic: the local
+    particles and the poses are drawn independently."""
+    rng = np.random.default_rng(seed)
+    m = n_actors * per_actor
+    face = rng.integers(0, 5, m)
+    u, v = rng.uniform(-0.5, 0.5, m), rng.uniform(-0.5, 0.5, m)
+    lx, ly, lz = 4.5, 1.9, 1.6
+    px = np.where(face == 0, 0.5 * lx, np.where(face == 1, -0.5 * lx, u * lx))
+    py = np.where(face == 2, 0.5 * ly, np.where(face == 3, -0.5 * ly, np.where(face < 2, u * ly, v * ly)))
+    pz = np.where(face == 4, lz, (v + 0.5) * lz)
+    means = np.stack([px, py, pz], 1)
+    quats = _random_quats(rng, m)
+    scales = np.concatenate([_logu(rng, 0.03, 0.10, (m, 2)), _logu(rng, 0.01, 0.02, (m, 1))], 1)
+    if kind == "lidar":
+        hi = rng.uniform(size=m) < 0.85
+        opac = np.where(hi, rng.uniform(0.9, 0.99, m), rng.uniform(0.01, 0.2, m))
+        sh = _sh_lidar(rng, m)
+    else:
+        opac = rng.uniform(0.05, 0.99, m)
+        sh = _sh_camera(rng, m)
+    ids = np.repeat(np.arange(n_actors, dtype=np.int32), per_actor)
+    yaw = rng.uniform(-math.pi, math.pi, n_actors)
+    tilt = np.zeros((n_actors, 2)) if yaw_only else rng.normal(0.0, 0.03, (n_actors, 2))
+    poses = np.zeros((n_actors, 7), np.float64)
+    for a in range(n_actors):  # q = q_z(yaw) q_y(pitch) q_x(roll), composed by hand
+        cz, sz = math.cos(yaw[a] / 2), math.sin(yaw[a] / 2)
+        cy, sy = math.cos(tilt[a, 1] / 2), math.sin(tilt[a, 1] / 2)
+        cx, sx = math.cos(tilt[a, 0] / 2), math.sin(tilt[a, 0] / 2)
+        poses[a, :4] = (cz * cy * cx + sz * sy * sx, cz * cy * sx - sz * sy * cx,
+                        cz * sy * cx + sz * cy * sx, sz * cy * cx - cz * sy * sx)
+    poses[:, 4] = rng.uniform(*x_range, n_actors)
+    poses[:, 5] = rng.uniform(3.0, 9.0, n_actors) * np.where(rng.uniform(size=n_actors) < 0.5, -1, 1)
+    poses[:, 6] = rng.uniform(-0.05, 0.05, n_actors)
+    n0 = scene["means"].shape[0]
+    out = {k: np.concatenate([scene[k], v.astype(np.float32).reshape((-1,) + scene[k].shape[1:])])
+           for k, v in (("means", means), ("quats", quats), ("scales", scales), ("opacity", opac), ("sh", sh))}
+    out["actor_id"] = np.concatenate([np.full(n0, -1, np.int32), ids])
+    out["actor_pose"] = poses.astype(np.float32)
+    perm = rng.permutation(n0 + m)  # unordered set (P:73)
+    for k in ("means", "quats", "scales", "opacity", "sh", "actor_id"):
+        out[k] = np.ascontiguousarray(out[k][perm])
+    return out

@@ -619,3 +619,56 @@ def test_compose_camera_parity(SM, oracle_mod, name):
         assert err < 2e-5
         if e is None:
             assert np.abs(got - ref).max() < 2e-5  # invalid pixels: no background term at all
+
+
+# ------------------------------------------------------------------ scene graph (A29)
+def test_actor_scene_lidar_parity(SM, oracle_mod):
+    """Dynamic objects in local frames + poses at t: the GPU projection maps them to world
+    (A29) -- depth keys bit-exact against the oracle's world means (O0), boxes / M / f
+    within the tier-1 tolerances, lists bit-exact, and the whole scan within tier 2."""
+    O = oracle_mod
+    cfg = S.lidar_config("B")
+    scene = S.with_actors(S.corridor_scene(41, 60_000, x_range=(-60.0, 60.0)), 42, n_actors=12, per_actor=2000,
+                          x_range=(-40.0, 40.0))
+    scene["actor_id"][:5] = [12, -3, 99, 12, 1000]  # out of range -> invalid
+    r = lidar_run(SM, cfg, scene, write_all_records=True)
+    rec = r.record.cpu().numpy()
+    proj = O.project_lidar(scene, cfg)
+    gv, ov, amb = np.isfinite(rec[:, 16]), proj["valid"] != 0, proj["ambiguous"] != 0
+    assert not gv[:5].any() and not ov[:5].any()
+    assert np.array_equal(gv[~amb], ov[~amb])
+    assert np.array_equal(r.depth_key.cpu().numpy().view(np.uint32), proj["key"].view(np.uint32))
+    both = gv & ov & ~amb
+    world = O.actors_to_world(scene)
+    assert np.array_equal(rec[both, 0:3], world["means"][both])  # record mu = the world mean
+    db = np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both].astype(np.float64))
+    assert db[:, :2].max() < LIDAR_EPS["a"] and db[:, 2:].max() < LIDAR_EPS["b"], db.max(0)
+    Mref = proj["Mrows"][both]
+    assert (np.abs(rec[both, 3:12] - Mref) / np.abs(Mref).max(1, keepdims=True)).max() < 2e-6
+    moving = both & (scene["actor_id"] >= 0)
+    assert moving.sum() > 1000
+    t = O.Tiling(cfg)
+    ref = O.render_lidar(scene, cfg, tiling=t, flag_eps=LIDAR_EPS)
+    ok = ref["flag"] == 0
+    assert ok.mean() > 1 - FLAG_BUDGET["default"], ok.mean()
+    compare_lidar(r.out, ref, ok)
+
+
+def test_actor_scene_camera_parity(SM, oracle_mod):
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    scene = S.with_actors(S.corridor_scene(43, 30_000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6)), 44,
+                          n_actors=6, per_actor=1500, kind="camera")
+    c = camera_run(SM, cam, scene, write_all_records=True)
+    rec = c.record.cpu().numpy()
+    proj = O.project_camera(scene, cam)
+    gv, ov, amb = np.isfinite(rec[:, 16]), proj["valid"] != 0, proj["ambiguous"] != 0
+    assert np.array_equal(gv[~amb], ov[~amb])
+    both = gv & ov
+    assert np.abs(rec[both, 16:20].astype(np.float64) - proj["box"][both]).max() < CAMERA_EPS["a"]
+    ref2 = O.render_camera(scene, cam, flag_eps=CAMERA_EPS)
+    ok2 = ref2["flag"] == 0
+    assert ok2.mean() > 0.995, ok2.mean()
+    assert np.abs(c.out["rgb"].cpu().numpy() - ref2["feat"])[ok2].max() < TOL_FEAT
+    seen = np.unique(scene["actor_id"][both & (scene["actor_id"] >= 0)])
+    assert len(seen) >= 3

@@ -783,8 +783,9 @@ def _dirs(lon, colat):
 
 
 def test_compose_identity_and_constant_background(oracle_mod):
-    """Eq. 2 with A = identity: c = omega c_f + (1 - omega) c_b; a constant environment gives
-    c_b = that constant for every direction; no map, no grid: c = omega c_f."""
+    """Eq. 2 with A = identity: c = omega c_f + (1 - omega) c_b, where omega c_f is the
+    renderer's Eq. 1 sum (A28); a constant environment gives c_b = that constant for every
+    direction; no map, no grid: c = the Eq. 1 sum."""
     O = oracle_mod
     cam = S.camera_config("D-small")
     rng = np.random.default_rng(41)
@@ -797,8 +798,8 @@ def test_compose_identity_and_constant_background(oracle_mod):
     ident = np.zeros((3, 4, 5, 12), np.float32)
     ident[..., 0] = ident[..., 5] = ident[..., 10] = 1.0
     out = O.compose_camera(cam, od, cf, om, env, ident)
-    assert np.allclose(out, om[:, None] * cf + (1 - om[:, None]) * k.astype(np.float64), atol=1e-6)
-    assert np.allclose(O.compose_camera(cam, od, cf, om), om[:, None] * cf, atol=1e-15)
+    assert np.allclose(out, cf + (1 - om[:, None]) * k.astype(np.float64), atol=1e-6)
+    assert np.allclose(O.compose_camera(cam, od, cf, om), cf, atol=1e-15)
 
 
 def test_compose_env_bilinear(oracle_mod):
@@ -851,3 +852,63 @@ def test_compose_grid_trilinear_exact_for_affine_fields(oracle_mod):
     ref = np.einsum("nij,nj->ni", M[:, :, :3], cf) + M[:, :, 3]
     assert inside.mean() > 0.3
     assert np.abs(out - ref)[inside].max() < 1e-6  # (grid stored as float32)
+
+
+# ------------------------------------------------------------------ scene graph (O0)
+def test_actors_to_world_vs_scipy(oracle_mod):
+    """O0: mu_w = R_a mu + t_a (scipy Rotation, double) rounded to float32 (<= 1 ulp);
+    Sigma_w = R_a Sigma R_a^T (scipy); static particles bit-unchanged; an out-of-range id
+    gives a zero quaternion (invalid particle)."""
+    O = oracle_mod
+    base = S.corridor_scene(5, 300, x_range=(0.0, 40.0))
+    sc = S.with_actors(base, 6, n_actors=5, per_actor=60)
+    sc["actor_id"][:3] = [7, -2, 5]  # out of range
+    w = O.actors_to_world(sc)
+    ids = sc["actor_id"]
+    st = ids == -1
+    assert np.array_equal(w["means"][st].view(np.uint32), sc["means"][st].view(np.uint32))
+    assert np.array_equal(w["quats"][st].view(np.uint32), sc["quats"][st].view(np.uint32))
+    assert np.all(w["quats"][:3] == 0)
+    P = sc["actor_pose"].astype(np.float64)
+    for i in np.nonzero((ids >= 0) & (ids < 5))[0]:
+        Ra = Rotation.from_quat(P[ids[i], [1, 2, 3, 0]]).as_matrix()
+        ref = Ra @ sc["means"][i].astype(np.float64) + P[ids[i], 4:]
+        assert np.all(np.abs(w["means"][i] - ref) <= np.spacing(np.abs(ref).astype(np.float32)))
+        ql = sc["quats"][i].astype(np.float64)
+        Rl = Rotation.from_quat(ql[[1, 2, 3, 0]]).as_matrix()
+        Sl = Rl @ np.diag(sc["scales"][i].astype(np.float64) ** 2) @ Rl.T
+        Sw = O.covariance(w["quats"][i].astype(np.float64), sc["scales"][i].astype(np.float64))
+        assert np.allclose(Sw, Ra @ Sl @ Ra.T, rtol=0, atol=1e-6 * np.abs(Sl).max())
+    pr = O.project_lidar(sc, S.lidar_config("A"))
+    assert np.all(pr["valid"][:3] == 0)
+
+
+def test_actor_rigid_invariance_lidar(oracle_mod):
+    """Moving the whole scene as one object by P and the sensor by P too (sensor pose
+    P o X) leaves the scan unchanged (rigid invariance of Eq. 3 / the response); compared
+    with the local scene scanned from X.  Differences come only from rounding the world
+    means to float32 and from rays near a decision threshold (flagged)."""
+    O = oracle_mod
+    cfg = S.lidar_config("tiny")
+    scene = S.scene_for("tiny", seed=31, n=300)
+    qP = np.array([np.cos(0.35), 0.05, -0.03, np.sin(0.35)])
+    qP /= np.linalg.norm(qP)
+    tP = np.array([12.0, -4.0, 0.5])
+    sc = dict(scene)
+    sc["actor_id"] = np.zeros(scene["means"].shape[0], np.int32)
+    sc["actor_pose"] = np.concatenate([qP, tP])[None].astype(np.float32)
+    P32 = sc["actor_pose"][0].astype(np.float64)
+    RP = Rotation.from_quat(P32[[1, 2, 3, 0]])
+    def moved(X):  # P o X
+        RX = Rotation.from_quat(np.asarray(X["q"], np.float64)[[1, 2, 3, 0]])
+        return S.pose((RP * RX).as_quat()[[3, 0, 1, 2]], RP.apply(np.asarray(X["t"], np.float64)) + P32[4:])
+
+    LIDAR_EPS_PIN = {"a": 3e-6, "b": 3e-6, "alpha": 1e-5, "T_rel": 1e-3, "tau": 1e-3, "impact": 5e-5}
+    ref = O.render_lidar(scene, cfg, flag_eps=LIDAR_EPS_PIN)
+    got = O.render_lidar(sc, cfg, pose0=moved(cfg.pose_start), pose1=moved(cfg.pose_end), flag_eps=LIDAR_EPS_PIN)
+    ok = (ref["flag"] == 0) & (got["flag"] == 0)
+    assert ok.mean() > 0.97
+    assert (ref["opacity"] > 0.1).mean() > 0.05
+    assert np.abs(got["opacity"] - ref["opacity"])[ok].max() < 2e-5
+    hit = ok & (ref["opacity"] > 0.5)
+    assert np.abs(got["depth"] - ref["depth"])[hit].max() < 1e-4
