@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 4
+#define SIMULI_ABI_VERSION 5
 
 enum {
   SIMULI_OK = 0,
@@ -265,9 +265,15 @@ int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles
 
 /* Compositing thresholds (A13, A14): skip alpha < alpha_min (default 1/255), clamp alpha
  * to alpha_max (0.99), stop a ray when T (1 - alpha) < T_min (1e-4) without compositing
- * that particle. */
+ * that particle.
+ * Features: sh == NULL -> each particle's record features f (SH evaluated once per particle
+ * at its view direction, A17); sh != NULL -> Eq. 1 literally (A30): SH_i(d)
+ * evaluated per (ray, particle) at the ray's unit direction d from sh (device, the
+ * particle set's [n][(sh_degree+1)^2][3] coefficients, indexed by the sorted ids). */
 typedef struct {
   float alpha_min, alpha_max, T_min;
+  const float* sh;
+  int32_t sh_degree;
 } simuli_render_params;
 
 /* Per-ray LiDAR outputs (device, [n_rays] each; any pointer may be NULL to skip it).

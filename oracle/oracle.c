@@ -1182,7 +1182,16 @@ int or_composite(int64_t n_gauss, const double* mu, const double* Mrows, const d
         double Tn = T * (1.0 - alpha);
         if (p->flag_mode && fabs(Tn - p->T_min) < p->eps_T_rel * p->T_min) flag |= 4;
         if (Tn < p->T_min) break;
-        for (int c = 0; c < 3; ++c) acc[c] += alpha * T * feat[(int64_t)g * 3 + c];
+        double f[3] = {feat[(int64_t)g * 3], feat[(int64_t)g * 3 + 1], feat[(int64_t)g * 3 + 2]};
+        if (p->sh) { /* Eq. 1 literally: SH_i(d), d the ray's unit direction (A30) */
+          const int nco = (p->sh_degree + 1) * (p->sh_degree + 1);
+          double shd[48], dn[3];
+          const double dl = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+          for (int c = 0; c < 3; ++c) dn[c] = d[c] / dl;
+          for (int k = 0; k < nco * 3; ++k) shd[k] = p->sh[(int64_t)g * nco * 3 + k];
+          or_sh_eval(shd, p->sh_degree, dn, f);
+        }
+        for (int c = 0; c < 3; ++c) acc[c] += alpha * T * f[c];
         D += alpha * T * tau;
         w += alpha * T;
         nc++;

@@ -134,6 +134,9 @@ typedef struct {
   double eps_alpha, eps_T_rel, eps_tau;
   double eps_impact;         /* box-edge flags only when alpha*T of the particle > this  */
   double eps_amb_a, eps_amb_b; /* margins around validity-ambiguous particles' boxes       */
+  const float* sh;           /* NULL: per-particle features feat (A17); else literal Eq. 1:
+                                SH_i(d) per (ray, particle) at the ray direction (A30)   */
+  int32_t sh_degree;
 } or_render_params;
 
 typedef struct {

@@ -74,7 +74,8 @@ class OrRenderParams(C.Structure):
                 ("T_min", C.c_double), ("wrap", C.c_int32), ("pi_f", C.c_float), ("two_pi_f", C.c_float),
                 ("flag_mode", C.c_int32), ("eps_a", C.c_double), ("eps_b", C.c_double),
                 ("eps_alpha", C.c_double), ("eps_T_rel", C.c_double), ("eps_tau", C.c_double),
-                ("eps_impact", C.c_double), ("eps_amb_a", C.c_double), ("eps_amb_b", C.c_double)]
+                ("eps_impact", C.c_double), ("eps_amb_a", C.c_double), ("eps_amb_b", C.c_double),
+                ("sh", C.c_void_p), ("sh_degree", C.c_int32)]
 
 
 class OrRenderOut(C.Structure):
@@ -381,6 +382,11 @@ def composite(records, ids, ranges, ray_tile, ray_a, ray_b, ray_od, *, wrap, nea
                          fe.get("a", 0.0), fe.get("b", 0.0), fe.get("alpha", 0.0), fe.get("T_rel", 0.0),
                          fe.get("tau", 0.0), fe.get("impact", 0.0), fe.get("amb_a", AMBIGUOUS_MARGIN[0]),
                          fe.get("amb_b", AMBIGUOUS_MARGIN[1]))
+    sh = records.get("sh")  # per-ray SH (literal Eq. 1, A30)
+    if sh is not None:
+        sh = np.ascontiguousarray(sh, np.float32).reshape(mu.shape[0], -1)
+        prm.sh = sh.ctypes.data
+        prm.sh_degree = {3: 0, 12: 1, 27: 2, 48: 3}[sh.shape[1]]
     out = {"feat": np.zeros((R, 3)), "opacity": np.zeros(R), "depth_accum": np.zeros(R), "depth": np.zeros(R),
            "T_final": np.zeros(R), "n_contrib": np.zeros(R, np.int32), "flag": np.zeros(R, np.int32),
            "scanned": np.zeros(R, np.int64), "inbox": np.zeros(R, np.int64)}
@@ -429,16 +435,18 @@ def expand_box(box, ea, eb):
 
 def render_lidar(scene, cfg, tiling: Tiling | None = None, pose0=None, pose1=None, mode="tiled", enable_cull=True,
                  flag_eps=None, alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4, ut=None, K=None,
-                 ray_od=None, proj=None):
+                 ray_od=None, proj=None, per_ray_sh=False):
     """Full oracle LiDAR scan (O1-O13).  mode='tiled' (O7-O12) or 'brute' (O13).  With
     flag_eps, lists come from boxes grown by the margins and rays near a threshold are
-    flagged (A23)."""
+    flagged (A23).  per_ray_sh: features SH_i(d) at each ray's direction (Eq. 1, A30)."""
     tiling = tiling or Tiling(cfg)
     pose0 = pose0 or cfg.pose_start
     pose1 = pose1 or cfg.pose_end
     if proj is None:
         proj = project_lidar(scene, cfg, pose0, pose1, K=K, ut=ut)
     rec = records_from_projection(proj, scene)
+    if per_ray_sh:
+        rec["sh"] = scene["sh"]
     valid = proj["valid"]
     gamb = None
     if flag_eps is not None:
@@ -471,12 +479,14 @@ def render_lidar(scene, cfg, tiling: Tiling | None = None, pose0=None, pose1=Non
 
 
 def render_camera(scene, cam, pose0=None, pose1=None, mode="tiled", flag_eps=None, alpha_min=1.0 / 255.0,
-                  alpha_max=0.99, T_min=1e-4, ut=None, K=None, rays=None, proj=None):
+                  alpha_max=0.99, T_min=1e-4, ut=None, K=None, rays=None, proj=None, per_ray_sh=False):
     pose0 = pose0 or cam.pose_start
     pose1 = pose1 or cam.pose_end
     if proj is None:
         proj = project_camera(scene, cam, pose0, pose1, K=K, ut=ut)
     rec = records_from_projection(proj, scene)
+    if per_ray_sh:
+        rec["sh"] = scene["sh"]
     valid = proj["valid"]
     gamb = None
     if flag_eps is not None:

@@ -196,6 +196,28 @@ __device__ __forceinline__ void sh_basis3(float x, float y, float z, float b[16]
   b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
 }
 
+// Eq. 1 literally (A30): one particle's SH features at a ray direction whose
+// basis b (sh_basis3) the caller computed once per ray; ncoef = (degree + 1)^2 coefficients
+// [ncoef][3], summed in coefficient order.  Degree 3 reads the 192-byte block as 12 float4.
+__device__ __forceinline__ void sh_dot(const float* __restrict__ sh, int ncoef, const float b[16], float f[3]) {
+  float acc[3] = {0.f, 0.f, 0.f};
+  if (ncoef == 16) {
+    const float4* s4 = reinterpret_cast<const float4*>(sh);
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      const float4 v4 = __ldg(s4 + c);
+      const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[(4 * c + j) % 3] = fmaf(b[(4 * c + j) / 3], v[j], acc[(4 * c + j) % 3]);
+    }
+  } else {
+    for (int k = 0; k < ncoef; ++k)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c] = fmaf(b[k], __ldg(sh + 3 * k + c), acc[c]);
+  }
+  f[0] = acc[0]; f[1] = acc[1]; f[2] = acc[2];
+}
+
 // Ray in double, split into float hi + lo parts for the compensated response.
 struct RayF {
   float o_hi[3], o_lo[3], d_hi[3], d_lo[3];

@@ -55,6 +55,8 @@ struct CameraArgs {
   int* n_contrib;
   double* ray_od;
   int *n_visited, *n_inbox;
+  const float* sh;  // per-ray SH (A30) or NULL
+  int sh_ncoef;
 };
 
 // inverse lens model in double (A22): KB by Newton on theta_d(theta) = r_d, radtan by
@@ -110,11 +112,12 @@ __device__ bool unproject(const CameraArgs& A, double u, double v, double dir[3]
 // One CTA per (tile, band of TP / SPLIT pixel rows): the bands of a tile read the same list,
 // so a long list (near-field particles covering many pixels) is spread over SPLIT CTAs
 // instead of one; items are scheduled longest list first (tile_order).
-template <int TP, int SPLIT>
+template <int TP, int SPLIT, bool PRAY>
 __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraArgs A) {
   constexpr int NTH = TP * TP / SPLIT;  // threads = pixels of the band
   constexpr int NT = 128;               // list entries staged per batch
   __shared__ float4 s_rec[NT][5];
+  __shared__ uint32_t s_id[PRAY ? NT : 1];  // particle ids of the batch (per-ray SH)
   const int tid = threadIdx.x;
   const int slot = (int)(blockIdx.x / SPLIT), band = (int)(blockIdx.x % SPLIT);
   const int tile = A.order ? __ldg(A.order + slot) : slot;
@@ -135,6 +138,8 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
   }
   RayF rf;
   split_ray(o, d, rf);
+  float shb[16];
+  if (PRAY) sh_basis3((float)d[0], (float)d[1], (float)d[2], shb);
   float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
   int nc = 0, nv = 0, ni = 0, term_at = -1;
   bool done = !(inside && valid);
@@ -147,6 +152,7 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
       const float4* src = A.record + (size_t)g * 5;
 #pragma unroll
       for (int c = 0; c < 5; ++c) s_rec[e][c] = __ldg(src + c);
+      if (PRAY) s_id[e] = g;
     }
     __syncthreads();
     // warp-level pre-cull: the warp's pixels form a strip of 32 / TP rows x TP columns; an
@@ -187,9 +193,11 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
             continue;
           }
           const float w = alpha * T;
-          acc0 = fmaf(w, r3.y, acc0);
-          acc1 = fmaf(w, r3.z, acc1);
-          acc2 = fmaf(w, r3.w, acc2);
+          float f[3] = {r3.y, r3.z, r3.w};
+          if (PRAY) sh_dot(A.sh + (size_t)s_id[jj] * A.sh_ncoef * 3, A.sh_ncoef, shb, f);
+          acc0 = fmaf(w, f[0], acc0);
+          acc1 = fmaf(w, f[1], acc1);
+          acc2 = fmaf(w, f[2], acc2);
           D = fmaf(w, tau, D);
           W += w;
           ++nc;
@@ -239,6 +247,8 @@ struct LidarArgs {
   int* n_contrib;
   double* ray_od;
   int *n_visited, *n_inbox;
+  const float* sh;  // per-ray SH (A30) or NULL
+  int sh_ncoef;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -275,6 +285,7 @@ struct LidarSmem {
   float2 at[SLOTB][32][32 * NP + 1];   // (alpha, tau) of member pairs, per slot buffer
   uint8_t ent[SLOTB][32][32 * NP + 4]; // entry index within the round
   float4 feat[SLOTB][32 * NP];     // (sigma, features) of the round's entries
+  uint32_t pid[SLOTB][32 * NP];    // particle ids of the round's entries (per-ray SH)
   uint32_t memb[SLOTB][NP][32];    // [warp][ray] member entries of the warp's 32
   int rowoff[NP][32];              // members of ray r in warps before w (current round)
   uint16_t plist[NP][1024];        // the warp's member pairs (entry << 5 | ray)
@@ -316,7 +327,7 @@ constexpr int kLidarNP = 4, kLidarStages = 2, kLidarSlotBuffers = 1;
 // SLOTB = 2: double-buffered slots, producers up to two rounds ahead of the consumer;
 // SLOTB = 1: one slot buffer (less shared memory, more CTAs per SM), producers wait for the
 // consumer's previous round after their box tests, before writing the slots.
-template <int NP, int STAGES, int SLOTB>
+template <int NP, int STAGES, int SLOTB, bool PRAY>
 __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarArgs A) {
   constexpr int E = 32 * NP;
   constexpr int NT = 32 * (NP + 1);
@@ -383,6 +394,8 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
     }
     __threadfence_block();
     named_arrive(BAR_RAYS, NT);
+    float shb[16];
+    if (PRAY) sh_basis3((float)dd[0], (float)dd[1], (float)dd[2], shb);
     float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
     int ncontrib = 0, nv = 0, ni = 0;
     bool done = lane >= R;
@@ -428,9 +441,11 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
               break;
             }
             const float w = a.x * T;
-            acc0 = fmaf(w, f.y, acc0);
-            acc1 = fmaf(w, f.z, acc1);
-            acc2 = fmaf(w, f.w, acc2);
+            float fv[3] = {f.y, f.z, f.w};
+            if (PRAY) sh_dot(A.sh + (size_t)S.pid[sb][e] * A.sh_ncoef * 3, A.sh_ncoef, shb, fv);
+            acc0 = fmaf(w, fv[0], acc0);
+            acc1 = fmaf(w, fv[1], acc1);
+            acc2 = fmaf(w, fv[2], acc2);
             D = fmaf(w, a.y, D);
             W += w;
             ++ncontrib;
@@ -594,7 +609,10 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
       alive = ~S.done_mask[b ^ 1];
     }
     if (warp == 0) RMARK(r, 4);
-    if (valid) S.feat[sb][tid] = S.rec[st][tid][3];
+    if (valid) {
+      S.feat[sb][tid] = S.rec[st][tid][3];
+      if (PRAY) S.pid[sb][tid] = __ldg(A.ids + start + tid);
+    }
     m &= alive;  // no member pairs for terminated rays
     const uint32_t my = warp_transpose32(m, lane);  // lane r: entries of this warp holding ray r
     S.memb[sb][warp][lane] = my;
@@ -706,14 +724,27 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   A.zeta = out->zeta; A.opacity = out->opacity; A.depth_accum = out->depth_accum; A.depth = out->depth;
   A.intensity = out->intensity; A.raydrop = out->raydrop; A.final_T = out->final_T; A.n_contrib = out->n_contrib;
   A.ray_od = out->ray_od; A.n_visited = out->n_visited; A.n_inbox = out->n_inbox;
+  if (rp->sh) {
+    SIMULI_REQUIRE(rp->sh_degree >= 0 && rp->sh_degree <= 3, "simuli_render_lidar: sh_degree not in 0..3");
+    SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(rp->sh) % 16 == 0, "simuli_render_lidar: sh must be 16-byte aligned");
+    A.sh = rp->sh;
+    A.sh_ncoef = (rp->sh_degree + 1) * (rp->sh_degree + 1);
+  }
   if (A.n_items == 0) return SIMULI_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   auto launch = [&](auto np_tag, auto stages_tag, auto slot_tag) {
     constexpr int NP = decltype(np_tag)::value, STG = decltype(stages_tag)::value, SB = decltype(slot_tag)::value;
     constexpr size_t smem = sizeof(LidarSmem<NP, STG, SB>);
-    cudaFuncSetAttribute(k_render_lidar<NP, STG, SB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_render_lidar<NP, STG, SB><<<(unsigned)A.n_items, 32 * (NP + 1), smem, st>>>(A);
+    cudaFuncSetAttribute(k_render_lidar<NP, STG, SB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_render_lidar<NP, STG, SB, false><<<(unsigned)A.n_items, 32 * (NP + 1), smem, st>>>(A);
   };
+  if (A.sh) {  // per-ray SH (A30): the default pipeline shape only
+    constexpr size_t smem = sizeof(LidarSmem<kLidarNP, kLidarStages, kLidarSlotBuffers>);
+    auto kern = k_render_lidar<kLidarNP, kLidarStages, kLidarSlotBuffers, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)A.n_items, 32 * (kLidarNP + 1), smem, st>>>(A);
+    return launch_check("simuli_render_lidar");
+  }
   using std::integral_constant;
   static const int variant = [] {
     const char* v = getenv("SIMULI_LIDAR_VARIANT");  // tuning only
@@ -768,11 +799,24 @@ extern "C" int32_t simuli_render_camera(const simuli_projected* proj, const uint
   A.final_T = out->final_T; A.n_contrib = out->n_contrib; A.ray_od = out->ray_od;
   A.order = tile_order;
   A.n_visited = out->n_visited; A.n_inbox = out->n_inbox;
+  if (rp->sh) {
+    SIMULI_REQUIRE(rp->sh_degree >= 0 && rp->sh_degree <= 3, "simuli_render_camera: sh_degree not in 0..3");
+    SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(rp->sh) % 16 == 0, "simuli_render_camera: sh must be 16-byte aligned");
+    A.sh = rp->sh;
+    A.sh_ncoef = (rp->sh_degree + 1) * (rp->sh_degree + 1);
+  }
   const unsigned blocks = (unsigned)(A.Wt * Ht);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  switch (C.tile_px) {
-    case 8: k_render_camera<8, 1><<<blocks, 64, 0, st>>>(A); break;
-    default: k_render_camera<16, 4><<<blocks * 4, 64, 0, st>>>(A); break;
+  if (A.sh) {
+    switch (C.tile_px) {
+      case 8: k_render_camera<8, 1, true><<<blocks, 64, 0, st>>>(A); break;
+      default: k_render_camera<16, 4, true><<<blocks * 4, 64, 0, st>>>(A); break;
+    }
+  } else {
+    switch (C.tile_px) {
+      case 8: k_render_camera<8, 1, false><<<blocks, 64, 0, st>>>(A); break;
+      default: k_render_camera<16, 4, false><<<blocks * 4, 64, 0, st>>>(A); break;
+    }
   }
   return launch_check("simuli_render_camera");
 }

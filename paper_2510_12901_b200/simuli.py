@@ -111,7 +111,8 @@ class Projected(C.Structure):
 
 
 class RenderParams(C.Structure):
-    _fields_ = [("alpha_min", C.c_float), ("alpha_max", C.c_float), ("T_min", C.c_float)]
+    _fields_ = [("alpha_min", C.c_float), ("alpha_max", C.c_float), ("T_min", C.c_float), ("sh", C.c_void_p),
+                ("sh_degree", C.c_int32)]
 
 
 class LidarOut(C.Structure):
@@ -335,7 +336,7 @@ class LidarRenderer(_Frame):
     """One spinning LiDAR + one Gaussian set G_l resident on the device."""
 
     def __init__(self, cfg, scene_dev, capacity=None, device="cuda", enable_culling=True, write_all_records=False,
-                 ut=(1.0, 2.0, 0.0), extent_sigma=3.0, render_params=(1.0 / 255.0, 0.99, 1e-4)):
+                 ut=(1.0, 2.0, 0.0), extent_sigma=3.0, render_params=(1.0 / 255.0, 0.99, 1e-4), per_ray_sh=False):
         import torch
         self.device = device
         self.cfg = cfg
@@ -360,7 +361,10 @@ class LidarRenderer(_Frame):
         self.params = ProjectParams(SENSOR_LIDAR, C.pointer(self.lidar), C.pointer(self.tiling_dev), None,
                                     make_pose(cfg.pose_start), make_pose(cfg.pose_end), int(cfg.rs_iterations),
                                     ut[0], ut[1], ut[2], extent_sigma, int(enable_culling), int(write_all_records))
-        self.rparams = RenderParams(*render_params)
+        self.rparams = RenderParams(*render_params, None, 0)
+        if per_ray_sh:  # Eq. 1 literally: SH_i(d) per (ray, particle) (A30)
+            self.rparams.sh = scene_dev["sh"].data_ptr()
+            self.rparams.sh_degree = self.gauss.sh_degree
         self.n_tiles = th["n_tiles"]
         self.n_cols_total = th["n_theta"]
         self.n_rays = th["n_rays"]
@@ -408,7 +412,7 @@ class CameraRenderer(_Frame):
     """One distorted rolling-shutter camera + one Gaussian set G_c resident on the device."""
 
     def __init__(self, cam, scene_dev, capacity=None, device="cuda", write_all_records=False, ut=(1.0, 2.0, 0.0),
-                 extent_sigma=3.0, render_params=(1.0 / 255.0, 0.99, 1e-4)):
+                 extent_sigma=3.0, render_params=(1.0 / 255.0, 0.99, 1e-4), per_ray_sh=False):
         import torch
         self.device = device
         self.cam_cfg = cam
@@ -420,7 +424,10 @@ class CameraRenderer(_Frame):
         self.params = ProjectParams(SENSOR_CAMERA, None, None, C.pointer(self.camera), make_pose(cam.pose_start),
                                     make_pose(cam.pose_end), int(cam.rs_iterations), ut[0], ut[1], ut[2],
                                     extent_sigma, 0, int(write_all_records))
-        self.rparams = RenderParams(*render_params)
+        self.rparams = RenderParams(*render_params, None, 0)
+        if per_ray_sh:  # Eq. 1 literally: SH_i(d) per (ray, particle) (A30)
+            self.rparams.sh = scene_dev["sh"].data_ptr()
+            self.rparams.sh_degree = self.gauss.sh_degree
         tp = cam.tile_px
         self.Wt, self.Ht = (cam.width + tp - 1) // tp, (cam.height + tp - 1) // tp
         self.n_tiles = self.Wt * self.Ht

@@ -672,3 +672,35 @@ def test_actor_scene_camera_parity(SM, oracle_mod):
     assert np.abs(c.out["rgb"].cpu().numpy() - ref2["feat"])[ok2].max() < TOL_FEAT
     seen = np.unique(scene["actor_id"][both & (scene["actor_id"] >= 0)])
     assert len(seen) >= 3
+
+
+# ------------------------------------------------------------------ per-ray SH (Eq. 1 literally, A30)
+@pytest.mark.parametrize("config", ["A", "B-sub"])
+def test_per_ray_sh_lidar_parity(SM, oracle_mod, config):
+    O = oracle_mod
+    if config == "B-sub":
+        cfg, scene = S.lidar_config("B"), S.scene_for("B", n=200_000)
+    else:
+        cfg, scene = S.lidar_config(config), S.scene_for(config)
+    r = lidar_run(SM, cfg, scene, per_ray_sh=True)
+    ref = O.render_lidar(scene, cfg, flag_eps=LIDAR_EPS, per_ray_sh=True)
+    ok = ref["flag"] == 0
+    assert ok.mean() > 1 - FLAG_BUDGET["default"], ok.mean()
+    e = compare_lidar(r.out, ref, ok)
+    print(config, e)
+    base = lidar_run(SM, cfg, scene)  # per-particle features: same weights, other zeta
+    assert torch.equal(base.out["opacity"], r.out["opacity"])
+    assert (base.out["zeta"] - r.out["zeta"]).abs().max().item() > 1e-4
+
+
+def test_per_ray_sh_camera_parity(SM, oracle_mod):
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    scene = S.corridor_scene(21, 40000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    c = camera_run(SM, cam, scene, per_ray_sh=True)
+    ref2 = O.render_camera(scene, cam, flag_eps=CAMERA_EPS, per_ray_sh=True)
+    ok2 = ref2["flag"] == 0
+    assert ok2.mean() > 0.995, ok2.mean()
+    err = np.abs(c.out["rgb"].cpu().numpy() - ref2["feat"])[ok2].max()
+    print("camera per-ray SH max |gpu - oracle|", err)
+    assert err < TOL_FEAT

@@ -912,3 +912,35 @@ def test_actor_rigid_invariance_lidar(oracle_mod):
     assert np.abs(got["opacity"] - ref["opacity"])[ok].max() < 2e-5
     hit = ok & (ref["opacity"] > 0.5)
     assert np.abs(got["depth"] - ref["depth"])[hit].max() < 1e-4
+
+
+# ------------------------------------------------------------------ per-ray SH (Eq. 1 literally, A30)
+def test_per_ray_sh_closed_forms(oracle_mod):
+    """Per-ray SH (zeta = sum_i SH_i(d) alpha_i T_i, d the ray direction): (1) degree 0: the
+    same as per-particle features (Y_00 is constant); (2) every particle with the same
+    coefficients c: zeta(r) = omega(r) SH_c(d_r) exactly (sh_eval is pinned against scipy
+    above), whereas per-particle features are not -- they see each particle's own view
+    direction."""
+    O = oracle_mod
+    cfg = S.lidar_config("tiny")
+    scene = S.scene_for("tiny", seed=17, n=400)
+    s0 = dict(scene)
+    s0["sh"] = np.ascontiguousarray(scene["sh"][:, :1])
+    a = O.render_lidar(s0, cfg)
+    b = O.render_lidar(s0, cfg, per_ray_sh=True)
+    assert np.abs(a["feat"] - b["feat"]).max() < 1e-13
+    assert np.array_equal(a["opacity"], b["opacity"])
+    rng = np.random.default_rng(18)
+    c = rng.normal(size=(16, 3))
+    s1 = dict(scene)
+    s1["sh"] = np.ascontiguousarray(np.broadcast_to(c.astype(np.float32), scene["sh"].shape))
+    pr = O.render_lidar(s1, cfg, per_ray_sh=True)
+    pp = O.render_lidar(s1, cfg)
+    od = pr["ray_od"]
+    hit = pr["opacity"] > 0.05
+    assert hit.mean() > 0.05
+    for r in np.nonzero(hit)[0][:200]:
+        d = od[r, 3:] / np.linalg.norm(od[r, 3:])
+        ref = pr["opacity"][r] * O.sh_eval(c.astype(np.float32).astype(np.float64), d)
+        assert np.allclose(pr["feat"][r], ref, rtol=0, atol=1e-12)
+    assert np.abs(pp["feat"] - pr["feat"])[hit].max() > 1e-3  # the two readings differ
