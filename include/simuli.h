@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 5
+#define SIMULI_ABI_VERSION 6
 
 enum {
   SIMULI_OK = 0,
@@ -222,6 +222,8 @@ typedef struct {
   int32_t* tile_rect;
   float* depth_key;
   int32_t* tile_count;
+  float* view_dir;  /* [n][3] or NULL: the unit SH view direction of each written record
+                       (A17; 0 if invalid) -- the backward's SH chain needs it (A31) */
 } simuli_projected;
 
 /* UT projection: 7 sigma points mu, mu +- sqrt(3+lambda) l_k (l_k = s_k R e_k,
@@ -327,6 +329,59 @@ typedef struct {
 int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorted_ids, const int32_t* tile_ranges,
                              const int32_t* tile_order, const simuli_project_params* params,
                              const simuli_render_params* rparams, simuli_camera_out* out, void* stream);
+
+/* ---- Backward pass ("differentiable renderer", P:160-171 training; readings A31) ----
+ * Gradients of a loss L with respect to the particle parameters, given the upstream
+ * gradients of the rendered outputs.  The forward decisions (box membership A12, the
+ * alpha_min / near skips A13, the T_min termination A14) are replayed exactly (same
+ * float32 arithmetic as the render kernels) and are not differentiated; the response
+ * is: alpha = min(alpha_max, sigma rho(tau_max)) with tau_max and delta^2 of the
+ * canonical transform M = diag(1/s) R(q/|q|)^T (clamped alpha: no gradient).  Features are
+ * the per-particle SH at the projection's view direction (A17), held fixed (no gradient
+ * through the direction).  Not supported (UNSUPPORTED): beam divergence, per-ray SH,
+ * scene-graph particles (actor_id).
+ * Upstream gradients (device, [n_rays] or [n_rays][3]; NULL = 0): LiDAR zeta, opacity
+ * (omega), depth_accum (D), depth (D / omega), intensity (zeta_0), raydrop
+ * (1 / (1 + exp(zeta_1 - zeta_2))); camera rgb (c_f), opacity, depth_accum, depth. */
+typedef struct {
+  const float *zeta, *opacity, *depth_accum, *depth, *intensity, *raydrop;
+} simuli_lidar_grad_in;
+
+typedef struct {
+  const float *rgb, *opacity, *depth_accum, *depth;
+} simuli_camera_grad_in;
+
+/* Per-particle parameter gradients (device, caller-allocated, n entries each; overwritten,
+ * zero for particles that composite into no ray): means [n][3], quats [n][4] (w.r.t. the
+ * unnormalised input quaternion), scales [n][3], opacity [n] (post-activation sigma),
+ * sh [n][(deg+1)^2][3]. */
+typedef struct {
+  float *means, *quats, *scales, *opacity, *sh;
+} simuli_gaussian_grads;
+
+/* Scratch bytes for the backward of n particles (16 floats each). */
+int32_t simuli_backward_workspace_size(int64_t n, size_t* bytes);
+
+/* LiDAR backward.  gaussians / params / rparams / proj / sorted_ids / tile_ranges: exactly
+ * the forward frame's (proj->view_dir must have been written by simuli_project).  Launches:
+ * workspace clear, one warp per (tile, 32-ray chunk) replaying the tile's list twice
+ * (totals, then gradients with suffix sums; warp-reduced float atomics into the workspace),
+ * then one thread per particle for the parameter chain.  Asynchronous on `stream`;
+ * gradient sums are in atomic (nondeterministic) order.
+ * Errors: INVALID_ARGUMENT (NULL, view_dir missing, workspace too small), UNSUPPORTED
+ * (see above), CUDA. */
+int32_t simuli_backward_lidar(const simuli_gaussians* gaussians, const simuli_projected* proj,
+                              const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                              const simuli_project_params* params, const simuli_render_params* rparams,
+                              const simuli_lidar_grad_in* grad_in, simuli_gaussian_grads* grad_out,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* Camera backward: as simuli_backward_lidar, one CTA per tile (pixel per thread). */
+int32_t simuli_backward_camera(const simuli_gaussians* gaussians, const simuli_projected* proj,
+                               const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                               const simuli_project_params* params, const simuli_render_params* rparams,
+                               const simuli_camera_grad_in* grad_in, simuli_gaussian_grads* grad_out,
+                               void* workspace, size_t workspace_bytes, void* stream);
 
 /* Final camera colour, Eq. 2: c = A(omega c_f + (1 - omega) c_b(d)), with the
  * background c_b(d) from a learned environment map and A an affine colour transform from a

@@ -900,6 +900,8 @@ static int project_common(const or_gaussians* G, const void* sensor, int wrap_a,
     for (int c = 0; c < 3; ++c) v[c] /= vn;
     for (int k = 0; k < ncoef * 3; ++k) shd[k] = G->sh[g * ncoef * 3 + k];
     or_sh_eval(shd, G->sh_degree, v, &out->feat[g * 3]);
+    if (out->viewdir)
+      for (int c = 0; c < 3; ++c) out->viewdir[g * 3 + c] = v[c];
   }
   return 0;
 }
@@ -1402,3 +1404,189 @@ void or_actors_to_world(int64_t n, const float* means, const float* quats, const
     quats_w[4 * i + 3] = (float)z;
   }
 }
+
+/* ------------------------------------------------------------------------------------
+ * O15 backward of Eq. 1 (reading A31).  For one ray with contributions
+ * k = 1..K in list order (the members or_composite composites: not skipped, before the
+ * terminating particle):
+ *   w_k = alpha_k T_k,  T_k = prod_{j<k} (1 - alpha_j),
+ *   zeta = sum w_k f_k,  omega = sum w_k,  D = sum w_k tau_k.
+ * With upstream gradients (Gz, Go, GD) and suffix sums S_k(x) = sum_{i>k} w_i x_i:
+ *   dL/dalpha_k = T_k (Gz.f_k + Go + GD tau_k) - (Gz.S_k(f) + Go S_k(1) + GD S_k(tau)) / (1 - alpha_k)
+ *   dL/dtau_k = GD w_k,   dL/df_k = Gz w_k.
+ * alpha = min(alpha_max, sigma rho), rho = exp(-delta^2 / 2): if not clamped,
+ *   dL/dsigma = dL/dalpha rho,  dL/d(delta^2) = -dL/dalpha alpha / 2 (clamped: 0).
+ * Response (O12) with u = M d, w = M (o - mu), n2 = |u|^2:
+ *   tau = -(w.u)/n2,  delta^2 = |w|^2 - (w.u)^2/n2
+ *   d(delta^2)/dw = 2 (w + tau u),  d(delta^2)/du = 2 tau (w + tau u)
+ *   dtau/dw = -u/n2,               dtau/du = -(w + 2 tau u)/n2
+ *   dL/dM = gw (o - mu)^T + gu d^T,  dL/dmu = -M^T gw.
+ * Membership, skips and termination are discrete: no gradient through them.
+ * ---------------------------------------------------------------------------------- */
+int or_backward_composite(const double* mu, const double* Mrows, const double* sigma, const double* feat,
+                          const float* box, const uint32_t* ids, const int32_t* ranges, int32_t n_rays,
+                          const int32_t* ray_tile, const float* ray_a, const float* ray_b, const double* ray_od,
+                          const int32_t* ray_valid, const or_render_params* p, const double* g_feat,
+                          const double* g_opacity, const double* g_daccum, double* d_mu, double* d_M,
+                          double* d_sigma, double* d_feat) {
+  int64_t max_len = 0;
+  for (int32_t r = 0; r < n_rays; ++r) {
+    const int32_t t = ray_tile[r];
+    if (ranges[2 * t + 1] - ranges[2 * t] > max_len) max_len = ranges[2 * t + 1] - ranges[2 * t];
+  }
+  int fail = 0;
+#pragma omp parallel
+  {
+    uint32_t* kg = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(max_len + 1));
+    double* ka = (double*)malloc(sizeof(double) * (size_t)(max_len + 1) * 4); /* alpha, tau, T, rho */
+    int* kc = (int*)malloc(sizeof(int) * (size_t)(max_len + 1));              /* clamped */
+    if (!kg || !ka || !kc) {
+#pragma omp atomic write
+      fail = 1;
+    } else {
+#pragma omp for schedule(dynamic, 64)
+      for (int32_t r = 0; r < n_rays; ++r) {
+        if (ray_valid && !ray_valid[r]) continue;
+        const double* o = &ray_od[(int64_t)r * 6];
+        const double* d = o + 3;
+        const int32_t t = ray_tile[r];
+        const float xa = ray_a[r], xb = ray_b[r];
+        /* forward: the contributions in list order (or_composite's rules) */
+        int K = 0;
+        double T = 1.0;
+        for (int32_t i = ranges[2 * t]; i < ranges[2 * t + 1]; ++i) {
+          const uint32_t g = ids[i];
+          const float* bx = &box[(int64_t)g * 4];
+          if (!(in_interval_a(bx[0], bx[1], xa, p->wrap, p->pi_f, p->two_pi_f) && bx[2] <= xb && xb <= bx[3]))
+            continue;
+          double rs[2];
+          or_response(&mu[(int64_t)g * 3], &Mrows[(int64_t)g * 9], o, d, rs);
+          const double rho = exp(-0.5 * rs[1]);
+          const double a = sigma[g] * rho;
+          const double alpha = a < p->alpha_max ? a : p->alpha_max;
+          if (rs[0] < p->near_tau || alpha < p->alpha_min) continue;
+          const double Tn = T * (1.0 - alpha);
+          if (Tn < p->T_min) break;
+          kg[K] = g;
+          ka[4 * K] = alpha;
+          ka[4 * K + 1] = rs[0];
+          ka[4 * K + 2] = T;
+          ka[4 * K + 3] = rho;
+          kc[K] = !(a < p->alpha_max);
+          ++K;
+          T = Tn;
+        }
+        const double Gz[3] = {g_feat ? g_feat[3 * (int64_t)r] : 0.0, g_feat ? g_feat[3 * (int64_t)r + 1] : 0.0,
+                              g_feat ? g_feat[3 * (int64_t)r + 2] : 0.0};
+        const double Go = g_opacity ? g_opacity[r] : 0.0, GD = g_daccum ? g_daccum[r] : 0.0;
+        /* backward, last contribution first, carrying the suffix sums */
+        double Sf = 0.0, S1 = 0.0, St = 0.0; /* Gz.S(f), S(1), S(tau) */
+        for (int k = K - 1; k >= 0; --k) {
+          const uint32_t g = kg[k];
+          const double alpha = ka[4 * k], tau = ka[4 * k + 1], Tk = ka[4 * k + 2], rho = ka[4 * k + 3];
+          const double* f = &feat[(int64_t)g * 3];
+          const double wk = alpha * Tk;
+          const double gzf = Gz[0] * f[0] + Gz[1] * f[1] + Gz[2] * f[2];
+          const double dalpha = Tk * (gzf + Go + GD * tau) - (Sf + Go * S1 + GD * St) / (1.0 - alpha);
+          const double dtau = GD * wk;
+          double dsig = 0.0, dd2 = 0.0;
+          if (!kc[k]) {
+            dsig = dalpha * rho;
+            dd2 = -0.5 * dalpha * alpha;
+          }
+          /* response gradients */
+          const double* M = &Mrows[(int64_t)g * 9];
+          const double pw[3] = {o[0] - mu[g * 3], o[1] - mu[g * 3 + 1], o[2] - mu[g * 3 + 2]};
+          double u[3], w[3];
+          for (int a = 0; a < 3; ++a) {
+            u[a] = M[3 * a] * d[0] + M[3 * a + 1] * d[1] + M[3 * a + 2] * d[2];
+            w[a] = M[3 * a] * pw[0] + M[3 * a + 1] * pw[1] + M[3 * a + 2] * pw[2];
+          }
+          const double n2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+          const double tr = -(w[0] * u[0] + w[1] * u[1] + w[2] * u[2]) / n2; /* = tau */
+          double gw[3], gu[3];
+          for (int a = 0; a < 3; ++a) {
+            const double h = w[a] + tr * u[a];
+            gw[a] = dd2 * 2.0 * h + dtau * (-u[a] / n2);
+            gu[a] = dd2 * 2.0 * tr * h + dtau * (-(w[a] + 2.0 * tr * u[a]) / n2);
+          }
+#pragma omp critical(or_bwd_acc)
+          {
+            for (int a = 0; a < 3; ++a) {
+              for (int b = 0; b < 3; ++b) d_M[(int64_t)g * 9 + 3 * a + b] += gw[a] * pw[b] + gu[a] * d[b];
+              double mt = 0.0;
+              for (int b = 0; b < 3; ++b) mt += M[3 * b + a] * gw[b];
+              d_mu[(int64_t)g * 3 + a] -= mt;
+              d_feat[(int64_t)g * 3 + a] += Gz[a] * wk;
+            }
+            d_sigma[g] += dsig;
+          }
+          Sf += wk * gzf;
+          S1 += wk;
+          St += wk * tau;
+        }
+      }
+    }
+    free(kg);
+    free(ka);
+    free(kc);
+  }
+  return fail ? -1 : 0;
+}
+
+/* ------------------------------------------------------------------------------------
+ * O16 chain to the particle parameters:  M[k][j] = R[j][k] / s_k with R = R(q^),
+ *   q^ = q/|q| (O1):  dL/dR[j][k] = dL/dM[k][j] / s_k,  dL/ds_k = -sum_j dL/dM[k][j] R[j][k] / s_k^2;
+ *   dR/dq^ by differentiating O1's entries;  dL/dq = (dL/dq^ - q^ (q^ . dL/dq^)) / |q|.
+ *   f = sum_k Y_k(v) c_k (O9):  dL/dc_k = Y_k(v) dL/df (v held fixed, A31).
+ * ---------------------------------------------------------------------------------- */
+void or_backward_params(int64_t n, const float* quats, const float* scales, const double* viewdir,
+                        int32_t sh_degree, const double* d_M, const double* d_feat, double* g_quats,
+                        double* g_scales, double* g_sh) {
+  const int nco = (sh_degree + 1) * (sh_degree + 1);
+  for (int64_t g = 0; g < n; ++g) {
+    double q[4], qn = 0.0;
+    for (int c = 0; c < 4; ++c) {
+      q[c] = quats[4 * g + c];
+      qn += q[c] * q[c];
+    }
+    qn = sqrt(qn);
+    for (int c = 0; c < 4; ++c) g_quats[4 * g + c] = 0.0;
+    for (int c = 0; c < 3; ++c) g_scales[3 * g + c] = 0.0;
+    for (int k = 0; k < nco * 3; ++k) g_sh[(int64_t)g * nco * 3 + k] = 0.0;
+    if (!(qn > 0.0) || !isfinite(qn)) continue;
+    double R[9];
+    or_quat_to_rot(q, R); /* normalises */
+    const double w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
+    double G[9]; /* dL/dR[j][k] */
+    for (int k = 0; k < 3; ++k) {
+      const double s = scales[3 * g + k];
+      double ds = 0.0;
+      for (int j = 0; j < 3; ++j) {
+        const double dm = d_M[g * 9 + 3 * k + j];
+        G[3 * j + k] = dm / s;
+        ds -= dm * R[3 * j + k] / (s * s);
+      }
+      g_scales[3 * g + k] = ds;
+    }
+    /* R = [[1-2(y2+z2), 2(xy-wz), 2(xz+wy)], [2(xy+wz), 1-2(x2+z2), 2(yz-wx)], [2(xz-wy), 2(yz+wx), 1-2(x2+y2)]] */
+    const double dw = 2.0 * (-z * G[1] + y * G[2] + z * G[3] - x * G[5] - y * G[6] + x * G[7]);
+    const double dx = 2.0 * (y * G[1] + z * G[2] + y * G[3] - 2.0 * x * G[4] - w * G[5] + z * G[6] + w * G[7] -
+                             2.0 * x * G[8]);
+    const double dy = 2.0 * (-2.0 * y * G[0] + x * G[1] + w * G[2] + x * G[3] + z * G[5] - w * G[6] + z * G[7] -
+                             2.0 * y * G[8]);
+    const double dz = 2.0 * (-2.0 * z * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.0 * z * G[4] + y * G[5] +
+                             x * G[6] + y * G[7]);
+    const double dq[4] = {dw, dx, dy, dz}, qh[4] = {w, x, y, z};
+    const double dot = dw * w + dx * x + dy * y + dz * z;
+    for (int c = 0; c < 4; ++c) g_quats[4 * g + c] = (dq[c] - qh[c] * dot) / qn;
+    /* SH: the basis at v, one coefficient at a time through O9 */
+    for (int k = 0; k < nco; ++k) {
+      double e[48] = {0}, yk[3];
+      e[3 * k] = 1.0;
+      or_sh_eval(e, sh_degree, &viewdir[3 * g], yk); /* yk[0] = Y_k(v) */
+      for (int c = 0; c < 3; ++c) g_sh[(int64_t)g * nco * 3 + 3 * k + c] = yk[0] * d_feat[3 * g + c];
+    }
+  }
+}
+

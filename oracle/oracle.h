@@ -101,6 +101,7 @@ typedef struct {
   double*  feat;            /* [n][3] SH features                                          */
   float*   key;             /* [n] float32 depth key (O10)                                 */
   double*  minrange;        /* [n] smallest sigma-point range / camera distance            */
+  double*  viewdir;         /* [n][3] unit SH view direction (A17) or NULL                 */
 } or_proj_out;
 
 typedef struct {
@@ -166,6 +167,23 @@ int  or_get_threads(void);
 int or_compose_camera(const or_camera* C, const double* ray_od, const double* rgb_fg, const double* omega,
                       const float* env, int32_t He, int32_t We, const float* grid, int32_t gh, int32_t gw,
                       int32_t gd, double* rgb_out);
+
+/* O15: backward of Eq. 1 compositing ("differentiable renderer"; A31).  Per ray, the
+ * forward contributions are collected in list order (same rules as or_composite) and
+ * dL/d(mu, M, sigma, f) of every contributing particle accumulated from the upstream
+ * gradients g_feat [R][3], g_opacity [R], g_daccum [R] (NULL = 0).  Outputs [n][3], [n][9],
+ * [n], [n][3] are accumulated (caller zeroes). */
+int or_backward_composite(const double* mu, const double* Mrows, const double* sigma, const double* feat,
+                          const float* box, const uint32_t* ids, const int32_t* ranges, int32_t n_rays,
+                          const int32_t* ray_tile, const float* ray_a, const float* ray_b, const double* ray_od,
+                          const int32_t* ray_valid, const or_render_params* p, const double* g_feat,
+                          const double* g_opacity, const double* g_daccum, double* d_mu, double* d_M,
+                          double* d_sigma, double* d_feat);
+/* O16: chain to the particle parameters: M = diag(1/s) R(q/|q|)^T -> dq, ds;
+ * f = SH(v) -> dSH (v = the projection's view direction, no gradient through v, A31). */
+void or_backward_params(int64_t n, const float* quats, const float* scales, const double* viewdir,
+                        int32_t sh_degree, const double* d_M, const double* d_feat, double* g_quats,
+                        double* g_scales, double* g_sh);
 
 /* O0: scene graph, object particles -> world at the frame's timestamp (A29) */
 void or_actors_to_world(int64_t n, const float* means, const float* quats, const int32_t* actor_id,

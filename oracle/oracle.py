@@ -61,7 +61,7 @@ class OrTiling(C.Structure):
 
 class OrProjOut(C.Structure):
     _fields_ = [("valid", i32p), ("ambiguous", i32p), ("mean2d", f64p), ("cov2d", f64p), ("box", f32p),
-                ("Mrows", f64p), ("feat", f64p), ("key", f32p), ("minrange", f64p)]
+                ("Mrows", f64p), ("feat", f64p), ("key", f32p), ("minrange", f64p), ("viewdir", f64p)]
 
 
 class OrGaussians(C.Structure):
@@ -124,6 +124,10 @@ def lib():
         L.or_elev_tile.argtypes = [C.POINTER(OrTiling), C.c_float]
         L.or_az_col.argtypes = [C.POINTER(OrTiling), C.c_float]
         L.or_set_threads.argtypes = [C.c_int]
+        L.or_backward_composite.argtypes = [f64p, f64p, f64p, f64p, f32p, u32p, i32p, C.c_int32, i32p, f32p, f32p,
+                                            f64p, i32p, C.POINTER(OrRenderParams), f64p, f64p, f64p, f64p, f64p,
+                                            f64p, f64p]
+        L.or_backward_params.argtypes = [C.c_int64, f32p, f32p, f64p, C.c_int32, f64p, f64p, f64p, f64p, f64p]
         L.or_actors_to_world.argtypes = [C.c_int64, f32p, f32p, i32p, C.c_int32, f64p, f32p, f32p]
         _lib = L
     return _lib
@@ -237,10 +241,11 @@ def _gauss(scene):
 def _proj_out(n):
     o = {"valid": np.zeros(n, np.int32), "ambiguous": np.zeros(n, np.int32), "mean2d": np.zeros((n, 2)),
          "cov2d": np.zeros((n, 3)), "box": np.zeros((n, 4), np.float32), "Mrows": np.zeros((n, 9)),
-         "feat": np.zeros((n, 3)), "key": np.zeros(n, np.float32), "minrange": np.zeros(n)}
+         "feat": np.zeros((n, 3)), "key": np.zeros(n, np.float32), "minrange": np.zeros(n),
+         "viewdir": np.zeros((n, 3))}
     s = OrProjOut(_p(o["valid"], i32p), _p(o["ambiguous"], i32p), _p(o["mean2d"], f64p), _p(o["cov2d"], f64p),
                   _p(o["box"], f32p), _p(o["Mrows"], f64p), _p(o["feat"], f64p), _p(o["key"], f32p),
-                  _p(o["minrange"], f64p))
+                  _p(o["minrange"], f64p), _p(o["viewdir"], f64p))
     return o, s
 
 
@@ -551,6 +556,121 @@ def compose_camera(cam, ray_od, rgb_fg, omega, env=None, grid=None):
                             0 if e is None else e.shape[0], 0 if e is None else e.shape[1],
                             None if g is None else _p(g, f32p), 0 if g is None else g.shape[1],
                             0 if g is None else g.shape[2], 0 if g is None else g.shape[0], _p(out, f64p))
+    return out
+
+
+# ------------------------------------------------------------------------------------
+# backward (O15, O16; reading A31)
+# ------------------------------------------------------------------------------------
+
+def fold_upstream(fwd, grads, lidar):
+    """Upstream gradients of the decoded outputs -> (G_feat [R,3], G_omega [R], G_D [R]):
+    depth = D / omega (omega > 0, else 0), LiDAR intensity = zeta_0, ray drop
+    beta = 1 / (1 + exp(zeta_1 - zeta_2)) (P:126)."""
+    R = fwd["opacity"].shape[0]
+    g = lambda k, shape: (np.zeros(shape) if grads.get(k) is None  # noqa: E731
+                          else np.asarray(grads[k], np.float64).reshape(shape).copy())
+    Gz = g("rgb" if not lidar else "zeta", (R, 3))
+    Go = g("opacity", R)
+    GD = g("depth_accum", R)
+    gd = g("depth", R)
+    om, D = fwd["opacity"], fwd["depth_accum"]
+    pos = om > 0
+    GD[pos] += gd[pos] / om[pos]
+    Go[pos] -= gd[pos] * D[pos] / om[pos] ** 2
+    if lidar:
+        Gz[:, 0] += g("intensity", R)
+        beta = 1.0 / (1.0 + np.exp(fwd["feat"][:, 1] - fwd["feat"][:, 2]))
+        gr = g("raydrop", R) * beta * (1.0 - beta)
+        Gz[:, 1] -= gr
+        Gz[:, 2] += gr
+    return Gz, Go, GD
+
+
+def backward_composite(records, ids, ranges, ray_tile, ray_a, ray_b, ray_od, Gz, Go, GD, *, wrap, near,
+                       ray_valid=None, alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4, pi_f=None, two_pi_f=None):
+    """O15: dL/d(mu, M, sigma, f) per particle (double)."""
+    n = records["mu"].shape[0]
+    pf = np.float32(np.pi) if pi_f is None else np.float32(pi_f)
+    tpf = np.float32(2 * np.pi) if two_pi_f is None else np.float32(two_pi_f)
+    prm = OrRenderParams(float(np.float32(near)), float(np.float32(alpha_min)), float(np.float32(alpha_max)),
+                         float(np.float32(T_min)), int(wrap), pf, tpf, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0)
+    out = {"mu": np.zeros((n, 3)), "M": np.zeros((n, 9)), "sigma": np.zeros(n), "feat": np.zeros((n, 3))}
+    mu, Mr, sg, ft = _d(records["mu"]), _d(records["Mrows"]), _d(records["sigma"]), _d(records["feat"])
+    box = np.ascontiguousarray(records["box"], np.float32)
+    ids = np.ascontiguousarray(ids, np.uint32)
+    ranges = np.ascontiguousarray(ranges, np.int32)
+    rt = np.ascontiguousarray(ray_tile, np.int32)
+    ra, rb = np.ascontiguousarray(ray_a, np.float32), np.ascontiguousarray(ray_b, np.float32)
+    rv = None if ray_valid is None else np.ascontiguousarray(ray_valid, np.int32)
+    od, Gz, Go, GD = _d(ray_od), _d(Gz), _d(Go), _d(GD)
+    rc = lib().or_backward_composite(_p(mu, f64p), _p(Mr, f64p), _p(sg, f64p), _p(ft, f64p), _p(box, f32p),
+                                     _p(ids, u32p), _p(ranges, i32p), int(rt.shape[0]), _p(rt, i32p), _p(ra, f32p),
+                                     _p(rb, f32p), _p(od, f64p), _p(rv, i32p), C.byref(prm), _p(Gz, f64p),
+                                     _p(Go, f64p), _p(GD, f64p), _p(out["mu"], f64p), _p(out["M"], f64p),
+                                     _p(out["sigma"], f64p), _p(out["feat"], f64p))
+    assert rc == 0
+    return out
+
+
+def backward_params(scene, proj, d):
+    """O16: gradients of the particle parameters (means, quats, scales, opacity, sh)."""
+    if scene.get("actor_id") is not None:
+        raise NotImplementedError("backward through the scene graph is not modelled (A31)")
+    n = int(scene["means"].shape[0])
+    q = np.ascontiguousarray(scene["quats"], np.float32)
+    s = np.ascontiguousarray(scene["scales"], np.float32)
+    ncoef = scene["sh"].size // max(n, 1) // 3
+    deg = {1: 0, 4: 1, 9: 2, 16: 3}[ncoef]
+    gq, gs, gsh = np.zeros((n, 4)), np.zeros((n, 3)), np.zeros((n, ncoef, 3))
+    vd = _d(proj["viewdir"])
+    lib().or_backward_params(n, _p(q, f32p), _p(s, f32p), _p(vd, f64p), deg, _p(_d(d["M"]), f64p),
+                             _p(_d(d["feat"]), f64p), _p(gq, f64p), _p(gs, f64p), _p(gsh, f64p))
+    return {"means": d["mu"].copy(), "quats": gq, "scales": gs, "opacity": d["sigma"].copy(), "sh": gsh}
+
+
+def backward_lidar(scene, cfg, grads, tiling: Tiling | None = None, pose0=None, pose1=None, K=None, ut=None,
+                   alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4):
+    """Whole-path LiDAR backward (O1-O12 forward, O15, O16).  grads: upstream gradients by
+    output name (zeta, opacity, depth_accum, depth, intensity, raydrop; missing = 0)."""
+    tiling = tiling or Tiling(cfg)
+    pose0 = pose0 or cfg.pose_start
+    pose1 = pose1 or cfg.pose_end
+    fwd = render_lidar(scene, cfg, tiling=tiling, pose0=pose0, pose1=pose1, K=K, ut=ut, alpha_min=alpha_min,
+                       alpha_max=alpha_max, T_min=T_min)
+    proj = fwd["proj"]
+    rec = records_from_projection(proj, scene)
+    count, rect = cull_lidar(proj["valid"], proj["box"], tiling, True)
+    _, ids, ranges = bin_pairs(count, rect, proj["key"], tiling.n_tiles, tiling.n_theta)
+    Gz, Go, GD = fold_upstream(fwd, grads, lidar=True)
+    d = backward_composite(rec, ids, ranges, tiling.ray_tile, tiling.ray_az, tiling.ray_el, fwd["ray_od"], Gz, Go,
+                           GD, wrap=1, near=cfg.min_range, alpha_min=alpha_min, alpha_max=alpha_max, T_min=T_min,
+                           pi_f=tiling.pi_f, two_pi_f=tiling.two_pi_f)
+    out = backward_params(scene, proj, d)
+    out["fwd"] = fwd
+    out["d"] = d
+    return out
+
+
+def backward_camera(scene, cam, grads, pose0=None, pose1=None, K=None, ut=None, alpha_min=1.0 / 255.0,
+                    alpha_max=0.99, T_min=1e-4):
+    """Whole-path camera backward; grads keys rgb, opacity, depth_accum, depth."""
+    pose0 = pose0 or cam.pose_start
+    pose1 = pose1 or cam.pose_end
+    fwd = render_camera(scene, cam, pose0=pose0, pose1=pose1, K=K, ut=ut, alpha_min=alpha_min, alpha_max=alpha_max,
+                        T_min=T_min)
+    proj, rays = fwd["proj"], fwd["rays"]
+    rec = records_from_projection(proj, scene)
+    Wt, Ht = camera_tiles(cam)
+    count, rect = cull_camera(proj["valid"], proj["box"], cam)
+    _, ids, ranges = bin_pairs(count, rect, proj["key"], Wt * Ht, Wt)
+    Gz, Go, GD = fold_upstream(fwd, grads, lidar=False)
+    d = backward_composite(rec, ids, ranges, rays["tile"], rays["u"], rays["v"], rays["od"], Gz, Go, GD, wrap=0,
+                           near=cam.near, ray_valid=rays["valid"], alpha_min=alpha_min, alpha_max=alpha_max,
+                           T_min=T_min)
+    out = backward_params(scene, proj, d)
+    out["fwd"] = fwd
+    out["d"] = d
     return out
 
 

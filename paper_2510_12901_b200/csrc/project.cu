@@ -104,6 +104,7 @@ struct ProjArgs {
   float fx, fy, cx, cy, k[5], near_m, max_theta, inv_tile;
   // out
   float* record;
+  float* view_dir;  // optional [n][3] (backward: the SH direction, A31)
   int* rect;
   float* key;
   int* count;
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
   int rect[4] = {0, 0, 0, 0};
   float box[4] = {NAN, NAN, NAN, NAN};
   float M[9] = {NAN, NAN, NAN, NAN, NAN, NAN, NAN, NAN, NAN}, f[3] = {0.f, 0.f, 0.f};
+  float vdir[3] = {0.f, 0.f, 0.f};
   bool ok = true;
 
   const float qn2 = q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w;
@@ -667,6 +669,7 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
       const float vn = rsqrtf(vx * vx + vy * vy + vz * vz);
       vx *= vn; vy *= vn; vz *= vn;
       if (isfinite(vn)) {
+        vdir[0] = vx; vdir[1] = vy; vdir[2] = vz;
         if (stage_sh) {
           asm volatile("cp.async.wait_group 0;" ::: "memory");
           // coefficients streamed from shared memory one float4 at a time (coefficient
@@ -697,6 +700,11 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
     rec[2] = make_float4(M[5], M[6], M[7], M[8]);
     rec[3] = make_float4(sigma, f[0], f[1], f[2]);
     rec[4] = ok ? make_float4(box[0], box[1], box[2], box[3]) : make_float4(NAN, NAN, NAN, NAN);
+    if (A.view_dir) {
+      A.view_dir[3 * g] = vdir[0];
+      A.view_dir[3 * g + 1] = vdir[1];
+      A.view_dir[3 * g + 2] = vdir[2];
+    }
   }
 }
 
@@ -771,6 +779,7 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
   depth_origin(P->pose_start, P->pose_end, A.o_mid);
   A.write_all = P->write_all_records;
   A.record = out->record; A.rect = out->tile_rect; A.key = out->depth_key; A.count = out->tile_count;
+  A.view_dir = out->view_dir;
   const int threads = 256;
   const unsigned blocks = static_cast<unsigned>((G->n + threads - 1) / threads);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

@@ -956,3 +956,521 @@ extern "C" int32_t simuli_compose_camera(const simuli_project_params* P, const s
   k_compose_camera<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A);
   return launch_check("simuli_compose_camera");
 }
+
+// ====================================================================== backward (A31)
+// Gradients of the compositing (Eq. 1) and of the response with respect
+// to the particle records, chained to the parameters.  Per ray the tile's list is
+// replayed twice with the forward kernels' float32 arithmetic, so every discrete decision
+// (membership, skips, termination) is the forward's: pass 1 -> totals (zeta, omega, D),
+// pass 2 -> per contribution k with suffix sums S_k = total - prefix_k:
+//   dL/dalpha_k = T_k (Gz.f_k + Go + GD tau_k) - (Gz.S_k(f) + Go S_k(1) + GD S_k(tau)) / (1 - alpha_k)
+// (oracle O15).  All lanes of a warp walk the same list entry, so a contribution's 16
+// gradient values (dmu 3, dM 9, dsigma, df 3) are warp-reduced by shuffles and added with one
+// set of float atomics per entry.
+namespace simuli {
+namespace {
+
+struct BwdArgs {
+  const float4* record;
+  const uint32_t* ids;
+  const int2* ranges;
+  const int *tile_ray_off, *tile_rays;  // LiDAR
+  const float *ray_az, *ray_el, *ray_s;
+  int n_az, chunks;
+  float pi_f, two_pi_f;
+  CameraArgs cam;  // camera geometry (unproject, pose)
+  PoseInterpD pose;
+  float near_tau, alpha_min, alpha_max, T_min;
+  const float *g_feat, *g_opacity, *g_daccum, *g_depth, *g_intensity, *g_raydrop;
+  float* ws;  // [n][16]
+};
+
+constexpr int kBwdVals = 16;
+
+// d(tau, delta^2) -> d(mu, M) for one (ray, particle); p = o - mu compensated as in
+// response(), a = M (p - t d), u = M d:  h = a + tau_s u (= w + tau u),
+//   gw = 2 dd2 h - dtau u / n2,  gu = 2 dd2 tau h - dtau (w + 2 tau u) / n2,
+//   dL/dM = gw p^T + gu d^T,  dL/dmu = -M^T gw.
+__device__ __forceinline__ void response_grad(const RayF& r, const float mu[3], const float M[9], float dtau,
+                                              float dd2, float g[12]) {
+  float ph[3], pl[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float a = r.o_hi[k], b = -mu[k];
+    const float s = __fadd_rn(a, b);
+    const float bb = __fsub_rn(s, a);
+    const float err = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+    ph[k] = s;
+    pl[k] = err + r.o_lo[k];
+  }
+  const float t = ph[0] * r.d_hi[0] + ph[1] * r.d_hi[1] + ph[2] * r.d_hi[2];
+  float pp[3], p[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    pp[k] = fmaf(-t, r.d_hi[k], ph[k]) + fmaf(-t, r.d_lo[k], pl[k]);
+    p[k] = ph[k] + pl[k];
+  }
+  float a[3], u[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    a[k] = M[3 * k] * pp[0] + M[3 * k + 1] * pp[1] + M[3 * k + 2] * pp[2];
+    u[k] = M[3 * k] * r.d_hi[0] + M[3 * k + 1] * r.d_hi[1] + M[3 * k + 2] * r.d_hi[2];
+  }
+  const float inv = 1.0f / (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  const float ts = -(a[0] * u[0] + a[1] * u[1] + a[2] * u[2]) * inv;
+  const float tau = ts - t;
+  float gw[3], gu[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float h = fmaf(ts, u[k], a[k]);
+    const float w = fmaf(t, u[k], a[k]);
+    gw[k] = 2.f * dd2 * h - dtau * u[k] * inv;
+    gu[k] = 2.f * dd2 * tau * h - dtau * fmaf(2.f * tau, u[k], w) * inv;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g[k] = -(M[k] * gw[0] + M[3 + k] * gw[1] + M[6 + k] * gw[2]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) g[3 + 3 * k + j] = gw[k] * p[j] + gu[k] * r.d_hi[j];
+}
+
+// One lane's ray against one list entry, forward rules: 0 = no contribution, 1 = contributes
+// (alpha, tau, rho, clamped filled), 2 = terminates the ray.
+__device__ __forceinline__ int bwd_step(const BwdArgs& A, const RayF& rf, const float4 r[4], float T, float* alpha,
+                                        float* tau, float* rho, bool* clamped) {
+  const float mu[3] = {r[0].x, r[0].y, r[0].z};
+  const float M[9] = {r[0].w, r[1].x, r[1].y, r[1].z, r[1].w, r[2].x, r[2].y, r[2].z, r[2].w};
+  float d2;
+  response(rf, mu, M, tau, &d2);
+  *rho = expf(-0.5f * d2);
+  const float av = r[3].x * *rho;
+  *alpha = fminf(A.alpha_max, av);
+  *clamped = !(av < A.alpha_max);
+  if (*tau < A.near_tau || *alpha < A.alpha_min) return 0;
+  if (T * (1.f - *alpha) < A.T_min) return 2;
+  return 1;
+}
+
+// Walks the list [rg.x, rg.y) in order for a warp whose lanes hold rays (ray lane r has
+// coordinates (ra[r], rb[r]) in shared memory: LiDAR azimuth / elevation, camera pixel
+// centre).  32 entries at a time are fetched in parallel (lane = entry: id + 80-byte
+// record) and each lane tests its entry against all 32 rays (member(bx, a, b), the A12 box
+// test), so entries that hold none of the warp's rays cost nothing further; the others are
+// visited in list order with the record broadcast by shuffles.  body(member, id, rec) runs
+// on all lanes (it may use warp collectives); the walk ends once every lane is done.
+template <typename Member, typename Body>
+__device__ __forceinline__ void walk_list(const BwdArgs& A, int2 rg, const bool& done, const float* ra,
+                                          const float* rb, Member member, Body body) {
+  const int lane = threadIdx.x & 31;
+  for (int base = rg.x; base < rg.y; base += 32) {
+    const uint32_t open = __ballot_sync(0xffffffffu, !done);
+    if (open == 0u) return;
+    const int i = base + lane;
+    uint32_t g = 0, mm = 0;
+    float4 q[5];
+    if (i < rg.y) {
+      g = __ldg(A.ids + i);
+      const float4* src = A.record + (size_t)g * 5;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) q[c] = __ldg(src + c);
+      for (uint32_t o = open; o; o &= o - 1u) {
+        const int r = __ffs(o) - 1;
+        mm |= (uint32_t)member(q[4], ra[r], rb[r]) << r;
+      }
+    }
+    uint32_t ent = __ballot_sync(0xffffffffu, mm != 0u);
+    while (ent) {
+      const int k = __ffs(ent) - 1;
+      ent &= ent - 1u;
+      const uint32_t mk = __shfl_sync(0xffffffffu, mm, k);  // all lanes (not under a short circuit)
+      const bool m = !done && ((mk >> lane) & 1u);
+      if (!__any_sync(0xffffffffu, m)) continue;
+      float4 r[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        r[c] = make_float4(__shfl_sync(0xffffffffu, q[c].x, k), __shfl_sync(0xffffffffu, q[c].y, k),
+                           __shfl_sync(0xffffffffu, q[c].z, k), __shfl_sync(0xffffffffu, q[c].w, k));
+      body(m, __shfl_sync(0xffffffffu, g, k), r);
+      if (__all_sync(0xffffffffu, done)) return;
+    }
+  }
+}
+
+// The two passes of one warp whose lanes hold rays (LiDAR / camera: the same tile) over the
+// tile's list; member(bx) is the lane's A12 box test.
+template <bool LIDAR, typename Member>
+__device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF& rf, bool live, int ray,
+                                                    int2 rg, const float* ra, const float* rb, Member member) {
+  const int lane = threadIdx.x & 31;
+  // ---- pass 1: totals
+  float T = 1.f, z0 = 0.f, z1 = 0.f, z2 = 0.f, D = 0.f, W = 0.f;
+  bool done = !live;
+  walk_list(A, rg, done, ra, rb, member, [&](bool m, uint32_t, const float4 r[4]) {
+    if (!m) return;
+    float alpha, tau, rho;
+    bool cl;
+    const int st = bwd_step(A, rf, r, T, &alpha, &tau, &rho, &cl);
+    if (st == 0) return;
+    if (st == 2) {
+      done = true;
+      return;
+    }
+    const float w = alpha * T;
+    z0 = fmaf(w, r[3].y, z0);
+    z1 = fmaf(w, r[3].z, z1);
+    z2 = fmaf(w, r[3].w, z2);
+    D = fmaf(w, tau, D);
+    W += w;
+    T = T * (1.f - alpha);
+  });
+  // ---- upstream gradients of the decoded outputs -> (Gz, Go, GD)
+  float Gz[3] = {0.f, 0.f, 0.f}, Go = 0.f, GD = 0.f;
+  if (live) {
+    if (A.g_feat)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) Gz[c] = __ldg(A.g_feat + 3 * (size_t)ray + c);
+    if (A.g_opacity) Go = __ldg(A.g_opacity + ray);
+    if (A.g_daccum) GD = __ldg(A.g_daccum + ray);
+    if (A.g_depth && W > 0.f) {
+      const float gd = __ldg(A.g_depth + ray);
+      GD += gd / W;
+      Go -= gd * D / (W * W);
+    }
+    if (LIDAR) {
+      if (A.g_intensity) Gz[0] += __ldg(A.g_intensity + ray);
+      if (A.g_raydrop) {
+        const float beta = raydrop_prob(z1, z2);
+        const float gr = __ldg(A.g_raydrop + ray) * beta * (1.f - beta);
+        Gz[1] -= gr;
+        Gz[2] += gr;
+      }
+    }
+  }
+  // ---- pass 2: gradients
+  const float tot_f = Gz[0] * z0 + Gz[1] * z1 + Gz[2] * z2;
+  float pz0 = 0.f, pz1 = 0.f, pz2 = 0.f, pD = 0.f, pW = 0.f;
+  T = 1.f;
+  done = !live;
+  walk_list(A, rg, done, ra, rb, member, [&](bool m, uint32_t g, const float4 r[4]) {
+    float v[kBwdVals];
+#pragma unroll
+    for (int q = 0; q < kBwdVals; ++q) v[q] = 0.f;
+    bool contributed = false;
+    if (m) {
+      float alpha, tau, rho;
+      bool cl;
+      const int st = bwd_step(A, rf, r, T, &alpha, &tau, &rho, &cl);
+      if (st == 2) done = true;
+      if (st == 1) {
+        contributed = true;
+        const float w = alpha * T;
+        pz0 = fmaf(w, r[3].y, pz0);
+        pz1 = fmaf(w, r[3].z, pz1);
+        pz2 = fmaf(w, r[3].w, pz2);
+        pD = fmaf(w, tau, pD);
+        pW += w;
+        const float gzf = Gz[0] * r[3].y + Gz[1] * r[3].z + Gz[2] * r[3].w;
+        const float suf = (tot_f - (Gz[0] * pz0 + Gz[1] * pz1 + Gz[2] * pz2)) + Go * (W - pW) + GD * (D - pD);
+        const float dalpha = T * (gzf + Go + GD * tau) - suf / (1.f - alpha);
+        const float dtau = GD * w;
+        float dd2 = 0.f;
+        if (!cl) {
+          v[12] = dalpha * rho;
+          dd2 = -0.5f * dalpha * alpha;
+        }
+        const float mu[3] = {r[0].x, r[0].y, r[0].z};
+        const float M[9] = {r[0].w, r[1].x, r[1].y, r[1].z, r[1].w, r[2].x, r[2].y, r[2].z, r[2].w};
+        float g12[12];
+        response_grad(rf, mu, M, dtau, dd2, g12);
+#pragma unroll
+        for (int q = 0; q < 12; ++q) v[q] = g12[q];
+        v[13] = Gz[0] * w;
+        v[14] = Gz[1] * w;
+        v[15] = Gz[2] * w;
+        T = T * (1.f - alpha);
+      }
+    }
+    if (__any_sync(0xffffffffu, contributed)) {
+#pragma unroll
+      for (int q = 0; q < kBwdVals; ++q)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+      if (lane < kBwdVals) {
+        float mine = v[0];
+#pragma unroll
+        for (int q = 1; q < kBwdVals; ++q)
+          if (lane == q) mine = v[q];
+        atomicAdd(A.ws + (size_t)g * kBwdVals + lane, mine);
+      }
+    }
+  });
+}
+
+__global__ void __launch_bounds__(32) k_backward_lidar(const BwdArgs A) {
+  const int tile = (int)(blockIdx.x / A.chunks), chunk = (int)(blockIdx.x % A.chunks);
+  const int lane = threadIdx.x;
+  const int off0 = __ldg(A.tile_ray_off + tile), off1 = __ldg(A.tile_ray_off + tile + 1);
+  const int k = off0 + chunk * 32 + lane;
+  const bool live = k < off1;
+  if (__ballot_sync(0xffffffffu, live) == 0) return;
+  const int ray = live ? __ldg(A.tile_rays + k) : 0;
+  const int b = ray / A.n_az, j = ray % A.n_az;
+  // the ray exactly as k_render_lidar builds it
+  const float phi = live ? __ldg(A.ray_az + j) : 0.f, el = live ? __ldg(A.ray_el + (size_t)b * A.n_az) : 0.f;
+  double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
+  if (live) {
+    double Rm[9];
+    pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
+    double sa, ca, se, ce;
+    sincos((double)phi, &sa, &ca);
+    sincos((double)el, &se, &ce);
+    const double u[3] = {ce * ca, ce * sa, se};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
+  }
+  RayF rf;
+  split_ray(o, dd, rf);
+  __shared__ float s_a[32], s_b[32];
+  s_a[lane] = phi;
+  s_b[lane] = el;
+  __syncwarp();
+  const float pi_f = A.pi_f, two_pi_f = A.two_pi_f;
+  auto member = [&](const float4 bx, float p, float w) {  // k_render_lidar's column x beam test
+    bool col;
+    if (__fsub_rn(bx.y, bx.x) >= two_pi_f) {
+      col = true;
+    } else {
+      const float lo2 = bx.x < -pi_f ? __fadd_rn(bx.x, two_pi_f) : INFINITY;
+      const float hi2 = bx.y > pi_f ? __fsub_rn(bx.y, two_pi_f) : -INFINITY;
+      col = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
+    }
+    return col && bx.z <= w && w <= bx.w;
+  };
+  bwd_ray_pair_passes<true>(A, rf, live, ray, __ldg(A.ranges + tile), s_a, s_b, member);
+}
+
+template <int TP>
+__global__ void __launch_bounds__(TP* TP) k_backward_camera(const BwdArgs A) {
+  const CameraArgs& C = A.cam;
+  const int tile = blockIdx.x;
+  const int ty = tile / C.Wt, tx = tile % C.Wt;
+  const int i = tx * TP + (threadIdx.x % TP), j = ty * TP + (threadIdx.x / TP);
+  const bool inside = i < C.width && j < C.height;
+  double o[3] = {0, 0, 0}, d[3] = {0, 0, 0};
+  bool valid = false;
+  if (inside) {  // the pixel ray exactly as k_render_camera builds it
+    double dc[3];
+    valid = unproject(C, (double)i + 0.5, (double)j + 0.5, dc);
+    const double s = C.rolling ? ((double)j + 0.5) / (double)C.height : 0.0;
+    double R[9];
+    pose_at_d(C.pose, s, R, o);
+    if (valid)
+      for (int k = 0; k < 3; ++k) d[k] = R[3 * k] * dc[0] + R[3 * k + 1] * dc[1] + R[3 * k + 2] * dc[2];
+  }
+  RayF rf;
+  split_ray(o, d, rf);
+  __shared__ float s_a[TP * TP], s_b[TP * TP];
+  s_a[threadIdx.x] = (float)i + 0.5f;
+  s_b[threadIdx.x] = (float)j + 0.5f;
+  __syncwarp();
+  auto member = [&](const float4 bx, float pu, float pv) { return bx.x <= pu && pu <= bx.y && bx.z <= pv && pv <= bx.w; };
+  const int ray = inside ? j * C.width + i : 0;
+  const int w0 = threadIdx.x & ~31;
+  bwd_ray_pair_passes<false>(A, rf, inside && valid, ray, __ldg(A.ranges + tile), s_a + w0, s_b + w0, member);
+}
+
+// parameter chain (O16): M = diag(1/s) R(q^)^T -> (q, s); f = SH(v) -> SH coefficients
+__global__ void __launch_bounds__(256) k_backward_params(const float* __restrict__ ws, const float* __restrict__ quats,
+                                                         const float* __restrict__ scales,
+                                                         const float* __restrict__ view_dir, int ncoef, int64_t n,
+                                                         simuli_gaussian_grads out) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  float v[kBwdVals];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(ws) + g * 4 + c);
+    v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w;
+  }
+  for (int c = 0; c < 3; ++c) out.means[3 * g + c] = v[c];
+  out.opacity[g] = v[12];
+  const float4 q4 = __ldg(reinterpret_cast<const float4*>(quats) + g);
+  const float qn2 = q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w;
+  float gq[4] = {0.f, 0.f, 0.f, 0.f}, gs[3] = {0.f, 0.f, 0.f};
+  if (qn2 > 0.f && isfinite(qn2)) {
+    const float inv = rsqrtf(qn2);
+    const float q[4] = {q4.x * inv, q4.y * inv, q4.z * inv, q4.w * inv};
+    float R[9];
+    quat_rot(q, R);
+    float G[9];  // dL/dR[j][k] = dL/dM[k][j] / s_k
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float s = __ldg(scales + 3 * g + k);
+      float ds = 0.f;
+#pragma unroll
+      for (int jj = 0; jj < 3; ++jj) {
+        const float dm = v[3 + 3 * k + jj];
+        G[3 * jj + k] = dm / s;
+        ds -= dm * R[3 * jj + k] / (s * s);
+      }
+      gs[k] = ds;
+    }
+    const float w = q[0], x = q[1], y = q[2], z = q[3];
+    const float dq[4] = {
+        2.f * (-z * G[1] + y * G[2] + z * G[3] - x * G[5] - y * G[6] + x * G[7]),
+        2.f * (y * G[1] + z * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + z * G[6] + w * G[7] - 2.f * x * G[8]),
+        2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + z * G[5] - w * G[6] + z * G[7] - 2.f * y * G[8]),
+        2.f * (-2.f * z * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * z * G[4] + y * G[5] + x * G[6] + y * G[7])};
+    const float dot = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) gq[c] = (dq[c] - q[c] * dot) * inv;
+  }
+  reinterpret_cast<float4*>(out.quats)[g] = make_float4(gq[0], gq[1], gq[2], gq[3]);
+  for (int c = 0; c < 3; ++c) out.scales[3 * g + c] = gs[c];
+  float b[16];
+  sh_basis3(__ldg(view_dir + 3 * g), __ldg(view_dir + 3 * g + 1), __ldg(view_dir + 3 * g + 2), b);
+  float* o = out.sh + (size_t)g * ncoef * 3;
+  for (int k = 0; k < ncoef; ++k)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) o[3 * k + c] = b[k] * v[13 + c];
+}
+
+int32_t bwd_common_checks(const simuli_gaussians* G, const simuli_projected* proj, const uint32_t* ids,
+                          const int32_t* ranges, const simuli_project_params* P, const simuli_render_params* rp,
+                          const simuli_gaussian_grads* gout, void* ws, size_t ws_bytes, const char* what) {
+  if (!(G && proj && proj->record && ids && ranges && P && rp && gout && ws)) {
+    set_error("%s: NULL argument", what);
+    return SIMULI_ERR_INVALID_ARGUMENT;
+  }
+  if (!proj->view_dir) {
+    set_error("%s: proj->view_dir was not written (simuli_project with a view_dir buffer)", what);
+    return SIMULI_ERR_INVALID_ARGUMENT;
+  }
+  if (!(gout->means && gout->quats && gout->scales && gout->opacity && gout->sh)) {
+    set_error("%s: NULL gradient output", what);
+    return SIMULI_ERR_INVALID_ARGUMENT;
+  }
+  if (ws_bytes < (size_t)G->n * kBwdVals * sizeof(float) || reinterpret_cast<uintptr_t>(ws) % 16 != 0 ||
+      reinterpret_cast<uintptr_t>(gout->quats) % 16 != 0) {
+    set_error("%s: workspace too small / workspace or quats gradient not 16-byte aligned", what);
+    return SIMULI_ERR_INVALID_ARGUMENT;
+  }
+  if (rp->sh || G->actor_id) {
+    set_error("%s: per-ray SH / scene-graph particles have no backward (A31)", what);
+    return SIMULI_ERR_UNSUPPORTED;
+  }
+  if (G->sh_degree < 0 || G->sh_degree > 3) {
+    set_error("%s: sh_degree not in 0..3", what);
+    return SIMULI_ERR_UNSUPPORTED;
+  }
+  return SIMULI_OK;
+}
+
+void bwd_fill_common(BwdArgs& A, const simuli_projected* proj, const uint32_t* ids, const int32_t* ranges,
+                     const simuli_project_params* P, const simuli_render_params* rp, void* ws) {
+  A.record = reinterpret_cast<const float4*>(proj->record);
+  A.ids = ids;
+  A.ranges = reinterpret_cast<const int2*>(ranges);
+  A.pose = make_pose_interp_d(P->pose_start, P->pose_end);
+  A.alpha_min = rp->alpha_min; A.alpha_max = rp->alpha_max; A.T_min = rp->T_min;
+  A.ws = static_cast<float*>(ws);
+}
+
+int32_t bwd_params(const simuli_gaussians* G, const simuli_projected* proj, const simuli_gaussian_grads* gout,
+                   const float* ws, cudaStream_t st, const char* what) {
+  const int ncoef = (G->sh_degree + 1) * (G->sh_degree + 1);
+  if (G->n > 0)
+    k_backward_params<<<(unsigned)((G->n + 255) / 256), 256, 0, st>>>(ws, G->quats, G->scales, proj->view_dir,
+                                                                       ncoef, G->n, *gout);
+  return launch_check(what);
+}
+
+}  // namespace
+}  // namespace simuli
+
+extern "C" int32_t simuli_backward_workspace_size(int64_t n, size_t* bytes) {
+  using namespace simuli;
+  clear_error();
+  SIMULI_REQUIRE(n >= 0 && bytes, "simuli_backward_workspace_size: bad argument");
+  *bytes = (size_t)n * kBwdVals * sizeof(float);
+  return SIMULI_OK;
+}
+
+extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli_projected* proj,
+                                         const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                                         const simuli_project_params* P, const simuli_render_params* rp,
+                                         const simuli_lidar_grad_in* gin, simuli_gaussian_grads* gout,
+                                         void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace simuli;
+  clear_error();
+  const int32_t rc = bwd_common_checks(G, proj, sorted_ids, tile_ranges, P, rp, gout, workspace, workspace_bytes,
+                                       "simuli_backward_lidar");
+  if (rc != SIMULI_OK) return rc;
+  SIMULI_REQUIRE(gin, "simuli_backward_lidar: NULL grad_in");
+  SIMULI_REQUIRE(P->kind == SIMULI_SENSOR_LIDAR && P->lidar && P->tiling, "simuli_backward_lidar: needs LiDAR params");
+  if (P->lidar->beam_divergence_rad > 0.f) {
+    set_error("simuli_backward_lidar: beam divergence has no backward (A31)");
+    return SIMULI_ERR_UNSUPPORTED;
+  }
+  const simuli_tiling_dev& T = *P->tiling;
+  SIMULI_REQUIRE(T.tile_ray_offsets && T.tile_rays && T.ray_az && T.ray_el && T.ray_s && T.n_tiles >= 1,
+                 "simuli_backward_lidar: incomplete device tiling");
+  BwdArgs A{};
+  bwd_fill_common(A, proj, sorted_ids, tile_ranges, P, rp, workspace);
+  A.tile_ray_off = T.tile_ray_offsets; A.tile_rays = T.tile_rays;
+  A.ray_az = T.ray_az; A.ray_el = T.ray_el; A.ray_s = T.ray_s;
+  A.n_az = T.n_azimuth;
+  A.chunks = (T.max_rays_in_tile + 31) / 32;
+  A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f;
+  A.near_tau = P->lidar->min_range_m;
+  A.g_feat = gin->zeta; A.g_opacity = gin->opacity; A.g_daccum = gin->depth_accum; A.g_depth = gin->depth;
+  A.g_intensity = gin->intensity; A.g_raydrop = gin->raydrop;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (G->n == 0) return SIMULI_OK;
+  cudaMemsetAsync(workspace, 0, (size_t)G->n * kBwdVals * sizeof(float), st);
+  k_backward_lidar<<<(unsigned)(T.n_tiles * A.chunks), 32, 0, st>>>(A);
+  const int32_t lc = launch_check("simuli_backward_lidar");
+  if (lc != SIMULI_OK) return lc;
+  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), st, "simuli_backward_lidar");
+}
+
+extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simuli_projected* proj,
+                                          const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                                          const simuli_project_params* P, const simuli_render_params* rp,
+                                          const simuli_camera_grad_in* gin, simuli_gaussian_grads* gout,
+                                          void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace simuli;
+  clear_error();
+  const int32_t rc = bwd_common_checks(G, proj, sorted_ids, tile_ranges, P, rp, gout, workspace, workspace_bytes,
+                                       "simuli_backward_camera");
+  if (rc != SIMULI_OK) return rc;
+  SIMULI_REQUIRE(gin, "simuli_backward_camera: NULL grad_in");
+  SIMULI_REQUIRE(P->kind == SIMULI_SENSOR_CAMERA && P->camera, "simuli_backward_camera: needs camera params");
+  const simuli_camera& C = *P->camera;
+  if (C.tile_px != 8 && C.tile_px != 16) {
+    set_error("simuli_backward_camera: tile_px %d not supported (8 or 16)", C.tile_px);
+    return SIMULI_ERR_UNSUPPORTED;
+  }
+  BwdArgs A{};
+  bwd_fill_common(A, proj, sorted_ids, tile_ranges, P, rp, workspace);
+  CameraArgs& K = A.cam;
+  K.model = C.model; K.width = C.width; K.height = C.height; K.rolling = C.rolling_shutter; K.tile_px = C.tile_px;
+  K.Wt = (C.width + C.tile_px - 1) / C.tile_px;
+  K.fx = C.fx; K.fy = C.fy; K.cx = C.cx; K.cy = C.cy;
+  for (int i = 0; i < 5; ++i) K.k[i] = C.k[i];
+  K.max_theta = C.max_theta_rad;
+  K.pose = A.pose;
+  A.near_tau = C.near_m;
+  A.g_feat = gin->rgb; A.g_opacity = gin->opacity; A.g_daccum = gin->depth_accum; A.g_depth = gin->depth;
+  const int Ht = (C.height + C.tile_px - 1) / C.tile_px;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (G->n == 0) return SIMULI_OK;
+  cudaMemsetAsync(workspace, 0, (size_t)G->n * kBwdVals * sizeof(float), st);
+  const unsigned blocks = (unsigned)(K.Wt * Ht);
+  if (C.tile_px == 8) k_backward_camera<8><<<blocks, 64, 0, st>>>(A);
+  else k_backward_camera<16><<<blocks, 256, 0, st>>>(A);
+  const int32_t lc = launch_check("simuli_backward_camera");
+  if (lc != SIMULI_OK) return lc;
+  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), st, "simuli_backward_camera");
+}

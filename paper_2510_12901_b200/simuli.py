@@ -26,7 +26,8 @@ RECORD_FLOATS = 20
 
 EXPORTED = ["simuli_last_error", "simuli_abi_version", "simuli_build_tiles", "simuli_project",
             "simuli_bin_sort_workspace_size", "simuli_bin_sort", "simuli_render_lidar", "simuli_render_camera",
-            "simuli_compose_camera"]
+            "simuli_compose_camera", "simuli_backward_workspace_size", "simuli_backward_lidar",
+            "simuli_backward_camera"]
 
 f32p, i32p, f64p = C.POINTER(C.c_float), C.POINTER(C.c_int32), C.POINTER(C.c_double)
 
@@ -85,6 +86,18 @@ class Gaussians(C.Structure):
                 ("actor_id", C.c_void_p), ("actor_pose", C.c_void_p), ("n_actors", C.c_int32)]
 
 
+class LidarGradIn(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("zeta", "opacity", "depth_accum", "depth", "intensity", "raydrop")]
+
+
+class CameraGradIn(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("rgb", "opacity", "depth_accum", "depth")]
+
+
+class GaussianGrads(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("means", "quats", "scales", "opacity", "sh")]
+
+
 class CameraCompose(C.Structure):
     _fields_ = [("env_map", C.c_void_p), ("env_h", C.c_int32), ("env_w", C.c_int32), ("grid", C.c_void_p),
                 ("grid_h", C.c_int32), ("grid_w", C.c_int32), ("grid_d", C.c_int32)]
@@ -107,7 +120,7 @@ class ProjectParams(C.Structure):
 
 class Projected(C.Structure):
     _fields_ = [("record", C.c_void_p), ("tile_rect", C.c_void_p), ("depth_key", C.c_void_p),
-                ("tile_count", C.c_void_p)]
+                ("tile_count", C.c_void_p), ("view_dir", C.c_void_p)]
 
 
 class RenderParams(C.Structure):
@@ -150,6 +163,11 @@ def load():
     L.simuli_render_camera.argtypes = [C.POINTER(Projected), C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(CameraOut),
                                        C.c_void_p]
+    L.simuli_backward_workspace_size.argtypes = [C.c_int64, C.POINTER(C.c_size_t)]
+    for nm, gin in (("simuli_backward_lidar", LidarGradIn), ("simuli_backward_camera", CameraGradIn)):
+        getattr(L, nm).argtypes = [C.POINTER(Gaussians), C.POINTER(Projected), C.c_void_p, C.c_void_p,
+                                   C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(gin),
+                                   C.POINTER(GaussianGrads), C.c_void_p, C.c_size_t, C.c_void_p]
     L.simuli_compose_camera.argtypes = [C.POINTER(ProjectParams), C.POINTER(CameraCompose), C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.c_void_p]
     for name in EXPORTED:
@@ -248,6 +266,38 @@ def simuli_compose_camera(params, env, grid, rgb_fg, opacity, rgb_out, stream=No
                                         _stream(stream)))
 
 
+def simuli_backward_workspace_size(n):
+    b = C.c_size_t(0)
+    _check(load().simuli_backward_workspace_size(int(n), C.byref(b)))
+    return int(b.value)
+
+
+def _grad_structs(frame, grads, names, gin_cls):
+    import torch
+    sc = frame.scene
+    out = {k: torch.empty_like(sc[k]) for k in ("means", "quats", "scales", "opacity", "sh")}
+    gin = gin_cls(*[_ptr(grads.get(k)) if grads.get(k) is not None else None for k in names])
+    gout = GaussianGrads(*[_ptr(out[k]) for k in ("means", "quats", "scales", "opacity", "sh")])
+    return out, gin, gout
+
+
+def simuli_backward(frame, grads, stream=None):
+    """Backward of the frame's last forward (A31): grads = upstream gradients by output
+    name (device float32; missing = 0).  Returns the particle parameter gradients."""
+    lidar = isinstance(frame, LidarRenderer)
+    names = ("zeta", "opacity", "depth_accum", "depth", "intensity", "raydrop") if lidar else \
+        ("rgb", "opacity", "depth_accum", "depth")
+    grads = {k: v.contiguous() for k, v in grads.items() if v is not None}
+    out, gin, gout = _grad_structs(frame, grads, names, LidarGradIn if lidar else CameraGradIn)
+    ws = frame._bwd_workspace()
+    fn = load().simuli_backward_lidar if lidar else load().simuli_backward_camera
+    _check(fn(C.byref(frame.gauss), C.byref(frame.projected), _ptr(frame.sorted_ids), _ptr(frame.tile_ranges),
+              C.byref(frame.params), C.byref(frame.rparams), C.byref(gin), C.byref(gout), _ptr(ws), ws.numel(),
+              _stream(stream)))
+    frame._keep_grads = grads  # alive until the enqueued work has run
+    return out
+
+
 def simuli_render_camera(proj, sorted_ids, tile_ranges, params, rparams, out: CameraOut, stream=None,
                          tile_order=None):
     _check(load().simuli_render_camera(C.byref(proj), _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order),
@@ -309,6 +359,23 @@ class _Frame:
 
     def project(self, stream=None):
         simuli_project(self.gauss, self.params, self.projected, stream)
+
+    def requires_grad(self, flag=True):
+        """Write the per-particle SH view directions the backward needs (A31)."""
+        import torch
+        self.view_dir = torch.zeros((max(self.n, 1), 3), dtype=torch.float32, device=self.device) if flag else None
+        self.projected.view_dir = _ptr(self.view_dir).value if flag else None
+
+    def _bwd_workspace(self):
+        import torch
+        need = simuli_backward_workspace_size(self.n)
+        if getattr(self, "_bws", None) is None or self._bws.numel() < need:
+            self._bws = torch.empty(max(need, 16), dtype=torch.uint8, device=self.device)
+        return self._bws
+
+    def backward(self, grads, stream=None):
+        """Gradients of the particle parameters from upstream output gradients (A31)."""
+        return simuli_backward(self, grads, stream)
 
     keep_keys = True  # also write the u64 (tile | depth) keys (tests); the renderer needs only ids
 

@@ -704,3 +704,103 @@ def test_per_ray_sh_camera_parity(SM, oracle_mod):
     err = np.abs(c.out["rgb"].cpu().numpy() - ref2["feat"])[ok2].max()
     print("camera per-ray SH max |gpu - oracle|", err)
     assert err < TOL_FEAT
+
+
+# ------------------------------------------------------------------ backward (O15, O16; A31)
+def _compare_grads(gpu, ref, what):
+    for k in ("means", "quats", "scales", "opacity", "sh"):
+        a = gpu[k].cpu().numpy().astype(np.float64).reshape(ref[k].shape)
+        b = ref[k]
+        scale = np.abs(b).max()
+        assert scale > 0, (what, k)
+        err = np.abs(a - b)
+        print(f"{what} d{k}: max |gpu - oracle| / max |oracle| = {err.max() / scale:.2e}")
+        assert err.max() <= 1e-3 * scale, (what, k, err.max(), scale)
+        big = np.abs(b) > 1e-2 * scale
+        assert (err[big] <= 1e-3 * np.abs(b[big]) + 1e-5 * scale).mean() > 0.999, (what, k)
+
+
+def _upstream(R, seed, lidar, mask):
+    rng = np.random.default_rng(seed)
+    m = mask.astype(np.float64)
+    g = {"opacity": rng.normal(size=R) * m, "depth_accum": 0.05 * rng.normal(size=R) * m,
+         "depth": 0.05 * rng.normal(size=R) * m}
+    if lidar:
+        g.update({"zeta": rng.normal(size=(R, 3)) * m[:, None], "intensity": rng.normal(size=R) * m,
+                  "raydrop": rng.normal(size=R) * m})
+    else:
+        g["rgb"] = rng.normal(size=(R, 3)) * m[:, None]
+    return g
+
+
+def _dev(g):
+    return {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).cuda() for k, v in g.items()}
+
+
+@pytest.mark.parametrize("config", ["A", "B-sub"])
+def test_backward_lidar_parity(SM, oracle_mod, config):
+    """GPU backward vs the oracle's O15/O16 on the GPU's own records, lists and rays (tier 1);
+    rays the tier-1 forward flags near a threshold get zero upstream gradient on both sides.
+    Config A also tier 2 (the oracle's own forward)."""
+    O = oracle_mod
+    if config == "B-sub":
+        cfg, scene = S.lidar_config("B"), S.scene_for("B", n=200_000)
+    else:
+        cfg, scene = S.lidar_config(config), S.scene_for(config)
+    r = SM.LidarRenderer(cfg, SM.to_device_scene(scene))
+    r.requires_grad(True)
+    r.want_ray_od(True)
+    r.scan(sync_capacity=True)
+    torch.cuda.synchronize()
+    t = O.Tiling(cfg)
+    _, ids, ranges = sorted_lists(r)
+    rec = gpu_records(r)
+    od = r.out["ray_od"].cpu().numpy()
+    fwd = O.composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, wrap=1, near=cfg.min_range,
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4},
+                      pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    ok = fwd["flag"] == 0
+    R = od.shape[0]
+    g = _upstream(R, 5, True, ok)
+    got = r.backward(_dev(g))
+    torch.cuda.synchronize()
+    gz, go, gd = O.fold_upstream(fwd, g, lidar=True)
+    d = O.backward_composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, gz, go, gd, wrap=1,
+                             near=cfg.min_range, pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    ref = O.backward_params(scene, {"viewdir": r.view_dir.cpu().numpy().astype(np.float64)}, d)
+    _compare_grads(got, ref, f"{config} tier 1")
+    if config == "A":
+        ref2f = O.render_lidar(scene, cfg, tiling=t, flag_eps=LIDAR_EPS)
+        ok2 = (ref2f["flag"] == 0) & ok
+        g2 = _upstream(R, 6, True, ok2)
+        got2 = r.backward(_dev(g2))
+        torch.cuda.synchronize()
+        ref2 = O.backward_lidar(scene, cfg, g2, tiling=t)
+        _compare_grads(got2, ref2, f"{config} tier 2")
+
+
+def test_backward_camera_parity(SM, oracle_mod):
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    scene = S.corridor_scene(21, 40000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    c = SM.CameraRenderer(cam, SM.to_device_scene(scene))
+    c.requires_grad(True)
+    c.want_ray_od(True)
+    c.frame(sync_capacity=True)
+    torch.cuda.synchronize()
+    _, ids, ranges = sorted_lists(c)
+    rays = O.camera_rays(cam)
+    rec = gpu_records(c)
+    od = c.out["ray_od"].cpu().numpy()
+    fwd = O.composite(rec, ids, ranges, rays["tile"], rays["u"], rays["v"], od, wrap=0, near=cam.near,
+                      ray_valid=rays["valid"], flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4,
+                                                         "tau": 1e-4})
+    ok = fwd["flag"] == 0
+    g = _upstream(od.shape[0], 7, False, ok)
+    got = c.backward(_dev(g))
+    torch.cuda.synchronize()
+    gz, go, gd = O.fold_upstream(fwd, g, lidar=False)
+    d = O.backward_composite(rec, ids, ranges, rays["tile"], rays["u"], rays["v"], od, gz, go, gd, wrap=0,
+                             near=cam.near, ray_valid=rays["valid"])
+    ref = O.backward_params(scene, {"viewdir": c.view_dir.cpu().numpy().astype(np.float64)}, d)
+    _compare_grads(got, ref, "D-small tier 1")

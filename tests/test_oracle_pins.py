@@ -944,3 +944,98 @@ def test_per_ray_sh_closed_forms(oracle_mod):
         ref = pr["opacity"][r] * O.sh_eval(c.astype(np.float32).astype(np.float64), d)
         assert np.allclose(pr["feat"][r], ref, rtol=0, atol=1e-12)
     assert np.abs(pp["feat"] - pr["feat"])[hit].max() > 1e-3  # the two readings differ
+
+
+# ------------------------------------------------------------------ backward (O15, O16; A31)
+def _bwd_setup(O, seed=3, n=120, deg0=True):
+    cfg = S.lidar_config("tiny")
+    sc = S.scene_for("tiny", seed=seed, n=n)
+    if deg0:  # constant features: the SH view direction carries no gradient (A31)
+        sc["sh"] = np.ascontiguousarray(sc["sh"][:, :1])
+    fwd = O.render_lidar(sc, cfg)
+    R = fwd["opacity"].shape[0]
+    rng = np.random.default_rng(seed + 100)
+    g = {"zeta": rng.normal(size=(R, 3)), "opacity": rng.normal(size=R), "depth_accum": rng.normal(size=R) * 0.1,
+         "depth": rng.normal(size=R) * 0.1, "intensity": rng.normal(size=R), "raydrop": rng.normal(size=R)}
+    return cfg, sc, g
+
+
+def _loss(O, sc, cfg, g):
+    f = O.render_lidar(sc, cfg)
+    return (np.sum(g["zeta"] * f["feat"]) + np.sum(g["opacity"] * f["opacity"]) +
+            np.sum(g["depth_accum"] * f["depth_accum"]) + np.sum(g["depth"] * f["depth"]) +
+            np.sum(g["intensity"] * f["intensity"]) + np.sum(g["raydrop"] * f["raydrop"]))
+
+
+def test_backward_vs_finite_differences(oracle_mod):
+    """O15/O16 against central differences of the oracle's own forward (a different
+    computation: the derivative is fixed by the forward map).  The particles with the
+    largest gradients are perturbed in every parameter (mean, quaternion, scale, opacity);
+    the step is small enough that no membership / skip / termination decision flips for
+    almost all of them."""
+    O = oracle_mod
+    cfg, sc, g = _bwd_setup(O)
+    b = O.backward_lidar(sc, cfg, g)
+    top = np.argsort(-np.abs(b["opacity"]))[:6]
+    checked = bad = 0
+    for i in top:
+        for key, h, dims in (("means", 2e-4, 3), ("quats", 2e-4, 4), ("scales", 1e-4, 3), ("opacity", 1e-4, 1)):
+            for c in range(dims):
+                vals = []
+                deltas = []
+                for sgn in (1, -1):
+                    s2 = {k: v.copy() for k, v in sc.items()}
+                    arr = s2[key].reshape(sc["means"].shape[0], -1)
+                    x0 = np.float32(arr[i, c])
+                    arr[i, c] = np.float32(x0 + sgn * h * max(1.0, abs(float(x0))))
+                    deltas.append(float(arr[i, c]) - float(x0))
+                    vals.append(_loss(O, s2, cfg, g))
+                fd = (vals[0] - vals[1]) / (deltas[0] - deltas[1])
+                an = b[key].reshape(sc["means"].shape[0], -1)[i, c]
+                checked += 1
+                if abs(fd - an) > 2e-3 * max(1.0, abs(an)):
+                    bad += 1
+                    print("mismatch", i, key, c, fd, an)
+    assert checked == 6 * 11
+    assert bad <= 2, bad  # a decision flip inside the stencil is possible but rare
+
+
+def test_backward_sh_exact_linearity(oracle_mod):
+    """zeta is linear in the SH coefficients: L(c + e_k) - L(c) = dL/dc_k exactly (up to
+    rounding) for a loss linear in zeta, on the particles with the largest SH gradients."""
+    O = oracle_mod
+    cfg, sc, g = _bwd_setup(O, seed=4, deg0=False)
+    g["raydrop"][:] = 0.0  # the sigmoid of the ray-drop decode is not linear in zeta
+    b = O.backward_lidar(sc, cfg, g)
+    L0 = _loss(O, sc, cfg, g)
+    top = np.argsort(-np.abs(b["sh"]).sum((1, 2)))[:3]
+    for i in top:
+        for k in (0, 1, 5, 15):
+            for c in range(3):
+                s2 = {kk: v.copy() for kk, v in sc.items()}
+                s2["sh"][i, k, c] += np.float32(0.5)
+                d = float(s2["sh"][i, k, c]) - float(sc["sh"][i, k, c])
+                assert abs((_loss(O, s2, cfg, g) - L0) / d - b["sh"][i, k, c]) < 1e-9 * max(1, abs(b["sh"][i, k, c]))
+
+
+def test_backward_transmittance_identity(oracle_mod):
+    """Euler-type identity: scaling every opacity sigma -> (1 + e) sigma changes
+    sum_r omega_r = sum_r (1 - T_final,r) at rate sum_i sigma_i dL/dsigma_i (G_omega = 1);
+    the rate is taken from T_final (omega = 1 - T, Eq. 1), not from the backward."""
+    O = oracle_mod
+    cfg = S.lidar_config("tiny")
+    sc = S.scene_for("tiny", seed=9, n=150)
+    sc["opacity"] = (sc["opacity"] * 0.5).astype(np.float32)  # no clamping at alpha_max
+    fwd = O.render_lidar(sc, cfg)
+    R = fwd["opacity"].shape[0]
+    b = O.backward_lidar(sc, cfg, {"opacity": np.ones(R)})
+    e = 1e-4
+    s2 = dict(sc)
+    s2["opacity"] = (sc["opacity"].astype(np.float64) * (1 + e)).astype(np.float32)
+    s3 = dict(sc)
+    s3["opacity"] = (sc["opacity"].astype(np.float64) * (1 - e)).astype(np.float32)
+    f2, f3 = O.render_lidar(s2, cfg), O.render_lidar(s3, cfg)
+    fd = (np.sum(1 - f2["T_final"]) - np.sum(1 - f3["T_final"])) / (2 * e)
+    an = np.sum(sc["opacity"].astype(np.float64) * b["opacity"])
+    assert np.allclose(f2["opacity"], 1 - f2["T_final"], atol=1e-12)  # omega = 1 - T (Eq. 1)
+    assert abs(fd - an) < 1e-3 * max(1.0, abs(an)), (fd, an)
