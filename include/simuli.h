@@ -345,10 +345,14 @@ int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorte
  * (1 / (1 + exp(zeta_1 - zeta_2))); camera rgb (c_f), opacity, depth_accum, depth. */
 typedef struct {
   const float *zeta, *opacity, *depth_accum, *depth, *intensity, *raydrop;
+  /* optional: the forward's own zeta [R][3], opacity [R], depth_accum [R] outputs of this
+     frame; given all three, the backward skips its first list pass (totals) */
+  const float *fwd_zeta, *fwd_opacity, *fwd_depth_accum;
 } simuli_lidar_grad_in;
 
 typedef struct {
   const float *rgb, *opacity, *depth_accum, *depth;
+  const float *fwd_rgb, *fwd_opacity, *fwd_depth_accum; /* optional, as above */
 } simuli_camera_grad_in;
 
 /* Per-particle parameter gradients (device, caller-allocated, n entries each; overwritten,

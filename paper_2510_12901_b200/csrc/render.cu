@@ -982,7 +982,9 @@ struct BwdArgs {
   PoseInterpD pose;
   float near_tau, alpha_min, alpha_max, T_min;
   const float *g_feat, *g_opacity, *g_daccum, *g_depth, *g_intensity, *g_raydrop;
+  const float *f_feat, *f_opacity, *f_daccum;  // forward totals (optional: skip pass 1)
   float* ws;  // [n][16]
+  int64_t n;
 };
 
 constexpr int kBwdVals = 16;
@@ -1061,52 +1063,104 @@ __device__ __forceinline__ int bwd_step(const BwdArgs& A, const RayF& rf, const 
 // on all lanes (it may use warp collectives); the walk ends once every lane is done.
 template <typename Member, typename Body>
 __device__ __forceinline__ void walk_list(const BwdArgs& A, int2 rg, const bool& done, const float* ra,
-                                          const float* rb, Member member, Body body) {
+                                          const float* rb, float4 (*srec)[5], Member member, Body body) {
   const int lane = threadIdx.x & 31;
   for (int base = rg.x; base < rg.y; base += 32) {
     const uint32_t open = __ballot_sync(0xffffffffu, !done);
     if (open == 0u) return;
     const int i = base + lane;
     uint32_t g = 0, mm = 0;
-    float4 q[5];
+    float4 q[5] = {};
+    __syncwarp();  // the previous batch's records are no longer read
     if (i < rg.y) {
       g = __ldg(A.ids + i);
+#ifdef SIMULI_BWD_CHECK
+      if ((int64_t)g >= A.n) {
+        printf("bwd: entry %d id %u >= n %lld (range %d..%d)\n", i, g, (long long)A.n, rg.x, rg.y);
+        __trap();
+      }
+#endif
       const float4* src = A.record + (size_t)g * 5;
 #pragma unroll
       for (int c = 0; c < 5; ++c) q[c] = __ldg(src + c);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) srec[lane][c] = q[c];
       for (uint32_t o = open; o; o &= o - 1u) {
         const int r = __ffs(o) - 1;
         mm |= (uint32_t)member(q[4], ra[r], rb[r]) << r;
       }
     }
+    __syncwarp();
     uint32_t ent = __ballot_sync(0xffffffffu, mm != 0u);
     while (ent) {
       const int k = __ffs(ent) - 1;
       ent &= ent - 1u;
       const uint32_t mk = __shfl_sync(0xffffffffu, mm, k);  // all lanes (not under a short circuit)
+      const uint32_t gk = __shfl_sync(0xffffffffu, g, k);
       const bool m = !done && ((mk >> lane) & 1u);
       if (!__any_sync(0xffffffffu, m)) continue;
       float4 r[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        r[c] = make_float4(__shfl_sync(0xffffffffu, q[c].x, k), __shfl_sync(0xffffffffu, q[c].y, k),
-                           __shfl_sync(0xffffffffu, q[c].z, k), __shfl_sync(0xffffffffu, q[c].w, k));
-      body(m, __shfl_sync(0xffffffffu, g, k), r);
+      for (int c = 0; c < 4; ++c) r[c] = srec[k][c];
+      body(m, gk, r);
       if (__all_sync(0xffffffffu, done)) return;
     }
   }
+}
+
+// Sum of 16 values over the warp as a reduce-scatter butterfly (16 shuffles instead of
+// 5 x 16): afterwards lanes 2i and 2i + 1 hold the total of value i' where i' is lane's
+// bits 4..1 read as (8, 4, 2, 1).
+__device__ __forceinline__ float warp_reduce16(float v[16], int lane) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const bool up = lane & 16;
+    const float send = up ? v[j] : v[j + 8];
+    const float keep = up ? v[j + 8] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool up = lane & 8;
+    const float send = up ? v[j] : v[j + 4];
+    const float keep = up ? v[j + 4] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const bool up = lane & 4;
+    const float send = up ? v[j] : v[j + 2];
+    const float keep = up ? v[j + 2] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool up = lane & 2;
+    const float send = up ? v[0] : v[1];
+    const float keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
 // The two passes of one warp whose lanes hold rays (LiDAR / camera: the same tile) over the
 // tile's list; member(bx) is the lane's A12 box test.
 template <bool LIDAR, typename Member>
 __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF& rf, bool live, int ray,
-                                                    int2 rg, const float* ra, const float* rb, Member member) {
+                                                    int2 rg, const float* ra, const float* rb, float4 (*srec)[5],
+                                                    Member member) {
   const int lane = threadIdx.x & 31;
   // ---- pass 1: totals
   float T = 1.f, z0 = 0.f, z1 = 0.f, z2 = 0.f, D = 0.f, W = 0.f;
   bool done = !live;
-  walk_list(A, rg, done, ra, rb, member, [&](bool m, uint32_t, const float4 r[4]) {
+  if (A.f_feat) {  // the forward's own totals of this frame
+    if (live) {
+      z0 = __ldg(A.f_feat + 3 * (size_t)ray);
+      z1 = __ldg(A.f_feat + 3 * (size_t)ray + 1);
+      z2 = __ldg(A.f_feat + 3 * (size_t)ray + 2);
+      W = __ldg(A.f_opacity + ray);
+      D = __ldg(A.f_daccum + ray);
+    }
+  } else walk_list(A, rg, done, ra, rb, srec, member, [&](bool m, uint32_t, const float4 r[4]) {
     if (!m) return;
     float alpha, tau, rho;
     bool cl;
@@ -1152,7 +1206,7 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
   float pz0 = 0.f, pz1 = 0.f, pz2 = 0.f, pD = 0.f, pW = 0.f;
   T = 1.f;
   done = !live;
-  walk_list(A, rg, done, ra, rb, member, [&](bool m, uint32_t g, const float4 r[4]) {
+  walk_list(A, rg, done, ra, rb, srec, member, [&](bool m, uint32_t g, const float4 r[4]) {
     float v[kBwdVals];
 #pragma unroll
     for (int q = 0; q < kBwdVals; ++q) v[q] = 0.f;
@@ -1192,16 +1246,10 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
       }
     }
     if (__any_sync(0xffffffffu, contributed)) {
-#pragma unroll
-      for (int q = 0; q < kBwdVals; ++q)
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
-      if (lane < kBwdVals) {
-        float mine = v[0];
-#pragma unroll
-        for (int q = 1; q < kBwdVals; ++q)
-          if (lane == q) mine = v[q];
-        atomicAdd(A.ws + (size_t)g * kBwdVals + lane, mine);
+      const float tot = warp_reduce16(v, lane);
+      if (!(lane & 1)) {
+        const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+        atomicAdd(A.ws + (size_t)g * kBwdVals + q, tot);
       }
     }
   });
@@ -1247,15 +1295,20 @@ __global__ void __launch_bounds__(32) k_backward_lidar(const BwdArgs A) {
     }
     return col && bx.z <= w && w <= bx.w;
   };
-  bwd_ray_pair_passes<true>(A, rf, live, ray, __ldg(A.ranges + tile), s_a, s_b, member);
+  __shared__ float4 s_rec[32][5];
+  bwd_ray_pair_passes<true>(A, rf, live, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, member);
 }
 
+// one warp per (tile, strip of 32 pixels): TP x TP tiles have TP * TP / 32 strips
 template <int TP>
-__global__ void __launch_bounds__(TP* TP) k_backward_camera(const BwdArgs A) {
+__global__ void __launch_bounds__(32) k_backward_camera(const BwdArgs A) {
+  constexpr int STRIPS = TP * TP / 32;
   const CameraArgs& C = A.cam;
-  const int tile = blockIdx.x;
+  const int tile = (int)(blockIdx.x / STRIPS), strip = (int)(blockIdx.x % STRIPS);
+  const int lane = threadIdx.x;
   const int ty = tile / C.Wt, tx = tile % C.Wt;
-  const int i = tx * TP + (threadIdx.x % TP), j = ty * TP + (threadIdx.x / TP);
+  const int idx = strip * 32 + lane;
+  const int i = tx * TP + (idx % TP), j = ty * TP + (idx / TP);
   const bool inside = i < C.width && j < C.height;
   double o[3] = {0, 0, 0}, d[3] = {0, 0, 0};
   bool valid = false;
@@ -1268,16 +1321,17 @@ __global__ void __launch_bounds__(TP* TP) k_backward_camera(const BwdArgs A) {
     if (valid)
       for (int k = 0; k < 3; ++k) d[k] = R[3 * k] * dc[0] + R[3 * k + 1] * dc[1] + R[3 * k + 2] * dc[2];
   }
+  if (__ballot_sync(0xffffffffu, inside && valid) == 0u) return;
   RayF rf;
   split_ray(o, d, rf);
-  __shared__ float s_a[TP * TP], s_b[TP * TP];
-  s_a[threadIdx.x] = (float)i + 0.5f;
-  s_b[threadIdx.x] = (float)j + 0.5f;
+  __shared__ float s_a[32], s_b[32];
+  __shared__ float4 s_rec[32][5];
+  s_a[lane] = (float)i + 0.5f;
+  s_b[lane] = (float)j + 0.5f;
   __syncwarp();
   auto member = [&](const float4 bx, float pu, float pv) { return bx.x <= pu && pu <= bx.y && bx.z <= pv && pv <= bx.w; };
   const int ray = inside ? j * C.width + i : 0;
-  const int w0 = threadIdx.x & ~31;
-  bwd_ray_pair_passes<false>(A, rf, inside && valid, ray, __ldg(A.ranges + tile), s_a + w0, s_b + w0, member);
+  bwd_ray_pair_passes<false>(A, rf, inside && valid, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, member);
 }
 
 // parameter chain (O16): M = diag(1/s) R(q^)^T -> (q, s); f = SH(v) -> SH coefficients
@@ -1368,7 +1422,8 @@ int32_t bwd_common_checks(const simuli_gaussians* G, const simuli_projected* pro
 }
 
 void bwd_fill_common(BwdArgs& A, const simuli_projected* proj, const uint32_t* ids, const int32_t* ranges,
-                     const simuli_project_params* P, const simuli_render_params* rp, void* ws) {
+                     const simuli_project_params* P, const simuli_render_params* rp, void* ws, int64_t n) {
+  A.n = n;
   A.record = reinterpret_cast<const float4*>(proj->record);
   A.ids = ids;
   A.ranges = reinterpret_cast<const int2*>(ranges);
@@ -1417,7 +1472,7 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
   SIMULI_REQUIRE(T.tile_ray_offsets && T.tile_rays && T.ray_az && T.ray_el && T.ray_s && T.n_tiles >= 1,
                  "simuli_backward_lidar: incomplete device tiling");
   BwdArgs A{};
-  bwd_fill_common(A, proj, sorted_ids, tile_ranges, P, rp, workspace);
+  bwd_fill_common(A, proj, sorted_ids, tile_ranges, P, rp, workspace, G->n);
   A.tile_ray_off = T.tile_ray_offsets; A.tile_rays = T.tile_rays;
   A.ray_az = T.ray_az; A.ray_el = T.ray_el; A.ray_s = T.ray_s;
   A.n_az = T.n_azimuth;
@@ -1426,13 +1481,16 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
   A.near_tau = P->lidar->min_range_m;
   A.g_feat = gin->zeta; A.g_opacity = gin->opacity; A.g_daccum = gin->depth_accum; A.g_depth = gin->depth;
   A.g_intensity = gin->intensity; A.g_raydrop = gin->raydrop;
+  if (gin->fwd_zeta && gin->fwd_opacity && gin->fwd_depth_accum) {
+    A.f_feat = gin->fwd_zeta; A.f_opacity = gin->fwd_opacity; A.f_daccum = gin->fwd_depth_accum;
+  }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (G->n == 0) return SIMULI_OK;
   cudaMemsetAsync(workspace, 0, (size_t)G->n * kBwdVals * sizeof(float), st);
   k_backward_lidar<<<(unsigned)(T.n_tiles * A.chunks), 32, 0, st>>>(A);
   const int32_t lc = launch_check("simuli_backward_lidar");
   if (lc != SIMULI_OK) return lc;
-  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), st, "simuli_backward_lidar");
+  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), st, "simuli_backward_lidar (params)");
 }
 
 extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simuli_projected* proj,
@@ -1453,7 +1511,7 @@ extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simul
     return SIMULI_ERR_UNSUPPORTED;
   }
   BwdArgs A{};
-  bwd_fill_common(A, proj, sorted_ids, tile_ranges, P, rp, workspace);
+  bwd_fill_common(A, proj, sorted_ids, tile_ranges, P, rp, workspace, G->n);
   CameraArgs& K = A.cam;
   K.model = C.model; K.width = C.width; K.height = C.height; K.rolling = C.rolling_shutter; K.tile_px = C.tile_px;
   K.Wt = (C.width + C.tile_px - 1) / C.tile_px;
@@ -1463,14 +1521,17 @@ extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simul
   K.pose = A.pose;
   A.near_tau = C.near_m;
   A.g_feat = gin->rgb; A.g_opacity = gin->opacity; A.g_daccum = gin->depth_accum; A.g_depth = gin->depth;
+  if (gin->fwd_rgb && gin->fwd_opacity && gin->fwd_depth_accum) {
+    A.f_feat = gin->fwd_rgb; A.f_opacity = gin->fwd_opacity; A.f_daccum = gin->fwd_depth_accum;
+  }
   const int Ht = (C.height + C.tile_px - 1) / C.tile_px;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (G->n == 0) return SIMULI_OK;
   cudaMemsetAsync(workspace, 0, (size_t)G->n * kBwdVals * sizeof(float), st);
-  const unsigned blocks = (unsigned)(K.Wt * Ht);
-  if (C.tile_px == 8) k_backward_camera<8><<<blocks, 64, 0, st>>>(A);
-  else k_backward_camera<16><<<blocks, 256, 0, st>>>(A);
+  const unsigned tiles = (unsigned)(K.Wt * Ht);
+  if (C.tile_px == 8) k_backward_camera<8><<<tiles * 2, 32, 0, st>>>(A);
+  else k_backward_camera<16><<<tiles * 8, 32, 0, st>>>(A);
   const int32_t lc = launch_check("simuli_backward_camera");
   if (lc != SIMULI_OK) return lc;
-  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), st, "simuli_backward_camera");
+  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), st, "simuli_backward_camera (params)");
 }

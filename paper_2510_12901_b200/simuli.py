@@ -87,11 +87,13 @@ class Gaussians(C.Structure):
 
 
 class LidarGradIn(C.Structure):
-    _fields_ = [(k, C.c_void_p) for k in ("zeta", "opacity", "depth_accum", "depth", "intensity", "raydrop")]
+    _fields_ = [(k, C.c_void_p) for k in ("zeta", "opacity", "depth_accum", "depth", "intensity", "raydrop",
+                                          "fwd_zeta", "fwd_opacity", "fwd_depth_accum")]
 
 
 class CameraGradIn(C.Structure):
-    _fields_ = [(k, C.c_void_p) for k in ("rgb", "opacity", "depth_accum", "depth")]
+    _fields_ = [(k, C.c_void_p) for k in ("rgb", "opacity", "depth_accum", "depth", "fwd_rgb", "fwd_opacity",
+                                          "fwd_depth_accum")]
 
 
 class GaussianGrads(C.Structure):
@@ -272,23 +274,30 @@ def simuli_backward_workspace_size(n):
     return int(b.value)
 
 
-def _grad_structs(frame, grads, names, gin_cls):
+def _grad_structs(frame, grads, names, gin_cls, fwd):
     import torch
     sc = frame.scene
     out = {k: torch.empty_like(sc[k]) for k in ("means", "quats", "scales", "opacity", "sh")}
-    gin = gin_cls(*[_ptr(grads.get(k)) if grads.get(k) is not None else None for k in names])
+    gin = gin_cls(*[_ptr(grads.get(k)) if grads.get(k) is not None else None for k in names],
+                  *[_ptr(t) if t is not None else None for t in fwd])
     gout = GaussianGrads(*[_ptr(out[k]) for k in ("means", "quats", "scales", "opacity", "sh")])
     return out, gin, gout
 
 
-def simuli_backward(frame, grads, stream=None):
+def simuli_backward(frame, grads, stream=None, use_forward_totals=True):
     """Backward of the frame's last forward (A31): grads = upstream gradients by output
-    name (device float32; missing = 0).  Returns the particle parameter gradients."""
+    name (device float32; missing = 0).  Returns the particle parameter gradients.
+    use_forward_totals: pass the forward's zeta / opacity / depth_accum outputs so the
+    backward skips its totals pass."""
     lidar = isinstance(frame, LidarRenderer)
     names = ("zeta", "opacity", "depth_accum", "depth", "intensity", "raydrop") if lidar else \
         ("rgb", "opacity", "depth_accum", "depth")
     grads = {k: v.contiguous() for k, v in grads.items() if v is not None}
-    out, gin, gout = _grad_structs(frame, grads, names, LidarGradIn if lidar else CameraGradIn)
+    fk = ("zeta" if lidar else "rgb", "opacity", "depth_accum")
+    fwd = [frame.out.get(k) for k in fk] if use_forward_totals else [None, None, None]
+    if any(t is None for t in fwd):
+        fwd = [None, None, None]
+    out, gin, gout = _grad_structs(frame, grads, names, LidarGradIn if lidar else CameraGradIn, fwd)
     ws = frame._bwd_workspace()
     fn = load().simuli_backward_lidar if lidar else load().simuli_backward_camera
     _check(fn(C.byref(frame.gauss), C.byref(frame.projected), _ptr(frame.sorted_ids), _ptr(frame.tile_ranges),
@@ -373,9 +382,9 @@ class _Frame:
             self._bws = torch.empty(max(need, 16), dtype=torch.uint8, device=self.device)
         return self._bws
 
-    def backward(self, grads, stream=None):
+    def backward(self, grads, stream=None, use_forward_totals=True):
         """Gradients of the particle parameters from upstream output gradients (A31)."""
-        return simuli_backward(self, grads, stream)
+        return simuli_backward(self, grads, stream, use_forward_totals)
 
     keep_keys = True  # also write the u64 (tile | depth) keys (tests); the renderer needs only ids
 

@@ -39,4 +39,5 @@ for name in sys.argv[1:] or ["B", "D"]:
         fwd = timed(lambda: f.frame())
     torch.cuda.synchronize()
     bwd = timed(lambda: f.backward(g))
-    print(f"{name}: forward {fwd:.1f} us, backward {bwd:.1f} us ({bwd / fwd:.2f}x forward)", flush=True)
+    bwd1 = timed(lambda: f.backward(g, use_forward_totals=False))
+    print(f"{name}: forward {fwd:.1f} us, backward {bwd:.1f} us ({bwd / fwd:.2f}x forward; {bwd1:.1f} us with its own totals pass)", flush=True)

@@ -763,7 +763,10 @@ def test_backward_lidar_parity(SM, oracle_mod, config):
     R = od.shape[0]
     g = _upstream(R, 5, True, ok)
     got = r.backward(_dev(g))
+    got_p1 = r.backward(_dev(g), use_forward_totals=False)  # the backward's own totals pass
     torch.cuda.synchronize()
+    for k in got:
+        assert torch.allclose(got[k], got_p1[k], rtol=1e-4, atol=1e-6 * got[k].abs().max().item()), k
     gz, go, gd = O.fold_upstream(fwd, g, lidar=True)
     d = O.backward_composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, gz, go, gd, wrap=1,
                              near=cfg.min_range, pi_f=t.pi_f, two_pi_f=t.two_pi_f)
