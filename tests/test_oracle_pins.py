@@ -1039,3 +1039,45 @@ def test_backward_transmittance_identity(oracle_mod):
     an = np.sum(sc["opacity"].astype(np.float64) * b["opacity"])
     assert np.allclose(f2["opacity"], 1 - f2["T_final"], atol=1e-12)  # omega = 1 - T (Eq. 1)
     assert abs(fd - an) < 1e-3 * max(1.0, abs(an)), (fd, an)
+
+
+def test_backward_camera_vs_finite_differences(oracle_mod):
+    """O15/O16 on the camera path (KB fisheye, rolling shutter) against central differences
+    of the oracle's camera forward: loss = sum of random weights x (rgb, omega, D, depth)."""
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    cam.width, cam.height, cam.cx, cam.cy = 96, 64, 48.0, 32.0
+    sc = S.corridor_scene(12, 2500, x_range=(3.0, 25.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    sc["sh"] = np.ascontiguousarray(sc["sh"][:, :1])  # constant colour: no view-direction term (A31)
+    R = cam.width * cam.height
+    rng = np.random.default_rng(13)
+    g = {"rgb": rng.normal(size=(R, 3)), "opacity": rng.normal(size=R), "depth_accum": 0.05 * rng.normal(size=R),
+         "depth": 0.05 * rng.normal(size=R)}
+
+    def loss(s):
+        f = O.render_camera(s, cam)
+        return (np.sum(g["rgb"] * f["feat"]) + np.sum(g["opacity"] * f["opacity"]) +
+                np.sum(g["depth_accum"] * f["depth_accum"]) + np.sum(g["depth"] * f["depth"]))
+
+    b = O.backward_camera(sc, cam, g)
+    assert (b["fwd"]["opacity"] > 0.1).mean() > 0.05
+    top = np.argsort(-np.abs(b["opacity"]))[:4]
+    checked = bad = 0
+    for i in top:
+        for key, h, dims in (("means", 2e-4, 3), ("quats", 2e-4, 4), ("scales", 1e-4, 3), ("opacity", 1e-4, 1)):
+            for c in range(dims):
+                vals, deltas = [], []
+                for sgn in (1, -1):
+                    s2 = {k: v.copy() for k, v in sc.items()}
+                    arr = s2[key].reshape(sc["means"].shape[0], -1)
+                    x0 = np.float32(arr[i, c])
+                    arr[i, c] = np.float32(x0 + sgn * h * max(1.0, abs(float(x0))))
+                    deltas.append(float(arr[i, c]) - float(x0))
+                    vals.append(loss(s2))
+                fd = (vals[0] - vals[1]) / (deltas[0] - deltas[1])
+                an = b[key].reshape(sc["means"].shape[0], -1)[i, c]
+                checked += 1
+                if abs(fd - an) > 2e-3 * max(1.0, abs(an)):
+                    bad += 1
+                    print("mismatch", i, key, c, fd, an)
+    assert checked == 4 * 11 and bad <= 2, bad
