@@ -218,6 +218,19 @@ __device__ __forceinline__ void sh_dot(const float* __restrict__ sh, int ncoef, 
   f[0] = acc[0]; f[1] = acc[1]; f[2] = acc[2];
 }
 
+// The same for degree 3 from a 192-byte block already staged (e.g. in shared memory).
+__device__ __forceinline__ void sh_dot16(const float4* s4, const float b[16], float f[3]) {
+  float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    const float4 v4 = s4[c];
+    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[(4 * c + j) % 3] = fmaf(b[(4 * c + j) / 3], v[j], acc[(4 * c + j) % 3]);
+  }
+  f[0] = acc[0]; f[1] = acc[1]; f[2] = acc[2];
+}
+
 // Ray in double, split into float hi + lo parts for the compensated response.
 struct RayF {
   float o_hi[3], o_lo[3], d_hi[3], d_lo[3];

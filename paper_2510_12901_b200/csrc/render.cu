@@ -334,6 +334,12 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
   constexpr int BAR_PROD = 1, BAR_FULL = 2, BAR_EMPTY = 4, BAR_RAYS = 6;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LidarSmem<NP, STAGES, SLOTB>& S = *reinterpret_cast<LidarSmem<NP, STAGES, SLOTB>*>(smem_raw);
+  // per-ray SH (A30), degree 3: the round's member entries' 192-byte coefficient blocks,
+  // staged by the producers after the box tests (one slot buffer: written only once the
+  // consumer has released the previous round)
+  static_assert(!PRAY || SLOTB == 1, "per-ray SH staging assumes one slot buffer");
+  float4* s_sh = reinterpret_cast<float4*>(smem_raw + sizeof(LidarSmem<NP, STAGES, SLOTB>));
+  const bool sh_smem = PRAY && A.sh_ncoef == 16;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef SIMULI_RENDER_PROFILE
   const long long t_start = gtime();
@@ -442,7 +448,10 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
             }
             const float w = a.x * T;
             float fv[3] = {f.y, f.z, f.w};
-            if (PRAY) sh_dot(A.sh + (size_t)S.pid[sb][e] * A.sh_ncoef * 3, A.sh_ncoef, shb, fv);
+            if (PRAY) {
+              if (sh_smem) sh_dot16(s_sh + e * 12, shb, fv);
+              else sh_dot(A.sh + (size_t)S.pid[sb][e] * A.sh_ncoef * 3, A.sh_ncoef, shb, fv);
+            }
             acc0 = fmaf(w, fv[0], acc0);
             acc1 = fmaf(w, fv[1], acc1);
             acc2 = fmaf(w, fv[2], acc2);
@@ -609,11 +618,23 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
       alive = ~S.done_mask[b ^ 1];
     }
     if (warp == 0) RMARK(r, 4);
+    uint32_t pid = 0;
     if (valid) {
       S.feat[sb][tid] = S.rec[st][tid][3];
-      if (PRAY) S.pid[sb][tid] = __ldg(A.ids + start + tid);
+      if (PRAY) {
+        pid = __ldg(A.ids + start + tid);
+        S.pid[sb][tid] = pid;
+      }
     }
     m &= alive;  // no member pairs for terminated rays
+    if (sh_smem) {  // asynchronous: lands while the round's responses are computed
+      if (m != 0u) {
+        const float4* src = reinterpret_cast<const float4*>(A.sh) + (size_t)pid * 12;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) cp_async16(s_sh + tid * 12 + c, src + c);
+      }
+      cp_async_commit();
+    }
     const uint32_t my = warp_transpose32(m, lane);  // lane r: entries of this warp holding ray r
     S.memb[sb][warp][lane] = my;
     const int k = __popc(m);
@@ -665,6 +686,7 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
       S.at[sb][rr][slot] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
       S.ent[sb][rr][slot] = (uint8_t)e;
     }
+    if (sh_smem) cp_async_wait<0>();  // the staged SH (and the record prefetch issued before it)
     __syncwarp();
     __threadfence_block();
     if (warp == 0) RMARK(r, 7);
@@ -739,7 +761,8 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
     k_render_lidar<NP, STG, SB, false><<<(unsigned)A.n_items, 32 * (NP + 1), smem, st>>>(A);
   };
   if (A.sh) {  // per-ray SH (A30): the default pipeline shape only
-    constexpr size_t smem = sizeof(LidarSmem<kLidarNP, kLidarStages, kLidarSlotBuffers>);
+    const size_t smem = sizeof(LidarSmem<kLidarNP, kLidarStages, kLidarSlotBuffers>) +
+                        (A.sh_ncoef == 16 ? sizeof(float4) * 12 * 32 * kLidarNP : 0);
     auto kern = k_render_lidar<kLidarNP, kLidarStages, kLidarSlotBuffers, true>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)A.n_items, 32 * (kLidarNP + 1), smem, st>>>(A);
