@@ -394,7 +394,7 @@ int32_t simuli_backward_camera(const simuli_gaussians* gaussians, const simuli_p
  *    longitude atan2(d_y, d_x) in [-pi, pi) -> [0, env_w), colatitude acos(d_z) in [0, pi]
  *    -> [0, env_h), texel centres at +0.5, bilinear, wrapping in longitude, clamped in
  *    colatitude; NULL -> c_b = 0.
- *  * grid: device [grid_d][grid_h][grid_w][12] float, row-major 3x4 affine matrices over
+ *  * grid: device [grid_d][grid_h][grid_w][12] float (16-byte aligned), row-major 3x4 affine matrices over
  *    (x / W, y / H, luminance), luminance = 0.299 r + 0.587 g + 0.114 b of the blended colour
  *    clamped to [0, 1], cell centres at +0.5, trilinear, clamped at the borders;
  *    c = M[:, :3] c_in + M[:, 3]; NULL -> A = identity.

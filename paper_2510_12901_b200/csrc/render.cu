@@ -896,20 +896,28 @@ __device__ void env_lookup(const ComposeArgs& A, const double d[3], float out[3]
 }
 
 // thread per pixel: ray direction, environment map, blend, bilateral-grid affine
+// grid (ceil(W / 256), H): a CTA covers 256 pixels of one row, whose (rolling-shutter) pose
+// is computed once per CTA
 __global__ void __launch_bounds__(256) k_compose_camera(const ComposeArgs A) {
   const int W = A.cam.width, H = A.cam.height;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= (int64_t)W * H) return;
-  const int i = (int)(p % W), j = (int)(p / W);
-  float cb[3] = {0.f, 0.f, 0.f};
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  __shared__ double s_R[9];
   if (A.env) {
-    double dc[3], d[3] = {0.0, 0.0, 0.0};
-    if (unproject(A.cam, (double)i + 0.5, (double)j + 0.5, dc)) {
+    if (threadIdx.x == 0) {
       const double s = A.cam.rolling ? ((double)j + 0.5) / (double)H : 0.0;
       double R[9], o[3];
       pose_at_d(A.cam.pose, s, R, o);
-      for (int k = 0; k < 3; ++k) d[k] = R[3 * k] * dc[0] + R[3 * k + 1] * dc[1] + R[3 * k + 2] * dc[2];
+      for (int k = 0; k < 9; ++k) s_R[k] = R[k];
     }
+    __syncthreads();
+  }
+  if (i >= W) return;
+  const int64_t p = (int64_t)j * W + i;
+  float cb[3] = {0.f, 0.f, 0.f};
+  if (A.env) {
+    double dc[3], d[3] = {0.0, 0.0, 0.0};
+    if (unproject(A.cam, (double)i + 0.5, (double)j + 0.5, dc))
+      for (int k = 0; k < 3; ++k) d[k] = s_R[3 * k] * dc[0] + s_R[3 * k + 1] * dc[1] + s_R[3 * k + 2] * dc[2];
     env_lookup(A, d, cb);
   }
   const float om = __ldg(A.opacity + p);
@@ -941,9 +949,15 @@ __global__ void __launch_bounds__(256) k_compose_camera(const ComposeArgs A) {
         for (int dx = 0; dx <= 1; ++dx) {
           const int xi = min(i0[0] + dx, A.gw - 1), yi = min(i0[1] + dy, A.gh - 1), zi = min(i0[2] + dz, A.gd - 1);
           const float w = (dx ? a[0] : 1.f - a[0]) * (dy ? a[1] : 1.f - a[1]) * (dz ? a[2] : 1.f - a[2]);
-          const float* m = A.grid + (((size_t)zi * A.gh + yi) * A.gw + xi) * 12;
+          const float4* m = reinterpret_cast<const float4*>(A.grid + (((size_t)zi * A.gh + yi) * A.gw + xi) * 12);
 #pragma unroll
-          for (int q = 0; q < 12; ++q) M[q] = fmaf(w, __ldg(m + q), M[q]);
+          for (int q = 0; q < 3; ++q) {
+            const float4 v = __ldg(m + q);
+            M[4 * q] = fmaf(w, v.x, M[4 * q]);
+            M[4 * q + 1] = fmaf(w, v.y, M[4 * q + 1]);
+            M[4 * q + 2] = fmaf(w, v.z, M[4 * q + 2]);
+            M[4 * q + 3] = fmaf(w, v.w, M[4 * q + 3]);
+          }
         }
 #pragma unroll
     for (int r = 0; r < 3; ++r) out[r] = M[4 * r] * cin[0] + M[4 * r + 1] * cin[1] + M[4 * r + 2] * cin[2] + M[4 * r + 3];
@@ -964,6 +978,7 @@ extern "C" int32_t simuli_compose_camera(const simuli_project_params* P, const s
   SIMULI_REQUIRE(!comp->env_map || (comp->env_h > 0 && comp->env_w > 0), "simuli_compose_camera: bad env map size");
   SIMULI_REQUIRE(!comp->grid || (comp->grid_h > 0 && comp->grid_w > 0 && comp->grid_d > 0),
                  "simuli_compose_camera: bad grid size");
+  SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(comp->grid) % 16 == 0, "simuli_compose_camera: grid must be 16-byte aligned");
   const simuli_camera& C = *P->camera;
   ComposeArgs A{};
   A.cam.model = C.model; A.cam.width = C.width; A.cam.height = C.height; A.cam.rolling = C.rolling_shutter;
@@ -976,7 +991,8 @@ extern "C" int32_t simuli_compose_camera(const simuli_project_params* P, const s
   A.rgb_fg = rgb_fg; A.opacity = opacity; A.rgb_out = rgb_out;
   const int64_t n = (int64_t)C.width * C.height;
   if (n == 0) return SIMULI_OK;
-  k_compose_camera<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A);
+  k_compose_camera<<<dim3((unsigned)((C.width + 255) / 256), (unsigned)C.height), 256, 0,
+                     reinterpret_cast<cudaStream_t>(stream)>>>(A);
   return launch_check("simuli_compose_camera");
 }
 
