@@ -122,3 +122,37 @@ def test_workspace_size_and_bad_args(lib):
     assert L.simuli_compose_camera(None, None, None, None, None, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
     size = ctypes.c_size_t(0)
     assert L.simuli_bin_sort_workspace_size(-1, 10, 1, ctypes.byref(size)) == lib.SIMULI_ERR_INVALID_ARGUMENT
+    # backward (A31): size query and argument checks run on the host
+    assert L.simuli_backward_workspace_size(1000, ctypes.byref(size)) == lib.SIMULI_OK and size.value == 1000 * 64
+    assert L.simuli_backward_workspace_size(-1, ctypes.byref(size)) == lib.SIMULI_ERR_INVALID_ARGUMENT
+    for fn in (L.simuli_backward_lidar, L.simuli_backward_camera):
+        assert fn(None, None, None, None, None, None, None, None, None, 0, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
+        assert b"NULL" in L.simuli_last_error()
+
+
+def test_backward_argument_errors(lib):
+    """Host-side checks of simuli_backward_* (no device memory is touched: dummy aligned
+    addresses): missing view_dir -> INVALID_ARGUMENT, per-ray SH / scene graph /
+    beam divergence -> UNSUPPORTED (A31), small workspace -> INVALID_ARGUMENT."""
+    C = ctypes
+    L = lib.load()
+    fake = 1 << 20  # never dereferenced: every check below fails before a launch
+    G = lib.Gaussians(10, fake, fake, fake, fake, fake, 3, None, None, 0)
+    proj = lib.Projected(fake, fake, fake, fake, None)
+    rp = lib.RenderParams(1 / 255, 0.99, 1e-4, None, 0)
+    gout = lib.GaussianGrads(fake, fake, fake, fake, fake)
+    gin = lib.CameraGradIn()
+    cam = lib.Camera(1, 64, 48, 50.0, 50.0, 32.0, 24.0, (C.c_float * 5)(0, 0, 0, 0, 0), 1, 0.05, 1.7, 16)
+    P = lib.ProjectParams(lib.SENSOR_CAMERA, None, None, C.pointer(cam), lib.make_pose({"q": [1, 0, 0, 0], "t": [0, 0, 0]}),
+                          lib.make_pose({"q": [1, 0, 0, 0], "t": [0, 0, 0]}), 1, 1.0, 2.0, 0.0, 3.0, 0, 0)
+    args = lambda ws: (C.byref(G), C.byref(proj), fake, fake, C.byref(P), C.byref(rp), C.byref(gin),  # noqa: E731
+                       C.byref(gout), fake, ws, None)
+    assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_INVALID_ARGUMENT
+    assert b"view_dir" in L.simuli_last_error()
+    proj.view_dir = fake
+    assert L.simuli_backward_camera(*args(639)) == lib.SIMULI_ERR_INVALID_ARGUMENT  # workspace < 10 x 64 B
+    rp.sh = fake
+    assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_UNSUPPORTED
+    rp.sh = None
+    G.actor_id, G.actor_pose, G.n_actors = fake, fake, 1
+    assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_UNSUPPORTED
