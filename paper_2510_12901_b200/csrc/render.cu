@@ -1432,6 +1432,7 @@ __global__ void __launch_bounds__(256) k_backward_params(const float* __restrict
 int32_t bwd_common_checks(const simuli_gaussians* G, const simuli_projected* proj, const uint32_t* ids,
                           const int32_t* ranges, const simuli_project_params* P, const simuli_render_params* rp,
                           const simuli_gaussian_grads* gout, void* ws, size_t ws_bytes, const char* what) {
+  if (G && G->n == 0) return SIMULI_OK;  // nothing to differentiate (callers return before any launch)
   if (!(G && proj && proj->record && ids && ranges && P && rp && gout && ws)) {
     set_error("%s: NULL argument", what);
     return SIMULI_ERR_INVALID_ARGUMENT;
@@ -1500,7 +1501,7 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
   clear_error();
   const int32_t rc = bwd_common_checks(G, proj, sorted_ids, tile_ranges, P, rp, gout, workspace, workspace_bytes,
                                        "simuli_backward_lidar");
-  if (rc != SIMULI_OK) return rc;
+  if (rc != SIMULI_OK || G->n == 0) return rc;
   SIMULI_REQUIRE(gin, "simuli_backward_lidar: NULL grad_in");
   SIMULI_REQUIRE(P->kind == SIMULI_SENSOR_LIDAR && P->lidar && P->tiling, "simuli_backward_lidar: needs LiDAR params");
   if (P->lidar->beam_divergence_rad > 0.f) {
@@ -1541,7 +1542,7 @@ extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simul
   clear_error();
   const int32_t rc = bwd_common_checks(G, proj, sorted_ids, tile_ranges, P, rp, gout, workspace, workspace_bytes,
                                        "simuli_backward_camera");
-  if (rc != SIMULI_OK) return rc;
+  if (rc != SIMULI_OK || G->n == 0) return rc;
   SIMULI_REQUIRE(gin, "simuli_backward_camera: NULL grad_in");
   SIMULI_REQUIRE(P->kind == SIMULI_SENSOR_CAMERA && P->camera, "simuli_backward_camera: needs camera params");
   const simuli_camera& C = *P->camera;

@@ -782,10 +782,16 @@ def test_backward_lidar_parity(SM, oracle_mod, config):
         _compare_grads(got2, ref2, f"{config} tier 2")
 
 
-def test_backward_camera_parity(SM, oracle_mod):
+@pytest.mark.parametrize("variant", ["D-small", "tile8_deg1", "pinhole_deg2"])
+def test_backward_camera_parity(SM, oracle_mod, variant):
     O = oracle_mod
-    cam = S.camera_config("D-small")
+    cam = S.camera_config("pinhole-small" if variant == "pinhole_deg2" else "D-small")
     scene = S.corridor_scene(21, 40000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    if variant == "tile8_deg1":
+        cam.tile_px = 8
+        scene["sh"] = np.ascontiguousarray(scene["sh"][:, :4])
+    elif variant == "pinhole_deg2":
+        scene["sh"] = np.ascontiguousarray(scene["sh"][:, :9])
     c = SM.CameraRenderer(cam, SM.to_device_scene(scene))
     c.requires_grad(True)
     c.want_ray_od(True)
@@ -806,4 +812,26 @@ def test_backward_camera_parity(SM, oracle_mod):
     d = O.backward_composite(rec, ids, ranges, rays["tile"], rays["u"], rays["v"], od, gz, go, gd, wrap=0,
                              near=cam.near, ray_valid=rays["valid"])
     ref = O.backward_params(scene, {"viewdir": c.view_dir.cpu().numpy().astype(np.float64)}, d)
-    _compare_grads(got, ref, "D-small tier 1")
+    _compare_grads(got, ref, f"{variant} tier 1")
+
+
+def test_backward_empty_and_unsupported(SM):
+    """n = 0 is a no-op; per-ray SH and beam divergence have no backward (UNSUPPORTED)."""
+    cfg = S.lidar_config("A")
+    sc = {k: v[:0] for k, v in S.scene_for("A").items()}
+    r = SM.LidarRenderer(cfg, SM.to_device_scene(sc))
+    r.requires_grad(True)
+    r.scan(sync_capacity=True)
+    out = r.backward({"opacity": torch.ones(r.n_rays, device="cuda")})
+    torch.cuda.synchronize()
+    assert out["means"].numel() == 0
+    sc = S.scene_for("A")
+    for kw, div in (({"per_ray_sh": True}, 0.0), ({}, 1.5e-3)):
+        c2 = S.lidar_config("A")
+        c2.beam_divergence = div
+        r = SM.LidarRenderer(c2, SM.to_device_scene(sc), **kw)
+        r.requires_grad(True)
+        r.scan(sync_capacity=True)
+        with pytest.raises(SM.SimuliError) as e:
+            r.backward({"opacity": torch.ones(r.n_rays, device="cuda")})
+        assert e.value.code == SM.SIMULI_ERR_UNSUPPORTED
