@@ -372,6 +372,7 @@ int32_t simuli_backward_workspace_size(int64_t n, size_t* bytes);
  * (totals, then gradients with suffix sums; warp-reduced float atomics into the workspace),
  * then one thread per particle for the parameter chain.  Asynchronous on `stream`;
  * gradient sums are in atomic (nondeterministic) order.
+ * n = 0: returns SIMULI_OK without reading any other argument.
  * Errors: INVALID_ARGUMENT (NULL, view_dir missing, workspace too small), UNSUPPORTED
  * (see above), CUDA. */
 int32_t simuli_backward_lidar(const simuli_gaussians* gaussians, const simuli_projected* proj,
