@@ -245,8 +245,10 @@ int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t
 /* Tile-Gaussian duplication and sort "as in 3DGS": one pair per (tile, particle)
  * overlap, ordered by (tile, bits(depth_key), particle id) -- unique and deterministic --
  * and tile_ranges[t] = [begin, end) of tile t in the sorted arrays (0,0 if empty).
- * Implementation: stable LSD onesweep radix sorts (8-bit digits) -- the visible particles
- * by depth key, then the pairs (emitted in that depth order) by tile.
+ * Implementation: the pairs are emitted as packed words (tile << b | depth bits - min,
+ * particle id) with b the bit width of the depth-key range, and sorted by a stable LSD
+ * onesweep radix sort with 8-bit digits (ceil((b + tile bits) / 8) passes, decided on the
+ * device).
  * n_cols_total: N_theta (LiDAR) or ceil(W / tile_px) (camera).
  * sorted_ids: device [pair_capacity] (u32 particle ids); sorted_keys: device
  *   [pair_capacity] u64 (tile << 32 | depth bits) or NULL to skip; tile_ranges: device
