@@ -276,6 +276,10 @@ def roofline_entries(stage_ms, counters, peaks, clocks_mhz):
                      "frac": ach / alu_peak, "algorithmic_lane_instr": int(lane_instr),
                      "algorithmic_bytes": int(b_render), "hbm_frac": b_render / t / 1e9 / hbm,
                      "ms": stage_ms["render"]}
+    # scan roofline t_roof = sum over stages of max(bytes / BW, instr / IR)
+    t_roof = (b_project / (hbm * 1e9) + b_sort / (hbm * 1e9) +
+              max(b_render / (hbm * 1e9), lane_instr / (alu_peak * 1e12)))
+    out["_scan"] = {"t_roof_ms": t_roof * 1e3}
     return out
 
 
@@ -413,6 +417,12 @@ def run_gpu(args):
 
     peaks = read_peaks()
     roof = roofline_entries(stage_ms, counters, peaks, clk.get("sm_mhz"))
+    scan_roof = roof.pop("_scan")
+    scan_roof.update({"latency_ms": latency_ms, "frac_of_latency": scan_roof["t_roof_ms"] / latency_ms,
+                      "throughput_ms_per_scan": max_ms / args.steps,
+                      "frac_of_throughput": scan_roof["t_roof_ms"] / (max_ms / args.steps),
+                      "note": "t_roof = sum_s max(B_s / HBM, I_s / issue peak) with the stages' algorithmic "
+                              "bytes / lane-instructions (project and sort: bytes only)"})
     dom = max(roof, key=lambda k: roof[k]["ms"])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -439,7 +449,8 @@ def run_gpu(args):
             "scans_per_s": value / r.n_rays,
             "latency_ms_per_scan": latency_ms,
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "roofline": roofline, "stages": roof, "counters": counters, "job_counters": job_counters,
+            "roofline": roofline, "stages": roof, "scan_roofline": scan_roof, "counters": counters,
+            "job_counters": job_counters,
             "clocks": clk,
             "wall_s_timed_region": wall}
     if ws == 1 and not args.no_cpu_baseline:
