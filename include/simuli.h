@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 6
+#define SIMULI_ABI_VERSION 7
 
 enum {
   SIMULI_OK = 0,
@@ -340,8 +340,7 @@ int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorte
  * is: alpha = min(alpha_max, sigma rho(tau_max)) with tau_max and delta^2 of the
  * canonical transform M = diag(1/s) R(q/|q|)^T (clamped alpha: no gradient).  Features are
  * the per-particle SH at the projection's view direction (A17), held fixed (no gradient
- * through the direction).  Not supported (UNSUPPORTED): beam divergence, per-ray SH,
- * scene-graph particles (actor_id).
+ * through the direction).  Not supported (UNSUPPORTED): beam divergence, per-ray SH.
  * Upstream gradients (device, [n_rays] or [n_rays][3]; NULL = 0): LiDAR zeta, opacity
  * (omega), depth_accum (D), depth (D / omega), intensity (zeta_0), raydrop
  * (1 / (1 + exp(zeta_1 - zeta_2))); camera rgb (c_f), opacity, depth_accum, depth. */
@@ -360,9 +359,13 @@ typedef struct {
 /* Per-particle parameter gradients (device, caller-allocated, n entries each; overwritten,
  * zero for particles that composite into no ray): means [n][3], quats [n][4] (w.r.t. the
  * unnormalised input quaternion), scales [n][3], opacity [n] (post-activation sigma),
- * sh [n][(deg+1)^2][3]. */
+ * sh [n][(deg+1)^2][3].  With a scene graph (simuli_gaussians.actor_id) means / quats are
+ * the gradients of the OBJECT-frame inputs and actor_pose [n_actors][7] (device, or NULL
+ * to skip) receives dL/dq_a (unnormalised, 4) and dL/dt_a (3) of every object pose
+ * (A29, A31: R_w = R_a R_l, mu_w = R_a mu_l + t_a). */
 typedef struct {
   float *means, *quats, *scales, *opacity, *sh;
+  float* actor_pose;
 } simuli_gaussian_grads;
 
 /* Scratch bytes for the backward of n particles (16 floats each). */

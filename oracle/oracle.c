@@ -1590,3 +1590,104 @@ void or_backward_params(int64_t n, const float* quats, const float* scales, cons
   }
 }
 
+/* ------------------------------------------------------------------------------------
+ * O16 with the scene graph (A29, A31).  For a particle of object a:
+ *   R_w = R_a R_l,  mu_w = R_a mu_l + t_a  (O0)
+ *   dL/dR_w = G from dL/dM (as in or_backward_params, R_w in ds),
+ *   dL/dR_l = R_a^T G,   dL/dmu_l = R_a^T dL/dmu_w,
+ *   dL/dR_a += G R_l^T + dL/dmu_w mu_l^T,   dL/dt_a += dL/dmu_w,
+ * each rotation gradient taken to its (unnormalised) quaternion by the O1 chain.  Static
+ * particles (id -1) are as in or_backward_params; ids outside [-1, n_actors) get zeros.
+ * g_actor [n_actors][7] = (dL/dq_a, dL/dt_a), accumulated over the object's particles.
+ * ---------------------------------------------------------------------------------- */
+static void rot_grad_to_quat(const double G[9], const double q_in[4], double dq_out[4]) {
+  double qn = sqrt(q_in[0] * q_in[0] + q_in[1] * q_in[1] + q_in[2] * q_in[2] + q_in[3] * q_in[3]);
+  const double w = q_in[0] / qn, x = q_in[1] / qn, y = q_in[2] / qn, z = q_in[3] / qn;
+  const double dw = 2.0 * (-z * G[1] + y * G[2] + z * G[3] - x * G[5] - y * G[6] + x * G[7]);
+  const double dx = 2.0 * (y * G[1] + z * G[2] + y * G[3] - 2.0 * x * G[4] - w * G[5] + z * G[6] + w * G[7] -
+                           2.0 * x * G[8]);
+  const double dy = 2.0 * (-2.0 * y * G[0] + x * G[1] + w * G[2] + x * G[3] + z * G[5] - w * G[6] + z * G[7] -
+                           2.0 * y * G[8]);
+  const double dz = 2.0 * (-2.0 * z * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.0 * z * G[4] + y * G[5] +
+                           x * G[6] + y * G[7]);
+  const double dq[4] = {dw, dx, dy, dz}, qh[4] = {w, x, y, z};
+  const double dot = dw * w + dx * x + dy * y + dz * z;
+  for (int c = 0; c < 4; ++c) dq_out[c] = (dq[c] - qh[c] * dot) / qn;
+}
+
+void or_backward_params_sg(int64_t n, const float* means, const float* quats, const float* scales,
+                           const double* viewdir, int32_t sh_degree, const int32_t* actor_id, int32_t n_actors,
+                           const double* actor_pose, const double* d_mu, const double* d_M, const double* d_feat,
+                           double* g_means, double* g_quats, double* g_scales, double* g_sh, double* g_actor) {
+  const int nco = (sh_degree + 1) * (sh_degree + 1);
+  double* Ga = (double*)calloc((size_t)(n_actors > 0 ? n_actors : 1) * 12, sizeof(double)); /* dR_a 9, dt_a 3 */
+  for (int64_t g = 0; g < n; ++g) {
+    for (int c = 0; c < 3; ++c) g_means[3 * g + c] = 0.0;
+    for (int c = 0; c < 4; ++c) g_quats[4 * g + c] = 0.0;
+    for (int c = 0; c < 3; ++c) g_scales[3 * g + c] = 0.0;
+    for (int k = 0; k < nco * 3; ++k) g_sh[(int64_t)g * nco * 3 + k] = 0.0;
+    const int32_t a = actor_id ? actor_id[g] : -1;
+    if (a < -1 || a >= n_actors) continue;
+    double ql[4], qn = 0.0;
+    for (int c = 0; c < 4; ++c) {
+      ql[c] = quats[4 * g + c];
+      qn += ql[c] * ql[c];
+    }
+    if (!(qn > 0.0) || !isfinite(qn)) continue;
+    double Rl[9], Ra[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    or_quat_to_rot(ql, Rl);
+    if (a >= 0) or_quat_to_rot(&actor_pose[7 * a], Ra);
+    double Rw[9];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += Ra[3 * i + k] * Rl[3 * k + j];
+        Rw[3 * i + j] = acc;
+      }
+    double G[9]; /* dL/dR_w[j][k] */
+    for (int k = 0; k < 3; ++k) {
+      const double s = scales[3 * g + k];
+      double ds = 0.0;
+      for (int j = 0; j < 3; ++j) {
+        const double dm = d_M[g * 9 + 3 * k + j];
+        G[3 * j + k] = dm / s;
+        ds -= dm * Rw[3 * j + k] / (s * s);
+      }
+      g_scales[3 * g + k] = ds;
+    }
+    double Gl[9], dmu_l[3];
+    for (int i = 0; i < 3; ++i) {
+      for (int j = 0; j < 3; ++j) {
+        double acc = 0.0;
+        for (int k = 0; k < 3; ++k) acc += Ra[3 * k + i] * G[3 * k + j]; /* R_a^T G */
+        Gl[3 * i + j] = acc;
+      }
+      double m = 0.0;
+      for (int k = 0; k < 3; ++k) m += Ra[3 * k + i] * d_mu[3 * g + k];
+      dmu_l[i] = m;
+    }
+    rot_grad_to_quat(Gl, ql, &g_quats[4 * g]);
+    for (int c = 0; c < 3; ++c) g_means[3 * g + c] = dmu_l[c];
+    if (a >= 0) {
+      double* A = &Ga[12 * a];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+          double acc = d_mu[3 * g + i] * (double)means[3 * g + j]; /* dL/dmu_w mu_l^T */
+          for (int k = 0; k < 3; ++k) acc += G[3 * i + k] * Rl[3 * j + k]; /* G R_l^T */
+          A[3 * i + j] += acc;
+        }
+      for (int c = 0; c < 3; ++c) A[9 + c] += d_mu[3 * g + c];
+    }
+    for (int k = 0; k < nco; ++k) {
+      double e[48] = {0}, yk[3];
+      e[3 * k] = 1.0;
+      or_sh_eval(e, sh_degree, &viewdir[3 * g], yk);
+      for (int c = 0; c < 3; ++c) g_sh[(int64_t)g * nco * 3 + 3 * k + c] = yk[0] * d_feat[3 * g + c];
+    }
+  }
+  for (int a = 0; a < n_actors; ++a) {
+    rot_grad_to_quat(&Ga[12 * a], &actor_pose[7 * a], &g_actor[7 * a]);
+    for (int c = 0; c < 3; ++c) g_actor[7 * a + 4 + c] = Ga[12 * a + 9 + c];
+  }
+  free(Ga);
+}

@@ -185,6 +185,13 @@ void or_backward_params(int64_t n, const float* quats, const float* scales, cons
                         int32_t sh_degree, const double* d_M, const double* d_feat, double* g_quats,
                         double* g_scales, double* g_sh);
 
+/* O16 with the scene graph: gradients of the LOCAL particle parameters and of the object
+ * poses (g_actor [n_actors][7] = dL/dq_a, dL/dt_a); d_mu / d_M are world-frame (O15). */
+void or_backward_params_sg(int64_t n, const float* means, const float* quats, const float* scales,
+                           const double* viewdir, int32_t sh_degree, const int32_t* actor_id, int32_t n_actors,
+                           const double* actor_pose, const double* d_mu, const double* d_M, const double* d_feat,
+                           double* g_means, double* g_quats, double* g_scales, double* g_sh, double* g_actor);
+
 /* O0: scene graph, object particles -> world at the frame's timestamp (A29) */
 void or_actors_to_world(int64_t n, const float* means, const float* quats, const int32_t* actor_id,
                         int32_t n_actors, const double* actor_pose, float* means_w, float* quats_w);

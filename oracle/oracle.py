@@ -128,6 +128,8 @@ def lib():
                                             f64p, i32p, C.POINTER(OrRenderParams), f64p, f64p, f64p, f64p, f64p,
                                             f64p, f64p]
         L.or_backward_params.argtypes = [C.c_int64, f32p, f32p, f64p, C.c_int32, f64p, f64p, f64p, f64p, f64p]
+        L.or_backward_params_sg.argtypes = [C.c_int64, f32p, f32p, f32p, f64p, C.c_int32, i32p, C.c_int32, f64p,
+                                            f64p, f64p, f64p, f64p, f64p, f64p, f64p, f64p]
         L.or_actors_to_world.argtypes = [C.c_int64, f32p, f32p, i32p, C.c_int32, f64p, f32p, f32p]
         _lib = L
     return _lib
@@ -614,9 +616,26 @@ def backward_composite(records, ids, ranges, ray_tile, ray_a, ray_b, ray_od, Gz,
 
 
 def backward_params(scene, proj, d):
-    """O16: gradients of the particle parameters (means, quats, scales, opacity, sh)."""
+    """O16: gradients of the particle parameters (means, quats, scales, opacity, sh); with a
+    scene graph also of the object poses ('actor_pose' [n_actors, 7]: dq_a, dt_a)."""
     if scene.get("actor_id") is not None:
-        raise NotImplementedError("backward through the scene graph is not modelled (A31)")
+        n = int(scene["means"].shape[0])
+        m = np.ascontiguousarray(scene["means"], np.float32)
+        q = np.ascontiguousarray(scene["quats"], np.float32)
+        s = np.ascontiguousarray(scene["scales"], np.float32)
+        ids = np.ascontiguousarray(scene["actor_id"], np.int32)
+        ap = _d(np.asarray(scene["actor_pose"], np.float32).astype(np.float64))
+        ncoef = scene["sh"].size // max(n, 1) // 3
+        deg = {1: 0, 4: 1, 9: 2, 16: 3}[ncoef]
+        out = {"means": np.zeros((n, 3)), "quats": np.zeros((n, 4)), "scales": np.zeros((n, 3)),
+               "sh": np.zeros((n, ncoef, 3)), "actor_pose": np.zeros((ap.shape[0], 7))}
+        lib().or_backward_params_sg(n, _p(m, f32p), _p(q, f32p), _p(s, f32p), _p(_d(proj["viewdir"]), f64p), deg,
+                                    _p(ids, i32p), int(ap.shape[0]), _p(ap, f64p), _p(_d(d["mu"]), f64p),
+                                    _p(_d(d["M"]), f64p), _p(_d(d["feat"]), f64p), _p(out["means"], f64p),
+                                    _p(out["quats"], f64p), _p(out["scales"], f64p), _p(out["sh"], f64p),
+                                    _p(out["actor_pose"], f64p))
+        out["opacity"] = d["sigma"].copy()
+        return out
     n = int(scene["means"].shape[0])
     q = np.ascontiguousarray(scene["quats"], np.float32)
     s = np.ascontiguousarray(scene["scales"], np.float32)

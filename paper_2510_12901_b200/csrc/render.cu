@@ -1373,58 +1373,120 @@ __global__ void __launch_bounds__(32) k_backward_camera(const BwdArgs A) {
   bwd_ray_pair_passes<false>(A, rf, inside && valid, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, member);
 }
 
-// parameter chain (O16): M = diag(1/s) R(q^)^T -> (q, s); f = SH(v) -> SH coefficients
-__global__ void __launch_bounds__(256) k_backward_params(const float* __restrict__ ws, const float* __restrict__ quats,
-                                                         const float* __restrict__ scales,
-                                                         const float* __restrict__ view_dir, int ncoef, int64_t n,
-                                                         simuli_gaussian_grads out) {
+// dL/dR (row-major 3x3) -> dL/dq of the unnormalised quaternion q behind R = R(q / |q|) (O1)
+__device__ __forceinline__ void rot_grad_to_quat(const float G[9], const float q[4], float inv, float dq_out[4]) {
+  const float w = q[0], x = q[1], y = q[2], z = q[3];  // normalised
+  const float dq[4] = {
+      2.f * (-z * G[1] + y * G[2] + z * G[3] - x * G[5] - y * G[6] + x * G[7]),
+      2.f * (y * G[1] + z * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + z * G[6] + w * G[7] - 2.f * x * G[8]),
+      2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + z * G[5] - w * G[6] + z * G[7] - 2.f * y * G[8]),
+      2.f * (-2.f * z * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * z * G[4] + y * G[5] + x * G[6] + y * G[7])};
+  const float dot = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) dq_out[c] = (dq[c] - q[c] * dot) * inv;
+}
+
+struct ParamsArgs {
+  const float *ws, *means, *quats, *scales, *view_dir;
+  const int* actor_id;
+  const float* actor_pose;  // [n_actors][7]
+  int n_actors, ncoef;
+  int64_t n;
+};
+
+// parameter chain (O16): M = diag(1/s) R_w^T with R_w = R_a R(q_l^) (R_a = I for static
+// particles), mu_w = R_a mu_l + t_a -> (mu_l, q_l, s) and the object poses (atomics into
+// out.actor_pose, each particle's share being linear in its own dL/dR_a, dL/dmu_w);
+// f = SH(v) -> SH coefficients
+__global__ void __launch_bounds__(256) k_backward_params(const ParamsArgs P, simuli_gaussian_grads out) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n) return;
+  if (g >= P.n) return;
   float v[kBwdVals];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    const float4 x = __ldg(reinterpret_cast<const float4*>(ws) + g * 4 + c);
+    const float4 x = __ldg(reinterpret_cast<const float4*>(P.ws) + g * 4 + c);
     v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w;
   }
-  for (int c = 0; c < 3; ++c) out.means[3 * g + c] = v[c];
   out.opacity[g] = v[12];
-  const float4 q4 = __ldg(reinterpret_cast<const float4*>(quats) + g);
+  int a = -1;
+  if (P.actor_id) a = __ldg(P.actor_id + g);
+  const bool in_range = a >= -1 && a < P.n_actors;
+  const float4 q4 = __ldg(reinterpret_cast<const float4*>(P.quats) + g);
   const float qn2 = q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w;
-  float gq[4] = {0.f, 0.f, 0.f, 0.f}, gs[3] = {0.f, 0.f, 0.f};
-  if (qn2 > 0.f && isfinite(qn2)) {
+  float gq[4] = {0.f, 0.f, 0.f, 0.f}, gs[3] = {0.f, 0.f, 0.f}, gm[3] = {v[0], v[1], v[2]};
+  if (in_range && qn2 > 0.f && isfinite(qn2)) {
     const float inv = rsqrtf(qn2);
     const float q[4] = {q4.x * inv, q4.y * inv, q4.z * inv, q4.w * inv};
-    float R[9];
-    quat_rot(q, R);
-    float G[9];  // dL/dR[j][k] = dL/dM[k][j] / s_k
+    float Rl[9], Ra[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f}, qa[4] = {1.f, 0.f, 0.f, 0.f}, inva = 1.f;
+    quat_rot(q, Rl);
+    const float* ap = nullptr;
+    if (a >= 0) {
+      ap = P.actor_pose + 7 * (size_t)a;
+      const float qa4[4] = {__ldg(ap), __ldg(ap + 1), __ldg(ap + 2), __ldg(ap + 3)};
+      inva = rsqrtf(qa4[0] * qa4[0] + qa4[1] * qa4[1] + qa4[2] * qa4[2] + qa4[3] * qa4[3]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) qa[c] = qa4[c] * inva;
+      quat_rot(qa, Ra);
+    }
+    float Rw[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Rw[3 * i + j] = Ra[3 * i] * Rl[j] + Ra[3 * i + 1] * Rl[3 + j] + Ra[3 * i + 2] * Rl[6 + j];
+    float G[9];  // dL/dR_w[j][k] = dL/dM[k][j] / s_k
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const float s = __ldg(scales + 3 * g + k);
+      const float s = __ldg(P.scales + 3 * g + k);
       float ds = 0.f;
 #pragma unroll
       for (int jj = 0; jj < 3; ++jj) {
         const float dm = v[3 + 3 * k + jj];
         G[3 * jj + k] = dm / s;
-        ds -= dm * R[3 * jj + k] / (s * s);
+        ds -= dm * Rw[3 * jj + k] / (s * s);
       }
       gs[k] = ds;
     }
-    const float w = q[0], x = q[1], y = q[2], z = q[3];
-    const float dq[4] = {
-        2.f * (-z * G[1] + y * G[2] + z * G[3] - x * G[5] - y * G[6] + x * G[7]),
-        2.f * (y * G[1] + z * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + z * G[6] + w * G[7] - 2.f * x * G[8]),
-        2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + z * G[5] - w * G[6] + z * G[7] - 2.f * y * G[8]),
-        2.f * (-2.f * z * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * z * G[4] + y * G[5] + x * G[6] + y * G[7])};
-    const float dot = dq[0] * w + dq[1] * x + dq[2] * y + dq[3] * z;
+    if (a < 0) {
+      rot_grad_to_quat(G, q, inv, gq);
+    } else {
+      float Gl[9];  // R_a^T G
 #pragma unroll
-    for (int c = 0; c < 4; ++c) gq[c] = (dq[c] - q[c] * dot) * inv;
+      for (int i = 0; i < 3; ++i) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Gl[3 * i + j] = Ra[i] * G[j] + Ra[3 + i] * G[3 + j] + Ra[6 + i] * G[6 + j];
+        gm[i] = Ra[i] * v[0] + Ra[3 + i] * v[1] + Ra[6 + i] * v[2];
+      }
+      rot_grad_to_quat(Gl, q, inv, gq);
+      if (out.actor_pose) {
+        const float ml[3] = {__ldg(P.means + 3 * g), __ldg(P.means + 3 * g + 1), __ldg(P.means + 3 * g + 2)};
+        float Ga[9];  // G R_l^T + dL/dmu_w mu_l^T
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            Ga[3 * i + j] = G[3 * i] * Rl[3 * j] + G[3 * i + 1] * Rl[3 * j + 1] + G[3 * i + 2] * Rl[3 * j + 2] +
+                            v[i] * ml[j];
+        float dqa[4];
+        rot_grad_to_quat(Ga, qa, inva, dqa);
+        float* o = out.actor_pose + 7 * (size_t)a;
+        if (dqa[0] != 0.f || dqa[1] != 0.f || dqa[2] != 0.f || dqa[3] != 0.f || v[0] != 0.f || v[1] != 0.f ||
+            v[2] != 0.f) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) atomicAdd(o + c, dqa[c]);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) atomicAdd(o + 4 + c, v[c]);
+        }
+      }
+    }
   }
+  if (!in_range) gm[0] = gm[1] = gm[2] = 0.f;
+  for (int c = 0; c < 3; ++c) out.means[3 * g + c] = gm[c];
   reinterpret_cast<float4*>(out.quats)[g] = make_float4(gq[0], gq[1], gq[2], gq[3]);
   for (int c = 0; c < 3; ++c) out.scales[3 * g + c] = gs[c];
   float b[16];
-  sh_basis3(__ldg(view_dir + 3 * g), __ldg(view_dir + 3 * g + 1), __ldg(view_dir + 3 * g + 2), b);
-  float* o = out.sh + (size_t)g * ncoef * 3;
-  for (int k = 0; k < ncoef; ++k)
+  sh_basis3(__ldg(P.view_dir + 3 * g), __ldg(P.view_dir + 3 * g + 1), __ldg(P.view_dir + 3 * g + 2), b);
+  float* o = out.sh + (size_t)g * P.ncoef * 3;
+  for (int k = 0; k < P.ncoef; ++k)
 #pragma unroll
     for (int c = 0; c < 3; ++c) o[3 * k + c] = b[k] * v[13 + c];
 }
@@ -1450,9 +1512,13 @@ int32_t bwd_common_checks(const simuli_gaussians* G, const simuli_projected* pro
     set_error("%s: workspace too small / workspace or quats gradient not 16-byte aligned", what);
     return SIMULI_ERR_INVALID_ARGUMENT;
   }
-  if (rp->sh || G->actor_id) {
-    set_error("%s: per-ray SH / scene-graph particles have no backward (A31)", what);
+  if (rp->sh) {
+    set_error("%s: per-ray SH has no backward (A31)", what);
     return SIMULI_ERR_UNSUPPORTED;
+  }
+  if (G->actor_id && (G->n_actors < 1 || !G->actor_pose)) {
+    set_error("%s: actor_id needs n_actors >= 1 and actor_pose", what);
+    return SIMULI_ERR_INVALID_ARGUMENT;
   }
   if (G->sh_degree < 0 || G->sh_degree > 3) {
     set_error("%s: sh_degree not in 0..3", what);
@@ -1474,10 +1540,20 @@ void bwd_fill_common(BwdArgs& A, const simuli_projected* proj, const uint32_t* i
 
 int32_t bwd_params(const simuli_gaussians* G, const simuli_projected* proj, const simuli_gaussian_grads* gout,
                    const float* ws, cudaStream_t st, const char* what) {
-  const int ncoef = (G->sh_degree + 1) * (G->sh_degree + 1);
-  if (G->n > 0)
-    k_backward_params<<<(unsigned)((G->n + 255) / 256), 256, 0, st>>>(ws, G->quats, G->scales, proj->view_dir,
-                                                                       ncoef, G->n, *gout);
+  ParamsArgs P{};
+  P.ws = ws; P.means = G->means; P.quats = G->quats; P.scales = G->scales; P.view_dir = proj->view_dir;
+  P.ncoef = (G->sh_degree + 1) * (G->sh_degree + 1);
+  P.n = G->n;
+  simuli_gaussian_grads o = *gout;
+  if (G->actor_id) {
+    P.actor_id = G->actor_id;
+    P.actor_pose = reinterpret_cast<const float*>(G->actor_pose);
+    P.n_actors = G->n_actors;
+    if (o.actor_pose) cudaMemsetAsync(o.actor_pose, 0, sizeof(float) * 7 * (size_t)G->n_actors, st);
+  } else {
+    o.actor_pose = nullptr;
+  }
+  if (G->n > 0) k_backward_params<<<(unsigned)((G->n + 255) / 256), 256, 0, st>>>(P, o);
   return launch_check(what);
 }
 

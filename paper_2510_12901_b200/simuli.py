@@ -97,7 +97,7 @@ class CameraGradIn(C.Structure):
 
 
 class GaussianGrads(C.Structure):
-    _fields_ = [(k, C.c_void_p) for k in ("means", "quats", "scales", "opacity", "sh")]
+    _fields_ = [(k, C.c_void_p) for k in ("means", "quats", "scales", "opacity", "sh", "actor_pose")]
 
 
 class CameraCompose(C.Structure):
@@ -277,10 +277,11 @@ def simuli_backward_workspace_size(n):
 def _grad_structs(frame, grads, names, gin_cls, fwd):
     import torch
     sc = frame.scene
-    out = {k: torch.empty_like(sc[k]) for k in ("means", "quats", "scales", "opacity", "sh")}
+    keys = ("means", "quats", "scales", "opacity", "sh") + (("actor_pose",) if sc.get("actor_pose") is not None else ())
+    out = {k: torch.empty_like(sc[k]) for k in keys}  # with a scene graph: object-frame and pose gradients
     gin = gin_cls(*[_ptr(grads.get(k)) if grads.get(k) is not None else None for k in names],
                   *[_ptr(t) if t is not None else None for t in fwd])
-    gout = GaussianGrads(*[_ptr(out[k]) for k in ("means", "quats", "scales", "opacity", "sh")])
+    gout = GaussianGrads(*[_ptr(out[k]) for k in keys])
     return out, gin, gout
 
 

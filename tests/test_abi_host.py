@@ -38,7 +38,7 @@ def test_exports_every_header_symbol(lib):
     exported = {ln.split()[-1] for ln in nm.splitlines() if " T " in ln}
     assert set(syms) <= exported
     assert set(lib.EXPORTED) == set(syms)
-    assert L.simuli_abi_version() == 6
+    assert L.simuli_abi_version() == 7
 
 
 def test_library_is_sm100a(lib):
@@ -132,8 +132,8 @@ def test_workspace_size_and_bad_args(lib):
 
 def test_backward_argument_errors(lib):
     """Host-side checks of simuli_backward_* (no device memory is touched: dummy aligned
-    addresses): missing view_dir -> INVALID_ARGUMENT, per-ray SH / scene graph /
-    beam divergence -> UNSUPPORTED (A31), small workspace -> INVALID_ARGUMENT."""
+    addresses): missing view_dir -> INVALID_ARGUMENT, per-ray SH -> UNSUPPORTED (A31),
+    small workspace or a scene graph without poses -> INVALID_ARGUMENT."""
     C = ctypes
     L = lib.load()
     fake = 1 << 20  # never dereferenced: every check below fails before a launch
@@ -154,5 +154,5 @@ def test_backward_argument_errors(lib):
     rp.sh = fake
     assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_UNSUPPORTED
     rp.sh = None
-    G.actor_id, G.actor_pose, G.n_actors = fake, fake, 1
-    assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_UNSUPPORTED
+    G.actor_id, G.actor_pose, G.n_actors = fake, None, 1  # scene graph without poses
+    assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_INVALID_ARGUMENT

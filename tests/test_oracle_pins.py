@@ -1081,3 +1081,59 @@ def test_backward_camera_vs_finite_differences(oracle_mod):
                     bad += 1
                     print("mismatch", i, key, c, fd, an)
     assert checked == 4 * 11 and bad <= 2, bad
+
+
+def test_backward_scene_graph_vs_finite_differences(oracle_mod):
+    """O16 through the scene graph (A29, A31): gradients of object-frame particle
+    parameters and of the object poses (q_a, t_a) against central differences of the
+    oracle's forward."""
+    O = oracle_mod
+    cfg = S.lidar_config("tiny")
+    base = S.scene_for("tiny", seed=21, n=80)
+    sc = S.with_actors(base, 22, n_actors=2, per_actor=60, x_range=(3.0, 6.0))
+    sc["actor_pose"][:, 5] = np.array([2.5, -3.0], np.float32)  # near the sensor, inside the beams
+    sc["actor_pose"][:, 6] = 0.6
+    sc["sh"] = np.ascontiguousarray(sc["sh"][:, :1])
+    fwd = O.render_lidar(sc, cfg)
+    R = fwd["opacity"].shape[0]
+    rng = np.random.default_rng(23)
+    g = {"zeta": rng.normal(size=(R, 3)), "opacity": rng.normal(size=R), "depth_accum": 0.1 * rng.normal(size=R),
+         "depth": 0.1 * rng.normal(size=R), "intensity": rng.normal(size=R), "raydrop": rng.normal(size=R)}
+    b = O.backward_lidar(sc, cfg, g)
+    ids = sc["actor_id"]
+    assert np.abs(b["actor_pose"]).max() > 0
+
+    def fd(key, idx, h):
+        vals, deltas = [], []
+        for sgn in (1, -1):
+            s2 = {k: v.copy() for k, v in sc.items()}
+            arr = s2[key].reshape(s2[key].shape[0], -1)
+            x0 = np.float32(arr[idx])
+            arr[idx] = np.float32(x0 + sgn * h * max(1.0, abs(float(x0))))
+            deltas.append(float(arr[idx]) - float(x0))
+            vals.append(_loss(O, s2, cfg, g))
+        return (vals[0] - vals[1]) / (deltas[0] - deltas[1])
+
+    checked = bad = 0
+    for a in range(2):
+        for c in range(7):
+            an = b["actor_pose"][a, c]
+            num = fd("actor_pose", (a, c), 1e-4)
+            checked += 1
+            # a pose step moves every object mean, and the forward rounds each world mean to
+            # float32 (A29): ~2.4e-7 m of quantisation per particle against a 1e-4 x 3 m step
+            # puts ~1e-2 of noise on the difference quotient (measured agreement 1e-4 .. 3e-2)
+            if abs(num - an) > 2e-3 * abs(an) + 0.05:
+                bad += 1
+                print("mismatch pose", a, c, num, an)
+    top = [i for i in np.argsort(-np.abs(b["opacity"])) if ids[i] >= 0][:3]
+    for i in top:
+        for key, h, dims in (("means", 2e-4, 3), ("quats", 2e-4, 4), ("scales", 1e-4, 3)):
+            for c in range(dims):
+                an = b[key].reshape(len(ids), -1)[i, c]
+                num = fd(key, (i, c), h)
+                checked += 1
+                if abs(num - an) > 2e-3 * max(1.0, abs(an)):
+                    bad += 1
+                    print("mismatch", i, key, c, num, an)
+    assert checked == 14 + 3 * 10 and bad <= 2, bad
