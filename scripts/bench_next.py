@@ -49,12 +49,23 @@ rows.append(("B + per-ray SH (NEXT-2, A30)", stages(SM.LidarRenderer(cfgB, devB,
 sa = synth.with_actors(sceneB, 7, n_actors=64, per_actor=3000, x_range=(-60.0, 60.0))
 rows.append(("B + 64 objects x 3000 particles in object frames (2.19M particles; NEXT-3, A29)",
              stages(SM.LidarRenderer(cfgB, SM.to_device_scene(sa)))))
-del devB
+# NEXT-3 x NEXT-4: backward through the scene graph (object-frame + object-pose gradients)
+fa = SM.LidarRenderer(cfgB, SM.to_device_scene(sa))
+fa.requires_grad(True)
+fa.scan(sync_capacity=True)
+ga = {k: torch.randn(fa.n_rays, device="cuda") for k in ("opacity", "depth")}
+ga["zeta"] = torch.randn(fa.n_rays, 3, device="cuda")
+torch.cuda.synchronize()
+bwd_sg = {"forward_us": timed(lambda: fa.scan()), "backward_us": timed(lambda: fa.backward(ga))}
+del fa, devB
 torch.cuda.empty_cache()
 
 # NEXT-3b: Eq. 2 composition on config D
 camD, sceneD = synth.camera_config("D"), synth.scene_for("D")
-c = SM.CameraRenderer(camD, SM.to_device_scene(sceneD))
+devD = SM.to_device_scene(sceneD)
+cam_stages = {"D": stages(SM.CameraRenderer(camD, devD), lidar=False),
+              "D + per-ray SH": stages(SM.CameraRenderer(camD, devD, per_ray_sh=True), lidar=False)}
+c = SM.CameraRenderer(camD, devD)
 c.frame(sync_capacity=True)
 rng = np.random.default_rng(3)
 env = torch.from_numpy(rng.uniform(0, 1, (512, 1024, 3)).astype(np.float32)).cuda()
@@ -90,7 +101,8 @@ for name in ("B", "C", "D"):
     del f
     torch.cuda.empty_cache()
 
-out = {"lidar_stages_us": {k: v for k, v in rows}, "compose_D": compose, "backward": bwd,
+out = {"lidar_stages_us": {k: v for k, v in rows}, "camera_stages_us": cam_stages, "compose_D": compose,
+       "backward": bwd, "backward_scene_graph_B": bwd_sg,
        "gpu": torch.cuda.get_device_name(0)}
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 json.dump(out, open(os.path.join(ROOT, "profiles", "r01_next.json"), "w"), indent=1)
@@ -104,13 +116,19 @@ for k, v in rows:
 na = sa["means"].shape[0]
 md += ["", f"Projection cost per particle: baseline {base['project'] / 2e6 * 1e3:.3f} ns, with the scene graph "
            f"{rows[-1][1]['project'] / na * 1e3:.3f} ns ({na} particles, 192k of them in 64 object frames)."]
+md += ["", "## Camera config D stages (µs)", "", "| variant | project | bin_sort | render | sum |", "|---|---|---|---|---|"]
+for k, v in cam_stages.items():
+    md.append(f"| {k} | {v['project']:.1f} | {v['bin_sort']:.1f} | {v['render']:.1f} | "
+              f"{v['project'] + v['bin_sort'] + v['render']:.1f} |")
 md += ["", "## Eq. 2 composition, config D (1920x1080)", "",
        f"{compose['us']:.1f} µs for {px} pixels; algorithmic HBM bytes {comp_bytes / 1e6:.1f} MB "
-       f"(rgb + omega in, rgb out) -> {compose['GB/s']:.0f} GB/s (env map 512x1024 and 16x16x8 grid stay in L2). The pass is FP64-bound, not HBM-bound: per pixel the KB inverse (Newton, double), the row pose (double slerp) and the equirectangular angles (double atan2 / acos) -- the same inverse lens model as the render kernel, kept in double for parity.",
+       f"(rgb + omega in, rgb out) -> {compose['GB/s']:.0f} GB/s (env map 512x1024 and 16x16x8 grid stay in L2). Not HBM-bound: per pixel the KB inverse (Newton, double) and the equirectangular angles (double atan2 / acos) -- the same inverse lens model as the render kernel, kept in double for parity -- and 24 float4 grid-cell reads for the trilinear affine (scripts/bench_compose.py: env only ~80 µs, grid only ~49 µs).",
        "", "## Backward (A31)", "", "| config | forward scan/frame µs | backward µs | ratio | backward without forward totals µs |",
        "|---|---|---|---|---|"]
 for k, v in bwd.items():
     md.append(f"| {k} | {v['forward_us']:.1f} | {v['backward_us']:.1f} | {v['backward_us'] / v['forward_us']:.2f} | "
               f"{v['backward_own_totals_us']:.1f} |")
+md += ["", f"Backward through the scene graph (B + 64 objects, object-frame and object-pose gradients): "
+           f"forward {bwd_sg['forward_us']:.1f} µs, backward {bwd_sg['backward_us']:.1f} µs."]
 open(os.path.join(ROOT, "profiles", "r01_next.md"), "w").write("\n".join(md) + "\n")
 print("\n".join(md))
