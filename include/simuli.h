@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 7
+#define SIMULI_ABI_VERSION 8
 
 enum {
   SIMULI_OK = 0,
@@ -381,14 +381,14 @@ int32_t simuli_backward_workspace_size(int64_t n, size_t* bytes);
  * Errors: INVALID_ARGUMENT (NULL, view_dir missing, workspace too small), UNSUPPORTED
  * (see above), CUDA. */
 int32_t simuli_backward_lidar(const simuli_gaussians* gaussians, const simuli_projected* proj,
-                              const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                              const uint32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
                               const simuli_project_params* params, const simuli_render_params* rparams,
                               const simuli_lidar_grad_in* grad_in, simuli_gaussian_grads* grad_out,
                               void* workspace, size_t workspace_bytes, void* stream);
 
 /* Camera backward: as simuli_backward_lidar, one CTA per tile (pixel per thread). */
 int32_t simuli_backward_camera(const simuli_gaussians* gaussians, const simuli_projected* proj,
-                               const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                               const uint32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
                                const simuli_project_params* params, const simuli_render_params* rparams,
                                const simuli_camera_grad_in* grad_in, simuli_gaussian_grads* grad_out,
                                void* workspace, size_t workspace_bytes, void* stream);

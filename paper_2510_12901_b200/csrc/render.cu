@@ -1013,6 +1013,7 @@ struct BwdArgs {
   const float4* record;
   const uint32_t* ids;
   const int2* ranges;
+  const int* order;  // longest-first tile order or NULL
   const int *tile_ray_off, *tile_rays;  // LiDAR
   const float *ray_az, *ray_el, *ray_s;
   int n_az, chunks;
@@ -1295,7 +1296,8 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
 }
 
 __global__ void __launch_bounds__(32) k_backward_lidar(const BwdArgs A) {
-  const int tile = (int)(blockIdx.x / A.chunks), chunk = (int)(blockIdx.x % A.chunks);
+  const int slot = (int)(blockIdx.x / A.chunks), chunk = (int)(blockIdx.x % A.chunks);
+  const int tile = A.order ? __ldg(A.order + slot) : slot;
   const int lane = threadIdx.x;
   const int off0 = __ldg(A.tile_ray_off + tile), off1 = __ldg(A.tile_ray_off + tile + 1);
   const int k = off0 + chunk * 32 + lane;
@@ -1343,7 +1345,8 @@ template <int TP>
 __global__ void __launch_bounds__(32) k_backward_camera(const BwdArgs A) {
   constexpr int STRIPS = TP * TP / 32;
   const CameraArgs& C = A.cam;
-  const int tile = (int)(blockIdx.x / STRIPS), strip = (int)(blockIdx.x % STRIPS);
+  const int slot = (int)(blockIdx.x / STRIPS), strip = (int)(blockIdx.x % STRIPS);
+  const int tile = A.order ? __ldg(A.order + slot) : slot;
   const int lane = threadIdx.x;
   const int ty = tile / C.Wt, tx = tile % C.Wt;
   const int idx = strip * 32 + lane;
@@ -1569,7 +1572,7 @@ extern "C" int32_t simuli_backward_workspace_size(int64_t n, size_t* bytes) {
 }
 
 extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli_projected* proj,
-                                         const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                                         const uint32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
                                          const simuli_project_params* P, const simuli_render_params* rp,
                                          const simuli_lidar_grad_in* gin, simuli_gaussian_grads* gout,
                                          void* workspace, size_t workspace_bytes, void* stream) {
@@ -1589,6 +1592,7 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
                  "simuli_backward_lidar: incomplete device tiling");
   BwdArgs A{};
   bwd_fill_common(A, proj, sorted_ids, tile_ranges, P, rp, workspace, G->n);
+  A.order = tile_order;
   A.tile_ray_off = T.tile_ray_offsets; A.tile_rays = T.tile_rays;
   A.ray_az = T.ray_az; A.ray_el = T.ray_el; A.ray_s = T.ray_s;
   A.n_az = T.n_azimuth;
@@ -1610,7 +1614,7 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
 }
 
 extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simuli_projected* proj,
-                                          const uint32_t* sorted_ids, const int32_t* tile_ranges,
+                                          const uint32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
                                           const simuli_project_params* P, const simuli_render_params* rp,
                                           const simuli_camera_grad_in* gin, simuli_gaussian_grads* gout,
                                           void* workspace, size_t workspace_bytes, void* stream) {
@@ -1628,6 +1632,7 @@ extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simul
   }
   BwdArgs A{};
   bwd_fill_common(A, proj, sorted_ids, tile_ranges, P, rp, workspace, G->n);
+  A.order = tile_order;
   CameraArgs& K = A.cam;
   K.model = C.model; K.width = C.width; K.height = C.height; K.rolling = C.rolling_shutter; K.tile_px = C.tile_px;
   K.Wt = (C.width + C.tile_px - 1) / C.tile_px;

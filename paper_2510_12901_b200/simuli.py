@@ -167,7 +167,7 @@ def load():
                                        C.c_void_p]
     L.simuli_backward_workspace_size.argtypes = [C.c_int64, C.POINTER(C.c_size_t)]
     for nm, gin in (("simuli_backward_lidar", LidarGradIn), ("simuli_backward_camera", CameraGradIn)):
-        getattr(L, nm).argtypes = [C.POINTER(Gaussians), C.POINTER(Projected), C.c_void_p, C.c_void_p,
+        getattr(L, nm).argtypes = [C.POINTER(Gaussians), C.POINTER(Projected), C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(gin),
                                    C.POINTER(GaussianGrads), C.c_void_p, C.c_size_t, C.c_void_p]
     L.simuli_compose_camera.argtypes = [C.POINTER(ProjectParams), C.POINTER(CameraCompose), C.c_void_p, C.c_void_p,
@@ -302,7 +302,7 @@ def simuli_backward(frame, grads, stream=None, use_forward_totals=True):
     ws = frame._bwd_workspace()
     fn = load().simuli_backward_lidar if lidar else load().simuli_backward_camera
     _check(fn(C.byref(frame.gauss), C.byref(frame.projected), _ptr(frame.sorted_ids), _ptr(frame.tile_ranges),
-              C.byref(frame.params), C.byref(frame.rparams), C.byref(gin), C.byref(gout), _ptr(ws), ws.numel(),
+              _ptr(frame.tile_order), C.byref(frame.params), C.byref(frame.rparams), C.byref(gin), C.byref(gout), _ptr(ws), ws.numel(),
               _stream(stream)))
     frame._keep_grads = grads  # alive until the enqueued work has run
     return out

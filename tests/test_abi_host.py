@@ -38,7 +38,7 @@ def test_exports_every_header_symbol(lib):
     exported = {ln.split()[-1] for ln in nm.splitlines() if " T " in ln}
     assert set(syms) <= exported
     assert set(lib.EXPORTED) == set(syms)
-    assert L.simuli_abi_version() == 7
+    assert L.simuli_abi_version() == 8
 
 
 def test_library_is_sm100a(lib):
@@ -126,7 +126,7 @@ def test_workspace_size_and_bad_args(lib):
     assert L.simuli_backward_workspace_size(1000, ctypes.byref(size)) == lib.SIMULI_OK and size.value == 1000 * 64
     assert L.simuli_backward_workspace_size(-1, ctypes.byref(size)) == lib.SIMULI_ERR_INVALID_ARGUMENT
     for fn in (L.simuli_backward_lidar, L.simuli_backward_camera):
-        assert fn(None, None, None, None, None, None, None, None, None, 0, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
+        assert fn(None, None, None, None, None, None, None, None, None, None, 0, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
         assert b"NULL" in L.simuli_last_error()
 
 
@@ -145,7 +145,7 @@ def test_backward_argument_errors(lib):
     cam = lib.Camera(1, 64, 48, 50.0, 50.0, 32.0, 24.0, (C.c_float * 5)(0, 0, 0, 0, 0), 1, 0.05, 1.7, 16)
     P = lib.ProjectParams(lib.SENSOR_CAMERA, None, None, C.pointer(cam), lib.make_pose({"q": [1, 0, 0, 0], "t": [0, 0, 0]}),
                           lib.make_pose({"q": [1, 0, 0, 0], "t": [0, 0, 0]}), 1, 1.0, 2.0, 0.0, 3.0, 0, 0)
-    args = lambda ws: (C.byref(G), C.byref(proj), fake, fake, C.byref(P), C.byref(rp), C.byref(gin),  # noqa: E731
+    args = lambda ws: (C.byref(G), C.byref(proj), fake, fake, None, C.byref(P), C.byref(rp), C.byref(gin),  # noqa: E731
                        C.byref(gout), fake, ws, None)
     assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_INVALID_ARGUMENT
     assert b"view_dir" in L.simuli_last_error()
