@@ -340,7 +340,9 @@ int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorte
  * is: alpha = min(alpha_max, sigma rho(tau_max)) with tau_max and delta^2 of the
  * canonical transform M = diag(1/s) R(q/|q|)^T (clamped alpha: no gradient).  Features are
  * the per-particle SH at the projection's view direction (A17), held fixed (no gradient
- * through the direction).  Not supported (UNSUPPORTED): beam divergence, per-ray SH.
+ * through the direction); with rparams->sh (per-ray SH, A30) the features are SH_i(d) per
+ * ray and the SH gradient sums Y_k(d) dL/dzeta alpha T over the rays (float atomics into
+ * grad_out->sh).  Not supported (UNSUPPORTED): beam divergence.
  * Upstream gradients (device, [n_rays] or [n_rays][3]; NULL = 0): LiDAR zeta, opacity
  * (omega), depth_accum (D), depth (D / omega), intensity (zeta_0), raydrop
  * (1 / (1 + exp(zeta_1 - zeta_2))); camera rgb (c_f), opacity, depth_accum, depth. */

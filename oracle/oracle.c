@@ -1428,7 +1428,7 @@ int or_backward_composite(const double* mu, const double* Mrows, const double* s
                           const int32_t* ray_tile, const float* ray_a, const float* ray_b, const double* ray_od,
                           const int32_t* ray_valid, const or_render_params* p, const double* g_feat,
                           const double* g_opacity, const double* g_daccum, double* d_mu, double* d_M,
-                          double* d_sigma, double* d_feat) {
+                          double* d_sigma, double* d_feat, double* d_sh) {
   int64_t max_len = 0;
   for (int32_t r = 0; r < n_rays; ++r) {
     const int32_t t = ray_tile[r];
@@ -1484,7 +1484,22 @@ int or_backward_composite(const double* mu, const double* Mrows, const double* s
         for (int k = K - 1; k >= 0; --k) {
           const uint32_t g = kg[k];
           const double alpha = ka[4 * k], tau = ka[4 * k + 1], Tk = ka[4 * k + 2], rho = ka[4 * k + 3];
-          const double* f = &feat[(int64_t)g * 3];
+          double f[3] = {feat[(int64_t)g * 3], feat[(int64_t)g * 3 + 1], feat[(int64_t)g * 3 + 2]};
+          double Y[16];
+          const int nco = p->sh ? (p->sh_degree + 1) * (p->sh_degree + 1) : 0;
+          if (p->sh) { /* per-ray SH (A30): f = SH_g(d) and the basis Y_k(d), through O9 */
+            double dn[3], shd[48];
+            const double dl = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+            for (int c = 0; c < 3; ++c) dn[c] = d[c] / dl;
+            for (int q = 0; q < nco * 3; ++q) shd[q] = p->sh[(int64_t)g * nco * 3 + q];
+            or_sh_eval(shd, p->sh_degree, dn, f);
+            for (int q = 0; q < nco; ++q) {
+              double e[48] = {0}, yq[3];
+              e[3 * q] = 1.0;
+              or_sh_eval(e, p->sh_degree, dn, yq);
+              Y[q] = yq[0];
+            }
+          }
           const double wk = alpha * Tk;
           const double gzf = Gz[0] * f[0] + Gz[1] * f[1] + Gz[2] * f[2];
           const double dalpha = Tk * (gzf + Go + GD * tau) - (Sf + Go * S1 + GD * St) / (1.0 - alpha);
@@ -1520,6 +1535,9 @@ int or_backward_composite(const double* mu, const double* Mrows, const double* s
               d_feat[(int64_t)g * 3 + a] += Gz[a] * wk;
             }
             d_sigma[g] += dsig;
+            if (p->sh && d_sh) /* dL/dc_qc = Y_q(d) Gz_c w (A30, A31) */
+              for (int q = 0; q < nco; ++q)
+                for (int c = 0; c < 3; ++c) d_sh[((int64_t)g * nco + q) * 3 + c] += Y[q] * Gz[c] * wk;
           }
           Sf += wk * gzf;
           S1 += wk;

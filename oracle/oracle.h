@@ -172,13 +172,14 @@ int or_compose_camera(const or_camera* C, const double* ray_od, const double* rg
  * forward contributions are collected in list order (same rules as or_composite) and
  * dL/d(mu, M, sigma, f) of every contributing particle accumulated from the upstream
  * gradients g_feat [R][3], g_opacity [R], g_daccum [R] (NULL = 0).  Outputs [n][3], [n][9],
- * [n], [n][3] are accumulated (caller zeroes). */
+ * [n], [n][3] are accumulated (caller zeroes); with p->sh (per-ray SH, A30) the features are
+ * SH_g(d) per ray and d_sh [n][(deg+1)^2][3] accumulates dL/dSH directly. */
 int or_backward_composite(const double* mu, const double* Mrows, const double* sigma, const double* feat,
                           const float* box, const uint32_t* ids, const int32_t* ranges, int32_t n_rays,
                           const int32_t* ray_tile, const float* ray_a, const float* ray_b, const double* ray_od,
                           const int32_t* ray_valid, const or_render_params* p, const double* g_feat,
                           const double* g_opacity, const double* g_daccum, double* d_mu, double* d_M,
-                          double* d_sigma, double* d_feat);
+                          double* d_sigma, double* d_feat, double* d_sh);
 /* O16: chain to the particle parameters: M = diag(1/s) R(q/|q|)^T -> dq, ds;
  * f = SH(v) -> dSH (v = the projection's view direction, no gradient through v, A31). */
 void or_backward_params(int64_t n, const float* quats, const float* scales, const double* viewdir,

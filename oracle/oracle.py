@@ -126,7 +126,7 @@ def lib():
         L.or_set_threads.argtypes = [C.c_int]
         L.or_backward_composite.argtypes = [f64p, f64p, f64p, f64p, f32p, u32p, i32p, C.c_int32, i32p, f32p, f32p,
                                             f64p, i32p, C.POINTER(OrRenderParams), f64p, f64p, f64p, f64p, f64p,
-                                            f64p, f64p]
+                                            f64p, f64p, f64p]
         L.or_backward_params.argtypes = [C.c_int64, f32p, f32p, f64p, C.c_int32, f64p, f64p, f64p, f64p, f64p]
         L.or_backward_params_sg.argtypes = [C.c_int64, f32p, f32p, f32p, f64p, C.c_int32, i32p, C.c_int32, f64p,
                                             f64p, f64p, f64p, f64p, f64p, f64p, f64p, f64p]
@@ -598,6 +598,12 @@ def backward_composite(records, ids, ranges, ray_tile, ray_a, ray_b, ray_od, Gz,
     prm = OrRenderParams(float(np.float32(near)), float(np.float32(alpha_min)), float(np.float32(alpha_max)),
                          float(np.float32(T_min)), int(wrap), pf, tpf, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0)
     out = {"mu": np.zeros((n, 3)), "M": np.zeros((n, 9)), "sigma": np.zeros(n), "feat": np.zeros((n, 3))}
+    sh = records.get("sh")  # per-ray SH (A30): dL/dSH accumulated per (ray, particle)
+    if sh is not None:
+        sh = np.ascontiguousarray(sh, np.float32).reshape(n, -1)
+        prm.sh = sh.ctypes.data
+        prm.sh_degree = {3: 0, 12: 1, 27: 2, 48: 3}[sh.shape[1]]
+        out["sh_perray"] = np.zeros((n, sh.shape[1] // 3, 3))
     mu, Mr, sg, ft = _d(records["mu"]), _d(records["Mrows"]), _d(records["sigma"]), _d(records["feat"])
     box = np.ascontiguousarray(records["box"], np.float32)
     ids = np.ascontiguousarray(ids, np.uint32)
@@ -610,7 +616,7 @@ def backward_composite(records, ids, ranges, ray_tile, ray_a, ray_b, ray_od, Gz,
                                      _p(ids, u32p), _p(ranges, i32p), int(rt.shape[0]), _p(rt, i32p), _p(ra, f32p),
                                      _p(rb, f32p), _p(od, f64p), _p(rv, i32p), C.byref(prm), _p(Gz, f64p),
                                      _p(Go, f64p), _p(GD, f64p), _p(out["mu"], f64p), _p(out["M"], f64p),
-                                     _p(out["sigma"], f64p), _p(out["feat"], f64p))
+                                     _p(out["sigma"], f64p), _p(out["feat"], f64p), _p(out.get("sh_perray"), f64p))
     assert rc == 0
     return out
 
@@ -635,6 +641,8 @@ def backward_params(scene, proj, d):
                                     _p(out["quats"], f64p), _p(out["scales"], f64p), _p(out["sh"], f64p),
                                     _p(out["actor_pose"], f64p))
         out["opacity"] = d["sigma"].copy()
+        if d.get("sh_perray") is not None:
+            out["sh"] = d["sh_perray"].copy()
         return out
     n = int(scene["means"].shape[0])
     q = np.ascontiguousarray(scene["quats"], np.float32)
@@ -645,20 +653,24 @@ def backward_params(scene, proj, d):
     vd = _d(proj["viewdir"])
     lib().or_backward_params(n, _p(q, f32p), _p(s, f32p), _p(vd, f64p), deg, _p(_d(d["M"]), f64p),
                              _p(_d(d["feat"]), f64p), _p(gq, f64p), _p(gs, f64p), _p(gsh, f64p))
+    if d.get("sh_perray") is not None:  # per-ray SH: the SH gradient came from O15 directly
+        gsh = d["sh_perray"].copy()
     return {"means": d["mu"].copy(), "quats": gq, "scales": gs, "opacity": d["sigma"].copy(), "sh": gsh}
 
 
 def backward_lidar(scene, cfg, grads, tiling: Tiling | None = None, pose0=None, pose1=None, K=None, ut=None,
-                   alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4):
+                   alpha_min=1.0 / 255.0, alpha_max=0.99, T_min=1e-4, per_ray_sh=False):
     """Whole-path LiDAR backward (O1-O12 forward, O15, O16).  grads: upstream gradients by
     output name (zeta, opacity, depth_accum, depth, intensity, raydrop; missing = 0)."""
     tiling = tiling or Tiling(cfg)
     pose0 = pose0 or cfg.pose_start
     pose1 = pose1 or cfg.pose_end
     fwd = render_lidar(scene, cfg, tiling=tiling, pose0=pose0, pose1=pose1, K=K, ut=ut, alpha_min=alpha_min,
-                       alpha_max=alpha_max, T_min=T_min)
+                       alpha_max=alpha_max, T_min=T_min, per_ray_sh=per_ray_sh)
     proj = fwd["proj"]
     rec = records_from_projection(proj, scene)
+    if per_ray_sh:
+        rec["sh"] = scene["sh"]
     count, rect = cull_lidar(proj["valid"], proj["box"], tiling, True)
     _, ids, ranges = bin_pairs(count, rect, proj["key"], tiling.n_tiles, tiling.n_theta)
     Gz, Go, GD = fold_upstream(fwd, grads, lidar=True)

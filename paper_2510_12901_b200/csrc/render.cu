@@ -1023,6 +1023,9 @@ struct BwdArgs {
   float near_tau, alpha_min, alpha_max, T_min;
   const float *g_feat, *g_opacity, *g_daccum, *g_depth, *g_intensity, *g_raydrop;
   const float *f_feat, *f_opacity, *f_daccum;  // forward totals (optional: skip pass 1)
+  const float* sh;  // per-ray SH (A30) or NULL
+  int sh_ncoef;
+  float* dsh;       // per-ray SH: dL/dSH accumulated here (the caller's gradient array)
   float* ws;  // [n][16]
   int64_t n;
 };
@@ -1187,7 +1190,7 @@ __device__ __forceinline__ float warp_reduce16(float v[16], int lane) {
 template <bool LIDAR, typename Member>
 __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF& rf, bool live, int ray,
                                                     int2 rg, const float* ra, const float* rb, float4 (*srec)[5],
-                                                    Member member) {
+                                                    const float shb[16], Member member) {
   const int lane = threadIdx.x & 31;
   // ---- pass 1: totals
   float T = 1.f, z0 = 0.f, z1 = 0.f, z2 = 0.f, D = 0.f, W = 0.f;
@@ -1200,7 +1203,7 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
       W = __ldg(A.f_opacity + ray);
       D = __ldg(A.f_daccum + ray);
     }
-  } else walk_list(A, rg, done, ra, rb, srec, member, [&](bool m, uint32_t, const float4 r[4]) {
+  } else walk_list(A, rg, done, ra, rb, srec, member, [&](bool m, uint32_t gid, const float4 r[4]) {
     if (!m) return;
     float alpha, tau, rho;
     bool cl;
@@ -1211,9 +1214,11 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
       return;
     }
     const float w = alpha * T;
-    z0 = fmaf(w, r[3].y, z0);
-    z1 = fmaf(w, r[3].z, z1);
-    z2 = fmaf(w, r[3].w, z2);
+    float f[3] = {r[3].y, r[3].z, r[3].w};
+    if (A.sh) sh_dot(A.sh + (size_t)gid * A.sh_ncoef * 3, A.sh_ncoef, shb, f);  // as the per-ray forward
+    z0 = fmaf(w, f[0], z0);
+    z1 = fmaf(w, f[1], z1);
+    z2 = fmaf(w, f[2], z2);
     D = fmaf(w, tau, D);
     W += w;
     T = T * (1.f - alpha);
@@ -1251,6 +1256,7 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
 #pragma unroll
     for (int q = 0; q < kBwdVals; ++q) v[q] = 0.f;
     bool contributed = false;
+    float wsh = 0.f;  // this lane's weight alpha T (per-ray SH gradient)
     if (m) {
       float alpha, tau, rho;
       bool cl;
@@ -1259,12 +1265,15 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
       if (st == 1) {
         contributed = true;
         const float w = alpha * T;
-        pz0 = fmaf(w, r[3].y, pz0);
-        pz1 = fmaf(w, r[3].z, pz1);
-        pz2 = fmaf(w, r[3].w, pz2);
+        float f[3] = {r[3].y, r[3].z, r[3].w};
+        if (A.sh) sh_dot(A.sh + (size_t)g * A.sh_ncoef * 3, A.sh_ncoef, shb, f);
+        pz0 = fmaf(w, f[0], pz0);
+        pz1 = fmaf(w, f[1], pz1);
+        pz2 = fmaf(w, f[2], pz2);
         pD = fmaf(w, tau, pD);
         pW += w;
-        const float gzf = Gz[0] * r[3].y + Gz[1] * r[3].z + Gz[2] * r[3].w;
+        wsh = w;
+        const float gzf = Gz[0] * f[0] + Gz[1] * f[1] + Gz[2] * f[2];
         const float suf = (tot_f - (Gz[0] * pz0 + Gz[1] * pz1 + Gz[2] * pz2)) + Go * (W - pW) + GD * (D - pD);
         const float dalpha = T * (gzf + Go + GD * tau) - suf / (1.f - alpha);
         const float dtau = GD * w;
@@ -1279,17 +1288,27 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
         response_grad(rf, mu, M, dtau, dd2, g12);
 #pragma unroll
         for (int q = 0; q < 12; ++q) v[q] = g12[q];
-        v[13] = Gz[0] * w;
-        v[14] = Gz[1] * w;
-        v[15] = Gz[2] * w;
+        if (!A.sh) {
+          v[13] = Gz[0] * w;
+          v[14] = Gz[1] * w;
+          v[15] = Gz[2] * w;
+        }
         T = T * (1.f - alpha);
       }
     }
     if (__any_sync(0xffffffffu, contributed)) {
       const float tot = warp_reduce16(v, lane);
-      if (!(lane & 1)) {
-        const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-        atomicAdd(A.ws + (size_t)g * kBwdVals + q, tot);
+      const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+      if (!(lane & 1)) atomicAdd(A.ws + (size_t)g * kBwdVals + q, tot);
+      if (A.sh) {  // per-ray SH: dL/dc_kc = Y_k(d) Gz_c w, summed over the warp's rays
+#pragma unroll 1
+        for (int c = 0; c < 3; ++c) {
+          float u[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) u[k] = k < A.sh_ncoef ? shb[k] * Gz[c] * wsh : 0.f;
+          const float t = warp_reduce16(u, lane);
+          if (!(lane & 1) && q < A.sh_ncoef) atomicAdd(A.dsh + ((size_t)g * A.sh_ncoef + q) * 3 + c, t);
+        }
       }
     }
   });
@@ -1337,7 +1356,9 @@ __global__ void __launch_bounds__(32) k_backward_lidar(const BwdArgs A) {
     return col && bx.z <= w && w <= bx.w;
   };
   __shared__ float4 s_rec[32][5];
-  bwd_ray_pair_passes<true>(A, rf, live, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, member);
+  float shb[16];
+  if (A.sh) sh_basis3((float)dd[0], (float)dd[1], (float)dd[2], shb);
+  bwd_ray_pair_passes<true>(A, rf, live, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, shb, member);
 }
 
 // one warp per (tile, strip of 32 pixels): TP x TP tiles have TP * TP / 32 strips
@@ -1373,7 +1394,9 @@ __global__ void __launch_bounds__(32) k_backward_camera(const BwdArgs A) {
   __syncwarp();
   auto member = [&](const float4 bx, float pu, float pv) { return bx.x <= pu && pu <= bx.y && bx.z <= pv && pv <= bx.w; };
   const int ray = inside ? j * C.width + i : 0;
-  bwd_ray_pair_passes<false>(A, rf, inside && valid, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, member);
+  float shb[16];
+  if (A.sh) sh_basis3((float)d[0], (float)d[1], (float)d[2], shb);
+  bwd_ray_pair_passes<false>(A, rf, inside && valid, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, shb, member);
 }
 
 // dL/dR (row-major 3x3) -> dL/dq of the unnormalised quaternion q behind R = R(q / |q|) (O1)
@@ -1394,6 +1417,7 @@ struct ParamsArgs {
   const int* actor_id;
   const float* actor_pose;  // [n_actors][7]
   int n_actors, ncoef;
+  int per_ray_sh;  // the SH gradient was accumulated by the list walk (A30)
   int64_t n;
 };
 
@@ -1486,6 +1510,7 @@ __global__ void __launch_bounds__(256) k_backward_params(const ParamsArgs P, sim
   for (int c = 0; c < 3; ++c) out.means[3 * g + c] = gm[c];
   reinterpret_cast<float4*>(out.quats)[g] = make_float4(gq[0], gq[1], gq[2], gq[3]);
   for (int c = 0; c < 3; ++c) out.scales[3 * g + c] = gs[c];
+  if (P.per_ray_sh) return;
   float b[16];
   sh_basis3(__ldg(P.view_dir + 3 * g), __ldg(P.view_dir + 3 * g + 1), __ldg(P.view_dir + 3 * g + 2), b);
   float* o = out.sh + (size_t)g * P.ncoef * 3;
@@ -1515,9 +1540,9 @@ int32_t bwd_common_checks(const simuli_gaussians* G, const simuli_projected* pro
     set_error("%s: workspace too small / workspace or quats gradient not 16-byte aligned", what);
     return SIMULI_ERR_INVALID_ARGUMENT;
   }
-  if (rp->sh) {
-    set_error("%s: per-ray SH has no backward (A31)", what);
-    return SIMULI_ERR_UNSUPPORTED;
+  if (rp->sh && (reinterpret_cast<uintptr_t>(rp->sh) % 16 != 0 || rp->sh_degree != G->sh_degree)) {
+    set_error("%s: per-ray SH must be 16-byte aligned and of the particles' degree", what);
+    return SIMULI_ERR_INVALID_ARGUMENT;
   }
   if (G->actor_id && (G->n_actors < 1 || !G->actor_pose)) {
     set_error("%s: actor_id needs n_actors >= 1 and actor_pose", what);
@@ -1539,11 +1564,16 @@ void bwd_fill_common(BwdArgs& A, const simuli_projected* proj, const uint32_t* i
   A.pose = make_pose_interp_d(P->pose_start, P->pose_end);
   A.alpha_min = rp->alpha_min; A.alpha_max = rp->alpha_max; A.T_min = rp->T_min;
   A.ws = static_cast<float*>(ws);
+  if (rp->sh) {
+    A.sh = rp->sh;
+    A.sh_ncoef = (rp->sh_degree + 1) * (rp->sh_degree + 1);
+  }
 }
 
 int32_t bwd_params(const simuli_gaussians* G, const simuli_projected* proj, const simuli_gaussian_grads* gout,
-                   const float* ws, cudaStream_t st, const char* what) {
+                   const float* ws, bool per_ray_sh, cudaStream_t st, const char* what) {
   ParamsArgs P{};
+  P.per_ray_sh = per_ray_sh ? 1 : 0;
   P.ws = ws; P.means = G->means; P.quats = G->quats; P.scales = G->scales; P.view_dir = proj->view_dir;
   P.ncoef = (G->sh_degree + 1) * (G->sh_degree + 1);
   P.n = G->n;
@@ -1607,10 +1637,15 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (G->n == 0) return SIMULI_OK;
   cudaMemsetAsync(workspace, 0, (size_t)G->n * kBwdVals * sizeof(float), st);
+  if (A.sh) {
+    A.dsh = gout->sh;
+    cudaMemsetAsync(gout->sh, 0, sizeof(float) * 3 * A.sh_ncoef * (size_t)G->n, st);
+  }
   k_backward_lidar<<<(unsigned)(T.n_tiles * A.chunks), 32, 0, st>>>(A);
   const int32_t lc = launch_check("simuli_backward_lidar");
   if (lc != SIMULI_OK) return lc;
-  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), st, "simuli_backward_lidar (params)");
+  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), A.sh != nullptr, st,
+                    "simuli_backward_lidar (params)");
 }
 
 extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simuli_projected* proj,
@@ -1649,10 +1684,15 @@ extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simul
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (G->n == 0) return SIMULI_OK;
   cudaMemsetAsync(workspace, 0, (size_t)G->n * kBwdVals * sizeof(float), st);
+  if (A.sh) {
+    A.dsh = gout->sh;
+    cudaMemsetAsync(gout->sh, 0, sizeof(float) * 3 * A.sh_ncoef * (size_t)G->n, st);
+  }
   const unsigned tiles = (unsigned)(K.Wt * Ht);
   if (C.tile_px == 8) k_backward_camera<8><<<tiles * 2, 32, 0, st>>>(A);
   else k_backward_camera<16><<<tiles * 8, 32, 0, st>>>(A);
   const int32_t lc = launch_check("simuli_backward_camera");
   if (lc != SIMULI_OK) return lc;
-  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), st, "simuli_backward_camera (params)");
+  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), A.sh != nullptr, st,
+                    "simuli_backward_camera (params)");
 }

@@ -132,8 +132,8 @@ def test_workspace_size_and_bad_args(lib):
 
 def test_backward_argument_errors(lib):
     """Host-side checks of simuli_backward_* (no device memory is touched: dummy aligned
-    addresses): missing view_dir -> INVALID_ARGUMENT, per-ray SH -> UNSUPPORTED (A31),
-    small workspace or a scene graph without poses -> INVALID_ARGUMENT."""
+    addresses): missing view_dir, a small workspace, per-ray SH of the wrong degree or a
+    scene graph without poses -> INVALID_ARGUMENT."""
     C = ctypes
     L = lib.load()
     fake = 1 << 20  # never dereferenced: every check below fails before a launch
@@ -151,8 +151,9 @@ def test_backward_argument_errors(lib):
     assert b"view_dir" in L.simuli_last_error()
     proj.view_dir = fake
     assert L.simuli_backward_camera(*args(639)) == lib.SIMULI_ERR_INVALID_ARGUMENT  # workspace < 10 x 64 B
-    rp.sh = fake
-    assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_UNSUPPORTED
+    rp.sh = fake  # per-ray SH of another degree than the particles'
+    assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_INVALID_ARGUMENT
+    assert b"degree" in L.simuli_last_error()
     rp.sh = None
     G.actor_id, G.actor_pose, G.n_actors = fake, None, 1  # scene graph without poses
     assert L.simuli_backward_camera(*args(640)) == lib.SIMULI_ERR_INVALID_ARGUMENT

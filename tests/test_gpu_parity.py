@@ -816,7 +816,7 @@ def test_backward_camera_parity(SM, oracle_mod, variant):
 
 
 def test_backward_empty_and_unsupported(SM):
-    """n = 0 is a no-op; per-ray SH and beam divergence have no backward (UNSUPPORTED)."""
+    """n = 0 is a no-op; beam divergence has no backward (UNSUPPORTED)."""
     cfg = S.lidar_config("A")
     sc = {k: v[:0] for k, v in S.scene_for("A").items()}
     r = SM.LidarRenderer(cfg, SM.to_device_scene(sc))
@@ -826,7 +826,7 @@ def test_backward_empty_and_unsupported(SM):
     torch.cuda.synchronize()
     assert out["means"].numel() == 0
     sc = S.scene_for("A")
-    for kw, div in (({"per_ray_sh": True}, 0.0), ({}, 1.5e-3)):
+    for kw, div in (({}, 1.5e-3),):
         c2 = S.lidar_config("A")
         c2.beam_divergence = div
         r = SM.LidarRenderer(c2, SM.to_device_scene(sc), **kw)
@@ -868,3 +868,42 @@ def test_backward_scene_graph_parity(SM, oracle_mod):
     scale = np.abs(ref["actor_pose"]).max()
     print("actor pose grads: max |gpu - oracle| / max", np.abs(a - ref["actor_pose"]).max() / scale)
     assert scale > 0 and np.abs(a - ref["actor_pose"]).max() <= 1e-3 * scale
+
+
+@pytest.mark.parametrize("sensor", ["lidar", "camera"])
+def test_backward_per_ray_sh_parity(SM, oracle_mod, sensor):
+    """Per-ray SH backward (A30, A31): SH gradients summed over rays with the ray's basis,
+    tier 1 against O15 with the same records, lists and rays."""
+    O = oracle_mod
+    if sensor == "lidar":
+        cfg, scene = S.lidar_config("A"), S.scene_for("A")
+        f = SM.LidarRenderer(cfg, SM.to_device_scene(scene), per_ray_sh=True)
+        f.requires_grad(True)
+        f.want_ray_od(True)
+        f.scan(sync_capacity=True)
+        t = O.Tiling(cfg)
+        ray_tile, ra, rb, rv, kw = t.ray_tile, t.ray_az, t.ray_el, None, dict(wrap=1, near=cfg.min_range,
+                                                                               pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    else:
+        cam = S.camera_config("D-small")
+        scene = S.corridor_scene(21, 40000, x_range=(0.0, 50.0), kind="camera", ego=(1.5, 0.0, 1.6))
+        f = SM.CameraRenderer(cam, SM.to_device_scene(scene), per_ray_sh=True)
+        f.requires_grad(True)
+        f.want_ray_od(True)
+        f.frame(sync_capacity=True)
+        rays = O.camera_rays(cam)
+        ray_tile, ra, rb, rv, kw = rays["tile"], rays["u"], rays["v"], rays["valid"], dict(wrap=0, near=cam.near)
+    torch.cuda.synchronize()
+    _, ids, ranges = sorted_lists(f)
+    rec = gpu_records(f)
+    rec["sh"] = scene["sh"]
+    od = f.out["ray_od"].cpu().numpy()
+    fwd = O.composite(rec, ids, ranges, ray_tile, ra, rb, od, ray_valid=rv,
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4}, **kw)
+    g = _upstream(od.shape[0], 11, sensor == "lidar", fwd["flag"] == 0)
+    got = f.backward(_dev(g))
+    torch.cuda.synchronize()
+    gz, go, gd = O.fold_upstream(fwd, g, lidar=sensor == "lidar")
+    d = O.backward_composite(rec, ids, ranges, ray_tile, ra, rb, od, gz, go, gd, ray_valid=rv, **kw)
+    ref = O.backward_params(scene, {"viewdir": f.view_dir.cpu().numpy().astype(np.float64)}, d)
+    _compare_grads(got, ref, f"per-ray SH {sensor} tier 1")

@@ -1137,3 +1137,54 @@ def test_backward_scene_graph_vs_finite_differences(oracle_mod):
                     bad += 1
                     print("mismatch", i, key, c, num, an)
     assert checked == 14 + 3 * 10 and bad <= 2, bad
+
+
+def test_backward_per_ray_sh_vs_finite_differences(oracle_mod):
+    """Per-ray SH (A30) backward: the features SH_i(d) do not depend on the particle's
+    position, so central differences of the forward check every parameter at full SH
+    degree 3; the SH gradient (per (ray, particle) basis) is exact by linearity."""
+    O = oracle_mod
+    cfg = S.lidar_config("tiny")
+    sc = S.scene_for("tiny", seed=33, n=120)
+    fwd = O.render_lidar(sc, cfg, per_ray_sh=True)
+    R = fwd["opacity"].shape[0]
+    rng = np.random.default_rng(34)
+    g = {"zeta": rng.normal(size=(R, 3)), "opacity": rng.normal(size=R), "depth_accum": 0.1 * rng.normal(size=R),
+         "depth": 0.1 * rng.normal(size=R), "intensity": rng.normal(size=R), "raydrop": np.zeros(R)}
+    b = O.backward_lidar(sc, cfg, g, per_ray_sh=True)
+
+    def loss(s):
+        f = O.render_lidar(s, cfg, per_ray_sh=True)
+        return (np.sum(g["zeta"] * f["feat"]) + np.sum(g["opacity"] * f["opacity"]) +
+                np.sum(g["depth_accum"] * f["depth_accum"]) + np.sum(g["depth"] * f["depth"]) +
+                np.sum(g["intensity"] * f["intensity"]))
+
+    L0 = loss(sc)
+    top = np.argsort(-np.abs(b["sh"]).sum((1, 2)))[:2]
+    for i in top:
+        for k in (0, 3, 9, 15):
+            s2 = {kk: v.copy() for kk, v in sc.items()}
+            s2["sh"][i, k, 1] += np.float32(0.5)
+            d = float(s2["sh"][i, k, 1]) - float(sc["sh"][i, k, 1])
+            assert abs((loss(s2) - L0) / d - b["sh"][i, k, 1]) < 1e-9 * max(1, abs(b["sh"][i, k, 1]))
+    checked = bad = 0
+    # small steps: the top particle sits 0.7 m from the sensor, where a 2e-4 step already
+    # flips a membership decision (the derivative itself matches to 1e-9 at 5e-5)
+    for i in np.argsort(-np.abs(b["opacity"]))[:3]:
+        for key, h, dims in (("means", 5e-5, 3), ("scales", 3e-5, 3), ("opacity", 1e-4, 1)):
+            for c in range(dims):
+                vals, deltas = [], []
+                for sgn in (1, -1):
+                    s2 = {kk: v.copy() for kk, v in sc.items()}
+                    arr = s2[key].reshape(sc["means"].shape[0], -1)
+                    x0 = np.float32(arr[i, c])
+                    arr[i, c] = np.float32(x0 + sgn * h * max(1.0, abs(float(x0))))
+                    deltas.append(float(arr[i, c]) - float(x0))
+                    vals.append(loss(s2))
+                num = (vals[0] - vals[1]) / (deltas[0] - deltas[1])
+                an = b[key].reshape(sc["means"].shape[0], -1)[i, c]
+                checked += 1
+                if abs(num - an) > 2e-3 * max(1.0, abs(an)):
+                    bad += 1
+                    print("mismatch", i, key, c, num, an)
+    assert checked == 21 and bad <= 1, bad
