@@ -9,7 +9,11 @@
  *
  * Parity status: every function below is pinned by tests/test_oracle_pins.py except the
  * whole-render composition on realistic scenes, which the paper gives no numbers for
- * ("parity unpinned" for the end-to-end render values).
+ * ("parity unpinned" for the end-to-end render values).  The NEXT-row
+ * functions are pinned too: O0 (scipy + rigid invariance), O14 (constant map / identity
+ * grid, texel centres, affine-field exactness), O15/O16 (central finite differences of the
+ * forward, LiDAR and camera, with scene graph and per-ray SH; SH linearity; the opacity
+ * scaling identity).
  */
 #include "oracle.h"
 
