@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 8
+#define SIMULI_ABI_VERSION 9
 
 enum {
   SIMULI_OK = 0,
@@ -370,8 +370,10 @@ typedef struct {
   float* actor_pose;
 } simuli_gaussian_grads;
 
-/* Scratch bytes for the backward of n particles (16 floats each). */
-int32_t simuli_backward_workspace_size(int64_t n, size_t* bytes);
+/* Scratch bytes for the backward of n particles (16 floats each) plus the segment area of
+ * the segmented list walk for up to pair_capacity pairs over n_tiles tiles (a smaller
+ * workspace of at least 64 n bytes falls back to the unsegmented walk). */
+int32_t simuli_backward_workspace_size(int64_t n, int64_t pair_capacity, int32_t n_tiles, size_t* bytes);
 
 /* LiDAR backward.  gaussians / params / rparams / proj / sorted_ids / tile_ranges: exactly
  * the forward frame's (proj->view_dir must have been written by simuli_project).  Launches:

@@ -1185,72 +1185,17 @@ __device__ __forceinline__ float warp_reduce16(float v[16], int lane) {
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-// The two passes of one warp whose lanes hold rays (LiDAR / camera: the same tile) over the
-// tile's list; member(bx) is the lane's A12 box test.
-template <bool LIDAR, typename Member>
-__device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF& rf, bool live, int ray,
-                                                    int2 rg, const float* ra, const float* rb, float4 (*srec)[5],
-                                                    const float shb[16], Member member) {
+// Gradient walk over [rg.x, rg.y) (the whole list, or one segment of it): T starts at T0
+// and the prefix sums (Gz.zeta, omega, D) at (pzf, pW, pD) -- 1 and 0 for a whole list, the
+// transmittance and sums of the earlier segments otherwise; (tot_f, W, D) are the ray's
+// totals.  The forward's decisions are replayed with the running T.
+template <typename Member>
+__device__ __forceinline__ void bwd_grad_walk(const BwdArgs& A, const RayF& rf, bool live, int2 rg, const float* ra,
+                                              const float* rb, float4 (*srec)[5], const float shb[16], Member member,
+                                              float T, float pzf, float pW, float pD, float tot_f, float W, float D,
+                                              const float Gz[3], float Go, float GD) {
   const int lane = threadIdx.x & 31;
-  // ---- pass 1: totals
-  float T = 1.f, z0 = 0.f, z1 = 0.f, z2 = 0.f, D = 0.f, W = 0.f;
-  bool done = !live;
-  if (A.f_feat) {  // the forward's own totals of this frame
-    if (live) {
-      z0 = __ldg(A.f_feat + 3 * (size_t)ray);
-      z1 = __ldg(A.f_feat + 3 * (size_t)ray + 1);
-      z2 = __ldg(A.f_feat + 3 * (size_t)ray + 2);
-      W = __ldg(A.f_opacity + ray);
-      D = __ldg(A.f_daccum + ray);
-    }
-  } else walk_list(A, rg, done, ra, rb, srec, member, [&](bool m, uint32_t gid, const float4 r[4]) {
-    if (!m) return;
-    float alpha, tau, rho;
-    bool cl;
-    const int st = bwd_step(A, rf, r, T, &alpha, &tau, &rho, &cl);
-    if (st == 0) return;
-    if (st == 2) {
-      done = true;
-      return;
-    }
-    const float w = alpha * T;
-    float f[3] = {r[3].y, r[3].z, r[3].w};
-    if (A.sh) sh_dot(A.sh + (size_t)gid * A.sh_ncoef * 3, A.sh_ncoef, shb, f);  // as the per-ray forward
-    z0 = fmaf(w, f[0], z0);
-    z1 = fmaf(w, f[1], z1);
-    z2 = fmaf(w, f[2], z2);
-    D = fmaf(w, tau, D);
-    W += w;
-    T = T * (1.f - alpha);
-  });
-  // ---- upstream gradients of the decoded outputs -> (Gz, Go, GD)
-  float Gz[3] = {0.f, 0.f, 0.f}, Go = 0.f, GD = 0.f;
-  if (live) {
-    if (A.g_feat)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) Gz[c] = __ldg(A.g_feat + 3 * (size_t)ray + c);
-    if (A.g_opacity) Go = __ldg(A.g_opacity + ray);
-    if (A.g_daccum) GD = __ldg(A.g_daccum + ray);
-    if (A.g_depth && W > 0.f) {
-      const float gd = __ldg(A.g_depth + ray);
-      GD += gd / W;
-      Go -= gd * D / (W * W);
-    }
-    if (LIDAR) {
-      if (A.g_intensity) Gz[0] += __ldg(A.g_intensity + ray);
-      if (A.g_raydrop) {
-        const float beta = raydrop_prob(z1, z2);
-        const float gr = __ldg(A.g_raydrop + ray) * beta * (1.f - beta);
-        Gz[1] -= gr;
-        Gz[2] += gr;
-      }
-    }
-  }
-  // ---- pass 2: gradients
-  const float tot_f = Gz[0] * z0 + Gz[1] * z1 + Gz[2] * z2;
-  float pz0 = 0.f, pz1 = 0.f, pz2 = 0.f, pD = 0.f, pW = 0.f;
-  T = 1.f;
-  done = !live;
+  bool done = !live || T < A.T_min;
   walk_list(A, rg, done, ra, rb, srec, member, [&](bool m, uint32_t g, const float4 r[4]) {
     float v[kBwdVals];
 #pragma unroll
@@ -1267,14 +1212,12 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
         const float w = alpha * T;
         float f[3] = {r[3].y, r[3].z, r[3].w};
         if (A.sh) sh_dot(A.sh + (size_t)g * A.sh_ncoef * 3, A.sh_ncoef, shb, f);
-        pz0 = fmaf(w, f[0], pz0);
-        pz1 = fmaf(w, f[1], pz1);
-        pz2 = fmaf(w, f[2], pz2);
+        const float gzf = Gz[0] * f[0] + Gz[1] * f[1] + Gz[2] * f[2];
+        pzf = fmaf(w, gzf, pzf);
         pD = fmaf(w, tau, pD);
         pW += w;
         wsh = w;
-        const float gzf = Gz[0] * f[0] + Gz[1] * f[1] + Gz[2] * f[2];
-        const float suf = (tot_f - (Gz[0] * pz0 + Gz[1] * pz1 + Gz[2] * pz2)) + Go * (W - pW) + GD * (D - pD);
+        const float suf = (tot_f - pzf) + Go * (W - pW) + GD * (D - pD);
         const float dalpha = T * (gzf + Go + GD * tau) - suf / (1.f - alpha);
         const float dtau = GD * w;
         float dd2 = 0.f;
@@ -1314,17 +1257,92 @@ __device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF
   });
 }
 
-__global__ void __launch_bounds__(32) k_backward_lidar(const BwdArgs A) {
-  const int slot = (int)(blockIdx.x / A.chunks), chunk = (int)(blockIdx.x % A.chunks);
-  const int tile = A.order ? __ldg(A.order + slot) : slot;
-  const int lane = threadIdx.x;
+// Upstream gradients of the decoded outputs -> (Gz, Go, GD) from the ray's totals
+template <bool LIDAR>
+__device__ __forceinline__ void bwd_fold(const BwdArgs& A, bool live, int ray, float z0, float z1, float z2, float W,
+                                         float D, float Gz[3], float* Go_, float* GD_) {
+  float Go = 0.f, GD = 0.f;
+  Gz[0] = Gz[1] = Gz[2] = 0.f;
+  if (live) {
+    if (A.g_feat)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) Gz[c] = __ldg(A.g_feat + 3 * (size_t)ray + c);
+    if (A.g_opacity) Go = __ldg(A.g_opacity + ray);
+    if (A.g_daccum) GD = __ldg(A.g_daccum + ray);
+    if (A.g_depth && W > 0.f) {
+      const float gd = __ldg(A.g_depth + ray);
+      GD += gd / W;
+      Go -= gd * D / (W * W);
+    }
+    if (LIDAR) {
+      if (A.g_intensity) Gz[0] += __ldg(A.g_intensity + ray);
+      if (A.g_raydrop) {
+        const float beta = raydrop_prob(z1, z2);
+        const float gr = __ldg(A.g_raydrop + ray) * beta * (1.f - beta);
+        Gz[1] -= gr;
+        Gz[2] += gr;
+      }
+    }
+  }
+  *Go_ = Go;
+  *GD_ = GD;
+}
+
+// The two passes of one warp whose lanes hold rays (LiDAR / camera: the same tile) over the
+// tile's list; member(bx) is the lane's A12 box test.
+template <bool LIDAR, typename Member>
+__device__ __forceinline__ void bwd_ray_pair_passes(const BwdArgs& A, const RayF& rf, bool live, int ray,
+                                                    int2 rg, const float* ra, const float* rb, float4 (*srec)[5],
+                                                    const float shb[16], Member member) {
+  const int lane = threadIdx.x & 31;
+  // ---- pass 1: totals
+  float T = 1.f, z0 = 0.f, z1 = 0.f, z2 = 0.f, D = 0.f, W = 0.f;
+  bool done = !live;
+  if (A.f_feat) {  // the forward's own totals of this frame
+    if (live) {
+      z0 = __ldg(A.f_feat + 3 * (size_t)ray);
+      z1 = __ldg(A.f_feat + 3 * (size_t)ray + 1);
+      z2 = __ldg(A.f_feat + 3 * (size_t)ray + 2);
+      W = __ldg(A.f_opacity + ray);
+      D = __ldg(A.f_daccum + ray);
+    }
+  } else walk_list(A, rg, done, ra, rb, srec, member, [&](bool m, uint32_t gid, const float4 r[4]) {
+    if (!m) return;
+    float alpha, tau, rho;
+    bool cl;
+    const int st = bwd_step(A, rf, r, T, &alpha, &tau, &rho, &cl);
+    if (st == 0) return;
+    if (st == 2) {
+      done = true;
+      return;
+    }
+    const float w = alpha * T;
+    float f[3] = {r[3].y, r[3].z, r[3].w};
+    if (A.sh) sh_dot(A.sh + (size_t)gid * A.sh_ncoef * 3, A.sh_ncoef, shb, f);  // as the per-ray forward
+    z0 = fmaf(w, f[0], z0);
+    z1 = fmaf(w, f[1], z1);
+    z2 = fmaf(w, f[2], z2);
+    D = fmaf(w, tau, D);
+    W += w;
+    T = T * (1.f - alpha);
+  });
+  float Gz[3], Go, GD;
+  bwd_fold<LIDAR>(A, live, ray, z0, z1, z2, W, D, Gz, &Go, &GD);
+  // ---- pass 2: gradients
+  bwd_grad_walk(A, rf, live, rg, ra, rb, srec, shb, member, 1.f, 0.f, 0.f, 0.f, Gz[0] * z0 + Gz[1] * z1 + Gz[2] * z2,
+                W, D, Gz, Go, GD);
+}
+
+// The rays of one warp, exactly as the render kernels build them.  LiDAR: rays chunk*32 +
+// lane of the tile (ra, rb = azimuth, elevation); camera: pixels strip*32 + lane of the TP x TP
+// tile (ra, rb = pixel centre).  Returns this lane's liveness; ray = output index.
+__device__ __forceinline__ bool lidar_ray_setup(const BwdArgs& A, int tile, int chunk, int lane, RayF& rf,
+                                                float shb[16], float* s_a, float* s_b, int& ray) {
   const int off0 = __ldg(A.tile_ray_off + tile), off1 = __ldg(A.tile_ray_off + tile + 1);
   const int k = off0 + chunk * 32 + lane;
   const bool live = k < off1;
-  if (__ballot_sync(0xffffffffu, live) == 0) return;
-  const int ray = live ? __ldg(A.tile_rays + k) : 0;
+  ray = live ? __ldg(A.tile_rays + k) : 0;
   const int b = ray / A.n_az, j = ray % A.n_az;
-  // the ray exactly as k_render_lidar builds it
   const float phi = live ? __ldg(A.ray_az + j) : 0.f, el = live ? __ldg(A.ray_el + (size_t)b * A.n_az) : 0.f;
   double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
   if (live) {
@@ -1337,14 +1355,47 @@ __global__ void __launch_bounds__(32) k_backward_lidar(const BwdArgs A) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
   }
-  RayF rf;
   split_ray(o, dd, rf);
-  __shared__ float s_a[32], s_b[32];
+  if (A.sh) sh_basis3((float)dd[0], (float)dd[1], (float)dd[2], shb);
+  __syncwarp();
   s_a[lane] = phi;
   s_b[lane] = el;
   __syncwarp();
-  const float pi_f = A.pi_f, two_pi_f = A.two_pi_f;
-  auto member = [&](const float4 bx, float p, float w) {  // k_render_lidar's column x beam test
+  return live;
+}
+
+template <int TP>
+__device__ __forceinline__ bool camera_ray_setup(const BwdArgs& A, int tile, int strip, int lane, RayF& rf,
+                                                 float shb[16], float* s_a, float* s_b, int& ray) {
+  const CameraArgs& C = A.cam;
+  const int ty = tile / C.Wt, tx = tile % C.Wt;
+  const int idx = strip * 32 + lane;
+  const int i = tx * TP + (idx % TP), j = ty * TP + (idx / TP);
+  const bool inside = i < C.width && j < C.height;
+  double o[3] = {0, 0, 0}, d[3] = {0, 0, 0};
+  bool valid = false;
+  if (inside) {
+    double dc[3];
+    valid = unproject(C, (double)i + 0.5, (double)j + 0.5, dc);
+    const double s = C.rolling ? ((double)j + 0.5) / (double)C.height : 0.0;
+    double R[9];
+    pose_at_d(C.pose, s, R, o);
+    if (valid)
+      for (int k = 0; k < 3; ++k) d[k] = R[3 * k] * dc[0] + R[3 * k + 1] * dc[1] + R[3 * k + 2] * dc[2];
+  }
+  split_ray(o, d, rf);
+  if (A.sh) sh_basis3((float)d[0], (float)d[1], (float)d[2], shb);
+  ray = inside ? j * C.width + i : 0;
+  __syncwarp();
+  s_a[lane] = (float)i + 0.5f;
+  s_b[lane] = (float)j + 0.5f;
+  __syncwarp();
+  return inside && valid;
+}
+
+struct LidarMember {  // k_render_lidar's column x beam test
+  float pi_f, two_pi_f;
+  __device__ __forceinline__ bool operator()(const float4 bx, float p, float w) const {
     bool col;
     if (__fsub_rn(bx.y, bx.x) >= two_pi_f) {
       col = true;
@@ -1354,49 +1405,194 @@ __global__ void __launch_bounds__(32) k_backward_lidar(const BwdArgs A) {
       col = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
     }
     return col && bx.z <= w && w <= bx.w;
-  };
+  }
+};
+struct CameraMember {
+  __device__ __forceinline__ bool operator()(const float4 bx, float pu, float pv) const {
+    return bx.x <= pu && pu <= bx.y && bx.z <= pv && pv <= bx.w;
+  }
+};
+
+// unsegmented: one warp per (tile, 32 rays) walks the whole list twice (no forward totals)
+__global__ void __launch_bounds__(32) k_backward_lidar(const BwdArgs A) {
+  const int slot = (int)(blockIdx.x / A.chunks), chunk = (int)(blockIdx.x % A.chunks);
+  const int tile = A.order ? __ldg(A.order + slot) : slot;
+  __shared__ float s_a[32], s_b[32];
   __shared__ float4 s_rec[32][5];
+  RayF rf;
   float shb[16];
-  if (A.sh) sh_basis3((float)dd[0], (float)dd[1], (float)dd[2], shb);
-  bwd_ray_pair_passes<true>(A, rf, live, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, shb, member);
+  int ray;
+  const bool live = lidar_ray_setup(A, tile, chunk, threadIdx.x, rf, shb, s_a, s_b, ray);
+  if (__ballot_sync(0xffffffffu, live) == 0u) return;
+  bwd_ray_pair_passes<true>(A, rf, live, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, shb,
+                            LidarMember{A.pi_f, A.two_pi_f});
 }
 
-// one warp per (tile, strip of 32 pixels): TP x TP tiles have TP * TP / 32 strips
 template <int TP>
 __global__ void __launch_bounds__(32) k_backward_camera(const BwdArgs A) {
   constexpr int STRIPS = TP * TP / 32;
-  const CameraArgs& C = A.cam;
   const int slot = (int)(blockIdx.x / STRIPS), strip = (int)(blockIdx.x % STRIPS);
   const int tile = A.order ? __ldg(A.order + slot) : slot;
-  const int lane = threadIdx.x;
-  const int ty = tile / C.Wt, tx = tile % C.Wt;
-  const int idx = strip * 32 + lane;
-  const int i = tx * TP + (idx % TP), j = ty * TP + (idx / TP);
-  const bool inside = i < C.width && j < C.height;
-  double o[3] = {0, 0, 0}, d[3] = {0, 0, 0};
-  bool valid = false;
-  if (inside) {  // the pixel ray exactly as k_render_camera builds it
-    double dc[3];
-    valid = unproject(C, (double)i + 0.5, (double)j + 0.5, dc);
-    const double s = C.rolling ? ((double)j + 0.5) / (double)C.height : 0.0;
-    double R[9];
-    pose_at_d(C.pose, s, R, o);
-    if (valid)
-      for (int k = 0; k < 3; ++k) d[k] = R[3 * k] * dc[0] + R[3 * k + 1] * dc[1] + R[3 * k + 2] * dc[2];
-  }
-  if (__ballot_sync(0xffffffffu, inside && valid) == 0u) return;
-  RayF rf;
-  split_ray(o, d, rf);
   __shared__ float s_a[32], s_b[32];
   __shared__ float4 s_rec[32][5];
-  s_a[lane] = (float)i + 0.5f;
-  s_b[lane] = (float)j + 0.5f;
-  __syncwarp();
-  auto member = [&](const float4 bx, float pu, float pv) { return bx.x <= pu && pu <= bx.y && bx.z <= pv && pv <= bx.w; };
-  const int ray = inside ? j * C.width + i : 0;
+  RayF rf;
   float shb[16];
-  if (A.sh) sh_basis3((float)d[0], (float)d[1], (float)d[2], shb);
-  bwd_ray_pair_passes<false>(A, rf, inside && valid, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, shb, member);
+  int ray;
+  const bool live = camera_ray_setup<TP>(A, tile, strip, threadIdx.x, rf, shb, s_a, s_b, ray);
+  if (__ballot_sync(0xffffffffu, live) == 0u) return;
+  bwd_ray_pair_passes<false>(A, rf, live, ray, __ldg(A.ranges + tile), s_a, s_b, s_rec, shb, CameraMember{});
+}
+
+// ---------------------------------------------------------------- segmented backward
+// With the forward's totals the first pass is not needed, and a long list can be cut into
+// segments of kBwdSeg entries walked by different warps: a stats pass gives each
+// (segment, ray) its transmittance product and local sums (no termination), and the
+// gradient pass of segment s starts from the product / sums of segments 0..s-1 of its tile
+// (A31; termination is replayed with the running T: a ray that stopped in an earlier
+// segment enters later ones with T < T_min).  Work items (slot, ray group, segment) are
+// numbered longest tile first and taken from an atomic counter by persistent warps.
+constexpr int kBwdSeg = 512;
+constexpr int kBwdGroupsMax = 8;  // ray groups (LiDAR chunks / camera strips) per tile, upper bound
+
+struct SegPlan {  // device scalars at the head of the segment area
+  int total, counter_stats, counter_grad, segmented;
+};
+
+__global__ void __launch_bounds__(1024) k_bwd_plan(const BwdArgs A, int n_tiles, int groups, int cap_items,
+                                                   int* item_off, SegPlan* plan) {
+  __shared__ int s_warp[32];
+  __shared__ int s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  int seg = 1;
+  for (int pass = 0; pass < 2; ++pass) {  // pass 1 only if pass 0 overflowed: one segment per tile
+    for (int base = 0; base < n_tiles; base += 1024) {
+      const int slot = base + threadIdx.x;
+      int items = 0;
+      if (slot < n_tiles) {
+        const int tile = A.order ? __ldg(A.order + slot) : slot;
+        const int2 rg = __ldg(A.ranges + tile);
+        const int nseg = seg ? max(1, (rg.y - rg.x + kBwdSeg - 1) / kBwdSeg) : 1;
+        items = nseg * groups;
+      }
+      int incl = items;
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) s_warp[w] = incl;
+      __syncthreads();
+      int wo = 0;
+      for (int k = 0; k < w; ++k) wo += s_warp[k];
+      const int carry = s_carry;
+      if (slot < n_tiles) item_off[slot] = carry + wo + incl - items;
+      __syncthreads();
+      if (threadIdx.x == 1023) s_carry = carry + wo + incl;
+      __syncthreads();
+    }
+    if (s_carry <= cap_items || !seg) break;
+    seg = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    item_off[n_tiles] = s_carry;
+    plan->total = s_carry;
+    plan->counter_stats = 0;
+    plan->counter_grad = 0;
+    plan->segmented = seg;
+  }
+}
+
+template <bool LIDAR, int TP, bool STATS>
+__global__ void __launch_bounds__(32) k_bwd_seg(const BwdArgs A, int n_tiles, int groups, const int* item_off,
+                                                SegPlan* plan, float4* stats) {
+  __shared__ float s_a[32], s_b[32];
+  __shared__ float4 s_rec[32][5];
+  const int lane = threadIdx.x;
+  const int total = *reinterpret_cast<volatile int*>(&plan->total);
+  const bool segmented = plan->segmented != 0;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(STATS ? &plan->counter_stats : &plan->counter_grad, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= total) return;
+    int lo = 0, hi = n_tiles;  // slot: last with item_off[slot] <= item
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(item_off + mid) <= item) lo = mid;
+      else hi = mid;
+    }
+    const int slot = lo, tile = A.order ? __ldg(A.order + slot) : slot;
+    const int2 rg = __ldg(A.ranges + tile);
+    const int nseg = segmented ? max(1, (rg.y - rg.x + kBwdSeg - 1) / kBwdSeg) : 1;
+    const int local = item - __ldg(item_off + slot), group = local / nseg, sgi = local % nseg;
+    if (STATS && nseg == 1) continue;  // a single segment starts from T = 1
+    RayF rf;
+    float shb[16];
+    int ray;
+    const bool live = LIDAR ? lidar_ray_setup(A, tile, group, lane, rf, shb, s_a, s_b, ray)
+                            : camera_ray_setup<TP>(A, tile, group, lane, rf, shb, s_a, s_b, ray);
+    if (__ballot_sync(0xffffffffu, live) == 0u) continue;
+    const int2 seg = make_int2(rg.x + sgi * kBwdSeg, min(rg.y, rg.x + (sgi + 1) * kBwdSeg));
+    float z0 = 0.f, z1 = 0.f, z2 = 0.f, W = 0.f, D = 0.f;
+    if (live) {
+      z0 = __ldg(A.f_feat + 3 * (size_t)ray);
+      z1 = __ldg(A.f_feat + 3 * (size_t)ray + 1);
+      z2 = __ldg(A.f_feat + 3 * (size_t)ray + 2);
+      W = __ldg(A.f_opacity + ray);
+      D = __ldg(A.f_daccum + ray);
+    }
+    float Gz[3], Go, GD;
+    bwd_fold<LIDAR>(A, live, ray, z0, z1, z2, W, D, Gz, &Go, &GD);
+    const int base_item = __ldg(item_off + slot) + group * nseg;  // segment 0 of this ray group
+    if (STATS) {
+      float P = 1.f, Af = 0.f, Wl = 0.f, Dl = 0.f, T = 1.f;
+      bool done = !live;
+      const auto mem = [&](const float4 bx, float a, float b) {
+        if (LIDAR) return LidarMember{A.pi_f, A.two_pi_f}(bx, a, b);
+        return CameraMember{}(bx, a, b);
+      };
+      walk_list(A, seg, done, s_a, s_b, s_rec, mem, [&](bool m, uint32_t g, const float4 r[4]) {
+        if (!m) return;
+        float alpha, tau, rho;
+        bool cl;
+        bwd_step(A, rf, r, 1.f, &alpha, &tau, &rho, &cl);  // skip rules only (T = 1: no stop)
+        if (tau < A.near_tau || alpha < A.alpha_min) return;
+        float f[3] = {r[3].y, r[3].z, r[3].w};
+        if (A.sh) sh_dot(A.sh + (size_t)g * A.sh_ncoef * 3, A.sh_ncoef, shb, f);
+        const float w = alpha * T;
+        Af = fmaf(w, Gz[0] * f[0] + Gz[1] * f[1] + Gz[2] * f[2], Af);
+        Wl += w;
+        Dl = fmaf(w, tau, Dl);
+        T = T * (1.f - alpha);
+        P = T;
+        // below T_min the ray stops in this segment or earlier: later segments only need
+        // T_in < T_min, which any partial product below T_min already guarantees
+        if (T < A.T_min) done = true;
+      });
+      stats[(size_t)item * 32 + lane] = make_float4(P, Af, Wl, Dl);
+    } else {
+      float T = 1.f, pzf = 0.f, pW = 0.f, pD = 0.f;
+      for (int s2 = 0; s2 < sgi; ++s2) {  // earlier segments of this ray group
+        const float4 st = stats[(size_t)(base_item + s2) * 32 + lane];
+        pzf = fmaf(T, st.y, pzf);
+        pW = fmaf(T, st.z, pW);
+        pD = fmaf(T, st.w, pD);
+        T *= st.x;
+      }
+      const float tot_f = Gz[0] * z0 + Gz[1] * z1 + Gz[2] * z2;
+      if (LIDAR)
+        bwd_grad_walk(A, rf, live, seg, s_a, s_b, s_rec, shb, LidarMember{A.pi_f, A.two_pi_f}, T, pzf, pW, pD, tot_f,
+                      W, D, Gz, Go, GD);
+      else
+        bwd_grad_walk(A, rf, live, seg, s_a, s_b, s_rec, shb, CameraMember{}, T, pzf, pW, pD, tot_f, W, D, Gz, Go,
+                      GD);
+    }
+  }
 }
 
 // dL/dR (row-major 3x3) -> dL/dq of the unnormalised quaternion q behind R = R(q / |q|) (O1)
@@ -1593,11 +1789,42 @@ int32_t bwd_params(const simuli_gaussians* G, const simuli_projected* proj, cons
 }  // namespace
 }  // namespace simuli
 
-extern "C" int32_t simuli_backward_workspace_size(int64_t n, size_t* bytes) {
+namespace simuli {
+namespace {
+// segment area of the backward workspace, after the n x 16 gradient floats:
+// SegPlan | item_off [n_tiles + 1] (16-byte padded) | stats [items][32] float4
+size_t seg_area_fixed(int32_t n_tiles) { return 16 + (((size_t)n_tiles + 1) * 4 + 15) / 16 * 16; }
+
+// runs the segmented walk if the forward totals are given and the workspace holds at least
+// one item per (tile, ray group); returns false to use the unsegmented kernels
+template <bool LIDAR, int TP>
+bool launch_segmented(BwdArgs A, int32_t n_tiles, int groups, int64_t n, void* workspace, size_t workspace_bytes,
+                      cudaStream_t st) {
+  if (!A.f_feat) return false;
+  const size_t head = (size_t)n * kBwdVals * sizeof(float);
+  if (workspace_bytes < head + seg_area_fixed(n_tiles)) return false;
+  const size_t cap = (workspace_bytes - head - seg_area_fixed(n_tiles)) / (32 * sizeof(float4));
+  if (cap < (size_t)n_tiles * groups) return false;
+  char* area = static_cast<char*>(workspace) + head;
+  SegPlan* plan = reinterpret_cast<SegPlan*>(area);
+  int* item_off = reinterpret_cast<int*>(area + 16);
+  float4* stats = reinterpret_cast<float4*>(area + seg_area_fixed(n_tiles));
+  const int cap_items = cap > (size_t)INT32_MAX ? INT32_MAX : (int)cap;
+  k_bwd_plan<<<1, 1024, 0, st>>>(A, n_tiles, groups, cap_items, item_off, plan);
+  const unsigned grid = 148 * 32;  // persistent warps, a full device
+  k_bwd_seg<LIDAR, TP, true><<<grid, 32, 0, st>>>(A, n_tiles, groups, item_off, plan, stats);
+  k_bwd_seg<LIDAR, TP, false><<<grid, 32, 0, st>>>(A, n_tiles, groups, item_off, plan, stats);
+  return true;
+}
+}  // namespace
+}  // namespace simuli
+
+extern "C" int32_t simuli_backward_workspace_size(int64_t n, int64_t pair_capacity, int32_t n_tiles, size_t* bytes) {
   using namespace simuli;
   clear_error();
-  SIMULI_REQUIRE(n >= 0 && bytes, "simuli_backward_workspace_size: bad argument");
-  *bytes = (size_t)n * kBwdVals * sizeof(float);
+  SIMULI_REQUIRE(n >= 0 && pair_capacity >= 0 && n_tiles >= 0 && bytes, "simuli_backward_workspace_size: bad argument");
+  const size_t items = ((size_t)n_tiles + (size_t)pair_capacity / kBwdSeg + 1) * kBwdGroupsMax;
+  *bytes = (size_t)n * kBwdVals * sizeof(float) + seg_area_fixed(n_tiles) + items * 32 * sizeof(float4);
   return SIMULI_OK;
 }
 
@@ -1641,7 +1868,8 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
     A.dsh = gout->sh;
     cudaMemsetAsync(gout->sh, 0, sizeof(float) * 3 * A.sh_ncoef * (size_t)G->n, st);
   }
-  k_backward_lidar<<<(unsigned)(T.n_tiles * A.chunks), 32, 0, st>>>(A);
+  if (!launch_segmented<true, 16>(A, T.n_tiles, A.chunks, G->n, workspace, workspace_bytes, st))
+    k_backward_lidar<<<(unsigned)(T.n_tiles * A.chunks), 32, 0, st>>>(A);
   const int32_t lc = launch_check("simuli_backward_lidar");
   if (lc != SIMULI_OK) return lc;
   return bwd_params(G, proj, gout, static_cast<const float*>(workspace), A.sh != nullptr, st,
@@ -1689,6 +1917,8 @@ extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simul
     cudaMemsetAsync(gout->sh, 0, sizeof(float) * 3 * A.sh_ncoef * (size_t)G->n, st);
   }
   const unsigned tiles = (unsigned)(K.Wt * Ht);
+  // camera: the unsegmented walk (its rays stop early behind opaque surfaces, which a
+  // segment's stats pass cannot know; config D: 2.42 ms unsegmented vs 2.88 ms segmented)
   if (C.tile_px == 8) k_backward_camera<8><<<tiles * 2, 32, 0, st>>>(A);
   else k_backward_camera<16><<<tiles * 8, 32, 0, st>>>(A);
   const int32_t lc = launch_check("simuli_backward_camera");

@@ -165,7 +165,7 @@ def load():
     L.simuli_render_camera.argtypes = [C.POINTER(Projected), C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(CameraOut),
                                        C.c_void_p]
-    L.simuli_backward_workspace_size.argtypes = [C.c_int64, C.POINTER(C.c_size_t)]
+    L.simuli_backward_workspace_size.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]
     for nm, gin in (("simuli_backward_lidar", LidarGradIn), ("simuli_backward_camera", CameraGradIn)):
         getattr(L, nm).argtypes = [C.POINTER(Gaussians), C.POINTER(Projected), C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(gin),
@@ -268,9 +268,9 @@ def simuli_compose_camera(params, env, grid, rgb_fg, opacity, rgb_out, stream=No
                                         _stream(stream)))
 
 
-def simuli_backward_workspace_size(n):
+def simuli_backward_workspace_size(n, pair_capacity=0, n_tiles=0):
     b = C.c_size_t(0)
-    _check(load().simuli_backward_workspace_size(int(n), C.byref(b)))
+    _check(load().simuli_backward_workspace_size(int(n), int(pair_capacity), int(n_tiles), C.byref(b)))
     return int(b.value)
 
 
@@ -378,7 +378,7 @@ class _Frame:
 
     def _bwd_workspace(self):
         import torch
-        need = simuli_backward_workspace_size(self.n)
+        need = simuli_backward_workspace_size(self.n, self.capacity, self.n_tiles)
         if getattr(self, "_bws", None) is None or self._bws.numel() < need:
             self._bws = torch.empty(max(need, 16), dtype=torch.uint8, device=self.device)
         return self._bws

@@ -38,7 +38,7 @@ def test_exports_every_header_symbol(lib):
     exported = {ln.split()[-1] for ln in nm.splitlines() if " T " in ln}
     assert set(syms) <= exported
     assert set(lib.EXPORTED) == set(syms)
-    assert L.simuli_abi_version() == 8
+    assert L.simuli_abi_version() == 9
 
 
 def test_library_is_sm100a(lib):
@@ -123,8 +123,11 @@ def test_workspace_size_and_bad_args(lib):
     size = ctypes.c_size_t(0)
     assert L.simuli_bin_sort_workspace_size(-1, 10, 1, ctypes.byref(size)) == lib.SIMULI_ERR_INVALID_ARGUMENT
     # backward (A31): size query and argument checks run on the host
-    assert L.simuli_backward_workspace_size(1000, ctypes.byref(size)) == lib.SIMULI_OK and size.value == 1000 * 64
-    assert L.simuli_backward_workspace_size(-1, ctypes.byref(size)) == lib.SIMULI_ERR_INVALID_ARGUMENT
+    assert L.simuli_backward_workspace_size(1000, 0, 0, ctypes.byref(size)) == lib.SIMULI_OK
+    assert 1000 * 64 <= size.value < 1000 * 64 + 8192
+    assert L.simuli_backward_workspace_size(1000, 4096, 10, ctypes.byref(size)) == lib.SIMULI_OK
+    assert size.value >= 1000 * 64 + (10 + 4) * 8 * 512
+    assert L.simuli_backward_workspace_size(-1, 0, 0, ctypes.byref(size)) == lib.SIMULI_ERR_INVALID_ARGUMENT
     for fn in (L.simuli_backward_lidar, L.simuli_backward_camera):
         assert fn(None, None, None, None, None, None, None, None, None, None, 0, None) == lib.SIMULI_ERR_INVALID_ARGUMENT
         assert b"NULL" in L.simuli_last_error()

@@ -907,3 +907,37 @@ def test_backward_per_ray_sh_parity(SM, oracle_mod, sensor):
     d = O.backward_composite(rec, ids, ranges, ray_tile, ra, rb, od, gz, go, gd, ray_valid=rv, **kw)
     ref = O.backward_params(scene, {"viewdir": f.view_dir.cpu().numpy().astype(np.float64)}, d)
     _compare_grads(got, ref, f"per-ray SH {sensor} tier 1")
+
+
+def test_backward_segmented_walk(SM, oracle_mod):
+    """Lists longer than one 1024-entry segment (config A sensor, 150k particles): the
+    segmented walk (stats pass + gradient pass from the earlier segments' transmittance and
+    sums) against the unsegmented walk and against O15/O16 (tier 1)."""
+    O = oracle_mod
+    cfg, scene = S.lidar_config("A"), S.scene_for("A", n=150_000)
+    r = SM.LidarRenderer(cfg, SM.to_device_scene(scene))
+    r.requires_grad(True)
+    r.want_ray_od(True)
+    r.scan(sync_capacity=True)
+    torch.cuda.synchronize()
+    lens = np.diff(r.tile_ranges.cpu().numpy(), axis=1)
+    assert lens.max() > 1024, lens.max()  # at least two segments
+    t = O.Tiling(cfg)
+    _, ids, ranges = sorted_lists(r)
+    rec = gpu_records(r)
+    od = r.out["ray_od"].cpu().numpy()
+    fwd = O.composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, wrap=1, near=cfg.min_range,
+                      flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4},
+                      pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    g = _upstream(od.shape[0], 12, True, fwd["flag"] == 0)
+    seg = r.backward(_dev(g))
+    whole = r.backward(_dev(g), use_forward_totals=False)
+    torch.cuda.synchronize()
+    for k in seg:
+        a, b = seg[k].cpu().numpy(), whole[k].cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-4 * np.abs(b).max(), k
+    gz, go, gd = O.fold_upstream(fwd, g, lidar=True)
+    d = O.backward_composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, gz, go, gd, wrap=1,
+                             near=cfg.min_range, pi_f=t.pi_f, two_pi_f=t.two_pi_f)
+    ref = O.backward_params(scene, {"viewdir": r.view_dir.cpu().numpy().astype(np.float64)}, d)
+    _compare_grads(seg, ref, "segmented tier 1")
