@@ -222,8 +222,10 @@ typedef struct {
   int32_t* tile_rect;
   float* depth_key;
   int32_t* tile_count;
-  float* view_dir;  /* [n][3] or NULL: the unit SH view direction of each written record
-                       (A17; 0 if invalid) -- the backward's SH chain needs it (A31) */
+  float* view_dir;  /* [n][3] or NULL: the view vector mu - o(s0) of each written record,
+                       unnormalised (A17: the SH direction is its unit vector; A27: the
+                       beam-divergence offset uses it whole; 0 if invalid) -- for the
+                       backward (A31) */
 } simuli_projected;
 
 /* UT projection: 7 sigma points mu, mu +- sqrt(3+lambda) l_k (l_k = s_k R e_k,
@@ -342,7 +344,9 @@ int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorte
  * the per-particle SH at the projection's view direction (A17), held fixed (no gradient
  * through the direction); with rparams->sh (per-ray SH, A30) the features are SH_i(d) per
  * ray and the SH gradient sums Y_k(d) dL/dzeta alpha T over the rays (float atomics into
- * grad_out->sh).  Not supported (UNSUPPORTED): beam divergence.
+ * grad_out->sh); with beam divergence (A27) M = chol(Sigma_hat)^-1 is differentiated through
+ * the Cholesky factor and Sigma_hat's view vector (the sensor position held at the mean's
+ * firing time).
  * Upstream gradients (device, [n_rays] or [n_rays][3]; NULL = 0): LiDAR zeta, opacity
  * (omega), depth_accum (D), depth (D / omega), intensity (zeta_0), raydrop
  * (1 / (1 + exp(zeta_1 - zeta_2))); camera rgb (c_f), opacity, depth_accum, depth. */

@@ -900,12 +900,12 @@ static int project_common(const or_gaussians* G, const void* sensor, int wrap_a,
     double Rs[9], ts[3], v[3], shd[48];
     or_pose_at(pose0, pose1, s0, Rs, ts);
     for (int c = 0; c < 3; ++c) v[c] = mu[c] - ts[c];
+    if (out->viewdir) /* the view vector mu - o(s0), unnormalised (backward, A31) */
+      for (int c = 0; c < 3; ++c) out->viewdir[g * 3 + c] = v[c];
     double vn = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
     for (int c = 0; c < 3; ++c) v[c] /= vn;
     for (int k = 0; k < ncoef * 3; ++k) shd[k] = G->sh[g * ncoef * 3 + k];
     or_sh_eval(shd, G->sh_degree, v, &out->feat[g * 3]);
-    if (out->viewdir)
-      for (int c = 0; c < 3; ++c) out->viewdir[g * 3 + c] = v[c];
   }
   return 0;
 }
@@ -1557,69 +1557,16 @@ int or_backward_composite(const double* mu, const double* Mrows, const double* s
 }
 
 /* ------------------------------------------------------------------------------------
- * O16 chain to the particle parameters:  M[k][j] = R[j][k] / s_k with R = R(q^),
- *   q^ = q/|q| (O1):  dL/dR[j][k] = dL/dM[k][j] / s_k,  dL/ds_k = -sum_j dL/dM[k][j] R[j][k] / s_k^2;
- *   dR/dq^ by differentiating O1's entries;  dL/dq = (dL/dq^ - q^ (q^ . dL/dq^)) / |q|.
- *   f = sum_k Y_k(v) c_k (O9):  dL/dc_k = Y_k(v) dL/df (v held fixed, A31).
- * ---------------------------------------------------------------------------------- */
-void or_backward_params(int64_t n, const float* quats, const float* scales, const double* viewdir,
-                        int32_t sh_degree, const double* d_M, const double* d_feat, double* g_quats,
-                        double* g_scales, double* g_sh) {
-  const int nco = (sh_degree + 1) * (sh_degree + 1);
-  for (int64_t g = 0; g < n; ++g) {
-    double q[4], qn = 0.0;
-    for (int c = 0; c < 4; ++c) {
-      q[c] = quats[4 * g + c];
-      qn += q[c] * q[c];
-    }
-    qn = sqrt(qn);
-    for (int c = 0; c < 4; ++c) g_quats[4 * g + c] = 0.0;
-    for (int c = 0; c < 3; ++c) g_scales[3 * g + c] = 0.0;
-    for (int k = 0; k < nco * 3; ++k) g_sh[(int64_t)g * nco * 3 + k] = 0.0;
-    if (!(qn > 0.0) || !isfinite(qn)) continue;
-    double R[9];
-    or_quat_to_rot(q, R); /* normalises */
-    const double w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
-    double G[9]; /* dL/dR[j][k] */
-    for (int k = 0; k < 3; ++k) {
-      const double s = scales[3 * g + k];
-      double ds = 0.0;
-      for (int j = 0; j < 3; ++j) {
-        const double dm = d_M[g * 9 + 3 * k + j];
-        G[3 * j + k] = dm / s;
-        ds -= dm * R[3 * j + k] / (s * s);
-      }
-      g_scales[3 * g + k] = ds;
-    }
-    /* R = [[1-2(y2+z2), 2(xy-wz), 2(xz+wy)], [2(xy+wz), 1-2(x2+z2), 2(yz-wx)], [2(xz-wy), 2(yz+wx), 1-2(x2+y2)]] */
-    const double dw = 2.0 * (-z * G[1] + y * G[2] + z * G[3] - x * G[5] - y * G[6] + x * G[7]);
-    const double dx = 2.0 * (y * G[1] + z * G[2] + y * G[3] - 2.0 * x * G[4] - w * G[5] + z * G[6] + w * G[7] -
-                             2.0 * x * G[8]);
-    const double dy = 2.0 * (-2.0 * y * G[0] + x * G[1] + w * G[2] + x * G[3] + z * G[5] - w * G[6] + z * G[7] -
-                             2.0 * y * G[8]);
-    const double dz = 2.0 * (-2.0 * z * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.0 * z * G[4] + y * G[5] +
-                             x * G[6] + y * G[7]);
-    const double dq[4] = {dw, dx, dy, dz}, qh[4] = {w, x, y, z};
-    const double dot = dw * w + dx * x + dy * y + dz * z;
-    for (int c = 0; c < 4; ++c) g_quats[4 * g + c] = (dq[c] - qh[c] * dot) / qn;
-    /* SH: the basis at v, one coefficient at a time through O9 */
-    for (int k = 0; k < nco; ++k) {
-      double e[48] = {0}, yk[3];
-      e[3 * k] = 1.0;
-      or_sh_eval(e, sh_degree, &viewdir[3 * g], yk); /* yk[0] = Y_k(v) */
-      for (int c = 0; c < 3; ++c) g_sh[(int64_t)g * nco * 3 + 3 * k + c] = yk[0] * d_feat[3 * g + c];
-    }
-  }
-}
-
-/* ------------------------------------------------------------------------------------
  * O16 with the scene graph (A29, A31).  For a particle of object a:
  *   R_w = R_a R_l,  mu_w = R_a mu_l + t_a  (O0)
- *   dL/dR_w = G from dL/dM (as in or_backward_params, R_w in ds),
+ *   dL/dR_w = G from dL/dM: M[k][j] = R_w[j][k] / s_k gives G[j][k] = dL/dM[k][j] / s_k and
+ *   dL/ds_k = -sum_j dL/dM[k][j] R_w[j][k] / s_k^2 (with beam divergence: the Cholesky chain below),
  *   dL/dR_l = R_a^T G,   dL/dmu_l = R_a^T dL/dmu_w,
  *   dL/dR_a += G R_l^T + dL/dmu_w mu_l^T,   dL/dt_a += dL/dmu_w,
  * each rotation gradient taken to its (unnormalised) quaternion by the O1 chain.  Static
- * particles (id -1) are as in or_backward_params; ids outside [-1, n_actors) get zeros.
+ * particles (id -1, or actor_id NULL) have R_a = I, t_a = 0; ids outside [-1, n_actors) get zeros.
+ * dR -> dq of the unnormalised quaternion by differentiating O1's entries, then
+ * dL/dq = (dL/dq^ - q^ (q^ . dL/dq^)) / |q|; f = sum_k Y_k(v) c_k (O9): dL/dc_k = Y_k(v) dL/df.
  * g_actor [n_actors][7] = (dL/dq_a, dL/dt_a), accumulated over the object's particles.
  * ---------------------------------------------------------------------------------- */
 static void rot_grad_to_quat(const double G[9], const double q_in[4], double dq_out[4]) {
@@ -1639,8 +1586,9 @@ static void rot_grad_to_quat(const double G[9], const double q_in[4], double dq_
 
 void or_backward_params_sg(int64_t n, const float* means, const float* quats, const float* scales,
                            const double* viewdir, int32_t sh_degree, const int32_t* actor_id, int32_t n_actors,
-                           const double* actor_pose, const double* d_mu, const double* d_M, const double* d_feat,
-                           double* g_means, double* g_quats, double* g_scales, double* g_sh, double* g_actor) {
+                           const double* actor_pose, double beam_div, const double* d_mu, const double* d_M,
+                           const double* d_feat, double* g_means, double* g_quats, double* g_scales, double* g_sh,
+                           double* g_actor) {
   const int nco = (sh_degree + 1) * (sh_degree + 1);
   double* Ga = (double*)calloc((size_t)(n_actors > 0 ? n_actors : 1) * 12, sizeof(double)); /* dR_a 9, dt_a 3 */
   for (int64_t g = 0; g < n; ++g) {
@@ -1666,16 +1614,84 @@ void or_backward_params_sg(int64_t n, const float* means, const float* quats, co
         for (int k = 0; k < 3; ++k) acc += Ra[3 * i + k] * Rl[3 * k + j];
         Rw[3 * i + j] = acc;
       }
-    double G[9]; /* dL/dR_w[j][k] */
-    for (int k = 0; k < 3; ++k) {
-      const double s = scales[3 * g + k];
-      double ds = 0.0;
-      for (int j = 0; j < 3; ++j) {
-        const double dm = d_M[g * 9 + 3 * k + j];
-        G[3 * j + k] = dm / s;
-        ds -= dm * Rw[3 * j + k] / (s * s);
+    double G[9];     /* dL/dR_w[j][k] */
+    double dmu_w[3] = {d_mu[3 * g], d_mu[3 * g + 1], d_mu[3 * g + 2]};
+    if (beam_div > 0.0) {
+      /* App. C (A27): M_hat = chol(Sigma_hat)^-1, Sigma_hat = R S^2 R^T + theta^2 (r^2 I - v v^T),
+       * v = mu - o (o held at the mean's firing time, A31).  Backward: Mbar (lower) ->
+       * Lbar = -M^T Mbar M^T (lower) -> Sigma_bar = sym(M^T Phi(L^T Lbar) M), Phi = lower
+       * triangle with the diagonal halved (Cholesky backward) -> v, R, s. */
+      const double* v = &viewdir[3 * g];
+      const double t2 = beam_div * beam_div, r2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2];
+      double Sh[9], Lh[9], Mh[9], s2[3];
+      for (int k = 0; k < 3; ++k) s2[k] = (double)scales[3 * g + k] * (double)scales[3 * g + k];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+          double acc = 0.0;
+          for (int k = 0; k < 3; ++k) acc += Rw[3 * i + k] * s2[k] * Rw[3 * j + k];
+          Sh[3 * i + j] = acc + t2 * ((i == j ? r2 : 0.0) - v[i] * v[j]);
+        }
+      if (or_cholesky3(Sh, Lh)) {
+        for (int c = 0; c < 3; ++c) g_scales[3 * g + c] = 0.0;
+        continue;
       }
-      g_scales[3 * g + k] = ds;
+      or_lower_inverse3(Lh, Mh);
+      double Mb[9], Lb[9], X[9], P[9], S[9], Sb[9];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Mb[3 * i + j] = j <= i ? d_M[g * 9 + 3 * i + j] : 0.0;
+      for (int i = 0; i < 3; ++i) /* Lbar = -(M^T Mbar M^T), lower part */
+        for (int j = 0; j < 3; ++j) {
+          double acc = 0.0;
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) acc += Mh[3 * a + i] * Mb[3 * a + b] * Mh[3 * j + b];
+          Lb[3 * i + j] = j <= i ? -acc : 0.0;
+        }
+      for (int i = 0; i < 3; ++i) /* X = L^T Lbar */
+        for (int j = 0; j < 3; ++j) {
+          double acc = 0.0;
+          for (int a = 0; a < 3; ++a) acc += Lh[3 * a + i] * Lb[3 * a + j];
+          X[3 * i + j] = acc;
+        }
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) P[3 * i + j] = j < i ? X[3 * i + j] : (j == i ? 0.5 * X[3 * i + j] : 0.0);
+      for (int i = 0; i < 3; ++i) /* S = M^T P M */
+        for (int j = 0; j < 3; ++j) {
+          double acc = 0.0;
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) acc += Mh[3 * a + i] * P[3 * a + b] * Mh[3 * b + j];
+          S[3 * i + j] = acc;
+        }
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Sb[3 * i + j] = 0.5 * (S[3 * i + j] + S[3 * j + i]);
+      const double tr = Sb[0] + Sb[4] + Sb[8];
+      for (int i = 0; i < 3; ++i) { /* dv = 2 theta^2 (tr(Sb) v - Sb v) */
+        double sv = 0.0;
+        for (int j = 0; j < 3; ++j) sv += Sb[3 * i + j] * v[j];
+        dmu_w[i] += 2.0 * t2 * (tr * v[i] - sv);
+      }
+      for (int i = 0; i < 3; ++i) /* dR = 2 Sb R S^2 */
+        for (int k = 0; k < 3; ++k) {
+          double acc = 0.0;
+          for (int j = 0; j < 3; ++j) acc += Sb[3 * i + j] * Rw[3 * j + k];
+          G[3 * i + k] = 2.0 * acc * s2[k];
+        }
+      for (int k = 0; k < 3; ++k) { /* ds_k = 2 s_k (R^T Sb R)_kk */
+        double acc = 0.0;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) acc += Rw[3 * i + k] * Sb[3 * i + j] * Rw[3 * j + k];
+        g_scales[3 * g + k] = 2.0 * (double)scales[3 * g + k] * acc;
+      }
+    } else {
+      for (int k = 0; k < 3; ++k) {
+        const double s = scales[3 * g + k];
+        double ds = 0.0;
+        for (int j = 0; j < 3; ++j) {
+          const double dm = d_M[g * 9 + 3 * k + j];
+          G[3 * j + k] = dm / s;
+          ds -= dm * Rw[3 * j + k] / (s * s);
+        }
+        g_scales[3 * g + k] = ds;
+      }
     }
     double Gl[9], dmu_l[3];
     for (int i = 0; i < 3; ++i) {
@@ -1685,7 +1701,7 @@ void or_backward_params_sg(int64_t n, const float* means, const float* quats, co
         Gl[3 * i + j] = acc;
       }
       double m = 0.0;
-      for (int k = 0; k < 3; ++k) m += Ra[3 * k + i] * d_mu[3 * g + k];
+      for (int k = 0; k < 3; ++k) m += Ra[3 * k + i] * dmu_w[k];
       dmu_l[i] = m;
     }
     rot_grad_to_quat(Gl, ql, &g_quats[4 * g]);
@@ -1694,16 +1710,20 @@ void or_backward_params_sg(int64_t n, const float* means, const float* quats, co
       double* A = &Ga[12 * a];
       for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) {
-          double acc = d_mu[3 * g + i] * (double)means[3 * g + j]; /* dL/dmu_w mu_l^T */
+          double acc = dmu_w[i] * (double)means[3 * g + j]; /* dL/dmu_w mu_l^T */
           for (int k = 0; k < 3; ++k) acc += G[3 * i + k] * Rl[3 * j + k]; /* G R_l^T */
           A[3 * i + j] += acc;
         }
-      for (int c = 0; c < 3; ++c) A[9 + c] += d_mu[3 * g + c];
+      for (int c = 0; c < 3; ++c) A[9 + c] += dmu_w[c];
     }
+    double vu[3];
+    const double vl = sqrt(viewdir[3 * g] * viewdir[3 * g] + viewdir[3 * g + 1] * viewdir[3 * g + 1] +
+                           viewdir[3 * g + 2] * viewdir[3 * g + 2]);
+    for (int c = 0; c < 3; ++c) vu[c] = vl > 0.0 ? viewdir[3 * g + c] / vl : 0.0;
     for (int k = 0; k < nco; ++k) {
       double e[48] = {0}, yk[3];
       e[3 * k] = 1.0;
-      or_sh_eval(e, sh_degree, &viewdir[3 * g], yk);
+      or_sh_eval(e, sh_degree, vu, yk);
       for (int c = 0; c < 3; ++c) g_sh[(int64_t)g * nco * 3 + 3 * k + c] = yk[0] * d_feat[3 * g + c];
     }
   }

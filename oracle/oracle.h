@@ -101,7 +101,7 @@ typedef struct {
   double*  feat;            /* [n][3] SH features                                          */
   float*   key;             /* [n] float32 depth key (O10)                                 */
   double*  minrange;        /* [n] smallest sigma-point range / camera distance            */
-  double*  viewdir;         /* [n][3] unit SH view direction (A17) or NULL                 */
+  double*  viewdir;         /* [n][3] view vector mu - o(s0) (unnormalised; A17) or NULL    */
 } or_proj_out;
 
 typedef struct {
@@ -190,8 +190,9 @@ void or_backward_params(int64_t n, const float* quats, const float* scales, cons
  * poses (g_actor [n_actors][7] = dL/dq_a, dL/dt_a); d_mu / d_M are world-frame (O15). */
 void or_backward_params_sg(int64_t n, const float* means, const float* quats, const float* scales,
                            const double* viewdir, int32_t sh_degree, const int32_t* actor_id, int32_t n_actors,
-                           const double* actor_pose, const double* d_mu, const double* d_M, const double* d_feat,
-                           double* g_means, double* g_quats, double* g_scales, double* g_sh, double* g_actor);
+                           const double* actor_pose, double beam_div, const double* d_mu, const double* d_M,
+                           const double* d_feat, double* g_means, double* g_quats, double* g_scales, double* g_sh,
+                           double* g_actor);
 
 /* O0: scene graph, object particles -> world at the frame's timestamp (A29) */
 void or_actors_to_world(int64_t n, const float* means, const float* quats, const int32_t* actor_id,

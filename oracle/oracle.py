@@ -127,9 +127,8 @@ def lib():
         L.or_backward_composite.argtypes = [f64p, f64p, f64p, f64p, f32p, u32p, i32p, C.c_int32, i32p, f32p, f32p,
                                             f64p, i32p, C.POINTER(OrRenderParams), f64p, f64p, f64p, f64p, f64p,
                                             f64p, f64p, f64p]
-        L.or_backward_params.argtypes = [C.c_int64, f32p, f32p, f64p, C.c_int32, f64p, f64p, f64p, f64p, f64p]
         L.or_backward_params_sg.argtypes = [C.c_int64, f32p, f32p, f32p, f64p, C.c_int32, i32p, C.c_int32, f64p,
-                                            f64p, f64p, f64p, f64p, f64p, f64p, f64p, f64p]
+                                            C.c_double, f64p, f64p, f64p, f64p, f64p, f64p, f64p, f64p]
         L.or_actors_to_world.argtypes = [C.c_int64, f32p, f32p, i32p, C.c_int32, f64p, f32p, f32p]
         _lib = L
     return _lib
@@ -621,41 +620,34 @@ def backward_composite(records, ids, ranges, ray_tile, ray_a, ray_b, ray_od, Gz,
     return out
 
 
-def backward_params(scene, proj, d):
+def backward_params(scene, proj, d, beam_div=0.0):
     """O16: gradients of the particle parameters (means, quats, scales, opacity, sh); with a
-    scene graph also of the object poses ('actor_pose' [n_actors, 7]: dq_a, dt_a)."""
-    if scene.get("actor_id") is not None:
-        n = int(scene["means"].shape[0])
-        m = np.ascontiguousarray(scene["means"], np.float32)
-        q = np.ascontiguousarray(scene["quats"], np.float32)
-        s = np.ascontiguousarray(scene["scales"], np.float32)
-        ids = np.ascontiguousarray(scene["actor_id"], np.int32)
-        ap = _d(np.asarray(scene["actor_pose"], np.float32).astype(np.float64))
-        ncoef = scene["sh"].size // max(n, 1) // 3
-        deg = {1: 0, 4: 1, 9: 2, 16: 3}[ncoef]
-        out = {"means": np.zeros((n, 3)), "quats": np.zeros((n, 4)), "scales": np.zeros((n, 3)),
-               "sh": np.zeros((n, ncoef, 3)), "actor_pose": np.zeros((ap.shape[0], 7))}
-        lib().or_backward_params_sg(n, _p(m, f32p), _p(q, f32p), _p(s, f32p), _p(_d(proj["viewdir"]), f64p), deg,
-                                    _p(ids, i32p), int(ap.shape[0]), _p(ap, f64p), _p(_d(d["mu"]), f64p),
-                                    _p(_d(d["M"]), f64p), _p(_d(d["feat"]), f64p), _p(out["means"], f64p),
-                                    _p(out["quats"], f64p), _p(out["scales"], f64p), _p(out["sh"], f64p),
-                                    _p(out["actor_pose"], f64p))
-        out["opacity"] = d["sigma"].copy()
-        if d.get("sh_perray") is not None:
-            out["sh"] = d["sh_perray"].copy()
-        return out
+    scene graph the object-frame ones plus the object poses ('actor_pose' [n_actors, 7]:
+    dq_a, dt_a); with beam divergence (theta > 0) through Sigma_hat's Cholesky inverse.
+    proj['viewdir'] is the view vector mu - o (unnormalised)."""
     n = int(scene["means"].shape[0])
+    m = np.ascontiguousarray(scene["means"], np.float32)
     q = np.ascontiguousarray(scene["quats"], np.float32)
     s = np.ascontiguousarray(scene["scales"], np.float32)
+    act = scene.get("actor_id")
+    ids = None if act is None else np.ascontiguousarray(act, np.int32)
+    ap = None if act is None else _d(np.asarray(scene["actor_pose"], np.float32).astype(np.float64))
+    na = 0 if ap is None else int(ap.shape[0])
     ncoef = scene["sh"].size // max(n, 1) // 3
     deg = {1: 0, 4: 1, 9: 2, 16: 3}[ncoef]
-    gq, gs, gsh = np.zeros((n, 4)), np.zeros((n, 3)), np.zeros((n, ncoef, 3))
-    vd = _d(proj["viewdir"])
-    lib().or_backward_params(n, _p(q, f32p), _p(s, f32p), _p(vd, f64p), deg, _p(_d(d["M"]), f64p),
-                             _p(_d(d["feat"]), f64p), _p(gq, f64p), _p(gs, f64p), _p(gsh, f64p))
+    out = {"means": np.zeros((n, 3)), "quats": np.zeros((n, 4)), "scales": np.zeros((n, 3)),
+           "sh": np.zeros((n, ncoef, 3))}
+    ga = np.zeros((max(na, 1), 7))
+    lib().or_backward_params_sg(n, _p(m, f32p), _p(q, f32p), _p(s, f32p), _p(_d(proj["viewdir"]), f64p), deg,
+                                _p(ids, i32p), na, _p(ap, f64p), float(beam_div), _p(_d(d["mu"]), f64p),
+                                _p(_d(d["M"]), f64p), _p(_d(d["feat"]), f64p), _p(out["means"], f64p),
+                                _p(out["quats"], f64p), _p(out["scales"], f64p), _p(out["sh"], f64p), _p(ga, f64p))
+    if act is not None:
+        out["actor_pose"] = ga[:na]
+    out["opacity"] = d["sigma"].copy()
     if d.get("sh_perray") is not None:  # per-ray SH: the SH gradient came from O15 directly
-        gsh = d["sh_perray"].copy()
-    return {"means": d["mu"].copy(), "quats": gq, "scales": gs, "opacity": d["sigma"].copy(), "sh": gsh}
+        out["sh"] = d["sh_perray"].copy()
+    return out
 
 
 def backward_lidar(scene, cfg, grads, tiling: Tiling | None = None, pose0=None, pose1=None, K=None, ut=None,
@@ -677,7 +669,7 @@ def backward_lidar(scene, cfg, grads, tiling: Tiling | None = None, pose0=None, 
     d = backward_composite(rec, ids, ranges, tiling.ray_tile, tiling.ray_az, tiling.ray_el, fwd["ray_od"], Gz, Go,
                            GD, wrap=1, near=cfg.min_range, alpha_min=alpha_min, alpha_max=alpha_max, T_min=T_min,
                            pi_f=tiling.pi_f, two_pi_f=tiling.two_pi_f)
-    out = backward_params(scene, proj, d)
+    out = backward_params(scene, proj, d, beam_div=getattr(cfg, "beam_divergence", 0.0))
     out["fwd"] = fwd
     out["d"] = d
     return out

@@ -666,10 +666,10 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
         pose_at(A.pose, s0, Rs, ts);
       }
       float vx = mu[0] - ts[0], vy = mu[1] - ts[1], vz = mu[2] - ts[2];
+      vdir[0] = vx; vdir[1] = vy; vdir[2] = vz;  // the view vector, unnormalised (backward, A31)
       const float vn = rsqrtf(vx * vx + vy * vy + vz * vz);
       vx *= vn; vy *= vn; vz *= vn;
       if (isfinite(vn)) {
-        vdir[0] = vx; vdir[1] = vy; vdir[2] = vz;
         if (stage_sh) {
           asm volatile("cp.async.wait_group 0;" ::: "memory");
           // coefficients streamed from shared memory one float4 at a time (coefficient

@@ -1614,6 +1614,7 @@ struct ParamsArgs {
   const float* actor_pose;  // [n_actors][7]
   int n_actors, ncoef;
   int per_ray_sh;  // the SH gradient was accumulated by the list walk (A30)
+  float beam_div;  // App. C theta (LiDAR), 0 = off
   int64_t n;
 };
 
@@ -1656,18 +1657,111 @@ __global__ void __launch_bounds__(256) k_backward_params(const ParamsArgs P, sim
     for (int i = 0; i < 3; ++i)
 #pragma unroll
       for (int j = 0; j < 3; ++j) Rw[3 * i + j] = Ra[3 * i] * Rl[j] + Ra[3 * i + 1] * Rl[3 + j] + Ra[3 * i + 2] * Rl[6 + j];
-    float G[9];  // dL/dR_w[j][k] = dL/dM[k][j] / s_k
+    float G[9];  // dL/dR_w[j][k]
+    if (P.beam_div > 0.f) {
+      // App. C (A27): M = chol(Sigma_hat)^-1 -> Lbar = -(M^T Mbar M^T) (lower) -> Sigma_bar =
+      // sym(M^T Phi(L^T Lbar) M), Phi = lower triangle with the diagonal halved -> dv, dR, ds
+      const float vv[3] = {__ldg(P.view_dir + 3 * g), __ldg(P.view_dir + 3 * g + 1), __ldg(P.view_dir + 3 * g + 2)};
+      const float t2 = P.beam_div * P.beam_div, r2 = vv[0] * vv[0] + vv[1] * vv[1] + vv[2] * vv[2];
+      float s2[3], Sh[9];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float s = __ldg(P.scales + 3 * g + k);
-      float ds = 0.f;
-#pragma unroll
-      for (int jj = 0; jj < 3; ++jj) {
-        const float dm = v[3 + 3 * k + jj];
-        G[3 * jj + k] = dm / s;
-        ds -= dm * Rw[3 * jj + k] / (s * s);
+      for (int k = 0; k < 3; ++k) {
+        const float sk = __ldg(P.scales + 3 * g + k);
+        s2[k] = sk * sk;
       }
-      gs[k] = ds;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          Sh[3 * i + j] = Rw[3 * i] * s2[0] * Rw[3 * j] + Rw[3 * i + 1] * s2[1] * Rw[3 * j + 1] +
+                          Rw[3 * i + 2] * s2[2] * Rw[3 * j + 2] + t2 * ((i == j ? r2 : 0.f) - vv[i] * vv[j]);
+      float Lh[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      Lh[0] = sqrtf(Sh[0]);
+      Lh[3] = Sh[3] / Lh[0];
+      Lh[6] = Sh[6] / Lh[0];
+      Lh[4] = sqrtf(Sh[4] - Lh[3] * Lh[3]);
+      Lh[7] = (Sh[7] - Lh[6] * Lh[3]) / Lh[4];
+      Lh[8] = sqrtf(Sh[8] - Lh[6] * Lh[6] - Lh[7] * Lh[7]);
+      float Mh[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // L^-1 (lower)
+      Mh[0] = 1.f / Lh[0];
+      Mh[4] = 1.f / Lh[4];
+      Mh[8] = 1.f / Lh[8];
+      Mh[3] = -Lh[3] * Mh[0] * Mh[4];
+      Mh[7] = -Lh[7] * Mh[4] * Mh[8];
+      Mh[6] = -(Lh[6] * Mh[0] + Lh[7] * Mh[3]) * Mh[8];
+      float Lb[9], X[9], Pm[9], S[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          float acc = 0.f;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b <= a; ++b) acc += Mh[3 * a + i] * v[3 + 3 * a + b] * Mh[3 * j + b];
+          Lb[3 * i + j] = j <= i ? -acc : 0.f;
+        }
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) X[3 * i + j] = Lh[i] * Lb[j] + Lh[3 + i] * Lb[3 + j] + Lh[6 + i] * Lb[6 + j];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Pm[3 * i + j] = j < i ? X[3 * i + j] : (j == i ? 0.5f * X[3 * i + j] : 0.f);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          float acc = 0.f;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) acc += Mh[3 * a + i] * Pm[3 * a + b] * Mh[3 * b + j];
+          S[3 * i + j] = acc;
+        }
+      float Sb[9];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Sb[3 * i + j] = 0.5f * (S[3 * i + j] + S[3 * j + i]);
+      const float tr = Sb[0] + Sb[4] + Sb[8];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        v[i] += 2.f * t2 * (tr * vv[i] - (Sb[3 * i] * vv[0] + Sb[3 * i + 1] * vv[1] + Sb[3 * i + 2] * vv[2]));
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          G[3 * i + k] = 2.f * (Sb[3 * i] * Rw[k] + Sb[3 * i + 1] * Rw[3 + k] + Sb[3 * i + 2] * Rw[6 + k]) * s2[k];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) acc += Rw[3 * i + k] * Sb[3 * i + j] * Rw[3 * j + k];
+        gs[k] = 2.f * __ldg(P.scales + 3 * g + k) * acc;
+      }
+      if (!isfinite(Lh[8]) || !(Lh[8] > 0.f)) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) G[q] = 0.f;
+        gs[0] = gs[1] = gs[2] = 0.f;
+      }
+      gm[0] = v[0]; gm[1] = v[1]; gm[2] = v[2];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float s = __ldg(P.scales + 3 * g + k);
+        float ds = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+          const float dm = v[3 + 3 * k + jj];
+          G[3 * jj + k] = dm / s;
+          ds -= dm * Rw[3 * jj + k] / (s * s);
+        }
+        gs[k] = ds;
+      }
     }
     if (a < 0) {
       rot_grad_to_quat(G, q, inv, gq);
@@ -1708,7 +1802,12 @@ __global__ void __launch_bounds__(256) k_backward_params(const ParamsArgs P, sim
   for (int c = 0; c < 3; ++c) out.scales[3 * g + c] = gs[c];
   if (P.per_ray_sh) return;
   float b[16];
-  sh_basis3(__ldg(P.view_dir + 3 * g), __ldg(P.view_dir + 3 * g + 1), __ldg(P.view_dir + 3 * g + 2), b);
+  {
+    const float vx = __ldg(P.view_dir + 3 * g), vy = __ldg(P.view_dir + 3 * g + 1), vz = __ldg(P.view_dir + 3 * g + 2);
+    const float l2 = vx * vx + vy * vy + vz * vz;
+    const float iv = l2 > 0.f ? rsqrtf(l2) : 0.f;
+    sh_basis3(vx * iv, vy * iv, vz * iv, b);
+  }
   float* o = out.sh + (size_t)g * P.ncoef * 3;
   for (int k = 0; k < P.ncoef; ++k)
 #pragma unroll
@@ -1767,9 +1866,10 @@ void bwd_fill_common(BwdArgs& A, const simuli_projected* proj, const uint32_t* i
 }
 
 int32_t bwd_params(const simuli_gaussians* G, const simuli_projected* proj, const simuli_gaussian_grads* gout,
-                   const float* ws, bool per_ray_sh, cudaStream_t st, const char* what) {
+                   const float* ws, bool per_ray_sh, float beam_div, cudaStream_t st, const char* what) {
   ParamsArgs P{};
   P.per_ray_sh = per_ray_sh ? 1 : 0;
+  P.beam_div = beam_div;
   P.ws = ws; P.means = G->means; P.quats = G->quats; P.scales = G->scales; P.view_dir = proj->view_dir;
   P.ncoef = (G->sh_degree + 1) * (G->sh_degree + 1);
   P.n = G->n;
@@ -1840,10 +1940,7 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
   if (rc != SIMULI_OK || G->n == 0) return rc;
   SIMULI_REQUIRE(gin, "simuli_backward_lidar: NULL grad_in");
   SIMULI_REQUIRE(P->kind == SIMULI_SENSOR_LIDAR && P->lidar && P->tiling, "simuli_backward_lidar: needs LiDAR params");
-  if (P->lidar->beam_divergence_rad > 0.f) {
-    set_error("simuli_backward_lidar: beam divergence has no backward (A31)");
-    return SIMULI_ERR_UNSUPPORTED;
-  }
+
   const simuli_tiling_dev& T = *P->tiling;
   SIMULI_REQUIRE(T.tile_ray_offsets && T.tile_rays && T.ray_az && T.ray_el && T.ray_s && T.n_tiles >= 1,
                  "simuli_backward_lidar: incomplete device tiling");
@@ -1872,8 +1969,8 @@ extern "C" int32_t simuli_backward_lidar(const simuli_gaussians* G, const simuli
     k_backward_lidar<<<(unsigned)(T.n_tiles * A.chunks), 32, 0, st>>>(A);
   const int32_t lc = launch_check("simuli_backward_lidar");
   if (lc != SIMULI_OK) return lc;
-  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), A.sh != nullptr, st,
-                    "simuli_backward_lidar (params)");
+  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), A.sh != nullptr,
+                    P->lidar->beam_divergence_rad, st, "simuli_backward_lidar (params)");
 }
 
 extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simuli_projected* proj,
@@ -1923,6 +2020,6 @@ extern "C" int32_t simuli_backward_camera(const simuli_gaussians* G, const simul
   else k_backward_camera<16><<<tiles * 8, 32, 0, st>>>(A);
   const int32_t lc = launch_check("simuli_backward_camera");
   if (lc != SIMULI_OK) return lc;
-  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), A.sh != nullptr, st,
+  return bwd_params(G, proj, gout, static_cast<const float*>(workspace), A.sh != nullptr, 0.f, st,
                     "simuli_backward_camera (params)");
 }

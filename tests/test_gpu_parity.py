@@ -815,8 +815,8 @@ def test_backward_camera_parity(SM, oracle_mod, variant):
     _compare_grads(got, ref, f"{variant} tier 1")
 
 
-def test_backward_empty_and_unsupported(SM):
-    """n = 0 is a no-op; beam divergence has no backward (UNSUPPORTED)."""
+def test_backward_empty(SM):
+    """n = 0 is a no-op."""
     cfg = S.lidar_config("A")
     sc = {k: v[:0] for k, v in S.scene_for("A").items()}
     r = SM.LidarRenderer(cfg, SM.to_device_scene(sc))
@@ -825,25 +825,18 @@ def test_backward_empty_and_unsupported(SM):
     out = r.backward({"opacity": torch.ones(r.n_rays, device="cuda")})
     torch.cuda.synchronize()
     assert out["means"].numel() == 0
-    sc = S.scene_for("A")
-    for kw, div in (({}, 1.5e-3),):
-        c2 = S.lidar_config("A")
-        c2.beam_divergence = div
-        r = SM.LidarRenderer(c2, SM.to_device_scene(sc), **kw)
-        r.requires_grad(True)
-        r.scan(sync_capacity=True)
-        with pytest.raises(SM.SimuliError) as e:
-            r.backward({"opacity": torch.ones(r.n_rays, device="cuda")})
-        assert e.value.code == SM.SIMULI_ERR_UNSUPPORTED
 
 
-def test_backward_scene_graph_parity(SM, oracle_mod):
-    """Backward through the scene graph (A29, A31): object-frame particle gradients and the
-    object-pose gradients (dq_a, dt_a) vs O15/O16 on the GPU's records, lists and rays."""
+@pytest.mark.parametrize("config", ["A", "B-sub"])
+def test_backward_beam_divergence_parity(SM, oracle_mod, config):
+    """Backward with the App. C filter (A27, A31): M = chol(Sigma_hat)^-1 through the
+    Cholesky factor and the view vector, tier 1 against O15/O16."""
     O = oracle_mod
-    cfg = S.lidar_config("B")
-    scene = S.with_actors(S.corridor_scene(41, 60_000, x_range=(-60.0, 60.0)), 42, n_actors=12, per_actor=2000,
-                          x_range=(-40.0, 40.0))
+    if config == "B-sub":
+        cfg, scene = S.lidar_config("B"), S.scene_for("B", n=200_000)
+    else:
+        cfg, scene = S.lidar_config(config), S.scene_for(config)
+    cfg.beam_divergence = 1.5e-3
     r = SM.LidarRenderer(cfg, SM.to_device_scene(scene))
     r.requires_grad(True)
     r.want_ray_od(True)
@@ -856,18 +849,15 @@ def test_backward_scene_graph_parity(SM, oracle_mod):
     fwd = O.composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, wrap=1, near=cfg.min_range,
                       flag_eps={"a": 0.0, "b": 0.0, "alpha": 2e-7, "T_rel": 1e-4, "tau": 1e-4},
                       pi_f=t.pi_f, two_pi_f=t.two_pi_f)
-    g = _upstream(od.shape[0], 9, True, fwd["flag"] == 0)
+    g = _upstream(od.shape[0], 13, True, fwd["flag"] == 0)
     got = r.backward(_dev(g))
     torch.cuda.synchronize()
     gz, go, gd = O.fold_upstream(fwd, g, lidar=True)
     d = O.backward_composite(rec, ids, ranges, t.ray_tile, t.ray_az, t.ray_el, od, gz, go, gd, wrap=1,
                              near=cfg.min_range, pi_f=t.pi_f, two_pi_f=t.two_pi_f)
-    ref = O.backward_params(scene, {"viewdir": r.view_dir.cpu().numpy().astype(np.float64)}, d)
-    _compare_grads(got, ref, "scene graph tier 1")
-    a = got["actor_pose"].cpu().numpy().astype(np.float64)
-    scale = np.abs(ref["actor_pose"]).max()
-    print("actor pose grads: max |gpu - oracle| / max", np.abs(a - ref["actor_pose"]).max() / scale)
-    assert scale > 0 and np.abs(a - ref["actor_pose"]).max() <= 1e-3 * scale
+    ref = O.backward_params(scene, {"viewdir": r.view_dir.cpu().numpy().astype(np.float64)}, d,
+                            beam_div=cfg.beam_divergence)
+    _compare_grads(got, ref, f"divergence {config} tier 1")
 
 
 @pytest.mark.parametrize("sensor", ["lidar", "camera"])

@@ -1188,3 +1188,40 @@ def test_backward_per_ray_sh_vs_finite_differences(oracle_mod):
                     bad += 1
                     print("mismatch", i, key, c, num, an)
     assert checked == 21 and bad <= 1, bad
+
+
+def test_backward_beam_divergence_vs_finite_differences(oracle_mod):
+    """App. C backward (A27, A31): M_hat = chol(Sigma_hat)^-1 differentiated through the
+    Cholesky factor (Sigma_bar = sym(M^T Phi(L^T Lbar) M)) and Sigma_hat's dependence on the
+    view vector; central differences of the forward on a static-pose sensor (the sensor
+    position does not move with the mean's firing time)."""
+    O = oracle_mod
+    cfg = S.lidar_config("A")
+    cfg.beam_divergence = 5e-3
+    sc = S.scene_for("A", seed=41, n=400)
+    sc["sh"] = np.ascontiguousarray(sc["sh"][:, :1])
+    fwd = O.render_lidar(sc, cfg)
+    R = fwd["opacity"].shape[0]
+    rng = np.random.default_rng(42)
+    g = {"zeta": rng.normal(size=(R, 3)), "opacity": rng.normal(size=R), "depth_accum": 0.1 * rng.normal(size=R),
+         "depth": 0.1 * rng.normal(size=R), "intensity": rng.normal(size=R), "raydrop": rng.normal(size=R)}
+    b = O.backward_lidar(sc, cfg, g)
+    checked = bad = 0
+    for i in np.argsort(-np.abs(b["opacity"]))[:4]:
+        for key, h, dims in (("means", 1e-4, 3), ("quats", 1e-4, 4), ("scales", 5e-5, 3)):
+            for c in range(dims):
+                vals, deltas = [], []
+                for sgn in (1, -1):
+                    s2 = {k: v.copy() for k, v in sc.items()}
+                    arr = s2[key].reshape(sc["means"].shape[0], -1)
+                    x0 = np.float32(arr[i, c])
+                    arr[i, c] = np.float32(x0 + sgn * h * max(1.0, abs(float(x0))))
+                    deltas.append(float(arr[i, c]) - float(x0))
+                    vals.append(_loss(O, s2, cfg, g))
+                num = (vals[0] - vals[1]) / (deltas[0] - deltas[1])
+                an = b[key].reshape(sc["means"].shape[0], -1)[i, c]
+                checked += 1
+                if abs(num - an) > 2e-3 * max(1.0, abs(an)):
+                    bad += 1
+                    print("mismatch", i, key, c, num, an)
+    assert checked == 40 and bad <= 2, bad
