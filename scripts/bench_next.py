@@ -57,7 +57,19 @@ ga = {k: torch.randn(fa.n_rays, device="cuda") for k in ("opacity", "depth")}
 ga["zeta"] = torch.randn(fa.n_rays, 3, device="cuda")
 torch.cuda.synchronize()
 bwd_sg = {"forward_us": timed(lambda: fa.scan()), "backward_us": timed(lambda: fa.backward(ga))}
-del fa, devB
+del fa
+# NEXT-2 x NEXT-4: backward with beam divergence and with per-ray SH
+bwd_var = {}
+for label, cfg_v, kw in (("beam divergence 1.5 mrad", cfgD, {}), ("per-ray SH", cfgB, {"per_ray_sh": True})):
+    fv = SM.LidarRenderer(cfg_v, devB, **kw)
+    fv.requires_grad(True)
+    fv.scan(sync_capacity=True)
+    gv = {k: torch.randn(fv.n_rays, device="cuda") for k in ("opacity", "depth")}
+    gv["zeta"] = torch.randn(fv.n_rays, 3, device="cuda")
+    torch.cuda.synchronize()
+    bwd_var[label] = {"forward_us": timed(lambda: fv.scan()), "backward_us": timed(lambda: fv.backward(gv))}
+    del fv
+del devB
 torch.cuda.empty_cache()
 
 # NEXT-3b: Eq. 2 composition on config D
@@ -102,7 +114,7 @@ for name in ("B", "C", "D"):
     torch.cuda.empty_cache()
 
 out = {"lidar_stages_us": {k: v for k, v in rows}, "camera_stages_us": cam_stages, "compose_D": compose,
-       "backward": bwd, "backward_scene_graph_B": bwd_sg,
+       "backward": bwd, "backward_scene_graph_B": bwd_sg, "backward_variants_B": bwd_var,
        "gpu": torch.cuda.get_device_name(0)}
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 json.dump(out, open(os.path.join(ROOT, "profiles", "r01_next.json"), "w"), indent=1)
@@ -130,5 +142,7 @@ for k, v in bwd.items():
               f"{v['backward_own_totals_us']:.1f} |")
 md += ["", f"Backward through the scene graph (B + 64 objects, object-frame and object-pose gradients): "
            f"forward {bwd_sg['forward_us']:.1f} µs, backward {bwd_sg['backward_us']:.1f} µs."]
+for k, v in bwd_var.items():
+    md += ["", f"Backward of config B with {k}: forward {v['forward_us']:.1f} µs, backward {v['backward_us']:.1f} µs."]
 open(os.path.join(ROOT, "profiles", "r01_next.md"), "w").write("\n".join(md) + "\n")
 print("\n".join(md))
