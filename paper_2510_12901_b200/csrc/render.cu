@@ -999,13 +999,17 @@ extern "C" int32_t simuli_compose_camera(const simuli_project_params* P, const s
 // ====================================================================== backward (A31)
 // Gradients of the compositing (Eq. 1) and of the response with respect
 // to the particle records, chained to the parameters.  Per ray the tile's list is
-// replayed twice with the forward kernels' float32 arithmetic, so every discrete decision
-// (membership, skips, termination) is the forward's: pass 1 -> totals (zeta, omega, D),
-// pass 2 -> per contribution k with suffix sums S_k = total - prefix_k:
+// replayed with the forward kernels' float32 arithmetic, so every discrete decision
+// (membership, skips, termination) is the forward's; per contribution k, with suffix sums
+// S_k = total - prefix_k:
 //   dL/dalpha_k = T_k (Gz.f_k + Go + GD tau_k) - (Gz.S_k(f) + Go S_k(1) + GD S_k(tau)) / (1 - alpha_k)
-// (oracle O15).  All lanes of a warp walk the same list entry, so a contribution's 16
-// gradient values (dmu 3, dM 9, dsigma, df 3) are warp-reduced by shuffles and added with one
-// set of float atomics per entry.
+// (oracle O15).  The totals come from the forward's outputs (or a first list pass).  All
+// lanes of a warp walk the same list entry, so a contribution's 16 gradient values (dmu 3,
+// dM 9, dsigma, df 3) are warp-reduced by a reduce-scatter butterfly and added with one set
+// of float atomics per entry.  LiDAR lists are cut into 512-entry segments (a stats pass of
+// per-segment transmittance products, then the gradient pass); k_backward_params chains
+// (dmu, dM, dsigma, df) to the particle parameters, the object poses (scene graph) and,
+// with beam divergence, through the Cholesky factor of Sigma_hat.
 namespace simuli {
 namespace {
 
