@@ -1804,7 +1804,7 @@ __global__ void __launch_bounds__(256) k_backward_params(const ParamsArgs P, sim
   for (int c = 0; c < 3; ++c) out.means[3 * g + c] = gm[c];
   reinterpret_cast<float4*>(out.quats)[g] = make_float4(gq[0], gq[1], gq[2], gq[3]);
   for (int c = 0; c < 3; ++c) out.scales[3 * g + c] = gs[c];
-  if (P.per_ray_sh) return;
+  if (P.per_ray_sh || P.ncoef == 16) return;  // degree 3: k_backward_sh16
   float b[16];
   {
     const float vx = __ldg(P.view_dir + 3 * g), vy = __ldg(P.view_dir + 3 * g + 1), vz = __ldg(P.view_dir + 3 * g + 2);
@@ -1816,6 +1816,35 @@ __global__ void __launch_bounds__(256) k_backward_params(const ParamsArgs P, sim
   for (int k = 0; k < P.ncoef; ++k)
 #pragma unroll
     for (int c = 0; c < 3; ++c) o[3 * k + c] = b[k] * v[13 + c];
+}
+
+// dL/dSH = Y_k(v) dL/df for degree 3: each thread builds its particle's 48 values in
+// shared memory, then the warp stores its 32 particles' 6 KB as coalesced float4 rows
+__global__ void __launch_bounds__(256) k_backward_sh16(const float* __restrict__ ws,
+                                                       const float* __restrict__ view_dir, int64_t n,
+                                                       float* __restrict__ gsh) {
+  __shared__ float4 s_rows[256 * 12];
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w0 = threadIdx.x & ~31;
+  if (g < n) {
+    const float vx = __ldg(view_dir + 3 * g), vy = __ldg(view_dir + 3 * g + 1), vz = __ldg(view_dir + 3 * g + 2);
+    const float l2 = vx * vx + vy * vy + vz * vz;
+    const float iv = l2 > 0.f ? rsqrtf(l2) : 0.f;
+    float b[16];
+    sh_basis3(vx * iv, vy * iv, vz * iv, b);
+    const float df[3] = {__ldg(ws + g * kBwdVals + 13), __ldg(ws + g * kBwdVals + 14), __ldg(ws + g * kBwdVals + 15)};
+    float4* row = s_rows + threadIdx.x * 12;
+#pragma unroll
+    for (int j = 0; j < 12; ++j)  // element q = 4 j + e: coefficient q / 3, channel q % 3
+      row[j] = make_float4(b[(4 * j) / 3] * df[(4 * j) % 3], b[(4 * j + 1) / 3] * df[(4 * j + 1) % 3],
+                           b[(4 * j + 2) / 3] * df[(4 * j + 2) % 3], b[(4 * j + 3) / 3] * df[(4 * j + 3) % 3]);
+  }
+  __syncwarp();
+  const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + w0;
+  const int np = n - g0 >= 32 ? 32 : (int)(n - g0);
+  float4* dst = reinterpret_cast<float4*>(gsh) + g0 * 12;
+  const float4* src = s_rows + w0 * 12;
+  for (int t = lane; t < np * 12; t += 32) dst[t] = src[t];
 }
 
 int32_t bwd_common_checks(const simuli_gaussians* G, const simuli_projected* proj, const uint32_t* ids,
@@ -1886,7 +1915,11 @@ int32_t bwd_params(const simuli_gaussians* G, const simuli_projected* proj, cons
   } else {
     o.actor_pose = nullptr;
   }
-  if (G->n > 0) k_backward_params<<<(unsigned)((G->n + 255) / 256), 256, 0, st>>>(P, o);
+  if (G->n > 0) {
+    k_backward_params<<<(unsigned)((G->n + 255) / 256), 256, 0, st>>>(P, o);
+    if (!per_ray_sh && P.ncoef == 16)
+      k_backward_sh16<<<(unsigned)((G->n + 255) / 256), 256, 0, st>>>(ws, proj->view_dir, G->n, o.sh);
+  }
   return launch_check(what);
 }
 
