@@ -386,8 +386,8 @@ int32_t simuli_backward_workspace_size(int64_t n, int64_t pair_capacity, int32_t
  * then one thread per particle for the parameter chain.  Asynchronous on `stream`;
  * gradient sums are in atomic (nondeterministic) order.
  * n = 0: returns SIMULI_OK without reading any other argument.
- * Errors: INVALID_ARGUMENT (NULL, view_dir missing, workspace too small), UNSUPPORTED
- * (see above), CUDA. */
+ * Errors: INVALID_ARGUMENT (NULL, view_dir missing, workspace below 64 n bytes, per-ray
+ * SH of another degree, scene graph without poses), UNSUPPORTED (sh_degree > 3), CUDA. */
 int32_t simuli_backward_lidar(const simuli_gaussians* gaussians, const simuli_projected* proj,
                               const uint32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
                               const simuli_project_params* params, const simuli_render_params* rparams,
