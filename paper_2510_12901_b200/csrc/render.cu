@@ -1534,7 +1534,7 @@ __global__ void __launch_bounds__(32) k_bwd_seg(const BwdArgs A, int n_tiles, in
     const int2 rg = __ldg(A.ranges + tile);
     const int nseg = segmented ? max(1, (rg.y - rg.x + kBwdSeg - 1) / kBwdSeg) : 1;
     const int local = item - __ldg(item_off + slot), group = local / nseg, sgi = local % nseg;
-    if (STATS && nseg == 1) continue;  // a single segment starts from T = 1
+    if (STATS && sgi == nseg - 1) continue;  // the last segment's stats are never read
     RayF rf;
     float shb[16];
     int ray;
