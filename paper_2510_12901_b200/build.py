@@ -19,9 +19,9 @@ LIB = os.path.join(HERE, "libsimuli.so")
 ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
 
-CU_SOURCES = ["project.cu", "binsort.cu", "render.cu"]
+CU_SOURCES = ["project.cu", "binsort.cu", "render.cu", "backward.cu"]
 CPP_SOURCES = ["tiling_host.cpp", "abi.cpp"]
-HEADERS = ["common.cuh", "abi_util.h"]
+HEADERS = ["common.cuh", "camera.cuh", "abi_util.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

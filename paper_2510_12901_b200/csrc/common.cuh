@@ -4,8 +4,19 @@
 #include <stdint.h>
 
 #include "../../include/simuli.h"
+#include "abi_util.h"
 
 namespace simuli {
+
+// status of the last kernel launch as a libsimuli error code (with the CUDA message)
+inline int32_t launch_check(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+    return SIMULI_ERR_CUDA;
+  }
+  return SIMULI_OK;
+}
 
 constexpr int kRecordFloats = 20;  // mu 3, M 9, opacity 1, f 3, box 4  (80 B)
 
