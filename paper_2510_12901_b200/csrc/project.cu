@@ -421,6 +421,13 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool stage_sh = A.sh_degree == 3;
+  // ---- loads first (SoA; quaternion as one 16-byte load): their latency overlaps the SH
+  // staging below (lanes past n read particle n - 1 and return after the staging)
+  const int64_t gl = g < A.n ? g : A.n - 1;
+  float mu[3] = {__ldg(A.means + 3 * gl), __ldg(A.means + 3 * gl + 1), __ldg(A.means + 3 * gl + 2)};
+  float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + gl);
+  const float sc[3] = {__ldg(A.scales + 3 * gl), __ldg(A.scales + 3 * gl + 1), __ldg(A.scales + 3 * gl + 2)};
+  const float sigma = __ldg(A.opacity + gl);
   if (stage_sh) {
     const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + wid * 32;
     const float4* src = reinterpret_cast<const float4*>(A.sh) + g0 * 12;
@@ -437,11 +444,6 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
     if (stage_sh) asm volatile("cp.async.wait_group 0;" ::: "memory");
     return;
   }
-  // ---- loads (SoA; quaternion as one 16-byte load)
-  float mu[3] = {__ldg(A.means + 3 * g), __ldg(A.means + 3 * g + 1), __ldg(A.means + 3 * g + 2)};
-  float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + g);
-  const float sc[3] = {__ldg(A.scales + 3 * g), __ldg(A.scales + 3 * g + 1), __ldg(A.scales + 3 * g + 2)};
-  const float sigma = __ldg(A.opacity + g);
   bool actor_ok = true;
   if (ACT) {
     // scene graph (A29): object particle -> world with its object's pose at t;
