@@ -26,11 +26,12 @@
 // hi / lo parts for the compensated response (common.cuh).
 // Camera (k_render_camera): one CTA per (16x16 tile, band of 4 pixel rows) -- a tile's four
 // bands share its list, so the long near-field lists are spread over four CTAs -- items
-// longest-list-first, pixel per thread, 128-record batches in shared memory; each warp
-// ballots which entries overlap its 2 x 16 pixel strip and walks only those; CTA-wide early
-// exit.  Config D (1920x1080 fisheye, 2M particles) render: 2.31 ms (one 256-thread CTA per
-// tile) -> 2.01 (strip pre-cull) -> 1.08 (4 bands; 8 bands: 1.15).  Pixel rays by the inverse
-// lens model in double.
+// longest-list-first, pixel per thread, 128-record batches in shared memory, double-buffered
+// (batch k + 1 arrives by cp.async, its ids prefetched a batch earlier, while batch k is
+// walked); each warp ballots which entries overlap its 2 x 16 pixel strip and walks only
+// those; CTA-wide early exit.  Config D (1920x1080 fisheye, 2M particles) render: 2.31 ms
+// (one 256-thread CTA per tile) -> 2.01 (strip pre-cull) -> 1.08 (4 bands; 8 bands: 1.15)
+// -> 0.97 (double-buffered batches).  Pixel rays by the inverse lens model in double.
 #include <cstdint>
 #include <cstdlib>
 #include <string>
@@ -42,6 +43,14 @@
 namespace simuli {
 namespace {
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // One CTA per (tile, band of TP / SPLIT pixel rows): the bands of a tile read the same list,
 // so a long list (near-field particles covering many pixels) is spread over SPLIT CTAs
 // instead of one; items are scheduled longest list first (tile_order).
@@ -49,8 +58,10 @@ template <int TP, int SPLIT, bool PRAY>
 __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraArgs A) {
   constexpr int NTH = TP * TP / SPLIT;  // threads = pixels of the band
   constexpr int NT = 128;               // list entries staged per batch
-  __shared__ float4 s_rec[NT][5];
-  __shared__ uint32_t s_id[PRAY ? NT : 1];  // particle ids of the batch (per-ray SH)
+  constexpr int PER = NT / NTH;         // entries per thread per batch
+  // two batch buffers: batch k + 1's records are copied (cp.async) while batch k is walked
+  __shared__ float4 s_rec2[2][NT][5];
+  __shared__ uint32_t s_id2[2][PRAY ? NT : 1];  // particle ids of the batch (per-ray SH)
   const int tid = threadIdx.x;
   const int slot = (int)(blockIdx.x / SPLIT), band = (int)(blockIdx.x % SPLIT);
   const int tile = A.order ? __ldg(A.order + slot) : slot;
@@ -77,17 +88,43 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
   int nc = 0, nv = 0, ni = 0, term_at = -1;
   bool done = !(inside && valid);
   const int2 rg = __ldg(A.ranges + tile);
-  for (int b = rg.x; b < rg.y; b += NT) {
-    if (__syncthreads_count(!done) == 0) break;
-    const int nb = min(NT, rg.y - b);
-    for (int e = tid; e < nb; e += NTH) {
-      const uint32_t g = __ldg(A.ids + b + e);
-      const float4* src = A.record + (size_t)g * 5;
+  const int nbatch = (rg.y - rg.x + NT - 1) / NT;
+  auto load_ids = [&](int bi, uint32_t out[PER]) {  // ids of batch bi (registers; used a batch later)
 #pragma unroll
-      for (int c = 0; c < 5; ++c) s_rec[e][c] = __ldg(src + c);
-      if (PRAY) s_id[e] = g;
+    for (int q = 0; q < PER; ++q) {
+      const int pos = rg.x + bi * NT + tid + q * NTH;
+      out[q] = (bi < nbatch && pos < rg.y) ? __ldg(A.ids + pos) : 0u;
     }
+  };
+  auto issue = [&](int bi, const uint32_t idv[PER]) {  // batch bi's records into buffer bi & 1
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * NTH, pos = rg.x + bi * NT + e;
+      if (bi < nbatch && pos < rg.y) {
+        const float4* src = A.record + (size_t)idv[q] * 5;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) cp_async16(&s_rec2[bi & 1][e][c], src + c);
+        if (PRAY) s_id2[bi & 1][e] = idv[q];
+      }
+    }
+    cp_async_commit();
+  };
+  uint32_t idn[PER];
+  load_ids(0, idn);
+  issue(0, idn);
+  load_ids(1, idn);
+  for (int bi = 0; bi < nbatch; ++bi) {
+    // the count barrier also means every thread is done with batch bi - 1, whose buffer
+    // batch bi + 1 reuses
+    if (__syncthreads_count(!done) == 0) break;
+    issue(bi + 1, idn);
+    load_ids(bi + 2, idn);
+    cp_async_wait<1>();  // this thread's copies of batch bi have landed
     __syncthreads();
+    const int b = rg.x + bi * NT;
+    const int nb = min(NT, rg.y - b);
+    float4 (*s_rec)[5] = s_rec2[bi & 1];
+    const uint32_t* s_id = s_id2[bi & 1];
     // warp-level pre-cull: the warp's pixels form a strip of 32 / TP rows x TP columns; an
     // entry whose box misses the strip's pixel-centre rectangle cannot contain any of them,
     // so the warp walks only the entries that overlap it (ballots over the batch, in order)
@@ -138,8 +175,8 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
         }
       }
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
   // entries visited: up to and including the terminating one, else the whole list
   nv = (inside && valid) ? (term_at >= 0 ? term_at + 1 : rg.y - rg.x) : 0;
   if (!inside) return;
@@ -184,13 +221,6 @@ struct LidarArgs {
   int sh_ncoef;
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
