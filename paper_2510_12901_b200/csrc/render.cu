@@ -60,8 +60,10 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
   constexpr int NT = 128;               // list entries staged per batch
   constexpr int PER = NT / NTH;         // entries per thread per batch
   // two batch buffers: batch k + 1's records are copied (cp.async) while batch k is walked
-  __shared__ float4 s_rec2[2][NT][5];
-  __shared__ uint32_t s_id2[2][PRAY ? NT : 1];  // particle ids of the batch (per-ray SH)
+  // (per-ray SH keeps one buffer: its extra registers leave no room for the second)
+  constexpr int NBUF = PRAY ? 1 : 2;
+  __shared__ float4 s_rec2[NBUF][NT][5];
+  __shared__ uint32_t s_id2[NBUF][PRAY ? NT : 1];  // particle ids of the batch (per-ray SH)
   const int tid = threadIdx.x;
   const int slot = (int)(blockIdx.x / SPLIT), band = (int)(blockIdx.x % SPLIT);
   const int tile = A.order ? __ldg(A.order + slot) : slot;
@@ -103,28 +105,36 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
       if (bi < nbatch && pos < rg.y) {
         const float4* src = A.record + (size_t)idv[q] * 5;
 #pragma unroll
-        for (int c = 0; c < 5; ++c) cp_async16(&s_rec2[bi & 1][e][c], src + c);
-        if (PRAY) s_id2[bi & 1][e] = idv[q];
+        for (int c = 0; c < 5; ++c) cp_async16(&s_rec2[bi % NBUF][e][c], src + c);
+        if (PRAY) s_id2[bi % NBUF][e] = idv[q];
       }
     }
     cp_async_commit();
   };
   uint32_t idn[PER];
-  load_ids(0, idn);
-  issue(0, idn);
-  load_ids(1, idn);
+  if (NBUF == 2) {
+    load_ids(0, idn);
+    issue(0, idn);
+    load_ids(1, idn);
+  }
   for (int bi = 0; bi < nbatch; ++bi) {
     // the count barrier also means every thread is done with batch bi - 1, whose buffer
     // batch bi + 1 reuses
     if (__syncthreads_count(!done) == 0) break;
-    issue(bi + 1, idn);
-    load_ids(bi + 2, idn);
-    cp_async_wait<1>();  // this thread's copies of batch bi have landed
+    if (NBUF == 2) {
+      issue(bi + 1, idn);
+      load_ids(bi + 2, idn);
+      cp_async_wait<1>();  // this thread's copies of batch bi have landed
+    } else {
+      load_ids(bi, idn);
+      issue(bi, idn);
+      cp_async_wait<0>();
+    }
     __syncthreads();
     const int b = rg.x + bi * NT;
     const int nb = min(NT, rg.y - b);
-    float4 (*s_rec)[5] = s_rec2[bi & 1];
-    const uint32_t* s_id = s_id2[bi & 1];
+    float4 (*s_rec)[5] = s_rec2[bi % NBUF];
+    const uint32_t* s_id = s_id2[bi % NBUF];
     // warp-level pre-cull: the warp's pixels form a strip of 32 / TP rows x TP columns; an
     // entry whose box misses the strip's pixel-centre rectangle cannot contain any of them,
     // so the warp walks only the entries that overlap it (ballots over the batch, in order)
