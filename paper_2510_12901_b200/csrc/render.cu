@@ -231,11 +231,6 @@ struct LidarArgs {
   int sh_ncoef;
 };
 
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void named_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 // 32x32 bit-matrix transpose across a warp: in: lane i holds row i; out: lane r holds
 // the word whose bit e is bit r of row e (5-stage shuffle butterfly).
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
@@ -249,75 +244,137 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
   return x;
 }
 
-template <int NP, int STAGES, int SLOTB>
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// mbarriers (CTA scope): the LiDAR render's chunk-slot ring between producers and consumer.
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(b))),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(b)))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
+  unsigned ok;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 10000000;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+  } while (!ok);
+}
+
+// LiDAR render: one CTA per work item (<= 32 rays of one tile) = P producer warps + one
+// consumer warp over the item's list in 32-entry chunks (producer p takes chunks p, p + P,
+// ...), handed over through a ring of NS chunk slots with one full / empty mbarrier pair
+// per slot:
+//  producer, per chunk (lane = entry):
+//   [A] the entry's box (16 B, cp.async two chunks ahead) against the item's columns and
+//       beams -> the exact A12 ray mask m; only entries with m != 0 fetch the rest of their
+//       record (64 B: mu, M, opacity, features) -- most listed entries contain none of the
+//       tile's rays;
+//   [B] (one chunk later, when that fetch has landed) the producer claims the chunk's slot
+//       (the consumer has released the chunk NS before), a 32x32 bit transpose gives every ray
+//       its member entries; the pairs are numbered ray-major (ray r's k-th member = pair
+//       off_r + k), listed by the ray lanes, and their responses (alpha, tau) computed with
+//       every lane busy; up to CAP per chunk (the rare rest: the consumer, from the
+//       record); the member entries' (opacity, features) go to the slot;
+//  consumer (lane = ray): the transmittance chain over the ray's members in list order,
+//       state in registers; it publishes the terminated rays (later box tests skip them)
+//       and ends the item once all have terminated.
+// The per-ray arithmetic (responses, chain order and operands) does not depend on the
+// tiling, on culling or on the chunking, so results are bit-identical across (N_phi, M)
+// and culling on/off.
+// pipeline shape: P producers, NS chunk slots (NS = 2P: a producer claims a slot one
+// iteration after the box test), CAP pairs per slot
+constexpr int kLidarProducers = 3;
+constexpr int kLidarSlots = 6;
+constexpr int kPairCap = 512;
+
+template <int CAP>
+struct LidarSlot {
+  float2 at[CAP];   // (alpha, tau) of the chunk's pairs, ray-major
+  float4 f[32];          // (opacity, features) of the chunk's member entries
+  uint32_t my[32];       // ray r: member entries of the chunk
+  int off[32];           // ray r: index of its first pair
+  uint32_t pid[32];      // particle ids of the member entries
+};
+template <int P, int NS, int CAP>
 struct LidarSmem {
-  float4 rec[STAGES][32 * NP][5];  // record ring (cp.async, STAGES - 1 rounds ahead)
-  // ray-major slots, rows padded so that the consumer's lane-per-ray accesses (lane r reads
-  // row r) hit distinct banks: without the pad every row starts in the same bank and each
-  // consumer load / store was a 32-way conflict
-  float2 at[SLOTB][32][32 * NP + 1];   // (alpha, tau) of member pairs, per slot buffer
-  uint8_t ent[SLOTB][32][32 * NP + 4]; // entry index within the round
-  float4 feat[SLOTB][32 * NP];     // (sigma, features) of the round's entries
-  uint32_t pid[SLOTB][32 * NP];    // particle ids of the round's entries (per-ray SH)
-  uint32_t memb[SLOTB][NP][32];    // [warp][ray] member entries of the warp's 32
-  int rowoff[NP][32];              // members of ray r in warps before w (current round)
-  uint16_t plist[NP][1024];        // the warp's member pairs (entry << 5 | ray)
-  float ray_oh[32][3], ray_ol[32][3], ray_dh[32][3], ray_dl[32][3];
+  float4 ray[32][3];        // o_hi, o_lo, d_hi, d_lo packed
+  float4 rest[P][2][32][4];  // producer p: mu, M, opacity, f of the member entries (two chunks)
+  float4 box[P][3][32];      // producer p: chunk boxes (prefetched two chunks ahead)
+  uint16_t pairs[P][CAP];  // producer p: the chunk's pairs (ray << 5 | entry), ray-major
+  LidarSlot<CAP> slot[NS];
   float col_phi[32], beam_el[32];
   int col_id[32], beam_id[32];
-  int stop_at[2];
-  uint32_t done_mask[2];  // rays terminated by the end of the round that released buffer b
+  unsigned long long full[NS], empty[NS];
+  uint32_t done_mask;
+  int stop;
 };
 
+__device__ __forceinline__ void unpack_ray(const float4* q, RayF& r) {
+  const float4 a = q[0], b = q[1], c = q[2];
+  r.o_hi[0] = a.x; r.o_hi[1] = a.y; r.o_hi[2] = a.z; r.o_lo[0] = a.w;
+  r.o_lo[1] = b.x; r.o_lo[2] = b.y; r.d_hi[0] = b.z; r.d_hi[1] = b.w;
+  r.d_hi[2] = c.x; r.d_lo[0] = c.y; r.d_lo[1] = c.z; r.d_lo[2] = c.w;
+}
+
+// producer-side wait for a slot release that also gives up once the consumer has stopped
+// (the consumer ends an item early, without draining, when all its rays have terminated);
+// a non-blocking test + nanosleep: a suspended try_wait (NANOSLEEP.SYNCS) wakes on every
+// barrier event of the SM, and the spinning producers took the consumer's issue slots
+__device__ __forceinline__ bool mbar_wait_or_stop(unsigned long long* b, unsigned parity, volatile int* stop) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
+  for (;;) {
+    unsigned ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+    if (ok) return true;
+    if (*stop) return false;
+    __nanosleep(256);  // a waiting producer is ahead of the consumer: poll slowly, leave it the issue slots
+  }
+}
+
+__device__ __forceinline__ float pair_alpha(const float4* rec, const RayF& rf, float alpha_max, float* tau) {
+  const float4 r0 = rec[0], r1 = rec[1], r2 = rec[2];
+  const float sig = rec[3].x;
+  const float mu[3] = {r0.x, r0.y, r0.z};
+  const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
+  float d2;
+  response(rf, mu, M, tau, &d2);
+  return fminf(alpha_max, sig * expf(-0.5f * d2));
+}
+
 #ifdef SIMULI_RENDER_PROFILE
-__device__ long long g_render_prof[1 << 20];  // per item: start ns, end ns, rounds run, list length | smid << 32
-__device__ long long g_render_trace[64][16];  // item traced: clock64 marks per round (see RMARK)
-__device__ int g_render_trace_item;
-#define RMARK(r, k)                                                                                  \
-  do {                                                                                               \
-    if (blockIdx.x == (unsigned)g_render_trace_item && (r) < 64 && (threadIdx.x & 31) == 0) g_render_trace[(r)][(k)] = clock64(); \
-  } while (0)
+// profiling builds only: per item start ns, end ns, chunks run, list length | smid << 32
+__device__ long long g_render_prof[1 << 20];
+// clock64 cycles summed over all items: [0] consumer waiting full, [1] consumer chain,
+// [2] producer waiting cp.async, [3] producer [A], [4] producer waiting empty, [5] producer [B]
+__device__ unsigned long long g_render_phase[8];
+#define PROF_T(v) long long v = clock64()
+#define PROF_ADD(i, t0) if (lane == 0) atomicAdd(&g_render_phase[i], (unsigned long long)(clock64() - (t0)))
 __device__ __forceinline__ long long gtime() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 #else
-#define RMARK(r, k) \
-  do {              \
-  } while (0)
+#define PROF_T(v)
+#define PROF_ADD(i, t0)
 #endif
 
-// LiDAR pipeline shape: 4 producer warps (128 list entries per round), 2 record stages, one
-// slot buffer (~69 KB shared memory, 3 CTAs per SM).  Render-only means over 10 poses of the
-// B-batch trajectory, L2 flushed (NP, stages, slot buffers):
-//   config B: (4,2,1) 260 us [252-275], (3,2,1) 254 [215-305], (2,2,2) 266 [211-324],
-//             (2,2,1) 296, (2,3,1) 295, (4,2,2) 298;
-//   config C: (4,2,1) 489 us, (3,2,1) 554, (2,2,2) 664.
-// Fewer, larger rounds keep the long near-field lists off the critical path.
-constexpr int kLidarNP = 4, kLidarStages = 2, kLidarSlotBuffers = 1;
-
-// SLOTB = 2: double-buffered slots, producers up to two rounds ahead of the consumer;
-// SLOTB = 1: one slot buffer (less shared memory, more CTAs per SM), producers wait for the
-// consumer's previous round after their box tests, before writing the slots.
-template <int NP, int STAGES, int SLOTB, bool PRAY>
-__global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarArgs A) {
-  constexpr int E = 32 * NP;
-  constexpr int NT = 32 * (NP + 1);
-  constexpr int BAR_PROD = 1, BAR_FULL = 2, BAR_EMPTY = 4, BAR_RAYS = 6;
+template <int P, int NS, int CAP, bool PRAY>
+__global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  LidarSmem<NP, STAGES, SLOTB>& S = *reinterpret_cast<LidarSmem<NP, STAGES, SLOTB>*>(smem_raw);
-  // per-ray SH (A30), degree 3: the round's member entries' 192-byte coefficient blocks,
-  // staged by the producers after the box tests (one slot buffer: written only once the
-  // consumer has released the previous round)
-  static_assert(!PRAY || SLOTB == 1, "per-ray SH staging assumes one slot buffer");
-  float4* s_sh = reinterpret_cast<float4*>(smem_raw + sizeof(LidarSmem<NP, STAGES, SLOTB>));
-  const bool sh_smem = PRAY && A.sh_ncoef == 16;
+  LidarSmem<P, NS, CAP>& S = *reinterpret_cast<LidarSmem<P, NS, CAP>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-#ifdef SIMULI_RENDER_PROFILE
-  const long long t_start = gtime();
-  int rounds_run = 0;
-#endif
   const int64_t item = blockIdx.x;
   const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
   const int tile = A.order ? __ldg(A.order + tslot) : tslot;
@@ -328,142 +385,182 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
   const int nb = b1 - b0, nc = c1 - c0;
   if (nb <= 0 || nc <= 0) return;  // CTA-uniform
   const int R = nb * nc;
-  if (tid < nc) {
-    const int j = __ldg(A.atc + c0 + tid);
-    S.col_id[tid] = j;
-    S.col_phi[tid] = __ldg(A.ray_az + j);
+#ifdef SIMULI_RENDER_PROFILE
+  const long long t_start = gtime();
+#endif
+  if (warp == P) {
+    const int j = lane < nc ? __ldg(A.atc + c0 + lane) : 0;
+    S.col_id[lane] = j;
+    S.col_phi[lane] = lane < nc ? __ldg(A.ray_az + j) : 0.f;
+    const int b = lane < nb ? __ldg(A.etb + b0 + lane) : 0;
+    S.beam_id[lane] = b;
+    S.beam_el[lane] = lane < nb ? __ldg(A.ray_el + (size_t)b * A.n_az) : 0.f;
   }
-  if (tid >= 32 && tid < 32 + nb) {
-    const int b = __ldg(A.etb + b0 + tid - 32);
-    S.beam_id[tid - 32] = b;
-    S.beam_el[tid - 32] = __ldg(A.ray_el + (size_t)b * A.n_az);
+  if (tid < NS) {
+    mbar_init(&S.full[tid], 1);
+    mbar_init(&S.empty[tid], 1);
   }
-  if (tid < 2) S.stop_at[tid] = 0;
+  if (tid == 0) {
+    S.stop = 0;
+    S.done_mask = R == 32 ? 0u : ~((1u << R) - 1u);  // lanes >= R: no ray
+  }
   __syncthreads();
   const int2 rg = __ldg(A.ranges + tile);
-  const int n_rounds = (rg.y - rg.x + E - 1) / E;
+  const int len = rg.y - rg.x;
+  const int nchunks = (len + 31) >> 5;
+  volatile uint32_t* vdone = &S.done_mask;
+  volatile int* vstop = &S.stop;
 
-  if (warp == NP) {
+  if (warp == P) {
     // ================= consumer: lane = ray
     int ray = 0;
-    double o[3] = {0, 0, 0}, dd[3] = {1, 0, 0};
     RayF rf;
-    if (lane < R) {
-      const int bi = lane / nc, ci = lane % nc;
-      const int j = S.col_id[ci];
-      ray = S.beam_id[bi] * A.n_az + j;
-      double Rm[9];
-      pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
-      double sa, ca, se, ce;
-      sincos((double)S.col_phi[ci], &sa, &ca);
-      sincos((double)S.beam_el[bi], &se, &ce);
-      const double u[3] = {ce * ca, ce * sa, se};
+    {
+      double o[3] = {0, 0, 0}, dd[3] = {0, 0, 0};
+      if (lane < R) {
+        // rays in double: origin t(s_j), direction R(s_j) u(phi_j, omega_b) (A5), split hi / lo
+        const int bi = lane / nc, ci = lane % nc;
+        const int j = S.col_id[ci];
+        ray = S.beam_id[bi] * A.n_az + j;
+        double Rm[9];
+        pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
+        double sa, ca, se, ce;
+        sincos((double)S.col_phi[ci], &sa, &ca);
+        sincos((double)S.beam_el[bi], &se, &ce);
+        const double u[3] = {ce * ca, ce * sa, se};
 #pragma unroll
-      for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
-    }
-    split_ray(o, dd, rf);
-    if (lane < R) {
+        for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
+        if (A.ray_od) {
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        S.ray_oh[lane][i] = rf.o_hi[i];
-        S.ray_ol[lane][i] = rf.o_lo[i];
-        S.ray_dh[lane][i] = rf.d_hi[i];
-        S.ray_dl[lane][i] = rf.d_lo[i];
+          for (int i = 0; i < 3; ++i) {
+            A.ray_od[6 * (size_t)ray + i] = o[i];
+            A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
+          }
+        }
       }
+      split_ray(o, dd, rf);
+      S.ray[lane][0] = make_float4(rf.o_hi[0], rf.o_hi[1], rf.o_hi[2], rf.o_lo[0]);
+      S.ray[lane][1] = make_float4(rf.o_lo[1], rf.o_lo[2], rf.d_hi[0], rf.d_hi[1]);
+      S.ray[lane][2] = make_float4(rf.d_hi[2], rf.d_lo[0], rf.d_lo[1], rf.d_lo[2]);
     }
-    __threadfence_block();
-    named_arrive(BAR_RAYS, NT);
-    float shb[16];
-    if (PRAY) sh_basis3((float)dd[0], (float)dd[1], (float)dd[2], shb);
-    float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
-    int ncontrib = 0, nv = 0, ni = 0;
+    float shb[PRAY ? 16 : 1];
+    if (PRAY) {
+      const float dx = rf.d_hi[0] + rf.d_lo[0], dy = rf.d_hi[1] + rf.d_lo[1], dz = rf.d_hi[2] + rf.d_lo[2];
+      sh_basis3(dx, dy, dz, shb);
+    }
+    named_sync(1, 32 * (P + 1));  // rays visible to the producers
+    float T = 1.f, z0 = 0.f, z1 = 0.f, z2 = 0.f, D = 0.f, Wt = 0.f;
+    int ncon = 0, ni = 0, nv = len;
     bool done = lane >= R;
-    for (int r = 0; r < n_rounds; ++r) {
-      const int b = r & 1, sb = SLOTB == 2 ? b : 0;
-      RMARK(r, 8);
-      named_sync(BAR_FULL + b, NT);
-      RMARK(r, 9);
-      const int start = rg.x + r * E;
-      if (!done) {
-        const int n_in = min(E, rg.y - start);
-        int cnt = 0;
-#pragma unroll
-        for (int w = 0; w < NP; ++w) cnt += __popc(S.memb[sb][w][lane]);
-        bool stopped = false;
-        // one pass over the ray's slots in list order; the slot loads run two members ahead
-        // and the feature load (indexed by the entry) one ahead, off the transmittance chain
-        int stop_k = -1, stop_e = 0;
-        if (cnt > 0) {
-          float2 a1 = S.at[sb][lane][0], a2 = make_float2(0.f, 0.f);
-          int e1 = S.ent[sb][lane][0], e2 = 0;
-          if (cnt > 1) {
-            a2 = S.at[sb][lane][1];
-            e2 = S.ent[sb][lane][1];
+    uint32_t dmask = *vdone;
+    int c = 0;
+    for (; c < nchunks; ++c) {
+      const int s = c % NS;
+      LidarSlot<CAP>& sl = S.slot[s];
+      PROF_T(t_w);
+      mbar_wait(&S.full[s], (unsigned)((c / NS) & 1));
+      PROF_ADD(0, t_w);
+      PROF_T(t_c);
+      uint32_t rem = done ? 0u : sl.my[lane];
+      int idx = sl.off[lane];
+      if (!PRAY) {
+        // branch-free over the ray's members in list order; the next member's (alpha, tau)
+        // and features are loaded one ahead, off the transmittance chain
+        int e = rem ? __ffs(rem) - 1 : 0;
+        float2 a = sl.at[min(idx, CAP - 1)];
+        float4 f = sl.f[e];
+        while (__any_sync(0xffffffffu, rem != 0u)) {
+          const bool has = rem != 0u;
+          const uint32_t rem2 = rem & (rem - 1u);
+          const int e2 = rem2 ? __ffs(rem2) - 1 : e;
+          const float2 a2 = sl.at[min(idx + 1, CAP - 1)];
+          const float4 f2 = sl.f[e2];
+          if (has && idx >= CAP) {  // beyond the slot's pair capacity (dense chunks, rare)
+            const float4* rec = A.record + (size_t)sl.pid[e] * 5;
+            const float4 q[4] = {__ldg(rec), __ldg(rec + 1), __ldg(rec + 2), __ldg(rec + 3)};
+            a.x = pair_alpha(q, rf, A.alpha_max, &a.y);
           }
-          float4 f1 = S.feat[sb][e1];
-          for (int k = 0; k < cnt; ++k) {
-            const float2 a = a1;
-            const float4 f = f1;
-            const int e = e1;
-            a1 = a2;
-            e1 = e2;
-            if (k + 2 < cnt) {
-              a2 = S.at[sb][lane][k + 2];
-              e2 = S.ent[sb][lane][k + 2];
-            }
-            if (k + 1 < cnt) f1 = S.feat[sb][e1];
-            if (a.y < A.near_tau || a.x < A.alpha_min) continue;  // skipped member
-            const float Tn = T * (1.f - a.x);
-            if (Tn < A.T_min) {  // terminated: this member is not composited (A14)
-              stop_k = k;
-              stop_e = e;
-              break;
-            }
-            const float w = a.x * T;
-            float fv[3] = {f.y, f.z, f.w};
-            if (PRAY) {
-              if (sh_smem) sh_dot16(s_sh + e * 12, shb, fv);
-              else sh_dot(A.sh + (size_t)S.pid[sb][e] * A.sh_ncoef * 3, A.sh_ncoef, shb, fv);
-            }
-            acc0 = fmaf(w, fv[0], acc0);
-            acc1 = fmaf(w, fv[1], acc1);
-            acc2 = fmaf(w, fv[2], acc2);
-            D = fmaf(w, a.y, D);
-            W += w;
-            ++ncontrib;
-            T = Tn;
+          const bool valid = has && !(a.y < A.near_tau || a.x < A.alpha_min);  // A13, A15
+          const float Tn = T * (1.f - a.x);
+          const bool term = valid && Tn < A.T_min;  // terminated: not composited (A14)
+          const bool comp = valid && !term;
+          const float w = a.x * T;
+          z0 = comp ? fmaf(w, f.y, z0) : z0;
+          z1 = comp ? fmaf(w, f.z, z1) : z1;
+          z2 = comp ? fmaf(w, f.w, z2) : z2;
+          D = comp ? fmaf(w, a.y, D) : D;
+          Wt = comp ? Wt + w : Wt;
+          T = comp ? Tn : T;
+          ncon += comp ? 1 : 0;
+          ni += has ? 1 : 0;
+          if (term) {
+            done = true;
+            nv = 32 * c + e + 1;
           }
+          rem = term ? 0u : rem2;
+          e = e2;
+          a = a2;
+          f = f2;
+          ++idx;
         }
-        RMARK(r, 10);
-        if (stop_k >= 0) {
-          stopped = true;
-          nv += stop_e + 1;
-          ni += stop_k + 1;
-        }
-        if (stopped) done = true;
-        else {
-          nv += n_in;
-          ni += cnt;
+      } else {
+        while (__any_sync(0xffffffffu, rem != 0u)) {
+          if (rem != 0u) {
+            const int e = __ffs(rem) - 1;
+            rem &= rem - 1u;
+            float2 a;
+            if (idx < CAP) {
+              a = sl.at[idx];
+            } else {  // beyond the slot's pair capacity (dense chunks, rare): from the record
+              const float4* rec = A.record + (size_t)sl.pid[e] * 5;
+              const float4 q[4] = {__ldg(rec), __ldg(rec + 1), __ldg(rec + 2), __ldg(rec + 3)};
+              a.x = pair_alpha(q, rf, A.alpha_max, &a.y);
+            }
+            ++idx;
+            ++ni;
+            if (!(a.y < A.near_tau || a.x < A.alpha_min)) {  // skipped member (A13, A15)
+              const float Tn = T * (1.f - a.x);
+              if (Tn < A.T_min) {  // terminated: this member is not composited (A14)
+                done = true;
+                rem = 0u;
+                nv = 32 * c + e + 1;
+              } else {
+                const float w = a.x * T;
+                float fv[3];
+                if (PRAY) {
+                  sh_dot(A.sh + (size_t)sl.pid[e] * A.sh_ncoef * 3, A.sh_ncoef, shb, fv);
+                } else {
+                  const float4 f = sl.f[e];
+                  fv[0] = f.y; fv[1] = f.z; fv[2] = f.w;
+                }
+                z0 = fmaf(w, fv[0], z0);
+                z1 = fmaf(w, fv[1], z1);
+                z2 = fmaf(w, fv[2], z2);
+                D = fmaf(w, a.y, D);
+                Wt += w;
+                ++ncon;
+                T = Tn;
+              }
+            }
+          }
         }
       }
-      const uint32_t dmask = __ballot_sync(0xffffffffu, done);
-      const bool all = dmask == 0xffffffffu;
-      RMARK(r, 11);
-#ifdef SIMULI_RENDER_PROFILE
-      rounds_run = r + 1;
-#endif
-      if (r + SLOTB < n_rounds) {
+      PROF_ADD(1, t_c);
+      const uint32_t dm = __ballot_sync(0xffffffffu, done);
+      const bool all = dm == 0xffffffffu;
+      if (dm != dmask) {
+        dmask = dm;
         if (lane == 0) {
-          S.stop_at[b] = all ? 1 : 0;
-          S.done_mask[b] = dmask;
+          *vdone = dm;
+          if (all) *vstop = 1;
         }
+      }
+      __syncwarp();
+      if (lane == 0) {
         __threadfence_block();
-        named_arrive(BAR_EMPTY + b, NT);
+        mbar_arrive(&S.empty[s]);
       }
-      if (all) {
-        if (SLOTB == 2 && r + 1 < n_rounds) named_sync(BAR_FULL + (b ^ 1), NT);  // drain the round in flight
-        break;
-      }
+      if (all) break;
     }
 #ifdef SIMULI_RENDER_PROFILE
     if (lane == 0 && item < (1 << 18)) {
@@ -471,57 +568,45 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       g_render_prof[4 * item] = t_start;
       g_render_prof[4 * item + 1] = gtime();
-      g_render_prof[4 * item + 2] = rounds_run;
-      g_render_prof[4 * item + 3] = (long long)(rg.y - rg.x) | ((long long)smid << 32);
+      g_render_prof[4 * item + 2] = c < nchunks ? c + 1 : nchunks;
+      g_render_prof[4 * item + 3] = (long long)len | ((long long)smid << 32);
     }
 #endif
     if (lane >= R) return;
     if (A.zeta) {
-      A.zeta[3 * (size_t)ray] = acc0;
-      A.zeta[3 * (size_t)ray + 1] = acc1;
-      A.zeta[3 * (size_t)ray + 2] = acc2;
+      A.zeta[3 * (size_t)ray] = z0;
+      A.zeta[3 * (size_t)ray + 1] = z1;
+      A.zeta[3 * (size_t)ray + 2] = z2;
     }
-    if (A.opacity) A.opacity[ray] = W;
+    if (A.opacity) A.opacity[ray] = Wt;
     if (A.depth_accum) A.depth_accum[ray] = D;
-    if (A.depth) A.depth[ray] = W > 0.f ? D / W : 0.f;
-    if (A.intensity) A.intensity[ray] = acc0;
-    if (A.raydrop) A.raydrop[ray] = raydrop_prob(acc1, acc2);
+    if (A.depth) A.depth[ray] = Wt > 0.f ? D / Wt : 0.f;
+    if (A.intensity) A.intensity[ray] = z0;
+    if (A.raydrop) A.raydrop[ray] = raydrop_prob(z1, z2);
     if (A.final_T) A.final_T[ray] = T;
-    if (A.n_contrib) A.n_contrib[ray] = ncontrib;
+    if (A.n_contrib) A.n_contrib[ray] = ncon;
     if (A.n_visited) A.n_visited[ray] = nv;
     if (A.n_inbox) A.n_inbox[ray] = ni;
-    if (A.ray_od) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        A.ray_od[6 * (size_t)ray + i] = o[i];
-        A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
-      }
-    }
     return;
   }
 
-  // ================= producers: thread = list entry of the round
-  constexpr int D = STAGES - 1;  // record prefetch distance (rounds)
-  auto issue = [&](int round, uint32_t id) {
-    if (round < n_rounds && rg.x + round * E + tid < rg.y) {
-      const float4* src = A.record + (size_t)id * 5;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) cp_async16(&S.rec[round % STAGES][tid][c], src + c);
-    }
-    cp_async_commit();  // one group per round, empty or not (keeps the wait_group count exact)
+  // ================= producers: lane = entry of the chunk
+  float4(&pbox)[3][32] = S.box[warp];
+  float4(&prest)[2][32][4] = S.rest[warp];
+  uint16_t* ppair = S.pairs[warp];
+  auto load_id = [&](int c) -> uint32_t {
+    const int p = 32 * c + lane;
+    return (c < nchunks && p < len) ? __ldg(A.ids + rg.x + p) : 0u;
   };
-  auto load_id = [&](int round) -> uint32_t {
-    const int e = rg.x + round * E + tid;
-    return (round < n_rounds && e < rg.y) ? __ldg(A.ids + e) : 0u;
+  auto issue_box = [&](int c, uint32_t id, int b) {
+    if (c < nchunks && 32 * c + lane < len) cp_async16(&pbox[b][lane], A.record + (size_t)id * 5 + 4);
+    cp_async_commit();  // one group per call (empty or not): keeps the wait_group count exact
   };
-  {
-    uint32_t ids[D];
-#pragma unroll
-    for (int q = 0; q < D; ++q) ids[q] = load_id(q);
-#pragma unroll
-    for (int q = 0; q < D; ++q) issue(q, ids[q]);
-  }
-  uint32_t id_pf = load_id(D);
+  uint32_t id_c = load_id(warp);      // chunk c_k (this lane's entry)
+  uint32_t id_n = load_id(warp + P);  // chunk c_{k+1}
+  issue_box(warp, id_c, 0);
+  issue_box(warp + P, id_n, 1);
+  uint32_t id_nn = load_id(warp + 2 * P);  // chunk c_{k+2}
   // the item's first 8 column azimuths / 4 beam elevations in registers (the usual item;
   // unused slots are masked by nc / nb below)
   float cphi[8], bel[4];
@@ -529,141 +614,125 @@ __global__ void __launch_bounds__(32 * (NP + 1), 1) k_render_lidar(const LidarAr
   for (int ci = 0; ci < 8; ++ci) cphi[ci] = S.col_phi[ci];
 #pragma unroll
   for (int bi = 0; bi < 4; ++bi) bel[bi] = S.beam_el[bi];
-  named_sync(BAR_RAYS, NT);
-  uint32_t alive = 0xffffffffu;  // rays the consumer has not terminated (2 rounds behind)
-  for (int r = 0; r < n_rounds; ++r) {
-    const int b = r & 1, st = r % STAGES, sb = SLOTB == 2 ? b : 0;
-    if (warp == 0) RMARK(r, 0);
-    if (SLOTB == 2 && r >= 2) {
-      named_sync(BAR_EMPTY + b, NT);
-      if (S.stop_at[b]) break;
-      alive = ~S.done_mask[b];
+  auto box_mask = [&](const float4 bx) -> uint32_t {
+    uint32_t colbits = 0;
+    if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
+      colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
+    } else {
+      const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
+      const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
+#pragma unroll
+      for (int ci = 0; ci < 8; ++ci) {
+        const float p = cphi[ci];
+        const bool in = ci < nc && ((bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2);
+        colbits |= (uint32_t)in << ci;
+      }
+      for (int ci = 8; ci < nc; ++ci) {
+        const float p = S.col_phi[ci];
+        const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
+        colbits |= (uint32_t)in << ci;
+      }
     }
-    const int start = rg.x + r * E;
-    cp_async_wait<D - 1>();   // this thread's copies of round r have landed
-    if (warp == 0) RMARK(r, 1);
-    named_sync(BAR_PROD, E);  // everyone's: round r's records visible; stage of round r - 1 and rowoff free
-    if (warp == 0) RMARK(r, 2);
-    issue(r + D, id_pf);
-    id_pf = load_id(r + D + 1);
-    const bool valid = start + tid < rg.y;
     uint32_t m = 0;
-    if (valid) {
-      const float4 bx = S.rec[st][tid][4];
-      uint32_t colbits = 0;
-      if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
-        colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
-      } else {
-        const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
-        const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
-        // the usual item has <= 8 columns and <= 4 beams: fixed-trip unrolled, independent
-        // compares (general shapes fall through to the loops)
+    if (colbits) {
+      uint32_t beambits = 0;
 #pragma unroll
-        for (int ci = 0; ci < 8; ++ci) {
-          const float p = cphi[ci];
-          const bool in = ci < nc && ((bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2);
-          colbits |= (uint32_t)in << ci;
-        }
-        for (int ci = 8; ci < nc; ++ci) {
-          const float p = S.col_phi[ci];
-          const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
-          colbits |= (uint32_t)in << ci;
-        }
+      for (int bi = 0; bi < 4; ++bi) {
+        const float w = bel[bi];
+        beambits |= (uint32_t)(bi < nb && bx.z <= w && w <= bx.w) << bi;
       }
-      if (colbits) {
-        uint32_t beambits = 0;
+      for (int bi = 4; bi < nb; ++bi) {
+        const float w = S.beam_el[bi];
+        beambits |= (uint32_t)(bx.z <= w && w <= bx.w) << bi;
+      }
+      for (uint32_t bb = beambits; bb; bb &= bb - 1u) m |= colbits << ((__ffs(bb) - 1) * nc);
+    }
+    return m;
+  };
+  named_sync(1, 32 * (P + 1));  // rays (consumer) visible
+
+  uint32_t m_prev = 0, id_p = 0;  // ray mask and particle id of chunk c_{k-1} (this lane's entry)
+  for (int k = 0;; ++k) {
+    const int cc = warp + k * P;  // chunk c_k: [A] this iteration
+    const int cp = cc - P;        // chunk c_{k-1}: [B] this iteration
+    if (*vstop) break;
+    const bool has_cur = cc < nchunks;
+    if (!has_cur && k == 0) break;
+    PROF_T(t_cp);
+    cp_async_wait<1>();  // box(c_k) and rest(c_{k-1}) (this lane's copies; box(c_{k+1}) may fly)
+    __syncwarp();
+    PROF_ADD(2, t_cp);
+    PROF_T(t_a);
+    uint32_t m_cur = 0;
+    const uint32_t id_k = id_c;
+    if (has_cur) {
+      // ---- [A] chunk c_k: box test, fetch the member entries' records (one chunk ahead)
+      if (32 * cc + lane < len) m_cur = box_mask(pbox[k % 3][lane]) & ~*vdone;
+      if (m_cur) {
+        const float4* src = A.record + (size_t)id_c * 5;
 #pragma unroll
-        for (int bi = 0; bi < 4; ++bi) {
-          const float w = bel[bi];
-          beambits |= (uint32_t)(bi < nb && bx.z <= w && w <= bx.w) << bi;
-        }
-        for (int bi = 4; bi < nb; ++bi) {
-          const float w = S.beam_el[bi];
-          beambits |= (uint32_t)(bx.z <= w && w <= bx.w) << bi;
-        }
-        for (uint32_t bb = beambits; bb; bb &= bb - 1u) m |= colbits << ((__ffs(bb) - 1) * nc);
-      }
-    }
-    if (warp == 0) RMARK(r, 3);
-    if (SLOTB == 1 && r >= 1) {  // the consumer is done with round r - 1's slots
-      named_sync(BAR_EMPTY + (b ^ 1), NT);
-      if (S.stop_at[b ^ 1]) break;
-      alive = ~S.done_mask[b ^ 1];
-    }
-    if (warp == 0) RMARK(r, 4);
-    uint32_t pid = 0;
-    if (valid) {
-      S.feat[sb][tid] = S.rec[st][tid][3];
-      if (PRAY) {
-        pid = __ldg(A.ids + start + tid);
-        S.pid[sb][tid] = pid;
-      }
-    }
-    m &= alive;  // no member pairs for terminated rays
-    if (sh_smem) {  // asynchronous: lands while the round's responses are computed
-      if (m != 0u) {
-        const float4* src = reinterpret_cast<const float4*>(A.sh) + (size_t)pid * 12;
-#pragma unroll
-        for (int c = 0; c < 12; ++c) cp_async16(s_sh + tid * 12 + c, src + c);
+        for (int q = 0; q < 4; ++q) cp_async16(&prest[k & 1][lane][q], src + q);
       }
       cp_async_commit();
+      issue_box(cc + 2 * P, id_nn, (k + 2) % 3);
+      id_c = id_n;
+      id_n = id_nn;
+      id_nn = load_id(cc + 3 * P);
     }
-    const uint32_t my = warp_transpose32(m, lane);  // lane r: entries of this warp holding ray r
-    S.memb[sb][warp][lane] = my;
-    const int k = __popc(m);
-    int inc = k;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= off) inc += t;
-    }
-    const int K = __shfl_sync(0xffffffffu, inc, 31);
-    const int ex = inc - k;
-    {
-      int pos = ex;
-      uint32_t mm = m;
-      while (mm) {
-        const int rr = __ffs(mm) - 1;
-        mm &= mm - 1u;
-        S.plist[warp][pos++] = (uint16_t)((lane << 5) | rr);
+    PROF_ADD(3, t_a);
+    if (k >= 1) {
+      // ---- [B] chunk c_{k-1}: claim its slot, pairs (ray-major) and their responses
+      const int s = cp % NS;
+      PROF_T(t_e);
+      if (cp >= NS) {
+        if (!mbar_wait_or_stop(&S.empty[s], (unsigned)((cp / NS - 1) & 1), vstop)) break;
+        if (*vstop) break;
       }
-    }
-    if (warp == 0) RMARK(r, 5);
-    named_sync(BAR_PROD, E);  // every producer warp's member words are in
-    if (warp == 0) RMARK(r, 6);
-    {
-      int off = 0;
+      PROF_ADD(4, t_e);
+      PROF_T(t_b);
+      LidarSlot<CAP>& sl = S.slot[s];
+      const float4(&rest)[32][4] = prest[(k - 1) & 1];
+      const uint32_t my = warp_transpose32(m_prev, lane);  // lane r: the chunk's entries holding ray r
+      const int cnt = __popc(my);
+      int inc = cnt;
 #pragma unroll
-      for (int w = 0; w < NP; ++w)
-        if (w < warp) off += __popc(S.memb[sb][w][lane]);
-      S.rowoff[warp][lane] = off;
-    }
-    __syncwarp();
-    for (int idx = lane; idx < K; idx += 32) {
-      const int v = S.plist[warp][idx];
-      const int rr = v & 31, el = v >> 5, e = warp * 32 + el;
-      const int slot = S.rowoff[warp][rr] + __popc(S.memb[sb][warp][rr] & ((1u << el) - 1u));
-      const float4 r0 = S.rec[st][e][0], r1 = S.rec[st][e][1], r2 = S.rec[st][e][2], r3 = S.rec[st][e][3];
-      const float mu[3] = {r0.x, r0.y, r0.z};
-      const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
-      RayF rf;
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        rf.o_hi[i] = S.ray_oh[rr][i];
-        rf.o_lo[i] = S.ray_ol[rr][i];
-        rf.d_hi[i] = S.ray_dh[rr][i];
-        rf.d_lo[i] = S.ray_dl[rr][i];
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += t;
       }
-      float tau, d2;
-      response(rf, mu, M, &tau, &d2);
-      S.at[sb][rr][slot] = make_float2(fminf(A.alpha_max, r3.x * expf(-0.5f * d2)), tau);
-      S.ent[sb][rr][slot] = (uint8_t)e;
+      const int off_r = inc - cnt;
+      const int K = min(__shfl_sync(0xffffffffu, inc, 31), CAP);
+      sl.my[lane] = my;
+      sl.off[lane] = off_r;
+      if (m_prev) {
+        sl.f[lane] = rest[lane][3];
+        sl.pid[lane] = id_p;
+      }
+      // the pair list, ray-major: ray r's k-th member e -> pairs[off_r + k] = r << 5 | e
+      {
+        int i = off_r;
+        for (uint32_t t = my; t && i < CAP; t &= t - 1u, ++i) ppair[i] = (uint16_t)((lane << 5) | (__ffs(t) - 1));
+      }
+      __syncwarp();
+      for (int i = lane; i < K; i += 32) {
+        const int v = ppair[i];
+        const int r = v >> 5, e = v & 31;
+        RayF rf;
+        unpack_ray(S.ray[r], rf);
+        float tau;
+        const float a = pair_alpha(rest[e], rf, A.alpha_max, &tau);
+        sl.at[i] = make_float2(a, tau);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        mbar_arrive(&S.full[s]);
+      }
+      PROF_ADD(5, t_b);
     }
-    if (sh_smem) cp_async_wait<0>();  // the staged SH (and the record prefetch issued before it)
-    __syncwarp();
-    __threadfence_block();
-    if (warp == 0) RMARK(r, 7);
-    named_arrive(BAR_FULL + b, NT);
+    m_prev = m_cur;
+    id_p = id_k;
+    if (!has_cur) break;
   }
   cp_async_wait<0>();
 }
@@ -719,38 +788,33 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   }
   if (A.n_items == 0) return SIMULI_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  auto launch = [&](auto np_tag, auto stages_tag, auto slot_tag) {
-    constexpr int NP = decltype(np_tag)::value, STG = decltype(stages_tag)::value, SB = decltype(slot_tag)::value;
-    constexpr size_t smem = sizeof(LidarSmem<NP, STG, SB>);
-    cudaFuncSetAttribute(k_render_lidar<NP, STG, SB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_render_lidar<NP, STG, SB, false><<<(unsigned)A.n_items, 32 * (NP + 1), smem, st>>>(A);
-  };
-  if (A.sh) {  // per-ray SH (A30): the default pipeline shape only
-    const size_t smem = sizeof(LidarSmem<kLidarNP, kLidarStages, kLidarSlotBuffers>) +
-                        (A.sh_ncoef == 16 ? sizeof(float4) * 12 * 32 * kLidarNP : 0);
-    auto kern = k_render_lidar<kLidarNP, kLidarStages, kLidarSlotBuffers, true>;
+  auto launch = [&](auto p_tag, auto ns_tag, auto cap_tag) {
+    constexpr int P_ = decltype(p_tag)::value, NS_ = decltype(ns_tag)::value, CAP_ = decltype(cap_tag)::value;
+    constexpr size_t smem = sizeof(LidarSmem<P_, NS_, CAP_>);
+    auto kern = A.sh ? k_render_lidar<P_, NS_, CAP_, true> : k_render_lidar<P_, NS_, CAP_, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)A.n_items, 32 * (kLidarNP + 1), smem, st>>>(A);
-    return launch_check("simuli_render_lidar");
-  }
+    kern<<<(unsigned)A.n_items, 32 * (P_ + 1), smem, st>>>(A);
+  };
   using std::integral_constant;
   static const int variant = [] {
-    const char* v = getenv("SIMULI_LIDAR_VARIANT");  // tuning only
+    const char* v = getenv("SIMULI_LIDAR_VARIANT");  // tuning only: P * 10000 + NS * 1000 + CAP
     return v ? atoi(v) : 0;
   }();
-  using I1 = integral_constant<int, 1>;
   using I2 = integral_constant<int, 2>;
   using I3 = integral_constant<int, 3>;
   using I4 = integral_constant<int, 4>;
-  switch (variant) {  // NP * 100 + STAGES * 10 + SLOTB
-    case 221: launch(I2{}, I2{}, I1{}); break;
-    case 231: launch(I2{}, I3{}, I1{}); break;
-    case 421: launch(I4{}, I2{}, I1{}); break;
-    case 321: launch(I3{}, I2{}, I1{}); break;
-    case 422: launch(I4{}, I2{}, I2{}); break;
-    case 222: launch(I2{}, I2{}, I2{}); break;
-    default: launch(integral_constant<int, kLidarNP>{}, integral_constant<int, kLidarStages>{},
-                    integral_constant<int, kLidarSlotBuffers>{}); break;
+  using I6 = integral_constant<int, 6>;
+  using I8 = integral_constant<int, 8>;
+  switch (variant) {
+    case 24512: launch(I2{}, I4{}, integral_constant<int, 512>{}); break;
+    case 24384: launch(I2{}, I4{}, integral_constant<int, 384>{}); break;
+    case 48256: launch(I4{}, I8{}, integral_constant<int, 256>{}); break;
+    case 48384: launch(I4{}, I8{}, integral_constant<int, 384>{}); break;
+    case 36384: launch(I3{}, I6{}, integral_constant<int, 384>{}); break;
+    default:
+      launch(integral_constant<int, kLidarProducers>{}, integral_constant<int, kLidarSlots>{},
+             integral_constant<int, kPairCap>{});
+      break;
   }
   return launch_check("simuli_render_lidar");
 }
@@ -810,9 +874,8 @@ extern "C" int32_t simuli_render_camera(const simuli_projected* proj, const uint
 }
 
 #ifdef SIMULI_RENDER_PROFILE
-extern "C" int32_t simuli_debug_render_trace(long long* host, int item) {
-  cudaMemcpyToSymbol(simuli::g_render_trace_item, &item, sizeof(int));
-  return cudaMemcpyFromSymbol(host, simuli::g_render_trace, sizeof(long long) * 64 * 16) == cudaSuccess ? 0 : 3;
+extern "C" int32_t simuli_debug_render_phase(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, simuli::g_render_phase, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 3;
 }
 extern "C" int32_t simuli_debug_render_prof(long long* host, int64_t n) {
   return cudaMemcpyFromSymbol(host, simuli::g_render_prof, sizeof(long long) * 4 * n) == cudaSuccess ? 0 : 3;

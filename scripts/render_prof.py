@@ -1,4 +1,4 @@
-"""Per-item timeline of the LiDAR render kernel (profiling build: SIMULI_EXTRA_NVCC=-DSIMULI_RENDER_PROFILE)."""
+"""Per-item timeline of the LiDAR render kernel (chunks = 32-entry chunks run) (profiling build: SIMULI_EXTRA_NVCC=-DSIMULI_RENDER_PROFILE)."""
 import os, sys, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -21,40 +21,27 @@ p = buf.reshape(n, 4)
 used = p[:, 1] > 0
 p = p[used]
 t0 = p[:, 0].min()
-st, en, rounds = (p[:, 0] - t0) / 1e3, (p[:, 1] - t0) / 1e3, p[:, 2]
+st, en, chunks = (p[:, 0] - t0) / 1e3, (p[:, 1] - t0) / 1e3, p[:, 2]
 ln, sm = p[:, 3] & 0xffffffff, p[:, 3] >> 32
 dur = en - st
 print(f"items {used.sum()}, kernel span {en.max():.1f} us, last start {st.max():.1f} us")
 print(f"item duration: mean {dur.mean():.2f} p50 {np.median(dur):.2f} p99 {np.percentile(dur, 99):.2f} max {dur.max():.2f} us")
-print(f"rounds: total {rounds.sum()} mean {rounds.mean():.2f} max {rounds.max()}")
-ok = rounds > 0
-print(f"us per round (items with rounds): median {np.median(dur[ok] / rounds[ok]):.3f}, "
-      f"weighted {dur[ok].sum() / rounds[ok].sum():.3f}")
+print(f"chunks: total {chunks.sum()} mean {chunks.mean():.2f} max {chunks.max()}")
+ok = chunks > 0
+print(f"us per chunk (items with chunks): median {np.median(dur[ok] / chunks[ok]):.3f}, "
+      f"weighted {dur[ok].sum() / chunks[ok].sum():.3f}")
 for q in (0.5, 0.9, 0.99, 1.0):
     print(f"  items ending by {q:.2f} of span: {(en <= q * en.max()).mean():.3f}")
 top = np.argsort(-dur)[:8]
-print("longest items: dur", dur[top].round(1), "rounds", rounds[top], "len", ln[top], "start", st[top].round(1))
+print("longest items: dur", dur[top].round(1), "chunks", chunks[top], "len", ln[top], "start", st[top].round(1))
 busy = np.zeros(200)
 for s_, e_, m in zip(st, en, sm):
     busy[m] += e_ - s_
 print(f"per-SM busy (sum of item durations): mean {busy[:148].mean():.1f} max {busy[:148].max():.1f} us")
 
-# per-round phase trace of one long item (clock64 marks, RMARK in render.cu)
-item = int(np.argmax(dur))  # the longest item of the timeline above
-tr = np.zeros(64 * 16, np.int64)
-L.simuli_debug_render_trace(tr.ctypes.data_as(C.c_void_p), C.c_int(int(item)))  # select the item
-flush.zero_(); r.render(); torch.cuda.synchronize()
-L.simuli_debug_render_trace(tr.ctypes.data_as(C.c_void_p), C.c_int(int(item)))
-tr = tr.reshape(64, 16).astype(np.float64)
-names = ["p:start", "p:cp.wait", "p:BAR_PROD1", "p:boxtest", "p:EMPTY", "p:plist", "p:BAR_PROD2", "p:resp",
-         "c:start", "c:FULL", "c:phase1", "c:end"]
-print(f"item {item}: per-round phase durations (cycles), rounds 2..12:")
-for rr in range(2, 13):
-    row = tr[rr]
-    if row[0] == 0:
-        break
-    p = [row[k + 1] - row[k] for k in range(0, 7)]
-    c = [row[k + 1] - row[k] for k in range(8, 11)]
-    print(f"  r{rr:2d} prod " + " ".join(f"{names[k+1]}={v:6.0f}" for k, v in enumerate(p)) +
-          " | cons " + " ".join(f"{names[8 + k + 1]}={v:6.0f}" for k, v in enumerate(c)) +
-          f" | round {tr[rr + 1][0] - row[0] if tr[rr + 1][0] else 0:6.0f}")
+ph = np.zeros(8, np.uint64)
+if hasattr(L, "simuli_debug_render_phase"):
+    L.simuli_debug_render_phase(ph.ctypes.data_as(C.c_void_p))
+    names = ["cons wait full", "cons chain", "prod wait cp.async", "prod [A]", "prod wait empty", "prod [B]"]
+    runs = 4  # renders since the kernel start (scan + 3 timed)
+    print("phase cycles per render (summed over warps):", ", ".join(f"{n} {ph[i] / runs / 1e6:.1f} M" for i, n in enumerate(names)))
