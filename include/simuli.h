@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 9
+#define SIMULI_ABI_VERSION 10
 
 enum {
   SIMULI_OK = 0,
@@ -128,6 +128,8 @@ typedef struct {
   int32_t* elev_tile_beams;        /* [n_beams]                                             */
   int32_t* az_tile_col_offsets;    /* [n_theta+1] CSR azimuth tile -> columns               */
   int32_t* az_tile_cols;           /* [n_azimuth]                                           */
+  float* beam_el_sorted;           /* [n_beams] beam elevations, ascending (exact culling)  */
+  float* col_az_sorted;            /* [n_azimuth] column azimuths phi_j, ascending (ditto)  */
 } simuli_tiling;
 
 /* Proc. ElevationTiling with the corrections of A8: histogram of per-ray
@@ -152,6 +154,7 @@ typedef struct {
   const float *elev_bounds, *cull_row_scale, *ray_az, *ray_el, *ray_s;
   const int32_t *ray_tile, *tile_ray_offsets, *tile_rays, *sat;
   const int32_t *elev_tile_beam_offsets, *elev_tile_beams, *az_tile_col_offsets, *az_tile_cols;
+  const float *beam_el_sorted, *col_az_sorted;
 } simuli_tiling_dev;
 
 /* Gaussian particle set G_l or G_c: device pointers.
@@ -204,7 +207,10 @@ typedef struct {
   int32_t rs_iterations;            /* K firing-time fixed-point iterations (A3), >= 0     */
   float ut_alpha, ut_beta, ut_kappa;/* scaled-UT parameters (A1): default 1, 2, 0          */
   float extent_sigma;               /* box half-width in std-devs (A11): default 3         */
-  int32_t enable_culling;           /* ray-based culling, LiDAR only: default 1    */
+  int32_t enable_culling;           /* ray-based culling, LiDAR only (see below): 0 off,
+                                       1 the paper's dense-grid SAT test (Proc.
+                                       RayOccupancyCount / ProjectParticles), 2 exact
+                                       ray containment per render tile (reading A32)      */
   int32_t write_all_records;        /* 1: write the record of every particle (invalid ->
                                        NaN box); 0: only particles with tile count > 0     */
 } simuli_project_params;
@@ -232,9 +238,17 @@ typedef struct {
  * A2) pushed through the time-dependent sensor model: each sigma point is projected with
  * the pose at its own firing time (K fixed-point iterations from s = 0, A3), LiDAR by
  * Eq. 3, cameras by the lens model; UT mean / covariance -> axis-aligned box of
- * extent_sigma std-devs (A11), rounded outward.  LiDAR: ray-based culling by the SAT
- * rectangle count (Proc. RayOccupancyCount / ProjectParticles) and the
- * coarse tile count; camera: tiles of tile_px pixels, no culling.
+ * extent_sigma std-devs (A11), rounded outward.  LiDAR, enable_culling = 1: ray-based
+ * culling by the SAT rectangle count over the dense 1600 x 8-per-tile ray mask (Proc.
+ * RayOccupancyCount / ProjectParticles) and the coarse tile rectangle of the
+ * box; enable_culling = 2 (reading A32): the same idea at full resolution -- a spinning
+ * LiDAR's rays are the product beams x columns (one firing time per column, A5), so the
+ * render tiles containing a ray inside the box are exactly the elevation tiles of the
+ * beams with lo_b <= omega_b <= hi_b times the azimuth tiles of the columns with phi_j in
+ * the (seam-shifted, A12) azimuth interval: a rectangle, found by binary search in
+ * beam_el_sorted / col_az_sorted; a particle with no such beam or column is culled.  The
+ * lists then hold only (tile, particle) pairs with a ray inside the box; render outputs are
+ * identical in all three modes (A12).  Camera: tiles of tile_px pixels, no culling.
  * Errors: INVALID_ARGUMENT (NULL / size mismatch / kind; actor_id set with n_actors < 1 or
  * actor_pose NULL), UNSUPPORTED (sh_degree > 3),
  * CUDA (launch failure).  Device pointers in `out` must hold n entries. */

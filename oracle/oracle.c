@@ -686,6 +686,8 @@ int or_build_tiling(const or_lidar* L, int32_t n_phi, int32_t M, int32_t r, int3
    * s_j = (j + 0.5)/A (A5); omega_b as given. */
   int32_t R = B * A;
   out->n_rays = R;
+  out->n_beams = B;
+  out->n_az = A;
   out->ray_az = (float*)malloc(sizeof(float) * R);
   out->ray_el = (float*)malloc(sizeof(float) * R);
   out->ray_s = (float*)malloc(sizeof(float) * R);
@@ -950,6 +952,8 @@ static void az_set(const or_tiling* t, float lo, float hi, idx_fn f, int32_t n, 
   }
 }
 
+static int in_interval_a(float lo, float hi, float x, int wrap, float pi_f, float two_pi_f);
+
 /* circular interval (start, length) of a bitmap that is one circular run (or full) */
 static int set_to_interval(const uint8_t* set, int32_t n, int32_t* start, int32_t* len) {
   int32_t cnt = 0;
@@ -976,12 +980,54 @@ int or_cull_lidar(int64_t n, const int32_t* valid, const float* box, const or_ti
   {
     uint8_t* cset = (uint8_t*)malloc(t->cull_az_cells);
     uint8_t* tset = (uint8_t*)malloc(t->n_theta);
+    uint8_t* rset = (uint8_t*)malloc(t->n_phi);
 #pragma omp for schedule(dynamic, 4096)
     for (int64_t g = 0; g < n; ++g) {
       count[g] = 0;
       for (int c = 0; c < 4; ++c) rect[g * 4 + c] = 0;
       if (!valid[g]) continue;
       float lo_a = box[g * 4], hi_a = box[g * 4 + 1], lo_b = box[g * 4 + 2], hi_b = box[g * 4 + 3];
+      if (enable_cull == 2) {
+        /* Exact ray containment per render tile (reading A32): the tiles holding at least one
+         * ray (b, j) with lo_b <= omega_b <= hi_b and phi_j inside the azimuth interval under
+         * the compositing membership rule (O12, A12).  Plain scans over every beam and every
+         * column: a tile (elevation tile of b, azimuth tile of j) holds such a ray iff one of
+         * its beams and one of its columns pass. */
+        memset(rset, 0, t->n_phi);
+        memset(tset, 0, t->n_theta);
+        int any_b = 0, any_c = 0;
+        for (int32_t b = 0; b < t->n_beams; ++b) {
+          float w = t->ray_el[(int64_t)b * t->n_az];
+          if (lo_b <= w && w <= hi_b) {
+            rset[or_elev_tile(t, w)] = 1;
+            any_b = 1;
+          }
+        }
+        for (int32_t j = 0; j < t->n_az && any_b; ++j) {
+          float p = t->ray_az[j];
+          if (in_interval_a(lo_a, hi_a, p, 1, t->pi_f, t->two_pi_f)) {
+            tset[or_az_col(t, p)] = 1;
+            any_c = 1;
+          }
+        }
+        if (!any_b || !any_c) continue; /* culled: no ray inside the extent */
+        int32_t e_lo = 0, e_hi = t->n_phi - 1;
+        while (!rset[e_lo]) ++e_lo;
+        while (!rset[e_hi]) --e_hi;
+        for (int32_t e = e_lo; e <= e_hi; ++e)
+          if (!rset[e]) err = 1; /* elevation tiles of a beam interval are contiguous */
+        int32_t cs, cl;
+        if (set_to_interval(tset, t->n_theta, &cs, &cl)) {
+          err = 1;
+          continue;
+        }
+        rect[g * 4 + 0] = e_lo;
+        rect[g * 4 + 1] = e_hi;
+        rect[g * 4 + 2] = cs;
+        rect[g * 4 + 3] = cl;
+        count[g] = (e_hi - e_lo + 1) * cl;
+        continue;
+      }
       float b0 = t->bounds[0], bl = t->bounds[t->n_phi];
       if (hi_b < b0 || lo_b > bl) continue; /* box misses the beam band */
       if (enable_cull) {                     /* Proc. RayOccupancyCount over the dense rectangle */
@@ -1017,6 +1063,7 @@ int or_cull_lidar(int64_t n, const int32_t* valid, const float* box, const or_ti
     }
     free(cset);
     free(tset);
+    free(rset);
   }
   return err ? -1 : 0;
 }

@@ -55,6 +55,7 @@ typedef struct {
   int32_t* tile_rays;       /* [n_rays]   */
   int32_t* sat;             /* [sat_rows*sat_cols] */
   int32_t* ray_cell_row; int32_t* ray_cell_col; /* dense cell of each ray (diagnostic) */
+  int32_t n_beams, n_az;    /* B, A: ray id = b*A + j                                       */
 } or_tiling;
 
 /* ---- primitives (exposed for pins) ---- */

@@ -56,7 +56,8 @@ class OrTiling(C.Structure):
                 ("pi_f", C.c_float), ("two_pi_f", C.c_float), ("az_tile_scale", C.c_float),
                 ("az_cell_scale", C.c_float), ("bounds", f32p), ("cull_row_scale", f32p), ("ray_az", f32p),
                 ("ray_el", f32p), ("ray_s", f32p), ("ray_tile", i32p), ("tile_ray_offsets", i32p),
-                ("tile_rays", i32p), ("sat", i32p), ("ray_cell_row", i32p), ("ray_cell_col", i32p)]
+                ("tile_rays", i32p), ("sat", i32p), ("ray_cell_row", i32p), ("ray_cell_col", i32p),
+                ("n_beams", C.c_int32), ("n_az", C.c_int32)]
 
 
 class OrProjOut(C.Structure):
@@ -285,6 +286,8 @@ def project_camera(scene, cam, pose0=None, pose1=None, K=None, ut=None, extent_s
 # ------------------------------------------------------------------------------------
 
 def cull_lidar(valid, box, tiling: Tiling, enable_cull=True):
+    """Counts and tile rects (O8).  enable_cull: 0/False off, 1/True the paper's dense-grid
+    SAT test (Proc. RayOccupancyCount / ProjectParticles), 2 exact ray containment (A32)."""
     n = int(valid.shape[0])
     valid = np.ascontiguousarray(valid, np.int32)
     box = np.ascontiguousarray(box, np.float32)
@@ -466,7 +469,7 @@ def render_lidar(scene, cfg, tiling: Tiling | None = None, pose0=None, pose1=Non
         listed = valid != 0
         lbox = proj["box"]
     if mode == "tiled":
-        count, rect = cull_lidar(listed.astype(np.int32), lbox, tiling, enable_cull and flag_eps is None)
+        count, rect = cull_lidar(listed.astype(np.int32), lbox, tiling, int(enable_cull) if flag_eps is None else 0)
         _, ids, ranges = bin_pairs(count, rect, proj["key"], tiling.n_tiles, tiling.n_theta)
         ray_tile = tiling.ray_tile
     else:

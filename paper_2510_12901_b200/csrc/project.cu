@@ -99,6 +99,9 @@ struct ProjArgs {
   float pi_f, two_pi_f, az_tile_scale, az_cell_scale;
   const float *bounds, *row_scale;
   const int* sat;
+  const float *beam_sorted, *col_sorted;  // exact culling (A32): ascending beam / column angles
+  int n_beams, n_az;
+  float col_step;                         // (float)(n_az / 2 pi): search start estimate
   // camera
   int cam_model, width, height, rolling, tile_px, Wt, Ht;
   float fx, fy, cx, cy, k[5], near_m, max_theta, inv_tile;
@@ -124,6 +127,93 @@ __device__ __forceinline__ int elev_tile(const ProjArgs& A, float w) {
 __device__ __forceinline__ int dense_row_e(const ProjArgs& A, float w, int e) {
   const float u = __fmul_rn(__fsub_rn(w, A.bounds[e]), A.row_scale[e]);
   return e * A.rows_per_tile + clamp_floor(u, A.rows_per_tile);
+}
+
+// first index i in [0, n) with a[i] >= x (n if none); a ascending
+__device__ __forceinline__ int lower_bound_f(const float* a, int n, float x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+// first index i in [0, n) with a[i] > x (n if none); a ascending
+__device__ __forceinline__ int upper_bound_f(const float* a, int n, float x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) <= x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+// the same on the (near-uniform) ascending column azimuths: start from the uniform-grid
+// estimate and walk (the result is exact; the estimate only saves the log-step search)
+__device__ __forceinline__ int col_bound(const ProjArgs& A, float x, bool upper) {
+  const float* a = A.col_sorted;
+  const float p0 = __ldg(a);
+  const int i0 = (int)fminf(fmaxf(floorf((x - p0) * A.col_step), 0.f), (float)A.n_az);
+  int i = i0;
+  if (upper) {  // first a[i] > x
+    while (i > 0 && __ldg(a + i - 1) > x) --i;
+    while (i < A.n_az && __ldg(a + i) <= x) ++i;
+  } else {      // first a[i] >= x
+    while (i > 0 && __ldg(a + i - 1) >= x) --i;
+    while (i < A.n_az && __ldg(a + i) < x) ++i;
+  }
+  return i;
+}
+
+// Exact ray-containment culling (reading A32): the render tiles holding a ray inside the
+// box.  Rays are beams x columns, so they are the elevation tiles of the beams with
+// lo_b <= omega <= hi_b times the azimuth tiles of the columns inside the azimuth interval
+// under the render's membership rule (A12: seam-shifted box edges) -- a circular run of the
+// ascending column azimuths.  Returns the tile count (0: no ray inside) and the rectangle.
+__device__ __forceinline__ int exact_rect(const ProjArgs& A, const float box[4], int rect[4]) {
+  const int bl = lower_bound_f(A.beam_sorted, A.n_beams, box[2]);
+  const int bh = upper_bound_f(A.beam_sorted, A.n_beams, box[3]) - 1;
+  if (bl > bh) return 0;
+  const float lo = box[0], hi = box[1];
+  const int NA = A.n_az;
+  int first, n;  // run of sorted columns: first, length (circular)
+  if (__fsub_rn(hi, lo) >= A.two_pi_f || (lo < -A.pi_f && hi > A.pi_f)) {
+    first = 0;
+    n = NA;
+  } else if (lo < -A.pi_f) {  // [lo, hi] covers a prefix, [lo + 2 pi, ...) a suffix
+    const int a2 = col_bound(A, hi, true);
+    const int s2 = col_bound(A, __fadd_rn(lo, A.two_pi_f), false);
+    if (s2 <= a2) { first = 0; n = NA; }
+    else { first = s2; n = (NA - s2) + a2; }
+  } else if (hi > A.pi_f) {   // [lo, hi] covers a suffix, (..., hi - 2 pi] a prefix
+    const int a1 = col_bound(A, lo, false);
+    const int s3 = col_bound(A, __fsub_rn(hi, A.two_pi_f), true);
+    if (s3 >= a1) { first = 0; n = NA; }
+    else { first = a1; n = (NA - a1) + s3; }
+  } else {
+    first = col_bound(A, lo, false);
+    n = col_bound(A, hi, true) - first;
+  }
+  if (n <= 0) return 0;
+  if (first >= NA) first -= NA;  // a run starting past the last column starts at column 0
+  int cs, cl;
+  if (n >= NA) {
+    cs = 0;
+    cl = A.n_theta;
+  } else {
+    const int last = first + n - 1;
+    const int cF = az_index(__ldg(A.col_sorted + first), A.pi_f, A.az_tile_scale, A.n_theta);
+    const int cL = az_index(__ldg(A.col_sorted + (last < NA ? last : last - NA)), A.pi_f, A.az_tile_scale, A.n_theta);
+    if (last < NA) { cs = cF; cl = cL - cF + 1; }
+    else if (cL >= cF) { cs = 0; cl = A.n_theta; }
+    else { cs = cF; cl = A.n_theta - cF + cL + 1; }
+  }
+  rect[0] = elev_tile(A, __ldg(A.beam_sorted + bl));
+  rect[1] = elev_tile(A, __ldg(A.beam_sorted + bh));
+  rect[2] = cs;
+  rect[3] = cl;
+  return (rect[1] - rect[0] + 1) * cl;
 }
 
 __device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c0, int c1) {
@@ -613,7 +703,9 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
     }
     if (ok) {
       // ---- culling + render-tile rectangle
-      if (KIND == SIMULI_SENSOR_LIDAR) {
+      if (KIND == SIMULI_SENSOR_LIDAR && A.enable_cull == 2) {
+        count = exact_rect(A, box, rect);
+      } else if (KIND == SIMULI_SENSOR_LIDAR) {
         const float b0 = A.bounds[0], bl = A.bounds[A.n_phi];
         bool keep = !(box[3] < b0 || box[2] > bl);
         const int e0 = elev_tile(A, box[2]), e1 = elev_tile(A, box[3]);
@@ -829,6 +921,14 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     A.az_cells = T.cull_az_cells; A.sat_cols = T.sat_cols; A.enable_cull = P->enable_culling;
     A.pi_f = T.pi_f; A.two_pi_f = T.two_pi_f; A.az_tile_scale = T.az_tile_scale; A.az_cell_scale = T.az_cell_scale;
     A.bounds = T.elev_bounds; A.row_scale = T.cull_row_scale; A.sat = T.sat;
+    SIMULI_REQUIRE(P->enable_culling >= 0 && P->enable_culling <= 2, "simuli_project: enable_culling must be 0, 1 or 2");
+    if (P->enable_culling == 2) {
+      SIMULI_REQUIRE(T.beam_el_sorted && T.col_az_sorted && T.n_beams >= 1 && T.n_azimuth >= 1,
+                     "simuli_project: exact culling needs beam_el_sorted / col_az_sorted");
+      A.beam_sorted = T.beam_el_sorted; A.col_sorted = T.col_az_sorted;
+      A.n_beams = T.n_beams; A.n_az = T.n_azimuth;
+      A.col_step = (float)(T.n_azimuth / (2.0 * 3.14159265358979323846));
+    }
     if (A.beam_div > 0.f) {
       if (act) launch_project<SIMULI_SENSOR_LIDAR, true, true>(A, blocks, threads, st);
       else launch_project<SIMULI_SENSOR_LIDAR, true, false>(A, blocks, threads, st);

@@ -212,12 +212,12 @@ extern "C" int32_t simuli_build_tiles(const simuli_lidar* lidar, const simuli_ti
   const bool sizing = !out->elev_bounds && !out->cull_row_scale && !out->ray_az && !out->ray_el && !out->ray_s &&
                       !out->ray_tile && !out->tile_ray_offsets && !out->tile_rays && !out->sat &&
                       !out->elev_tile_beam_offsets && !out->elev_tile_beams && !out->az_tile_col_offsets &&
-                      !out->az_tile_cols;
+                      !out->az_tile_cols && !out->beam_el_sorted && !out->col_az_sorted;
   if (sizing) return SIMULI_OK;
   SIMULI_REQUIRE(out->elev_bounds && out->cull_row_scale && out->ray_az && out->ray_el && out->ray_s &&
                      out->ray_tile && out->tile_ray_offsets && out->tile_rays && out->sat &&
                      out->elev_tile_beam_offsets && out->elev_tile_beams && out->az_tile_col_offsets &&
-                     out->az_tile_cols,
+                     out->az_tile_cols && out->beam_el_sorted && out->col_az_sorted,
                  "simuli_build_tiles: either all or none of the array pointers must be set");
 
   std::copy(tm.bounds.begin(), tm.bounds.end(), out->elev_bounds);
@@ -246,6 +246,11 @@ extern "C" int32_t simuli_build_tiles(const simuli_lidar* lidar, const simuli_ti
   for (int32_t c = 0; c < tm.n_theta; ++c) out->az_tile_col_offsets[c + 1] = out->az_tile_col_offsets[c] + cols_in[c];
   std::vector<int32_t> cc(out->az_tile_col_offsets, out->az_tile_col_offsets + tm.n_theta);
   for (int32_t j = 0; j < A; ++j) out->az_tile_cols[cc[col_tile[j]]++] = j;
+  // ascending beam elevations / column azimuths: the exact culling's binary searches (A32)
+  std::copy(elev.begin(), elev.end(), out->beam_el_sorted);
+  std::sort(out->beam_el_sorted, out->beam_el_sorted + B);
+  std::copy(col_phi.begin(), col_phi.end(), out->col_az_sorted);
+  std::sort(out->col_az_sorted, out->col_az_sorted + A);
   // dense ray mask (cells hit by >= 1 ray) -> summed-area table, zero first row/column
   std::vector<uint8_t> mask(static_cast<size_t>(rows) * cols, 0);
   std::vector<int32_t> beam_row(B);

@@ -24,6 +24,7 @@ SENSOR_LIDAR, SENSOR_CAMERA = 0, 1
 CAM_PINHOLE_RADTAN, CAM_FISHEYE_KB = 0, 1
 RECORD_FLOATS = 20
 
+ABI_VERSION = 10  # include/simuli.h SIMULI_ABI_VERSION
 EXPORTED = ["simuli_last_error", "simuli_abi_version", "simuli_build_tiles", "simuli_project",
             "simuli_bin_sort_workspace_size", "simuli_bin_sort", "simuli_render_lidar", "simuli_render_camera",
             "simuli_compose_camera", "simuli_backward_workspace_size", "simuli_backward_lidar",
@@ -63,7 +64,8 @@ _TILING_SCALARS = [("n_phi", C.c_int32), ("n_theta", C.c_int32), ("n_tiles", C.c
 _TILING_ARRAYS = [("elev_bounds", f32p), ("cull_row_scale", f32p), ("ray_az", f32p), ("ray_el", f32p),
                   ("ray_s", f32p), ("ray_tile", i32p), ("tile_ray_offsets", i32p), ("tile_rays", i32p),
                   ("sat", i32p), ("elev_tile_beam_offsets", i32p), ("elev_tile_beams", i32p),
-                  ("az_tile_col_offsets", i32p), ("az_tile_cols", i32p)]
+                  ("az_tile_col_offsets", i32p), ("az_tile_cols", i32p), ("beam_el_sorted", f32p),
+                  ("col_az_sorted", f32p)]
 
 
 class Tiling(C.Structure):
@@ -153,6 +155,8 @@ def load():
     L = C.CDLL(LIB_PATH)
     L.simuli_last_error.restype = C.c_char_p
     L.simuli_abi_version.restype = C.c_int32
+    if L.simuli_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"libsimuli.so ABI {L.simuli_abi_version()} != binding {ABI_VERSION}; rebuild it")
     L.simuli_build_tiles.argtypes = [C.POINTER(Lidar), C.POINTER(TilingParams), C.POINTER(Tiling)]
     L.simuli_project.argtypes = [C.POINTER(Gaussians), C.POINTER(ProjectParams), C.POINTER(Projected), C.c_void_p]
     L.simuli_bin_sort_workspace_size.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]
@@ -215,7 +219,8 @@ def simuli_build_tiles(cfg) -> dict:
              "ray_tile": (t.n_rays, np.int32), "tile_ray_offsets": (t.n_tiles + 1, np.int32),
              "tile_rays": (t.n_rays, np.int32), "sat": (t.sat_rows * t.sat_cols, np.int32),
              "elev_tile_beam_offsets": (t.n_phi + 1, np.int32), "elev_tile_beams": (t.n_beams, np.int32),
-             "az_tile_col_offsets": (t.n_theta + 1, np.int32), "az_tile_cols": (t.n_azimuth, np.int32)}
+             "az_tile_col_offsets": (t.n_theta + 1, np.int32), "az_tile_cols": (t.n_azimuth, np.int32),
+             "beam_el_sorted": (t.n_beams, np.float32), "col_az_sorted": (t.n_azimuth, np.float32)}
     arrays = {k: np.zeros(n, dt) for k, (n, dt) in sizes.items()}
     for k, a in arrays.items():
         setattr(t, k, a.ctypes.data_as(f32p if a.dtype == np.float32 else i32p))
@@ -410,9 +415,13 @@ class _Frame:
 
 
 class LidarRenderer(_Frame):
-    """One spinning LiDAR + one Gaussian set G_l resident on the device."""
+    """One spinning LiDAR + one Gaussian set G_l resident on the device.
 
-    def __init__(self, cfg, scene_dev, capacity=None, device="cuda", enable_culling=True, write_all_records=False,
+    enable_culling: 0 off, 1 the paper's dense-grid SAT culling (Proc. RayOccupancyCount /
+    ProjectParticles), 2 exact ray containment per render tile (A32, default); the rendered
+    outputs are identical in all three modes, only the tile lists differ."""
+
+    def __init__(self, cfg, scene_dev, capacity=None, device="cuda", enable_culling=2, write_all_records=False,
                  ut=(1.0, 2.0, 0.0), extent_sigma=3.0, render_params=(1.0 / 255.0, 0.99, 1e-4), per_ray_sh=False):
         import torch
         self.device = device

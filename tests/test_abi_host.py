@@ -38,7 +38,7 @@ def test_exports_every_header_symbol(lib):
     exported = {ln.split()[-1] for ln in nm.splitlines() if " T " in ln}
     assert set(syms) <= exported
     assert set(lib.EXPORTED) == set(syms)
-    assert L.simuli_abi_version() == 9
+    assert L.simuli_abi_version() == 10
 
 
 def test_library_is_sm100a(lib):
@@ -74,6 +74,10 @@ def _compare_tiling(cfg, SM, O):
     assert p["elev_tile_beam_offsets"][-1] == B and p["az_tile_col_offsets"][-1] == A
     assert p["max_beams_per_elev_tile"] == np.diff(p["elev_tile_beam_offsets"]).max()
     assert p["max_cols_per_az_tile"] == np.diff(p["az_tile_col_offsets"]).max()
+    # exact culling's search arrays (A32): the beam elevations / column azimuths, ascending
+    A = p["n_azimuth"]
+    assert np.array_equal(p["beam_el_sorted"], np.sort(p["ray_el"][::A]))
+    assert np.array_equal(p["col_az_sorted"], np.sort(p["ray_az"][:A]))
 
 
 @pytest.mark.parametrize("name", ["A", "B", "C", "tiny"])

@@ -102,18 +102,21 @@ def test_project_lidar_tier1(SM, oracle_mod, config):
 
 
 # ------------------------------------------------------------------ stages 3-4 (a2-a4): cull, pairs, sort
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("config", ["A", "tiny", "B-sub"])
-def test_cull_bin_sort_tier1_bit_exact(SM, oracle_mod, config):
+def test_cull_bin_sort_tier1_bit_exact(SM, oracle_mod, config, mode):
+    """Counts, tile rects, sorted (key, id) pairs and tile ranges bit-exact vs the oracle fed
+    the GPU's boxes and keys; mode 1 = the paper's SAT culling, 2 = exact containment (A32)."""
     O = oracle_mod
     if config == "B-sub":
         cfg, scene = S.lidar_config("B"), S.scene_for("B", n=300_000)
     else:
         cfg, scene = S.lidar_config(config), S.scene_for(config, seed=9 if config == "tiny" else None)
-    r = lidar_run(SM, cfg, scene, write_all_records=True)
+    r = lidar_run(SM, cfg, scene, write_all_records=True, enable_culling=mode)
     t = O.Tiling(cfg)
     box = r.record.cpu().numpy()[:, 16:20].copy()
     valid = np.isfinite(box[:, 0]).astype(np.int32)
-    count, rect = O.cull_lidar(valid, box, t, True)
+    count, rect = O.cull_lidar(valid, box, t, mode)
     assert np.array_equal(r.tile_count.cpu().numpy(), count)
     gr = r.tile_rect.cpu().numpy()
     nz = count > 0
@@ -185,10 +188,11 @@ def test_lidar_tiny_scenes_vs_bruteforce(SM, oracle_mod):
 def test_gpu_invariance_tiling_and_culling(SM):
     scene = S.scene_for("B", n=200_000)
     outs = []
-    for n_phi, M, cull in ((16, 32, 1), (16, 32, 0), (8, 64, 1), (32, 16, 1), (4, 256, 1), (1, 8, 1)):
+    for n_phi, M, cull in ((16, 32, 2), (16, 32, 1), (16, 32, 0), (8, 64, 1), (32, 16, 2), (4, 256, 1),
+                           (1, 8, 2)):
         cfg = S.lidar_config("B")
         cfg.n_phi, cfg.max_rays_per_tile = n_phi, M
-        r = lidar_run(SM, cfg, scene, enable_culling=bool(cull))
+        r = lidar_run(SM, cfg, scene, enable_culling=cull)
         outs.append({k: v.cpu().numpy().copy() for k, v in r.out.items() if v is not None and k != "ray_od"})
     for o in outs[1:]:
         for k in outs[0]:
@@ -198,9 +202,11 @@ def test_gpu_invariance_tiling_and_culling(SM):
 def test_culling_reduces_pairs(SM):
     scene = S.scene_for("B", n=300_000)
     cfg = S.lidar_config("B")
-    on = lidar_run(SM, cfg, scene, enable_culling=True)
-    off = lidar_run(SM, cfg, scene, enable_culling=False)
+    exact = lidar_run(SM, cfg, scene, enable_culling=2)
+    on = lidar_run(SM, cfg, scene, enable_culling=1)
+    off = lidar_run(SM, cfg, scene, enable_culling=0)
     assert on.n_pairs.item() < off.n_pairs.item()  # direction of tab:culling
+    assert exact.n_pairs.item() < on.n_pairs.item()  # exact containment refines it (A32)
 
 
 # ------------------------------------------------------------------ sort + edge cases

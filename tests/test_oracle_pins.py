@@ -508,6 +508,49 @@ def test_culling_exact_and_rect_contains_members(oracle_mod, config):
             assert {int(t.ray_tile[r]) for r in members} <= tiles_of(g)
 
 
+@pytest.mark.parametrize("config", ["A", "tiny", "B-small"])
+def test_exact_culling_is_the_brute_force_tile_set(oracle_mod, config):
+    """Exact ray-containment culling (A32): the tile set of every particle equals, by brute
+    force over every ray, the set of render tiles holding a ray inside its box under the
+    compositing membership rule (A12); it refines the paper's SAT culling (subset)."""
+    O = oracle_mod
+    if config == "B-small":  # Pandar64 beams, rolling shutter, a random subset of the corridor
+        cfg = S.lidar_config("B")
+        cfg.n_azimuth = 600
+        scene = S.scene_for("B", n=3000)
+    else:
+        cfg = S.lidar_config(config)
+        scene = S.scene_for(config, seed=5)
+    t = O.Tiling(cfg)
+    proj = O.project_lidar(scene, cfg)
+    count2, rect2 = O.cull_lidar(proj["valid"], proj["box"], t, 2)
+    count1, rect1 = O.cull_lidar(proj["valid"], proj["box"], t, 1)
+    tiles = lambda rect, g: {r * t.n_theta + (rect[g, 2] + c) % t.n_theta  # noqa: E731
+                             for r in range(rect[g, 0], rect[g, 1] + 1) for c in range(rect[g, 3])}
+    n_checked = n_refined = 0
+    for g in np.nonzero(proj["valid"])[0][:400]:
+        members = np.nonzero(_membership(proj["box"][g], t.ray_az, t.ray_el, t.pi_f, t.two_pi_f))[0]
+        brute = {int(t.ray_tile[r]) for r in members}
+        got = tiles(rect2, g) if count2[g] else set()
+        assert got == brute, g
+        assert count2[g] == len(brute)
+        assert count2[g] == 0 or brute <= tiles(rect1, g)
+        n_checked += 1
+        n_refined += count2[g] < count1[g]
+    assert n_checked > 50 and n_refined > 0
+
+
+def test_exact_culling_render_unchanged(oracle_mod):
+    """Outputs do not depend on the culling mode (A12): off, SAT and exact (A32)."""
+    O = oracle_mod
+    cfg = S.lidar_config("A")
+    scene = S.scene_for("A")
+    outs = [O.render_lidar(scene, cfg, mode="tiled", enable_cull=m) for m in (0, 1, 2)]
+    for o in outs[1:]:
+        for k in ("feat", "opacity", "depth_accum", "T_final", "n_contrib"):
+            assert np.array_equal(outs[0][k], o[k]), k
+
+
 # ---------------------------------------------------------------- O13 tiled == brute force
 def test_tiled_equals_bruteforce_config_a(oracle_mod):
     O = oracle_mod
@@ -529,7 +572,7 @@ def test_tiled_equals_bruteforce_tiny_scenes(oracle_mod):
         if seed % 3 == 2:
             cfg.cull_az_cells = 1600
         scene = S.scene_for("tiny", seed=seed)
-        a = O.render_lidar(scene, cfg, mode="tiled", enable_cull=(seed % 2 == 0))
+        a = O.render_lidar(scene, cfg, mode="tiled", enable_cull=seed % 3)
         b = O.render_lidar(scene, cfg, mode="brute")
         for k in ("feat", "opacity", "depth_accum", "T_final", "n_contrib"):
             assert np.array_equal(a[k], b[k]), (seed, k)
