@@ -9,7 +9,10 @@
  *
  * Parity status: every function below is pinned by tests/test_oracle_pins.py except the
  * whole-render composition on realistic scenes, which the paper gives no numbers for
- * ("parity unpinned" for the end-to-end render values).  The NEXT-row
+ * ("parity unpinned" for the end-to-end render values).  O6's lens models
+ * (KB fisheye, OpenCV radtan) and their inverses are pinned to OpenCV (cv2.fisheye /
+ * cv2.projectPoints / undistortPoints, <= 1e-9 px, <= 1e-12 rad).  O8's exact culling mode
+ * (A32) is pinned by brute force over every ray.  The NEXT-row
  * functions are pinned too: O0 (scipy + rigid invariance), O14 (constant map / identity
  * grid, texel centres, affine-field exactness), O15/O16 (central finite differences of the
  * forward, LiDAR and camera, with scene graph and per-ray SH; SH linearity; the opacity

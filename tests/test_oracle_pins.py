@@ -652,6 +652,57 @@ def test_camera_closed_forms(oracle_mod):
             assert ok2 and abs(uv[0] - u) < 1e-8 and abs(uv[1] - v) < 1e-8
 
 
+@pytest.mark.parametrize("name", ["D", "D-small", "pinhole-small", "kb-random", "radtan-random"])
+def test_camera_models_vs_opencv(oracle_mod, name):
+    """O6 pinned to an independent implementation (A22): the oracle's KB fisheye
+    and radtan projections equal OpenCV's cv2.fisheye.projectPoints / cv2.projectPoints, and
+    its inverses equal cv2.fisheye.undistortPoints / cv2.undistortPointsIter, on >= 300
+    random points inside the field of view (OpenCV's fisheye model is defined for z > 0)."""
+    cv2 = pytest.importorskip("cv2")
+    O = oracle_mod
+    rng = np.random.default_rng(hash(name) % 1000)
+    if name == "kb-random":
+        cam = S.camera_config("D-small")
+        cam.k = tuple(rng.uniform(-0.01, 0.01, 4)) + (0.0,)
+    elif name == "radtan-random":
+        cam = S.camera_config("pinhole-small")
+        cam.k = tuple(rng.uniform(-0.05, 0.05, 5))
+    else:
+        cam = S.camera_config(name)
+    n = 300
+    th = rng.uniform(0, min(cam.max_theta * 0.9, math.radians(89.0)), n)
+    ph = rng.uniform(-math.pi, math.pi, n)
+    r = rng.uniform(0.5, 50, n)
+    X = np.stack([r * np.sin(th) * np.cos(ph), r * np.sin(th) * np.sin(ph), r * np.cos(th)], 1)
+    f = lambda v: float(np.float32(v))  # noqa: E731  the interface's float32 camera parameters
+    Km = np.array([[f(cam.fx), 0, f(cam.cx)], [0, f(cam.fy), f(cam.cy)], [0, 0, 1.0]])
+    ident = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    ours = np.array([O.camera_point(x, cam, ident, ident, 0)[1][:2] for x in X])
+    crit = (cv2.TERM_CRITERIA_COUNT | cv2.TERM_CRITERIA_EPS, 100, 1e-15)
+    if cam.model == 1:
+        D = np.array([f(v) for v in cam.k[:4]])
+        ref, _ = cv2.fisheye.projectPoints(X.reshape(-1, 1, 3), np.zeros(3), np.zeros(3), Km, D)
+        und = cv2.fisheye.undistortPoints(ours.reshape(-1, 1, 2), Km, D, criteria=crit).reshape(-1, 2)
+    else:
+        D = np.array([f(v) for v in cam.k])
+        ref, _ = cv2.projectPoints(X.reshape(-1, 1, 3), np.zeros(3), np.zeros(3), Km, D)
+        und = cv2.undistortPointsIter(ours.reshape(-1, 1, 2), Km, D, None, None, crit).reshape(-1, 2)
+    assert np.abs(ours - ref.reshape(-1, 2)).max() < 1e-9  # pixels
+    dirs = np.array([O.camera_unproject(cam, u, v)[1] for u, v in ours])
+    rd = np.concatenate([und, np.ones((n, 1))], 1)
+    rd /= np.linalg.norm(rd, axis=1, keepdims=True)
+    # OpenCV's iterative undistortion does not always converge near 90 deg: compare where its
+    # own answer reprojects onto the pixel
+    if cam.model == 1:
+        back, _ = cv2.fisheye.projectPoints(rd.reshape(-1, 1, 3), np.zeros(3), np.zeros(3), Km, D)
+    else:
+        back, _ = cv2.projectPoints(rd.reshape(-1, 1, 3), np.zeros(3), np.zeros(3), Km, D)
+    conv = np.abs(back.reshape(-1, 2) - ours).max(1) < 1e-9
+    assert conv.mean() > 0.9
+    assert np.abs(dirs - rd)[conv].max() < 1e-12
+    assert np.abs(dirs - X / np.linalg.norm(X, axis=1, keepdims=True)).max() < 1e-12
+
+
 def test_camera_rolling_shutter_degenerate(oracle_mod):
     O = oracle_mod
     cam = S.camera_config("D-small")
