@@ -47,6 +47,10 @@ WORKLOAD = ("B: PandaSet-like Pandar64 scan, 64x1800 rays, 2M Gaussians (driving
 # Algorithmic lane-instruction costs per compositing event; the counts
 # come from the kernel's own workload counters (entries visited / in box / composited).
 C_BOX, C_RESP, C_ACC, C_RAY = 8, 45, 8, 80
+# SURVEY §8(d) projection instruction model (lane-instructions): per sigma point C_PROJ
+# (transform + atan2 + asin + sqrt) and, per rolling-shutter iteration, C_PROJ + C_POSE;
+# per particle C_UT + C_MISC; per visible particle C_SH
+C_PROJ, C_POSE, C_UT, C_MISC, C_SH = 75, 60, 60, 240, 90
 
 
 def read_peaks():
@@ -136,6 +140,10 @@ def dist_env():
     return ws, rank, local
 
 
+N_STAGE = 60  # scans of the per-stage timing pass (>= 50 timed iterations)
+# k_project; k_count_reduce, k_count_top, k_duplicate, 6 x k_onesweep (passes beyond the
+# device-side pass count exit at once), k_ranges, k_tile_order; k_render_lidar
+LAUNCHES_PER_SCAN = 1 + (3 + 6 + 2) + 1
 B_BATCH = 512  # scans in the B-batch trajectory (poses 0.2 m apart, x in [-51, +51] m)
 
 
@@ -276,11 +284,77 @@ def roofline_entries(stage_ms, counters, peaks, clocks_mhz):
                      "frac": ach / alu_peak, "algorithmic_lane_instr": int(lane_instr),
                      "algorithmic_bytes": int(b_render), "hbm_frac": b_render / t / 1e9 / hbm,
                      "ms": stage_ms["render"]}
-    # scan roofline t_roof = sum over stages of max(bytes / BW, instr / IR)
+    # strict scan roofline: the stages' algorithmic bytes (project, sort) and bytes /
+    # lane-instructions (render), t_roof = sum over stages of max(bytes / BW, instr / IR)
     t_roof = (b_project / (hbm * 1e9) + b_sort / (hbm * 1e9) +
               max(b_render / (hbm * 1e9), lane_instr / (alu_peak * 1e12)))
-    out["_scan"] = {"t_roof_ms": t_roof * 1e3}
+    # SURVEY §8(d) as written: projection bytes N 48 + N_vis (192 + 96) against its
+    # instruction model; duplication 8N + 16 N_vis + 12P; the radix passes counted,
+    # P (8 + passes 24) + 8P with passes = ceil(key bits / 8); render as above
+    K = counters["K"]
+    i_proj = n * (7 * (C_PROJ + K * (C_PROJ + C_POSE)) + C_UT + C_MISC) + n_vis * C_SH
+    b_proj8 = n * 48 + n_vis * (192 + 96)
+    b_dup8 = 8 * n + 16 * n_vis + 12 * P
+    b_sort8 = P * (8 + counters["passes"] * 24) + 8 * P
+    parts = {"project": max(b_proj8 / (hbm * 1e9), i_proj / (alu_peak * 1e12)),
+             "duplicate": b_dup8 / (hbm * 1e9), "sort": b_sort8 / (hbm * 1e9),
+             "render": max(b_render / (hbm * 1e9), lane_instr / (alu_peak * 1e12))}
+    out["_scan"] = {"t_roof_ms": t_roof * 1e3, "t_roof_ms_survey_8d": sum(parts.values()) * 1e3,
+                    "survey_8d_parts_ms": {k: v * 1e3 for k, v in parts.items()},
+                    "survey_8d_inputs": {"projection_lane_instr": int(i_proj), "key_bits": counters["key_bits"],
+                                         "passes": counters["passes"]}}
     return out
+
+
+def pct(v, q):
+    return float(np.percentile(np.asarray(v, np.float64), q))
+
+
+def workload_counters(r, cfg):
+    """SURVEY §8(d) workload counters of one config-B scan (outside every timed region):
+    the Gaussian funnel, tile expansion, tile-list lengths, per-ray work and the
+    warp-granularity ratio.  Needs r.want_counters(True) and write_all_records for N_valid."""
+    import torch
+    rec_box = r.record[:, 16]
+    cnt = r.tile_count
+    n = r.n
+    n_valid = int(torch.isfinite(rec_box).sum().item())
+    n_vis = int((cnt > 0).sum().item())
+    P = int(r.n_pairs.item())
+    rg = r.tile_ranges.cpu().numpy().astype(np.int64)
+    L = rg[:, 1] - rg[:, 0]
+    kb = r.depth_key[cnt > 0].view(torch.int32)
+    kspan = int(kb.max().item()) - int(kb.min().item()) if n_vis else 0
+    b = kspan.bit_length()
+    tbits = max(1, (r.n_tiles - 1).bit_length())
+    th = r.tiling_host
+    ray_tile = th["ray_tile"].reshape(-1)
+    nv = r.out["n_visited"].cpu().numpy().astype(np.int64)
+    ni = r.out["n_inbox"].cpu().numpy().astype(np.int64)
+    nc = r.out["n_contrib"].cpu().numpy().astype(np.int64)
+    list_len = L[ray_tile]
+    term = nv < list_len
+    # warp granularity: a warp-per-tile kernel issues max over the tile's rays of the
+    # entries scanned, for every ray of the tile
+    off = th["tile_ray_offsets"].reshape(-1)
+    rays = th["tile_rays"].reshape(-1)
+    per_tile_max = np.maximum.reduceat(nv[rays], off[:-1]) if len(rays) else np.zeros(0)
+    rays_in_tile = np.diff(off)
+    nonempty = rays_in_tile > 0
+    warp_gran = int((per_tile_max[nonempty] * rays_in_tile[nonempty]).sum())
+    return {"n": n, "n_valid": n_valid, "n_culled": n_valid - n_vis, "n_vis": n_vis, "P": P,
+            "tiles_per_visible_mean": P / max(n_vis, 1), "tiles_per_visible_max": int(cnt.max().item()),
+            "list_len_mean": float(L.mean()), "list_len_p99": pct(L, 99), "list_len_max": int(L.max()),
+            "R": r.n_rays, "n_tiles": r.n_tiles,
+            "visited": int(nv.sum()), "inbox": int(ni.sum()), "contrib": int(nc.sum()),
+            "visited_per_ray_mean": float(nv.mean()), "inbox_per_ray_mean": float(ni.mean()),
+            "contrib_per_ray_mean": float(nc.mean()),
+            "rays_terminated": int(term.sum()), "rays_exhausted": int((~term).sum()),
+            "warp_granularity_entries": warp_gran, "warp_granularity_ratio": warp_gran / max(int(nv.sum()), 1),
+            "key_bits": b + tbits, "depth_key_bits": b, "tile_bits": tbits, "passes": max(1, -(-(b + tbits) // 8)),
+            "K": int(cfg.rs_iterations),
+            "note": "terminated = the ray stopped before the end of its tile's list (T' < T_min, A14); a ray "
+                    "terminated by its list's last entry counts as exhausted"}
 
 
 def run_gpu(args):
@@ -290,9 +364,15 @@ def run_gpu(args):
     from paper_2510_12901_b200 import simuli as SM
 
     ws, rank, local = dist_env()
+    comm = None
     if ws > 1:
+        # NCCL communicator init logged (stderr) so the rank count is verifiable
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", init_method="env://")
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -310,7 +390,9 @@ def run_gpu(args):
         x.keep_keys = False  # the renderer reads only the sorted ids
     n_total = (args.steps + args.warmup) * ws
     my = shard_poses(n_total, ws, rank)
-    # size the pair buffers once (one sync), with head room for every pose of the shard
+    # size the pair buffers once (one sync) from a few poses of the shard, with head room;
+    # every timed scan's pair count is tracked on the device (sticky max) and checked after
+    # each timed region (a scan over capacity would have rendered truncated lists)
     need = 0
     for p0, p1 in my[:: max(1, len(my) // 4)]:
         r.scan(p0, p1, sync_capacity=True)
@@ -321,20 +403,22 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
+    def check_capacity(where):
+        mx = max(x.check_capacity() for x in rs)  # raises on overflow
+        return {"where": where, "max_pairs": mx, "capacity": min(x.capacity for x in rs)}
+
     for i in range(args.warmup):
         rs[i % S].scan(*my[i], stream=streams[i % S])
     torch.cuda.synchronize()
-    # counters of one scan (outside the timed region)
+    # workload counters of one scan (outside the timed regions)
     r.want_counters(True)
+    r.params.write_all_records = 1
     r.scan(*my[args.warmup])
     torch.cuda.synchronize()
-    counters = {"n": r.n, "n_vis": int((r.tile_count > 0).sum().item()), "P": int(r.n_pairs.item()),
-                "R": r.n_rays, "n_tiles": r.n_tiles,
-                "visited": int(r.out["n_visited"].sum().item()), "inbox": int(r.out["n_inbox"].sum().item()),
-                "contrib": int(r.out["n_contrib"].sum().item())}
+    counters = workload_counters(r, cfg)
+    r.params.write_all_records = 0
     r.want_counters(False)
-    if int(r.n_pairs.item()) > r.capacity:
-        raise RuntimeError("pair capacity too small")
+    cap_checks = [check_capacity("warm-up + counters")]
 
     # ---- timed region (headline): K scans, S in flight; device time between two events on
     # the launching (main) stream, the S scan streams forked from / joined into it; no L2
@@ -362,14 +446,16 @@ def run_gpu(args):
     wall = time.perf_counter() - wall0
     total_ms = e_beg.elapsed_time(e_end)
     max_ms = batch.reduce_max(total_ms, dev)  # slowest rank (device time)
+    cap_checks.append(check_capacity("headline timed region"))
 
-    # ---- stage breakdown (roofline evidence): one scan at a time on the main stream, L2
-    # flushed (256 MB write) before every scan outside the events, per-stage CUDA events
-    n_stage = min(args.steps, 60)
+    # ---- stage breakdown (roofline evidence): N_STAGE scans one at a time on the main
+    # stream, L2 flushed (256 MB write) before every scan outside the events, per-stage
+    # CUDA events; median / p10 / p90 (SURVEY §8(d) timing protocol)
+    n_stage = N_STAGE
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_stage)]
     for i in range(n_stage):
         flush.zero_()
-        p0, p1 = my[args.warmup + i]
+        p0, p1 = my[(args.warmup + i) % len(my)]
         r.set_poses(p0, p1)
         e = ev[i]
         e[0].record(stream)
@@ -381,10 +467,13 @@ def run_gpu(args):
         e[3].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    stage_ms = {"project": sum(e[0].elapsed_time(e[1]) for e in ev) / n_stage,
-                "bin_sort": sum(e[1].elapsed_time(e[2]) for e in ev) / n_stage,
-                "render": sum(e[2].elapsed_time(e[3]) for e in ev) / n_stage}
-    latency_ms = batch.reduce_max(sum(e[0].elapsed_time(e[3]) for e in ev) / n_stage, dev)
+    cap_checks.append(check_capacity("stage pass"))
+    samples = {"project": [e[0].elapsed_time(e[1]) for e in ev], "bin_sort": [e[1].elapsed_time(e[2]) for e in ev],
+               "render": [e[2].elapsed_time(e[3]) for e in ev], "scan": [e[0].elapsed_time(e[3]) for e in ev]}
+    dist_ms = {k: {"median": statistics.median(v), "p10": pct(v, 10), "p90": pct(v, 90), "mean": statistics.fmean(v)}
+               for k, v in samples.items()}
+    stage_ms = {k: dist_ms[k]["median"] for k in ("project", "bin_sort", "render")}
+    latency_ms = batch.reduce_max(dist_ms["scan"]["median"], dev)
     job_counters = batch.reduce_sum({"pairs": counters["P"], "scans": args.steps}, dev)
 
     # ---- e2e through the public API with host buffers: every scan takes its pose pair in
@@ -408,6 +497,7 @@ def run_gpu(args):
         st.synchronize()
     tt = time.perf_counter() - t0
     e2e_s = batch.reduce_max(tt, dev)
+    cap_checks.append(check_capacity("e2e timed region"))
     e2e = {"value": ws * args.steps * r.n_rays / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": 2 * 28, "d2h_bytes_per_step": int(d2h),
            "note": f"per scan: start/end pose (2 x 28 B) in as kernel parameters, all per-ray outputs "
@@ -415,14 +505,47 @@ def run_gpu(args):
                    f"stream; {S} scans in flight; host wall clock from first launch to last byte; "
                    f"scene resident in HBM"}
 
+    # ---- B-batch spot check: every 64th scan of the batch (the ones this
+    # rank rendered in the timed region) re-rendered, gathered to rank 0 (NCCL all_gather
+    # for N > 1) and compared bit for bit with rank 0 rendering the same poses itself (G=1)
+    spot = [i for i in range(args.warmup, n_total, 64)]
+    mine_idx = set(batch.shard_indices(n_total, ws, rank))
+    local = {}
+    for j, i in enumerate(spot):
+        if i in mine_idx:
+            k = batch.shard_indices(n_total, ws, rank).index(i)
+            out = r.scan(*my[k])
+            local[j] = torch.stack([out["depth"], out["intensity"], out["raydrop"], out["opacity"]]).clone()
+    torch.cuda.synchronize()
+    g0 = time.perf_counter()
+    like = torch.empty((4, r.n_rays), dtype=torch.float32, device=dev)
+    full = batch.gather_frames(local, len(spot), dev, owner=lambda j: spot[j] % ws, like=like)
+    gather_ms = 1e3 * (time.perf_counter() - g0)
+    identical = None
+    if rank == 0:
+        all_poses = shard_poses(n_total, 1, 0)
+        identical = True
+        for j, i in enumerate(spot):
+            out = r.scan(*all_poses[i])
+            ref = torch.stack([out["depth"], out["intensity"], out["raydrop"], out["opacity"]])
+            identical &= bool(torch.equal(full[j].to(dev), ref))
+    spot_check = {"scans": len(spot), "gather_ms": gather_ms, "gather_identical": identical,
+                  "note": "every 64th B-batch scan, rendered by its owner rank, gathered to rank 0 and compared "
+                          "bit for bit with rank 0's own render of the same pose (depth, intensity, ray drop, "
+                          "opacity)"}
+
     peaks = read_peaks()
     roof = roofline_entries(stage_ms, counters, peaks, clk.get("sm_mhz"))
     scan_roof = roof.pop("_scan")
+    thr = max_ms / args.steps
     scan_roof.update({"latency_ms": latency_ms, "frac_of_latency": scan_roof["t_roof_ms"] / latency_ms,
-                      "throughput_ms_per_scan": max_ms / args.steps,
-                      "frac_of_throughput": scan_roof["t_roof_ms"] / (max_ms / args.steps),
-                      "note": "t_roof = sum_s max(B_s / HBM, I_s / issue peak) with the stages' algorithmic "
-                              "bytes / lane-instructions (project and sort: bytes only)"})
+                      "throughput_ms_per_scan": thr, "frac_of_throughput": scan_roof["t_roof_ms"] / thr,
+                      "frac_of_throughput_survey_8d": scan_roof["t_roof_ms_survey_8d"] / thr,
+                      "frac_of_latency_survey_8d": scan_roof["t_roof_ms_survey_8d"] / latency_ms,
+                      "note": "t_roof = sum_s max(B_s / HBM, I_s / issue peak). strict: the stages' algorithmic "
+                              "bytes (project, sort: bytes only) and render lane-instructions; survey_8d: "
+                              "SURVEY §8(d) as written (projection instruction model, duplication bytes, radix "
+                              "passes counted)"})
     dom = max(roof, key=lambda k: roof[k]["ms"])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -435,11 +558,8 @@ def run_gpu(args):
         dist.destroy_process_group()
         return 0
     value = ws * args.steps * r.n_rays / (max_ms * 1e-3)
-    # k_project; k_count_reduce, k_count_top, k_duplicate, 6 x k_onesweep (passes beyond the
-    # device-side pass count exit at once), k_ranges, k_tile_order; k_render
-    launches_per_step = 1 + (3 + 6 + 2) + 1
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": thr, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "n_gaussians": r.n, "rays_per_scan": r.n_rays,
                        "scans_per_rank": args.steps, "scans_in_flight": S,
@@ -448,9 +568,10 @@ def run_gpu(args):
                        "parallelism": f"dp{ws}"},
             "scans_per_s": value / r.n_rays,
             "latency_ms_per_scan": latency_ms,
-            "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "roofline": roofline, "stages": roof, "scan_roofline": scan_roof, "counters": counters,
-            "job_counters": job_counters,
+            "e2e": e2e, "gpu_launches": LAUNCHES_PER_SCAN * args.steps,
+            "roofline": roofline, "stages": roof, "stage_ms_distribution": dict(dist_ms, n=n_stage),
+            "scan_roofline": scan_roof, "counters": counters, "job_counters": job_counters,
+            "capacity_checks": cap_checks, "spot_check": spot_check, "comm": comm,
             "clocks": clk,
             "wall_s_timed_region": wall}
     if ws == 1 and not args.no_cpu_baseline:

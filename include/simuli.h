@@ -183,7 +183,8 @@ typedef struct {
 /* Camera (A22).  model PINHOLE_RADTAN: k = (k1, k2, p1, p2, k3) (OpenCV);
  * FISHEYE_KB: k = (k1, k2, k3, k4, unused), theta_d = theta (1 + k1 th^2 + ... + k4 th^8).
  * Pixel centres at (i + 0.5, j + 0.5); rolling shutter: row j fires at s = (j + 0.5)/H
- * (top -> bottom); global shutter: s = 0.  tile_px must be a power of two (8, 16, 32). */
+ * (top -> bottom); global shutter: s = 0.  tile_px must be 8 or 16 (the render and backward kernels' tile
+ * shapes); simuli_project rejects any other value with SIMULI_ERR_UNSUPPORTED. */
 typedef struct {
   int32_t model;
   int32_t width, height;
@@ -351,8 +352,14 @@ int32_t simuli_render_camera(const simuli_projected* proj, const uint32_t* sorte
 /* ---- Backward pass ("differentiable renderer", P:160-171 training; readings A31) ----
  * Gradients of a loss L with respect to the particle parameters, given the upstream
  * gradients of the rendered outputs.  The forward decisions (box membership A12, the
- * alpha_min / near skips A13, the T_min termination A14) are replayed exactly (same
- * float32 arithmetic as the render kernels) and are not differentiated; the response
+ * alpha_min / near skips A13, the T_min termination A14) are replayed with the same
+ * float32 arithmetic as the render kernels and are not differentiated.  One exception: the
+ * LiDAR backward cuts a list into 512-entry segments and enters segment s with T = the
+ * product of the earlier segments' transmittance products (each formed from T = 1), whose
+ * float32 rounding can differ from the forward's single running product; a ray whose T
+ * crosses T_min within a few ulps of the threshold in a later segment can therefore
+ * terminate one member earlier or later than in the forward (A23 flags such rays).  The
+ * response
  * is: alpha = min(alpha_max, sigma rho(tau_max)) with tau_max and delta^2 of the
  * canonical transform M = diag(1/s) R(q/|q|)^T (clamped alpha: no gradient).  Features are
  * the per-particle SH at the projection's view direction (A17), held fixed (no gradient

@@ -39,19 +39,23 @@ def reduce_sum(values: dict, device="cpu") -> dict:
     return {k: int(v) for k, v in zip(keys, t.tolist())}
 
 
-def gather_frames(local: dict, n_total: int, device="cpu"):
+def gather_frames(local: dict, n_total: int, device="cpu", owner=None, like=None):
     """Gather {frame index: tensor} from every rank onto rank 0 (fixed-size all_gather of
-    a stacked buffer; frames of one batch have equal shapes).  Returns the full
-    {index: tensor} dict on rank 0, None elsewhere."""
+    a stacked buffer; frames of one batch have equal shapes).  owner(i) = the rank holding
+    frame i (default: round robin, i mod world); like = a tensor of the frame shape / dtype
+    (needed when a rank holds no frame).  Returns the full {index: tensor} dict on rank 0,
+    None elsewhere."""
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return dict(local)
     world, rank = dist.get_world_size(), dist.get_rank()
-    per = (n_total + world - 1) // world
-    sample = next(iter(local.values()))
+    own = owner if owner is not None else (lambda i: i % world)
+    frames_of = [[i for i in range(n_total) if own(i) == r] for r in range(world)]
+    per = max(1, max(len(f) for f in frames_of))
+    sample = like if like is not None else next(iter(local.values()))
     buf = torch.zeros((per,) + tuple(sample.shape), dtype=sample.dtype, device=device)
-    for k, i in enumerate(shard_indices(n_total, world, rank)):
+    for k, i in enumerate(frames_of[rank]):
         buf[k] = local[i].to(device)
     out = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(out, buf)
@@ -59,6 +63,6 @@ def gather_frames(local: dict, n_total: int, device="cpu"):
         return None
     full = {}
     for r in range(world):
-        for k, i in enumerate(shard_indices(n_total, world, r)):
+        for k, i in enumerate(frames_of[r]):
             full[i] = out[r][k]
     return full

@@ -10,7 +10,10 @@
 // Gradients of the compositing (Eq. 1) and of the response with respect
 // to the particle records, chained to the parameters.  Per ray the tile's list is
 // replayed with the forward kernels' float32 arithmetic, so every discrete decision
-// (membership, skips, termination) is the forward's; per contribution k, with suffix sums
+// (membership, skips, termination) is the forward's -- except that a LiDAR ray enters list
+// segment s > 0 with the product of the earlier segments' products, which can round
+// differently from the forward's running product (a T_min crossing within ulps of the
+// threshold may move by one member; simuli.h); per contribution k, with suffix sums
 // S_k = total - prefix_k:
 //   dL/dalpha_k = T_k (Gz.f_k + Go + GD tau_k) - (Gz.S_k(f) + Go S_k(1) + GD S_k(tau)) / (1 - alpha_k)
 // (oracle O15).  The totals come from the forward's outputs (or a first list pass).  All

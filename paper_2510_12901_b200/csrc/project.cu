@@ -940,8 +940,10 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
     SIMULI_REQUIRE(P->camera, "camera projection needs camera");
     const simuli_camera& C = *P->camera;
     SIMULI_REQUIRE(C.width > 0 && C.height > 0 && C.fx > 0 && C.fy > 0, "invalid camera size / focal");
-    SIMULI_REQUIRE(C.tile_px > 0 && (C.tile_px & (C.tile_px - 1)) == 0 && C.tile_px <= 32,
-                   "tile_px must be a power of two <= 32");
+    if (C.tile_px != 8 && C.tile_px != 16) {  // the camera render / backward tile shapes
+      set_error("simuli_project: camera tile_px %d not supported (8 or 16)", C.tile_px);
+      return SIMULI_ERR_UNSUPPORTED;
+    }
     SIMULI_REQUIRE(C.model == SIMULI_CAM_FISHEYE_KB || C.model == SIMULI_CAM_PINHOLE_RADTAN, "unknown camera model");
     A.cam_model = C.model; A.width = C.width; A.height = C.height; A.rolling = C.rolling_shutter;
     A.tile_px = C.tile_px; A.Wt = (C.width + C.tile_px - 1) / C.tile_px; A.Ht = (C.height + C.tile_px - 1) / C.tile_px;

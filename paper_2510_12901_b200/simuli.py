@@ -192,6 +192,14 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def _stream(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -305,6 +313,7 @@ def simuli_backward(frame, grads, stream=None, use_forward_totals=True):
         fwd = [None, None, None]
     out, gin, gout = _grad_structs(frame, grads, names, LidarGradIn if lidar else CameraGradIn, fwd)
     ws = frame._bwd_workspace()
+    frame._on_stream(stream, ws, *out.values())
     fn = load().simuli_backward_lidar if lidar else load().simuli_backward_camera
     _check(fn(C.byref(frame.gauss), C.byref(frame.projected), _ptr(frame.sorted_ids), _ptr(frame.tile_ranges),
               _ptr(frame.tile_order), C.byref(frame.params), C.byref(frame.rparams), C.byref(gin), C.byref(gout), _ptr(ws), ws.numel(),
@@ -359,6 +368,9 @@ class _Frame:
         self.tile_ranges = torch.empty((n_tiles, 2), dtype=torch.int32, device=dev)
         self.tile_order = torch.empty(n_tiles, dtype=torch.int32, device=dev)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=dev)
+        # running maximum of the pair count over asynchronous bin_sort calls (device-side,
+        # updated on the call's stream); check_capacity() compares it with the capacity
+        self.max_pairs = torch.zeros(1, dtype=torch.int64, device=dev)
         self.projected = Projected(_ptr(self.record), _ptr(self.tile_rect), _ptr(self.depth_key),
                                    _ptr(self.tile_count))
         self.set_capacity(capacity)
@@ -371,6 +383,32 @@ class _Frame:
         self.sorted_ids = torch.empty(capacity, dtype=torch.int32, device=self.device)
         ws = simuli_bin_sort_workspace_size(self.n, capacity, self.n_tiles)
         self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        if getattr(self, "max_pairs", None) is not None:
+            self.max_pairs.zero_()
+
+    def _on_stream(self, stream, *tensors):
+        """Tensors allocated on the current torch stream but used by kernels enqueued on
+        `stream`: tell the caching allocator (record_stream) so their memory is not reused
+        by current-stream work before `stream` has finished with it."""
+        if stream is None:
+            return
+        import torch
+        st = stream if isinstance(stream, torch.cuda.Stream) else None
+        if st is None or st == torch.cuda.current_stream(self.device):
+            return
+        for t in tensors:
+            if t is not None:
+                t.record_stream(st)
+
+    def check_capacity(self):
+        """Raise if any asynchronous bin_sort since the last set_capacity() had more pairs
+        than the capacity (its tile lists were truncated; simuli.h: simuli_bin_sort).
+        Synchronises with the device."""
+        mp = int(self.max_pairs.item())
+        if mp > self.capacity:
+            raise SimuliError(2, f"bin_sort: {mp} pairs exceeded the pair capacity {self.capacity}: outputs of "
+                                 f"that frame are incomplete; call set_capacity() or bin_sort(sync_capacity=True)")
+        return mp
 
     def project(self, stream=None):
         simuli_project(self.gauss, self.params, self.projected, stream)
@@ -389,7 +427,10 @@ class _Frame:
         return self._bws
 
     def backward(self, grads, stream=None, use_forward_totals=True):
-        """Gradients of the particle parameters from upstream output gradients (A31)."""
+        """Gradients of the particle parameters from upstream output gradients (A31).
+        Checks first that no asynchronous bin_sort overflowed its pair capacity (one
+        device sync): gradients of a truncated forward would be silently wrong."""
+        self.check_capacity()
         return simuli_backward(self, grads, stream, use_forward_totals)
 
     keep_keys = True  # also write the u64 (tile | depth) keys (tests); the renderer needs only ids
@@ -408,6 +449,12 @@ class _Frame:
                                    -self.capacity, keys, self.sorted_ids, self.tile_ranges,
                                    self.n_pairs, stream, self.tile_order)
             assert need is None
+        self._on_stream(stream, self.sorted_keys, self.sorted_ids, self.workspace)
+        if not sync_capacity:  # sticky device-side maximum, checked by check_capacity()
+            import torch
+            st = stream if isinstance(stream, torch.cuda.Stream) else None
+            with torch.cuda.stream(st) if st is not None else _nullctx():
+                torch.maximum(self.max_pairs, self.n_pairs, out=self.max_pairs)
 
     def set_poses(self, pose_start, pose_end):
         self.params.pose_start = make_pose(pose_start)

@@ -1,4 +1,4 @@
-"""Multi-rank host logic on CPU (gloo, world size 2; -m "not gpu").
+"""Multi-rank host logic on CPU (gloo, world sizes 2 and 3 with uneven shards; -m "not gpu").
 
 The GPU path shards independent scans round-robin with no data-path collective
 (SURVEY §8(e)); here each rank renders its shard of tiny scans with the CPU oracle as the
@@ -38,8 +38,14 @@ def _worker(rank, world, port, q):
         full = batch.gather_frames(local, N_SCANS)
         tmax = batch.reduce_max(10.0 + rank)
         csum = batch.reduce_sum({"scans": len(mine), "rank1": rank})
+        # bench.py's spot-check gather: frame j owned by rank spot[j] mod world, ranks that
+        # own none contribute an empty (zero-padded) buffer shaped like `like`
+        spot = [1, 5]
+        own = lambda j: spot[j] % world  # noqa: E731
+        sl = {j: torch.full((3,), float(spot[j]) + 0.5) for j in range(len(spot)) if own(j) == rank}
+        sfull = batch.gather_frames(sl, len(spot), owner=own, like=torch.empty(3))
         if rank == 0:
-            q.put(({i: v.numpy() for i, v in full.items()}, tmax, csum))
+            q.put(({i: v.numpy() for i, v in full.items()}, tmax, csum, {j: v.numpy() for j, v in sfull.items()}))
     finally:
         dist.destroy_process_group()
 
@@ -60,19 +66,21 @@ def test_shard_indices_partition():
         batch.shard_indices(4, 2, 2)
 
 
-def test_gloo_world2_gather_equals_single_rank():
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_gather_equals_single_rank(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    full, tmax, csum = q.get(timeout=300)
+    full, tmax, csum, sfull = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert tmax == 11.0
-    assert csum == {"scans": N_SCANS, "rank1": 1}
+    assert tmax == 10.0 + world - 1
+    assert csum == {"scans": N_SCANS, "rank1": sum(range(world))}
+    assert sorted(sfull) == [0, 1] and sfull[0].tolist() == [1.5] * 3 and sfull[1].tolist() == [5.5] * 3
     assert sorted(full) == list(range(N_SCANS))
     for i in range(N_SCANS):
         assert np.array_equal(full[i], _render(i).numpy())
