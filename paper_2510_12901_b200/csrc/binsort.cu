@@ -16,15 +16,17 @@
 //                   map of (tile, depth bits) -- plus the digit histograms of every pass
 //   k_onesweep x 6  stable LSD onesweep, 8-bit digits; passes beyond the device-side pass
 //                   count exit at once (buffer parity is chosen on the device so the
-//                   last real pass lands in the caller's arrays).  Per 3072-key partition
-//                   a warp-level ballot multisplit ranks the keys, a decoupled look-back
+//                   last real pass lands in the caller's arrays).  Per 6144-key partition
+//                   (512 threads x 12 keys) a warp-level multisplit (ballot-built peer
+//                   masks) ranks the keys, the partition publishes its digit counts, stages
+//                   its keys in digit order in shared memory, then a decoupled look-back
 //                   over partitions (dynamic partition ids for forward progress) yields
-//                   the global digit offsets, keys are staged in shared memory in digit
-//                   order and written out coalesced.
+//                   the global digit offsets and the keys are written out coalesced.
 //   k_ranges        [begin, end) per tile from tile changes of the sorted keys
 //   k_tile_order    longest-first tile order
 //   [k_keys64]      the u64 (tile << 32 | depth bits) keys, only if the caller wants them
 #include <cstdint>
+#include <cstdlib>
 
 #include "abi_util.h"
 #include "common.cuh"
@@ -39,7 +41,7 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = 12;
 constexpr int kLookW = 8;      // look-back window (predecessor partitions loaded per round trip)
 constexpr int kRankBatch = 4;  // ranking items whose match.any latencies overlap
-constexpr int kPart = kSortThreads * kSortItems;
+constexpr int kPart = kSortThreads * kSortItems;  // smallest partition of any sweep shape (status rows)
 constexpr int kMaxPasses = 6;  // 48 key bits: 16 tile bits + 32 depth bits at most
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
@@ -371,27 +373,89 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <bool Packed>
-__global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A) {
-  __shared__ uint32_t s_part;
-  __shared__ uint32_t s_warp_hist[8][256];
-  __shared__ uint32_t s_digit_excl[256];
-  __shared__ uint32_t s_global[256];
-  __shared__ uint64_t s_keys[kPart];
-  __shared__ uint32_t s_vals[Packed ? 1 : kPart];
-  __shared__ int scratch[8];
+#ifdef SIMULI_SORT_PROFILE
+// profiling builds only: per (pass, partition) globaltimer stamps: start, keys loaded,
+// ranked, aggregate published, look-back done, end; [6] = look-back rounds (max over digits)
+__device__ long long g_sort_prof[kMaxPasses][4096][8];
+__device__ __forceinline__ long long sort_gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SORT_STAMP(i) if (tid == 0 && part < 4096) g_sort_prof[A.pass][part][i] = sort_gtime()
+#else
+#define SORT_STAMP(i)
+#endif
+
+// lanes of the warp holding the same 8-bit digit: the AND over the digit's bits of the
+// bit's ballot (or its complement) -- 8 ballots instead of one match.any, whose cost grows
+// with the number of distinct values in the warp (measured: ~5 us per 3072-key partition
+// with random digits, vs ~2 us with a few distinct values)
+__device__ __forceinline__ uint32_t warp_peers8(uint32_t dg) {
+  uint32_t m = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, (dg >> b) & 1u);
+    m &= ((dg >> b) & 1u) ? bal : ~bal;
+  }
+  return m;
+}
+
+// exclusive scan of one value per thread over an NT-thread block (NT / 32 <= 32 warps)
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int* scratch, int* total) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int inc = warp_incl_scan(v);
+  if (lane == 31) scratch[warp] = inc;
+  __syncthreads();
+  int wpre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const int s = scratch[w];
+    if (w < warp) wpre += s;
+    tot += s;
+  }
+  __syncthreads();
+  *total = tot;
+  return wpre + inc - v;
+}
+
+// One onesweep pass: NT threads x ITEMS keys per partition; the 256 digit threads look
+// back LOOKW predecessor partitions per round trip.
+template <bool Packed, int NT, int ITEMS>
+struct SweepSmem {
+  uint32_t warp_hist[NT / 32][256];
+  uint32_t digit_excl[256];
+  uint32_t global[256];
+  uint64_t keys[NT * ITEMS];
+  uint32_t vals[Packed ? 1 : NT * ITEMS];
+  int scratch[32];
+  uint32_t part;
+};
+
+template <bool Packed, int NT, int ITEMS, int LOOKW, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
+  constexpr int NW = NT / 32;
+  constexpr int PART = NT * ITEMS;
+  extern __shared__ __align__(16) unsigned char sweep_smem[];
+  SweepSmem<Packed, NT, ITEMS>& S = *reinterpret_cast<SweepSmem<Packed, NT, ITEMS>*>(sweep_smem);
   const int passes = (int)A.scal[S_PASSES];
   if (A.pass >= passes) return;  // grid-uniform: this digit is beyond the key width
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t P = min(A.scal[S_P], A.capacity);
-  const int64_t n_parts = (P + kPart - 1) / kPart;
+  const int64_t n_parts = (P + PART - 1) / PART;
   // the grid is sized for the capacity; exactly the first n_parts CTAs take a partition
   // number from the counter, so every partition is claimed once
   if ((int64_t)blockIdx.x >= n_parts) return;
-  if (tid == 0) s_part = atomicAdd(A.counter, 1u);
-  for (int i = tid; i < 8 * 256; i += kSortThreads) (&s_warp_hist[0][0])[i] = 0;
+  if (tid == 0) S.part = atomicAdd(A.counter, 1u);
+  for (int i = tid; i < NW * 256; i += NT) (&S.warp_hist[0][0])[i] = 0;
   __syncthreads();
-  const int64_t part = s_part;
+  const int64_t part = S.part;
+#ifdef SIMULI_SORT_PROFILE
+  long long t_start = sort_gtime();
+  if (tid == 0 && part < 4096) g_sort_prof[A.pass][part][0] = t_start;
+#endif
   const int in = ((passes & 1) + A.pass) & 1;
   // selects, not A.keys[in]: a dynamic index into the parameter struct would copy it to
   // local memory
@@ -401,15 +465,15 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A)
   uint32_t* vals_out = in ? A.vals[0] : A.vals[1];
   const int shift = 8 * A.pass + (Packed ? A.id_bits : 0);
   const bool last = A.pass == passes - 1;
-  const int64_t base = part * kPart;
-  const int valid = (int)min((int64_t)kPart, P - base);
+  const int64_t base = part * PART;
+  const int valid = (int)min((int64_t)PART, P - base);
 
-  uint64_t k[kSortItems];
-  uint32_t v[kSortItems];
-  uint32_t rank[kSortItems];
-  const int64_t wbase = base + warp * (32 * kSortItems);
+  uint64_t k[ITEMS];
+  uint32_t v[ITEMS];
+  uint32_t rank[ITEMS];
+  const int64_t wbase = base + warp * (32 * ITEMS);
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = wbase + i * 32 + lane;
     if (idx < P) {
       k[i] = keys_in[idx];
@@ -420,22 +484,32 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A)
     }
   }
   const uint32_t lt_mask = (1u << lane) - 1u;
+#ifdef SIMULI_SORT_PROFILE
+  {
+    uint64_t x = 0;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) x ^= k[i];
+    if (x == 0x123456789ull) S.part = 0;  // forces the loads to complete before the stamp
+  }
+  __syncthreads();
+  SORT_STAMP(1);
+#endif
   // warp multisplit: lanes with equal digits (match.any), the highest of them bumps the
   // warp's digit counter once and broadcasts the previous value.  Items go in batches of
   // kRankBatch so the match latencies overlap; the counter updates stay in item order
   // (one warp's shared-memory atomics execute in program order), which keeps the sort stable.
 #pragma unroll
-  for (int i0 = 0; i0 < kSortItems; i0 += kRankBatch) {
+  for (int i0 = 0; i0 < ITEMS; i0 += kRankBatch) {
     uint32_t peers[kRankBatch], dg[kRankBatch], prev[kRankBatch];
 #pragma unroll
     for (int j = 0; j < kRankBatch; ++j) {
       dg[j] = (uint32_t)(k[i0 + j] >> shift) & 0xFFu;
-      peers[j] = __match_any_sync(0xffffffffu, dg[j]);
+      peers[j] = warp_peers8(dg[j]);
     }
 #pragma unroll
     for (int j = 0; j < kRankBatch; ++j) {
       prev[j] = 0;
-      if (lane == 31 - __clz(peers[j])) prev[j] = atomicAdd(&s_warp_hist[warp][dg[j]], (uint32_t)__popc(peers[j]));
+      if (lane == 31 - __clz(peers[j])) prev[j] = atomicAdd(&S.warp_hist[warp][dg[j]], (uint32_t)__popc(peers[j]));
     }
 #pragma unroll
     for (int j = 0; j < kRankBatch; ++j) {
@@ -444,68 +518,131 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const SweepArgs A)
     }
   }
   __syncthreads();
-  const int d = tid;
+  SORT_STAMP(2);
+  // digit threads (tid < 256): per-warp exclusive offsets, the partition's digit counts
+  const int d = tid & 255;
   uint32_t run = 0;
+  if (tid < 256) {
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    const uint32_t c = s_warp_hist[w][d];
-    s_warp_hist[w][d] = run;
-    run += c;
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t c = S.warp_hist[w][d];
+      S.warp_hist[w][d] = run;
+      run += c;
+    }
   }
-  const uint32_t pad = (uint32_t)(kPart - valid);
+  const uint32_t pad = (uint32_t)(PART - valid);
   const uint32_t cnt_pub = run - (d == 255 ? pad : 0u);
   uint32_t* st = A.status + part * 256 + d;
-  if (part == 0) st_relaxed(st, kFlagInc | cnt_pub);
-  else st_relaxed(st, kFlagAgg | cnt_pub);
+  if (tid < 256) {
+    if (part == 0) st_relaxed(st, kFlagInc | cnt_pub);
+    else st_relaxed(st, kFlagAgg | cnt_pub);
+  }
+  SORT_STAMP(3);
   int tot;
-  s_digit_excl[d] = (uint32_t)block_excl_scan256((int)run, scratch, &tot);
+  const uint32_t dex = (uint32_t)block_excl_scan<NT>(tid < 256 ? (int)run : 0, S.scratch, &tot);
+  if (tid < 256) S.digit_excl[d] = dex;
   int htot;
-  const int hex = block_excl_scan256((int)A.hist[d], scratch, &htot);
-  uint32_t excl = 0;
-  if (part > 0) {
-    // windowed look-back: kLookW predecessors are loaded at once (independent loads, one
-    // round trip), then consumed in order up to the first inclusive prefix or the first
-    // partition that has not published yet (retried from there)
-    int64_t p = part - 1;
-    while (true) {
-      uint32_t s[kLookW];
+  const int hex = block_excl_scan<NT>(tid < 256 ? (int)A.hist[d] : 0, S.scratch, &htot);
+  // keys staged in digit order in shared memory while the predecessors publish (the
+  // scatter needs only partition-local offsets; block_excl_scan's barrier made digit_excl
+  // visible)
 #pragma unroll
-      for (int w = 0; w < kLookW; ++w) s[w] = (p - w >= 0) ? ld_relaxed(A.status + (p - w) * 256 + d) : 0u;
-      int adv = 0;
-      bool done = false;
-#pragma unroll
-      for (int w = 0; w < kLookW; ++w) {
-        if (adv == w && !done) {
-          const uint32_t f = s[w] & ~kValMask;
-          if (f != 0) {
-            excl += s[w] & kValMask;
-            ++adv;
-            done = (f == kFlagInc);
-          }
-        }
-      }
-      if (done) break;
-      p -= adv;
-    }
-    st_relaxed(st, kFlagInc | (excl + cnt_pub));
-  }
-  s_global[d] = (uint32_t)hex + excl;
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const uint32_t dd = (uint32_t)(k[i] >> shift) & 0xFFu;
-    const uint32_t pos = s_digit_excl[dd] + s_warp_hist[warp][dd] + rank[i];
-    s_keys[pos] = k[i];
-    if (!Packed) s_vals[pos] = v[i];
+    const uint32_t pos = S.digit_excl[dd] + S.warp_hist[warp][dd] + rank[i];
+    S.keys[pos] = k[i];
+    if (!Packed) S.vals[pos] = v[i];
+  }
+  if (tid < 256) {
+    uint32_t excl = 0;
+    if (part > 0) {
+      // windowed look-back: LOOKW predecessors are loaded at once (independent loads, one
+      // round trip), then consumed in order up to the first inclusive prefix or the first
+      // partition that has not published yet (retried from there, after a short sleep so
+      // the spinning digit threads leave the issue slots to the SM's other partitions)
+      int64_t p = part - 1;
+      while (true) {
+        uint32_t sv[LOOKW];
+#pragma unroll
+        for (int w = 0; w < LOOKW; ++w) sv[w] = (p - w >= 0) ? ld_relaxed(A.status + (p - w) * 256 + d) : 0u;
+        int adv = 0;
+        bool done = false, blocked = false;
+#pragma unroll
+        for (int w = 0; w < LOOKW; ++w) {
+          const uint32_t f = sv[w] & ~kValMask;
+          const bool take = !done && !blocked && f != 0;
+          blocked = blocked || (!done && f == 0);
+          excl += take ? (sv[w] & kValMask) : 0u;
+          adv += take ? 1 : 0;
+          done = done || (take && f == kFlagInc);
+        }
+        if (done) break;
+        p -= adv;
+        if (blocked) __nanosleep(64);
+      }
+      st_relaxed(st, kFlagInc | (excl + cnt_pub));
+    }
+    S.global[d] = (uint32_t)hex + excl;
   }
   __syncthreads();
-  for (int j = tid; j < valid; j += kSortThreads) {
-    const uint64_t key = s_keys[j];
+  SORT_STAMP(4);
+  for (int j = tid; j < valid; j += NT) {
+    const uint64_t key = S.keys[j];
     const uint32_t dd = (uint32_t)(key >> shift) & 0xFFu;
-    const int64_t out = (int64_t)s_global[dd] + (j - (int64_t)s_digit_excl[dd]);
+    const int64_t out = (int64_t)S.global[dd] + (j - (int64_t)S.digit_excl[dd]);
     keys_out[out] = key;
-    if (!Packed) vals_out[out] = s_vals[j];
+    if (!Packed) vals_out[out] = S.vals[j];
     else if (last) A.ids_final[out] = (uint32_t)(key & ((1ull << A.id_bits) - 1ull));
+  }
+#ifdef SIMULI_SORT_PROFILE
+  __syncthreads();
+  SORT_STAMP(5);
+  if (tid == 0 && part < 4096) g_sort_prof[A.pass][part][7] = 1;
+#endif
+}
+
+// pass launcher: sweep shape (threads, items, look-back window); the default and the
+// tuning variants (SIMULI_SORT_VARIANT = NT * 10000 + ITEMS * 100 + LOOKW)
+template <bool Packed, int NT, int ITEMS, int LOOKW, int MINB = 1024 / NT>
+void launch_sweep(const SweepArgs& S, int64_t cap, cudaStream_t st) {
+  constexpr int PART = NT * ITEMS;
+  constexpr size_t smem = sizeof(SweepSmem<Packed, NT, ITEMS>);
+  static bool once = [] {
+    cudaFuncSetAttribute(k_onesweep<Packed, NT, ITEMS, LOOKW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    return true;
+  }();
+  (void)once;
+  const unsigned grid = (unsigned)((cap + PART - 1) / PART);
+  if (grid > 0) k_onesweep<Packed, NT, ITEMS, LOOKW, MINB><<<grid, NT, smem, st>>>(S);
+}
+
+template <bool Packed>
+void launch_sweep_variant(const SweepArgs& S, int64_t cap, cudaStream_t st) {
+  static const int variant = [] {
+    const char* v = getenv("SIMULI_SORT_VARIANT");
+    return v ? atoi(v) : 0;
+  }();
+  switch (variant) {
+    case 2561216: launch_sweep<Packed, 256, 12, 16>(S, cap, st); break;
+    case 2561232: launch_sweep<Packed, 256, 12, 32>(S, cap, st); break;
+    case 2561233: launch_sweep<Packed, 256, 12, 32, 3>(S, cap, st); break;
+    case 2561633: launch_sweep<Packed, 256, 16, 32, 3>(S, cap, st); break;
+    case 2561616: launch_sweep<Packed, 256, 16, 16>(S, cap, st); break;
+    case 2561632: launch_sweep<Packed, 256, 16, 32>(S, cap, st); break;
+    case 2562432: launch_sweep<Packed, 256, 24, 32>(S, cap, st); break;
+    case 5121232: launch_sweep<Packed, 512, 12, 32>(S, cap, st); break;
+    case 5121208: launch_sweep<Packed, 512, 12, 8>(S, cap, st); break;
+    case 5121216: launch_sweep<Packed, 512, 12, 16>(S, cap, st); break;
+    case 2562408: launch_sweep<Packed, 256, 24, 8, 3>(S, cap, st); break;
+    case 2561608: launch_sweep<Packed, 256, 16, 8>(S, cap, st); break;
+    case 10241208: launch_sweep<Packed, 1024, 12, 8>(S, cap, st); break;
+    case 10241216: launch_sweep<Packed, 1024, 12, 16>(S, cap, st); break;
+    case 5121632: launch_sweep<Packed, 512, 16, 32>(S, cap, st); break;
+    case 2561208: launch_sweep<Packed, 256, 12, 8>(S, cap, st); break;
+    // default: 512 x 12 keys (6144 per partition, half the look-back chain of 3072-key
+    // partitions): config-B bin_sort 201.6 -> 190.0 us (L2 warm)
+    default: launch_sweep<Packed, 512, kSortItems, kLookW>(S, cap, st); break;
   }
 }
 
@@ -642,8 +779,8 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     for (int p = 0; p < max_passes; ++p) {
       SweepArgs S{{w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.scal, cap, p, id_bits, sorted_ids,
                   w.hist + p * 256, w.status + (size_t)p * w.parts * 256, w.counters + p};
-      if (packed) k_onesweep<true><<<(unsigned)w.parts, kSortThreads, 0, st>>>(S);
-      else k_onesweep<false><<<(unsigned)w.parts, kSortThreads, 0, st>>>(S);
+      if (packed) launch_sweep_variant<true>(S, cap, st);
+      else launch_sweep_variant<false>(S, cap, st);
     }
     if (int32_t e = check("onesweep")) return e;
   }
@@ -657,3 +794,10 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
   if (sorted_keys && cap > 0) k_keys64<<<148 * 4, 256, 0, st>>>(w.keys[0], w.scal, cap, key_shift, sorted_keys);
   return check("tile metadata");
 }
+
+#ifdef SIMULI_SORT_PROFILE
+extern "C" int32_t simuli_debug_sort_prof(long long* host) {
+  return cudaMemcpyFromSymbol(host, simuli::g_sort_prof, sizeof(long long) * simuli::kMaxPasses * 4096 * 8) ==
+                 cudaSuccess ? 0 : 3;
+}
+#endif
