@@ -485,12 +485,17 @@ __device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3],
   return valid;
 }
 
+#ifndef SIMULI_PROJ_MINB
+#define SIMULI_PROJ_MINB 4
+#endif
+#ifndef SIMULI_PROJ_THREADS
+#define SIMULI_PROJ_THREADS 256
+#endif
 constexpr double kPiD = 3.141592653589793;
 constexpr int kSmemBounds = 264;
-constexpr int kShSmem = 8 * 12 * 32 * 16;
 
 template <int KIND, bool DIV, bool ACT>
-__global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
+__global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_project(const ProjArgs Ain) {
   // tiling boundaries / row scales staged in shared memory (binary searches hit smem)
   __shared__ float s_bounds[kSmemBounds], s_rscale[kSmemBounds];
   ProjArgs A = Ain;
@@ -503,37 +508,13 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
     A.bounds = s_bounds;
     A.row_scale = s_rscale;
   }
-  // degree-3 SH of the warp's 32 particles (32 x 192 B contiguous) staged into shared memory
-  // by coalesced 16-byte cp.async at kernel start, overlapping the projection arithmetic;
-  // layout [chunk][particle] so each lane's later reads are conflict-free
-  extern __shared__ float4 s_sh_raw[];  // [8 warps][12 chunks][32 lanes] (48 KB, dynamic)
-  float4 (*s_sh)[12][32] = reinterpret_cast<float4 (*)[12][32]>(s_sh_raw);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool stage_sh = A.sh_degree == 3;
-  // ---- loads first (SoA; quaternion as one 16-byte load): their latency overlaps the SH
-  // staging below (lanes past n read particle n - 1 and return after the staging)
-  const int64_t gl = g < A.n ? g : A.n - 1;
-  float mu[3] = {__ldg(A.means + 3 * gl), __ldg(A.means + 3 * gl + 1), __ldg(A.means + 3 * gl + 2)};
-  float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + gl);
-  const float sc[3] = {__ldg(A.scales + 3 * gl), __ldg(A.scales + 3 * gl + 1), __ldg(A.scales + 3 * gl + 2)};
-  const float sigma = __ldg(A.opacity + gl);
-  if (stage_sh) {
-    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + wid * 32;
-    const float4* src = reinterpret_cast<const float4*>(A.sh) + g0 * 12;
-    for (int j = lane; j < 32 * 12; j += 32) {
-      const int p = j / 12, c = j - p * 12;
-      if (g0 + p < A.n) {
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(&s_sh[wid][c][p]));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src + j) : "memory");
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  if (g >= A.n) {
-    if (stage_sh) asm volatile("cp.async.wait_group 0;" ::: "memory");
-    return;
-  }
+  if (g >= A.n) return;
+  // SoA loads (quaternion as one 16-byte load)
+  float mu[3] = {__ldg(A.means + 3 * g), __ldg(A.means + 3 * g + 1), __ldg(A.means + 3 * g + 2)};
+  float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + g);
+  const float sc[3] = {__ldg(A.scales + 3 * g), __ldg(A.scales + 3 * g + 1), __ldg(A.scales + 3 * g + 2)};
+  const float sigma = __ldg(A.opacity + g);
   bool actor_ok = true;
   if (ACT) {
     // scene graph (A29): object particle -> world with its object's pose at t;
@@ -744,11 +725,14 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
 #pragma unroll
         for (int i = 0; i < 9; ++i) M[i] = Mh[i];
       } else {
+        // R recomputed from the normalised quaternion (not kept live through the UT: registers)
+        float Rm[9];
+        quat_rot(q, Rm);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           const float is = 1.0f / sc[k];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) M[3 * k + c] = R[3 * c + k] * is;
+          for (int c = 0; c < 3; ++c) M[3 * k + c] = Rm[3 * c + k] * is;
         }
       }
       float Rs[9], ts[3];
@@ -764,21 +748,11 @@ __global__ void __launch_bounds__(256, 3) k_project(const ProjArgs Ain) {
       const float vn = rsqrtf(vx * vx + vy * vy + vz * vz);
       vx *= vn; vy *= vn; vz *= vn;
       if (isfinite(vn)) {
-        if (stage_sh) {
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-          // coefficients streamed from shared memory one float4 at a time (coefficient
-          // i = 4c + j belongs to basis function i / 3, channel i % 3)
+        // the SH block (192 B, degree 3) is read only for kept particles (A17): 12 float4
+        if (A.sh_degree == 3) {
           float bsh[16];
           sh_basis3(vx, vy, vz, bsh);
-          float acc[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-          for (int c = 0; c < 12; ++c) {
-            const float4 v4 = s_sh[wid][c][lane];
-            const float v[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[(4 * c + j) % 3] = fmaf(bsh[(4 * c + j) / 3], v[j], acc[(4 * c + j) % 3]);
-          }
-          f[0] = acc[0]; f[1] = acc[1]; f[2] = acc[2];
+          sh_dot(A.sh + g * 48, 16, bsh, f);
         } else {
           sh_eval(A.sh + g * A.n_coef * 3, A.sh_degree, vx, vy, vz, f);
         }
@@ -827,8 +801,7 @@ static void depth_origin(const simuli_pose& a, const simuli_pose& b, float out[3
 
 template <int KIND, bool DIV, bool ACT>
 void launch_project(const ProjArgs& A, unsigned blocks, int threads, cudaStream_t st) {
-  cudaFuncSetAttribute(k_project<KIND, DIV, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kShSmem);
-  k_project<KIND, DIV, ACT><<<blocks, threads, kShSmem, st>>>(A);
+  k_project<KIND, DIV, ACT><<<blocks, threads, 0, st>>>(A);
 }
 
 }  // namespace simuli
@@ -846,6 +819,8 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
   if (G->n == 0) return SIMULI_OK;
   SIMULI_REQUIRE(G->means && G->quats && G->scales && G->opacity && G->sh, "simuli_project: NULL Gaussian array");
   SIMULI_REQUIRE(out->record && out->tile_rect && out->depth_key && out->tile_count, "simuli_project: NULL output");
+  SIMULI_REQUIRE(G->sh_degree != 3 || reinterpret_cast<uintptr_t>(G->sh) % 16 == 0,
+                 "simuli_project: sh must be 16-byte aligned for degree 3 (read as float4)");
   SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(G->quats) % 16 == 0 && reinterpret_cast<uintptr_t>(out->record) % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(out->tile_rect) % 16 == 0,
                  "simuli_project: quats / record / tile_rect must be 16-byte aligned");
@@ -874,7 +849,7 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
   A.write_all = P->write_all_records;
   A.record = out->record; A.rect = out->tile_rect; A.key = out->depth_key; A.count = out->tile_count;
   A.view_dir = out->view_dir;
-  const int threads = 256;
+  const int threads = SIMULI_PROJ_THREADS;
   const unsigned blocks = static_cast<unsigned>((G->n + threads - 1) / threads);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (P->kind == SIMULI_SENSOR_LIDAR) {
