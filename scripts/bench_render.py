@@ -24,7 +24,7 @@ for p0, p1 in poses:  # the B-batch trajectory (bench.py's workload), 10 poses a
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e3)
     per_pose.append(np.median(times[2:]))
-kind = os.environ.get("SIMULI_LIDAR_VARIANT", "default") + (" per-ray SH" if per_ray else "")
+kind = os.environ.get("SIMULI_LIDAR_RENDER", "split") + ":" + os.environ.get("SIMULI_LIDAR_VARIANT", "0") + (" per-ray SH" if per_ray else "")
 print(f"{name} render[{kind}]: mean over {len(poses)} poses {np.mean(per_pose):.1f} us  "
       f"(min {np.min(per_pose):.1f}, max {np.max(per_pose):.1f})", flush=True)
 if len(sys.argv) > 2:
