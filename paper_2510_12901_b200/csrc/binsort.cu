@@ -6,9 +6,10 @@
 // the "Sort" kernel of tab:culling.
 //
 // Launch sequence (caller's stream; no host sync when pair_capacity >= 0):
-//   k_count_reduce  per-1024-particle tile-count sums + min / max depth-key bits of the
-//                   particles that emit pairs
-//   k_count_top     exclusive scan of the block sums (1 CTA) -> P; key width
+//   memset          one: pass histograms, counters, key range, every look-back status word
+//   k_count_scan    single-pass scan of the tile counts (decoupled look-back over
+//                   1024-particle blocks) + min / max depth-key bits of the pair-emitting
+//                   particles; the last block derives P, the key width
 //                   b = bits(max - min) and the pass count ceil((b + tile bits) / 8)
 //   k_duplicate     balanced, coalesced pair emission (each thread emits pairs k = tid,
 //                   tid+256, ... binary-searching its owner in shared memory) of the
@@ -59,13 +60,15 @@ int tile_bits_of(int32_t n_tiles) {
 
 struct Workspace {
   int64_t* block_sums;  // [nb+1]
-  uint32_t* block_kmin; // [nb]
-  uint32_t* block_kmax; // [nb]
   int64_t* scal;        // [S_N]
+  // zeroed by one memset per call: zero .. zero + zero_bytes
   uint32_t* hist;       // [kMaxPasses][256]
+  uint32_t* counters;   // [kMaxPasses] sweep partition counters, [kMaxPasses..+4) scan / ranges counters
+  uint32_t* kminmax;    // [2]: ~min, max depth-key bits of the pair-emitting particles (atomicMax)
+  uint32_t* cstatus;    // [nb] look-back status of the count scan
   uint32_t* status;     // [kMaxPasses][n_parts][256]
-  uint32_t* counters;   // [kMaxPasses]
-  int32_t* tile_cnt;    // [n_tiles]
+  char* zero;
+  size_t zero_bytes;
   uint64_t* keys[2];    // [cap]
   uint32_t* vals_alt;   // [cap]
   int64_t parts;
@@ -84,13 +87,16 @@ Workspace carve(void* base, int64_t n, int64_t cap, int32_t n_tiles) {
     return r;
   };
   w.block_sums = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * (nb + 1)));
-  w.block_kmin = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (nb + 1)));
-  w.block_kmax = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (nb + 1)));
   w.scal = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * S_N));
+  const size_t z0 = off;
   w.hist = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses * 256));
-  w.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses));
+  w.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (kMaxPasses + 4)));
+  w.kminmax = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 2));
+  w.cstatus = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (nb > 0 ? nb : 1)));
   w.status = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses * (w.parts > 0 ? w.parts : 1) * 256));
-  w.tile_cnt = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * n_tiles));
+  w.zero = p ? p + z0 : nullptr;
+  w.zero_bytes = off - z0;
+  (void)n_tiles;
   for (int i = 0; i < 2; ++i) w.keys[i] = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * cap));
   w.vals_alt = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * cap));
   w.bytes = off;
@@ -127,122 +133,171 @@ __device__ __forceinline__ int block_excl_scan256(int v, int* scratch, int* tota
 }
 
 // ------------------------------------------------------------------ counts, key range
-__global__ void __launch_bounds__(kDupThreads) k_count_reduce(const int* __restrict__ count,
-                                                              const float* __restrict__ key, int64_t n,
-                                                              int64_t* __restrict__ block_sums,
-                                                              uint32_t* __restrict__ block_kmin,
-                                                              uint32_t* __restrict__ block_kmax) {
-  __shared__ int scratch[8];
-  __shared__ uint32_t s_min[8], s_max[8];
-  const int64_t base = (int64_t)blockIdx.x * kDupBlock;
-  int s = 0;
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Single-pass scan of the tile counts: 1024-thread blocks of kScanPer = 8 x 1024 particles
+// (8 consecutive particles per thread, two 16-byte loads each for counts and keys), a
+// decoupled look-back over blocks (dynamic block ids for forward progress; warp 0 reads 32
+// predecessors per round trip) -> block_sums[d] = pairs emitted before duplicate block d
+// (1024 particles); min / max depth-key bits of the pair-emitting particles by atomics;
+// the block that finishes last derives P, the key width b = bits(max - min) and the pass
+// count ceil((b + tile bits) / 8).  (One kernel instead of a block reduce + a one-CTA scan.)
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;
+constexpr int kScanPer = kScanThreads * kScanItems;  // = 8 duplicate blocks
+static_assert(kScanPer % kDupBlock == 0, "scan blocks cover whole duplicate blocks");
+__global__ void __launch_bounds__(kScanThreads) k_count_scan(const int* __restrict__ count,
+                                                             const float* __restrict__ key, int64_t n, int64_t nsb,
+                                                             int64_t nb, int tile_bits, int64_t* __restrict__ block_sums,
+                                                             uint32_t* __restrict__ cstatus, uint32_t* __restrict__ kminmax,
+                                                             uint32_t* __restrict__ ctr, int64_t* __restrict__ scal,
+                                                             int64_t* __restrict__ n_pairs) {
+  constexpr int DB = kScanPer / kDupBlock;  // duplicate blocks per scan block
+  constexpr int TPD = kDupBlock / kScanItems;  // threads per duplicate block
+  __shared__ int s_wsum[32];
+  __shared__ uint32_t s_min[32], s_max[32];
+  __shared__ uint32_t s_blk, s_tot;
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_blk = atomicAdd(&ctr[0], 1u);
+  __syncthreads();
+  const int64_t blk = s_blk;
+  const int64_t g0 = blk * kScanPer + (int64_t)tid * kScanItems;
+  int sum = 0;
   uint32_t kmin = 0xffffffffu, kmax = 0u;
+  if (g0 + kScanItems <= n) {
+    const int4* c4 = reinterpret_cast<const int4*>(count + g0);
+    const uint4* k4 = reinterpret_cast<const uint4*>(key + g0);
 #pragma unroll
-  for (int i = 0; i < kDupItems; ++i) {
-    const int64_t g = base + i * kDupThreads + threadIdx.x;
-    if (g < n) {
-      const int c = __ldg(count + g);
-      s += c;
-      if (c > 0) {
-        const uint32_t kb = __float_as_uint(__ldg(key + g));
-        kmin = min(kmin, kb);
-        kmax = max(kmax, kb);
+    for (int h = 0; h < 2; ++h) {
+      const int4 c = __ldg(c4 + h);
+      const uint4 k = __ldg(k4 + h);
+      const int cc[4] = {c.x, c.y, c.z, c.w};
+      const uint32_t kk[4] = {k.x, k.y, k.z, k.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        sum += cc[j];
+        if (cc[j] > 0) {
+          kmin = min(kmin, kk[j]);
+          kmax = max(kmax, kk[j]);
+        }
+      }
+    }
+  } else {
+    for (int j = 0; j < kScanItems; ++j) {
+      const int64_t g = g0 + j;
+      if (g < n) {
+        const int c = __ldg(count + g);
+        sum += c;
+        if (c > 0) {
+          const uint32_t kb = __float_as_uint(__ldg(key + g));
+          kmin = min(kmin, kb);
+          kmax = max(kmax, kb);
+        }
       }
     }
   }
+  int ws = sum;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    s_min[threadIdx.x >> 5] = kmin;
-    s_max[threadIdx.x >> 5] = kmax;
-  }
-  int tot;
-  block_excl_scan256(s, scratch, &tot);
-  if (threadIdx.x == 0) {
-    block_sums[blockIdx.x] = tot;
-    for (int w = 0; w < 8; ++w) {
-      kmin = min(kmin, s_min[w]);
-      kmax = max(kmax, s_max[w]);
-    }
-    block_kmin[blockIdx.x] = kmin;
-    block_kmax[blockIdx.x] = kmax;
-  }
-}
-
-__global__ void __launch_bounds__(1024) k_count_top(int64_t* __restrict__ block_sums,
-                                                    const uint32_t* __restrict__ block_kmin,
-                                                    const uint32_t* __restrict__ block_kmax, int64_t nb,
-                                                    int tile_bits, int64_t* __restrict__ scal,
-                                                    int64_t* __restrict__ n_pairs, uint32_t* __restrict__ hist,
-                                                    uint32_t* __restrict__ counters, int32_t* __restrict__ tile_cnt,
-                                                    int n_tiles) {
-  __shared__ int64_t warp_tot[32];
-  __shared__ uint32_t w_min[32], w_max[32];
-  __shared__ int64_t carry;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = 0;
-  for (int i = threadIdx.x; i < kMaxPasses * 256; i += blockDim.x) hist[i] = 0;
-  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) tile_cnt[i] = 0;
-  if (threadIdx.x < kMaxPasses) counters[threadIdx.x] = 0;
-  uint32_t kmin = 0xffffffffu, kmax = 0u;
-  __syncthreads();
-  for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
-    const int64_t i = b0 + threadIdx.x;
-    int64_t v = 0;
-    if (i < nb) {
-      v = block_sums[i];
-      kmin = min(kmin, block_kmin[i]);
-      kmax = max(kmax, block_kmax[i]);
-    }
-    int64_t inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    if (lane == 31) warp_tot[warp] = inc;
-    __syncthreads();
-    int64_t wpre = 0, tot = 0;
-    for (int w = 0; w < 32; ++w) {
-      const int64_t x = warp_tot[w];
-      wpre += (w < warp) ? x : 0;
-      tot += x;
-    }
-    if (i < nb) block_sums[i] = carry + wpre + inc - v;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+    ws += __shfl_xor_sync(0xffffffffu, ws, o);
     kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
     kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
   }
   if (lane == 0) {
-    w_min[warp] = kmin;
-    w_max[warp] = kmax;
+    s_wsum[warp] = ws;
+    s_min[warp] = kmin;
+    s_max[warp] = kmax;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < 32; ++w) {
-      kmin = min(kmin, w_min[w]);
-      kmax = max(kmax, w_max[w]);
+  if (warp == 0) {
+    // block total and range, published as an aggregate at once
+    int t = s_wsum[lane];
+    uint32_t mn = s_min[lane], mx = s_max[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    block_sums[nb] = carry;
-    *n_pairs = carry;
-    int b = 0;
-    if (carry > 0 && kmax > kmin) b = 32 - __clz(kmax - kmin);
-    if (carry == 0) kmin = 0;
-    scal[S_P] = carry;
-    scal[S_KMIN] = kmin;
-    scal[S_KMAX] = kmax;
-    scal[S_B] = b;
-    // at least one pass whenever there are pairs: it also writes the ids
-    scal[S_PASSES] = carry > 0 ? max(1, (b + tile_bits + 7) / 8) : 0;
+    if (lane == 0) {
+      st_relaxed(cstatus + blk, (blk == 0 ? kFlagInc : kFlagAgg) | (uint32_t)t);
+      if (mx >= mn) {
+        atomicMax(&kminmax[0], ~mn);
+        atomicMax(&kminmax[1], mx);
+      }
+    }
+    // look-back: 32 predecessors per round trip, summed up to the first inclusive prefix
+    // (or up to the first block that has not published, retried from there)
+    uint32_t excl = 0;
+    int64_t p = blk - 1;
+    while (p >= 0) {
+      const int64_t q = p - lane;
+      const uint32_t v = q >= 0 ? ld_relaxed(cstatus + q) : kFlagInc;
+      const uint32_t f = v & ~kValMask;
+      const uint32_t unpub = __ballot_sync(0xffffffffu, f == 0), inc = __ballot_sync(0xffffffffu, f == kFlagInc);
+      const int fu = unpub ? __ffs(unpub) - 1 : 32, fi = inc ? __ffs(inc) - 1 : 32;
+      const int upto = fi < fu ? fi + 1 : fu;  // lanes [0, upto) are consumed
+      uint32_t x = lane < upto ? (v & kValMask) : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      excl += x;
+      if (fi < fu) break;
+      p -= upto;
+      if (upto == 0) __nanosleep(32);
+    }
+    if (lane == 0) {
+      if (blk > 0) st_relaxed(cstatus + blk, kFlagInc | (excl + (uint32_t)t));
+      s_tot = excl;
+    }
+  }
+  __syncthreads();
+  // per duplicate block d of this scan block: exclusive prefix of the warp sums
+  if (tid < DB) {
+    uint32_t pre = s_tot;
+    for (int d = 0; d < tid; ++d)
+      for (int w = 0; w < TPD / 32; ++w) pre += (uint32_t)s_wsum[d * (TPD / 32) + w];
+    const int64_t db = blk * DB + tid;
+    if (db < nb) block_sums[db] = pre;
+  }
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(&ctr[1], 1u) == (uint32_t)(nsb - 1);
+  }
+  __syncthreads();
+  if (!s_last || tid != 0) return;
+  // the last block: every block has published its inclusive prefix and key range
+  __threadfence();
+  const int64_t P = (int64_t)(ld_relaxed(cstatus + nsb - 1) & kValMask);
+  uint32_t mn = ~ld_relaxed(&kminmax[0]), mx = ld_relaxed(&kminmax[1]);
+  block_sums[nb] = P;
+  *n_pairs = P;
+  int b = 0;
+  if (P > 0 && mx > mn) b = 32 - __clz(mx - mn);
+  if (P == 0) mn = 0;
+  scal[S_P] = P;
+  scal[S_KMIN] = mn;
+  scal[S_KMAX] = mx;
+  scal[S_B] = b;
+  // at least one pass whenever there are pairs: it also writes the ids
+  scal[S_PASSES] = P > 0 ? max(1, (b + tile_bits + 7) / 8) : 0;
+  scal[S_TBITS] = tile_bits;
+}
+
+// n = 0: no pairs
+__global__ void k_count_empty(int tile_bits, int64_t* scal, int64_t* n_pairs, int64_t* block_sums) {
+  if (threadIdx.x == 0) {
+    scal[S_P] = 0; scal[S_KMIN] = 0; scal[S_KMAX] = 0; scal[S_B] = 0; scal[S_PASSES] = 0;
     scal[S_TBITS] = tile_bits;
+    *n_pairs = 0;
+    block_sums[0] = 0;
   }
 }
 
@@ -364,14 +419,6 @@ struct SweepArgs {
   uint32_t* counter;
 };
 
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 #ifdef SIMULI_SORT_PROFILE
 // profiling builds only: per (pass, partition) globaltimer stamps: start, keys loaded,
@@ -493,6 +540,7 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
   }
   __syncthreads();
   SORT_STAMP(1);
+  const long long ck_rank0 = clock64();
 #endif
   // warp multisplit: lanes with equal digits (match.any), the highest of them bumps the
   // warp's digit counter once and broadcasts the previous value.  Items go in batches of
@@ -519,6 +567,9 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
   }
   __syncthreads();
   SORT_STAMP(2);
+#ifdef SIMULI_SORT_PROFILE
+  if (tid == 0 && part < 4096) g_sort_prof[A.pass][part][6] = clock64() - ck_rank0;
+#endif
   // digit threads (tid < 256): per-warp exclusive offsets, the partition's digit counts
   const int d = tid & 255;
   uint32_t run = 0;
@@ -743,11 +794,20 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     }
     return SIMULI_OK;
   };
-  if (nb > 0)
-    k_count_reduce<<<(unsigned)nb, kDupThreads, 0, st>>>(proj->tile_count, proj->depth_key, n, w.block_sums,
-                                                          w.block_kmin, w.block_kmax);
-  k_count_top<<<1, 1024, 0, st>>>(w.block_sums, w.block_kmin, w.block_kmax, nb, tbits, w.scal, n_pairs_dev, w.hist,
-                                  w.counters, w.tile_cnt, n_tiles);
+  // one memset zeroes the pass histograms, all counters, the key range and every
+  // look-back status word (count scan and sweep passes)
+  if (cudaMemsetAsync(w.zero, 0, w.zero_bytes, st) != cudaSuccess) return check("memset workspace");
+  uint32_t* ctr = w.counters + kMaxPasses;  // [0] scan block ids, [1] scan blocks done
+  if (nb > 0) {
+    const int64_t nsb = (n + kScanPer - 1) / kScanPer;
+    SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(proj->tile_count) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(proj->depth_key) % 16 == 0,
+                   "simuli_bin_sort: tile_count / depth_key must be 16-byte aligned");
+    k_count_scan<<<(unsigned)nsb, kScanThreads, 0, st>>>(proj->tile_count, proj->depth_key, n, nsb, nb, tbits,
+                                                         w.block_sums, w.cstatus, w.kminmax, ctr, w.scal, n_pairs_dev);
+  } else {
+    k_count_empty<<<1, 32, 0, st>>>(tbits, w.scal, n_pairs_dev, w.block_sums);
+  }
   if (int32_t e = check("scan")) return e;
   if (sync_mode) {
     int64_t P = 0;
@@ -761,9 +821,6 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     }
   }
   const int max_passes = (32 + tbits + 7) / 8;
-  if (w.parts > 0 &&
-      cudaMemsetAsync(w.status, 0, sizeof(uint32_t) * (size_t)max_passes * w.parts * 256, st) != cudaSuccess)
-    return check("memset status");
   uint32_t* vals[2] = {sorted_ids, w.vals_alt};
   // packed mode: depth-key span b <= 31 bits (positive floats), so one u64 word holds
   // (tile << b | depth - min) << id_bits | id whenever 31 + tile bits + id bits <= 64
@@ -772,7 +829,7 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
   const bool packed = 31 + tbits + id_bits <= 64;
   if (nb > 0 && cap > 0) {
     DupArgs D{proj->tile_count, reinterpret_cast<const int4*>(proj->tile_rect), proj->depth_key, n, cap,
-              w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, w.tile_cnt,
+              w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, nullptr,
               id_bits, packed ? 1 : 0};
     k_duplicate<<<(unsigned)nb, kDupThreads, 0, st>>>(D);
     if (int32_t e = check("duplicate")) return e;

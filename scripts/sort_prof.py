@@ -26,7 +26,8 @@ for ps in range(6):
     span = (q[:, 5].max() - t0) / 1e3
     ph = np.diff(q[:, :6], axis=1) / 1e3
     print(f"pass {ps}: partitions {len(q)}, span {span:.1f} us, last start {(q[:, 0].max() - t0) / 1e3:.1f} us; "
-          + ", ".join(f"{n} mean {ph[:, i].mean():.2f} max {ph[:, i].max():.2f}" for i, n in enumerate(names)))
+          + ", ".join(f"{n} mean {ph[:, i].mean():.2f} max {ph[:, i].max():.2f}" for i, n in enumerate(names))
+          + f"; rank clock64 cycles mean {q[:, 6].mean():.0f} p50 {np.median(q[:, 6]):.0f} max {q[:, 6].max():.0f}")
     order = np.argsort(q[:, 0])
     lb_end = (q[:, 4] - t0) / 1e3
     idx = np.arange(len(q))
