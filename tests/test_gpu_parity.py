@@ -199,6 +199,25 @@ def test_gpu_invariance_tiling_and_culling(SM):
             assert np.array_equal(o[k], outs[0][k]), k  # tiling "does not affect quality"
 
 
+@pytest.mark.parametrize("config", ["A", "tiny"])
+def test_gpu_single_tile_bruteforce(SM, config):
+    """GPU brute force ("does not affect quality"): one render tile holding every ray
+    (N_phi = 1, M >= all rays, so N_theta = 1) and culling off, i.e. ONE list with every valid
+    particle, tested by every ray -- bitwise equal to the default tiled, culled render."""
+    scene = S.scene_for(config, seed=5 if config == "tiny" else None)
+    cfg = S.lidar_config(config)
+    tiled = lidar_run(SM, cfg, scene)
+    one = S.lidar_config(config)
+    one.n_phi, one.max_rays_per_tile = 1, 1 << 30
+    brute = lidar_run(SM, one, scene, enable_culling=0)
+    assert brute.n_tiles == 1
+    assert int(brute.n_pairs.item()) == int((brute.tile_count > 0).sum().item())  # every valid particle, once
+    assert int(brute.n_pairs.item()) >= int((tiled.tile_count > 0).sum().item())
+    for k, v in tiled.out.items():
+        if v is not None:
+            assert torch.equal(v, brute.out[k]), k
+
+
 def test_culling_reduces_pairs(SM):
     scene = S.scene_for("B", n=300_000)
     cfg = S.lidar_config("B")
