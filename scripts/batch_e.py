@@ -59,8 +59,15 @@ for i in mine[:2]:
 torch.cuda.synchronize()
 
 
-def pack(out, keys):
-    return torch.cat([out[k].reshape(-1) for k in keys])
+def pack(out, keys, dst=None):
+    return torch.cat([out[k].reshape(-1) for k in keys], out=dst)
+
+
+# gather buffers allocated up front (an allocation inside the timed loop would synchronise)
+UNITS = max(len(batch.shard_indices(N, ws, r)) for r in range(ws))
+SIZES = {"s": pack(lids[0].out, LKEYS).numel(), "f": pack(cams[0].out, CKEYS).numel()}
+STAGE = {k: [torch.zeros(n, device=dev) for _ in range(2)] for k, n in SIZES.items()}
+GBUF = {k: torch.zeros((UNITS, ws, n), device=dev) for k, n in SIZES.items()}
 
 
 def run(gather: bool):
@@ -88,17 +95,13 @@ def run(gather: bool):
                 ev.record(main)
                 with torch.cuda.stream(side):
                     side.wait_event(ev)
-                    buf = pack(obj.out, keys) if have else torch.zeros_like(pack(obj.out, keys))
+                    buf = STAGE[kind][slot]
+                    if have:
+                        pack(obj.out, keys, buf)
                     if ws > 1:
-                        allb = torch.empty((ws,) + tuple(buf.shape), dtype=buf.dtype, device=dev)
-                        dist.all_gather_into_tensor(allb, buf)
+                        dist.all_gather_into_tensor(GBUF[kind][k], buf)
                     else:
-                        allb = buf.clone()[None]
-                    if rank == 0:
-                        for r in range(ws):
-                            idx = batch.shard_indices(N, ws, r)
-                            if k < len(idx):
-                                got[(kind, idx[k])] = allb[r]
+                        GBUF[kind][k][0].copy_(buf)
                     de = torch.cuda.Event()
                     de.record(side)
                     done[slot] = de
@@ -109,6 +112,10 @@ def run(gather: bool):
         e1.record(main)
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1))
+        if gather and rank == 0:
+            for r in range(ws):
+                for k, i in enumerate(batch.shard_indices(N, ws, r)):
+                    got[(kind, i)] = GBUF[kind][k][r]
     return res[0], res[1], got
 
 
