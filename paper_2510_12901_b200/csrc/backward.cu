@@ -134,12 +134,7 @@ __device__ __forceinline__ void walk_list(const BwdArgs& A, int2 rg, const bool&
     __syncwarp();  // the previous batch's records are no longer read
     if (i < rg.y) {
       g = __ldg(A.ids + i);
-#ifdef SIMULI_BWD_CHECK
-      if ((int64_t)g >= A.n) {
-        printf("bwd: entry %d id %u >= n %lld (range %d..%d)\n", i, g, (long long)A.n, rg.x, rg.y);
-        __trap();
-      }
-#endif
+      SIMULI_CHECK((int64_t)g < A.n, g, A.n);
       const float4* src = A.record + (size_t)g * 5;
 #pragma unroll
       for (int c = 0; c < 5; ++c) q[c] = __ldg(src + c);
@@ -259,6 +254,7 @@ __device__ __forceinline__ void bwd_grad_walk(const BwdArgs& A, const RayF& rf, 
     if (__any_sync(0xffffffffu, contributed)) {
       const float tot = warp_reduce16(v, lane);
       const int q = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+      SIMULI_CHECK((int64_t)g < A.n, g, A.n);
       if (!(lane & 1)) atomicAdd(A.ws + (size_t)g * kBwdVals + q, tot);
       if (A.sh) {  // per-ray SH: dL/dc_kc = Y_k(d) Gz_c w, summed over the warp's rays
 #pragma unroll 1

@@ -313,8 +313,9 @@ struct DupArgs {
   uint64_t* keys[2];
   uint32_t* vals[2];
   uint32_t* hist;      // [kMaxPasses][256]
-  int32_t* tile_cnt;   // [n_tiles]
+  int32_t* tile_cnt;   // unused
   int id_bits, packed; // packed: one u64 word = (key << id_bits) | id
+  int n_tiles;
 };
 
 // Warp-balanced emission: warp w of the CTA takes particles [128 w, 128 w + 128) of the
@@ -385,6 +386,8 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
       int col = rz + j % rw;
       if (col >= A.n_cols_total) col -= A.n_cols_total;
       const uint32_t tile = (uint32_t)row * (uint32_t)A.n_cols_total + (uint32_t)col;
+      SIMULI_CHECK(col >= 0 && col < A.n_cols_total && tile < (uint32_t)A.n_tiles, col, tile);
+      SIMULI_CHECK(kk < (1u << b) || b == 32 || kq == 0, kk, b);
       const uint64_t key = ((uint64_t)tile << b) | (uint64_t)kk;
       const int64_t pos = base + k;
       if (pos < A.capacity) {
@@ -601,6 +604,7 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
   for (int i = 0; i < ITEMS; ++i) {
     const uint32_t dd = (uint32_t)(k[i] >> shift) & 0xFFu;
     const uint32_t pos = S.digit_excl[dd] + S.warp_hist[warp][dd] + rank[i];
+    SIMULI_CHECK(pos < (uint32_t)PART, pos, PART);
     S.keys[pos] = k[i];
     if (!Packed) S.vals[pos] = v[i];
   }
@@ -641,6 +645,7 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
     const uint64_t key = S.keys[j];
     const uint32_t dd = (uint32_t)(key >> shift) & 0xFFu;
     const int64_t out = (int64_t)S.global[dd] + (j - (int64_t)S.digit_excl[dd]);
+    SIMULI_CHECK(out >= 0 && out < P, out, P);
     keys_out[out] = key;
     if (!Packed) vals_out[out] = S.vals[j];
     else if (last) A.ids_final[out] = (uint32_t)(key & ((1ull << A.id_bits) - 1ull));
@@ -700,11 +705,13 @@ void launch_sweep_variant(const SweepArgs& S, int64_t cap, cudaStream_t st) {
 // ------------------------------------------------------------------ tile metadata
 // [begin, end) of every tile from the tile changes of the sorted keys (tile = key >> b)
 __global__ void k_ranges(const uint64_t* __restrict__ keys, const int64_t* __restrict__ scal, int64_t capacity,
-                         int id_bits, int2* __restrict__ ranges) {
+                         int id_bits, int2* __restrict__ ranges, int n_tiles) {
   const int64_t P = min(scal[S_P], capacity);
   const int b = (int)scal[S_B] + id_bits;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t t = (uint32_t)(keys[i] >> b);
+    SIMULI_CHECK(t < (uint32_t)n_tiles, t, n_tiles);
+    SIMULI_CHECK(i == 0 || keys[i - 1] <= keys[i], i, P);  // sorted
     if (i == 0 || (uint32_t)(keys[i - 1] >> b) != t) ranges[t].x = (int)i;
     if (i == P - 1 || (uint32_t)(keys[i + 1] >> b) != t) ranges[t].y = (int)(i + 1);
   }
@@ -736,7 +743,9 @@ __global__ void __launch_bounds__(1024) k_tile_order(const int2* __restrict__ ra
   for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
     const int2 r = ranges[t];
     const int len = r.y - r.x;
-    order[atomicAdd(&s_off[len > 0 ? 32 - __clz(len) : 0], 1)] = t;
+    const int o = atomicAdd(&s_off[len > 0 ? 32 - __clz(len) : 0], 1);
+    SIMULI_CHECK(o >= 0 && o < n_tiles && r.x >= 0 && len >= 0, o, len);
+    order[o] = t;
   }
 }
 
@@ -830,7 +839,7 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
   if (nb > 0 && cap > 0) {
     DupArgs D{proj->tile_count, reinterpret_cast<const int4*>(proj->tile_rect), proj->depth_key, n, cap,
               w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, nullptr,
-              id_bits, packed ? 1 : 0};
+              id_bits, packed ? 1 : 0, n_tiles};
     k_duplicate<<<(unsigned)nb, kDupThreads, 0, st>>>(D);
     if (int32_t e = check("duplicate")) return e;
     for (int p = 0; p < max_passes; ++p) {
@@ -845,7 +854,8 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
   if (cudaMemsetAsync(tile_ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, st) != cudaSuccess)
     return check("memset ranges");
   if (cap > 0)
-    k_ranges<<<148 * 8, 256, 0, st>>>(w.keys[0], w.scal, cap, key_shift, reinterpret_cast<int2*>(tile_ranges));
+    k_ranges<<<148 * 8, 256, 0, st>>>(w.keys[0], w.scal, cap, key_shift, reinterpret_cast<int2*>(tile_ranges),
+                                      n_tiles);
   if (tile_order)
     k_tile_order<<<1, 1024, 0, st>>>(reinterpret_cast<const int2*>(tile_ranges), n_tiles, tile_order);
   if (sorted_keys && cap > 0) k_keys64<<<148 * 4, 256, 0, st>>>(w.keys[0], w.scal, cap, key_shift, sorted_keys);

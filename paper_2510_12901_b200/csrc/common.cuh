@@ -6,6 +6,27 @@
 #include "../../include/simuli.h"
 #include "abi_util.h"
 
+// Checked builds (SIMULI_EXTRA_NVCC=-DSIMULI_CHECKED, scripts/checked_run.sh): device-side
+// bounds / invariant assertions on the kernels' computed indices -- the substitute for
+// compute-sanitizer, which is closed on the GPU pool.  A failed check prints the kernel's
+// file:line and the operands, then traps (the launch fails with an illegal-instruction
+// error the caller sees).  Compiled out otherwise.
+#ifdef SIMULI_CHECKED
+#include <cstdio>
+#define SIMULI_CHECK(cond, a, b)                                                                            \
+  do {                                                                                                    \
+    if (!(cond)) {                                                                                        \
+      printf("SIMULI_CHECK failed %s:%d: %s (%lld, %lld) block %d thread %d\n", __FILE__, __LINE__, #cond, \
+             (long long)(a), (long long)(b), (int)blockIdx.x, (int)threadIdx.x);                          \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
+#else
+#define SIMULI_CHECK(cond, a, b) \
+  do {                           \
+  } while (0)
+#endif
+
 namespace simuli {
 
 // status of the last kernel launch as a libsimuli error code (with the CUDA message)

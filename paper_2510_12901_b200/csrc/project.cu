@@ -209,15 +209,20 @@ __device__ __forceinline__ int exact_rect(const ProjArgs& A, const float box[4],
     else if (cL >= cF) { cs = 0; cl = A.n_theta; }
     else { cs = cF; cl = A.n_theta - cF + cL + 1; }
   }
+  SIMULI_CHECK(bl >= 0 && bh < A.n_beams && first >= 0 && first < NA, bl, first);
   rect[0] = elev_tile(A, __ldg(A.beam_sorted + bl));
   rect[1] = elev_tile(A, __ldg(A.beam_sorted + bh));
   rect[2] = cs;
   rect[3] = cl;
+  SIMULI_CHECK(rect[0] >= 0 && rect[0] <= rect[1] && rect[1] < A.n_phi, rect[0], rect[1]);
+  SIMULI_CHECK(cs >= 0 && cs < A.n_theta && cl >= 1 && cl <= A.n_theta, cs, cl);
   return (rect[1] - rect[0] + 1) * cl;
 }
 
 __device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c0, int c1) {
   const int sc = A.sat_cols;
+  SIMULI_CHECK(r0 >= 0 && r0 <= r1 && r1 < A.n_phi * A.rows_per_tile, r0, r1);
+  SIMULI_CHECK(c0 >= 0 && c0 <= c1 && c1 < A.az_cells && c1 + 1 < sc, c0, c1);
   return __ldg(A.sat + (r1 + 1) * sc + (c1 + 1)) - __ldg(A.sat + r0 * sc + (c1 + 1)) -
          __ldg(A.sat + (r1 + 1) * sc + c0) + __ldg(A.sat + r0 * sc + c0);
 }
@@ -759,6 +764,8 @@ __global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_proje
       }
     }
   }
+  SIMULI_CHECK(count >= 0 && (KIND != SIMULI_SENSOR_LIDAR || count <= A.n_phi * A.n_theta), count, g);
+  SIMULI_CHECK(count == 0 || (rect[0] >= 0 && rect[2] >= 0 && rect[3] >= 1), rect[0], rect[2]);
   A.count[g] = count;
   reinterpret_cast<int4*>(A.rect)[g] = make_int4(rect[0], rect[1], rect[2], rect[3]);
   if (count > 0 || A.write_all) {

@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
   float T = 1.f, acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, D = 0.f, W = 0.f;
   int nc = 0, nv = 0, ni = 0, term_at = -1;
   bool done = !(inside && valid);
+  SIMULI_CHECK(tile >= 0 && tile < A.Wt * ((A.height + A.tile_px - 1) / A.tile_px), tile, A.Wt);
   const int2 rg = __ldg(A.ranges + tile);
+  SIMULI_CHECK(rg.x >= 0 && rg.x <= rg.y, rg.x, rg.y);
   const int nbatch = (rg.y - rg.x + NT - 1) / NT;
   auto load_ids = [&](int bi, uint32_t out[PER]) {  // ids of batch bi (registers; used a batch later)
 #pragma unroll
@@ -378,6 +380,7 @@ __global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A
   const int64_t item = blockIdx.x;
   const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
   const int tile = A.order ? __ldg(A.order + tslot) : tslot;
+  SIMULI_CHECK(tile >= 0 && (int64_t)tile * A.items_per_tile < A.n_items, tile, A.n_items);
   const int et = tile / A.n_theta, at_ = tile % A.n_theta;
   const int bgi = sub / A.n_cg, cgi = sub % A.n_cg;
   const int b0 = __ldg(A.etb_off + et) + bgi * A.bg, b1 = min(__ldg(A.etb_off + et + 1), b0 + A.bg);
@@ -385,6 +388,7 @@ __global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A
   const int nb = b1 - b0, nc = c1 - c0;
   if (nb <= 0 || nc <= 0) return;  // CTA-uniform
   const int R = nb * nc;
+  SIMULI_CHECK(R <= 32, nb, nc);
 #ifdef SIMULI_RENDER_PROFILE
   const long long t_start = gtime();
 #endif
@@ -406,6 +410,7 @@ __global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A
   }
   __syncthreads();
   const int2 rg = __ldg(A.ranges + tile);
+  SIMULI_CHECK(rg.x >= 0 && rg.x <= rg.y, rg.x, rg.y);
   const int len = rg.y - rg.x;
   const int nchunks = (len + 31) >> 5;
   volatile uint32_t* vdone = &S.done_mask;
@@ -422,6 +427,7 @@ __global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A
         const int bi = lane / nc, ci = lane % nc;
         const int j = S.col_id[ci];
         ray = S.beam_id[bi] * A.n_az + j;
+        SIMULI_CHECK(j >= 0 && j < A.n_az && ray >= 0, j, ray);
         double Rm[9];
         pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
         double sa, ca, se, ce;
@@ -713,6 +719,7 @@ __global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A
         int i = off_r;
         for (uint32_t t = my; t && i < CAP; t &= t - 1u, ++i) ppair[i] = (uint16_t)((lane << 5) | (__ffs(t) - 1));
       }
+      SIMULI_CHECK(K >= 0 && K <= CAP && off_r >= 0, K, off_r);
       __syncwarp();
       for (int i = lane; i < K; i += 32) {
         const int v = ppair[i];
