@@ -291,11 +291,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 // The per-ray arithmetic (responses, chain order and operands) does not depend on the
 // tiling, on culling or on the chunking, so results are bit-identical across (N_phi, M)
 // and culling on/off.
-// pipeline shape: P producers, NS chunk slots (NS = 2P: a producer claims a slot one
-// iteration after the box test), CAP pairs per slot
+// pipeline shape: P producers, NS chunk slots (a producer claims its chunk's slot one
+// iteration after the box test), CAP pairs per slot; (3, 3, 384): config-B render 182 ->
+// 173 us vs (3, 6, 512) -- smaller slots, more CTAs per SM (SIMULI_LIDAR_VARIANT sweep)
 constexpr int kLidarProducers = 3;
-constexpr int kLidarSlots = 6;
-constexpr int kPairCap = 512;
+constexpr int kLidarSlots = 3;
+constexpr int kPairCap = 384;
 
 template <int CAP>
 struct LidarSlot {
@@ -340,7 +341,10 @@ __device__ __forceinline__ bool mbar_wait_or_stop(unsigned long long* b, unsigne
                  : "memory");
     if (ok) return true;
     if (*stop) return false;
-    __nanosleep(256);  // a waiting producer is ahead of the consumer: poll slowly, leave it the issue slots
+#ifndef SIMULI_PROD_SLEEP
+#define SIMULI_PROD_SLEEP 256
+#endif
+    __nanosleep(SIMULI_PROD_SLEEP);  // a waiting producer is ahead of the consumer: poll slowly, leave it the issue slots
   }
 }
 
@@ -774,8 +778,13 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   A.ray_az = T.ray_az; A.ray_el = T.ray_el; A.ray_s = T.ray_s;
   A.n_theta = T.n_theta; A.n_az = T.n_azimuth;
   // work items: beam groups x column groups of <= 32 rays per tile, uniform over tiles
-  A.cg = T.max_cols_per_az_tile < 32 ? T.max_cols_per_az_tile : 32;
-  A.bg = 32 / A.cg;
+  static const int item_rays = [] {
+    const char* v = getenv("SIMULI_LIDAR_ITEM_RAYS");  // tuning only: rays per work item (<= 32)
+    const int r = v ? atoi(v) : 32;
+    return r >= 1 && r <= 32 ? r : 32;
+  }();
+  A.cg = T.max_cols_per_az_tile < item_rays ? T.max_cols_per_az_tile : item_rays;
+  A.bg = item_rays / A.cg;
   A.n_cg = (T.max_cols_per_az_tile + A.cg - 1) / A.cg;
   const int nbg = (T.max_beams_per_elev_tile + A.bg - 1) / A.bg;
   A.items_per_tile = A.n_cg * nbg;
@@ -818,6 +827,11 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
     case 48256: launch(I4{}, I8{}, integral_constant<int, 256>{}); break;
     case 48384: launch(I4{}, I8{}, integral_constant<int, 384>{}); break;
     case 36384: launch(I3{}, I6{}, integral_constant<int, 384>{}); break;
+    case 36256: launch(I3{}, I6{}, integral_constant<int, 256>{}); break;
+    case 33256: launch(I3{}, I3{}, integral_constant<int, 256>{}); break;
+    case 33384: launch(I3{}, I3{}, integral_constant<int, 384>{}); break;
+    case 44256: launch(I4{}, I4{}, integral_constant<int, 256>{}); break;
+    case 26256: launch(I2{}, I6{}, integral_constant<int, 256>{}); break;
     default:
       launch(integral_constant<int, kLidarProducers>{}, integral_constant<int, kLidarSlots>{},
              integral_constant<int, kPairCap>{});
