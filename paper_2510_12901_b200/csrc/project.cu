@@ -681,7 +681,9 @@ __global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_proje
         if (ya_bar >= kPiD) ya_bar -= 2.0 * kPiD;
         else if (ya_bar < -kPiD) ya_bar += 2.0 * kPiD;
       }
-      const double ha = (double)A.ks * sqrt((double)caa), hb = (double)A.ks * sqrt((double)cbb);
+      // half-widths: a float32 root (relative error 2^-24 of ~1e-3 rad: ~1e-10 rad) is exact
+      // enough; the edges themselves are summed and rounded outward in double
+      const double ha = (double)(A.ks * __fsqrt_rn(caa)), hb = (double)(A.ks * __fsqrt_rn(cbb));
       box[0] = __double2float_rd(ya_bar - ha);
       box[1] = __double2float_ru(ya_bar + ha);
       box[2] = __double2float_rd(yb_bar - hb);
