@@ -260,44 +260,49 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------ GPU leg
 def roofline_entries(stage_ms, counters, peaks, clocks_mhz):
-    """Roofline of every stage from ALGORITHMIC bytes / instructions per launch."""
+    """Roofline of every stage per launch.  Each stage reports (a) its binding bound under
+    SURVEY §8(d) -- projection: max(bytes N 48 + N_vis (192 + 96) over HBM, the §8(d)
+    instruction model over the FP32 issue peak) = issue-bound at K = 1; bin_sort: the
+    duplication bytes 8N + 16 N_vis + 12P plus the radix passes P (8 + passes 24) + 8P over
+    HBM; render: the counted lane-instructions over the issue peak -- and (b) a strict
+    variant beside it (algorithmic bytes only: inputs read once, outputs written once)."""
     hbm = peaks["hbm_gbs"]
     n, n_vis, P, R, n_tiles = (counters[k] for k in ("n", "n_vis", "P", "R", "n_tiles"))
-    # stage bytes: inputs the method must read + outputs it must write (SURVEY §8(d))
+    alu_peak = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e12  # T lane-instr/s at max clock
+    K = counters["K"]
+    # strict algorithmic bytes: inputs the method must read + outputs it must write
     b_project = n * (12 + 16 + 12 + 4) + n * (4 + 16 + 4) + n_vis * (192 + 80)
-    # sort: read each particle's count, rect and key once, write each pair's id once, plus the
-    # tile ranges and order (the radix passes of the implementation are not algorithmic)
     b_sort = n * (4 + 16 + 4) + 4 * P + 12 * n_tiles
     lane_instr = (C_BOX * counters["visited"] + C_RESP * counters["inbox"] + C_ACC * counters["contrib"] +
                   C_RAY * R)
     b_render = n_vis * 80 + P * 4 + R * (40 + 12)
-    alu_peak = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e12  # T lane-instr/s at max clock
+    # SURVEY §8(d) model
+    i_proj = n * (7 * (C_PROJ + K * (C_PROJ + C_POSE)) + C_UT + C_MISC) + n_vis * C_SH
+    b_proj8 = n * 48 + n_vis * (192 + 96)
+    b_sort8 = (8 * n + 16 * n_vis + 12 * P) + P * (8 + counters["passes"] * 24) + 8 * P
     out = {}
-    for name, bytes_, bound in (("project", b_project, "hbm"), ("bin_sort", b_sort, "hbm")):
-        t = stage_ms[name] * 1e-3
-        ach = bytes_ / t / 1e9
-        out[name] = {"bound": bound, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                     "algorithmic_bytes": int(bytes_), "ms": stage_ms[name]}
+    t = stage_ms["project"] * 1e-3
+    hb, ib = b_proj8 / (hbm * 1e9), i_proj / (alu_peak * 1e12)
+    out["project"] = ({"bound": "alu", "achieved": i_proj / t / 1e12, "peak": alu_peak, "unit": "T lane-instr/s",
+                       "frac": ib / t} if ib >= hb else
+                      {"bound": "hbm", "achieved": b_proj8 / t / 1e9, "peak": hbm, "unit": "GB/s", "frac": hb / t})
+    out["project"].update({"model_lane_instr": int(i_proj), "survey_8d_bytes": int(b_proj8),
+                           "hbm_frac_survey_8d": hb / t, "strict_bytes": int(b_project),
+                           "strict_hbm_frac": b_project / t / 1e9 / hbm, "ms": stage_ms["project"]})
+    t = stage_ms["bin_sort"] * 1e-3
+    out["bin_sort"] = {"bound": "hbm", "achieved": b_sort8 / t / 1e9, "peak": hbm, "unit": "GB/s",
+                       "frac": b_sort8 / t / 1e9 / hbm, "survey_8d_bytes": int(b_sort8), "strict_bytes": int(b_sort),
+                       "strict_hbm_frac": b_sort / t / 1e9 / hbm, "ms": stage_ms["bin_sort"]}
     t = stage_ms["render"] * 1e-3
     ach = lane_instr / t / 1e12
     out["render"] = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "T lane-instr/s",
                      "frac": ach / alu_peak, "algorithmic_lane_instr": int(lane_instr),
                      "algorithmic_bytes": int(b_render), "hbm_frac": b_render / t / 1e9 / hbm,
                      "ms": stage_ms["render"]}
-    # strict scan roofline: the stages' algorithmic bytes (project, sort) and bytes /
-    # lane-instructions (render), t_roof = sum over stages of max(bytes / BW, instr / IR)
     t_roof = (b_project / (hbm * 1e9) + b_sort / (hbm * 1e9) +
               max(b_render / (hbm * 1e9), lane_instr / (alu_peak * 1e12)))
-    # SURVEY §8(d) as written: projection bytes N 48 + N_vis (192 + 96) against its
-    # instruction model; duplication 8N + 16 N_vis + 12P; the radix passes counted,
-    # P (8 + passes 24) + 8P with passes = ceil(key bits / 8); render as above
-    K = counters["K"]
-    i_proj = n * (7 * (C_PROJ + K * (C_PROJ + C_POSE)) + C_UT + C_MISC) + n_vis * C_SH
-    b_proj8 = n * 48 + n_vis * (192 + 96)
-    b_dup8 = 8 * n + 16 * n_vis + 12 * P
-    b_sort8 = P * (8 + counters["passes"] * 24) + 8 * P
-    parts = {"project": max(b_proj8 / (hbm * 1e9), i_proj / (alu_peak * 1e12)),
-             "duplicate": b_dup8 / (hbm * 1e9), "sort": b_sort8 / (hbm * 1e9),
+    parts = {"project": max(hb, ib), "duplicate": (8 * n + 16 * n_vis + 12 * P) / (hbm * 1e9),
+             "sort": (P * (8 + counters["passes"] * 24) + 8 * P) / (hbm * 1e9),
              "render": max(b_render / (hbm * 1e9), lane_instr / (alu_peak * 1e12))}
     out["_scan"] = {"t_roof_ms": t_roof * 1e3, "t_roof_ms_survey_8d": sum(parts.values()) * 1e3,
                     "survey_8d_parts_ms": {k: v * 1e3 for k, v in parts.items()},
@@ -553,7 +558,10 @@ def run_gpu(args):
         traffic = json.load(open(tpath)).get(dom)
     d = roof[dom]
     roofline = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
-                "frac": d["frac"], "traffic": traffic, "kernel": dom, "peak_source": peaks["source"]}
+                "frac": d["frac"], "traffic": traffic, "kernel": dom, "peak_source": peaks["source"],
+                "note": "the dominant stage's binding bound under SURVEY §8(d) (projection: its instruction model "
+                        "over the FP32 issue peak 148 SM x 128 lanes x max clock; bytes in stages[...]); traffic = "
+                        "ncu dram read + write bytes of that stage's launches in one scan (profiles/ncu_traffic.json)"}
     if rank != 0:
         dist.destroy_process_group()
         return 0
