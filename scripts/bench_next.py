@@ -1,5 +1,5 @@
 """Timing of the SURVEY §8(f) NEXT variants at full size (one GPU), L2 flushed before every
-timed call, CUDA events, median of 8 after 2 warm-ups.  Writes profiles/r01_next.{md,json}.
+timed call, CUDA events, median of 8 after 2 warm-ups.  Writes profiles/r<ROUND>_next.{md,json} (ROUND env, default 02).
 
     python scripts/bench_next.py
 """
@@ -117,7 +117,10 @@ out = {"lidar_stages_us": {k: v for k, v in rows}, "camera_stages_us": cam_stage
        "backward": bwd, "backward_scene_graph_B": bwd_sg, "backward_variants_B": bwd_var,
        "gpu": torch.cuda.get_device_name(0)}
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-json.dump(out, open(os.path.join(ROOT, "profiles", "r01_next.json"), "w"), indent=1)
+RND = os.environ.get("ROUND", "02")
+OUT = os.environ.get("OUT_DIR", os.path.join(ROOT, "gpurun_out"))  # copied to profiles/ afterwards
+os.makedirs(OUT, exist_ok=True)
+json.dump(out, open(os.path.join(OUT, f"r{RND}_next.json"), "w"), indent=1)
 md = ["# NEXT variants at full size (SURVEY §8(f)), one B200", "",
       "`python scripts/bench_next.py`: CUDA events, L2 flushed (256 MB write) before every timed call, "
       "median of 8 after 2 warm-ups.", "", "## LiDAR config B stages (µs)", "",
@@ -144,5 +147,5 @@ md += ["", f"Backward through the scene graph (B + 64 objects, object-frame and 
            f"forward {bwd_sg['forward_us']:.1f} µs, backward {bwd_sg['backward_us']:.1f} µs."]
 for k, v in bwd_var.items():
     md += ["", f"Backward of config B with {k}: forward {v['forward_us']:.1f} µs, backward {v['backward_us']:.1f} µs."]
-open(os.path.join(ROOT, "profiles", "r01_next.md"), "w").write("\n".join(md) + "\n")
+open(os.path.join(OUT, f"r{RND}_next.md"), "w").write("\n".join(md) + "\n")
 print("\n".join(md))

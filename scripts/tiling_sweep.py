@@ -18,7 +18,7 @@ poses = synth.batch_poses(200)[::40]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 
-def run(n_phi, M, cull=True, reps=4):
+def run(n_phi, M, cull=2, reps=4):
     cfg = synth.lidar_config("B")
     cfg.n_phi, cfg.max_rays_per_tile = n_phi, M
     r = SM.LidarRenderer(cfg, scene, enable_culling=cull)
@@ -57,8 +57,9 @@ for n_phi in (64, 32, 16, 8):
         grid[(n_phi, M)] = res
         identical[(n_phi, M)] = all(np.array_equal(o[k], q[k]) for o, q in zip(outs, ref_out) for k in q)
         print(n_phi, M, res, identical[(n_phi, M)], flush=True)
-nocull, nocull_out = run(16, 32, cull=False)
-ident_cull = all(np.array_equal(o[k], q[k]) for o, q in zip(nocull_out, ref_out) for k in q)
+nocull, nocull_out = run(16, 32, cull=0)
+sat, sat_out = run(16, 32, cull=1)
+ident_cull = all(np.array_equal(o[k], q[k]) for outs in (nocull_out, sat_out) for o, q in zip(outs, ref_out) for k in q)
 
 L = ["# B200 analogs of tab:lidar-tiling and tab:culling (config B, 2M particles)", "",
      f"Scan = project + bin_sort + render, each stage timed alone (CUDA events, L2 flushed), "
@@ -78,11 +79,14 @@ for n_phi in (64, 32, 16, 8):
     L.append(f"| {n_phi} | " + " | ".join(cells) + " |")
 L += ["", f"Outputs bit-identical to (16, 32) in every cell: {all(identical.values())}.", "",
       "## Ray-based culling at (16, 32) (ms per scan)", "",
-      "| kernel | w/ culling | w/o culling | speedup (%) |", "|---|---|---|---|"]
-for s in ("project", "bin_sort", "render"):
-    a, b = ref_res[s], nocull[s]
-    L.append(f"| {s} | {a:.3f} | {b:.3f} | {100 * (b - a) / b:.1f} |")
-L += ["", f"Pairs: {ref_res['pairs']} with culling, {nocull['pairs']} without; outputs bit-identical: {ident_cull}."]
+      "Modes: exact ray containment (A32, default), the paper's SAT test on the dense grid "
+      "(Proc. RayOccupancyCount), off.", "",
+      "| kernel | exact | SAT (paper) | off | exact vs off (%) | SAT vs off (%) |", "|---|---|---|---|---|---|"]
+for st in ("project", "bin_sort", "render"):
+    a, m, b = ref_res[st], sat[st], nocull[st]
+    L.append(f"| {st} | {a:.3f} | {m:.3f} | {b:.3f} | {100 * (b - a) / b:.1f} | {100 * (b - m) / b:.1f} |")
+L += ["", f"Pairs: {ref_res['pairs']} exact, {sat['pairs']} SAT, {nocull['pairs']} off; outputs bit-identical in "
+          f"all three modes: {ident_cull}."]
 os.makedirs(os.path.dirname(out_path) or ".", exist_ok=True)
 open(out_path, "w").write("\n".join(L) + "\n")
 print("\n".join(L))
