@@ -50,5 +50,21 @@ head = [f"# Round {rnd} ncu evidence (config B, bench.py launch configuration)",
         "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of `bench.py --steps 2 --warmup 3` "
         "(cold-cache, serialised: compare SHARES). Full capture: `ncu --set full` of one steady-state scan "
         "(scripts/ncu_scan.sh).", ""]
-open(os.path.join(HERE, f"r{rnd}_summary.md"), "w").write("\n".join(head) + summ)
+# SM clock ncu observed per kernel (--clock-control none) and the issue peak at that clock
+txt2 = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                       "sm__cycles_elapsed.avg.per_second,gpu__time_duration.sum,smsp__inst_executed.sum"],
+                      capture_output=True, text=True).stdout
+r2 = list(csv.reader(io.StringIO(txt2)))
+h2 = r2[0]
+clk = ["", "## SM clock ncu observed (--clock-control none) and issue utilisation at that clock", "",
+       "| kernel | us | SM GHz | warp-instr | issue util at observed clock | FP32 issue peak at that clock (T lane-instr/s) |",
+       "|---|---|---|---|---|---|"]
+for r in r2[2:]:
+    f = float(r[h2.index("sm__cycles_elapsed.avg.per_second")].replace(",", ""))
+    us = float(r[h2.index("gpu__time_duration.sum")].replace(",", ""))
+    wi = float(r[h2.index("smsp__inst_executed.sum")].replace(",", ""))
+    util = wi / (148 * 4 * f * 1e9 * us * 1e-6)
+    clk.append(f"| `{r[h2.index('Kernel Name')].split('(')[0].split('::')[-1]}` | {us:.1f} | {f:.3f} | {wi / 1e6:.1f} M | "
+               f"{100 * util:.1f} % | {148 * 128 * f / 1e3:.1f} |")
+open(os.path.join(HERE, f"r{rnd}_summary.md"), "w").write("\n".join(head) + summ + "\n".join(clk) + "\n")
 print("\n".join(head))
