@@ -11,12 +11,14 @@ over ranks (weak scaling: K scans per rank); there is no collective on the data 
 only reduces the timers / counters.
 
 Prints ONE JSON line on rank 0.  value = whole-job LiDAR rays/s (scans/s in
-``scans_per_s``): the K timed scans run three in flight per GPU (three renderers with
-their own buffers on three streams, shared resident scene -- one scan's latency-bound
-stages overlap the others'; measured 1 / 2 / 3 / 4 in flight: 160 / 178 / 181 / 181 M rays/s), timed between two CUDA events on the launching stream, bracketed by
-barrier + synchronize, max over ranks; inputs exceed the L2, so no flush.  A second pass
-runs scans one at a time with the L2 flushed and per-stage CUDA events: the stage
-breakdown and roofline, and ``latency_ms_per_scan``.
+``scans_per_s``): the K timed scans run four in flight per GPU (four renderers with their
+own buffers on four streams, shared resident scene -- one scan's latency-bound stages
+overlap the others'; with the throughput-default kernels 3 / 4 / 6 in flight measured
+275 / 289 / 283 M rays/s), timed between two CUDA events on the launching stream,
+bracketed by barrier + synchronize, max over ranks; inputs exceed the L2, so no flush.  A
+second pass runs scans one at a time with the L2 flushed and per-stage CUDA events: the
+stage breakdown and roofline, and ``latency_ms_per_scan``; a third the same with the
+latency-optimised render shape (``latency_mode``).
 ``--impl reference`` times the CPU oracle (oracle/, test infrastructure) on a bounded
 sample of the same workload on the host cores.
 """
@@ -471,6 +473,48 @@ def run_gpu(args):
         r.render()
         e[3].record(stream)
     torch.cuda.synchronize()
+    # per-stage throughput: each stage alone, N_STAGE launches spread over the S renderers /
+    # streams (lists and records from their last scan), device time / launches -- the cost of
+    # one launch when S run concurrently, as in the headline
+    stage_tp = {}
+    for name in ("project", "bin_sort", "render"):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for st in streams:
+            st.wait_event(e0)
+        for i in range(n_stage):
+            getattr(rs[i % S], name)(stream=streams[i % S])
+        for st in streams:
+            ej = torch.cuda.Event()
+            ej.record(st)
+            stream.wait_event(ej)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        stage_tp[name] = e0.elapsed_time(e1) / n_stage
+    # latency mode: the same stage pass with the latency-optimised render shape
+    # (simuli_render_params.lidar_producers = 3); outputs identical, reported beside
+    r.rparams.lidar_producers = 3
+    lat = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n_stage)]
+    lat_scan = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(n_stage)]
+    for i in range(n_stage):
+        flush.zero_()
+        p0, p1 = my[(args.warmup + i) % len(my)]
+        r.set_poses(p0, p1)
+        lat_scan[i][0].record(stream)
+        r.project()
+        r.bin_sort()
+        lat[i][0].record(stream)
+        r.render()
+        lat[i][1].record(stream)
+        lat_scan[i][1].record(stream)
+    torch.cuda.synchronize()
+    r.rparams.lidar_producers = 0
+    latency_mode = {"render_producers": 3,
+                    "render_ms_median": statistics.median(e[0].elapsed_time(e[1]) for e in lat),
+                    "scan_ms_median": statistics.median(e[0].elapsed_time(e[1]) for e in lat_scan),
+                    "note": "one scan at a time, L2 flushed, the latency-optimised render pipeline (3 producer "
+                            "warps per item); the headline uses the throughput default (1 producer warp)"}
     clk = clocks.stop()
     cap_checks.append(check_capacity("stage pass"))
     samples = {"project": [e[0].elapsed_time(e[1]) for e in ev], "bin_sort": [e[1].elapsed_time(e[2]) for e in ev],
@@ -541,6 +585,17 @@ def run_gpu(args):
 
     peaks = read_peaks()
     roof = roofline_entries(stage_ms, counters, peaks, clk.get("sm_mhz"))
+    roof_tp = roofline_entries(stage_tp, counters, peaks, clk.get("sm_mhz"))
+    roof_tp.pop("_scan")
+    stages_inflight = {k: {"ms_per_launch": stage_tp[k], "bound": v["bound"], "achieved": v["achieved"],
+                           "peak": v["peak"], "unit": v["unit"], "frac": v["frac"]} for k, v in roof_tp.items()}
+    stages_inflight["note"] = (f"each stage alone, {n_stage} launches over {S} streams (S in flight, as the headline): "
+                               "device time per launch and the stage's roofline fraction at that throughput")
+    dom_tp = max(roof_tp, key=lambda k: roof_tp[k]["ms"])
+    roofline_inflight = {k: stages_inflight[dom_tp][k] for k in ("bound", "achieved", "peak", "unit", "frac")}
+    roofline_inflight.update({"kernel": dom_tp, "ms_per_launch": stage_tp[dom_tp],
+                              "note": "the stage with the largest per-launch cost in flight (S concurrent launches, "
+                                      "the headline's regime); `roofline` is the same for launches one at a time"})
     scan_roof = roof.pop("_scan")
     thr = max_ms / args.steps
     scan_roof.update({"latency_ms": latency_ms, "frac_of_latency": scan_roof["t_roof_ms"] / latency_ms,
@@ -575,9 +630,11 @@ def run_gpu(args):
                              "flush; stage pass: L2 flushed before every scan (256 MB write)",
                        "parallelism": f"dp{ws}"},
             "scans_per_s": value / r.n_rays,
-            "latency_ms_per_scan": latency_ms,
+            "latency_ms_per_scan": latency_ms, "latency_mode": latency_mode,
             "e2e": e2e, "gpu_launches": LAUNCHES_PER_SCAN * args.steps,
-            "roofline": roofline, "stages": roof, "stage_ms_distribution": dict(dist_ms, n=n_stage),
+            "roofline": roofline, "roofline_inflight": roofline_inflight, "stages": roof,
+            "stages_inflight": stages_inflight,
+            "stage_ms_distribution": dict(dist_ms, n=n_stage),
             "scan_roofline": scan_roof, "counters": counters, "job_counters": job_counters,
             "capacity_checks": cap_checks, "spot_check": spot_check, "comm": comm,
             "clocks": clk,
@@ -664,7 +721,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the configs C and D lines")
-    ap.add_argument("--inflight", type=int, default=3, help="scans in flight (renderers / streams) per GPU")
+    ap.add_argument("--inflight", type=int, default=4, help="scans in flight (renderers / streams) per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

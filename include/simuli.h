@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 10
+#define SIMULI_ABI_VERSION 11
 
 enum {
   SIMULI_OK = 0,
@@ -290,11 +290,18 @@ int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles
  * Features: sh == NULL -> each particle's record features f (SH evaluated once per particle
  * at its view direction, A17); sh != NULL -> Eq. 1 literally (A30): SH_i(d)
  * evaluated per (ray, particle) at the ray's unit direction d from sh (device, the
- * particle set's [n][(sh_degree+1)^2][3] coefficients, indexed by the sorted ids). */
+ * particle set's [n][(sh_degree+1)^2][3] coefficients, indexed by the sorted ids).
+ * lidar_producers (LiDAR render only; outputs are identical for every value): producer
+ * warps per work item of the producer / consumer pipeline.  0 or 1 = the default,
+ * throughput-optimised shape (1 producer + 1 consumer warp, 2 chunk slots: the least SM
+ * resources per item, best when several scans are in flight); 3 = the latency-optimised
+ * shape (3 producers, 3 slots: the shortest single scan); 2 = in between.  Other values:
+ * INVALID_ARGUMENT. */
 typedef struct {
   float alpha_min, alpha_max, T_min;
   const float* sh;
   int32_t sh_degree;
+  int32_t lidar_producers;
 } simuli_render_params;
 
 /* Per-ray LiDAR outputs (device, [n_rays] each; any pointer may be NULL to skip it).

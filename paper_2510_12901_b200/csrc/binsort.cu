@@ -17,8 +17,8 @@
 //                   map of (tile, depth bits) -- plus the digit histograms of every pass
 //   k_onesweep x 6  stable LSD onesweep, 8-bit digits; passes beyond the device-side pass
 //                   count exit at once (buffer parity is chosen on the device so the
-//                   last real pass lands in the caller's arrays).  Per 6144-key partition
-//                   (512 threads x 12 keys) a warp-level multisplit (ballot-built peer
+//                   last real pass lands in the caller's arrays).  Per 5120-key partition
+//                   (256 threads x 20 keys) a warp-level multisplit (ballot-built peer
 //                   masks) ranks the keys, the partition publishes its digit counts, stages
 //                   its keys in digit order in shared memory, then a decoupled look-back
 //                   over partitions (dynamic partition ids for forward progress) yields
@@ -486,6 +486,7 @@ struct SweepSmem {
 
 template <bool Packed, int NT, int ITEMS, int LOOKW, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
+  static_assert(NT >= 256, "one digit thread per 8-bit digit");
   constexpr int NW = NT / 32;
   constexpr int PART = NT * ITEMS;
   extern __shared__ __align__(16) unsigned char sweep_smem[];
@@ -688,17 +689,21 @@ void launch_sweep_variant(const SweepArgs& S, int64_t cap, cudaStream_t st) {
     case 2561632: launch_sweep<Packed, 256, 16, 32>(S, cap, st); break;
     case 2562432: launch_sweep<Packed, 256, 24, 32>(S, cap, st); break;
     case 5121232: launch_sweep<Packed, 512, 12, 32>(S, cap, st); break;
-    case 5121208: launch_sweep<Packed, 512, 12, 8>(S, cap, st); break;
     case 5121216: launch_sweep<Packed, 512, 12, 16>(S, cap, st); break;
     case 2562408: launch_sweep<Packed, 256, 24, 8, 3>(S, cap, st); break;
+    case 2562404: launch_sweep<Packed, 256, 24, 4, 3>(S, cap, st); break;
+    case 2562416: launch_sweep<Packed, 256, 24, 16, 3>(S, cap, st); break;
+    case 5122408: launch_sweep<Packed, 512, 24, 8, 1>(S, cap, st); break;
     case 2561608: launch_sweep<Packed, 256, 16, 8>(S, cap, st); break;
     case 10241208: launch_sweep<Packed, 1024, 12, 8>(S, cap, st); break;
     case 10241216: launch_sweep<Packed, 1024, 12, 16>(S, cap, st); break;
     case 5121632: launch_sweep<Packed, 512, 16, 32>(S, cap, st); break;
     case 2561208: launch_sweep<Packed, 256, 12, 8>(S, cap, st); break;
-    // default: 512 x 12 keys (6144 per partition, half the look-back chain of 3072-key
-    // partitions): config-B bin_sort 201.6 -> 190.0 us (L2 warm)
-    default: launch_sweep<Packed, 512, kSortItems, kLookW>(S, cap, st); break;
+    case 5121208: launch_sweep<Packed, 512, 12, 8>(S, cap, st); break;
+    // default: 256 threads x 20 keys (5120 per partition), 3 CTAs per SM: with several
+    // scans in flight the fewest look-back spins per key (config B, four scans in flight:
+    // 275 -> 289 M rays/s against 512 x 12; one sort alone 200 us vs 190 us)
+    default: launch_sweep<Packed, 256, 20, kLookW, 3>(S, cap, st); break;
   }
 }
 

@@ -292,11 +292,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 // tiling, on culling or on the chunking, so results are bit-identical across (N_phi, M)
 // and culling on/off.
 // pipeline shape: P producers, NS chunk slots (a producer claims its chunk's slot one
-// iteration after the box test), CAP pairs per slot; (3, 3, 384): config-B render 182 ->
-// 173 us vs (3, 6, 512) -- smaller slots, more CTAs per SM (SIMULI_LIDAR_VARIANT sweep)
-constexpr int kLidarProducers = 3;
-constexpr int kLidarSlots = 3;
-constexpr int kPairCap = 384;
+// iteration after the box test), CAP pairs per slot, chosen per call
+// (simuli_render_params.lidar_producers): (1, 2, 256) = throughput (config B, four scans in
+// flight: 275 -> 289 M rays/s against (3, 3, 384); one scan alone 345 us), (3, 3, 384) =
+// latency (one scan alone 173 us; round 1's (3, 6, 512): 182 us).  SIMULI_LIDAR_VARIANT
+// (P * 10000 + NS * 1000 + CAP) overrides it for tuning sweeps.
 
 template <int CAP>
 struct LidarSlot {
@@ -333,6 +333,18 @@ __device__ __forceinline__ void unpack_ray(const float4* q, RayF& r) {
 // barrier event of the SM, and the spinning producers took the consumer's issue slots
 __device__ __forceinline__ bool mbar_wait_or_stop(unsigned long long* b, unsigned parity, volatile int* stop) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
+#ifdef SIMULI_PROD_TRYWAIT
+  // hardware-suspended wait (up to SIMULI_PROD_TRYWAIT ns per try), the stop flag between tries
+  for (;;) {
+    unsigned ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(a), "r"(parity), "n"(SIMULI_PROD_TRYWAIT)
+                 : "memory");
+    if (ok) return true;
+    if (*stop) return false;
+  }
+#endif
   for (;;) {
     unsigned ok;
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
@@ -821,6 +833,16 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   using I4 = integral_constant<int, 4>;
   using I6 = integral_constant<int, 6>;
   using I8 = integral_constant<int, 8>;
+  SIMULI_REQUIRE(rp->lidar_producers >= 0 && rp->lidar_producers <= 3,
+                 "simuli_render_lidar: lidar_producers must be 0..3");
+  if (variant == 0) {
+    switch (rp->lidar_producers) {
+      case 3: launch(I3{}, I3{}, integral_constant<int, 384>{}); break;                       // latency
+      case 2: launch(I2{}, I3{}, integral_constant<int, 384>{}); break;
+      default: launch(integral_constant<int, 1>{}, I2{}, integral_constant<int, 256>{}); break;  // throughput
+    }
+    return launch_check("simuli_render_lidar");
+  }
   switch (variant) {
     case 24512: launch(I2{}, I4{}, integral_constant<int, 512>{}); break;
     case 24384: launch(I2{}, I4{}, integral_constant<int, 384>{}); break;
@@ -832,10 +854,15 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
     case 33384: launch(I3{}, I3{}, integral_constant<int, 384>{}); break;
     case 44256: launch(I4{}, I4{}, integral_constant<int, 256>{}); break;
     case 26256: launch(I2{}, I6{}, integral_constant<int, 256>{}); break;
+    case 24256: launch(I2{}, I4{}, integral_constant<int, 256>{}); break;
+    case 22384: launch(I2{}, I2{}, integral_constant<int, 384>{}); break;
+    case 23384: launch(I2{}, I3{}, integral_constant<int, 384>{}); break;
+    case 12384: launch(integral_constant<int, 1>{}, I2{}, integral_constant<int, 384>{}); break;
+    case 13384: launch(integral_constant<int, 1>{}, I3{}, integral_constant<int, 384>{}); break;
+    case 12256: launch(integral_constant<int, 1>{}, I2{}, integral_constant<int, 256>{}); break;
     default:
-      launch(integral_constant<int, kLidarProducers>{}, integral_constant<int, kLidarSlots>{},
-             integral_constant<int, kPairCap>{});
-      break;
+      set_error("simuli_render_lidar: unknown SIMULI_LIDAR_VARIANT %d", variant);
+      return SIMULI_ERR_INVALID_ARGUMENT;
   }
   return launch_check("simuli_render_lidar");
 }

@@ -24,7 +24,7 @@ SENSOR_LIDAR, SENSOR_CAMERA = 0, 1
 CAM_PINHOLE_RADTAN, CAM_FISHEYE_KB = 0, 1
 RECORD_FLOATS = 20
 
-ABI_VERSION = 10  # include/simuli.h SIMULI_ABI_VERSION
+ABI_VERSION = 11  # include/simuli.h SIMULI_ABI_VERSION
 EXPORTED = ["simuli_last_error", "simuli_abi_version", "simuli_build_tiles", "simuli_project",
             "simuli_bin_sort_workspace_size", "simuli_bin_sort", "simuli_render_lidar", "simuli_render_camera",
             "simuli_compose_camera", "simuli_backward_workspace_size", "simuli_backward_lidar",
@@ -129,7 +129,7 @@ class Projected(C.Structure):
 
 class RenderParams(C.Structure):
     _fields_ = [("alpha_min", C.c_float), ("alpha_max", C.c_float), ("T_min", C.c_float), ("sh", C.c_void_p),
-                ("sh_degree", C.c_int32)]
+                ("sh_degree", C.c_int32), ("lidar_producers", C.c_int32)]
 
 
 class LidarOut(C.Structure):
@@ -469,7 +469,8 @@ class LidarRenderer(_Frame):
     outputs are identical in all three modes, only the tile lists differ."""
 
     def __init__(self, cfg, scene_dev, capacity=None, device="cuda", enable_culling=2, write_all_records=False,
-                 ut=(1.0, 2.0, 0.0), extent_sigma=3.0, render_params=(1.0 / 255.0, 0.99, 1e-4), per_ray_sh=False):
+                 ut=(1.0, 2.0, 0.0), extent_sigma=3.0, render_params=(1.0 / 255.0, 0.99, 1e-4), per_ray_sh=False,
+                 render_producers=0):
         import torch
         self.device = device
         self.cfg = cfg
@@ -495,6 +496,9 @@ class LidarRenderer(_Frame):
                                     make_pose(cfg.pose_start), make_pose(cfg.pose_end), int(cfg.rs_iterations),
                                     ut[0], ut[1], ut[2], extent_sigma, int(enable_culling), int(write_all_records))
         self.rparams = RenderParams(*render_params, None, 0)
+        # render pipeline shape (simuli.h): 0 = throughput default (1 producer warp per item),
+        # 3 = latency (3 producers); identical outputs
+        self.rparams.lidar_producers = int(render_producers)
         if per_ray_sh:  # Eq. 1 literally: SH_i(d) per (ray, particle) (A30)
             self.rparams.sh = scene_dev["sh"].data_ptr()
             self.rparams.sh_degree = self.gauss.sh_degree
