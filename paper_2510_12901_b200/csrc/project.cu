@@ -246,23 +246,6 @@ __device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c
 // Firing times are decisions of float32 accuracy only (an error of 1e-7 in s moves a point by
 // < 1e-9 rad), so they stay in float32.
 
-// sin(a theta), 1 - cos(a theta) in double (Taylor for |a theta| <= 0.5: truncation < 1e-16)
-__device__ __forceinline__ void rot_sc_d(const ProjArgs& A, double s, double* sn, double* omc) {
-  const double a = s * A.theta_d;
-  if (A.small_rot) {
-    const double a2 = a * a;
-    *sn = a * (1. - a2 * (1. / 6.) * (1. - a2 * (1. / 20.) * (1. - a2 * (1. / 42.) * (1. - a2 * (1. / 72.) *
-                                                 (1. - a2 * (1. / 110.) * (1. - a2 * (1. / 156.)))))));
-    *omc = 0.5 * a2 * (1. - a2 * (1. / 12.) * (1. - a2 * (1. / 30.) * (1. - a2 * (1. / 56.) * (1. - a2 * (1. / 90.) *
-                                                 (1. - a2 * (1. / 132.) * (1. - a2 * (1. / 182.)))))));
-  } else {
-    double sh, ch;
-    sincos(0.5 * a, &sh, &ch);
-    *sn = 2. * sh * ch;
-    *omc = 2. * sh * sh;
-  }
-}
-
 // sin(a theta), 1 - cos(a theta) in float (Taylor for |a theta| <= 0.5: error < 1e-10)
 __device__ __forceinline__ void rot_sc_f(const ProjArgs& A, float s, float* sn, float* omc) {
   const float a = s * A.theta;
@@ -337,8 +320,12 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
   double p0d[3] = {cd[0], cd[1], cd[2]};
   float E[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};  // E(s0)^T, row-major
   if (moving) {
-    double sn, omc;
-    rot_sc_d(A, (double)s_c, &sn, &omc);
+    // sin / 1 - cos of the rotation to s0 in float32: a relative error of ~6e-8 on terms of
+    // at most |a| |y| (a = s0 theta <= the sweep's yaw) moves a 100 m point by < 2e-7 m, i.e.
+    // < 2e-9 rad -- far below the box-edge tolerance; the rotation itself stays in double
+    float fsn, fomc;
+    rot_sc_f(A, s_c, &fsn, &fomc);
+    const double sn = fsn, omc = fomc;
     const double y[3] = {cd[0] - (double)s_c * A.vd[0], cd[1] - (double)s_c * A.vd[1],
                          cd[2] - (double)s_c * A.vd[2]};
     rot_apply(A.axis_d, sn, omc, y, p0d);
