@@ -291,12 +291,13 @@ int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles
  * at its view direction, A17); sh != NULL -> Eq. 1 literally (A30): SH_i(d)
  * evaluated per (ray, particle) at the ray's unit direction d from sh (device, the
  * particle set's [n][(sh_degree+1)^2][3] coefficients, indexed by the sorted ids).
- * lidar_producers (LiDAR render only; outputs are identical for every value): producer
- * warps per work item of the producer / consumer pipeline.  0 or 1 = the default,
- * throughput-optimised shape (1 producer + 1 consumer warp, 2 chunk slots: the least SM
- * resources per item, best when several scans are in flight); 3 = the latency-optimised
- * shape (3 producers, 3 slots: the shortest single scan); 2 = in between.  Other values:
- * INVALID_ARGUMENT. */
+ * lidar_producers (LiDAR render only; outputs are identical for every value): the
+ * pipeline shape per work item (<= 32 rays of one tile).  0 = the default, throughput-
+ * optimised shape: one warp per item doing box tests, member pairs, responses and the
+ * per-ray chain itself (the least SM resources per item -- best when several scans are in
+ * flight); 1, 2, 3 = a producer / consumer pipeline with that many producer warps feeding one
+ * consumer warp; 3 is the latency-optimised shape (the shortest single scan).  Other
+ * values: INVALID_ARGUMENT. */
 typedef struct {
   float alpha_min, alpha_max, T_min;
   const float* sh;

@@ -293,10 +293,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 // and culling on/off.
 // pipeline shape: P producers, NS chunk slots (a producer claims its chunk's slot one
 // iteration after the box test), CAP pairs per slot, chosen per call
-// (simuli_render_params.lidar_producers): (1, 2, 256) = throughput (config B, four scans in
-// flight: 275 -> 289 M rays/s against (3, 3, 384); one scan alone 345 us), (3, 3, 384) =
-// latency (one scan alone 173 us; round 1's (3, 6, 512): 182 us).  SIMULI_LIDAR_VARIANT
-// (P * 10000 + NS * 1000 + CAP) overrides it for tuning sweeps.
+// (simuli_render_params.lidar_producers): 3 -> (3, 3, 384), the latency shape (one config-B
+// scan alone: 173 us; round 1's (3, 6, 512): 182 us), 2 -> (2, 3, 384), 1 -> (1, 2, 256);
+// 0 (default) -> k_render_lidar_w below, one warp per item, the throughput shape (config B
+// with scans in flight: 258 / 289 / 309 M rays/s for 3 producers / 1 producer / warp per
+// item).  SIMULI_LIDAR_VARIANT (P * 10000 + NS * 1000 + CAP, or 1..8 for warp-per-item
+// shapes) overrides it for tuning sweeps.
 
 template <int CAP>
 struct LidarSlot {
@@ -761,6 +763,259 @@ __global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A
 }
 
 
+// ---------------------------------------------------------------- LiDAR, warp per item
+// One warp per work item, W items per CTA, no inter-warp hand-off: the warp walks the
+// item's list in 32-entry chunks with a software pipeline -- box(c + 3) by cp.async (ids a
+// chunk earlier), the exact A12 masks of chunk c + 1 and its member entries' records by
+// cp.async, while chunk c is finished (transpose, member pairs ray-major, responses with
+// every lane busy, then the per-ray chain).  Same responses, chain order and operands as
+// k_render_lidar: identical outputs.  The fewest SM resources per item; the longest lists
+// become a serial chain (one scan alone: 348 us).
+template <int CAP>
+struct WarpItemSmem {
+  float4 ray[32][3];
+  float4 box[3][32];
+  float4 rec[2][32][4];
+  float2 at[CAP];
+  uint16_t pairs[CAP];
+  uint32_t pid[2][32];
+  float col_phi[32], beam_el[32];
+  int col_id[32], beam_id[32];
+};
+
+template <int W, int CAP, bool PRAY>
+__global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpItemSmem<CAP>& S = reinterpret_cast<WarpItemSmem<CAP>*>(smem_raw)[warp];
+  const int64_t item = (int64_t)blockIdx.x * W + warp;
+  if (item >= A.n_items) return;  // warp-uniform
+  const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
+  const int tile = A.order ? __ldg(A.order + tslot) : tslot;
+  const int et = tile / A.n_theta, at_ = tile % A.n_theta;
+  const int bgi = sub / A.n_cg, cgi = sub % A.n_cg;
+  const int b0 = __ldg(A.etb_off + et) + bgi * A.bg, b1 = min(__ldg(A.etb_off + et + 1), b0 + A.bg);
+  const int c0 = __ldg(A.atc_off + at_) + cgi * A.cg, c1 = min(__ldg(A.atc_off + at_ + 1), c0 + A.cg);
+  const int nb = b1 - b0, nc = c1 - c0;
+  if (nb <= 0 || nc <= 0) return;  // warp-uniform
+  const int R = nb * nc;
+  {
+    const int j = lane < nc ? __ldg(A.atc + c0 + lane) : 0;
+    S.col_id[lane] = j;
+    S.col_phi[lane] = lane < nc ? __ldg(A.ray_az + j) : 0.f;
+    const int b = lane < nb ? __ldg(A.etb + b0 + lane) : 0;
+    S.beam_id[lane] = b;
+    S.beam_el[lane] = lane < nb ? __ldg(A.ray_el + (size_t)b * A.n_az) : 0.f;
+  }
+  const int2 rg = __ldg(A.ranges + tile);
+  const int len = rg.y - rg.x;
+  const int nchunks = (len + 31) >> 5;
+  auto ld_id = [&](int c) -> uint32_t {
+    const int p = 32 * c + lane;
+    return (c < nchunks && p < len) ? __ldg(A.ids + rg.x + p) : 0u;
+  };
+  auto issue_box = [&](int c, uint32_t id) {
+    if (c < nchunks && 32 * c + lane < len) cp_async16(&S.box[c % 3][lane], A.record + (size_t)id * 5 + 4);
+  };
+  uint32_t idq0 = ld_id(0), idq1 = ld_id(1), idq2 = ld_id(2);
+  issue_box(0, idq0);
+  issue_box(1, idq1);
+  cp_async_commit();
+  __syncwarp();
+  int ray = 0;
+  RayF rf;
+  {
+    double o[3] = {0, 0, 0}, dd[3] = {0, 0, 0};
+    if (lane < R) {
+      const int bi = lane / nc, ci = lane % nc;
+      const int j = S.col_id[ci];
+      ray = S.beam_id[bi] * A.n_az + j;
+      double Rm[9];
+      pose_at_d(A.pose, (double)__ldg(A.ray_s + j), Rm, o);
+      double sa, ca, se, ce;
+      sincos((double)S.col_phi[ci], &sa, &ca);
+      sincos((double)S.beam_el[bi], &se, &ce);
+      const double u[3] = {ce * ca, ce * sa, se};
+#pragma unroll
+      for (int i = 0; i < 3; ++i) dd[i] = Rm[3 * i] * u[0] + Rm[3 * i + 1] * u[1] + Rm[3 * i + 2] * u[2];
+      if (A.ray_od) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          A.ray_od[6 * (size_t)ray + i] = o[i];
+          A.ray_od[6 * (size_t)ray + 3 + i] = dd[i];
+        }
+      }
+    }
+    split_ray(o, dd, rf);
+    S.ray[lane][0] = make_float4(rf.o_hi[0], rf.o_hi[1], rf.o_hi[2], rf.o_lo[0]);
+    S.ray[lane][1] = make_float4(rf.o_lo[1], rf.o_lo[2], rf.d_hi[0], rf.d_hi[1]);
+    S.ray[lane][2] = make_float4(rf.d_hi[2], rf.d_lo[0], rf.d_lo[1], rf.d_lo[2]);
+  }
+  float shb[PRAY ? 16 : 1];
+  if (PRAY) {
+    const float dx = rf.d_hi[0] + rf.d_lo[0], dy = rf.d_hi[1] + rf.d_lo[1], dz = rf.d_hi[2] + rf.d_lo[2];
+    sh_basis3(dx, dy, dz, shb);
+  }
+  float cphi[8], bel[4];
+#pragma unroll
+  for (int ci = 0; ci < 8; ++ci) cphi[ci] = S.col_phi[ci];
+#pragma unroll
+  for (int bi = 0; bi < 4; ++bi) bel[bi] = S.beam_el[bi];
+  auto box_mask = [&](const float4 bx) -> uint32_t {
+    uint32_t colbits = 0;
+    if (__fsub_rn(bx.y, bx.x) >= A.two_pi_f) {
+      colbits = (nc == 32) ? 0xffffffffu : ((1u << nc) - 1u);
+    } else {
+      const float lo2 = bx.x < -A.pi_f ? __fadd_rn(bx.x, A.two_pi_f) : INFINITY;
+      const float hi2 = bx.y > A.pi_f ? __fsub_rn(bx.y, A.two_pi_f) : -INFINITY;
+#pragma unroll
+      for (int ci = 0; ci < 8; ++ci) {
+        const float p = cphi[ci];
+        const bool in = ci < nc && ((bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2);
+        colbits |= (uint32_t)in << ci;
+      }
+      for (int ci = 8; ci < nc; ++ci) {
+        const float p = S.col_phi[ci];
+        const bool in = (bx.x <= p && p <= bx.y) || lo2 <= p || p <= hi2;
+        colbits |= (uint32_t)in << ci;
+      }
+    }
+    uint32_t m = 0;
+    if (colbits) {
+      uint32_t beambits = 0;
+#pragma unroll
+      for (int bi = 0; bi < 4; ++bi) {
+        const float w = bel[bi];
+        beambits |= (uint32_t)(bi < nb && bx.z <= w && w <= bx.w) << bi;
+      }
+      for (int bi = 4; bi < nb; ++bi) {
+        const float w = S.beam_el[bi];
+        beambits |= (uint32_t)(bx.z <= w && w <= bx.w) << bi;
+      }
+      for (uint32_t bb = beambits; bb; bb &= bb - 1u) m |= colbits << ((__ffs(bb) - 1) * nc);
+    }
+    return m;
+  };
+  auto fetch_rec = [&](int c, uint32_t m, uint32_t id) {
+    if (m) {
+      const float4* src = A.record + (size_t)id * 5;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cp_async16(&S.rec[c & 1][lane][q], src + q);
+    }
+    S.pid[c & 1][lane] = id;
+  };
+  uint32_t done_mask = R == 32 ? 0u : ~((1u << R) - 1u);
+  cp_async_wait<0>();
+  __syncwarp();
+  uint32_t m_next = (nchunks > 0 && lane < len) ? box_mask(S.box[0][lane]) : 0u;
+  fetch_rec(0, m_next, idq0);
+  issue_box(2, idq2);
+  cp_async_commit();
+  uint32_t idq3 = ld_id(3);
+  float T = 1.f, z0 = 0.f, z1 = 0.f, z2 = 0.f, D = 0.f, Wt = 0.f;
+  int ncon = 0, ni = 0, nv = len;
+  bool done = lane >= R;
+  for (int c = 0; c < nchunks; ++c) {
+    const uint32_t m_cur = m_next;
+    m_next = 0u;
+    if (c + 1 < nchunks) {
+      if (32 * (c + 1) + lane < len) m_next = box_mask(S.box[(c + 1) % 3][lane]) & ~done_mask;
+      fetch_rec(c + 1, m_next, idq1);
+      issue_box(c + 3, idq3);
+    }
+    cp_async_commit();
+    idq1 = idq2;
+    idq2 = idq3;
+    idq3 = ld_id(c + 4);
+    cp_async_wait<1>();
+    __syncwarp();
+    const uint32_t my = warp_transpose32(m_cur, lane);
+    const uint32_t mine = done ? 0u : my;
+    const int cnt = __popc(mine);
+    int inc = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += t;
+    }
+    const int off_r = inc - cnt;
+    const int K = min(__shfl_sync(0xffffffffu, inc, 31), CAP);
+    {
+      int i = off_r;
+      for (uint32_t t = mine; t && i < CAP; t &= t - 1u, ++i) S.pairs[i] = (uint16_t)((lane << 5) | (__ffs(t) - 1));
+    }
+    __syncwarp();
+    const float4(&rec)[32][4] = S.rec[c & 1];
+    for (int i = lane; i < K; i += 32) {
+      const int v = S.pairs[i];
+      RayF rr;
+      unpack_ray(S.ray[v >> 5], rr);
+      float tau;
+      const float a = pair_alpha(rec[v & 31], rr, A.alpha_max, &tau);
+      S.at[i] = make_float2(a, tau);
+    }
+    __syncwarp();
+    uint32_t rem = mine;
+    int idx = off_r;
+    while (rem) {
+      const int e = __ffs(rem) - 1;
+      rem &= rem - 1u;
+      float2 a;
+      if (idx < CAP) {
+        a = S.at[idx];
+      } else {
+        a.x = pair_alpha(rec[e], rf, A.alpha_max, &a.y);
+      }
+      ++idx;
+      ++ni;
+      if (!(a.y < A.near_tau || a.x < A.alpha_min)) {
+        const float Tn = T * (1.f - a.x);
+        if (Tn < A.T_min) {
+          done = true;
+          rem = 0u;
+          nv = 32 * c + e + 1;
+        } else {
+          const float w = a.x * T;
+          float fv[3];
+          if (PRAY) {
+            sh_dot(A.sh + (size_t)S.pid[c & 1][e] * A.sh_ncoef * 3, A.sh_ncoef, shb, fv);
+          } else {
+            const float4 f = rec[e][3];
+            fv[0] = f.y; fv[1] = f.z; fv[2] = f.w;
+          }
+          z0 = fmaf(w, fv[0], z0);
+          z1 = fmaf(w, fv[1], z1);
+          z2 = fmaf(w, fv[2], z2);
+          D = fmaf(w, a.y, D);
+          Wt += w;
+          ++ncon;
+          T = Tn;
+        }
+      }
+    }
+    done_mask = __ballot_sync(0xffffffffu, done);
+    if (done_mask == 0xffffffffu) break;
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  if (lane >= R) return;
+  if (A.zeta) {
+    A.zeta[3 * (size_t)ray] = z0;
+    A.zeta[3 * (size_t)ray + 1] = z1;
+    A.zeta[3 * (size_t)ray + 2] = z2;
+  }
+  if (A.opacity) A.opacity[ray] = Wt;
+  if (A.depth_accum) A.depth_accum[ray] = D;
+  if (A.depth) A.depth[ray] = Wt > 0.f ? D / Wt : 0.f;
+  if (A.intensity) A.intensity[ray] = z0;
+  if (A.raydrop) A.raydrop[ray] = raydrop_prob(z1, z2);
+  if (A.final_T) A.final_T[ray] = T;
+  if (A.n_contrib) A.n_contrib[ray] = ncon;
+  if (A.n_visited) A.n_visited[ray] = nv;
+  if (A.n_inbox) A.n_inbox[ray] = ni;
+}
+
+
 }  // namespace
 }  // namespace simuli
 
@@ -833,17 +1088,33 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
   using I4 = integral_constant<int, 4>;
   using I6 = integral_constant<int, 6>;
   using I8 = integral_constant<int, 8>;
+  auto launch_w = [&](auto w_tag, auto cap_tag) {
+    constexpr int W_ = decltype(w_tag)::value, CAP_ = decltype(cap_tag)::value;
+    constexpr size_t smem = sizeof(WarpItemSmem<CAP_>) * W_;
+    auto kern = A.sh ? k_render_lidar_w<W_, CAP_, true> : k_render_lidar_w<W_, CAP_, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)((A.n_items + W_ - 1) / W_), 32 * W_, smem, st>>>(A);
+  };
   SIMULI_REQUIRE(rp->lidar_producers >= 0 && rp->lidar_producers <= 3,
                  "simuli_render_lidar: lidar_producers must be 0..3");
   if (variant == 0) {
     switch (rp->lidar_producers) {
-      case 3: launch(I3{}, I3{}, integral_constant<int, 384>{}); break;                       // latency
+      case 3: launch(I3{}, I3{}, integral_constant<int, 384>{}); break;  // latency
       case 2: launch(I2{}, I3{}, integral_constant<int, 384>{}); break;
-      default: launch(integral_constant<int, 1>{}, I2{}, integral_constant<int, 256>{}); break;  // throughput
+      case 1: launch(integral_constant<int, 1>{}, I2{}, integral_constant<int, 256>{}); break;
+      default: launch_w(I4{}, integral_constant<int, 128>{}); break;    // throughput: warp per item
     }
     return launch_check("simuli_render_lidar");
   }
   switch (variant) {
+    case 1: launch_w(I4{}, integral_constant<int, 256>{}); break;
+    case 2: launch_w(I2{}, integral_constant<int, 256>{}); break;
+    case 3: launch_w(I4{}, integral_constant<int, 128>{}); break;
+    case 4: launch_w(I8{}, integral_constant<int, 128>{}); break;
+    case 5: launch_w(I4{}, integral_constant<int, 64>{}); break;
+    case 6: launch_w(I2{}, integral_constant<int, 128>{}); break;
+    case 7: launch_w(integral_constant<int, 1>{}, integral_constant<int, 128>{}); break;
+    case 8: launch_w(I8{}, integral_constant<int, 64>{}); break;
     case 24512: launch(I2{}, I4{}, integral_constant<int, 512>{}); break;
     case 24384: launch(I2{}, I4{}, integral_constant<int, 384>{}); break;
     case 48256: launch(I4{}, I8{}, integral_constant<int, 256>{}); break;
