@@ -957,6 +957,49 @@ __global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
     __syncwarp();
     uint32_t rem = mine;
     int idx = off_r;
+    if (!PRAY) {
+      // branch-free, two members per step: both members' loads issued together, only T
+      // carries a dependency (same operations and order as the per-member form)
+      while (__any_sync(0xffffffffu, rem != 0u)) {
+        int e2[2];
+        bool h2[2];
+        float2 a2[2];
+        float4 f2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          h2[u] = rem != 0u;
+          e2[u] = h2[u] ? __ffs(rem) - 1 : 0;
+          rem &= rem - 1u;
+          a2[u] = S.at[min(idx + u, CAP - 1)];
+          f2[u] = rec[e2[u]][3];
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const bool has = h2[u] && !done;
+          float2 a = a2[u];
+          if (has && idx >= CAP) a.x = pair_alpha(rec[e2[u]], rf, A.alpha_max, &a.y);
+          const bool valid = has && !(a.y < A.near_tau || a.x < A.alpha_min);  // A13, A15
+          const float Tn = T * (1.f - a.x);
+          const bool term = valid && Tn < A.T_min;  // A14
+          const bool comp = valid && !term;
+          const float w = a.x * T;
+          z0 = comp ? fmaf(w, f2[u].y, z0) : z0;
+          z1 = comp ? fmaf(w, f2[u].z, z1) : z1;
+          z2 = comp ? fmaf(w, f2[u].w, z2) : z2;
+          D = comp ? fmaf(w, a.y, D) : D;
+          Wt = comp ? Wt + w : Wt;
+          T = comp ? Tn : T;
+          ncon += comp ? 1 : 0;
+          ni += has ? 1 : 0;
+          if (term) {
+            done = true;
+            nv = 32 * c + e2[u] + 1;
+          }
+          idx += has ? 1 : 0;
+        }
+        if (done) rem = 0u;
+      }
+    } else
     while (rem) {
       const int e = __ffs(rem) - 1;
       rem &= rem - 1u;
