@@ -440,8 +440,10 @@ def run_gpu(args):
     e_beg.record(stream)
     for st in streams:
         st.wait_event(e_beg)
+    torch.cuda.nvtx.range_push(f"headline: {args.steps} scans, {S} in flight")
     for i in range(args.steps):
         rs[i % S].scan(*my[args.warmup + i], stream=streams[i % S])
+    torch.cuda.nvtx.range_pop()
     for st in streams:
         ej = torch.cuda.Event()
         ej.record(st)
@@ -460,17 +462,24 @@ def run_gpu(args):
     # CUDA events; median / p10 / p90 (SURVEY §8(d) timing protocol)
     n_stage = N_STAGE
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_stage)]
+    nvtx = torch.cuda.nvtx
     for i in range(n_stage):
         flush.zero_()
         p0, p1 = my[(args.warmup + i) % len(my)]
         r.set_poses(p0, p1)
         e = ev[i]
         e[0].record(stream)
+        nvtx.range_push("project")
         r.project()
+        nvtx.range_pop()
         e[1].record(stream)
+        nvtx.range_push("bin_sort")
         r.bin_sort()
+        nvtx.range_pop()
         e[2].record(stream)
+        nvtx.range_push("render")
         r.render()
+        nvtx.range_pop()
         e[3].record(stream)
     torch.cuda.synchronize()
     # per-stage throughput: each stage alone, N_STAGE launches spread over the S renderers /
