@@ -40,9 +40,17 @@ def SM():
 
 
 def gpu_records(r):
-    rec = r.record.cpu().numpy().astype(np.float64)
+    """The GPU's 80-byte records as the oracle's record dict.  Rows of particles the GPU did
+    not write (tile count 0 without write_all_records: never listed, never read) are set to
+    NaN explicitly instead of passing on whatever the buffer held."""
+    raw = r.record.cpu().numpy().copy()
+    written = r.tile_count.cpu().numpy() > 0
+    if r.params.write_all_records:
+        written |= np.isfinite(raw[:, 16])
+    raw[~written] = np.nan
+    rec = raw.astype(np.float64)
     return {"mu": rec[:, 0:3], "Mrows": rec[:, 3:12], "sigma": rec[:, 12], "feat": rec[:, 13:16],
-            "box": r.record.cpu().numpy()[:, 16:20].copy()}
+            "box": raw[:, 16:20].copy()}
 
 
 def lidar_run(SM, cfg, scene, **kw):
