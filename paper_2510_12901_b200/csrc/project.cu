@@ -246,6 +246,32 @@ __device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c
 // Firing times are decisions of float32 accuracy only (an error of 1e-7 in s moves a point by
 // < 1e-9 rad), so they stay in float32.
 
+// atan2 in double to ~1e-13 rad (the box edges need ~1e-9; libdevice's full-precision
+// atan2 costs ~75 instructions, half of them materialising its 64-bit coefficients): |t| =
+// min / max reduced to [0, tan(pi/8)] by atan t = pi/4 + atan((t - 1) / (t + 1)), then
+// atan t = t + t u P(u), u = t^2, P a degree-7 least-squares Chebyshev fit (max error
+// 1.1e-13 on the interval) with its coefficients in constant memory (DFMA operands, no
+// immediate moves).  Quadrants and signed zeros as C's atan2 except atan2(+-0, -0) = 0.
+__constant__ double c_atan_p[8] = {-0.33333333333168147, 0.19999999929984685, -0.14285707051757754,
+                                   0.11110796545187183, -0.09083864602009568, 0.07603707049930997,
+                                   -0.06025842127055635, 0.03297683826326521};
+__device__ __forceinline__ double atan2_fast(double y, double x) {
+  const double ax = fabs(x), ay = fabs(y);
+  const double mx = fmax(ax, ay), mn = fmin(ax, ay);
+  double t = mx > 0.0 ? mn / mx : 0.0;
+  const bool big = t > 0.41421356237309503;
+  if (big) t = (t - 1.0) / (t + 1.0);
+  const double u = t * t;
+  double p = c_atan_p[7];
+#pragma unroll
+  for (int i = 6; i >= 0; --i) p = fma(p, u, c_atan_p[i]);
+  double r = fma(t * u, p, t);
+  if (big) r += 0.78539816339744828;
+  if (ay > ax) r = 1.5707963267948966 - r;
+  if (x < 0.0) r = 3.1415926535897931 - r;
+  return signbit(y) ? -r : r;
+}
+
 // sin(a theta), 1 - cos(a theta) in float (Taylor for |a theta| <= 0.5: error < 1e-10)
 __device__ __forceinline__ void rot_sc_f(const ProjArgs& A, float s, float* sn, float* omc) {
   const float a = s * A.theta;
@@ -337,8 +363,8 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
     E[6] = fs * k[1] + fo * k[2] * k[0]; E[7] = -fs * k[0] + fo * k[2] * k[1]; E[8] = 1.f + fo * (k[2] * k[2] - 1.f);
   }
   const double rho0d = sqrt(p0d[0] * p0d[0] + p0d[1] * p0d[1]);
-  *a0 = atan2(p0d[1], p0d[0]);
-  *e0 = atan2(p0d[2], rho0d);
+  *a0 = atan2_fast(p0d[1], p0d[0]);
+  *e0 = atan2_fast(p0d[2], rho0d);
   const float p0[3] = {(float)p0d[0], (float)p0d[1], (float)p0d[2]};
   const float rho0 = (float)rho0d, rho02 = (float)(rho0d * rho0d);
   bool ok = rho0d * rho0d + p0d[2] * p0d[2] >= (double)A.r_min * (double)A.r_min;
