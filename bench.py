@@ -13,8 +13,8 @@ only reduces the timers / counters.
 Prints ONE JSON line on rank 0.  value = whole-job LiDAR rays/s (scans/s in
 ``scans_per_s``): the K timed scans run six in flight per GPU (six renderers with their
 own buffers on six streams, shared resident scene -- one scan's latency-bound stages
-overlap the others'; with the throughput-default kernels 3 / 4 / 5 / 6 / 8 in flight
-measured 286 / 302 / 308 / 309 / 306 M rays/s), timed between two CUDA events on the launching stream,
+overlap the others'; with the default kernels 5 / 6 / 8 in flight measured 301 / 305 /
+301 M rays/s), timed between two CUDA events on the launching stream,
 bracketed by barrier + synchronize, max over ranks; inputs exceed the L2, so no flush.  A
 second pass runs scans one at a time with the L2 flushed and per-stage CUDA events: the
 stage breakdown and roofline, and ``latency_ms_per_scan``; a third the same with the
@@ -523,8 +523,8 @@ def run_gpu(args):
                     "render_ms_median": statistics.median(e[0].elapsed_time(e[1]) for e in lat),
                     "scan_ms_median": statistics.median(e[0].elapsed_time(e[1]) for e in lat_scan),
                     "note": "one scan at a time, L2 flushed, the latency-optimised render pipeline (3 producer "
-                            "warps + 1 consumer warp per item); the headline uses the throughput default (one warp "
-                            "per item)"}
+                            "warps + 1 consumer warp per item); the headline uses the default hybrid (the longest "
+                            "items by that pipeline, the rest one warp per item)"}
     clk = clocks.stop()
     cap_checks.append(check_capacity("stage pass"))
     samples = {"project": [e[0].elapsed_time(e[1]) for e in ev], "bin_sort": [e[1].elapsed_time(e[2]) for e in ev],

@@ -292,12 +292,13 @@ int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles
  * evaluated per (ray, particle) at the ray's unit direction d from sh (device, the
  * particle set's [n][(sh_degree+1)^2][3] coefficients, indexed by the sorted ids).
  * lidar_producers (LiDAR render only; outputs are identical for every value): the
- * pipeline shape per work item (<= 32 rays of one tile).  0 = the default, throughput-
- * optimised shape: one warp per item doing box tests, member pairs, responses and the
- * per-ray chain itself (the least SM resources per item -- best when several scans are in
- * flight); 1, 2, 3 = a producer / consumer pipeline with that many producer warps feeding one
- * consumer warp; 3 is the latency-optimised shape (the shortest single scan).  Other
- * values: INVALID_ARGUMENT. */
+ * pipeline shape per work item (<= 32 rays of one tile).  1, 2, 3 = a producer / consumer
+ * pipeline with that many producer warps feeding one consumer warp (3: the shortest single
+ * scan); 4 = one warp per item doing box tests, member pairs, responses and the per-ray
+ * chain itself (the least SM resources per item: the highest throughput when several scans
+ * are in flight, a long single scan); 0 = the default hybrid: the longest items (one per
+ * SM) by the 3-producer pipeline, the rest one warp per item.  Other values:
+ * INVALID_ARGUMENT. */
 typedef struct {
   float alpha_min, alpha_max, T_min;
   const float* sh;

@@ -223,6 +223,7 @@ struct LidarArgs {
   const float *ray_az, *ray_el, *ray_s;
   int n_theta, n_az, items_per_tile, cg, bg, n_cg;
   int64_t n_items;
+  int64_t n_long;  // hybrid render: items taken by the producer / consumer path
   PoseInterpD pose;
   float pi_f, two_pi_f, near_tau, alpha_min, alpha_max, T_min;
   float *zeta, *opacity, *depth_accum, *depth, *intensity, *raydrop, *final_T;
@@ -295,10 +296,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 // iteration after the box test), CAP pairs per slot, chosen per call
 // (simuli_render_params.lidar_producers): 3 -> (3, 3, 384), the latency shape (one config-B
 // scan alone: 173 us; round 1's (3, 6, 512): 182 us), 2 -> (2, 3, 384), 1 -> (1, 2, 256);
-// 0 (default) -> k_render_lidar_w below, one warp per item, the throughput shape (config B
-// with scans in flight: 258 / 289 / 309 M rays/s for 3 producers / 1 producer / warp per
-// item).  SIMULI_LIDAR_VARIANT (P * 10000 + NS * 1000 + CAP, or 1..8 for warp-per-item
-// shapes) overrides it for tuning sweeps.
+// 4 -> k_render_lidar_w below, one warp per item, the leanest (config B with scans in
+// flight: 258 / 289 / 311 M rays/s for 3 producers / 1 producer / warp per item; one scan
+// alone 176 / 345 / 331 us); 0 (default) -> k_render_lidar_h, the hybrid: one (3, 3, 384)
+// producer / consumer item per SM for the longest lists, one warp per item for the rest
+// (305 M rays/s in flight, 175 us alone).  SIMULI_LIDAR_VARIANT (P * 10000 + NS * 1000 +
+// CAP, 1..8 warp-per-item shapes, 9 hybrid with SIMULI_LIDAR_NLONG) overrides it for sweeps.
 
 template <int CAP>
 struct LidarSlot {
@@ -391,11 +394,9 @@ __device__ __forceinline__ long long gtime() {
 #endif
 
 template <int P, int NS, int CAP, bool PRAY>
-__global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void pc_item(const LidarArgs& A, const int64_t item, unsigned char* smem_raw) {
   LidarSmem<P, NS, CAP>& S = *reinterpret_cast<LidarSmem<P, NS, CAP>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t item = blockIdx.x;
   const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
   const int tile = A.order ? __ldg(A.order + tslot) : tslot;
   SIMULI_CHECK(tile >= 0 && (int64_t)tile * A.items_per_tile < A.n_items, tile, A.n_items);
@@ -762,6 +763,12 @@ __global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A
   cp_async_wait<0>();
 }
 
+template <int P, int NS, int CAP, bool PRAY>
+__global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pc_item<P, NS, CAP, PRAY>(A, blockIdx.x, smem_raw);
+}
+
 
 // ---------------------------------------------------------------- LiDAR, warp per item
 // One warp per work item, W items per CTA, no inter-warp hand-off: the warp walks the
@@ -783,12 +790,9 @@ struct WarpItemSmem {
   int col_id[32], beam_id[32];
 };
 
-template <int W, int CAP, bool PRAY>
-__global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpItemSmem<CAP>& S = reinterpret_cast<WarpItemSmem<CAP>*>(smem_raw)[warp];
-  const int64_t item = (int64_t)blockIdx.x * W + warp;
+template <int CAP, bool PRAY>
+__device__ __forceinline__ void w_item(const LidarArgs& A, const int64_t item, WarpItemSmem<CAP>& S) {
+  const int lane = threadIdx.x & 31;
   if (item >= A.n_items) return;  // warp-uniform
   const int tslot = (int)(item / A.items_per_tile), sub = (int)(item % A.items_per_tile);
   const int tile = A.order ? __ldg(A.order + tslot) : tslot;
@@ -1058,6 +1062,29 @@ __global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
   if (A.n_inbox) A.n_inbox[ray] = ni;
 }
 
+template <int W, int CAP, bool PRAY>
+__global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  w_item<CAP, PRAY>(A, (int64_t)blockIdx.x * W + warp, reinterpret_cast<WarpItemSmem<CAP>*>(smem_raw)[warp]);
+}
+
+// Hybrid: the n_long longest items (the first ones: items follow the longest-first tile
+// order) by the producer / consumer pipeline (3 producers, its shortest critical path), the
+// rest one warp per item (the least resources): one scan alone is then bounded by the P/C
+// time of the longest lists while most items keep the lean path.
+template <int CAP, int WCAP, bool PRAY>
+__global__ void __launch_bounds__(128) k_render_lidar_h(const LidarArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if ((int64_t)blockIdx.x < A.n_long) {
+    pc_item<3, 3, CAP, PRAY>(A, blockIdx.x, smem_raw);
+  } else {
+    const int warp = threadIdx.x >> 5;
+    w_item<WCAP, PRAY>(A, A.n_long + ((int64_t)blockIdx.x - A.n_long) * 4 + warp,
+                       reinterpret_cast<WarpItemSmem<WCAP>*>(smem_raw)[warp]);
+  }
+}
+
 
 }  // namespace
 }  // namespace simuli
@@ -1138,18 +1165,41 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)((A.n_items + W_ - 1) / W_), 32 * W_, smem, st>>>(A);
   };
-  SIMULI_REQUIRE(rp->lidar_producers >= 0 && rp->lidar_producers <= 3,
-                 "simuli_render_lidar: lidar_producers must be 0..3");
+  auto launch_h = [&](int64_t n_long) {
+    constexpr int CAP_ = 384, WCAP_ = 128;
+    constexpr size_t s1 = sizeof(LidarSmem<3, 3, CAP_>), s2 = sizeof(WarpItemSmem<WCAP_>) * 4;
+    constexpr size_t smem = s1 > s2 ? s1 : s2;
+    A.n_long = n_long < A.n_items ? n_long : A.n_items;
+    auto kern = A.sh ? k_render_lidar_h<CAP_, WCAP_, true> : k_render_lidar_h<CAP_, WCAP_, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)(A.n_long + (A.n_items - A.n_long + 3) / 4), 128, smem, st>>>(A);
+  };
+  static const int64_t n_long_env = [] {
+    const char* v = getenv("SIMULI_LIDAR_NLONG");  // tuning only
+    return v ? (int64_t)atoll(v) : (int64_t)-1;
+  }();
+  // hybrid default: one producer / consumer item per SM (the longest lists), the rest one
+  // warp per item
+  static const int64_t n_long_default = [] {
+    int d = 0, v = 148;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    return (int64_t)v;
+  }();
+  SIMULI_REQUIRE(rp->lidar_producers >= 0 && rp->lidar_producers <= 4,
+                 "simuli_render_lidar: lidar_producers must be 0..4");
   if (variant == 0) {
     switch (rp->lidar_producers) {
       case 3: launch(I3{}, I3{}, integral_constant<int, 384>{}); break;  // latency
       case 2: launch(I2{}, I3{}, integral_constant<int, 384>{}); break;
       case 1: launch(integral_constant<int, 1>{}, I2{}, integral_constant<int, 256>{}); break;
-      default: launch_w(I4{}, integral_constant<int, 128>{}); break;    // throughput: warp per item
+      case 4: launch_w(I4{}, integral_constant<int, 128>{}); break;     // warp per item only
+      default: launch_h(n_long_env >= 0 ? n_long_env : n_long_default); break;  // hybrid
     }
     return launch_check("simuli_render_lidar");
   }
   switch (variant) {
+    case 9: launch_h(n_long_env >= 0 ? n_long_env : n_long_default); break;
     case 1: launch_w(I4{}, integral_constant<int, 256>{}); break;
     case 2: launch_w(I2{}, integral_constant<int, 256>{}); break;
     case 3: launch_w(I4{}, integral_constant<int, 128>{}); break;

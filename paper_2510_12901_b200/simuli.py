@@ -496,8 +496,8 @@ class LidarRenderer(_Frame):
                                     make_pose(cfg.pose_start), make_pose(cfg.pose_end), int(cfg.rs_iterations),
                                     ut[0], ut[1], ut[2], extent_sigma, int(enable_culling), int(write_all_records))
         self.rparams = RenderParams(*render_params, None, 0)
-        # render pipeline shape (simuli.h): 0 = throughput default (one warp per item),
-        # 1..3 = producer / consumer with that many producers (3 = latency); identical outputs
+        # render pipeline shape (simuli.h): 0 = hybrid default, 1..3 = producer / consumer
+        # with that many producers (3 = latency), 4 = one warp per item; identical outputs
         self.rparams.lidar_producers = int(render_producers)
         if per_ray_sh:  # Eq. 1 literally: SH_i(d) per (ray, particle) (A30)
             self.rparams.sh = scene_dev["sh"].data_ptr()

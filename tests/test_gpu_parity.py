@@ -228,13 +228,13 @@ def test_gpu_single_tile_bruteforce(SM, config):
 
 @pytest.mark.parametrize("per_ray_sh", [False, True])
 def test_lidar_render_pipeline_shapes_identical(SM, per_ray_sh):
-    """The LiDAR render's pipeline shapes (simuli_render_params.lidar_producers: 0 = one
-    warp per item, 1..3 = producer / consumer) run the same responses and chain: outputs
-    bit-identical (B subset, and tiles with more than 32 rays)."""
+    """The LiDAR render's pipeline shapes (simuli_render_params.lidar_producers: 0 = hybrid,
+    1..3 = producer / consumer, 4 = one warp per item) run the same responses and chain:
+    outputs bit-identical (B subset, and tiles with more than 32 rays)."""
     for cfg_name, n_phi, M in (("B", 16, 32), ("A", 2, 128)):
         scene = S.scene_for(cfg_name, n=200_000) if cfg_name == "B" else S.scene_for(cfg_name)
         outs = []
-        for prod in (0, 1, 2, 3):
+        for prod in (0, 1, 2, 3, 4):
             cfg = S.lidar_config(cfg_name)
             cfg.n_phi, cfg.max_rays_per_tile = n_phi, M
             r = lidar_run(SM, cfg, scene, render_producers=prod, per_ray_sh=per_ray_sh)
