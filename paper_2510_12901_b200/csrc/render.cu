@@ -338,18 +338,6 @@ __device__ __forceinline__ void unpack_ray(const float4* q, RayF& r) {
 // barrier event of the SM, and the spinning producers took the consumer's issue slots
 __device__ __forceinline__ bool mbar_wait_or_stop(unsigned long long* b, unsigned parity, volatile int* stop) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(b));
-#ifdef SIMULI_PROD_TRYWAIT
-  // hardware-suspended wait (up to SIMULI_PROD_TRYWAIT ns per try), the stop flag between tries
-  for (;;) {
-    unsigned ok;
-    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                 : "=r"(ok)
-                 : "r"(a), "r"(parity), "n"(SIMULI_PROD_TRYWAIT)
-                 : "memory");
-    if (ok) return true;
-    if (*stop) return false;
-  }
-#endif
   for (;;) {
     unsigned ok;
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
@@ -358,10 +346,7 @@ __device__ __forceinline__ bool mbar_wait_or_stop(unsigned long long* b, unsigne
                  : "memory");
     if (ok) return true;
     if (*stop) return false;
-#ifndef SIMULI_PROD_SLEEP
-#define SIMULI_PROD_SLEEP 256
-#endif
-    __nanosleep(SIMULI_PROD_SLEEP);  // a waiting producer is ahead of the consumer: poll slowly, leave it the issue slots
+    __nanosleep(256);  // a waiting producer is ahead of the consumer: poll slowly, leave it the issue slots
   }
 }
 
