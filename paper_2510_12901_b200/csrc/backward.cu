@@ -105,7 +105,7 @@ __device__ __forceinline__ int bwd_step(const BwdArgs& A, const RayF& rf, const 
   const float M[9] = {r[0].w, r[1].x, r[1].y, r[1].z, r[1].w, r[2].x, r[2].y, r[2].z, r[2].w};
   float d2;
   response(rf, mu, M, tau, &d2);
-  *rho = expf(-0.5f * d2);
+  *rho = __expf(-0.5f * d2);  // same as the render kernels (__expf)
   const float av = r[3].x * *rho;
   *alpha = fminf(A.alpha_max, av);
   *clamped = !(av < A.alpha_max);

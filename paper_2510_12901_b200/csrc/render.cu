@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
           const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
           float tau, d2;
           response(rf, mu, M, &tau, &d2);
-          const float alpha = fminf(A.alpha_max, r3.x * expf(-0.5f * d2));
+          const float alpha = fminf(A.alpha_max, r3.x * __expf(-0.5f * d2));
           if (tau < A.near_tau || alpha < A.alpha_min) continue;
           const float Tn = T * (1.f - alpha);
           if (Tn < A.T_min) {
@@ -357,7 +357,7 @@ __device__ __forceinline__ float pair_alpha(const float4* rec, const RayF& rf, f
   const float M[9] = {r0.w, r1.x, r1.y, r1.z, r1.w, r2.x, r2.y, r2.z, r2.w};
   float d2;
   response(rf, mu, M, tau, &d2);
-  return fminf(alpha_max, sig * expf(-0.5f * d2));
+  return fminf(alpha_max, sig * __expf(-0.5f * d2));
 }
 
 #ifdef SIMULI_RENDER_PROFILE
