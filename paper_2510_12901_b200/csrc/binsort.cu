@@ -6,7 +6,8 @@
 // the "Sort" kernel of tab:culling.
 //
 // Launch sequence (caller's stream; no host sync when pair_capacity >= 0):
-//   memset          one: pass histograms, counters, key range, every look-back status word
+//   memset          one: pass histograms, counters, key range, the look-back status words
+//                   of the count scan and the first pass (each pass clears the next's)
 //   k_count_scan    single-pass scan of the tile counts (decoupled look-back over
 //                   1024-particle blocks) + min / max depth-key bits of the pair-emitting
 //                   particles; the last block derives P, the key width
@@ -15,7 +16,8 @@
 //                   tid+256, ... binary-searching its owner in shared memory) of the
 //                   trimmed key (tile << b) | (depth bits - min) -- an order-preserving
 //                   map of (tile, depth bits) -- plus the digit histograms of every pass
-//   k_onesweep x 6  stable LSD onesweep, 8-bit digits; passes beyond the device-side pass
+//   k_onesweep x 6  stable LSD onesweep, 8-bit digits (10-bit: SIMULI_SORT_RB=10, tuning
+//                   only -- slower, profiles/r02_experiments.md); passes beyond the device-side pass
 //                   count exit at once (buffer parity is chosen on the device so the
 //                   last real pass lands in the caller's arrays).  Per 5120-key partition
 //                   (256 threads x 20 keys) a warp-level multisplit (ballot-built peer
@@ -44,6 +46,7 @@ constexpr int kLookW = 8;      // look-back window (predecessor partitions loade
 constexpr int kRankBatch = 4;  // ranking items whose match.any latencies overlap
 constexpr int kPart = kSortThreads * kSortItems;  // smallest partition of any sweep shape (status rows)
 constexpr int kMaxPasses = 6;  // 48 key bits: 16 tile bits + 32 depth bits at most
+constexpr int kRadixMax = 1024;  // digits of up to 10 bits
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 30) - 1;
 
 // device scalars: [0] P, [1] key-min bits, [2] key-max bits, [3] depth bits b,
@@ -51,6 +54,18 @@ constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kValMask = (1u << 3
 enum { S_P = 0, S_KMIN, S_KMAX, S_B, S_PASSES, S_TBITS, S_N };
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// digit width of the radix passes: 8 bits (256 digits) or 10 bits (1024 digits, one pass
+// fewer for the 38-bit keys of config B); SIMULI_SORT_RB overrides the default (tuning)
+int sort_rb() {
+  static const int rb = [] {
+    const char* v = getenv("SIMULI_SORT_RB");
+    const int r = v ? atoi(v) : 8;
+    return r == 10 ? 10 : 8;
+  }();
+  return rb;
+}
+int max_passes_of(int tbits, int rb) { return (32 + tbits + rb - 1) / rb; }
 
 int tile_bits_of(int32_t n_tiles) {
   int bits = 0;
@@ -62,11 +77,12 @@ struct Workspace {
   int64_t* block_sums;  // [nb+1]
   int64_t* scal;        // [S_N]
   // zeroed by one memset per call: zero .. zero + zero_bytes
-  uint32_t* hist;       // [kMaxPasses][256]
+  uint32_t* hist;       // [kMaxPasses][kRadixMax]
   uint32_t* counters;   // [kMaxPasses] sweep partition counters, [kMaxPasses..+4) scan / ranges counters
   uint32_t* kminmax;    // [2]: ~min, max depth-key bits of the pair-emitting particles (atomicMax)
   uint32_t* cstatus;    // [nb] look-back status of the count scan
-  uint32_t* status;     // [kMaxPasses][n_parts][256]
+  uint32_t* status;     // [max passes][n_parts][2^rb]; pass 0's rows in the zeroed region,
+                        // pass p + 1's rows zeroed by pass p's partitions
   char* zero;
   size_t zero_bytes;
   uint64_t* keys[2];    // [cap]
@@ -75,7 +91,7 @@ struct Workspace {
   size_t bytes;
 };
 
-Workspace carve(void* base, int64_t n, int64_t cap, int32_t n_tiles) {
+Workspace carve(void* base, int64_t n, int64_t cap, int32_t n_tiles, int rb) {
   Workspace w{};
   const int64_t nb = (n + kDupBlock - 1) / kDupBlock;
   w.parts = (cap + kPart - 1) / kPart;
@@ -89,14 +105,15 @@ Workspace carve(void* base, int64_t n, int64_t cap, int32_t n_tiles) {
   w.block_sums = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * (nb + 1)));
   w.scal = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * S_N));
   const size_t z0 = off;
-  w.hist = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses * 256));
+  w.hist = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses * kRadixMax));
   w.counters = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (kMaxPasses + 4)));
   w.kminmax = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * 2));
   w.cstatus = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * (nb > 0 ? nb : 1)));
-  w.status = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * kMaxPasses * (w.parts > 0 ? w.parts : 1) * 256));
+  const size_t row = sizeof(uint32_t) * (size_t)(w.parts > 0 ? w.parts : 1) << rb;  // one pass's status
+  w.status = reinterpret_cast<uint32_t*>(take(row));
   w.zero = p ? p + z0 : nullptr;
   w.zero_bytes = off - z0;
-  (void)n_tiles;
+  take(row * (size_t)(max_passes_of(tile_bits_of(n_tiles), rb) - 1));  // status of passes 1..
   for (int i = 0; i < 2; ++i) w.keys[i] = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * cap));
   w.vals_alt = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * cap));
   w.bytes = off;
@@ -155,7 +172,8 @@ constexpr int kScanPer = kScanThreads * kScanItems;  // = 8 duplicate blocks
 static_assert(kScanPer % kDupBlock == 0, "scan blocks cover whole duplicate blocks");
 __global__ void __launch_bounds__(kScanThreads) k_count_scan(const int* __restrict__ count,
                                                              const float* __restrict__ key, int64_t n, int64_t nsb,
-                                                             int64_t nb, int tile_bits, int64_t* __restrict__ block_sums,
+                                                             int64_t nb, int tile_bits, int rb,
+                                                             int64_t* __restrict__ block_sums,
                                                              uint32_t* __restrict__ cstatus, uint32_t* __restrict__ kminmax,
                                                              uint32_t* __restrict__ ctr, int64_t* __restrict__ scal,
                                                              int64_t* __restrict__ n_pairs) {
@@ -287,7 +305,7 @@ __global__ void __launch_bounds__(kScanThreads) k_count_scan(const int* __restri
   scal[S_KMAX] = mx;
   scal[S_B] = b;
   // at least one pass whenever there are pairs: it also writes the ids
-  scal[S_PASSES] = P > 0 ? max(1, (b + tile_bits + 7) / 8) : 0;
+  scal[S_PASSES] = P > 0 ? max(1, (b + tile_bits + rb - 1) / rb) : 0;
   scal[S_TBITS] = tile_bits;
 }
 
@@ -312,7 +330,7 @@ struct DupArgs {
   int n_cols_total;
   uint64_t* keys[2];
   uint32_t* vals[2];
-  uint32_t* hist;      // [kMaxPasses][256]
+  uint32_t* hist;      // [kMaxPasses][kRadixMax]
   int32_t* tile_cnt;   // unused
   int id_bits, packed; // packed: one u64 word = (key << id_bits) | id
   int n_tiles;
@@ -324,8 +342,10 @@ struct DupArgs {
 // prefix of the counts (no shared-memory binary search, no bank conflicts), so a particle
 // spanning hundreds of tiles does not serialise one lane.  Pairs are written in particle
 // order (the stable sort then keeps equal keys in id order).
+template <int RB>
 __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
-  __shared__ uint32_t s_hist[kMaxPasses * 256];
+  constexpr int R = 1 << RB;
+  __shared__ uint32_t s_hist[(RB == 8 ? kMaxPasses : 5) * R];
   __shared__ int s_wtot[kDupThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t gb = (int64_t)blockIdx.x * kDupBlock;
@@ -335,7 +355,7 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
   const int s0 = passes & 1;  // output buffer parity so the last pass lands in buffer 0
   uint64_t* kout = s0 ? A.keys[1] : A.keys[0];
   uint32_t* vout = s0 ? A.vals[1] : A.vals[0];
-  for (int i = tid; i < passes * 256; i += kDupThreads) s_hist[i] = 0;
+  for (int i = tid; i < passes * R; i += kDupThreads) s_hist[i] = 0;
   constexpr int kGroups = kDupBlock / kDupThreads;  // groups of 32 particles per warp
   const int64_t gw = gb + (int64_t)warp * 32 * kGroups;
   int c[kGroups], wsum = 0;
@@ -398,14 +418,14 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
           kout[pos] = key;
           vout[pos] = (uint32_t)id;
         }
-        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * 256 + (int)((key >> (8 * p)) & 0xFF)], 1u);
+        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p * R + (int)((key >> (RB * p)) & (R - 1))], 1u);
       }
     }
     base += total;
   }
   __syncthreads();
-  for (int i = tid; i < passes * 256; i += kDupThreads)
-    if (s_hist[i]) atomicAdd(&A.hist[i], s_hist[i]);
+  for (int i = tid; i < passes * R; i += kDupThreads)
+    if (s_hist[i]) atomicAdd(&A.hist[(i / R) * kRadixMax + (i % R)], s_hist[i]);
 }
 
 // ------------------------------------------------------------------ onesweep pass
@@ -417,8 +437,9 @@ struct SweepArgs {
   int pass;
   int id_bits;          // packed mode: low id_bits of every word are the particle id
   uint32_t* ids_final;  // packed mode: the last pass also writes the ids here
-  const uint32_t* hist;  // [256] of this pass
-  uint32_t* status;      // [n_parts][256] of this pass
+  const uint32_t* hist;  // [2^rb] of this pass
+  uint32_t* status;      // [n_parts][2^rb] of this pass
+  uint32_t* status_next; // the next pass's rows (zeroed here, one row per partition) or NULL
   uint32_t* counter;
 };
 
@@ -437,14 +458,15 @@ __device__ __forceinline__ long long sort_gtime() {
 #define SORT_STAMP(i)
 #endif
 
-// lanes of the warp holding the same 8-bit digit: the AND over the digit's bits of the
-// bit's ballot (or its complement) -- 8 ballots instead of one match.any, whose cost grows
+// lanes of the warp holding the same RB-bit digit: the AND over the digit's bits of the
+// bit's ballot (or its complement) -- RB ballots instead of one match.any, whose cost grows
 // with the number of distinct values in the warp (measured: ~5 us per 3072-key partition
 // with random digits, vs ~2 us with a few distinct values)
-__device__ __forceinline__ uint32_t warp_peers8(uint32_t dg) {
+template <int RB>
+__device__ __forceinline__ uint32_t warp_peers(uint32_t dg) {
   uint32_t m = 0xffffffffu;
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
+  for (int b = 0; b < RB; ++b) {
     const uint32_t bal = __ballot_sync(0xffffffffu, (dg >> b) & 1u);
     m &= ((dg >> b) & 1u) ? bal : ~bal;
   }
@@ -471,26 +493,29 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scratch, int* total) 
   return wpre + inc - v;
 }
 
-// One onesweep pass: NT threads x ITEMS keys per partition; the 256 digit threads look
-// back LOOKW predecessor partitions per round trip.
-template <bool Packed, int NT, int ITEMS>
+// One onesweep pass: NT threads x ITEMS keys per partition, RB-bit digits; DT digit threads
+// own DPT consecutive digits each and look back LOOKW predecessor partitions per round trip.
+template <bool Packed, int NT, int ITEMS, int R>
 struct SweepSmem {
-  uint32_t warp_hist[NT / 32][256];
-  uint32_t digit_excl[256];
-  uint32_t global[256];
+  uint32_t warp_hist[NT / 32][R];
+  uint32_t digit_excl[R];
+  uint32_t global[R];
   uint64_t keys[NT * ITEMS];
   uint32_t vals[Packed ? 1 : NT * ITEMS];
   int scratch[32];
   uint32_t part;
 };
 
-template <bool Packed, int NT, int ITEMS, int LOOKW, int MINB>
+template <bool Packed, int NT, int ITEMS, int LOOKW, int MINB, int RB>
 __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
-  static_assert(NT >= 256, "one digit thread per 8-bit digit");
+  constexpr int R = 1 << RB;
+  constexpr int DT = NT < R ? NT : R;  // digit threads
+  constexpr int DPT = R / DT;          // consecutive digits per digit thread
+  static_assert(NT >= 256 && R % DT == 0, "digit threads cover the digits");
   constexpr int NW = NT / 32;
   constexpr int PART = NT * ITEMS;
   extern __shared__ __align__(16) unsigned char sweep_smem[];
-  SweepSmem<Packed, NT, ITEMS>& S = *reinterpret_cast<SweepSmem<Packed, NT, ITEMS>*>(sweep_smem);
+  SweepSmem<Packed, NT, ITEMS, R>& S = *reinterpret_cast<SweepSmem<Packed, NT, ITEMS, R>*>(sweep_smem);
   const int passes = (int)A.scal[S_PASSES];
   if (A.pass >= passes) return;  // grid-uniform: this digit is beyond the key width
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -500,9 +525,13 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
   // number from the counter, so every partition is claimed once
   if ((int64_t)blockIdx.x >= n_parts) return;
   if (tid == 0) S.part = atomicAdd(A.counter, 1u);
-  for (int i = tid; i < NW * 256; i += NT) (&S.warp_hist[0][0])[i] = 0;
+  for (int i = tid; i < NW * R; i += NT) (&S.warp_hist[0][0])[i] = 0;
   __syncthreads();
   const int64_t part = S.part;
+  // the next pass has the same partitions: this one clears its status row there (the next
+  // launch follows this one on the stream)
+  if (A.status_next && A.pass + 1 < passes)
+    for (int i = tid; i < R; i += NT) A.status_next[part * R + i] = 0u;
 #ifdef SIMULI_SORT_PROFILE
   long long t_start = sort_gtime();
   if (tid == 0 && part < 4096) g_sort_prof[A.pass][part][0] = t_start;
@@ -514,7 +543,7 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
   const uint32_t* vals_in = in ? A.vals[1] : A.vals[0];
   uint64_t* keys_out = in ? A.keys[0] : A.keys[1];
   uint32_t* vals_out = in ? A.vals[0] : A.vals[1];
-  const int shift = 8 * A.pass + (Packed ? A.id_bits : 0);
+  const int shift = RB * A.pass + (Packed ? A.id_bits : 0);
   const bool last = A.pass == passes - 1;
   const int64_t base = part * PART;
   const int valid = (int)min((int64_t)PART, P - base);
@@ -530,7 +559,7 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
       k[i] = keys_in[idx];
       if (!Packed) v[i] = vals_in[idx];
     } else {
-      k[i] = ~0ull;  // padding: digit 0xFF, ranked after every real key of the partition
+      k[i] = ~0ull;  // padding: the top digit, ranked after every real key of the partition
       if (!Packed) v[i] = 0;
     }
   }
@@ -546,17 +575,18 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
   SORT_STAMP(1);
   const long long ck_rank0 = clock64();
 #endif
-  // warp multisplit: lanes with equal digits (match.any), the highest of them bumps the
-  // warp's digit counter once and broadcasts the previous value.  Items go in batches of
-  // kRankBatch so the match latencies overlap; the counter updates stay in item order
-  // (one warp's shared-memory atomics execute in program order), which keeps the sort stable.
+  // warp multisplit: lanes with equal digits (ballot-built peer masks), the highest of them
+  // bumps the warp's digit counter once and broadcasts the previous value.  Items go in
+  // batches of kRankBatch so the ballot latencies overlap; the counter updates stay in item
+  // order (one warp's shared-memory atomics execute in program order), which keeps the sort
+  // stable.
 #pragma unroll
   for (int i0 = 0; i0 < ITEMS; i0 += kRankBatch) {
     uint32_t peers[kRankBatch], dg[kRankBatch], prev[kRankBatch];
 #pragma unroll
     for (int j = 0; j < kRankBatch; ++j) {
-      dg[j] = (uint32_t)(k[i0 + j] >> shift) & 0xFFu;
-      peers[j] = warp_peers8(dg[j]);
+      dg[j] = (uint32_t)(k[i0 + j] >> shift) & (R - 1);
+      peers[j] = warp_peers<RB>(dg[j]);
     }
 #pragma unroll
     for (int j = 0; j < kRankBatch; ++j) {
@@ -574,77 +604,109 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
 #ifdef SIMULI_SORT_PROFILE
   if (tid == 0 && part < 4096) g_sort_prof[A.pass][part][6] = clock64() - ck_rank0;
 #endif
-  // digit threads (tid < 256): per-warp exclusive offsets, the partition's digit counts
-  const int d = tid & 255;
-  uint32_t run = 0;
-  if (tid < 256) {
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const uint32_t c = S.warp_hist[w][d];
-      S.warp_hist[w][d] = run;
-      run += c;
-    }
-  }
+  // digit threads (tid < DT, digits d0 .. d0 + DPT - 1): per-warp exclusive offsets, the
+  // partition's digit counts, published as aggregates at once
+  const int d0 = tid * DPT;
   const uint32_t pad = (uint32_t)(PART - valid);
-  const uint32_t cnt_pub = run - (d == 255 ? pad : 0u);
-  uint32_t* st = A.status + part * 256 + d;
-  if (tid < 256) {
-    if (part == 0) st_relaxed(st, kFlagInc | cnt_pub);
-    else st_relaxed(st, kFlagAgg | cnt_pub);
+  uint32_t run[DPT], cnt_pub[DPT], hv[DPT];
+  uint32_t tsum = 0, hsum = 0;
+  uint32_t* st = A.status + part * R + d0;
+  if (tid < DT) {
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      uint32_t r = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t c = S.warp_hist[w][d0 + j];
+        S.warp_hist[w][d0 + j] = r;
+        r += c;
+      }
+      run[j] = r;
+      cnt_pub[j] = r - (d0 + j == R - 1 ? pad : 0u);
+      tsum += r;
+      st_relaxed(st + j, (part == 0 ? kFlagInc : kFlagAgg) | cnt_pub[j]);
+      hv[j] = A.hist[d0 + j];
+      hsum += hv[j];
+    }
   }
   SORT_STAMP(3);
   int tot;
-  const uint32_t dex = (uint32_t)block_excl_scan<NT>(tid < 256 ? (int)run : 0, S.scratch, &tot);
-  if (tid < 256) S.digit_excl[d] = dex;
+  const uint32_t tex = (uint32_t)block_excl_scan<NT>(tid < DT ? (int)tsum : 0, S.scratch, &tot);
+  if (tid < DT) {
+    uint32_t e = tex;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      S.digit_excl[d0 + j] = e;
+      e += run[j];
+    }
+  }
   int htot;
-  const int hex = block_excl_scan<NT>(tid < 256 ? (int)A.hist[d] : 0, S.scratch, &htot);
+  const uint32_t hex = (uint32_t)block_excl_scan<NT>(tid < DT ? (int)hsum : 0, S.scratch, &htot);
   // keys staged in digit order in shared memory while the predecessors publish (the
   // scatter needs only partition-local offsets; block_excl_scan's barrier made digit_excl
   // visible)
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const uint32_t dd = (uint32_t)(k[i] >> shift) & 0xFFu;
+    const uint32_t dd = (uint32_t)(k[i] >> shift) & (R - 1);
     const uint32_t pos = S.digit_excl[dd] + S.warp_hist[warp][dd] + rank[i];
     SIMULI_CHECK(pos < (uint32_t)PART, pos, PART);
     S.keys[pos] = k[i];
     if (!Packed) S.vals[pos] = v[i];
   }
-  if (tid < 256) {
-    uint32_t excl = 0;
+  if (tid < DT) {
+    uint32_t excl[DPT];
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) excl[j] = 0;
     if (part > 0) {
       // windowed look-back: LOOKW predecessors are loaded at once (independent loads, one
-      // round trip), then consumed in order up to the first inclusive prefix or the first
-      // partition that has not published yet (retried from there, after a short sleep so
-      // the spinning digit threads leave the issue slots to the SM's other partitions)
+      // round trip), then consumed in order; a digit closes at its first inclusive prefix,
+      // a round stops at the first partition that has not published every still-open digit
+      // (retried from there, after a short sleep so the spinning digit threads leave the
+      // issue slots to the SM's other partitions)
+      uint32_t open = (1u << DPT) - 1u;
       int64_t p = part - 1;
       while (true) {
-        uint32_t sv[LOOKW];
+        uint32_t sv[LOOKW][DPT];
 #pragma unroll
-        for (int w = 0; w < LOOKW; ++w) sv[w] = (p - w >= 0) ? ld_relaxed(A.status + (p - w) * 256 + d) : 0u;
+        for (int w = 0; w < LOOKW; ++w)
+#pragma unroll
+          for (int j = 0; j < DPT; ++j) sv[w][j] = (p - w >= 0) ? ld_relaxed(A.status + (p - w) * R + d0 + j) : 0u;
         int adv = 0;
-        bool done = false, blocked = false;
+        bool blocked = false;
 #pragma unroll
         for (int w = 0; w < LOOKW; ++w) {
-          const uint32_t f = sv[w] & ~kValMask;
-          const bool take = !done && !blocked && f != 0;
-          blocked = blocked || (!done && f == 0);
-          excl += take ? (sv[w] & kValMask) : 0u;
+          bool pub = true;
+#pragma unroll
+          for (int j = 0; j < DPT; ++j) pub = pub && (!((open >> j) & 1u) || (sv[w][j] & ~kValMask) != 0);
+          const bool take = !blocked && open != 0u && pub;
+          blocked = blocked || (open != 0u && !pub);
+#pragma unroll
+          for (int j = 0; j < DPT; ++j) {
+            const bool tj = take && ((open >> j) & 1u);
+            excl[j] += tj ? (sv[w][j] & kValMask) : 0u;
+            if (tj && (sv[w][j] & ~kValMask) == kFlagInc) open &= ~(1u << j);
+          }
           adv += take ? 1 : 0;
-          done = done || (take && f == kFlagInc);
         }
-        if (done) break;
+        if (open == 0u) break;
         p -= adv;
         if (blocked) __nanosleep(64);
       }
-      st_relaxed(st, kFlagInc | (excl + cnt_pub));
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) st_relaxed(st + j, kFlagInc | (excl[j] + cnt_pub[j]));
     }
-    S.global[d] = (uint32_t)hex + excl;
+    uint32_t h = hex;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      S.global[d0 + j] = h + excl[j];
+      h += hv[j];
+    }
   }
   __syncthreads();
   SORT_STAMP(4);
   for (int j = tid; j < valid; j += NT) {
     const uint64_t key = S.keys[j];
-    const uint32_t dd = (uint32_t)(key >> shift) & 0xFFu;
+    const uint32_t dd = (uint32_t)(key >> shift) & (R - 1);
     const int64_t out = (int64_t)S.global[dd] + (j - (int64_t)S.digit_excl[dd]);
     SIMULI_CHECK(out >= 0 && out < P, out, P);
     keys_out[out] = key;
@@ -658,54 +720,67 @@ __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
 #endif
 }
 
-// pass launcher: sweep shape (threads, items, look-back window); the default and the
-// tuning variants (SIMULI_SORT_VARIANT = NT * 10000 + ITEMS * 100 + LOOKW)
-template <bool Packed, int NT, int ITEMS, int LOOKW, int MINB = 1024 / NT>
+// pass launcher: sweep shape (threads, items, look-back window, digit bits); the default
+// and the tuning variants (SIMULI_SORT_VARIANT = NT * 10000 + ITEMS * 100 + LOOKW)
+template <bool Packed, int NT, int ITEMS, int LOOKW, int MINB, int RB>
 void launch_sweep(const SweepArgs& S, int64_t cap, cudaStream_t st) {
   constexpr int PART = NT * ITEMS;
-  constexpr size_t smem = sizeof(SweepSmem<Packed, NT, ITEMS>);
+  static_assert(PART >= kPart, "status rows are sized for partitions of >= kPart keys");
+  constexpr size_t smem = sizeof(SweepSmem<Packed, NT, ITEMS, (1 << RB)>);
   static bool once = [] {
-    cudaFuncSetAttribute(k_onesweep<Packed, NT, ITEMS, LOOKW, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_onesweep<Packed, NT, ITEMS, LOOKW, MINB, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     return true;
   }();
   (void)once;
   const unsigned grid = (unsigned)((cap + PART - 1) / PART);
-  if (grid > 0) k_onesweep<Packed, NT, ITEMS, LOOKW, MINB><<<grid, NT, smem, st>>>(S);
+  if (grid > 0) k_onesweep<Packed, NT, ITEMS, LOOKW, MINB, RB><<<grid, NT, smem, st>>>(S);
 }
 
 template <bool Packed>
-void launch_sweep_variant(const SweepArgs& S, int64_t cap, cudaStream_t st) {
+void launch_sweep_variant(const SweepArgs& S, int64_t cap, cudaStream_t st, int rb) {
   static const int variant = [] {
     const char* v = getenv("SIMULI_SORT_VARIANT");
     return v ? atoi(v) : 0;
   }();
+  if (rb == 10) {
+    // 1024 digits: 256 threads x 4 digits each; shared memory 72 KB at 16 keys per thread
+    switch (variant) {
+      case 2561204: launch_sweep<Packed, 256, 12, 4, 3, 10>(S, cap, st); break;
+      case 2561608: launch_sweep<Packed, 256, 16, 8, 3, 10>(S, cap, st); break;
+      case 2562004: launch_sweep<Packed, 256, 20, 4, 2, 10>(S, cap, st); break;
+      case 5121204: launch_sweep<Packed, 512, 12, 4, 1, 10>(S, cap, st); break;
+      default: launch_sweep<Packed, 256, 16, 4, 3, 10>(S, cap, st); break;
+    }
+    return;
+  }
   switch (variant) {
-    case 2561216: launch_sweep<Packed, 256, 12, 16>(S, cap, st); break;
-    case 2561232: launch_sweep<Packed, 256, 12, 32>(S, cap, st); break;
-    case 2561233: launch_sweep<Packed, 256, 12, 32, 3>(S, cap, st); break;
-    case 2561633: launch_sweep<Packed, 256, 16, 32, 3>(S, cap, st); break;
-    case 2561616: launch_sweep<Packed, 256, 16, 16>(S, cap, st); break;
-    case 2561632: launch_sweep<Packed, 256, 16, 32>(S, cap, st); break;
-    case 2562432: launch_sweep<Packed, 256, 24, 32>(S, cap, st); break;
-    case 5121232: launch_sweep<Packed, 512, 12, 32>(S, cap, st); break;
-    case 5121216: launch_sweep<Packed, 512, 12, 16>(S, cap, st); break;
-    case 2562408: launch_sweep<Packed, 256, 24, 8, 3>(S, cap, st); break;
-    case 2562404: launch_sweep<Packed, 256, 24, 4, 3>(S, cap, st); break;
-    case 2562416: launch_sweep<Packed, 256, 24, 16, 3>(S, cap, st); break;
-    case 5122408: launch_sweep<Packed, 512, 24, 8, 1>(S, cap, st); break;
-    case 2561608: launch_sweep<Packed, 256, 16, 8>(S, cap, st); break;
-    case 10241208: launch_sweep<Packed, 1024, 12, 8>(S, cap, st); break;
-    case 10241216: launch_sweep<Packed, 1024, 12, 16>(S, cap, st); break;
-    case 5121632: launch_sweep<Packed, 512, 16, 32>(S, cap, st); break;
-    case 2561208: launch_sweep<Packed, 256, 12, 8>(S, cap, st); break;
-    case 5121208: launch_sweep<Packed, 512, 12, 8>(S, cap, st); break;
+    case 2561216: launch_sweep<Packed, 256, 12, 16, 4, 8>(S, cap, st); break;
+    case 2561232: launch_sweep<Packed, 256, 12, 32, 4, 8>(S, cap, st); break;
+    case 2561233: launch_sweep<Packed, 256, 12, 32, 3, 8>(S, cap, st); break;
+    case 2561633: launch_sweep<Packed, 256, 16, 32, 3, 8>(S, cap, st); break;
+    case 2561616: launch_sweep<Packed, 256, 16, 16, 4, 8>(S, cap, st); break;
+    case 2561632: launch_sweep<Packed, 256, 16, 32, 4, 8>(S, cap, st); break;
+    case 2562432: launch_sweep<Packed, 256, 24, 32, 4, 8>(S, cap, st); break;
+    case 5121232: launch_sweep<Packed, 512, 12, 32, 2, 8>(S, cap, st); break;
+    case 5121216: launch_sweep<Packed, 512, 12, 16, 2, 8>(S, cap, st); break;
+    case 2562408: launch_sweep<Packed, 256, 24, 8, 3, 8>(S, cap, st); break;
+    case 2562404: launch_sweep<Packed, 256, 24, 4, 3, 8>(S, cap, st); break;
+    case 2562416: launch_sweep<Packed, 256, 24, 16, 3, 8>(S, cap, st); break;
+    case 5122408: launch_sweep<Packed, 512, 24, 8, 1, 8>(S, cap, st); break;
+    case 2561608: launch_sweep<Packed, 256, 16, 8, 4, 8>(S, cap, st); break;
+    case 10241208: launch_sweep<Packed, 1024, 12, 8, 1, 8>(S, cap, st); break;
+    case 10241216: launch_sweep<Packed, 1024, 12, 16, 1, 8>(S, cap, st); break;
+    case 5121632: launch_sweep<Packed, 512, 16, 32, 2, 8>(S, cap, st); break;
+    case 2561208: launch_sweep<Packed, 256, 12, 8, 4, 8>(S, cap, st); break;
+    case 5121208: launch_sweep<Packed, 512, 12, 8, 2, 8>(S, cap, st); break;
     // default: 256 threads x 20 keys (5120 per partition), 3 CTAs per SM: with several
     // scans in flight the fewest look-back spins per key (config B, four scans in flight:
     // 275 -> 289 M rays/s against 512 x 12; one sort alone 200 us vs 190 us)
-    default: launch_sweep<Packed, 256, 20, kLookW, 3>(S, cap, st); break;
+    default: launch_sweep<Packed, 256, 20, kLookW, 3, 8>(S, cap, st); break;
   }
 }
+
 
 // ------------------------------------------------------------------ tile metadata
 // [begin, end) of every tile from the tile changes of the sorted keys (tile = key >> b)
@@ -775,7 +850,7 @@ extern "C" int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t cap, int32_
   clear_error();
   SIMULI_REQUIRE(bytes && n >= 0 && n_tiles >= 1, "simuli_bin_sort_workspace_size: bad argument");
   if (cap < 0) cap = -cap;
-  *bytes = carve(nullptr, n, cap, n_tiles).bytes;
+  *bytes = carve(nullptr, n, cap, n_tiles, sort_rb()).bytes;
   return SIMULI_OK;
 }
 
@@ -795,9 +870,10 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
   SIMULI_REQUIRE(cap < (1ll << 30), "pair capacity must be < 2^30");
   const int tbits = tile_bits_of(n_tiles);
   SIMULI_REQUIRE(tbits <= 16, "n_tiles must be <= 65536");
-  const Workspace need = carve(nullptr, n, cap, n_tiles);
+  const int rb = sort_rb();
+  const Workspace need = carve(nullptr, n, cap, n_tiles, rb);
   SIMULI_REQUIRE(workspace && ws_bytes >= need.bytes, "workspace too small: need %zu bytes", need.bytes);
-  Workspace w = carve(workspace, n, cap, n_tiles);
+  Workspace w = carve(workspace, n, cap, n_tiles, rb);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int64_t nb = (n + kDupBlock - 1) / kDupBlock;
   auto check = [&](const char* what) -> int32_t {
@@ -808,8 +884,8 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     }
     return SIMULI_OK;
   };
-  // one memset zeroes the pass histograms, all counters, the key range and every
-  // look-back status word (count scan and sweep passes)
+  // one memset zeroes the pass histograms, all counters, the key range and the look-back
+  // status words of the count scan and the first sweep pass (each pass clears the next's)
   if (cudaMemsetAsync(w.zero, 0, w.zero_bytes, st) != cudaSuccess) return check("memset workspace");
   uint32_t* ctr = w.counters + kMaxPasses;  // [0] scan block ids, [1] scan blocks done
   if (nb > 0) {
@@ -817,7 +893,7 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(proj->tile_count) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(proj->depth_key) % 16 == 0,
                    "simuli_bin_sort: tile_count / depth_key must be 16-byte aligned");
-    k_count_scan<<<(unsigned)nsb, kScanThreads, 0, st>>>(proj->tile_count, proj->depth_key, n, nsb, nb, tbits,
+    k_count_scan<<<(unsigned)nsb, kScanThreads, 0, st>>>(proj->tile_count, proj->depth_key, n, nsb, nb, tbits, rb,
                                                          w.block_sums, w.cstatus, w.kminmax, ctr, w.scal, n_pairs_dev);
   } else {
     k_count_empty<<<1, 32, 0, st>>>(tbits, w.scal, n_pairs_dev, w.block_sums);
@@ -834,7 +910,7 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
       return SIMULI_ERR_CAPACITY;
     }
   }
-  const int max_passes = (32 + tbits + 7) / 8;
+  const int max_passes = max_passes_of(tbits, rb);
   uint32_t* vals[2] = {sorted_ids, w.vals_alt};
   // packed mode: depth-key span b <= 31 bits (positive floats), so one u64 word holds
   // (tile << b | depth - min) << id_bits | id whenever 31 + tile bits + id bits <= 64
@@ -845,13 +921,16 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     DupArgs D{proj->tile_count, reinterpret_cast<const int4*>(proj->tile_rect), proj->depth_key, n, cap,
               w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, nullptr,
               id_bits, packed ? 1 : 0, n_tiles};
-    k_duplicate<<<(unsigned)nb, kDupThreads, 0, st>>>(D);
+    if (rb == 10) k_duplicate<10><<<(unsigned)nb, kDupThreads, 0, st>>>(D);
+    else k_duplicate<8><<<(unsigned)nb, kDupThreads, 0, st>>>(D);
     if (int32_t e = check("duplicate")) return e;
     for (int p = 0; p < max_passes; ++p) {
+      const size_t row = (size_t)w.parts << rb;  // one pass's status words
       SweepArgs S{{w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.scal, cap, p, id_bits, sorted_ids,
-                  w.hist + p * 256, w.status + (size_t)p * w.parts * 256, w.counters + p};
-      if (packed) launch_sweep_variant<true>(S, cap, st);
-      else launch_sweep_variant<false>(S, cap, st);
+                  w.hist + p * kRadixMax, w.status + p * row, p + 1 < max_passes ? w.status + (p + 1) * row : nullptr,
+                  w.counters + p};
+      if (packed) launch_sweep_variant<true>(S, cap, st, rb);
+      else launch_sweep_variant<false>(S, cap, st, rb);
     }
     if (int32_t e = check("onesweep")) return e;
   }
