@@ -7,9 +7,10 @@
  * listed in DESIGN.md §3.  Plain loops, double precision, no blocking or fusion.
  * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC.
  *
- * Parity status: every function below is pinned by tests/test_oracle_pins.py except the
- * whole-render composition on realistic scenes, which the paper gives no numbers for
- * ("parity unpinned" for the end-to-end render values).  O6's lens models
+ * Parity status: every function below is pinned by tests/test_oracle_pins.py.  The whole
+ * render on realistic scenes, which the paper gives no numbers for, is pinned by bitwise
+ * scale covariance (2x lengths -> 2x depth, every other output identical), rigid
+ * invariance, tiled == brute force and conservation.  O6's lens models
  * (KB fisheye, OpenCV radtan) and their inverses are pinned to OpenCV (cv2.fisheye /
  * cv2.projectPoints / undistortPoints, <= 1e-9 px, <= 1e-12 rad).  O8's exact culling mode
  * (A32) is pinned by brute force over every ray.  The NEXT-row

@@ -369,6 +369,64 @@ def test_opaque_wall_depth(oracle_mod):
     assert np.abs(out["depth"][hit] - expect).max() < 0.05
 
 
+def _scaled_scene(scene, f):
+    out = dict(scene)
+    out["means"] = scene["means"] * np.float32(f)
+    out["scales"] = scene["scales"] * np.float32(f)
+    return out
+
+
+@pytest.mark.parametrize("divergence", [0.0, 1.5e-3])
+def test_whole_scan_scale_covariance(oracle_mod, divergence):
+    """Whole LiDAR scan on a realistic scene (config-B sensor, rolling shutter, a 20k
+    corridor subset): a scan is a function of lengths only through dimensionless ratios
+    -- the sensor model (Eq. 3) sees directions, the canonical response and the
+    beam-divergence covariance (App. C, theta^2 r^2) are homogeneous, the depth key (A19)
+    orders by distance -- so scaling every length by 2 (means, scales, sensor track,
+    minimum range; exact in binary floating point) must return depth x 2 and every other
+    output bit for bit.  A term of the wrong dimension anywhere in O1-O13 (a dropped
+    square, Sigma for Sigma^-1, an absolute epsilon) breaks it."""
+    import copy
+    O = oracle_mod
+    cfg = S.lidar_config("B")
+    cfg.beam_divergence = divergence
+    scene = S.corridor_scene(7, 20000, x_range=(-30.0, 30.0))
+    scene["means"] = (scene["means"] - np.float32([0.0, 0.0, 1.8])).astype(np.float32)  # sensor at the origin
+    p0 = S.pose([1, 0, 0, 0], [0, 0, 0])
+    ref = O.render_lidar(scene, cfg, pose0=p0, pose1=S.pose(S.yaw_quat(0.03), [1.0, 0.0, 0.0]))
+    cfg2 = copy.deepcopy(cfg)
+    cfg2.min_range = cfg.min_range * 2
+    got = O.render_lidar(_scaled_scene(scene, 2), cfg2, pose0=p0, pose1=S.pose(S.yaw_quat(0.03), [2.0, 0.0, 0.0]))
+    assert (ref["opacity"] > 0.5).mean() > 0.2 and (ref["n_contrib"] > 0).mean() > 0.3
+    for k in ("depth", "depth_accum"):
+        assert np.array_equal(got[k], 2 * ref[k]), k
+    for k in ("feat", "opacity", "T_final", "n_contrib", "scanned", "inbox", "intensity", "raydrop"):
+        assert np.array_equal(got[k], ref[k]), k
+    assert np.array_equal(got["ray_od"][:, :3], 2 * ref["ray_od"][:, :3])
+    assert np.array_equal(got["ray_od"][:, 3:], ref["ray_od"][:, 3:])
+
+
+def test_whole_frame_scale_covariance(oracle_mod):
+    """The same for a rolling-shutter KB-fisheye frame (D-small, a 20k camera corridor
+    subset): projection is scale free (x/z, atan2(rho, z)), the near plane scales."""
+    import copy
+    O = oracle_mod
+    cam = S.camera_config("D-small")
+    scene = S.corridor_scene(8, 20000, x_range=(-5.0, 40.0), kind="camera", ego=(1.5, 0.0, 1.6))
+    scene["means"] = (scene["means"] - np.float32([1.5, 0.0, 1.6])).astype(np.float32)
+    c0 = S.pose(S.CAM_FORWARD_Q, [0, 0, 0])
+    ref = O.render_camera(scene, cam, pose0=c0, pose1=S.pose(S.yaw_quat(0.009, S.CAM_FORWARD_Q), [0.3, 0, 0]))
+    cam2 = copy.deepcopy(cam)
+    cam2.near = cam.near * 2
+    got = O.render_camera(_scaled_scene(scene, 2), cam2, pose0=c0,
+                          pose1=S.pose(S.yaw_quat(0.009, S.CAM_FORWARD_Q), [0.6, 0, 0]))
+    assert (ref["opacity"] > 0.2).mean() > 0.1
+    for k in ("depth", "depth_accum"):
+        assert np.array_equal(got[k], 2 * ref[k]), k
+    for k in ("feat", "opacity", "T_final", "n_contrib", "scanned", "inbox"):
+        assert np.array_equal(got[k], ref[k]), k
+
+
 # ---------------------------------------------------------------- O7 tiling (P:494-517)
 def _tiling_for(beams_rad, A, n_phi, M, cull_az=1600):
     cfg = S.LidarConfig("t", np.asarray(beams_rad, np.float32), A, n_phi=n_phi, max_rays_per_tile=M,
