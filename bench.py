@@ -31,7 +31,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -65,74 +64,94 @@ def read_peaks():
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled DURING the timed region: an NVML thread polling
-    every 2 ms (the timed region of a default run is a few hundred ms, too short for
-    ``nvidia-smi -lms``); falls back to ``nvidia-smi -lms 100`` if NVML is unavailable."""
+    """SM clock + throttle reasons sampled DURING the timed region by a separate process (an
+    NVML poll every 2 ms, monotonic timestamps, written to a temp file; a thread of this
+    process would need the GIL the launch loop holds) and kept for the window
+    [mark_begin, mark_end]; falls back to ``nvidia-smi -lms 100`` if NVML is unavailable."""
 
     REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
                ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
+    POLL = (
+        "import sys, time\n"
+        "import pynvml as n\n"
+        "n.nvmlInit(); h = n.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))\n"
+        "smax = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)\n"
+        "out = open(sys.argv[2], 'w', buffering=1)\n"
+        "out.write('ready\\n')\n"
+        "while True:\n"
+        "    out.write('%.6f %d %d %d\\n' % (time.monotonic(), n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM), smax,\n"
+        "              n.nvmlDeviceGetCurrentClocksEventReasons(h)))\n"
+        "    time.sleep(0.002)\n")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
-        self.stop_ev = threading.Event()
-        self.thread = None
-        self.nvml = None
-
-    def _poll(self):
-        n, h = self.nvml
-        smax = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
-        while not self.stop_ev.is_set():
-            try:
-                self.samples.append((n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM), smax,
-                                     n.nvmlDeviceGetCurrentClocksEventReasons(h)))
-            except Exception:
-                pass
-            time.sleep(0.002)
+        self.samples = []  # (t, sm_mhz, max_mhz, reasons bitmask)
+        self.proc = None
+        self.path = None
+        self.window = [None, None]
+        self.source = "nvml 2 ms (poller process)"
 
     def start(self):
+        import tempfile
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
+        fd, self.path = tempfile.mkstemp(prefix="bench_clk_", suffix=".txt")
+        os.close(fd)
         try:
-            import pynvml as n
-            n.nvmlInit()
-            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
-            self.nvml = (n, n.nvmlDeviceGetHandleByIndex(idx))
-            self.thread = threading.Thread(target=self._poll, daemon=True)
+            import pynvml  # noqa: F401  (the poller imports it too)
+            self.proc = subprocess.Popen([sys.executable, "-c", self.POLL, str(idx), self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except Exception:
-            self.nvml = None
-            self.thread = threading.Thread(target=self._smi, daemon=True)
-        self.thread.start()
-        time.sleep(0.01)
-
-    def _smi(self):
-        try:
-            p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
-                                  "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "100"],
-                                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            return
-        while not self.stop_ev.is_set():
-            ln = p.stdout.readline()
-            if not ln:
+            self.source = "nvidia-smi 100 ms"
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(idx), "--query-gpu=timestamp,clocks.sm,clocks.max.sm,"
+                                          "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms",
+                                          "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        t0 = time.monotonic()
+        while time.monotonic() - t0 < 20.0:  # wait for the poller's first line
+            if os.path.getsize(self.path) > 0 or self.proc.poll() is not None:
                 break
-            try:
-                a, b, c = [x.strip() for x in ln.split(",")]
-                self.samples.append((float(a), float(b), int(c, 16)))
-            except ValueError:
-                continue
-        p.terminate()
+            time.sleep(0.01)
+
+    def mark_begin(self):
+        self.window[0] = time.monotonic()
+
+    def mark_end(self):
+        self.window[1] = time.monotonic()
 
     def stop(self):
-        self.stop_ev.set()
-        if self.thread is not None:
-            self.thread.join(timeout=3)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        t_lo = self.window[0] if self.window[0] is not None else -1e30
+        t_hi = self.window[1] if self.window[1] is not None else 1e30
+        try:
+            lines = open(self.path).read().splitlines()
+            os.unlink(self.path)
+        except OSError:
+            lines = []
+        for ln in lines:
+            try:
+                if self.source.startswith("nvml"):
+                    t, a, b, c = ln.split()
+                    t, a, b, c = float(t), float(a), float(b), int(c)
+                else:  # nvidia-smi: no monotonic stamp -- every sample of the run
+                    _, a, b, c = [x.strip() for x in ln.split(",")]
+                    t, a, b, c = 0.0, float(a), float(b), int(c, 16)
+                    t_lo, t_hi = -1e30, 1e30
+            except ValueError:
+                continue
+            if t_lo <= t <= t_hi:
+                self.samples.append((t, a, b, c))
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0}
-        sm = [s[0] for s in self.samples]
-        reasons = sorted({name for _, _, m in self.samples for name, bit in self.REASONS if m & bit})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
-                "sm_mhz_min": min(sm), "reasons": reasons, "samples": len(sm),
-                "source": "nvml 2 ms" if self.nvml else "nvidia-smi 100 ms"}
+        sm = [s[1] for s in self.samples]
+        reasons = sorted({name for _, _, _, m in self.samples for name, bit in self.REASONS if m & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[2] for s in self.samples),
+                "sm_mhz_min": min(sm), "reasons": reasons, "samples": len(sm), "source": self.source,
+                "window": "the headline timed region"}
 
 
 def dist_env():
@@ -433,8 +452,9 @@ def run_gpu(args):
     clocks = ClockSampler(dev.index if ws == 1 else local)
     if ws > 1:
         dist.barrier()
-    torch.cuda.synchronize()
     clocks.start()
+    torch.cuda.synchronize()
+    clocks.mark_begin()
     wall0 = time.perf_counter()
     e_beg, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_beg.record(stream)
@@ -453,6 +473,7 @@ def run_gpu(args):
     if ws > 1:
         dist.barrier()
     wall = time.perf_counter() - wall0
+    clocks.mark_end()
     total_ms = e_beg.elapsed_time(e_end)
     max_ms = batch.reduce_max(total_ms, dev)  # slowest rank (device time)
     cap_checks.append(check_capacity("headline timed region"))
