@@ -16,8 +16,8 @@
 //                   tid+256, ... binary-searching its owner in shared memory) of the
 //                   trimmed key (tile << b) | (depth bits - min) -- an order-preserving
 //                   map of (tile, depth bits) -- plus the digit histograms of every pass
-//   k_onesweep x 6  stable LSD onesweep, 8-bit digits (10-bit: SIMULI_SORT_RB=10, tuning
-//                   only -- slower, profiles/r02_experiments.md); passes beyond the device-side pass
+//   k_onesweep x 6  stable LSD onesweep, 8-bit digits (10-bit measured slower,
+//                   profiles/r02_experiments.md); passes beyond the device-side pass
 //                   count exit at once (buffer parity is chosen on the device so the
 //                   last real pass lands in the caller's arrays).  Per 5120-key partition
 //                   (256 threads x 20 keys) a warp-level multisplit (ballot-built peer
@@ -55,16 +55,11 @@ enum { S_P = 0, S_KMIN, S_KMAX, S_B, S_PASSES, S_TBITS, S_N };
 
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-// digit width of the radix passes: 8 bits (256 digits) or 10 bits (1024 digits, one pass
-// fewer for the 38-bit keys of config B); SIMULI_SORT_RB overrides the default (tuning)
-int sort_rb() {
-  static const int rb = [] {
-    const char* v = getenv("SIMULI_SORT_RB");
-    const int r = v ? atoi(v) : 8;
-    return r == 10 ? 10 : 8;
-  }();
-  return rb;
-}
+// digit width of the radix passes: 8 bits (256 digits).  The sweep and the duplication's
+// histograms are written for any width; 10-bit digits (one pass fewer for config B's 38-bit
+// keys) measured slower -- 231 vs 199 us per sort, profiles/r02_experiments.md
+constexpr int kRB = 8;
+int sort_rb() { return kRB; }
 int max_passes_of(int tbits, int rb) { return (32 + tbits + rb - 1) / rb; }
 
 int tile_bits_of(int32_t n_tiles) {
@@ -743,17 +738,7 @@ void launch_sweep_variant(const SweepArgs& S, int64_t cap, cudaStream_t st, int 
     const char* v = getenv("SIMULI_SORT_VARIANT");
     return v ? atoi(v) : 0;
   }();
-  if (rb == 10) {
-    // 1024 digits: 256 threads x 4 digits each; shared memory 72 KB at 16 keys per thread
-    switch (variant) {
-      case 2561204: launch_sweep<Packed, 256, 12, 4, 3, 10>(S, cap, st); break;
-      case 2561608: launch_sweep<Packed, 256, 16, 8, 3, 10>(S, cap, st); break;
-      case 2562004: launch_sweep<Packed, 256, 20, 4, 2, 10>(S, cap, st); break;
-      case 5121204: launch_sweep<Packed, 512, 12, 4, 1, 10>(S, cap, st); break;
-      default: launch_sweep<Packed, 256, 16, 4, 3, 10>(S, cap, st); break;
-    }
-    return;
-  }
+  (void)rb;  // kRB
   switch (variant) {
     case 2561216: launch_sweep<Packed, 256, 12, 16, 4, 8>(S, cap, st); break;
     case 2561232: launch_sweep<Packed, 256, 12, 32, 4, 8>(S, cap, st); break;
@@ -921,8 +906,7 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     DupArgs D{proj->tile_count, reinterpret_cast<const int4*>(proj->tile_rect), proj->depth_key, n, cap,
               w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, nullptr,
               id_bits, packed ? 1 : 0, n_tiles};
-    if (rb == 10) k_duplicate<10><<<(unsigned)nb, kDupThreads, 0, st>>>(D);
-    else k_duplicate<8><<<(unsigned)nb, kDupThreads, 0, st>>>(D);
+    k_duplicate<kRB><<<(unsigned)nb, kDupThreads, 0, st>>>(D);
     if (int32_t e = check("duplicate")) return e;
     for (int p = 0; p < max_passes; ++p) {
       const size_t row = (size_t)w.parts << rb;  // one pass's status words

@@ -1,3 +1,4 @@
+# round-2 experiment (commit 5ae5bdc; the SIMULI_SORT_RB switch was removed afterwards)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null || exit 1
 timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -2
 SIMULI_SORT_RB=10 timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -3
