@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SIMULI_ABI_VERSION 11
+#define SIMULI_ABI_VERSION 12
 
 enum {
   SIMULI_OK = 0,
@@ -274,6 +274,9 @@ int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t
  *   (power-of-two buckets; a longest-first schedule for the render kernels, which is a
  *   performance hint only: results do not depend on it);
  * n_pairs_dev: device int64 (receives P).
+ * n_pairs_max_dev: device int64 or NULL -- if given, raised to max(*n_pairs_max_dev, P) on
+ *   the device (a sticky maximum over asynchronous calls: one later read checks a whole
+ *   batch of scans against pair_capacity; the caller zeroes it).
  * pair_capacity >= 0: fully asynchronous; if P > pair_capacity only the first
  *   pair_capacity pairs are sorted and the result is INCOMPLETE -- the caller must check
  *   *n_pairs_dev <= pair_capacity and retry with larger buffers.
@@ -282,7 +285,7 @@ int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t
 int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles, int32_t n_cols_total,
                         void* workspace, size_t workspace_bytes, int64_t pair_capacity,
                         uint64_t* sorted_keys, uint32_t* sorted_ids, int32_t* tile_ranges, int32_t* tile_order,
-                        int64_t* n_pairs_dev, int64_t* pairs_required, void* stream);
+                        int64_t* n_pairs_dev, int64_t* n_pairs_max_dev, int64_t* pairs_required, void* stream);
 
 /* Compositing thresholds (A13, A14): skip alpha < alpha_min (default 1/255), clamp alpha
  * to alpha_max (0.99), stop a ray when T (1 - alpha) < T_min (1e-4) without compositing

@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(kScanThreads) k_count_scan(const int* __restri
                                                              int64_t* __restrict__ block_sums,
                                                              uint32_t* __restrict__ cstatus, uint32_t* __restrict__ kminmax,
                                                              uint32_t* __restrict__ ctr, int64_t* __restrict__ scal,
-                                                             int64_t* __restrict__ n_pairs) {
+                                                             int64_t* __restrict__ n_pairs,
+                                                             int64_t* __restrict__ n_pairs_max) {
   constexpr int DB = kScanPer / kDupBlock;  // duplicate blocks per scan block
   constexpr int TPD = kDupBlock / kScanItems;  // threads per duplicate block
   __shared__ int s_wsum[32];
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kScanThreads) k_count_scan(const int* __restri
   uint32_t mn = ~ld_relaxed(&kminmax[0]), mx = ld_relaxed(&kminmax[1]);
   block_sums[nb] = P;
   *n_pairs = P;
+  if (n_pairs_max) atomicMax(reinterpret_cast<unsigned long long*>(n_pairs_max), (unsigned long long)P);
   int b = 0;
   if (P > 0 && mx > mn) b = 32 - __clz(mx - mn);
   if (P == 0) mn = 0;
@@ -842,7 +844,8 @@ extern "C" int32_t simuli_bin_sort_workspace_size(int64_t n, int64_t cap, int32_
 extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int32_t n_tiles, int32_t n_cols_total,
                                    void* workspace, size_t ws_bytes, int64_t pair_capacity, uint64_t* sorted_keys,
                                    uint32_t* sorted_ids, int32_t* tile_ranges, int32_t* tile_order,
-                                   int64_t* n_pairs_dev, int64_t* pairs_required, void* stream) {
+                                   int64_t* n_pairs_dev, int64_t* n_pairs_max_dev, int64_t* pairs_required,
+                                   void* stream) {
   using namespace simuli;
   clear_error();
   SIMULI_REQUIRE(proj && n >= 0 && n_tiles >= 1 && n_cols_total >= 1 && n_cols_total <= n_tiles,
@@ -879,7 +882,8 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
                        reinterpret_cast<uintptr_t>(proj->depth_key) % 16 == 0,
                    "simuli_bin_sort: tile_count / depth_key must be 16-byte aligned");
     k_count_scan<<<(unsigned)nsb, kScanThreads, 0, st>>>(proj->tile_count, proj->depth_key, n, nsb, nb, tbits, rb,
-                                                         w.block_sums, w.cstatus, w.kminmax, ctr, w.scal, n_pairs_dev);
+                                                         w.block_sums, w.cstatus, w.kminmax, ctr, w.scal, n_pairs_dev,
+                                                         n_pairs_max_dev);
   } else {
     k_count_empty<<<1, 32, 0, st>>>(tbits, w.scal, n_pairs_dev, w.block_sums);
   }

@@ -24,7 +24,7 @@ SENSOR_LIDAR, SENSOR_CAMERA = 0, 1
 CAM_PINHOLE_RADTAN, CAM_FISHEYE_KB = 0, 1
 RECORD_FLOATS = 20
 
-ABI_VERSION = 11  # include/simuli.h SIMULI_ABI_VERSION
+ABI_VERSION = 12  # include/simuli.h SIMULI_ABI_VERSION
 EXPORTED = ["simuli_last_error", "simuli_abi_version", "simuli_build_tiles", "simuli_project",
             "simuli_bin_sort_workspace_size", "simuli_bin_sort", "simuli_render_lidar", "simuli_render_camera",
             "simuli_compose_camera", "simuli_backward_workspace_size", "simuli_backward_lidar",
@@ -162,7 +162,7 @@ def load():
     L.simuli_bin_sort_workspace_size.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]
     L.simuli_bin_sort.argtypes = [C.POINTER(Projected), C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t,
                                   C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                  C.POINTER(C.c_int64), C.c_void_p]
+                                  C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
     L.simuli_render_lidar.argtypes = [C.POINTER(Projected), C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(ProjectParams), C.POINTER(RenderParams), C.POINTER(LidarOut),
                                       C.c_void_p]
@@ -190,14 +190,6 @@ def _check(code):
 
 def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
-
-
-class _nullctx:
-    def __enter__(self):
-        return self
-
-    def __exit__(self, *a):
-        return False
 
 
 def _stream(stream=None):
@@ -252,12 +244,12 @@ def simuli_bin_sort_workspace_size(n, capacity, n_tiles) -> int:
 
 
 def simuli_bin_sort(proj: Projected, n, n_tiles, n_cols_total, workspace, capacity, sorted_keys, sorted_ids,
-                    tile_ranges, n_pairs_dev, stream=None, tile_order=None) -> int | None:
+                    tile_ranges, n_pairs_dev, stream=None, tile_order=None, n_pairs_max=None) -> int | None:
     req = C.c_int64(-1)
     code = load().simuli_bin_sort(C.byref(proj), int(n), int(n_tiles), int(n_cols_total), _ptr(workspace),
                                   workspace.numel() * workspace.element_size(), int(capacity), _ptr(sorted_keys),
                                   _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order), _ptr(n_pairs_dev),
-                                  C.byref(req),
+                                  _ptr(n_pairs_max), C.byref(req),
                                   _stream(stream))
     if code == SIMULI_ERR_CAPACITY:
         return int(req.value)
@@ -439,9 +431,10 @@ class _Frame:
         """Duplicate + sort.  sync_capacity=True: one host sync to grow buffers if needed."""
         cap = -self.capacity if sync_capacity else self.capacity
         keys = self.sorted_keys if self.keep_keys else None
+        # asynchronous calls raise the sticky device-side maximum checked by check_capacity()
         need = simuli_bin_sort(self.projected, self.n, self.n_tiles, self.n_cols_total, self.workspace, cap,
                                keys, self.sorted_ids, self.tile_ranges, self.n_pairs, stream,
-                               self.tile_order)
+                               self.tile_order, None if sync_capacity else self.max_pairs)
         if need is not None:
             self.set_capacity(int(need * 1.25) + 1024)
             keys = self.sorted_keys if self.keep_keys else None
@@ -450,11 +443,6 @@ class _Frame:
                                    self.n_pairs, stream, self.tile_order)
             assert need is None
         self._on_stream(stream, self.sorted_keys, self.sorted_ids, self.workspace)
-        if not sync_capacity:  # sticky device-side maximum, checked by check_capacity()
-            import torch
-            st = stream if isinstance(stream, torch.cuda.Stream) else None
-            with torch.cuda.stream(st) if st is not None else _nullctx():
-                torch.maximum(self.max_pairs, self.n_pairs, out=self.max_pairs)
 
     def set_poses(self, pose_start, pose_end):
         self.params.pose_start = make_pose(pose_start)
