@@ -144,6 +144,18 @@ __device__ __forceinline__ int block_excl_scan256(int v, int* scratch, int* tota
   return wpre + inc - v;
 }
 
+// zeroing on the stream as a kernel (a memset node would break the programmatic launch chain)
+__global__ void __launch_bounds__(256) k_zero(uint32_t* __restrict__ p, int64_t n_words) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_words; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0u;
+}
+unsigned zero_blocks(int64_t n_words) {
+  const int64_t b = (n_words + 255) / 256;
+  return (unsigned)(b < 148 * 4 ? (b > 0 ? b : 1) : 148 * 4);
+}
+
 // ------------------------------------------------------------------ counts, key range
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
@@ -173,6 +185,8 @@ __global__ void __launch_bounds__(kScanThreads) k_count_scan(const int* __restri
                                                              uint32_t* __restrict__ ctr, int64_t* __restrict__ scal,
                                                              int64_t* __restrict__ n_pairs,
                                                              int64_t* __restrict__ n_pairs_max) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int DB = kScanPer / kDupBlock;  // duplicate blocks per scan block
   constexpr int TPD = kDupBlock / kScanItems;  // threads per duplicate block
   __shared__ int s_wsum[32];
@@ -308,6 +322,8 @@ __global__ void __launch_bounds__(kScanThreads) k_count_scan(const int* __restri
 
 // n = 0: no pairs
 __global__ void k_count_empty(int tile_bits, int64_t* scal, int64_t* n_pairs, int64_t* block_sums) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0) {
     scal[S_P] = 0; scal[S_KMIN] = 0; scal[S_KMAX] = 0; scal[S_B] = 0; scal[S_PASSES] = 0;
     scal[S_TBITS] = tile_bits;
@@ -341,6 +357,8 @@ struct DupArgs {
 // order (the stable sort then keeps equal keys in id order).
 template <int RB>
 __global__ void __launch_bounds__(kDupThreads) k_duplicate(const DupArgs A) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int R = 1 << RB;
   __shared__ uint32_t s_hist[(RB == 8 ? kMaxPasses : 5) * R];
   __shared__ int s_wtot[kDupThreads / 32];
@@ -505,6 +523,8 @@ struct SweepSmem {
 
 template <bool Packed, int NT, int ITEMS, int LOOKW, int MINB, int RB>
 __global__ void __launch_bounds__(NT, MINB) k_onesweep(const SweepArgs A) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int R = 1 << RB;
   constexpr int DT = NT < R ? NT : R;  // digit threads
   constexpr int DPT = R / DT;          // consecutive digits per digit thread
@@ -731,7 +751,7 @@ void launch_sweep(const SweepArgs& S, int64_t cap, cudaStream_t st) {
   }();
   (void)once;
   const unsigned grid = (unsigned)((cap + PART - 1) / PART);
-  if (grid > 0) k_onesweep<Packed, NT, ITEMS, LOOKW, MINB, RB><<<grid, NT, smem, st>>>(S);
+  if (grid > 0) launch_pdl(k_onesweep<Packed, NT, ITEMS, LOOKW, MINB, RB>, grid, NT, smem, st, S);
 }
 
 template <bool Packed>
@@ -773,6 +793,8 @@ void launch_sweep_variant(const SweepArgs& S, int64_t cap, cudaStream_t st, int 
 // [begin, end) of every tile from the tile changes of the sorted keys (tile = key >> b)
 __global__ void k_ranges(const uint64_t* __restrict__ keys, const int64_t* __restrict__ scal, int64_t capacity,
                          int id_bits, int2* __restrict__ ranges, int n_tiles) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t P = min(scal[S_P], capacity);
   const int b = (int)scal[S_B] + id_bits;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
@@ -789,6 +811,8 @@ __global__ void k_ranges(const uint64_t* __restrict__ keys, const int64_t* __res
 // scheduling, never results).  One CTA.
 __global__ void __launch_bounds__(1024) k_tile_order(const int2* __restrict__ ranges, int n_tiles,
                                                      int* __restrict__ order) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_hist[33];
   __shared__ int s_off[33];
   for (int i = threadIdx.x; i < 33; i += blockDim.x) s_hist[i] = 0;
@@ -819,6 +843,8 @@ __global__ void __launch_bounds__(1024) k_tile_order(const int2* __restrict__ ra
 // (tile << 32 | depth bits) from the trimmed keys
 __global__ void k_keys64(const uint64_t* __restrict__ keys, const int64_t* __restrict__ scal, int64_t capacity,
                          int id_bits, uint64_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t P = min(scal[S_P], capacity);
   const int b = (int)scal[S_B];
   const uint32_t kmin = (uint32_t)scal[S_KMIN];
@@ -874,18 +900,19 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
   };
   // one memset zeroes the pass histograms, all counters, the key range and the look-back
   // status words of the count scan and the first sweep pass (each pass clears the next's)
-  if (cudaMemsetAsync(w.zero, 0, w.zero_bytes, st) != cudaSuccess) return check("memset workspace");
+  launch_pdl(k_zero, zero_blocks((int64_t)(w.zero_bytes / 4)), 256, 0, st, reinterpret_cast<uint32_t*>(w.zero),
+             (int64_t)(w.zero_bytes / 4));
   uint32_t* ctr = w.counters + kMaxPasses;  // [0] scan block ids, [1] scan blocks done
   if (nb > 0) {
     const int64_t nsb = (n + kScanPer - 1) / kScanPer;
     SIMULI_REQUIRE(reinterpret_cast<uintptr_t>(proj->tile_count) % 16 == 0 &&
                        reinterpret_cast<uintptr_t>(proj->depth_key) % 16 == 0,
                    "simuli_bin_sort: tile_count / depth_key must be 16-byte aligned");
-    k_count_scan<<<(unsigned)nsb, kScanThreads, 0, st>>>(proj->tile_count, proj->depth_key, n, nsb, nb, tbits, rb,
+    launch_pdl(k_count_scan, (unsigned)nsb, kScanThreads, 0, st, proj->tile_count, proj->depth_key, n, nsb, nb, tbits, rb,
                                                          w.block_sums, w.cstatus, w.kminmax, ctr, w.scal, n_pairs_dev,
                                                          n_pairs_max_dev);
   } else {
-    k_count_empty<<<1, 32, 0, st>>>(tbits, w.scal, n_pairs_dev, w.block_sums);
+    launch_pdl(k_count_empty, 1, 32, 0, st, tbits, w.scal, n_pairs_dev, w.block_sums);
   }
   if (int32_t e = check("scan")) return e;
   if (sync_mode) {
@@ -910,7 +937,7 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     DupArgs D{proj->tile_count, reinterpret_cast<const int4*>(proj->tile_rect), proj->depth_key, n, cap,
               w.block_sums, w.scal, n_cols_total, {w.keys[0], w.keys[1]}, {vals[0], vals[1]}, w.hist, nullptr,
               id_bits, packed ? 1 : 0, n_tiles};
-    k_duplicate<kRB><<<(unsigned)nb, kDupThreads, 0, st>>>(D);
+    launch_pdl(k_duplicate<kRB>, (unsigned)nb, kDupThreads, 0, st, D);
     if (int32_t e = check("duplicate")) return e;
     for (int p = 0; p < max_passes; ++p) {
       const size_t row = (size_t)w.parts << rb;  // one pass's status words
@@ -923,14 +950,14 @@ extern "C" int32_t simuli_bin_sort(const simuli_projected* proj, int64_t n, int3
     if (int32_t e = check("onesweep")) return e;
   }
   const int key_shift = packed ? id_bits : 0;
-  if (cudaMemsetAsync(tile_ranges, 0, sizeof(int32_t) * 2 * (size_t)n_tiles, st) != cudaSuccess)
-    return check("memset ranges");
+  launch_pdl(k_zero, zero_blocks(2 * (int64_t)n_tiles), 256, 0, st, reinterpret_cast<uint32_t*>(tile_ranges),
+             2 * (int64_t)n_tiles);
   if (cap > 0)
-    k_ranges<<<148 * 8, 256, 0, st>>>(w.keys[0], w.scal, cap, key_shift, reinterpret_cast<int2*>(tile_ranges),
+    launch_pdl(k_ranges, 148 * 8, 256, 0, st, w.keys[0], w.scal, cap, key_shift, reinterpret_cast<int2*>(tile_ranges),
                                       n_tiles);
   if (tile_order)
-    k_tile_order<<<1, 1024, 0, st>>>(reinterpret_cast<const int2*>(tile_ranges), n_tiles, tile_order);
-  if (sorted_keys && cap > 0) k_keys64<<<148 * 4, 256, 0, st>>>(w.keys[0], w.scal, cap, key_shift, sorted_keys);
+    launch_pdl(k_tile_order, 1, 1024, 0, st, reinterpret_cast<const int2*>(tile_ranges), n_tiles, tile_order);
+  if (sorted_keys && cap > 0) launch_pdl(k_keys64, 148 * 4, 256, 0, st, w.keys[0], w.scal, cap, key_shift, sorted_keys);
   return check("tile metadata");
 }
 

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/simuli.h"
 #include "abi_util.h"
@@ -28,6 +29,45 @@
 #endif
 
 namespace simuli {
+
+// Programmatic dependent launch (sm_90+): the forward path's kernels are launched with
+// programmatic stream serialization, so kernel k + 1's CTAs are scheduled while kernel k's
+// last CTAs finish (hiding the launch gap between dependent kernels on one stream).  Every
+// such kernel starts with pdl_wait() -- it blocks until the previous grid on the stream has
+// completed and its writes are visible, so nothing before it may read what that grid
+// produced -- then pdl_trigger() lets the next grid launch once all CTAs of this one have
+// started.  Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SIMULI_PDL");  // tuning / A-B only: 0 = plain launches
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// kernel<<<grid, block, smem, st>>>(args...) with programmatic stream serialization
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  if (!pdl_enabled()) {
+    kernel<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // status of the last kernel launch as a libsimuli error code (with the CUDA message)
 inline int32_t launch_check(const char* what) {

@@ -514,6 +514,8 @@ constexpr int kSmemBounds = 264;
 
 template <int KIND, bool DIV, bool ACT>
 __global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_project(const ProjArgs Ain) {
+  pdl_wait();
+  pdl_trigger();
   // tiling boundaries / row scales staged in shared memory (binary searches hit smem)
   __shared__ float s_bounds[kSmemBounds], s_rscale[kSmemBounds];
   ProjArgs A = Ain;
@@ -823,7 +825,7 @@ static void depth_origin(const simuli_pose& a, const simuli_pose& b, float out[3
 
 template <int KIND, bool DIV, bool ACT>
 void launch_project(const ProjArgs& A, unsigned blocks, int threads, cudaStream_t st) {
-  k_project<KIND, DIV, ACT><<<blocks, threads, 0, st>>>(A);
+  launch_pdl(k_project<KIND, DIV, ACT>, blocks, threads, 0, st, A);
 }
 
 }  // namespace simuli

@@ -56,6 +56,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // instead of one; items are scheduled longest list first (tile_order).
 template <int TP, int SPLIT, bool PRAY>
 __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraArgs A) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NTH = TP * TP / SPLIT;  // threads = pixels of the band
   constexpr int NT = 128;               // list entries staged per batch
   constexpr int PER = NT / NTH;         // entries per thread per batch
@@ -750,6 +752,8 @@ __device__ __forceinline__ void pc_item(const LidarArgs& A, const int64_t item, 
 
 template <int P, int NS, int CAP, bool PRAY>
 __global__ void __launch_bounds__(32 * (P + 1)) k_render_lidar(const LidarArgs A) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   pc_item<P, NS, CAP, PRAY>(A, blockIdx.x, smem_raw);
 }
@@ -1049,6 +1053,8 @@ __device__ __forceinline__ void w_item(const LidarArgs& A, const int64_t item, W
 
 template <int W, int CAP, bool PRAY>
 __global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5;
   w_item<CAP, PRAY>(A, (int64_t)blockIdx.x * W + warp, reinterpret_cast<WarpItemSmem<CAP>*>(smem_raw)[warp]);
@@ -1060,6 +1066,8 @@ __global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
 // time of the longest lists while most items keep the lean path.
 template <int CAP, int WCAP, bool PRAY>
 __global__ void __launch_bounds__(128) k_render_lidar_h(const LidarArgs A) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if ((int64_t)blockIdx.x < A.n_long) {
     pc_item<3, 3, CAP, PRAY>(A, blockIdx.x, smem_raw);
@@ -1131,7 +1139,7 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
     constexpr size_t smem = sizeof(LidarSmem<P_, NS_, CAP_>);
     auto kern = A.sh ? k_render_lidar<P_, NS_, CAP_, true> : k_render_lidar<P_, NS_, CAP_, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)A.n_items, 32 * (P_ + 1), smem, st>>>(A);
+    launch_pdl(kern, (unsigned)A.n_items, 32 * (P_ + 1), smem, st, A);
   };
   using std::integral_constant;
   static const int variant = [] {
@@ -1148,7 +1156,7 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
     constexpr size_t smem = sizeof(WarpItemSmem<CAP_>) * W_;
     auto kern = A.sh ? k_render_lidar_w<W_, CAP_, true> : k_render_lidar_w<W_, CAP_, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)((A.n_items + W_ - 1) / W_), 32 * W_, smem, st>>>(A);
+    launch_pdl(kern, (unsigned)((A.n_items + W_ - 1) / W_), 32 * W_, smem, st, A);
   };
   auto launch_h = [&](int64_t n_long) {
     constexpr int CAP_ = 384, WCAP_ = 128;
@@ -1157,7 +1165,7 @@ extern "C" int32_t simuli_render_lidar(const simuli_projected* proj, const uint3
     A.n_long = n_long < A.n_items ? n_long : A.n_items;
     auto kern = A.sh ? k_render_lidar_h<CAP_, WCAP_, true> : k_render_lidar_h<CAP_, WCAP_, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)(A.n_long + (A.n_items - A.n_long + 3) / 4), 128, smem, st>>>(A);
+    launch_pdl(kern, (unsigned)(A.n_long + (A.n_items - A.n_long + 3) / 4), 128, smem, st, A);
   };
   static const int64_t n_long_env = [] {
     const char* v = getenv("SIMULI_LIDAR_NLONG");  // tuning only
@@ -1258,13 +1266,13 @@ extern "C" int32_t simuli_render_camera(const simuli_projected* proj, const uint
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (A.sh) {
     switch (C.tile_px) {
-      case 8: k_render_camera<8, 1, true><<<blocks, 64, 0, st>>>(A); break;
-      default: k_render_camera<16, 4, true><<<blocks * 4, 64, 0, st>>>(A); break;
+      case 8: launch_pdl(k_render_camera<8, 1, true>, blocks, 64, 0, st, A); break;
+      default: launch_pdl(k_render_camera<16, 4, true>, blocks * 4, 64, 0, st, A); break;
     }
   } else {
     switch (C.tile_px) {
-      case 8: k_render_camera<8, 1, false><<<blocks, 64, 0, st>>>(A); break;
-      default: k_render_camera<16, 4, false><<<blocks * 4, 64, 0, st>>>(A); break;
+      case 8: launch_pdl(k_render_camera<8, 1, false>, blocks, 64, 0, st, A); break;
+      default: launch_pdl(k_render_camera<16, 4, false>, blocks * 4, 64, 0, st, A); break;
     }
   }
   return launch_check("simuli_render_camera");
