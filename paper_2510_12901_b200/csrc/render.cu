@@ -28,10 +28,13 @@
 // bands share its list, so the long near-field lists are spread over four CTAs -- items
 // longest-list-first, pixel per thread, 128-record batches in shared memory, double-buffered
 // (batch k + 1 arrives by cp.async, its ids prefetched a batch earlier, while batch k is
-// walked); each warp ballots which entries overlap its 2 x 16 pixel strip and walks only
-// those; CTA-wide early exit.  Config D (1920x1080 fisheye, 2M particles) render: 2.31 ms
-// (one 256-thread CTA per tile) -> 2.01 (strip pre-cull) -> 1.08 (4 bands; 8 bands: 1.15)
-// -> 0.97 (double-buffered batches).  Pixel rays by the inverse lens model in double.
+// walked); each warp ballots which entries overlap its 2 x 16 pixel strip, every lane marks
+// its pixel's member entries among those, and the lanes walk their own members in list order
+// (one member per live lane per step: 11 of 32 lanes were busy when the warp walked the
+// strip's entries together); CTA-wide early exit.  Config D (1920x1080 fisheye, 2M
+// particles) render: 2.31 ms (one 256-thread CTA per tile) -> 2.01 (strip pre-cull) -> 1.08
+// (4 bands; 8 bands: 1.15) -> 0.97 (double-buffered batches) -> 0.78 (per-lane member
+// walk; per-ray SH 2.26 -> 1.42).  Pixel rays by the inverse lens model in double.
 #include <cstdint>
 #include <cstdlib>
 #include <string>
@@ -155,13 +158,22 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
           const float4 bx = s_rec[jl][4];
           ov = bx.x <= su1 && su0 <= bx.y && bx.z <= sv1 && sv0 <= bx.w;
         }
-        uint32_t mask = __ballot_sync(0xffffffffu, ov);
-        while (mask) {
-          const int jj = k0 + __ffs(mask) - 1;
-          mask &= mask - 1u;
-          if (done) continue;
-          const float4 bx = s_rec[jj][4];
-          if (!(bx.x <= pu && pu <= bx.y && bx.z <= pv && pv <= bx.w)) continue;
+        // this pixel's member entries among those (the same box test per entry as the walk
+        // over the strip's entries); then every lane walks its own members in list order, so
+        // a step evaluates one member per live lane instead of one entry for the lanes it
+        // covers
+        uint32_t mine = 0u;
+        const uint32_t strip = __ballot_sync(0xffffffffu, ov);  // all lanes (done or not)
+        if (!done) {
+          for (uint32_t t = strip; t; t &= t - 1u) {
+            const int e = __ffs(t) - 1;
+            const float4 bx = s_rec[k0 + e][4];
+            if (bx.x <= pu && pu <= bx.y && bx.z <= pv && pv <= bx.w) mine |= 1u << e;
+          }
+        }
+        while (mine) {
+          const int jj = k0 + __ffs(mine) - 1;
+          mine &= mine - 1u;
           ++ni;
           const float4 r0 = s_rec[jj][0], r1 = s_rec[jj][1], r2 = s_rec[jj][2], r3 = s_rec[jj][3];
           const float mu[3] = {r0.x, r0.y, r0.z};
@@ -173,6 +185,7 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
           const float Tn = T * (1.f - alpha);
           if (Tn < A.T_min) {
             done = true;
+            mine = 0u;
             term_at = b - rg.x + jj;
             continue;
           }
