@@ -530,6 +530,18 @@ __global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_proje
   }
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= A.n) return;
+#ifndef SIMULI_NO_SH_PREFETCH
+  // the degree-3 SH blocks (192 B each) are read only for kept particles, ~2000
+  // instructions later; one bulk L2 prefetch of the warp's 32 contiguous blocks now (every
+  // particle: culling is not known yet) turns those reads from DRAM misses into L2 hits --
+  // they were the kernel's largest stall (long_scoreboard at the first SH FMA: 14 % of its
+  // warp samples, r02k_scan)
+  if (A.sh_degree == 3 && (threadIdx.x & 31) == 0) {
+    const int64_t cnt = A.n - g < 32 ? A.n - g : 32;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.sh + g * 48), "r"((unsigned)(cnt * 192))
+                 : "memory");
+  }
+#endif
   // SoA loads (quaternion as one 16-byte load)
   float mu[3] = {__ldg(A.means + 3 * g), __ldg(A.means + 3 * g + 1), __ldg(A.means + 3 * g + 2)};
   float4 q4 = __ldg(reinterpret_cast<const float4*>(A.quats) + g);
