@@ -126,24 +126,6 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
   return v;
 }
 
-// exclusive scan of one value per thread over a 256-thread block; *total = block sum.
-__device__ __forceinline__ int block_excl_scan256(int v, int* scratch, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int inc = warp_incl_scan(v);
-  if (lane == 31) scratch[warp] = inc;
-  __syncthreads();
-  int wpre = 0, tot = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    const int s = scratch[w];
-    if (w < warp) wpre += s;
-    tot += s;
-  }
-  __syncthreads();
-  *total = tot;
-  return wpre + inc - v;
-}
-
 // zeroing on the stream as a kernel (a memset node would break the programmatic launch chain)
 __global__ void __launch_bounds__(256) k_zero(uint32_t* __restrict__ p, int64_t n_words) {
   pdl_wait();
