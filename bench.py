@@ -65,7 +65,7 @@ def read_peaks():
 
 class ClockSampler:
     """SM clock + throttle reasons sampled DURING the timed region by a separate process (an
-    NVML poll every 2 ms, monotonic timestamps, written to a temp file; a thread of this
+    NVML poll every 0.5 ms, monotonic timestamps, written to a temp file; a thread of this
     process would need the GIL the launch loop holds) and kept for the window
     [mark_begin, mark_end]; falls back to ``nvidia-smi -lms 100`` if NVML is unavailable."""
 
@@ -81,7 +81,7 @@ class ClockSampler:
         "while True:\n"
         "    out.write('%.6f %d %d %d\\n' % (time.monotonic(), n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM), smax,\n"
         "              n.nvmlDeviceGetCurrentClocksEventReasons(h)))\n"
-        "    time.sleep(0.002)\n")
+        "    time.sleep(0.0005)\n")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
@@ -89,7 +89,7 @@ class ClockSampler:
         self.proc = None
         self.path = None
         self.window = [None, None]
-        self.source = "nvml 2 ms (poller process)"
+        self.source = "nvml 0.5 ms (poller process)"
 
     def start(self):
         import tempfile
