@@ -320,6 +320,11 @@ __device__ __forceinline__ float fire_time(const ProjArgs& A, float px, float py
 // Outputs: *a0, *e0 = azimuth / elevation of sigma point 0 (double); ma, me = UT mean offsets
 // from them (azimuth unwrapped about sigma point 0, A21); caa, cab, cbb = UT covariance;
 // s0 = firing time of sigma point 0.
+// YAW: the sweep's rotation axis is the sensor z axis (A.axis = (0, 0, +-1) exactly, the
+// spinning sensor of a ground vehicle turning in the plane): E(s0) and the small rotation
+// between firing times act in the xy plane only, and the general Rodrigues forms reduce to
+// the planar ones below (same quantities, fewer operations)
+template <bool YAW>
 __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[3], const float L[3][3], double* a0,
                                               double* e0, float* ma, float* me, float* caa, float* cab, float* cbb,
                                               float* s0, bool* valid) {
@@ -403,8 +408,16 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
         }
         const float ds = s - s_c;
         const float y[3] = {l[0] - ds * A.v[0], l[1] - ds * A.v[1], l[2] - ds * A.v[2]};
-        const float w[3] = {E[0] * y[0] + E[1] * y[1] + E[2] * y[2], E[3] * y[0] + E[4] * y[1] + E[5] * y[2],
-                            E[6] * y[0] + E[7] * y[1] + E[8] * y[2]};
+        float w[3];
+        if (YAW) {  // E = [[c, s, 0], [-s, c, 0], [0, 0, 1]]
+          w[0] = E[0] * y[0] + E[1] * y[1];
+          w[1] = E[3] * y[0] + E[4] * y[1];
+          w[2] = y[2];
+        } else {
+          w[0] = E[0] * y[0] + E[1] * y[1] + E[2] * y[2];
+          w[1] = E[3] * y[0] + E[4] * y[1] + E[5] * y[2];
+          w[2] = E[6] * y[0] + E[7] * y[1] + E[8] * y[2];
+        }
         // E(ds) - I for the small rotation between the two firing times (|ds theta| is the
         // particle's angular size times the sweep's yaw, ~1e-3): Taylor to a^4 below 1e-2
         // (truncation < 1e-11), the general form otherwise
@@ -418,12 +431,19 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
           rot_sc_f(A, ds, &sn, &omc);
         }
         const float z[3] = {p0[0] + w[0], p0[1] + w[1], p0[2] + w[2]};
-        const float* kk = A.axis;
-        const float cx = kk[1] * z[2] - kk[2] * z[1], cy = kk[2] * z[0] - kk[0] * z[2], cz = kk[0] * z[1] - kk[1] * z[0];
-        const float kd = kk[0] * z[0] + kk[1] * z[1] + kk[2] * z[2];
-        D[0] = w[0] - sn * cx + omc * (kk[0] * kd - z[0]);
-        D[1] = w[1] - sn * cy + omc * (kk[1] * kd - z[1]);
-        D[2] = w[2] - sn * cz + omc * (kk[2] * kd - z[2]);
+        if (YAW) {  // k = (0, 0, kz): k x z = kz (-z1, z0, 0), k (k.z) - z = (-z0, -z1, 0)
+          const float snk = sn * A.axis[2];
+          D[0] = w[0] + snk * z[1] - omc * z[0];
+          D[1] = w[1] - snk * z[0] - omc * z[1];
+          D[2] = w[2];
+        } else {
+          const float* kk = A.axis;
+          const float cx = kk[1] * z[2] - kk[2] * z[1], cy = kk[2] * z[0] - kk[0] * z[2], cz = kk[0] * z[1] - kk[1] * z[0];
+          const float kd = kk[0] * z[0] + kk[1] * z[1] + kk[2] * z[2];
+          D[0] = w[0] - sn * cx + omc * (kk[0] * kd - z[0]);
+          D[1] = w[1] - sn * cy + omc * (kk[1] * kd - z[1]);
+          D[2] = w[2] - sn * cz + omc * (kk[2] * kd - z[2]);
+        }
       }
       const float pz = p0[2] + D[2];
       const float xy = p0[0] * D[0] + p0[1] * D[1];
@@ -512,7 +532,7 @@ __device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3],
 constexpr double kPiD = 3.141592653589793;
 constexpr int kSmemBounds = 264;
 
-template <int KIND, bool DIV, bool ACT>
+template <int KIND, bool DIV, bool ACT, bool YAW>
 __global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_project(const ProjArgs Ain) {
   pdl_wait();
   pdl_trigger();
@@ -658,7 +678,7 @@ __global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_proje
       Mh[6] = m20; Mh[7] = m21; Mh[8] = m22;
     }
     if (KIND == SIMULI_SENSOR_LIDAR) {
-      lidar_moments(A, mu, L, &a0, &e0, &ma, &mb, &caa, &cab, &cbb, &s0, &valid);
+      lidar_moments<YAW>(A, mu, L, &a0, &e0, &ma, &mb, &caa, &cab, &cbb, &s0, &valid);
     } else {
     // ---- 7 sigma points through the sensor model
     float ya[7], yb[7];
@@ -835,9 +855,9 @@ static void depth_origin(const simuli_pose& a, const simuli_pose& b, float out[3
   }
 }
 
-template <int KIND, bool DIV, bool ACT>
+template <int KIND, bool DIV, bool ACT, bool YAW = false>
 void launch_project(const ProjArgs& A, unsigned blocks, int threads, cudaStream_t st) {
-  launch_pdl(k_project<KIND, DIV, ACT>, blocks, threads, 0, st, A);
+  launch_pdl(k_project<KIND, DIV, ACT, YAW>, blocks, threads, 0, st, A);
 }
 
 }  // namespace simuli
@@ -940,12 +960,18 @@ extern "C" int32_t simuli_project(const simuli_gaussians* G, const simuli_projec
       A.n_beams = T.n_beams; A.n_az = T.n_azimuth;
       A.col_step = (float)(T.n_azimuth / (2.0 * 3.14159265358979323846));
     }
+    // rotation about the sensor z axis (yaw only): the planar sigma-point forms
+    const bool yaw = A.axis[0] == 0.f && A.axis[1] == 0.f && std::fabs(A.axis[2]) == 1.f;
     if (A.beam_div > 0.f) {
-      if (act) launch_project<SIMULI_SENSOR_LIDAR, true, true>(A, blocks, threads, st);
-      else launch_project<SIMULI_SENSOR_LIDAR, true, false>(A, blocks, threads, st);
+      if (act) yaw ? launch_project<SIMULI_SENSOR_LIDAR, true, true, true>(A, blocks, threads, st)
+                   : launch_project<SIMULI_SENSOR_LIDAR, true, true>(A, blocks, threads, st);
+      else yaw ? launch_project<SIMULI_SENSOR_LIDAR, true, false, true>(A, blocks, threads, st)
+               : launch_project<SIMULI_SENSOR_LIDAR, true, false>(A, blocks, threads, st);
     } else {
-      if (act) launch_project<SIMULI_SENSOR_LIDAR, false, true>(A, blocks, threads, st);
-      else launch_project<SIMULI_SENSOR_LIDAR, false, false>(A, blocks, threads, st);
+      if (act) yaw ? launch_project<SIMULI_SENSOR_LIDAR, false, true, true>(A, blocks, threads, st)
+                   : launch_project<SIMULI_SENSOR_LIDAR, false, true>(A, blocks, threads, st);
+      else yaw ? launch_project<SIMULI_SENSOR_LIDAR, false, false, true>(A, blocks, threads, st)
+               : launch_project<SIMULI_SENSOR_LIDAR, false, false>(A, blocks, threads, st);
     }
   } else if (P->kind == SIMULI_SENSOR_CAMERA) {
     SIMULI_REQUIRE(P->camera, "camera projection needs camera");

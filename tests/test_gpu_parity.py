@@ -612,12 +612,14 @@ def test_beam_divergence_parity(SM, oracle_mod, config):
 
 
 # ------------------------------------------------------------------ sensor-model variants
-@pytest.mark.parametrize("variant", ["cw_spin", "K2", "K0", "az_start", "static_pose", "rotating_fast"])
+@pytest.mark.parametrize("variant", ["cw_spin", "K2", "K0", "az_start", "static_pose", "rotating_fast", "tilted"])
 def test_lidar_sensor_variants(SM, oracle_mod, variant):
     """Paths of the sensor model the BASELINE configs do not exercise: clockwise spin,
     K = 2 and K = 0 firing-time iterations (A3), a non-default phi_start, a static pose, and
     a fast-rotating sweep (0.6 rad of yaw: the general rotation branch instead of the
-    small-angle series).  Tier 1 projection + compositing and tier 2 end to end on config A
+    small-angle series), and a sweep rotating about a tilted axis (the general Rodrigues form
+    of the sigma-point offsets instead of the planar yaw-only one).  Tier 1 projection +
+    compositing and tier 2 end to end on config A
     geometry (32 x 512 rays, 1k particles) moved through a 1.5 m / yawing sweep."""
     O = oracle_mod
     cfg, scene = S.lidar_config("A"), S.scene_for("A")
@@ -635,6 +637,15 @@ def test_lidar_sensor_variants(SM, oracle_mod, variant):
         cfg.pose_end = cfg.pose_start
     elif variant == "rotating_fast":
         cfg.pose_end = S.pose(S.yaw_quat(0.7), [1.5, 0.3, 1.8])
+    elif variant == "tilted":  # 0.05 rad about (0.1, 0.2, 1) after the start yaw
+        ax = np.array([0.1, 0.2, 1.0]) / np.linalg.norm([0.1, 0.2, 1.0])
+        qt = np.concatenate([[np.cos(0.025)], np.sin(0.025) * ax])
+        q0 = np.asarray(S.yaw_quat(0.1), np.float64)
+        w1, x1, y1, z1 = q0
+        w2, x2, y2, z2 = qt
+        q1 = [w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2, w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+              w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2, w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2]
+        cfg.pose_end = S.pose(q1, [1.5, 0.3, 1.8])
     r = lidar_run(SM, cfg, scene, write_all_records=True)
     rec = r.record.cpu().numpy()
     proj = O.project_lidar(scene, cfg)
