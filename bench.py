@@ -99,8 +99,9 @@ class ClockSampler:
         os.close(fd)
         try:
             import pynvml  # noqa: F401  (the poller imports it too)
+            self.err_path = self.path + ".err"
             self.proc = subprocess.Popen([sys.executable, "-c", self.POLL, str(idx), self.path],
-                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+                                         stdout=subprocess.DEVNULL, stderr=open(self.err_path, "w"))
         except Exception:
             self.source = "nvidia-smi 100 ms"
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(idx), "--query-gpu=timestamp,clocks.sm,clocks.max.sm,"
@@ -146,7 +147,13 @@ class ClockSampler:
             if t_lo <= t <= t_hi:
                 self.samples.append((t, a, b, c))
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0}
+            why = {"lines": len(lines), "window": [t_lo, t_hi], "poller_rc": self.proc.returncode if self.proc else None}
+            try:
+                why["first"] = lines[:2]
+                why["err"] = open(self.err_path).read()[-300:]
+            except (OSError, AttributeError):
+                pass
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0, "debug": why}
         sm = [s[1] for s in self.samples]
         reasons = sorted({name for _, _, _, m in self.samples for name, bit in self.REASONS if m & bit})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[2] for s in self.samples),
@@ -402,6 +409,9 @@ def run_gpu(args):
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
+    # clock poller started now, seconds before the timed region (its window is marked there)
+    clocks = ClockSampler(dev.index if ws == 1 else local)
+    clocks.start()
     SM.load()
     cfg = synth.lidar_config("B")
     scene_np = synth.scene_for("B")  # same seed on every rank: replicated scene
@@ -449,10 +459,8 @@ def run_gpu(args):
     # ---- timed region (headline): K scans, S in flight; device time between two events on
     # the launching (main) stream, the S scan streams forked from / joined into it; no L2
     # flush needed: the resident scene (472 MB) and records (160 MB) exceed the 126 MB L2
-    clocks = ClockSampler(dev.index if ws == 1 else local)
     if ws > 1:
         dist.barrier()
-    clocks.start()
     torch.cuda.synchronize()
     clocks.mark_begin()
     wall0 = time.perf_counter()
