@@ -248,7 +248,8 @@ __device__ __forceinline__ int sat_rect(const ProjArgs& A, int r0, int r1, int c
 
 // atan2 in double to ~1e-13 rad (the box edges need ~1e-9; libdevice's full-precision
 // atan2 costs ~75 instructions, half of them materialising its 64-bit coefficients): |t| =
-// min / max reduced to [0, tan(pi/8)] by atan t = pi/4 + atan((t - 1) / (t + 1)), then
+// min / max reduced to [0, tan(pi/8)] by atan t = pi/4 + atan((t - 1) / (t + 1)) (formed as
+// (min - max) / (min + max): one division), then
 // atan t = t + t u P(u), u = t^2, P a degree-7 least-squares Chebyshev fit (max error
 // 1.1e-13 on the interval) with its coefficients in constant memory (DFMA operands, no
 // immediate moves).  Quadrants and signed zeros as C's atan2 except atan2(+-0, -0) = 0.
@@ -258,9 +259,10 @@ __constant__ double c_atan_p[8] = {-0.33333333333168147, 0.19999999929984685, -0
 __device__ __forceinline__ double atan2_fast(double y, double x) {
   const double ax = fabs(x), ay = fabs(y);
   const double mx = fmax(ax, ay), mn = fmin(ax, ay);
-  double t = mx > 0.0 ? mn / mx : 0.0;
-  const bool big = t > 0.41421356237309503;
-  if (big) t = (t - 1.0) / (t + 1.0);
+  // t = mn / mx, reduced when t > tan(pi/8) to (t - 1) / (t + 1) = (mn - mx) / (mn + mx):
+  // one division either way (the test mn > tan(pi/8) mx is the same comparison)
+  const bool big = mn > 0.41421356237309503 * mx;
+  const double t = mx > 0.0 ? (big ? mn - mx : mn) / (big ? mn + mx : mx) : 0.0;
   const double u = t * t;
   double p = c_atan_p[7];
 #pragma unroll
