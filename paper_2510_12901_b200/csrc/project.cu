@@ -504,14 +504,23 @@ __device__ __forceinline__ int cam_frame(const ProjArgs& A, float px, float py, 
   return (pz >= A.near_m && th <= A.max_theta) ? 1 : 0;
 }
 
-__device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3], float* u, float* v, float* s_out) {
+// pose0: the pose at s = 0 (pose_at(A.pose, 0), computed once per CTA in shared memory --
+// the same values, without a sincos and a quaternion product per sigma point)
+__device__ __forceinline__ int camera_point(const ProjArgs& A, const float x[3], float* u, float* v, float* s_out,
+                                            const float* pose0) {
   float s = 0.f;
   int valid = 1;
   const int K = A.pose.same ? 0 : A.K;
   const float invH = 1.0f / (float)A.height;
   for (int it = 0; it <= K; ++it) {
     float R[9], t[3];
-    pose_at(A.pose, s, R, t);
+    if (s == 0.f) {
+#pragma unroll
+      for (int i = 0; i < 9; ++i) R[i] = pose0[i];
+      t[0] = pose0[9]; t[1] = pose0[10]; t[2] = pose0[11];
+    } else {
+      pose_at(A.pose, s, R, t);
+    }
     const float d0 = x[0] - t[0], d1 = x[1] - t[1], d2 = x[2] - t[2];
     const float px = R[0] * d0 + R[3] * d1 + R[6] * d2;
     const float py = R[1] * d0 + R[4] * d1 + R[7] * d2;
@@ -540,7 +549,12 @@ __global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_proje
   pdl_trigger();
   // tiling boundaries / row scales staged in shared memory (binary searches hit smem)
   __shared__ float s_bounds[kSmemBounds], s_rscale[kSmemBounds];
+  __shared__ float s_pose0[12];  // camera: the pose at s = 0
   ProjArgs A = Ain;
+  if (KIND == SIMULI_SENSOR_CAMERA) {
+    if (threadIdx.x == 0) pose_at(Ain.pose, 0.f, s_pose0, s_pose0 + 9);
+    __syncthreads();
+  }
   if (KIND == SIMULI_SENSOR_LIDAR && Ain.n_phi + 1 <= kSmemBounds) {
     for (int i = threadIdx.x; i <= Ain.n_phi; i += blockDim.x) {
       s_bounds[i] = __ldg(Ain.bounds + i);
@@ -695,7 +709,7 @@ __global__ void __launch_bounds__(SIMULI_PROJ_THREADS, SIMULI_PROJ_MINB) k_proje
         x[2] += sg * L[k][2];
       }
       float s;
-      const int st = camera_point(A, x, &ya[i], &yb[i], &s);
+      const int st = camera_point(A, x, &ya[i], &yb[i], &s, s_pose0);
       computable = computable && st >= 0;
       valid = valid && st == 1;
       if (i == 0) s0 = s;
