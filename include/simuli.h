@@ -25,7 +25,11 @@
  *   enqueued work on `stream` has completed.  Scratch is the caller's `workspace`.
  * Asynchrony: device work is enqueued on the caller's cudaStream_t (passed as void*, NULL =
  *   legacy default stream); no call synchronises, except simuli_bin_sort with
- *   pair_capacity < 0 (documented there).
+ *   pair_capacity < 0 (documented there).  The forward kernels are launched with
+ *   programmatic dependent launch (a kernel's CTAs may be scheduled while the previous
+ *   kernel on the stream finishes; each waits for that kernel's completion before reading
+ *   anything), so stream-order semantics are exactly those of plain launches
+ *   (SIMULI_PDL=0 in the environment disables it).
  * Degenerate particles are not errors: zero / non-finite quaternion or scale, a sigma
  *   point closer than the minimum range / near plane, or a singular projected covariance
  *   make a particle "invalid": tile count 0, never rendered (A20).
