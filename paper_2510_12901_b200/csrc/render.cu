@@ -28,13 +28,16 @@
 // bands share its list, so the long near-field lists are spread over four CTAs -- items
 // longest-list-first, pixel per thread, 128-record batches in shared memory, double-buffered
 // (batch k + 1 arrives by cp.async, its ids prefetched a batch earlier, while batch k is
-// walked); each warp ballots which entries overlap its 2 x 16 pixel strip, every lane marks
-// its pixel's member entries among those, and the lanes walk their own members in list order
-// (one member per live lane per step: 11 of 32 lanes were busy when the warp walked the
-// strip's entries together); CTA-wide early exit.  Config D (1920x1080 fisheye, 2M
-// particles) render: 2.31 ms (one 256-thread CTA per tile) -> 2.01 (strip pre-cull) -> 1.08
-// (4 bands; 8 bands: 1.15) -> 0.97 (double-buffered batches) -> 0.78 (per-lane member
-// walk; per-ray SH 2.26 -> 1.42).  Pixel rays by the inverse lens model in double.
+// walked); each warp ballots which entries overlap its 2 x 16 pixel strip; the pixel lanes'
+// member masks over those come from the entry lanes' strip masks (the per-pixel box test on
+// the strip's column and row centres) by a 32 x 32 bit transpose, and the lanes walk their
+// own members in list order (one member per live lane per step: 11 of 32 lanes were busy
+// when the warp walked the strip's entries together); CTA-wide early exit.  Config D
+// (1920x1080 fisheye, 2M particles) render: 2.31 ms (one 256-thread CTA per tile) -> 2.01
+// (strip pre-cull) -> 1.08 (4 bands; 8 bands: 1.15) -> 0.97 (double-buffered batches) ->
+// 0.78 (per-lane member walk; per-ray SH 2.26 -> 1.42) -> 0.59 (transposed member masks:
+// the near-field lists of 20k entries were the render's tail; per-ray SH 1.34).  Pixel
+// rays by the inverse lens model in double.
 #include <cstdint>
 #include <cstdlib>
 #include <string>
@@ -54,6 +57,22 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// 32x32 bit-matrix transpose across a warp: in: lane i holds row i; out: lane r holds
+// the word whose bit e is bit r of row e (5-stage shuffle butterfly).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  const uint32_t lm[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int j = 16 >> s;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    x = (lane & j) ? ((x & ~lm[s]) | ((y & ~lm[s]) >> j)) : ((x & lm[s]) | ((y & lm[s]) << j));
+  }
+  return x;
+}
+
+#ifndef SIMULI_CAM_DENSE
+#define SIMULI_CAM_DENSE 2  // strip-overlapping entries of a group from which the masks are transposed
+#endif
 // One CTA per (tile, band of TP / SPLIT pixel rows): the bands of a tile read the same list,
 // so a long list (near-field particles covering many pixels) is spread over SPLIT CTAs
 // instead of one; items are scheduled longest list first (tile_order).
@@ -164,7 +183,28 @@ __global__ void __launch_bounds__(TP* TP / SPLIT) k_render_camera(const CameraAr
         // covers
         uint32_t mine = 0u;
         const uint32_t strip = __ballot_sync(0xffffffffu, ov);  // all lanes (done or not)
-        if (!done) {
+        if (__popc(strip) >= SIMULI_CAM_DENSE) {  // warp-uniform: a dense group (near-field lists)
+          // lane = entry: the strip pixels inside its box (the same comparisons, column and
+          // row centres of the strip), then a 32 x 32 bit transpose gives every pixel lane
+          // its member entries
+          uint32_t pm = 0u;
+          if (ov) {
+            const float4 bx = s_rec[jl][4];
+            uint32_t colmask = 0u;
+#pragma unroll
+            for (int cc = 0; cc < TP; ++cc) {
+              const float u = (float)(tx * TP + cc) + 0.5f;
+              colmask |= (uint32_t)(bx.x <= u && u <= bx.y) << cc;
+            }
+#pragma unroll
+            for (int rr = 0; rr < 32 / TP; ++rr) {
+              const float v = (float)(row0 + rr) + 0.5f;
+              if (bx.z <= v && v <= bx.w) pm |= colmask << (rr * TP);
+            }
+          }
+          mine = warp_transpose32(pm, lane);
+          if (done) mine = 0u;
+        } else if (!done) {
           for (uint32_t t = strip; t; t &= t - 1u) {
             const int e = __ffs(t) - 1;
             const float4 bx = s_rec[k0 + e][4];
@@ -249,18 +289,6 @@ struct LidarArgs {
   int sh_ncoef;
 };
 
-// 32x32 bit-matrix transpose across a warp: in: lane i holds row i; out: lane r holds
-// the word whose bit e is bit r of row e (5-stage shuffle butterfly).
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
-  const uint32_t lm[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const int j = 16 >> s;
-    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-    x = (lane & j) ? ((x & ~lm[s]) | ((y & ~lm[s]) >> j)) : ((x & lm[s]) | ((y & lm[s]) << j));
-  }
-  return x;
-}
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
