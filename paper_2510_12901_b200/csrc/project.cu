@@ -379,11 +379,20 @@ __device__ __forceinline__ void lidar_moments(const ProjArgs& A, const float mu[
   const bool pax = rho0d > 0.0, pnz = pax || p0d[2] != 0.0;  // sigma point 0 off the sensor axis / origin
   float Sd = 0.f, Se = 0.f, Sdd = 0.f, See = 0.f, Sde = 0.f;
 #pragma unroll 1
+  // the three columns rotated through registers: a dynamically indexed L[k] in the
+  // non-unrolled loop lived in local memory (spills, 175 -> 171 us)
+  float La[3] = {L[0][0], L[0][1], L[0][2]}, Lb[3] = {L[1][0], L[1][1], L[1][2]},
+        Lc[3] = {L[2][0], L[2][1], L[2][2]};
   for (int k = 0; k < 3; ++k) {
     // l_k in the start frame
-    const float lr[3] = {A.R0[0] * L[k][0] + A.R0[3] * L[k][1] + A.R0[6] * L[k][2],
-                         A.R0[1] * L[k][0] + A.R0[4] * L[k][1] + A.R0[7] * L[k][2],
-                         A.R0[2] * L[k][0] + A.R0[5] * L[k][1] + A.R0[8] * L[k][2]};
+    const float lr[3] = {A.R0[0] * La[0] + A.R0[3] * La[1] + A.R0[6] * La[2],
+                         A.R0[1] * La[0] + A.R0[4] * La[1] + A.R0[7] * La[2],
+                         A.R0[2] * La[0] + A.R0[5] * La[1] + A.R0[8] * La[2]};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      La[c] = Lb[c];
+      Lb[c] = Lc[c];
+    }
 #pragma unroll
     for (int sg = 0; sg < 2; ++sg) {
       const float l[3] = {sg ? -lr[0] : lr[0], sg ? -lr[1] : lr[1], sg ? -lr[2] : lr[2]};
