@@ -1105,8 +1105,11 @@ __global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
 // order) by the producer / consumer pipeline (3 producers, its shortest critical path), the
 // rest one warp per item (the least resources): one scan alone is then bounded by the P/C
 // time of the longest lists while most items keep the lean path.
+#ifndef SIMULI_RENDER_H_MINB
+#define SIMULI_RENDER_H_MINB 1
+#endif
 template <int CAP, int WCAP, bool PRAY>
-__global__ void __launch_bounds__(128) k_render_lidar_h(const LidarArgs A) {
+__global__ void __launch_bounds__(128, SIMULI_RENDER_H_MINB) k_render_lidar_h(const LidarArgs A) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
