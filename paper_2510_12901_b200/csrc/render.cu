@@ -1105,11 +1105,15 @@ __global__ void __launch_bounds__(32 * W) k_render_lidar_w(const LidarArgs A) {
 // order) by the producer / consumer pipeline (3 producers, its shortest critical path), the
 // rest one warp per item (the least resources): one scan alone is then bounded by the P/C
 // time of the longest lists while most items keep the lean path.
-#ifndef SIMULI_RENDER_H_MINB
-#define SIMULI_RENDER_H_MINB 1
-#endif
+// tuning only: SIMULI_RENDER_H_MINB sets a minimum of resident CTAs per SM (without it,
+// 96 registers; an explicit minimum of 1 lets ptxas take 112 and runs slower --
+// profiles/r02_experiments.md)
 template <int CAP, int WCAP, bool PRAY>
+#ifdef SIMULI_RENDER_H_MINB
 __global__ void __launch_bounds__(128, SIMULI_RENDER_H_MINB) k_render_lidar_h(const LidarArgs A) {
+#else
+__global__ void __launch_bounds__(128) k_render_lidar_h(const LidarArgs A) {
+#endif
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];
